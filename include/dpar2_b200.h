@@ -1,0 +1,176 @@
+/*
+ * dpar2_b200.h -- C ABI of the B200-native DPar2 hot path (libdpar2_b200.so).
+ *
+ * The reference (dpar2, /root/reference/pkg/src/dpar2 = "P/") is pure
+ * Python/NumPy and has no FFI layer; its boundary is the Python API
+ * (fit_dpar2 / compress / the per-iteration kernels, P/__init__.py:19-32).
+ * This header is the native boundary underneath our Python mirror of that API
+ * (paper_2203_12798_b200/), bound with ctypes (INTEGRATION.md shows the stub).
+ *
+ * Conventions
+ *   - Every pointer named *_dev or documented "device" is device memory owned
+ *     by the caller; calls are stream-ordered on ``stream`` (cudaStream_t, may
+ *     be NULL for the legacy stream) and return before the GPU finishes.
+ *   - Return value: a dp2_status for argument / launch errors.  Numeric
+ *     failures found on the device (non-finite input, non-converged Jacobi,
+ *     rank-deficient slices) are written to a caller-owned device ``status``
+ *     block of DP2_STATUS_WORDS int64 (initialise with dp2_status_init) and
+ *     read by the host after synchronising -- mirroring the reference's
+ *     NonFiniteInputError / NumericFailure(slice_index) (P/errors.py:36-43).
+ *   - Row-major everywhere.  Irregular slices live in one packed store: slice
+ *     k is rows [row_off[k], row_off[k+1]) of a (total_rows x ldx) matrix.
+ *   - No torch types, no global mutable state.
+ */
+#ifndef DPAR2_B200_H_
+#define DPAR2_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DP2_ABI_VERSION 1
+#define DP2_STATUS_WORDS 8
+
+enum dp2_status {
+  DP2_OK = 0,
+  DP2_ERR_NONFINITE = 1, /* NonFiniteInputError       (P/linalg.py:57-58, P/tensor.py:61) */
+  DP2_ERR_NOCONV = 2,    /* NumericFailure             (P/linalg.py:88-89)                 */
+  DP2_ERR_SHAPE = 3,     /* RankTooLarge/ShapeMismatch (P/compress.py:84-90)               */
+  DP2_ERR_CUDA = 4,      /* launch / runtime failure; see dp2_last_error()                 */
+  DP2_ERR_ARG = 5        /* invalid argument (ValueError in the reference)                 */
+};
+
+enum dp2_dtype { DP2_F64 = 0, DP2_F32 = 1 };
+
+/* Device view of a packed irregular tensor plus its work plan.  The plan
+ * splits the global row space into ``nseg`` equal segments (one persistent
+ * CTA each); a "piece" is the intersection of a segment with a slice.  Build
+ * the host arrays with dp2_plan_pieces and copy them to the device. */
+typedef struct dp2_store {
+  const void* X;              /* device, total_rows x ldx, dtype; cols [J, ldx) zero  */
+  int32_t dtype;              /* dp2_dtype                                            */
+  int32_t nseg;               /* segments (CTAs of a streaming pass)                  */
+  int64_t ldx;                /* row stride in elements, ldx*size % 16 == 0           */
+  int64_t J;                  /* shared column count                                  */
+  int64_t K;                  /* slice count                                          */
+  int64_t total_rows;         /* sum_k I_k                                            */
+  int64_t npieces;            /* pieces in the plan                                   */
+  const int64_t* row_off;     /* device, K+1                                          */
+  const int32_t* piece_slice; /* device, npieces                                      */
+  const int64_t* piece_row0;  /* device, npieces: first global row of the piece       */
+  const int32_t* piece_rows;  /* device, npieces                                      */
+  const int32_t* seg_begin;   /* device, nseg+1: pieces of segment g                  */
+  const int32_t* slice_piece; /* device, K+1: pieces of slice k (contiguous)          */
+} dp2_store;
+
+/* ------------------------------------------------------------------ misc */
+int dp2_abi_version(void);
+const char* dp2_status_string(int status);
+const char* dp2_last_error(void);
+int dp2_device_sm_count(void);
+/* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
+int dp2_status_init(int64_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------ host planning
+ * Alg. 4 LPT partition, bit-exact with P/scheduler.py:29-51 (greedy_partition):
+ * visit slices by (-count, index); each goes to the lightest set, lowest set
+ * index on ties.  order_out[K] = visit order, owner_out[K] = set of slice k,
+ * loads_out[workers] = row loads.  Returns DP2_ERR_ARG like the reference's
+ * ValueError (P/scheduler.py:39-44). */
+int dp2_greedy_partition(const int64_t* row_counts, int64_t K, int32_t workers, int64_t* order_out,
+                         int32_t* owner_out, int64_t* loads_out);
+/* Upper bound on pieces for (K, nseg). */
+int64_t dp2_piece_capacity(int64_t K, int32_t nseg);
+/* Split rows [0, row_off[K]) into nseg equal segments, cut at slice bounds.
+ * Host arrays; sizes as in dp2_store.  Replaces the reference's per-thread
+ * slice groups (P/compress.py:93-105) with equal-row persistent segments. */
+int dp2_plan_pieces(const int64_t* row_off, int64_t K, int32_t nseg, int32_t* piece_slice,
+                    int64_t* piece_row0, int32_t* piece_rows, int32_t* seg_begin,
+                    int32_t* slice_piece, int64_t* npieces_out);
+
+/* ------------------------------------------------------------------ tensor checks
+ * Per-slice squared Frobenius norms (sqnorm_dev[K]) and the lowest slice with
+ * a NaN/Inf (status[0]); mirrors IrregularTensor's isfinite check
+ * (P/tensor.py:61) and total_sq_norm (P/tensor.py:79-80). */
+int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------ stage 1
+ * Per-slice randomized SVD (P/linalg.py:97-132 with power_iters = 1, as called
+ * from P/compress.py:96-105), two streaming passes over X:
+ *   pass 1: Z_k = X_k^T (X_k Omega_k)         -> Q_Z = orth(Z_k)
+ *   pass 2: Y_k = X_k Q_Z, C_k = Y_k^T X_k    -> range(Y_k) = range of the
+ *           reference's X (X^T X Omega) sketch; B_k = Q^T X_k via G = Y^T Y.
+ * Outputs: A_out (total_rows x rank) = U of each slice with the sign rule of
+ * P/linalg.py:62-70; M_out (J x K*rank, row-major) = [V_k S_k] in slice order
+ * (P/compress.py:108); rank_out[K] = numerical rank found (>= rank unless the
+ * slice is rank deficient, where A is completed orthonormally).
+ * omega_dev: K x J x sp (slice k's J x s_k Gaussian in the first s_k columns,
+ * zero padded; P/linalg.py:122-123).  s_dev[K] = per-slice sketch width.
+ * timing_ms (host, nullable, >= 8 floats): per-phase CUDA-event times
+ * [sketch1, orth, sketch2, factor, signs+A, total]; forces a sync. */
+size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank);
+int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
+               int32_t rank, double* A_out, double* M_out, int32_t* rank_out, void* ws,
+               size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
+
+/* ------------------------------------------------------------------ stage 2
+ * Randomized SVD of M (J x KR) (P/compress.py:109-111): D (J x rank), E (rank),
+ * F (KR x rank), sign rule on D.  omega2_dev: KR x s2 (P/linalg.py:122-123
+ * seeded with derived_seed(seed, K)). */
+size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank);
+int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2,
+               int32_t rank, double* D_out, double* E_out, double* F_out, void* ws, size_t ws_bytes,
+               int64_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------ ALS
+ * Compressed-space iterations (P/solver.py:152-190).  Inputs D (J x R), E (R),
+ * F (K*R x R); state H (R x R), V (J x R), W (K x R) in/out.  Runs up to
+ * max_iters iterations with the reference's stop rule on the device
+ * (``prev == 0 || |prev - e| <= tol * prev``, P/solver.py:180-184); writes the
+ * objective trace, globaltimer stamps (ns, max_iters+1) and the executed
+ * iteration count; polar_out (K x R x R) holds Z_k P_k^T of the last executed
+ * iteration.  use_graph != 0 captures the loop in a CUDA graph. */
+size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R);
+int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
+                double* H, double* V, double* W, double* polar_out, int32_t max_iters, double tol,
+                int32_t normalize, double* trace_out, int64_t* tstamp_out, int32_t* iters_out,
+                int32_t use_graph, void* ws, size_t ws_bytes, int64_t* status_dev, void* stream);
+
+/* Kernel-granular entry points (the reference's test-level API,
+ * P/solver.py:48-149).  theta (K x R x R) = (P_k Z_k^T) F_k. */
+int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J,
+                         int32_t R, const double* H, const double* V, const double* W,
+                         double* polar_out, double* theta_out, void* ws, size_t ws_bytes,
+                         int64_t* status_dev, void* stream);
+/* mode 1: out R x R (P/solver.py:81-89); mode 2: out J x R (:92-100);
+ * mode 3: out K x R (:103-111). */
+int dp2_mttkrp(int32_t mode, const double* theta, const double* D, const double* E, int64_t K,
+               int64_t J, int32_t R, const double* H, const double* V, const double* W, double* out,
+               void* ws, size_t ws_bytes, void* stream);
+/* One Gauss-Seidel sweep (P/solver.py:114-130); H, V, W updated in place. */
+int dp2_update_factors(const double* theta, const double* D, const double* E, int64_t K, int64_t J,
+                       int32_t R, double* H, double* V, double* W, int32_t normalize, void* ws,
+                       size_t ws_bytes, int64_t* status_dev, void* stream);
+/* e = sum_k ||Theta_k E D^T - (H * w_k) V^T||_F^2 (P/solver.py:133-149);
+ * out: one device double. */
+int dp2_convergence_metric(const double* theta, const double* D, const double* E, int64_t K,
+                           int64_t J, int32_t R, const double* H, const double* V, const double* W,
+                           double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ outputs
+ * Q_k = A_k (Z_k P_k^T) for every slice (P/solver.py:186-189). */
+int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar,
+                   double* Q_out, void* stream);
+/* fitness terms (P/analysis.py:23-45): out2_dev[0] = sum ||X_k||^2,
+ * out2_dev[1] = sum ||X_k - Q_k (H * w_k) V^T||^2, fixed-order reductions. */
+size_t dp2_fitness_workspace(const dp2_store* st);
+int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H, const double* V,
+                const double* W, double* out2_dev, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPAR2_B200_H_ */

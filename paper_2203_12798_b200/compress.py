@@ -1,0 +1,180 @@
+"""Two-stage compression on the GPU (P/compress.py:34-119).
+
+``compress`` keeps the reference signature and semantics: rank checks with the
+same messages, per-slice sketch seeds ``derived_seed(seed, k)``, M in slice
+order, stage-2 seed ``derived_seed(seed, K)``; ``plan`` / ``threads`` are
+accepted (they never change values in the reference either).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NumericFailure, RankTooLargeError
+from .linalg import RsvdParams, derived_seed, padded_width, sketch_width
+from .rng import omega_host, stage2_omega
+from .scheduler import resolve_threads
+from .tensor import IrregularTensor, new_status, sm_count, stream_ptr
+
+
+def _vp(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def workspace(nbytes, dev):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+@dataclass
+class CompressedTensor:
+    """A_k (I_k x R, column-orthonormal), D (J x R), E (R), F (KR x R).
+
+    Device tensors; ``slice_bases`` are views into the packed A buffer.
+    """
+
+    rank: int
+    A: torch.Tensor            # (sum I_k, R) packed slice bases
+    row_off: np.ndarray        # (K+1,)
+    col_basis: torch.Tensor    # D
+    weights: torch.Tensor      # E
+    cores: torch.Tensor        # F
+    rank_found: torch.Tensor | None = None
+
+    @property
+    def num_slices(self):
+        return len(self.row_off) - 1
+
+    @property
+    def num_cols(self):
+        return self.col_basis.shape[0]
+
+    @property
+    def row_counts(self):
+        return [int(b - a) for a, b in zip(self.row_off[:-1], self.row_off[1:])]
+
+    @property
+    def slice_bases(self):
+        return [self.A[a:b] for a, b in zip(self.row_off[:-1], self.row_off[1:])]
+
+    def core_block(self, k):
+        r = self.rank
+        return self.cores[k * r:(k + 1) * r]
+
+    def core_stack(self):
+        return self.cores.reshape(self.num_slices, self.rank, self.rank)
+
+    def float_count(self):
+        """sum(I_k) R + K R^2 + J R + R (P/compress.py:65-72)."""
+        return int(self.A.numel() + self.cores.numel() + self.col_basis.numel() + self.weights.numel())
+
+    def numpy(self):
+        a = self.A.cpu().numpy()
+        return dict(slice_bases=[a[x:y] for x, y in zip(self.row_off[:-1], self.row_off[1:])],
+                    col_basis=self.col_basis.cpu().numpy(), weights=self.weights.cpu().numpy(),
+                    cores=self.cores.cpu().numpy())
+
+
+def nseg_for(tensor: IrregularTensor):
+    """Persistent segments of the streaming passes: 1 CTA/SM for f64 tiles,
+    2 for f32 (smem-limited)."""
+    return sm_count() * (1 if tensor.dtype == "f64" else 2)
+
+
+def check_status(status, what):
+    s = status.cpu().tolist()
+    if s[0] != _lib.INT64_MAX:
+        from .errors import NonFiniteInputError
+        raise NonFiniteInputError(f"slice {s[0]} contains non-finite values")
+    if s[1] > 0:
+        raise NumericFailure(f"{what}: Jacobi iteration did not converge")
+    if s[3] != _lib.INT64_MAX:
+        raise NumericFailure("SVD did not converge", slice_index=int(s[3]))
+    return s
+
+
+def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
+             plan=None, threads=None, timings=None):
+    """Compress ``tensor`` at ``rank`` with two randomized-SVD stages."""
+    if not isinstance(tensor, IrregularTensor):
+        tensor = IrregularTensor(tensor)
+    if rank < 1:
+        raise RankTooLargeError(f"rank must be >= 1, got {rank}")
+    if rank > tensor.num_cols:
+        raise RankTooLargeError(f"rank {rank} exceeds column count {tensor.num_cols}")
+    for k, rows in enumerate(tensor.row_counts):
+        if rank > rows:
+            raise RankTooLargeError(f"rank {rank} exceeds row count {rows} of slice {k}")
+    if rank > 64:
+        raise RankTooLargeError(f"rank {rank} exceeds the device limit of 64")
+    resolve_threads(threads)
+    base = rsvd if rsvd is not None else RsvdParams(rank=rank)
+    if base.power_iters != 1:
+        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
+    J, K = tensor.num_cols, tensor.num_slices
+    widths = [sketch_width(m, J, rank, base.oversampling) for m in tensor.row_counts]
+    sp = padded_width(max(widths))
+    dev = tensor.X.device
+    t0 = time.perf_counter()
+    om_host = omega_host(base.seed, J, widths, sp)
+    omega = om_host.to(dev, non_blocking=True)
+    s_dev = torch.tensor(widths, dtype=torch.int32).to(dev, non_blocking=True)
+    t_omega = time.perf_counter() - t0
+    nseg = nseg_for(tensor)
+    st, keep = tensor.store(nseg)
+    lib = _lib.lib()
+    A = torch.empty((int(tensor.row_off_host[-1]), rank), dtype=torch.float64, device=dev)
+    M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
+    rank_found = torch.empty(K, dtype=torch.int32, device=dev)
+    status = new_status(dev)
+    ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), dev)
+    tm = (C.c_float * 8)() if timings is not None else None
+    _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
+                              _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
+    del ws
+    # stage 2 (P/compress.py:109-111)
+    second = stage2 if stage2 is not None else base
+    second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
+    if second.power_iters != 1:
+        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
+    KR = K * rank
+    s2 = sketch_width(J, KR, rank, second.oversampling)
+    om2 = torch.from_numpy(stage2_omega(second.seed, KR, s2)).to(dev)
+    D = torch.empty((J, rank), dtype=torch.float64, device=dev)
+    E = torch.empty(rank, dtype=torch.float64, device=dev)
+    F = torch.empty((KR, rank), dtype=torch.float64, device=dev)
+    ws2 = workspace(lib.dp2_stage2_workspace(J, KR, s2, rank), dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timings is not None else None
+    if ev:
+        ev[0].record()
+    _lib.check(lib.dp2_stage2(_vp(M), J, KR, _vp(om2), s2, rank, _vp(D), _vp(E), _vp(F), _vp(ws2), ws2.numel(),
+                              _vp(status), stream_ptr()), "stage2")
+    if ev:
+        ev[1].record()
+    check_status(status, "compress")
+    if timings is not None:
+        torch.cuda.synchronize()
+        timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
+                       stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
+                       stage1_ms=tm[5], stage2_ms=ev[0].elapsed_time(ev[1]), sp=sp, s2=s2, nseg=nseg,
+                       npieces=int(st.npieces))
+    del keep
+    return CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
+                            cores=F, rank_found=rank_found)
+
+
+def reconstruct_slice(comp: CompressedTensor, k):
+    """A_k (F_k (diag(E) D^T)) (P/compress.py:122-127)."""
+    if not 0 <= k < comp.num_slices:
+        raise IndexError(f"slice index {k} out of range [0, {comp.num_slices})")
+    small = comp.core_block(k) @ (comp.weights[:, None] * comp.col_basis.T)
+    return comp.slice_bases[k] @ small
+
+
+def as_numpy_compressed(comp: CompressedTensor):
+    """Host NumPy copy laid out like the reference's CompressedTensor fields."""
+    return comp.numpy()

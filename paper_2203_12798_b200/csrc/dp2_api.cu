@@ -1,0 +1,225 @@
+// extern "C" entry points of libdpar2_b200.so (declared in include/dpar2_b200.h).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "dp2_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return DP2_ERR_CUDA;
+}
+int fail_arg(const char* msg) {
+  g_last_error = msg;
+  return DP2_ERR_ARG;
+}
+bool store_ok(const dp2_store* st) {
+  if (!st || !st->X || st->J < 1 || st->K < 1 || st->ldx < st->J || st->nseg < 1) return false;
+  const int elem = st->dtype == DP2_F64 ? 8 : 4;
+  return (st->ldx * elem) % 16 == 0 && (st->dtype == DP2_F64 || st->dtype == DP2_F32);
+}
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+int dp2_abi_version(void) { return DP2_ABI_VERSION; }
+
+const char* dp2_status_string(int s) {
+  switch (s) {
+    case DP2_OK: return "ok";
+    case DP2_ERR_NONFINITE: return "non-finite input";
+    case DP2_ERR_NOCONV: return "iteration did not converge";
+    case DP2_ERR_SHAPE: return "shape / rank error";
+    case DP2_ERR_CUDA: return "CUDA error";
+    case DP2_ERR_ARG: return "invalid argument";
+    default: return "unknown status";
+  }
+}
+
+const char* dp2_last_error(void) { return g_last_error.c_str(); }
+
+int dp2_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+int dp2_status_init(int64_t* status_dev, void* stream) {
+  int64_t init[DP2_STATUS_WORDS] = {INT64_MAX, 0, INT64_MAX, INT64_MAX, 0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(status_dev, init, sizeof(init), cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_status_init");
+}
+
+// ---------------------------------------------------------------- planning
+int dp2_greedy_partition(const int64_t* counts, int64_t K, int32_t workers, int64_t* order_out,
+                         int32_t* owner_out, int64_t* loads_out) {
+  if (K < 1) return fail_arg("need at least one slice");
+  if (workers < 1) return fail_arg("need at least one worker");
+  for (int64_t k = 0; k < K; ++k)
+    if (counts[k] < 1) return fail_arg("row counts must be positive");
+  std::vector<int64_t> order(K);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return counts[a] != counts[b] ? counts[a] > counts[b] : a < b;
+  });
+  std::vector<int64_t> loads(workers, 0);
+  for (int64_t i = 0; i < K; ++i) {
+    const int64_t k = order[i];
+    int t = 0;
+    for (int w = 1; w < workers; ++w)
+      if (loads[w] < loads[t]) t = w;  // lowest index on ties
+    owner_out[k] = t;
+    loads[t] += counts[k];
+    order_out[i] = k;
+  }
+  for (int w = 0; w < workers; ++w) loads_out[w] = loads[w];
+  return DP2_OK;
+}
+
+int64_t dp2_piece_capacity(int64_t K, int32_t nseg) { return K + nseg; }
+
+int dp2_plan_pieces(const int64_t* row_off, int64_t K, int32_t nseg, int32_t* piece_slice,
+                    int64_t* piece_row0, int32_t* piece_rows, int32_t* seg_begin, int32_t* slice_piece,
+                    int64_t* npieces_out) {
+  if (K < 1 || nseg < 1) return fail_arg("bad plan arguments");
+  const int64_t N = row_off[K];
+  if (N < 1) return fail_arg("empty tensor");
+  int64_t np = 0;
+  int64_t k = 0;
+  for (int32_t g = 0; g < nseg; ++g) {
+    const int64_t a = N * g / nseg, b = N * (g + 1) / nseg;
+    seg_begin[g] = (int32_t)np;
+    int64_t r = a;
+    while (r < b) {
+      while (row_off[k + 1] <= r) ++k;
+      const int64_t e = std::min<int64_t>(b, row_off[k + 1]);
+      if (e - r > INT32_MAX) return fail_arg("piece too large");
+      piece_slice[np] = (int32_t)k;
+      piece_row0[np] = r;
+      piece_rows[np] = (int32_t)(e - r);
+      ++np;
+      r = e;
+    }
+  }
+  seg_begin[nseg] = (int32_t)np;
+  // slice -> first piece (pieces are in global row order, hence slice order)
+  int64_t p = 0;
+  for (int64_t s = 0; s <= K; ++s) {
+    while (p < np && piece_slice[p] < s) ++p;
+    slice_piece[s] = (int32_t)p;
+  }
+  *npieces_out = np;
+  return DP2_OK;
+}
+
+// ---------------------------------------------------------------- device calls
+int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream) {
+  if (!store_ok(st)) return fail_arg("invalid store");
+  cudaError_t e = dp2::run_slice_stats(st, sqnorm_dev, status_dev, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_slice_stats");
+}
+
+size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
+  return dp2::stage1_layout(st, sp, rank).total;
+}
+
+int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
+               double* A_out, double* M_out, int32_t* rank_out, void* ws, size_t ws_bytes,
+               int64_t* status_dev, float* timing_ms, void* stream) {
+  if (!store_ok(st)) return fail_arg("invalid store");
+  if (rank < 1 || rank > 64 || sp < rank || sp % 8 != 0 || (sp > 32 && sp % 32 != 0) || sp > 256)
+    return fail_arg("invalid rank / sketch width");
+  if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
+  cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
+                                  static_cast<char*>(ws), status_dev, timing_ms, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_stage1");
+}
+
+size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {
+  return dp2::stage2_bytes(J, KR, s2, rank);
+}
+
+int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2, int32_t rank,
+               double* D_out, double* E_out, double* F_out, void* ws, size_t ws_bytes, int64_t* status_dev,
+               void* stream) {
+  if (rank < 1 || rank > 64 || s2 < rank || s2 > 150 || J < 1 || KR < 1) return fail_arg("invalid stage-2 shape");
+  if (ws_bytes < dp2::stage2_bytes(J, KR, s2, rank)) return fail_arg("workspace too small");
+  cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
+                                  static_cast<char*>(ws), status_dev, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_stage2");
+}
+
+size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }
+
+int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R, double* H,
+                double* V, double* W, double* polar_out, int32_t max_iters, double tol, int32_t normalize,
+                double* trace_out, int64_t* tstamp_out, int32_t* iters_out, int32_t use_graph, void* ws,
+                size_t ws_bytes, int64_t* status_dev, void* stream) {
+  if (max_iters < 1) return fail_arg("max_iters must be >= 1");
+  if (R < 1 || R > 64 || K < 1 || J < 1) return fail_arg("invalid ALS shape");
+  if (ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("workspace too small");
+  cudaError_t e = dp2::als_run(F, D, E, K, J, R, H, V, W, polar_out, max_iters, tol, normalize, trace_out,
+                               tstamp_out, iters_out, use_graph, static_cast<char*>(ws), status_dev, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_als_run");
+}
+
+int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
+                         const double* H, const double* V, const double* W, double* polar_out, double* theta_out,
+                         void* ws, size_t ws_bytes, int64_t* status_dev, void* stream) {
+  if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::als_rotations(F, D, E, K, J, R, H, V, W, polar_out, theta_out, static_cast<char*>(ws),
+                                     status_dev, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_update_rotations");
+}
+
+int dp2_mttkrp(int32_t mode, const double* theta, const double* D, const double* E, int64_t K, int64_t J,
+               int32_t R, const double* H, const double* V, const double* W, double* out, void* ws,
+               size_t ws_bytes, void* stream) {
+  if (mode < 1 || mode > 3 || R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R))
+    return fail_arg("invalid arguments");
+  cudaError_t e = dp2::als_mttkrp(mode, theta, D, E, K, J, R, H, V, W, out, static_cast<char*>(ws), S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_mttkrp");
+}
+
+int dp2_update_factors(const double* theta, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
+                       double* H, double* V, double* W, int32_t normalize, void* ws, size_t ws_bytes,
+                       int64_t* status_dev, void* stream) {
+  if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::als_update_factors(theta, D, E, K, J, R, H, V, W, normalize, static_cast<char*>(ws),
+                                          status_dev, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_update_factors");
+}
+
+int dp2_convergence_metric(const double* theta, const double* D, const double* E, int64_t K, int64_t J,
+                           int32_t R, const double* H, const double* V, const double* W, double* out, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::als_metric(theta, D, E, K, J, R, H, V, W, out, static_cast<char*>(ws), S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_convergence_metric");
+}
+
+int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar, double* Q_out,
+                   void* stream) {
+  if (!store_ok(st) || R < 1 || R > 64) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::run_assemble_q(st, A, R, polar, Q_out, S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_assemble_q");
+}
+
+size_t dp2_fitness_workspace(const dp2_store* st) { return dp2::fitness_bytes(st); }
+
+int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H, const double* V,
+                const double* W, double* out2_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!store_ok(st) || R < 1 || R > 64 || ws_bytes < dp2::fitness_bytes(st)) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::run_fitness(st, Q, R, H, V, W, out2_dev, static_cast<char*>(ws), S(stream));
+  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_fitness");
+}
+
+}  // extern "C"

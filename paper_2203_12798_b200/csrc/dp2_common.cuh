@@ -1,0 +1,246 @@
+// Shared device helpers for the DPar2 B200 kernels (sm_100a).
+//
+// Everything numeric that is not a streaming pass lives here: warp/block
+// reductions, the fp64 m8n8k4 tensor-core MMA wrapper, a block-cooperative
+// cyclic Jacobi eigensolver for small symmetric matrices (the reference uses
+// LAPACK gesdd on the same tiny matrices: P/linalg.py:87,143) and a warp
+// one-sided Jacobi polar factor (P/solver.py:59 only ever consumes Z_k P_k^T).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/dpar2_b200.h"
+
+#define DP2_DEV __device__ __forceinline__
+
+namespace dp2 {
+
+constexpr double kEps = 1.1102230246251565e-16;  // 2^-53
+
+// ---------------------------------------------------------------- status
+// Device-side status block (int64 x 8), read by the host after a sync.
+//   [0] lowest slice index holding a non-finite value (INT64_MAX = none)
+//   [1] count of Jacobi sweeps that hit the cap (no convergence)
+//   [2] lowest slice index whose sketch had numerical rank < R
+//   [3] lowest slice index with a failed polar factor
+enum { ST_NONFINITE = 0, ST_NOCONV = 1, ST_RANKDEF = 2, ST_POLAR = 3 };
+
+DP2_DEV void status_min(int64_t* st, int slot, int64_t v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(st + slot), (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------- reductions
+DP2_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum: warp tree, then warp 0 sums the warp results in
+// warp order.  ``red`` must hold >= 32 doubles.  All threads get the result.
+DP2_DEV double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < nw ? red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) red[0] = t;
+  }
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- fp64 MMA
+// D(8x8) += A(8x4, row) * B(4x8, col); one double of A and B per lane,
+// two of C/D.  Fragment layout (PTX ISA, mma.m8n8k4.f64):
+//   a0 = A[lane>>2][lane&3]   b0 = B[lane&3][lane>>2]
+//   c0,c1 = C[lane>>2][2*(lane&3) + {0,1}]
+DP2_DEV void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- cp.async
+DP2_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+DP2_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+DP2_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---------------------------------------------------------------- pairing
+// Round-robin ("chess tournament") ordering for parallel Jacobi: in round r
+// of n_even-1 rounds, pair i couples positions i and n_even-1-i; position 0
+// is fixed, the others rotate.  Index n (odd n padding) is a dummy.
+DP2_DEV void rr_pair(int n_even, int r, int i, int& p, int& q) {
+  auto at = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + r) % (n_even - 1)); };
+  p = at(i);
+  q = at(n_even - 1 - i);
+  if (p > q) { int t = p; p = q; q = t; }
+}
+
+// ---------------------------------------------------------------- Jacobi eig
+// Block-cooperative cyclic Jacobi for a symmetric n x n matrix A (row-major,
+// leading dim lda, shared memory).  On return diag(A) holds the eigenvalues and
+// V (n x n, ldv) the eigenvectors as columns.  ``cs`` needs 3*(n/2+1) doubles
+// and ``flag`` one int of shared scratch.  Rotations are skipped when
+// |a_pq| <= eps * sqrt(|a_pp a_qq|) (relative criterion: PSD inputs keep
+// high relative accuracy in their small eigenvalues).  Returns sweeps used
+// (max_sweeps+1 on no convergence).
+DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, double* cs, int* flag,
+                             int max_sweeps = 40) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < n * n; i += nt) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
+  if (n < 2) { __syncthreads(); return 0; }
+  const int ne = n + (n & 1), np = ne / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < ne - 1; ++r) {
+      for (int i = tid; i < np; i += nt) {
+        int p, q;
+        rr_pair(ne, r, i, p, q);
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = A[p * lda + q], app = A[p * lda + p], aqq = A[q * lda + q];
+          if (apq != 0.0 && fabs(apq) > kEps * sqrt(fabs(app * aqq))) {
+            const double th = (aqq - app) / (2.0 * apq);
+            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            *flag = 1;
+          }
+        }
+        cs[3 * i] = c;
+        cs[3 * i + 1] = s;
+        cs[3 * i + 2] = (double)(p * 1024 + q);
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int it = tid; it < n * np; it += nt) {
+        const int i = it / np, pr = it % np;
+        const double s = cs[3 * pr + 1];
+        if (s == 0.0) continue;
+        const double c = cs[3 * pr];
+        const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
+        double a = A[i * lda + p], b = A[i * lda + q];
+        A[i * lda + p] = c * a - s * b;
+        A[i * lda + q] = s * a + c * b;
+        a = V[i * ldv + p];
+        b = V[i * ldv + q];
+        V[i * ldv + p] = c * a - s * b;
+        V[i * ldv + q] = s * a + c * b;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int it = tid; it < n * np; it += nt) {
+        const int pr = it / n, j = it % n;
+        const double s = cs[3 * pr + 1];
+        if (s == 0.0) continue;
+        const double c = cs[3 * pr];
+        const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
+        const double a = A[p * lda + j], b = A[q * lda + j];
+        A[p * lda + j] = c * a - s * b;
+        A[q * lda + j] = s * a + c * b;
+      }
+      __syncthreads();
+      for (int i = tid; i < np; i += nt) {
+        if (cs[3 * i + 1] == 0.0) continue;
+        const int pq = (int)cs[3 * i + 2], p = pq >> 10, q = pq & 1023;
+        A[p * lda + q] = 0.0;
+        A[q * lda + p] = 0.0;
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  return sweep + 1;
+}
+
+// Sort eigenpairs by descending eigenvalue (stable on index): writes the
+// permutation into ``perm`` (n ints, shared).  Single-threaded; n is tiny.
+DP2_DEV void sort_desc_perm(const double* A, int lda, int n, int* perm) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int i = 1; i < n; ++i) {
+      int v = perm[i];
+      double key = A[v * lda + v];
+      int j = i - 1;
+      while (j >= 0 && A[perm[j] * lda + perm[j]] < key) { perm[j + 1] = perm[j]; --j; }
+      perm[j + 1] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- polar
+// Warp one-sided (Hestenes) Jacobi on the columns of T (n x n, column-major,
+// leading dim ldt, shared).  On return T's columns are mutually orthogonal
+// (T_final = T0 Vr) and Vr (column-major, ldv) holds the accumulated right
+// rotations, so T0 = Z Sigma Vr^T with Z = normalised columns of T_final.
+// ``Vr`` may be pre-loaded with a warm-start orthogonal matrix when T0 was
+// already multiplied by it.  Lane i owns pair i (n <= 64).
+DP2_DEV int jacobi_onesided_warp(double* T, int ldt, double* Vr, int ldv, int n, int max_sweeps = 60) {
+  const int lane = threadIdx.x & 31;
+  if (n < 2) return 0;
+  const int ne = n + (n & 1), np = ne / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < ne - 1; ++r) {
+      for (int i = lane; i < np; i += 32) {
+        int p, q;
+        rr_pair(ne, r, i, p, q);
+        if (q >= n) continue;
+        double* tp = T + p * ldt;
+        double* tq = T + q * ldt;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int k = 0; k < n; ++k) {
+          const double x = tp[k], y = tq[k];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        if (ga != 0.0 && fabs(ga) > kEps * sqrt(al * be)) {
+          const double ze = (be - al) / (2.0 * ga);
+          const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
+          const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+          for (int k = 0; k < n; ++k) {
+            const double x = tp[k], y = tq[k];
+            tp[k] = c * x - s * y;
+            tq[k] = s * x + c * y;
+          }
+          double* vp = Vr + p * ldv;
+          double* vq = Vr + q * ldv;
+          for (int k = 0; k < n; ++k) {
+            const double x = vp[k], y = vq[k];
+            vp[k] = c * x - s * y;
+            vq[k] = s * x + c * y;
+          }
+          rotated = 1;
+        }
+      }
+      __syncwarp();
+    }
+    rotated = __any_sync(0xffffffffu, rotated);
+    if (!rotated) break;
+  }
+  return sweep + 1;
+}
+
+DP2_DEV int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+}  // namespace dp2

@@ -1,0 +1,55 @@
+// Host-side declarations shared between the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/dpar2_b200.h"
+
+namespace dp2 {
+
+struct Stage1Layout {
+  size_t part, qz, y2, Pm, Sv, Vt, cand_abs, cand_row, cand_neg, xsq, scr, total;
+};
+Stage1Layout stage1_layout(const dp2_store* st, int sp, int R);
+cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
+                       double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
+                       float* timing, cudaStream_t stream);
+cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                       double* xsq_part, int64_t* status, cudaStream_t stream);
+
+size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R);
+cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
+                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t stream);
+
+size_t als_bytes(int64_t K, int64_t J, int R);
+struct AlsCtx;  // defined in dp2_als.cu
+cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
+                    double* H, double* V, double* W, double* polar, int max_iters, double tol,
+                    int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
+                    char* ws, int64_t* status, cudaStream_t stream);
+cudaError_t als_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
+                          const double* H, const double* V, const double* W, double* polar,
+                          double* theta, char* ws, int64_t* status, cudaStream_t stream);
+cudaError_t als_mttkrp(int mode, const double* theta, const double* D, const double* E, int64_t K,
+                       int64_t J, int R, const double* H, const double* V, const double* W, double* out,
+                       char* ws, cudaStream_t stream);
+cudaError_t als_update_factors(const double* theta, const double* D, const double* E, int64_t K,
+                               int64_t J, int R, double* H, double* V, double* W, int normalize,
+                               char* ws, int64_t* status, cudaStream_t stream);
+cudaError_t als_metric(const double* theta, const double* D, const double* E, int64_t K, int64_t J,
+                       int R, const double* H, const double* V, const double* W, double* out, char* ws,
+                       cudaStream_t stream);
+
+cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const double* polar, double* Q,
+                           cudaStream_t stream);
+size_t fitness_bytes(const dp2_store* st);
+cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const double* H, const double* V,
+                        const double* W, double* out2, char* ws, cudaStream_t stream);
+cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status, cudaStream_t stream);
+
+// shared small kernels (stage 1 / stage 2)
+__global__ void cgs2_kernel(double* Q, int64_t rows, int ld, int ncols, int64_t batch_stride);
+
+}  // namespace dp2

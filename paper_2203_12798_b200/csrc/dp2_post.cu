@@ -1,0 +1,151 @@
+// Tensor checks, final Q assembly and fitness.
+//   slice_stats : isfinite + squared norms per slice (P/tensor.py:61,79-80)
+//   assemble_q  : Q_k = A_k (Z_k P_k^T)                (P/solver.py:186-189)
+//   fitness     : sum ||X_k||^2, sum ||X_k - Q_k (H*w_k) V^T||^2 in one pass
+//                 over X (P/analysis.py:23-45)
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+
+template <typename T>
+__global__ void __launch_bounds__(256) slice_stats_kernel(const T* X, int64_t ldx, int64_t J,
+                                                          const int64_t* row_off, double* sqnorm,
+                                                          int64_t* status) {
+  __shared__ double red[32];
+  const int64_t k = blockIdx.x;
+  const int64_t r0 = row_off[k], r1 = row_off[k + 1];
+  double s = 0.0;
+  int bad = 0;
+  const int64_t n = (r1 - r0) * J;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const double v = (double)X[(r0 + e / J) * ldx + e % J];
+    s = fma(v, v, s);
+    bad |= !isfinite(v);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) sqnorm[k] = s;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) status_min(status, ST_NONFINITE, k);
+}
+
+__global__ void __launch_bounds__(256) assemble_q_kernel(const double* A, const int32_t* piece_slice,
+                                                          const int64_t* piece_row0, const int32_t* piece_rows,
+                                                          int R, const double* polar, double* Q) {
+  extern __shared__ double pis[];
+  const int p = blockIdx.x;
+  const int64_t k = piece_slice[p];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) pis[e] = polar[k * R * R + e];
+  __syncthreads();
+  const int64_t r0 = piece_row0[p], nr = piece_rows[p];
+  for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) {
+    const int64_t i = r0 + e / R;
+    const int c = (int)(e % R);
+    double acc = 0.0;
+    for (int d = 0; d < R; ++d) acc = fma(A[i * R + d], pis[d * R + c], acc);
+    Q[i * R + c] = acc;
+  }
+}
+
+// one warp per row: u = q H * w_k (R), recon_j = sum_a u_a V[j][a]
+template <typename T>
+__global__ void __launch_bounds__(256) fitness_kernel(const T* X, int64_t ldx, int64_t J,
+                                                      const int32_t* piece_slice, const int64_t* piece_row0,
+                                                      const int32_t* piece_rows, const double* Q, int R,
+                                                      const double* H, const double* V, const double* W,
+                                                      int v_in_smem, double* part) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  double* Hs = sm;                 // R x R
+  double* us = Hs + R * R;         // 8 warps x R
+  double* Vs = us + 8 * R;         // J x R (optional)
+  const int p = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t k = piece_slice[p];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) Hs[e] = H[e] * W[k * R + e % R];
+  if (v_in_smem)
+    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) Vs[e] = V[e];
+  __syncthreads();
+  const double* Vp = v_in_smem ? Vs : V;
+  const int64_t r0 = piece_row0[p], nr = piece_rows[p];
+  double tot = 0.0, res = 0.0;
+  double* u = us + warp * R;
+  for (int64_t i = r0 + warp; i < r0 + nr; i += 8) {
+    for (int c = lane; c < R; c += 32) {
+      double acc = 0.0;
+      for (int d = 0; d < R; ++d) acc = fma(Q[i * R + d], Hs[d * R + c], acc);
+      u[c] = acc;
+    }
+    __syncwarp();
+    for (int64_t j = lane; j < J; j += 32) {
+      double rec = 0.0;
+      for (int a = 0; a < R; ++a) rec = fma(u[a], Vp[j * R + a], rec);
+      const double x = (double)X[i * ldx + j];
+      const double d = x - rec;
+      tot = fma(x, x, tot);
+      res = fma(d, d, res);
+    }
+    __syncwarp();
+  }
+  tot = block_sum(tot, red);
+  res = block_sum(res, red);
+  if (threadIdx.x == 0) {
+    part[2 * (size_t)p] = tot;
+    part[2 * (size_t)p + 1] = res;
+  }
+}
+
+__global__ void fitness_reduce_kernel(const double* part, int64_t np, double* out2) {
+  if (threadIdx.x == 0) {
+    double t = 0.0, r = 0.0;
+    for (int64_t p = 0; p < np; ++p) {
+      t += part[2 * p];
+      r += part[2 * p + 1];
+    }
+    out2[0] = t;
+    out2[1] = r;
+  }
+}
+
+cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status, cudaStream_t stream) {
+  if (st->dtype == DP2_F64)
+    slice_stats_kernel<double><<<(unsigned)st->K, 256, 0, stream>>>(
+        static_cast<const double*>(st->X), st->ldx, st->J, st->row_off, sqnorm, status);
+  else
+    slice_stats_kernel<float><<<(unsigned)st->K, 256, 0, stream>>>(
+        static_cast<const float*>(st->X), st->ldx, st->J, st->row_off, sqnorm, status);
+  return cudaGetLastError();
+}
+
+cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const double* polar, double* Q,
+                           cudaStream_t stream) {
+  assemble_q_kernel<<<(unsigned)st->npieces, 256, (size_t)R * R * 8, stream>>>(
+      A, st->piece_slice, st->piece_row0, st->piece_rows, R, polar, Q);
+  return cudaGetLastError();
+}
+
+size_t fitness_bytes(const dp2_store* st) { return (size_t)st->npieces * 2 * 8 + 256; }
+
+cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const double* H, const double* V,
+                        const double* W, double* out2, char* ws, cudaStream_t stream) {
+  double* part = reinterpret_cast<double*>(ws);
+  const size_t vbytes = (size_t)st->J * R * 8;
+  const int vin = vbytes <= 160 * 1024;
+  const size_t smem = ((size_t)R * R + 8 * R) * 8 + (vin ? vbytes : 0);
+  cudaError_t e;
+  if (st->dtype == DP2_F64) {
+    e = cudaFuncSetAttribute(fitness_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fitness_kernel<double><<<(unsigned)st->npieces, 256, smem, stream>>>(
+        static_cast<const double*>(st->X), st->ldx, st->J, st->piece_slice, st->piece_row0, st->piece_rows, Q,
+        R, H, V, W, vin, part);
+  } else {
+    e = cudaFuncSetAttribute(fitness_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fitness_kernel<float><<<(unsigned)st->npieces, 256, smem, stream>>>(
+        static_cast<const float*>(st->X), st->ldx, st->J, st->piece_slice, st->piece_row0, st->piece_rows, Q,
+        R, H, V, W, vin, part);
+  }
+  fitness_reduce_kernel<<<1, 32, 0, stream>>>(part, st->npieces, out2);
+  return cudaGetLastError();
+}
+
+}  // namespace dp2

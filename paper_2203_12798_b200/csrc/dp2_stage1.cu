@@ -1,0 +1,788 @@
+// Stage 1: per-slice randomized SVD of every X_k (P/linalg.py:97-132 as
+// driven by P/compress.py:93-105), restated as two streaming passes over the
+// packed store plus small per-slice factorizations.
+//
+//   pass 1  Z_k  = X_k^T (X_k Omega_k)            (sketch_kernel, no Y store)
+//   orth    Q_Z  = CGS2(Z_k)                      (range-preserving: range(X Q_Z)
+//                                                  = range(X X^T X Omega) = the
+//                                                  reference's Y after q = 1)
+//   pass 2  Y_k  = X_k Q_Z (stored), C_k^T = X_k^T Y_k
+//   factor  G = Y^T Y = W L W^T, T = W L^-1/2 (Q = Y T orthonormal),
+//           B B^T = T^T (C C^T) T = U mu U^T,  P = T U_R, S = sqrt(mu_R),
+//           V_k = C_k^T P / S                     (= Q^T X's truncated SVD,
+//                                                  P/linalg.py:128-129)
+//   signs   A_k = Y_k P, largest-|.| entry of each column >= 0, first index
+//           on ties (P/linalg.py:62-70); M[:, kR:(k+1)R] = V_k S_k
+//           (P/compress.py:108)
+//
+// Work decomposition: the global row space is cut into equal segments, one
+// persistent CTA each; a CTA walks its pieces (segment x slice) tile by tile
+// and emits one partial per piece; per-slice reductions then sum the
+// partials in piece order, so results are deterministic for a fixed plan.
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+
+// ============================================================ sketch pass
+struct SketchParams {
+  const void* X;
+  int64_t ldx;
+  int J, sp, lds, njs;
+  const double* B;          // K x J x sp (Omega or Q_Z)
+  const int32_t* piece_slice;
+  const int64_t* piece_row0;
+  const int32_t* piece_rows;
+  const int32_t* seg_begin;
+  double* out_part;         // npieces x J x sp
+  double* y_out;            // total_rows x sp or null
+  double* xsq_part;         // npieces x njs or null
+  int64_t* status;
+};
+
+template <typename T, int TM, int MT, int NT>
+__global__ void __launch_bounds__(256, 1) sketch_kernel(SketchParams prm) {
+  constexpr int SG = 8 * NT, YP = SG + 2, YS = SG + 1, NW = 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int LDS = prm.lds, J = prm.J, sp = prm.sp;
+  T* xs = reinterpret_cast<T*>(smem);
+  const size_t xbytes = (((size_t)2 * TM * LDS * sizeof(T)) + 15) & ~(size_t)15;
+  double* ypart = reinterpret_cast<double*>(smem + xbytes);
+  double* ys = ypart + NW * TM * YP;
+  double* red = ys + TM * YS;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int seg = blockIdx.x, col0 = blockIdx.y * SG, jsplit = blockIdx.z;
+  const int jbase = jsplit * 64 * MT;
+  const bool stats = (blockIdx.y == 0) && prm.xsq_part != nullptr;
+  const int J4 = (J + 3) / 4;
+  const int cpr = (int)((J * (int)sizeof(T) + 15) / 16);        // 16B chunks per row
+  const int loaded_cols = cpr * 16 / (int)sizeof(T);
+
+  // zero the never-loaded pad columns of both buffers once
+  for (int i = tid; i < 2 * TM * LDS; i += blockDim.x)
+    if (i % LDS >= loaded_cols) xs[i] = T(0);
+
+  const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
+  if (pbeg >= pend) return;
+  const char* Xb = reinterpret_cast<const char*>(prm.X);
+
+  auto issue = [&](int buf, int p, int t) {
+    const int64_t row0 = prm.piece_row0[p] + (int64_t)t * TM;
+    const int rows = min(TM, prm.piece_rows[p] - t * TM);
+    char* dst = reinterpret_cast<char*>(xs + (size_t)buf * TM * LDS);
+    for (int i = tid; i < TM * cpr; i += blockDim.x) {
+      const int r = i / cpr, c = i % cpr;
+      const bool ok = r < rows;
+      const char* src = ok ? Xb + ((row0 + r) * prm.ldx) * (int64_t)sizeof(T) + (int64_t)c * 16 : Xb;
+      cp_async16(dst + ((size_t)r * LDS) * sizeof(T) + (size_t)c * 16, src, ok ? 16 : 0);
+    }
+  };
+
+  int p = pbeg, t = 0, buf = 0;
+  issue(0, p, 0);
+  cp_async_commit();
+
+  double zacc[MT][NT][2];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) zacc[a][b][0] = zacc[a][b][1] = 0.0;
+  double sq = 0.0;
+  int bad = 0;
+
+  while (true) {
+    int np = p, ntl = t + 1;
+    if (ntl * TM >= prm.piece_rows[p]) { np = p + 1; ntl = 0; }
+    const bool has_next = np < pend;
+    if (has_next) issue(buf ^ 1, np, ntl);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    const T* X = xs + (size_t)buf * TM * LDS;
+    const int ks = prm.piece_slice[p];
+    const double* Bm = prm.B + (size_t)ks * J * sp + col0;
+
+    // ---- phase A: Y_t = X_t B (split-K over warps)
+    double ya[TM / 8][NT][2];
+#pragma unroll
+    for (int a = 0; a < TM / 8; ++a)
+#pragma unroll
+      for (int b = 0; b < NT; ++b) ya[a][b][0] = ya[a][b][1] = 0.0;
+    for (int kk = warp; kk < J4; kk += NW) {
+      const int kr = kk * 4 + (lane & 3);
+      double bf[NT];
+#pragma unroll
+      for (int b = 0; b < NT; ++b) bf[b] = kr < J ? __ldg(Bm + (size_t)kr * sp + b * 8 + (lane >> 2)) : 0.0;
+#pragma unroll
+      for (int a = 0; a < TM / 8; ++a) {
+        const double av = (double)X[(a * 8 + (lane >> 2)) * LDS + kr];
+#pragma unroll
+        for (int b = 0; b < NT; ++b) dmma_8x8x4(ya[a][b][0], ya[a][b][1], av, bf[b]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < TM / 8; ++a)
+#pragma unroll
+      for (int b = 0; b < NT; ++b) {
+        double* dst = ypart + (warp * TM + a * 8 + (lane >> 2)) * YP + b * 8 + 2 * (lane & 3);
+        dst[0] = ya[a][b][0];
+        dst[1] = ya[a][b][1];
+      }
+    __syncthreads();
+    for (int i = tid; i < TM * SG; i += blockDim.x) {
+      const int r = i / SG, c = i % SG;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) s += ypart[(w * TM + r) * YP + c];
+      ys[r * YS + c] = s;
+    }
+    __syncthreads();
+    const int rows = min(TM, prm.piece_rows[p] - t * TM);
+    if (prm.y_out != nullptr && jsplit == 0) {
+      const int64_t grow = prm.piece_row0[p] + (int64_t)t * TM;
+      for (int i = tid; i < rows * SG; i += blockDim.x) {
+        const int r = i / SG, c = i % SG;
+        prm.y_out[(grow + r) * sp + col0 + c] = ys[r * YS + c];
+      }
+    }
+
+    // ---- phase B: Z += X_t^T Y_t (each warp owns MT 8-row blocks of J)
+#pragma unroll
+    for (int kq = 0; kq < TM / 4; ++kq) {
+      const int kr = kq * 4 + (lane & 3);
+      double bf[NT];
+#pragma unroll
+      for (int b = 0; b < NT; ++b) bf[b] = ys[kr * YS + b * 8 + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        const int m = jbase + (warp * MT + a) * 8 + (lane >> 2);
+        double av = 0.0;
+        if (m < J) {
+          av = (double)X[kr * LDS + m];
+          if (stats) {
+            sq = fma(av, av, sq);
+            bad |= !isfinite(av);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < NT; ++b) dmma_8x8x4(zacc[a][b][0], zacc[a][b][1], av, bf[b]);
+      }
+    }
+
+    if ((t + 1) * TM >= prm.piece_rows[p]) {  // piece complete: flush partial
+      double* out = prm.out_part + (size_t)p * J * sp + col0;
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        const int m = jbase + (warp * MT + a) * 8 + (lane >> 2);
+        if (m < J) {
+#pragma unroll
+          for (int b = 0; b < NT; ++b) {
+            double* d = out + (size_t)m * sp + b * 8 + 2 * (lane & 3);
+            d[0] = zacc[a][b][0];
+            d[1] = zacc[a][b][1];
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < NT; ++b) zacc[a][b][0] = zacc[a][b][1] = 0.0;
+      }
+      if (stats) {
+        const double tot = block_sum(sq, red);
+        if (tid == 0) prm.xsq_part[(size_t)p * prm.njs + jsplit] = tot;
+        sq = 0.0;
+        if (__syncthreads_or(bad) && tid == 0) status_min(prm.status, ST_NONFINITE, ks);
+        bad = 0;
+      }
+    }
+    __syncthreads();
+    if (!has_next) break;
+    p = np;
+    t = ntl;
+    buf ^= 1;
+  }
+}
+
+// ============================================================ partial sum + CGS2
+// Sum the slice's piece partials (piece order) into Q, then orthonormalise the
+// first s_k columns with classical Gram-Schmidt + one reorthogonalisation.
+// Exactly-zero columns are replaced by unit vectors (the reference's
+// Householder QR likewise returns a full orthonormal Q for a zero sketch).
+__device__ void cgs2_columns(double* Q, int64_t rows, int ld, int ncols, double* h, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int c = 0; c < ncols; ++c) {
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 0) {  // replacement unit vector e_{(c + attempt - 1) mod rows}
+        const int64_t e = (int64_t)(c + attempt - 1) % rows;
+        for (int64_t i = tid; i < rows; i += nt) Q[i * ld + c] = (i == e) ? 1.0 : 0.0;
+        __syncthreads();
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int i = warp; i < c; i += nw) {
+          double s = 0.0;
+          for (int64_t r = lane; r < rows; r += 32) s = fma(Q[r * ld + i], Q[r * ld + c], s);
+          s = warp_sum(s);
+          if (lane == 0) h[i] = s;
+        }
+        __syncthreads();
+        for (int64_t r = tid; r < rows; r += nt) {
+          double acc = Q[r * ld + c];
+          for (int i = 0; i < c; ++i) acc = fma(-h[i], Q[r * ld + i], acc);
+          Q[r * ld + c] = acc;
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int64_t r = tid; r < rows; r += nt) part = fma(Q[r * ld + c], Q[r * ld + c], part);
+      const double nrm2 = block_sum(part, red);
+      const bool ok = attempt == 0 ? (nrm2 > 1e-300) : (nrm2 > 0.25);
+      if (ok || attempt > rows + 1) {
+        const double inv = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+        for (int64_t r = tid; r < rows; r += nt) Q[r * ld + c] *= inv;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) orth_kernel(const double* part, const int32_t* slice_piece,
+                                                    const int32_t* s_k, int J, int sp, double* Q) {
+  __shared__ double h[256];
+  __shared__ double red[32];
+  const int k = blockIdx.x;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  double* Qk = Q + (size_t)k * J * sp;
+  for (int64_t i = threadIdx.x; i < (int64_t)J * sp; i += blockDim.x) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * J * sp + i];
+    Qk[i] = acc;
+  }
+  __syncthreads();
+  cgs2_columns(Qk, J, sp, s_k[k], h, red);
+}
+
+// generic batched CGS2 (stage 2 uses it on single tall matrices)
+__global__ void __launch_bounds__(256) cgs2_kernel(double* Q, int64_t rows, int ld, int ncols,
+                                                    int64_t batch_stride) {
+  __shared__ double h[256];
+  __shared__ double red[32];
+  cgs2_columns(Q + blockIdx.x * batch_stride, rows, ld, ncols, h, red);
+}
+
+// ============================================================ per-slice factor
+// smem: G, CC, W (s x s each, ld = s+1), vectors.  Falls back to the global
+// scratch ``scr`` (3*sp*(sp+1) doubles per slice) when s is large.
+struct FactorParams {
+  const double* part;       // npieces x J x sp (C^T partials)
+  const int32_t* slice_piece;
+  const int64_t* row_off;
+  const int32_t* s_k;
+  const double* y2;         // total_rows x sp
+  double* ct;               // K x J x sp  (out: C^T)
+  double* Pm;               // K x sp x R
+  double* Sv;               // K x R
+  double* Vt;               // K x J x R
+  int32_t* rank_out;        // K
+  double* scr;              // global scratch
+  int64_t* status;
+  int J, sp, R, use_smem;
+};
+
+__global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int J = prm.J, sp = prm.sp, R = prm.R, s = prm.s_k[k];
+  const int ld = sp + 1;
+  double* base = prm.use_smem ? reinterpret_cast<double*>(smem_raw)
+                              : prm.scr + (size_t)k * (3 * (size_t)sp * ld + 4 * sp);
+  double* G = base;
+  double* CC = G + sp * ld;
+  double* W = CC + sp * ld;
+  double* lam = W + sp * ld;       // sp
+  double* cs = lam + sp;           // 3*(sp/2+1) <= 2 sp + 3
+  __shared__ int perm[160];
+  __shared__ int flag;
+  __shared__ double red[32];
+  __shared__ double tile[1056];
+
+  // 1. C^T = sum of piece partials
+  const int p0 = prm.slice_piece[k], p1 = prm.slice_piece[k + 1];
+  double* Ct = prm.ct + (size_t)k * J * sp;
+  for (int64_t i = tid; i < (int64_t)J * sp; i += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += prm.part[(size_t)p * J * sp + i];
+    Ct[i] = acc;
+  }
+  // 2./3. G = Y^T Y over the slice rows, CC = C C^T over J: upper triangles
+  const int ntri = s * (s + 1) / 2;
+  auto tri = [&](int e, int& a, int& b) {  // e -> (a <= b)
+    a = 0;
+    int rem = e;
+    while (rem >= s - a) { rem -= s - a; ++a; }
+    b = a + rem;
+  };
+  __syncthreads();
+  for (int which = 0; which < 2; ++which) {
+    const double* src = which == 0 ? prm.y2 + prm.row_off[k] * sp : Ct;
+    const int64_t nrows = which == 0 ? prm.row_off[k + 1] - prm.row_off[k] : J;
+    double* dst = which == 0 ? G : CC;
+    for (int e0 = 0; e0 < ntri; e0 += nt) {
+      const int e = e0 + tid;
+      int a = 0, b = 0;
+      if (e < ntri) tri(e, a, b);
+      double acc = 0.0;
+      const int trows = max(1, 1056 / max(s, 1));
+      for (int64_t r0 = 0; r0 < nrows; r0 += trows) {
+        const int rr = (int)(nrows - r0 < trows ? nrows - r0 : trows);
+        __syncthreads();
+        for (int i = tid; i < rr * s; i += nt) tile[i] = src[(r0 + i / s) * sp + (i % s)];
+        __syncthreads();
+        if (e < ntri)
+          for (int r = 0; r < rr; ++r) acc = fma(tile[r * s + a], tile[r * s + b], acc);
+      }
+      if (e < ntri) { dst[a * ld + b] = acc; dst[b * ld + a] = acc; }
+    }
+    __syncthreads();
+  }
+  // 4. eig(G) -> W, lambda (descending)
+  int sw = jacobi_eig_block(G, ld, W, ld, s, cs, &flag);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_NOCONV), 1ull);
+  sort_desc_perm(G, ld, s, perm);
+  for (int i = tid; i < s; i += nt) lam[i] = G[perm[i] * ld + perm[i]];
+  __syncthreads();
+  // T = W[:, perm] / sqrt(lambda) for lambda > tau * lambda_max  (into G)
+  const double lmax = lam[0] > 0.0 ? lam[0] : 0.0;
+  int rp = 0;
+  for (int i = 0; i < s; ++i) rp += (lam[i] > 1e-13 * lmax && lam[i] > 0.0) ? 1 : 0;
+  for (int i = tid; i < s * s; i += nt) {
+    const int a = i / s, c = i % s;
+    G[a * ld + c] = c < rp ? W[a * ld + perm[c]] / sqrt(lam[c]) : 0.0;
+  }
+  __syncthreads();
+  // tmp = CC T (s x rp) into W, then Bg = T^T tmp (rp x rp) into CC
+  for (int i = tid; i < s * rp; i += nt) {
+    const int a = i / rp, c = i % rp;
+    double acc = 0.0;
+    for (int b = 0; b < s; ++b) acc = fma(CC[a * ld + b], G[b * ld + c], acc);
+    W[a * ld + c] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < rp * rp; i += nt) {
+    const int a = i / rp, c = i % rp;
+    double acc = 0.0;
+    for (int b = 0; b < s; ++b) acc = fma(G[b * ld + a], W[b * ld + c], acc);
+    CC[a * ld + c] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < rp * rp; i += nt) {  // symmetrise
+    const int a = i / rp, c = i % rp;
+    if (a < c) {
+      const double m = 0.5 * (CC[a * ld + c] + CC[c * ld + a]);
+      CC[a * ld + c] = m;
+      CC[c * ld + a] = m;
+    }
+  }
+  __syncthreads();
+  sw = jacobi_eig_block(CC, ld, W, ld, rp, cs, &flag);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_NOCONV), 1ull);
+  sort_desc_perm(CC, ld, rp, perm);
+  // 5. P = T U[:, :R], S = sqrt(mu)
+  double* Pk = prm.Pm + (size_t)k * sp * R;
+  double* Sk = prm.Sv + (size_t)k * R;
+  for (int i = tid; i < sp * R; i += nt) {
+    const int a = i / R, r = i % R;
+    double acc = 0.0;
+    if (a < s && r < rp) {
+      const int col = perm[r];
+      for (int b = 0; b < rp; ++b) acc = fma(G[a * ld + b], W[b * ld + col], acc);
+    }
+    Pk[a * R + r] = acc;
+  }
+  __shared__ double Sloc[64];
+  for (int r = tid; r < R; r += nt) {
+    const double mu = r < rp ? CC[perm[r] * ld + perm[r]] : 0.0;
+    Sloc[r] = mu > 0.0 ? sqrt(mu) : 0.0;
+    Sk[r] = Sloc[r];
+  }
+  __syncthreads();
+  // 6. V = C^T P / S
+  double* Vk = prm.Vt + (size_t)k * J * R;
+  for (int64_t i = tid; i < (int64_t)J * R; i += nt) {
+    const int64_t j = i / R;
+    const int r = (int)(i % R);
+    double acc = 0.0;
+    for (int a = 0; a < s; ++a) acc = fma(Ct[j * sp + a], Pk[a * R + r], acc);
+    Vk[i] = Sloc[r] > 0.0 ? acc / Sloc[r] : 0.0;
+  }
+  int rk = 0;
+  for (int r = 0; r < R; ++r) rk += Sloc[r] > 0.0 ? 1 : 0;
+  if (tid == 0) {
+    prm.rank_out[k] = rk;
+    if (rk < R) status_min(prm.status, ST_RANKDEF, k);
+  }
+}
+
+// ============================================================ signs and A
+// a_r(i) = sum_c y2[i][c] P[c][r], fixed FMA order (shared by both kernels so
+// the argmax sees exactly the stored values up to an exact sign flip).
+struct RowsParams {
+  const double* y2;
+  const int64_t* row_off;
+  const int32_t* piece_slice;
+  const int64_t* piece_row0;
+  const int32_t* piece_rows;
+  const int32_t* s_k;
+  const double* Pm;     // K x sp x R
+  int sp, R;
+  double* cand_abs;     // npieces x R
+  int64_t* cand_row;    // npieces x R
+  int32_t* cand_neg;    // npieces x R
+  double* A;            // total_rows x R
+};
+
+__global__ void __launch_bounds__(256) argmax_kernel(RowsParams prm) {
+  const int p = blockIdx.x, tid = threadIdx.x, R = prm.R, sp = prm.sp;
+  const int k = prm.piece_slice[p], s = prm.s_k[k];
+  __shared__ double babs[256];
+  __shared__ int64_t brow[256];
+  __shared__ int bneg[256];
+  const double* Pk = prm.Pm + (size_t)k * sp * R;
+  const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
+  const int64_t base = prm.row_off[k];
+  for (int c0 = 0; c0 < R; c0 += 16) {
+    const int cw = min(16, R - c0);
+    double best[16];
+    int64_t brw[16];
+    int bng[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) { best[c] = -1.0; brw[c] = INT64_MAX; bng[c] = 0; }
+    for (int64_t i = r0 + tid; i < r0 + nr; i += blockDim.x) {
+      const double* y = prm.y2 + i * sp;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        if (c >= cw) break;
+        double acc = 0.0;
+        for (int a = 0; a < s; ++a) acc = fma(y[a], Pk[a * R + c0 + c], acc);
+        const double v = fabs(acc);
+        if (v > best[c]) { best[c] = v; brw[c] = i - base; bng[c] = acc < 0.0; }
+      }
+    }
+    for (int c = 0; c < cw; ++c) {
+      babs[tid] = best[c];
+      brow[tid] = brw[c];
+      bneg[tid] = bng[c];
+      __syncthreads();
+      for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (tid < o) {
+          const double va = babs[tid], vb = babs[tid + o];
+          const int64_t ra = brow[tid], rb = brow[tid + o];
+          if (vb > va || (vb == va && rb < ra)) {
+            babs[tid] = vb;
+            brow[tid] = rb;
+            bneg[tid] = bneg[tid + o];
+          }
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        prm.cand_abs[(size_t)p * R + c0 + c] = babs[0];
+        prm.cand_row[(size_t)p * R + c0 + c] = brow[0];
+        prm.cand_neg[(size_t)p * R + c0 + c] = bneg[0];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Combine candidates, fold the signs into P, write M's column block k.
+__global__ void __launch_bounds__(128) signs_kernel(const int32_t* slice_piece, const double* cand_abs,
+                                                     const int64_t* cand_row, const int32_t* cand_neg,
+                                                     double* Pm, const double* Sv, const double* Vt,
+                                                     int K, int J, int sp, int R, double* M) {
+  const int k = blockIdx.x, tid = threadIdx.x;
+  __shared__ double sgn[64];
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  for (int r = tid; r < R; r += blockDim.x) {
+    double ba = -1.0;
+    int64_t br = INT64_MAX;
+    int bn = 0;
+    for (int p = p0; p < p1; ++p) {
+      const double va = cand_abs[(size_t)p * R + r];
+      const int64_t ra = cand_row[(size_t)p * R + r];
+      if (va > ba || (va == ba && ra < br)) { ba = va; br = ra; bn = cand_neg[(size_t)p * R + r]; }
+    }
+    sgn[r] = bn ? -1.0 : 1.0;
+  }
+  __syncthreads();
+  double* Pk = Pm + (size_t)k * sp * R;
+  for (int i = tid; i < sp * R; i += blockDim.x) Pk[i] *= sgn[i % R];
+  const double* Vk = Vt + (size_t)k * J * R;
+  const double* Sk = Sv + (size_t)k * R;
+  const int64_t KR = (int64_t)K * R;
+  for (int64_t i = tid; i < (int64_t)J * R; i += blockDim.x) {
+    const int64_t j = i / R;
+    const int r = (int)(i % R);
+    M[j * KR + (int64_t)k * R + r] = (sgn[r] * Vk[i]) * Sk[r];
+  }
+}
+
+__global__ void __launch_bounds__(256) assemble_a_kernel(RowsParams prm) {
+  const int p = blockIdx.x, R = prm.R, sp = prm.sp;
+  const int k = prm.piece_slice[p], s = prm.s_k[k];
+  const double* Pk = prm.Pm + (size_t)k * sp * R;
+  const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
+  for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) {
+    const int64_t i = r0 + e / R;
+    const int c = (int)(e % R);
+    const double* y = prm.y2 + i * sp;
+    double acc = 0.0;
+    for (int a = 0; a < s; ++a) acc = fma(y[a], Pk[a * R + c], acc);
+    prm.A[i * R + c] = acc;
+  }
+}
+
+// Rank-deficient slices: complete A_k's trailing columns to an orthonormal set.
+__global__ void __launch_bounds__(256) complete_kernel(const int64_t* row_off, const int32_t* rank_out,
+                                                        int R, double* A) {
+  __shared__ double h[256];
+  __shared__ double red[32];
+  const int k = blockIdx.x;
+  const int rk = rank_out[k];
+  if (rk >= R) return;
+  const int64_t rows = row_off[k + 1] - row_off[k];
+  double* Ak = A + row_off[k] * R;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int c = rk; c < R; ++c) {
+    for (int64_t e = 0; e < rows; ++e) {
+      for (int64_t i = tid; i < rows; i += nt) Ak[i * R + c] = (i == (e + c) % rows) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int i = warp; i < c; i += nw) {
+          double sacc = 0.0;
+          for (int64_t r = lane; r < rows; r += 32) sacc = fma(Ak[r * R + i], Ak[r * R + c], sacc);
+          sacc = warp_sum(sacc);
+          if (lane == 0) h[i] = sacc;
+        }
+        __syncthreads();
+        for (int64_t r = tid; r < rows; r += nt) {
+          double acc = Ak[r * R + c];
+          for (int i = 0; i < c; ++i) acc = fma(-h[i], Ak[r * R + i], acc);
+          Ak[r * R + c] = acc;
+        }
+        __syncthreads();
+      }
+      double part = 0.0;
+      for (int64_t r = tid; r < rows; r += nt) part = fma(Ak[r * R + c], Ak[r * R + c], part);
+      const double n2 = block_sum(part, red);
+      if (n2 > 0.25) {
+        const double inv = 1.0 / sqrt(n2);
+        for (int64_t r = tid; r < rows; r += nt) Ak[r * R + c] *= inv;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+}
+
+// ============================================================ host side
+namespace {
+
+int pick_lds(int J, int elem) {
+  const int J4 = ((J + 3) / 4) * 4;
+  int lds = J4;
+  if (elem == 8) {
+    while (lds % 16 != 4) ++lds;
+  } else {
+    while (lds % 32 != 8) ++lds;
+  }
+  return lds;
+}
+
+template <typename T, int TM, int MT, int NT>
+cudaError_t launch_sketch(const SketchParams& prm, int nseg, int ng, int njs, cudaStream_t st) {
+  constexpr int SG = 8 * NT;
+  const size_t xbytes = (((size_t)2 * TM * prm.lds * sizeof(T)) + 15) & ~(size_t)15;
+  const size_t smem = xbytes + (size_t)(8 * TM * (SG + 2) + TM * (SG + 1) + 32) * sizeof(double);
+  auto kern = sketch_kernel<T, TM, MT, NT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(nseg, ng, njs), 256, smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+template <typename T, int TM, int MT>
+cudaError_t dispatch_nt(const SketchParams& prm, int nt, int nseg, int ng, int njs, cudaStream_t st) {
+  switch (nt) {
+    case 1: return launch_sketch<T, TM, MT, 1>(prm, nseg, ng, njs, st);
+    case 2: return launch_sketch<T, TM, MT, 2>(prm, nseg, ng, njs, st);
+    case 3: return launch_sketch<T, TM, MT, 3>(prm, nseg, ng, njs, st);
+    default: return launch_sketch<T, TM, MT, 4>(prm, nseg, ng, njs, st);
+  }
+}
+
+template <typename T, int TM>
+cudaError_t dispatch_mt(const SketchParams& prm, int mt, int nt, int nseg, int ng, int njs, cudaStream_t st) {
+  switch (mt) {
+    case 1: return dispatch_nt<T, TM, 1>(prm, nt, nseg, ng, njs, st);
+    case 2: return dispatch_nt<T, TM, 2>(prm, nt, nseg, ng, njs, st);
+    case 4: return dispatch_nt<T, TM, 4>(prm, nt, nseg, ng, njs, st);
+    default: return dispatch_nt<T, TM, 8>(prm, nt, nseg, ng, njs, st);
+  }
+}
+
+}  // namespace
+
+// Smem budget per CTA for the X tiles (both buffers).
+static constexpr size_t kXTileBudget = 150 * 1024;
+
+cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                       double* xsq_part, int64_t* status, cudaStream_t stream) {
+  const int J = (int)st->J;
+  const int elem = st->dtype == DP2_F64 ? 8 : 4;
+  SketchParams prm{};
+  prm.X = st->X;
+  prm.ldx = st->ldx;
+  prm.J = J;
+  prm.sp = sp;
+  prm.lds = pick_lds(J, elem);
+  prm.B = B;
+  prm.piece_slice = st->piece_slice;
+  prm.piece_row0 = st->piece_row0;
+  prm.piece_rows = st->piece_rows;
+  prm.seg_begin = st->seg_begin;
+  prm.out_part = out_part;
+  prm.y_out = y_out;
+  prm.xsq_part = xsq_part;
+  prm.status = status;
+  const int nt = sp >= 32 ? 4 : sp / 8;
+  const int ng = sp >= 32 ? sp / 32 : 1;
+  int mt = 1;
+  while (mt < 8 && 64 * mt < J) mt *= 2;
+  const int njs = (J + 64 * mt - 1) / (64 * mt);
+  prm.njs = njs;
+  const int tm = (size_t)2 * 16 * prm.lds * elem <= kXTileBudget ? 16 : 8;
+  if ((size_t)2 * tm * prm.lds * elem > 200 * 1024) return cudaErrorInvalidValue;
+  const int nseg = st->nseg;
+  if (elem == 8)
+    return tm == 16 ? dispatch_mt<double, 16>(prm, mt, nt, nseg, ng, njs, stream)
+                    : dispatch_mt<double, 8>(prm, mt, nt, nseg, ng, njs, stream);
+  return tm == 16 ? dispatch_mt<float, 16>(prm, mt, nt, nseg, ng, njs, stream)
+                  : dispatch_mt<float, 8>(prm, mt, nt, nseg, ng, njs, stream);
+}
+
+int sketch_njs(int J) {
+  int mt = 1;
+  while (mt < 8 && 64 * mt < J) mt *= 2;
+  return (J + 64 * mt - 1) / (64 * mt);
+}
+
+Stage1Layout stage1_layout(const dp2_store* st, int sp, int R) {
+  Stage1Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const size_t J = st->J, K = st->K, P = st->npieces, N = st->total_rows;
+  L.part = take(P * J * sp * 8);
+  L.qz = take(K * J * sp * 8);
+  L.y2 = take(N * sp * 8);
+  L.Pm = take(K * sp * R * 8);
+  L.Sv = take(K * R * 8);
+  L.Vt = take(K * J * R * 8);
+  L.cand_abs = take(P * R * 8);
+  L.cand_row = take(P * R * 8);
+  L.cand_neg = take(P * R * 4);
+  L.xsq = take(P * sketch_njs((int)J) * 8);
+  L.scr = take(K * (3 * (size_t)sp * (sp + 1) + 4 * sp) * 8);
+  L.total = off;
+  return L;
+}
+
+cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
+                       double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
+                       float* timing, cudaStream_t stream) {
+  const Stage1Layout L = stage1_layout(st, sp, R);
+  double* part = reinterpret_cast<double*>(ws + L.part);
+  double* qz = reinterpret_cast<double*>(ws + L.qz);
+  double* y2 = reinterpret_cast<double*>(ws + L.y2);
+  double* Pm = reinterpret_cast<double*>(ws + L.Pm);
+  double* Sv = reinterpret_cast<double*>(ws + L.Sv);
+  double* Vt = reinterpret_cast<double*>(ws + L.Vt);
+  double* xsq = reinterpret_cast<double*>(ws + L.xsq);
+  const int K = (int)st->K, J = (int)st->J;
+  cudaEvent_t ev[8];
+  if (timing) {
+    for (int i = 0; i < 7; ++i) cudaEventCreate(&ev[i]);
+    cudaEventRecord(ev[0], stream);
+  }
+  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, xsq, status, stream);
+  if (e != cudaSuccess) return e;
+  if (timing) cudaEventRecord(ev[1], stream);
+  orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
+  if (timing) cudaEventRecord(ev[2], stream);
+  e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream);
+  if (e != cudaSuccess) return e;
+  if (timing) cudaEventRecord(ev[3], stream);
+  FactorParams fp{};
+  fp.part = part;
+  fp.slice_piece = st->slice_piece;
+  fp.row_off = st->row_off;
+  fp.s_k = s_dev;
+  fp.y2 = y2;
+  fp.ct = qz;
+  fp.Pm = Pm;
+  fp.Sv = Sv;
+  fp.Vt = Vt;
+  fp.rank_out = rank_out;
+  fp.scr = reinterpret_cast<double*>(ws + L.scr);
+  fp.status = status;
+  fp.J = J;
+  fp.sp = sp;
+  fp.R = R;
+  const size_t fsm = (3 * (size_t)sp * (sp + 1) + 4 * sp) * 8;
+  fp.use_smem = fsm <= 96 * 1024;
+  if (fp.use_smem) {
+    e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    if (e != cudaSuccess) return e;
+  }
+  factor_kernel<<<K, 256, fp.use_smem ? fsm : 0, stream>>>(fp);
+  if (timing) cudaEventRecord(ev[4], stream);
+  RowsParams rp{};
+  rp.y2 = y2;
+  rp.row_off = st->row_off;
+  rp.piece_slice = st->piece_slice;
+  rp.piece_row0 = st->piece_row0;
+  rp.piece_rows = st->piece_rows;
+  rp.s_k = s_dev;
+  rp.Pm = Pm;
+  rp.sp = sp;
+  rp.R = R;
+  rp.cand_abs = reinterpret_cast<double*>(ws + L.cand_abs);
+  rp.cand_row = reinterpret_cast<int64_t*>(ws + L.cand_row);
+  rp.cand_neg = reinterpret_cast<int32_t*>(ws + L.cand_neg);
+  rp.A = A_out;
+  const int P = (int)st->npieces;
+  argmax_kernel<<<P, 256, 0, stream>>>(rp);
+  signs_kernel<<<K, 128, 0, stream>>>(st->slice_piece, rp.cand_abs, rp.cand_row, rp.cand_neg, Pm, Sv, Vt,
+                                      K, J, sp, R, M_out);
+  assemble_a_kernel<<<P, 256, 0, stream>>>(rp);
+  complete_kernel<<<K, 256, 0, stream>>>(st->row_off, rank_out, R, A_out);
+  e = cudaGetLastError();
+  if (timing) {
+    cudaEventRecord(ev[5], stream);
+    cudaEventSynchronize(ev[5]);
+    cudaEventElapsedTime(&timing[0], ev[0], ev[1]);
+    cudaEventElapsedTime(&timing[1], ev[1], ev[2]);
+    cudaEventElapsedTime(&timing[2], ev[2], ev[3]);
+    cudaEventElapsedTime(&timing[3], ev[3], ev[4]);
+    cudaEventElapsedTime(&timing[4], ev[4], ev[5]);
+    cudaEventElapsedTime(&timing[5], ev[0], ev[5]);
+    for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+  }
+  return e;
+}
+
+}  // namespace dp2

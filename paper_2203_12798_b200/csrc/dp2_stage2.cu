@@ -1,0 +1,246 @@
+// Stage 2: randomized SVD of the concatenated right parts
+// M = [V_1 S_1 | ... | V_K S_K] (J x KR, P/compress.py:108-111), fp64.
+//
+//   Y  = M Omega2           (J x s2)     nn split-K partials + ordered reduce
+//   Z  = orth(M^T Y)        (KR x s2)    tn + CGS2 (range-preserving)
+//   Y2 = M Z                (J x s2)     = range of the reference's M (M^T M Omega2)
+//   Q2 = orth(Y2)                        CGS2 (the reference's np.linalg.qr)
+//   C  = M^T Q2             (KR x s2)    B2 = Q2^T M = C^T
+//   B2 B2^T = C^T C = U mu U^T           Jacobi; E = sqrt(mu_R)
+//   D = Q2 U_R (sign rule, P/linalg.py:62-70), F = C U_R / E (same flips)
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+
+constexpr int kChunk = 1024;  // split-K chunk of the KR dimension
+
+// out_part[chunk][i][c] = sum_{n in chunk} A[i][n] * B[n][c],  c in [32g, 32g+32) & < sb
+__global__ void __launch_bounds__(256) nn_partial_kernel(const double* A, int64_t lda, int64_t N,
+                                                          const double* B, int ldb, int sb,
+                                                          double* out_part, int64_t m) {
+  __shared__ double red[32];
+  const int64_t i = blockIdx.x;
+  const int chunk = blockIdx.y, g = blockIdx.z;
+  const int64_t n0 = (int64_t)chunk * kChunk, n1 = imin64(N, n0 + kChunk);
+  const int c0 = g * 32, cw = min(32, sb - c0);
+  double acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+  for (int64_t n = n0 + threadIdx.x; n < n1; n += blockDim.x) {
+    const double a = A[i * lda + n];
+    const double* b = B + n * ldb + c0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < cw) acc[c] = fma(a, b[c], acc[c]);
+  }
+  for (int c = 0; c < cw; ++c) {
+    const double s = block_sum(acc[c], red);
+    if (threadIdx.x == 0) out_part[((size_t)chunk * m + i) * sb + c0 + c] = s;
+  }
+}
+
+__global__ void reduce_parts_kernel(const double* part, int nparts, int64_t size, double* out) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < size;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < nparts; ++c) acc += part[(size_t)c * size + idx];
+    out[idx] = acc;
+  }
+}
+
+// out[n][c] = sum_i A[i][n] * B[i][c]   (A m x N row-major, B m x sb), c group g
+__global__ void __launch_bounds__(256) tn_kernel(const double* A, int64_t lda, int64_t m, int64_t N,
+                                                  const double* B, int ldb, int sb, double* out,
+                                                  int ldo) {
+  __shared__ double bt[32 * 32];
+  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = blockIdx.y * 32, cw = min(32, sb - c0);
+  double acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+  for (int64_t i0 = 0; i0 < m; i0 += 32) {
+    const int ir = (int)imin64(32, m - i0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+      const int r = e / 32, c = e % 32;
+      bt[e] = (r < ir && c < cw) ? B[(i0 + r) * ldb + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (n < N) {
+      for (int r = 0; r < ir; ++r) {
+        const double a = A[(i0 + r) * lda + n];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fma(a, bt[r * 32 + c], acc[c]);
+      }
+    }
+  }
+  if (n < N)
+    for (int c = 0; c < cw; ++c) out[n * ldo + c0 + c] = acc[c];
+}
+
+// partial Gram over row chunks: part[chunk][a][b] = sum_{n in chunk} C[n][a] C[n][b]
+__global__ void __launch_bounds__(256) gram_partial_kernel(const double* C, int64_t N, int ld, int s,
+                                                            double* part) {
+  __shared__ double tile[1056];
+  const int chunk = blockIdx.x;
+  const int64_t n0 = (int64_t)chunk * kChunk, n1 = imin64(N, n0 + kChunk);
+  const int ntri = s * (s + 1) / 2;
+  const int trows = max(1, 1056 / s);
+  for (int e0 = 0; e0 < ntri; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    int a = 0, b = 0;
+    if (e < ntri) {
+      int rem = e;
+      while (rem >= s - a) { rem -= s - a; ++a; }
+      b = a + rem;
+    }
+    double acc = 0.0;
+    for (int64_t r0 = n0; r0 < n1; r0 += trows) {
+      const int rr = (int)imin64(trows, n1 - r0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < rr * s; i += blockDim.x) tile[i] = C[(r0 + i / s) * ld + (i % s)];
+      __syncthreads();
+      if (e < ntri)
+        for (int r = 0; r < rr; ++r) acc = fma(tile[r * s + a], tile[r * s + b], acc);
+    }
+    if (e < ntri) {
+      part[(size_t)chunk * s * s + a * s + b] = acc;
+      part[(size_t)chunk * s * s + b * s + a] = acc;
+    }
+  }
+}
+
+// single block: eig(BB) -> E, D = Q2 U_R with the sign rule, Uf = U_R * sign / E
+__global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, const double* Q2, int64_t J,
+                                                            int R, double* D, double* E, double* Uf,
+                                                            double* Ubuf, int64_t* status) {
+  __shared__ double cs[3 * 80];
+  __shared__ int flag;
+  __shared__ int perm[160];
+  __shared__ double babs[256];
+  __shared__ int64_t brow[256];
+  __shared__ int bneg[256];
+  __shared__ double sgn[64];
+  __shared__ double ev[64];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int sw = jacobi_eig_block(BB, s, Ubuf, s, s, cs, &flag);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_NOCONV), 1ull);
+  sort_desc_perm(BB, s, s, perm);
+  for (int r = tid; r < R; r += nt) {
+    const double mu = BB[perm[r] * s + perm[r]];
+    ev[r] = mu > 0.0 ? sqrt(mu) : 0.0;
+    E[r] = ev[r];
+  }
+  __syncthreads();
+  // D = Q2 U[:, perm[:R]]
+  for (int64_t e = tid; e < J * R; e += nt) {
+    const int64_t j = e / R;
+    const int r = (int)(e % R);
+    double acc = 0.0;
+    for (int c = 0; c < s; ++c) acc = fma(Q2[j * s + c], Ubuf[c * s + perm[r]], acc);
+    D[e] = acc;
+  }
+  __syncthreads();
+  for (int r = 0; r < R; ++r) {
+    double ba = -1.0;
+    int64_t br = INT64_MAX;
+    int bn = 0;
+    for (int64_t j = tid; j < J; j += nt) {
+      const double v = D[j * R + r], a = fabs(v);
+      if (a > ba) { ba = a; br = j; bn = v < 0.0; }
+    }
+    babs[tid] = ba;
+    brow[tid] = br;
+    bneg[tid] = bn;
+    __syncthreads();
+    for (int o = nt / 2; o > 0; o >>= 1) {
+      if (tid < o) {
+        const double va = babs[tid], vb = babs[tid + o];
+        const int64_t ra = brow[tid], rb = brow[tid + o];
+        if (vb > va || (vb == va && rb < ra)) { babs[tid] = vb; brow[tid] = rb; bneg[tid] = bneg[tid + o]; }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) sgn[r] = bneg[0] ? -1.0 : 1.0;
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < J * R; e += nt) D[e] *= sgn[e % R];
+  for (int e = tid; e < s * R; e += nt) {
+    const int c = e / R, r = e % R;
+    Uf[e] = ev[r] > 0.0 ? (Ubuf[c * s + perm[r]] * sgn[r]) / ev[r] : 0.0;
+  }
+}
+
+// F[n][r] = sum_c C[n][c] Uf[c][r]
+__global__ void f_kernel(const double* C, int64_t N, int s, const double* Uf, int R, double* F) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < N * R;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / R;
+    const int r = (int)(e % R);
+    double acc = 0.0;
+    for (int c = 0; c < s; ++c) acc = fma(C[n * s + c], Uf[c * R + r], acc);
+    F[e] = acc;
+  }
+}
+
+namespace {
+struct S2Layout {
+  size_t parts, Y, Z, Y2, C, bbp, BB, Uf, Ubuf, total;
+};
+S2Layout s2_layout(int64_t J, int64_t KR, int s2, int R) {
+  S2Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+  const size_t nch = (KR + kChunk - 1) / kChunk;
+  L.parts = take(nch * J * s2 * 8);
+  L.Y = take(J * s2 * 8);
+  L.Z = take(KR * s2 * 8);
+  L.Y2 = take(J * s2 * 8);
+  L.C = take(KR * s2 * 8);
+  L.bbp = take(nch * s2 * s2 * 8);
+  L.BB = take(s2 * s2 * 8);
+  L.Uf = take(s2 * R * 8);
+  L.Ubuf = take(s2 * s2 * 8);
+  L.total = off;
+  return L;
+}
+}  // namespace
+
+size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R) { return s2_layout(J, KR, s2, R).total; }
+
+cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
+                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t st) {
+  const S2Layout L = s2_layout(J, KR, s2, R);
+  double* parts = reinterpret_cast<double*>(ws + L.parts);
+  double* Y = reinterpret_cast<double*>(ws + L.Y);
+  double* Z = reinterpret_cast<double*>(ws + L.Z);
+  double* Y2 = reinterpret_cast<double*>(ws + L.Y2);
+  double* C = reinterpret_cast<double*>(ws + L.C);
+  double* bbp = reinterpret_cast<double*>(ws + L.bbp);
+  double* BB = reinterpret_cast<double*>(ws + L.BB);
+  double* Uf = reinterpret_cast<double*>(ws + L.Uf);
+  double* Ubuf = reinterpret_cast<double*>(ws + L.Ubuf);
+  const int nch = (int)((KR + kChunk - 1) / kChunk);
+  const int ng = (s2 + 31) / 32;
+  auto nn = [&](const double* B, double* out) {
+    nn_partial_kernel<<<dim3((unsigned)J, nch, ng), 256, 0, st>>>(M, KR, KR, B, s2, s2, parts, J);
+    reduce_parts_kernel<<<(unsigned)((J * s2 + 255) / 256), 256, 0, st>>>(parts, nch, J * s2, out);
+  };
+  auto tn = [&](const double* B, double* out) {
+    tn_kernel<<<dim3((unsigned)((KR + 255) / 256), ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, out, s2);
+  };
+  nn(omega2, Y);
+  tn(Y, Z);
+  cgs2_kernel<<<1, 256, 0, st>>>(Z, KR, s2, s2, 0);
+  nn(Z, Y2);
+  cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
+  tn(Y2, C);
+  gram_partial_kernel<<<nch, 256, 0, st>>>(C, KR, s2, s2, bbp);
+  reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(bbp, nch, (int64_t)s2 * s2, BB);
+  stage2_final_kernel<<<1, 256, 0, st>>>(BB, s2, Y2, J, R, D, E, Uf, Ubuf, status);
+  f_kernel<<<(unsigned)imin64((KR * R + 255) / 256, 4096), 256, 0, st>>>(C, KR, s2, Uf, R, F);
+  return cudaGetLastError();
+}
+
+}  // namespace dp2

@@ -1,0 +1,214 @@
+"""CUDA path vs the reference (golden fixtures) and vs the live CPU oracle.
+
+Tolerances (BASELINE.json north star): fp64 -- fitness within 1e-6 absolute,
+factors within 1e-5 relative (max-abs error / max-abs value, up to column
+sign); fp32 mode -- both within 1e-3.  Partition bit-exact (CPU tests).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FIT_TOL, FACTOR_TOL = 1e-6, 1e-5
+FIT_TOL32, FACTOR_TOL32 = 1e-3, 1e-3
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def rel_signed(a, b):
+    """Relative error after aligning each column's sign to b."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    s = np.sign(np.sum(a * b, axis=0))
+    s[s == 0] = 1.0
+    return rel(a * s, b)
+
+
+def load_fit(golden, name):
+    z = np.load(golden / f"fit_{name}.npz")
+    rows, J = z["rows"], int(z["J"])
+    xs, off = [], 0
+    for r in rows:
+        xs.append(z["X"][off:off + r * J].reshape(r, J))
+        off += r * J
+    return z, xs
+
+
+FIT_CASES = ["tiny0", "tiny1", "tiny2", "tiny3", "tiny4", "tiny5", "planted", "planted_tol", "planted_nonorm",
+             "f32vals", "wide"]
+
+
+@pytest.mark.parametrize("name", FIT_CASES)
+def test_fit_matches_reference_fp64(golden, name):
+    import paper_2203_12798_b200 as dp
+    z, xs = load_fit(golden, name)
+    t = dp.IrregularTensor(xs)
+    opts = dp.SolverOptions(max_iters=int(z["max_iters"]), tol=float(z["tol"]), seed=int(z["seed"]),
+                            normalize=bool(z["normalize"]))
+    f, tr = dp.fit_dpar2(t, int(z["rank"]), opts)
+    assert tr.iterations == len(z["objective"])
+    assert tr.converged == bool(z["converged"])
+    assert tr.compressed_float_count == int(z["float_count"])
+    assert rel(tr.objective, z["objective"]) <= 1e-6
+    fit = dp.fitness(t, f)
+    assert abs(fit - float(z["fitness"])) <= FIT_TOL
+    assert rel_signed(f.H, z["H"]) <= FACTOR_TOL
+    assert rel_signed(f.V, z["V"]) <= FACTOR_TOL
+    assert rel_signed(f.W, z["W"]) <= FACTOR_TOL
+    U = np.concatenate([q @ f.H for q in f.Q])
+    Uref = np.concatenate([z["Q"][a:b] for a, b in zip(np.r_[0, np.cumsum(z["rows"])][:-1],
+                                                        np.cumsum(z["rows"]))]) @ z["H"]
+    assert rel_signed(U, Uref) <= FACTOR_TOL
+
+
+@pytest.mark.parametrize("name", ["planted", "f32vals", "wide"])
+def test_fit_fp32_mode_within_1e3(golden, name):
+    import paper_2203_12798_b200 as dp
+    z, xs = load_fit(golden, name)
+    xs32 = [x.astype(np.float32) for x in xs]
+    t = dp.IrregularTensor(xs32, dtype="f32")
+    opts = dp.SolverOptions(max_iters=int(z["max_iters"]), tol=float(z["tol"]), seed=int(z["seed"]),
+                            normalize=bool(z["normalize"]))
+    f, tr = dp.fit_dpar2(t, int(z["rank"]), opts)
+    # reference on the exactly upcast fp32 values
+    from oracle import dpar2_oracle as orc
+    o = orc.fit_dpar2([x.astype(np.float64) for x in xs32], int(z["rank"]), int(z["max_iters"]), float(z["tol"]),
+                      int(z["seed"]), bool(z["normalize"]))
+    fit_o = orc.fitness([x.astype(np.float64) for x in xs32], o["H"], o["V"], o["W"], o["Q"])
+    assert abs(dp.fitness(t, f) - fit_o) <= FIT_TOL32
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL32, key
+
+
+def test_stage1_matches_reference(golden):
+    import paper_2203_12798_b200 as dp
+    z = np.load(golden / "stage1.npz")
+    rows, J = z["rows"], int(z["J"])
+    xs, off = [], 0
+    for r in rows:
+        xs.append(z["X"][off:off + r * J].reshape(r, J))
+        off += r * J
+    t = dp.IrregularTensor(xs)
+    comp = dp.compress(t, 4)
+    A = comp.A.cpu().numpy()
+    assert rel(A, z["A"]) <= 1e-8  # exact sign choices + rounding-level agreement
+    # A_k column-orthonormal
+    for a in comp.slice_bases:
+        a = a.cpu().numpy()
+        assert np.abs(a.T @ a - np.eye(4)).max() <= 1e-10
+    over = dp.compress(t, 4, rsvd=dp.RsvdParams(rank=4, oversampling=4, seed=2))
+    assert rel(over.cores.cpu().numpy(), z["over_F"]) <= 1e-8
+    assert rel(over.col_basis.cpu().numpy(), z["over_D"]) <= 1e-8
+    assert rel(over.weights.cpu().numpy(), z["over_E"]) <= 1e-10
+    assert rel(over.A.cpu().numpy(), z["over_A"]) <= 1e-8
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_als_kernels_match_reference(golden, tag):
+    import torch
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200.compress import CompressedTensor
+    z = np.load(golden / f"kernels_{tag}.npz")
+    R, rows = int(z["rank"]), int(z["rows"])
+    K = z["A"].shape[0] // rows
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    comp = CompressedTensor(rank=R, A=d(z["A"]), row_off=np.arange(K + 1) * rows, col_basis=d(z["D"]),
+                            weights=d(z["E"]), cores=d(z["F"]))
+    rots = dp.update_rotations(comp, z["H"], z["V"], z["W"])
+    assert rel(rots.polar.cpu().numpy(), z["polar"]) <= 1e-11
+    assert rel(dp.mttkrp_mode1(comp, rots, z["W"], z["V"]), z["g1"]) <= 1e-11
+    assert rel(dp.mttkrp_mode2(comp, rots, z["W"], z["H"]), z["g2"]) <= 1e-11
+    assert rel(dp.mttkrp_mode3(comp, rots, z["V"], z["H"]), z["g3"]) <= 1e-11
+    assert abs(dp.convergence_metric(comp, rots, z["H"], z["V"], z["W"]) - float(z["metric"])) <= \
+        1e-11 * float(z["metric"])
+    for norm, sfx in ((True, "n"), (False, "p")):
+        h, v, w = dp.update_factors(comp, rots, z["H"], z["V"], z["W"], normalize=norm)
+        assert rel(h, z["H" + sfx]) <= 1e-9 and rel(v, z["V" + sfx]) <= 1e-9 and rel(w, z["W" + sfx]) <= 1e-9
+
+
+def test_c1_config_matches_reference(golden):
+    """Config 1 (K=100, J=100, I_k~U{200..1000}, R=10, 32 iterations, seed 0)."""
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import synth
+    z = np.load(golden / "c1.npz")
+    xs = synth.generate(synth.CONFIGS["c1"], 0)
+    t = dp.IrregularTensor(xs)
+    f, tr = dp.fit_dpar2(t, 10, dp.SolverOptions(max_iters=32, tol=0.0, seed=0))
+    assert abs(dp.fitness(t, f) - float(z["fitness"])) <= FIT_TOL
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), z[key]) <= FACTOR_TOL, key
+    assert rel(tr.objective, z["objective"]) <= 1e-6
+    q = np.concatenate(f.Q)
+    nh = z["Q_head"].shape[0]
+    assert rel_signed(q[:nh] @ f.H, z["Q_head"] @ z["H"]) <= FACTOR_TOL
+    comp = dp.compress(t, 10)
+    assert rel_signed(comp.col_basis.cpu().numpy(), z["D"]) <= 1e-7
+    assert rel(comp.weights.cpu().numpy(), z["E"]) <= 1e-9
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_instances_vs_live_oracle(seed):
+    """Reference-test-style random instances (test_acceptance.py:35-45)."""
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    rng = np.random.default_rng(1000 + seed)
+    R = int(rng.integers(1, 5))
+    J = int(rng.integers(max(R, 4), 17))
+    K = int(rng.integers(1, 13))
+    xs = [rng.random((int(c), J)) for c in rng.integers(R, 21, size=K)]
+    o = orc.fit_dpar2(xs, R, 8, 0.0, 0)
+    f, tr = dp.fit_dpar2(dp.IrregularTensor(xs), R, dp.SolverOptions(max_iters=8, tol=0.0))
+    assert abs(dp.fitness(dp.IrregularTensor(xs), f) - orc.fitness(xs, o["H"], o["V"], o["W"], o["Q"])) <= FIT_TOL
+    assert rel(tr.objective, o["objective"]) <= 1e-6
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
+
+
+def test_errors_mirror_reference():
+    import paper_2203_12798_b200 as dp
+    rng = np.random.default_rng(0)
+    xs = [rng.random((6, 5)) for _ in range(4)]
+    bad = [x.copy() for x in xs]
+    bad[2][3, 1] = np.nan
+    with pytest.raises(dp.NonFiniteInputError, match="slice 2"):
+        dp.IrregularTensor(bad)
+    with pytest.raises(dp.ShapeMismatchError):
+        dp.IrregularTensor([np.ones((3, 4)), np.ones((3, 5))])
+    t = dp.IrregularTensor(xs)
+    with pytest.raises(dp.RankTooLargeError, match="column count"):
+        dp.compress(t, 6)
+    with pytest.raises(dp.RankTooLargeError, match="slice 1"):
+        dp.compress(dp.IrregularTensor([np.ones((6, 5)), np.ones((2, 5))]), 3)
+    with pytest.raises(ValueError):
+        dp.fit_dpar2(t, 2, dp.SolverOptions(max_iters=0))
+
+
+def test_degenerate_slices():
+    """Zero slice and exact-rank slices (test_compress.py:32-49)."""
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200.compress import reconstruct_slice
+    t = dp.IrregularTensor([np.zeros((5, 4)), np.eye(4)])
+    comp = dp.compress(t, 2)
+    assert float(reconstruct_slice(comp, 0).abs().max()) <= 1e-10
+    for a in comp.slice_bases:
+        a = a.cpu().numpy()
+        assert np.abs(a.T @ a - np.eye(2)).max() <= 1e-10
+    rng = np.random.default_rng(1)
+    u, v = rng.standard_normal(9), rng.standard_normal(6)
+    x = 3.0 * np.outer(u / np.linalg.norm(u), v / np.linalg.norm(v))
+    comp = dp.compress(dp.IrregularTensor([x]), 1)
+    assert float((reconstruct_slice(comp, 0).cpu() - x).abs().max()) <= 1e-8
+
+
+def test_fit_is_deterministic():
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=30)
+    t = dp.IrregularTensor(synth.generate(cfg, 4))
+    a, ta = dp.fit_dpar2(t, 10, dp.SolverOptions(max_iters=10, tol=0.0))
+    b, tb = dp.fit_dpar2(t, 10, dp.SolverOptions(max_iters=10, tol=0.0))
+    assert a.H.tobytes() == b.H.tobytes() and a.W.tobytes() == b.W.tobytes() and a.V.tobytes() == b.V.tobytes()
+    assert ta.objective == tb.objective
+    assert np.concatenate(a.Q).tobytes() == np.concatenate(b.Q).tobytes()
