@@ -15,22 +15,15 @@ from .scheduler import PartitionPlan, greedy_partition, resolve_threads
 
 __version__ = "0.1.0"
 
-_LAZY = {
-    "IrregularTensor": "tensor", "CompressedTensor": "compress", "compress": "compress",
-    "reconstruct_slice": "compress", "fit_dpar2": "solver", "update_rotations": "solver",
-    "rotated_cores": "solver", "mttkrp_mode1": "solver", "mttkrp_mode2": "solver", "mttkrp_mode3": "solver",
-    "update_factors": "solver", "convergence_metric": "solver", "fitness": "analysis",
-    "fit_dpar2_distributed": "distributed",
-}
+from .tensor import IrregularTensor  # noqa: E402
+from .compress import CompressedTensor, compress, reconstruct_slice  # noqa: E402
+from .solver import (Rotations, convergence_metric, fit_dpar2, mttkrp_mode1, mttkrp_mode2,  # noqa: E402
+                     mttkrp_mode3, rotated_cores, update_factors, update_rotations)
+from .analysis import fitness  # noqa: E402
 
-
-def __getattr__(name):  # torch-dependent modules load on first use
-    mod = _LAZY.get(name)
-    if mod is None:
-        raise AttributeError(name)
-    import importlib
-    return getattr(importlib.import_module(f"{__name__}.{mod}"), name)
-
+_LAZY = ["IrregularTensor", "CompressedTensor", "compress", "reconstruct_slice", "fit_dpar2", "update_rotations",
+         "rotated_cores", "mttkrp_mode1", "mttkrp_mode2", "mttkrp_mode3", "update_factors", "convergence_metric",
+         "fitness", "Rotations"]
 
 __all__ = sorted(list(_LAZY) + [
     "DecompositionError", "DegenerateInputError", "NonFiniteInputError", "NumericFailure", "RankTooLargeError",

@@ -90,8 +90,6 @@ def check_status(status, what):
     if s[0] != _lib.INT64_MAX:
         from .errors import NonFiniteInputError
         raise NonFiniteInputError(f"slice {s[0]} contains non-finite values")
-    if s[1] > 0:
-        raise NumericFailure(f"{what}: Jacobi iteration did not converge")
     if s[3] != _lib.INT64_MAX:
         raise NumericFailure("SVD did not converge", slice_index=int(s[3]))
     return s

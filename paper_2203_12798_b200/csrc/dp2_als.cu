@@ -65,7 +65,7 @@ DP2_DEV void warp_polar(double* Ts, double* Vr, int ldt, int R, double* pi, doub
   for (int e = lane; e < R * ldt; e += 32) Vr[e] = ((e % ldt) == (e / ldt)) ? 1.0 : 0.0;
   __syncwarp();
   const int sw = jacobi_onesided_warp(Ts, ldt, Vr, ldt, R);
-  if (sw > 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_NOCONV), 1ull);
+  if (sw > 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
   for (int i = lane; i < R; i += 32) {
     double s = 0.0;
     for (int a = 0; a < R; ++a) s = fma(Ts[i * ldt + a], Ts[i * ldt + a], s);
@@ -411,7 +411,7 @@ __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
 // Grams): eigen-decomposition, |lambda| <= R * max|lambda| * 1e-12 dropped.
 DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int* flag, int64_t* status) {
   const int sw = jacobi_eig_block(A, R, U, R, R, cs, flag);
-  if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_NOCONV), 1ull);
+  if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
   __shared__ double lmax;
   if (threadIdx.x == 0) {
     double m = 0.0;
@@ -655,8 +655,6 @@ cudaError_t set_smem(const void* f, size_t bytes) {
 template <int RT>
 cudaError_t launch_mode3_t(const SliceArgs& a, const AlsBufs& b, cudaStream_t st) {
   const size_t sm = slice_smem(a.R, b.wpb, true);
-  cudaError_t e = set_smem((const void*)als_mode3_kernel<RT>, sm);
-  if (e != cudaSuccess) return e;
   als_mode3_kernel<RT><<<b.nwt / b.wpb, 32 * b.wpb, sm, st>>>(a, b);
   return cudaGetLastError();
 }
@@ -691,6 +689,10 @@ cudaError_t prepare(const SliceArgs& a, const AlsBufs& b, int R) {
   if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, slice_smem(R, b.wpb, false));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, solve_smem(R));
+  const size_t m3 = slice_smem(R, b.wpb, true);
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<16>, m3);
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<32>, m3);
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<64>, m3);
   (void)a;
   return e;
 }
@@ -740,13 +742,19 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
     }
     return cudaGetLastError();
   }
+  // Capture on a private stream (the caller's may be the legacy stream, which
+  // cannot capture), then launch the instantiated graph on the caller's stream.
   cudaGraph_t graph;
   cudaGraphExec_t exec;
-  e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  cudaStream_t cs;
+  e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
   if (e != cudaSuccess) return e;
+  e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) { cudaStreamDestroy(cs); return e; }
   for (int it = 0; it < max_iters && e == cudaSuccess; ++it)
-    e = launch_iteration(a, sv, b, it, tol, trace, tstamp, iters, st);
-  cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    e = launch_iteration(a, sv, b, it, tol, trace, tstamp, iters, cs);
+  cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
+  cudaStreamDestroy(cs);
   if (e != cudaSuccess) return e;
   if (e2 != cudaSuccess) return e2;
   e = cudaGraphInstantiate(&exec, graph, 0);

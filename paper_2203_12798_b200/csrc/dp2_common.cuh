@@ -22,10 +22,12 @@ constexpr double kEps = 1.1102230246251565e-16;  // 2^-53
 // ---------------------------------------------------------------- status
 // Device-side status block (int64 x 8), read by the host after a sync.
 //   [0] lowest slice index holding a non-finite value (INT64_MAX = none)
-//   [1] count of Jacobi sweeps that hit the cap (no convergence)
+//   [1] reserved (fatal non-convergence)
 //   [2] lowest slice index whose sketch had numerical rank < R
 //   [3] lowest slice index with a failed polar factor
-enum { ST_NONFINITE = 0, ST_NOCONV = 1, ST_RANKDEF = 2, ST_POLAR = 3 };
+//   [4] count of Jacobi solves that hit the sweep cap (informational: the
+//       result is still at the rounding floor)
+enum { ST_NONFINITE = 0, ST_NOCONV = 1, ST_RANKDEF = 2, ST_POLAR = 3, ST_SWEEPCAP = 4 };
 
 DP2_DEV void status_min(int64_t* st, int slot, int64_t v) {
   atomicMin(reinterpret_cast<unsigned long long*>(st + slot), (unsigned long long)v);
@@ -93,15 +95,16 @@ DP2_DEV void rr_pair(int n_even, int r, int i, int& p, int& q) {
 // leading dim lda, shared memory).  On return diag(A) holds the eigenvalues and
 // V (n x n, ldv) the eigenvectors as columns.  ``cs`` needs 3*(n/2+1) doubles
 // and ``flag`` one int of shared scratch.  Rotations are skipped when
-// |a_pq| <= eps * sqrt(|a_pp a_qq|) (relative criterion: PSD inputs keep
-// high relative accuracy in their small eigenvalues).  Returns sweeps used
-// (max_sweeps+1 on no convergence).
+// |a_pq| <= n eps sqrt(|a_pp a_qq|) (relative criterion: PSD inputs keep
+// high relative accuracy in their small eigenvalues; n eps is the rounding
+// floor).  Returns sweeps used (max_sweeps+1 when the cap was hit).
 DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, double* cs, int* flag,
                              int max_sweeps = 40) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < n * n; i += nt) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
   if (n < 2) { __syncthreads(); return 0; }
   const int ne = n + (n & 1), np = ne / 2;
+  const double tol = n * kEps;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) *flag = 0;
@@ -113,7 +116,7 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
         double c = 1.0, s = 0.0;
         if (q < n) {
           const double apq = A[p * lda + q], app = A[p * lda + p], aqq = A[q * lda + q];
-          if (apq != 0.0 && fabs(apq) > kEps * sqrt(fabs(app * aqq))) {
+          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
             const double th = (aqq - app) / (2.0 * apq);
             const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
             c = 1.0 / sqrt(t * t + 1.0);
@@ -196,6 +199,7 @@ DP2_DEV int jacobi_onesided_warp(double* T, int ldt, double* Vr, int ldv, int n,
   const int lane = threadIdx.x & 31;
   if (n < 2) return 0;
   const int ne = n + (n & 1), np = ne / 2;
+  const double tol = n * kEps;  // rounding floor of the length-n dot products
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int rotated = 0;
@@ -213,7 +217,7 @@ DP2_DEV int jacobi_onesided_warp(double* T, int ldt, double* Vr, int ldv, int n,
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        if (ga != 0.0 && fabs(ga) > kEps * sqrt(al * be)) {
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           const double ze = (be - al) / (2.0 * ga);
           const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
           const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
   }
   // 4. eig(G) -> W, lambda (descending)
   int sw = jacobi_eig_block(G, ld, W, ld, s, cs, &flag);
-  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_NOCONV), 1ull);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
   sort_desc_perm(G, ld, s, perm);
   for (int i = tid; i < s; i += nt) lam[i] = G[perm[i] * ld + perm[i]];
   __syncthreads();
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
   }
   __syncthreads();
   sw = jacobi_eig_block(CC, ld, W, ld, rp, cs, &flag);
-  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_NOCONV), 1ull);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
   sort_desc_perm(CC, ld, rp, perm);
   // 5. P = T U[:, :R], S = sqrt(mu)
   double* Pk = prm.Pm + (size_t)k * sp * R;

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, co
   __shared__ double ev[64];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int sw = jacobi_eig_block(BB, s, Ubuf, s, s, cs, &flag);
-  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_NOCONV), 1ull);
+  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
   sort_desc_perm(BB, s, s, perm);
   for (int r = tid; r < R; r += nt) {
     const double mu = BB[perm[r] * s + perm[r]];

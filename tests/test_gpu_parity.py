@@ -36,6 +36,19 @@ def load_fit(golden, name):
     return z, xs
 
 
+def check_trace(tr, ref_obj, ref_converged, xs):
+    """Objective trace parity.  When the compressed model fits exactly (the
+    reference's e is rounding noise, e.g. R = 1), e and the tol = 0 stopping
+    point are noise-driven, so only the noise level is checked."""
+    scale = sum(float(np.dot(x.ravel(), x.ravel())) for x in xs)
+    if max(ref_obj) <= 1e-20 * scale:
+        assert max(tr.objective) <= 1e-18 * scale
+        return
+    assert tr.iterations == len(ref_obj)
+    assert tr.converged == ref_converged
+    assert rel(tr.objective, ref_obj) <= 1e-6
+
+
 FIT_CASES = ["tiny0", "tiny1", "tiny2", "tiny3", "tiny4", "tiny5", "planted", "planted_tol", "planted_nonorm",
              "f32vals", "wide"]
 
@@ -48,10 +61,8 @@ def test_fit_matches_reference_fp64(golden, name):
     opts = dp.SolverOptions(max_iters=int(z["max_iters"]), tol=float(z["tol"]), seed=int(z["seed"]),
                             normalize=bool(z["normalize"]))
     f, tr = dp.fit_dpar2(t, int(z["rank"]), opts)
-    assert tr.iterations == len(z["objective"])
-    assert tr.converged == bool(z["converged"])
     assert tr.compressed_float_count == int(z["float_count"])
-    assert rel(tr.objective, z["objective"]) <= 1e-6
+    check_trace(tr, list(z["objective"]), bool(z["converged"]), xs)
     fit = dp.fitness(t, f)
     assert abs(fit - float(z["fitness"])) <= FIT_TOL
     assert rel_signed(f.H, z["H"]) <= FACTOR_TOL
@@ -161,7 +172,7 @@ def test_random_instances_vs_live_oracle(seed):
     o = orc.fit_dpar2(xs, R, 8, 0.0, 0)
     f, tr = dp.fit_dpar2(dp.IrregularTensor(xs), R, dp.SolverOptions(max_iters=8, tol=0.0))
     assert abs(dp.fitness(dp.IrregularTensor(xs), f) - orc.fitness(xs, o["H"], o["V"], o["W"], o["Q"])) <= FIT_TOL
-    assert rel(tr.objective, o["objective"]) <= 1e-6
+    check_trace(tr, o["objective"], o["converged"], xs)
     for key in ("H", "V", "W"):
         assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
 
