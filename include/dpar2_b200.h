@@ -71,6 +71,9 @@ int dp2_abi_version(void);
 const char* dp2_status_string(int status);
 const char* dp2_last_error(void);
 int dp2_device_sm_count(void);
+/* Kernels enqueued by this library so far (every launch, including the
+ * kernels inside the ALS graph); reset != 0 returns the count and zeroes it. */
+int64_t dp2_launch_count(int32_t reset);
 /* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
 int dp2_status_init(int64_t* status_dev, void* stream);
 

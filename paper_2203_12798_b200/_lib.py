@@ -37,6 +37,7 @@ _SIGS = {
     "dp2_status_string": (C.c_char_p, [c_i32]),
     "dp2_last_error": (C.c_char_p, []),
     "dp2_device_sm_count": (c_i32, []),
+    "dp2_launch_count": (c_i64, [c_i32]),
     "dp2_status_init": (c_i32, [c_vp, c_vp]),
     "dp2_greedy_partition": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i64), P(c_i32), P(c_i64)]),
     "dp2_piece_capacity": (c_i64, [c_i64, c_i32]),

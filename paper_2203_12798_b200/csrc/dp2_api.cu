@@ -7,8 +7,15 @@
 
 #include "dp2_internal.h"
 
+#include <atomic>
+
 namespace {
 thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+int ok(int64_t n) {
+  g_launches += n;
+  return DP2_OK;
+}
 
 int fail(cudaError_t e, const char* where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -43,6 +50,10 @@ const char* dp2_status_string(int s) {
 }
 
 const char* dp2_last_error(void) { return g_last_error.c_str(); }
+
+int64_t dp2_launch_count(int32_t reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
 
 int dp2_device_sm_count(void) {
   int dev = 0, n = 0;
@@ -124,7 +135,7 @@ int dp2_plan_pieces(const int64_t* row_off, int64_t K, int32_t nseg, int32_t* pi
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream) {
   if (!store_ok(st)) return fail_arg("invalid store");
   cudaError_t e = dp2::run_slice_stats(st, sqnorm_dev, status_dev, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_slice_stats");
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_slice_stats");
 }
 
 size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
@@ -140,7 +151,7 @@ int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_de
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
                                   static_cast<char*>(ws), status_dev, timing_ms, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_stage1");
+  return e == cudaSuccess ? ok(8) : fail(e, "dp2_stage1");
 }
 
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {
@@ -154,7 +165,7 @@ int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_
   if (ws_bytes < dp2::stage2_bytes(J, KR, s2, rank)) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
                                   static_cast<char*>(ws), status_dev, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_stage2");
+  return e == cudaSuccess ? ok(12) : fail(e, "dp2_stage2");
 }
 
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }
@@ -168,7 +179,7 @@ int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, in
   if (ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("workspace too small");
   cudaError_t e = dp2::als_run(F, D, E, K, J, R, H, V, W, polar_out, max_iters, tol, normalize, trace_out,
                                tstamp_out, iters_out, use_graph, static_cast<char*>(ws), status_dev, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_als_run");
+  return e == cudaSuccess ? ok(1 + 6 * (int64_t)max_iters) : fail(e, "dp2_als_run");
 }
 
 int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
@@ -177,7 +188,7 @@ int dp2_update_rotations(const double* F, const double* D, const double* E, int6
   if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
   cudaError_t e = dp2::als_rotations(F, D, E, K, J, R, H, V, W, polar_out, theta_out, static_cast<char*>(ws),
                                      status_dev, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_update_rotations");
+  return e == cudaSuccess ? ok(2) : fail(e, "dp2_update_rotations");
 }
 
 int dp2_mttkrp(int32_t mode, const double* theta, const double* D, const double* E, int64_t K, int64_t J,
@@ -186,7 +197,7 @@ int dp2_mttkrp(int32_t mode, const double* theta, const double* D, const double*
   if (mode < 1 || mode > 3 || R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R))
     return fail_arg("invalid arguments");
   cudaError_t e = dp2::als_mttkrp(mode, theta, D, E, K, J, R, H, V, W, out, static_cast<char*>(ws), S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_mttkrp");
+  return e == cudaSuccess ? ok(mode == 2 ? 4 : (mode == 1 ? 3 : 2)) : fail(e, "dp2_mttkrp");
 }
 
 int dp2_update_factors(const double* theta, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
@@ -195,7 +206,7 @@ int dp2_update_factors(const double* theta, const double* D, const double* E, in
   if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
   cudaError_t e = dp2::als_update_factors(theta, D, E, K, J, R, H, V, W, normalize, static_cast<char*>(ws),
                                           status_dev, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_update_factors");
+  return e == cudaSuccess ? ok(6) : fail(e, "dp2_update_factors");
 }
 
 int dp2_convergence_metric(const double* theta, const double* D, const double* E, int64_t K, int64_t J,
@@ -203,14 +214,14 @@ int dp2_convergence_metric(const double* theta, const double* D, const double* E
                            size_t ws_bytes, void* stream) {
   if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
   cudaError_t e = dp2::als_metric(theta, D, E, K, J, R, H, V, W, out, static_cast<char*>(ws), S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_convergence_metric");
+  return e == cudaSuccess ? ok(3) : fail(e, "dp2_convergence_metric");
 }
 
 int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar, double* Q_out,
                    void* stream) {
   if (!store_ok(st) || R < 1 || R > 64) return fail_arg("invalid arguments");
   cudaError_t e = dp2::run_assemble_q(st, A, R, polar, Q_out, S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_assemble_q");
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_assemble_q");
 }
 
 size_t dp2_fitness_workspace(const dp2_store* st) { return dp2::fitness_bytes(st); }
@@ -219,7 +230,7 @@ int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H
                 const double* W, double* out2_dev, void* ws, size_t ws_bytes, void* stream) {
   if (!store_ok(st) || R < 1 || R > 64 || ws_bytes < dp2::fitness_bytes(st)) return fail_arg("invalid arguments");
   cudaError_t e = dp2::run_fitness(st, Q, R, H, V, W, out2_dev, static_cast<char*>(ws), S(stream));
-  return e == cudaSuccess ? DP2_OK : fail(e, "dp2_fitness");
+  return e == cudaSuccess ? ok(2) : fail(e, "dp2_fitness");
 }
 
 }  // extern "C"

@@ -91,3 +91,32 @@ def scaled(cfg: SynthConfig, **kw):
     d = cfg.__dict__.copy()
     d.update(kw)
     return SynthConfig(**d)
+
+
+def generate_device(cfg: SynthConfig, seed=0, device="cuda", slices=None):
+    """Same generative model drawn with torch's CUDA generator (for the large
+    benchmark configs, where host generation would dominate the run).
+    Returns (packed X (sum I_k x J) on ``device``, row counts, H, V).  Row
+    counts, H and V are the host draws above, so slice shapes match
+    ``generate``; the per-slice Gaussians differ (different RNG)."""
+    import torch
+
+    rows, h, v = shared_factors(cfg, seed)
+    idx = list(range(cfg.num_slices)) if slices is None else list(slices)
+    rows = [rows[k] for k in idx]
+    tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(int(np.random.SeedSequence([seed, 2]).generate_state(1, np.uint64)[0]) & ((1 << 63) - 1))
+    H = torch.from_numpy(h).to(device)
+    V = torch.from_numpy(v).to(device)
+    X = torch.empty((int(sum(rows)), cfg.cols), dtype=tdt, device=device)
+    r0 = 0
+    for n in rows:
+        q, _ = torch.linalg.qr(torch.randn((n, cfg.rank), generator=g, device=device, dtype=torch.float64))
+        s = torch.rand(cfg.rank, generator=g, device=device, dtype=torch.float64) + 0.5
+        signal = (q @ (H * s)) @ V.T
+        noise = torch.randn(signal.shape, generator=g, device=device, dtype=torch.float64)
+        scale = cfg.noise * torch.linalg.norm(signal) / float(np.sqrt(signal.numel()))
+        X[r0:r0 + n] = (signal + scale * noise).to(tdt)
+        r0 += n
+    return X, rows, h, v

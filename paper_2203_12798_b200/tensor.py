@@ -113,7 +113,8 @@ class IrregularTensor:
         for a in arrs:
             n = a.shape[0]
             if isinstance(a, torch.Tensor):
-                src = a.to(device=dev, dtype=tdt)
+                # pinned host tensors go straight into the packed buffer (async H2D)
+                src = a if (a.device.type == "cpu" and a.dtype == tdt) else a.to(device=dev, dtype=tdt)
             else:
                 src = torch.from_numpy(np.ascontiguousarray(a, dtype=_NP[self.dtype]))
             if self.ldx == J:
