@@ -94,6 +94,28 @@ int dp2_plan_pieces(const int64_t* row_off, int64_t K, int32_t nseg, int32_t* pi
                     int64_t* piece_row0, int32_t* piece_rows, int32_t* seg_begin,
                     int32_t* slice_piece, int64_t* npieces_out);
 
+/* ------------------------------------------------------------------ sketch matrices
+ * derived_seed(seed, index) of P/linalg.py:187-194 (numpy SeedSequence hash),
+ * computed natively (host). */
+uint64_t dp2_derived_seed(uint64_t seed, uint64_t index);
+/* Omega_k for K slices on the device, bit-exact with the reference's
+ * Generator(PCG64(derived_seed(seed, id_k))).standard_normal((J, s_k))
+ * (P/linalg.py:122-123): out is K x J x sp (zero padded beyond s_k).
+ * id_k = slice_ids_dev[k] (device, nullable -> k).  Layer-0 tail draws
+ * (~2.6e-4 of draws) depend on libm log1p rounding: each is written to
+ * ``recs`` (dp2_tail_record, capacity ``cap``, count in *nrec_dev) for the
+ * host to replay with the reference's log1p and patch; redo_dev[k] != 0 asks
+ * the host to regenerate slice k (record overflow).  See rng.py. */
+typedef struct dp2_tail_record {
+  int64_t slice, index;   /* local slice, output index (C order in J x s_k) */
+  int32_t attempts;       /* accepted on attempt #attempts (<= 4)           */
+  int32_t negative;       /* sign of the output                              */
+  double u[8];            /* (u1, u2) uniforms of each attempt               */
+} dp2_tail_record;
+int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev, int32_t sp,
+                       const int64_t* slice_ids_dev, double* out, dp2_tail_record* recs, int32_t cap,
+                       int32_t* nrec_dev, int32_t* redo_dev, void* stream);
+
 /* ------------------------------------------------------------------ tensor checks
  * Per-slice squared Frobenius norms (sqnorm_dev[K]) and the lowest slice with
  * a NaN/Inf (status[0]); mirrors IrregularTensor's isfinite check

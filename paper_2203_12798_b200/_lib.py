@@ -43,6 +43,9 @@ _SIGS = {
     "dp2_piece_capacity": (c_i64, [c_i64, c_i32]),
     "dp2_plan_pieces": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i32), P(c_i64), P(c_i32), P(c_i32), P(c_i32),
                                 P(c_i64)]),
+    "dp2_derived_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "dp2_omega_generate": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
+                                   c_vp]),
     "dp2_slice_stats": (c_i32, [P(Store), c_vp, c_vp, c_vp]),
     "dp2_stage1_workspace": (c_sz, [P(Store), c_i32, c_i32]),
     "dp2_stage1": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,

@@ -8,6 +8,7 @@ accepted (they never change values in the reference either).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
 from dataclasses import dataclass, replace
 
@@ -17,7 +18,7 @@ import torch
 from . import _lib
 from .errors import NumericFailure, RankTooLargeError
 from .linalg import RsvdParams, derived_seed, padded_width, sketch_width
-from .rng import omega_host, stage2_omega
+from .rng import omega_device, stage2_omega
 from .scheduler import resolve_threads
 from .tensor import IrregularTensor, new_status, sm_count, stream_ptr
 
@@ -117,9 +118,20 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
     widths = [sketch_width(m, J, rank, base.oversampling) for m in tensor.row_counts]
     sp = padded_width(max(widths))
     dev = tensor.X.device
+    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on a host
+    # thread while the device generates the stage-1 sketches and runs stage 1
+    second = stage2 if stage2 is not None else base
+    second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
+    if second.power_iters != 1:
+        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
+    KR = K * rank
+    s2 = sketch_width(J, KR, rank, second.oversampling)
+    om2_box = {}
+    om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, KR, s2)))
+    om2_thread.start()
     t0 = time.perf_counter()
-    om_host = omega_host(base.seed, J, widths, sp)
-    omega = om_host.to(dev, non_blocking=True)
+    rstats = {}
+    omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
     s_dev = torch.tensor(widths, dtype=torch.int32).to(dev, non_blocking=True)
     t_omega = time.perf_counter() - t0
     nseg = nseg_for(tensor)
@@ -135,13 +147,8 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
                               _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
     del ws
     # stage 2 (P/compress.py:109-111)
-    second = stage2 if stage2 is not None else base
-    second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
-    if second.power_iters != 1:
-        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
-    KR = K * rank
-    s2 = sketch_width(J, KR, rank, second.oversampling)
-    om2 = torch.from_numpy(stage2_omega(second.seed, KR, s2)).to(dev)
+    om2_thread.join()
+    om2 = torch.from_numpy(om2_box["v"]).to(dev)
     D = torch.empty((J, rank), dtype=torch.float64, device=dev)
     E = torch.empty(rank, dtype=torch.float64, device=dev)
     F = torch.empty((KR, rank), dtype=torch.float64, device=dev)
@@ -156,6 +163,7 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
     check_status(status, "compress")
     if timings is not None:
         torch.cuda.synchronize()
+        timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
                        stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
                        stage1_ms=tm[5], stage2_ms=ev[0].elapsed_time(ev[1]), sp=sp, s2=s2, nseg=nseg,

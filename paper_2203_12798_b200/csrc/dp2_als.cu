@@ -1,46 +1,52 @@
 // Compressed-space ALS (P/solver.py:39-190), fp64.
 //
-// One iteration = 6 launches, all stream-ordered and graph-capturable:
-//   rotate   (warp/slice) T_k = (F_k cc) diag(w_k) H^T, polar Pi_k = Z_k P_k^T
-//            (one-sided Jacobi), Theta_k = Pi_k^T F_k, mode-1 + gram(W) partials
-//   solve_h  (1 CTA)      H = G1 pinv(W'W * V'V), column norms -> nh
-//   mode2    (warp/slice) sum_k (w_k nh) (Theta_k^T H), gram(W nh) partials
-//   solve_v  (1 CTA)      V = D (E * summed) pinv(...), norms, V'V, cc', pinv3
-//   mode3    (warp/slice) G3 row, W_k = G3_k pinv3, metric e_k
-//   finish   (1 warp)     e = sum of partials (fixed order), trace, stop rule
-// Partials live in per-warp slots (each warp owns a slot and visits a fixed
-// slice set), reduced in slot order: deterministic for a given device.
-// Every kernel returns at once when the device stop flag is set, so the whole
-// max_iters loop can be one CUDA graph with no host round trip
-// (P/solver.py:180-184 evaluated on the device).
+// One iteration = 7 stream-ordered, graph-capturable launches:
+//   rotate  (warp/slice) T_k = (F_k cc) diag(w_k) H^T; polar Pi_k = Z_k P_k^T by
+//           one-sided Jacobi warm-started from the previous iteration's P_k;
+//           Theta_k = Pi_k^T F_k; mode-1 and gram(W) partials
+//   solve_h (1 CTA)      H = G1 pinv(W'W * V'V); column norms -> nh
+//   mode2   (warp/slice) sum_k (w_k nh) (Theta_k^T H), gram(W nh) partials
+//   solve_v (1 CTA)      V = D (E * summed) pinv(...); norms; V'V, cc', pinv3
+//   mode3   (warp/slice) G3 row, W_k = G3_k pinv3; L_k = [Theta_k E | -H W_k]
+//   metric  (DMMA)       e = ||L N^T||_F^2 with N = [D V] (J x 2R): the
+//           reference's sum_k ||Theta_k E D^T - H S_k V^T||^2 as one tall GEMM
+//           with a fused sum-of-squares epilogue (the R x J products are never
+//           stored)
+//   finish  (1 warp)     e = ordered sum of partials, trace, device stop rule
+// Partials go to per-CTA slots (warps combined in warp order, slots reduced in
+// slot order by a fixed warp tree): deterministic for a given device.  Every
+// kernel returns at once when the device stop flag is set, so the whole loop
+// is one CUDA graph (P/solver.py:180-184 evaluated on the device).
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
 namespace dp2 {
 
 struct AlsBufs {
-  double *theta, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2;
-  double *p_g1, *p_wtw, *p_m2, *p_wtw2, *p_e, *scratch, *g3;
-  int32_t* ctl;  // [0] stop flag
-  int nwt;       // total warps (partial slots)
+  double *theta, *pprev, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2, *L;
+  double *s_g1, *s_wtw, *s_m2, *s_wtw2, *s_e, *G2, *g3;
+  int32_t* ctl;  // [0] stop flag, [1] warm-start valid
+  int nwt;       // total warps in the per-slice kernels
   int wpb;       // warps per block
+  int nb;        // blocks == partial slots
+  int nbm;       // metric kernel blocks (slots)
 };
 
 __host__ __device__ inline int wpb_for(int R) { return R <= 16 ? 8 : (R <= 32 ? 4 : 1); }
 __host__ __device__ inline int ldt_for(int R) { return R | 1; }
+// per-warp smem: Ts, Vr (R x ldt), Fs, Th, Pi (R x R), two partial accumulators (R x R), tmp (4R)
 __host__ __device__ inline size_t warp_smem_doubles(int R) {
   const int ldt = ldt_for(R);
-  return (size_t)2 * R * ldt + 3 * (size_t)R * R + 4 * R;
+  return (size_t)2 * R * ldt + 5 * (size_t)R * R + 4 * R;
 }
+__host__ __device__ inline size_t cta_shared_doubles(int R) { return 3 * (size_t)R * R + 2 * R; }
 
-DP2_DEV double globaltimer_ns() {
+DP2_DEV uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return (double)t;
+  return t;
 }
 
-// ------------------------------------------------------------ common loads
-// Per-CTA shared: cc (R x R), H (R x R), E (R), aux (R x R), vec (R)
 struct CtaShared {
   double *cc, *H, *E, *aux, *vec;
 };
@@ -53,17 +59,14 @@ DP2_DEV CtaShared carve_cta(double* base, int R) {
   s.vec = s.aux + R * R;
   return s;
 }
-__host__ __device__ inline size_t cta_shared_doubles(int R) { return 3 * (size_t)R * R + 2 * R; }
 
 // ------------------------------------------------------------ polar factor
-// Pi = Z P^T of T (R x R) via one-sided Jacobi; exact-zero singular directions
-// are completed to an orthonormal set (LAPACK returns some such completion).
-// Ts, Vr: column-major (ldt); out: Pi row-major into ``pi``.
+// Pi = Z P^T of T (column-major in Ts, already multiplied by the warm start
+// Vr = P_prev) via one-sided Jacobi; exact-zero singular directions are
+// completed to an orthonormal set (LAPACK likewise returns some completion).
 DP2_DEV void warp_polar(double* Ts, double* Vr, int ldt, int R, double* pi, double* nrm, int64_t* status,
                         int64_t k) {
   const int lane = threadIdx.x & 31;
-  for (int e = lane; e < R * ldt; e += 32) Vr[e] = ((e % ldt) == (e / ldt)) ? 1.0 : 0.0;
-  __syncwarp();
   const int sw = jacobi_onesided_warp(Ts, ldt, Vr, ldt, R);
   if (sw > 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
   for (int i = lane; i < R; i += 32) {
@@ -108,8 +111,7 @@ DP2_DEV void warp_polar(double* Ts, double* Vr, int ldt, int R, double* pi, doub
     }
   }
   __syncwarp();
-  // Pi[a][d] = sum_i Z[a][i] P[d][i]   (Z = Ts columns, P = Vr columns)
-  for (int e = lane; e < R * R; e += 32) {
+  for (int e = lane; e < R * R; e += 32) {  // Pi[a][d] = sum_i Z[a][i] P[d][i]
     const int a = e / R, d = e % R;
     double s = 0.0;
     for (int i = 0; i < R; ++i) s = fma(Ts[i * ldt + a], Vr[i * ldt + d], s);
@@ -118,7 +120,7 @@ DP2_DEV void warp_polar(double* Ts, double* Vr, int ldt, int R, double* pi, doub
   __syncwarp();
 }
 
-// ------------------------------------------------------------ small helpers
+// ------------------------------------------------------------ helpers
 __global__ void reduce_parts_dev(const double* part, int nparts, int64_t size, double* out) {
   for (int64_t idx = threadIdx.x; idx < size; idx += blockDim.x) {
     double acc = 0.0;
@@ -139,7 +141,19 @@ __global__ void g2_kernel(const double* D, const double* E, const double* summed
   out[e] = acc;
 }
 
-// cc = E * (D^T V) and VtV = V^T V with one warp per entry (no block barriers)
+// Ordered reduction of per-CTA slots: warp w handles entries w, w+nw, ...;
+// lanes stride over slots, fixed xor tree.  Deterministic for a given nslots.
+DP2_DEV void reduce_slots_warp(const double* slots, int nslots, int n, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = warp; e < n; e += nw) {
+    double s = 0.0;
+    for (int w = lane; w < nslots; w += 32) s += slots[(size_t)w * n + e];
+    s = warp_sum(s);
+    if (lane == 0) out[e] = s;
+  }
+}
+
+// cc = E * (D^T V) and VtV = V^T V, one warp per entry
 DP2_DEV void gram_dv_warps(const double* D, const double* E, const double* V, int64_t J, int R, double* cc,
                            double* VtV, double* Mv, const double* HtH) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -161,14 +175,25 @@ DP2_DEV void gram_dv_warps(const double* D, const double* E, const double* V, in
   }
 }
 
+// CTA combine of per-warp smem partials (warp order) into the CTA's slot.
+DP2_DEV void combine_warps(const double* wbase, size_t wstride, int nwarps, int n, double* slot) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nwarps; ++w) s += wbase[w * wstride + e];
+    slot[e] = s;
+  }
+}
+
 // ------------------------------------------------------------ prep / finish
-// cc = E * (D^T V), VtV = V^T V, stop = 0, tstamp[0]
 __global__ void als_prep_kernel(const double* D, const double* E, const double* V, int64_t J, int R,
                                 AlsBufs b, int64_t* tstamp, int reset) {
   gram_dv_warps(D, E, V, J, R, b.cc, b.VtV, nullptr, nullptr);
   if (threadIdx.x == 0) {
     for (int r = 0; r < R; ++r) b.nh[r] = 1.0;
-    if (reset) b.ctl[0] = 0;
+    if (reset) {
+      b.ctl[0] = 0;
+      b.ctl[1] = 0;
+    }
     if (tstamp) tstamp[0] = (int64_t)globaltimer_ns();
   }
 }
@@ -176,12 +201,15 @@ __global__ void als_prep_kernel(const double* D, const double* E, const double* 
 __global__ void als_finish_kernel(AlsBufs b, int it, double tol, double* trace, int64_t* tstamp,
                                   int32_t* iters) {
   if (b.ctl[0]) return;
-  if (threadIdx.x != 0) return;
-  double e = 0.0;
-  for (int w = 0; w < b.nwt; ++w) e += b.p_e[w];
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int w = lane; w < b.nbm; w += 32) s += b.s_e[w];
+  const double e = warp_sum(s);
+  if (lane != 0) return;
   trace[it] = e;
   if (tstamp) tstamp[it + 1] = (int64_t)globaltimer_ns();
   *iters = it + 1;
+  b.ctl[1] = 1;  // warm start valid from now on
   if (it > 0) {
     const double prev = trace[it - 1];
     if (prev == 0.0 || fabs(prev - e) <= tol * prev) b.ctl[0] = 1;
@@ -195,8 +223,9 @@ struct SliceArgs {
   int64_t K, J;
   int R;
   int mode1;      // rotate: also emit mode-1 and gram(W) partials
-  int metric;     // mode3: also emit metric partials
+  int warm;       // rotate: warm start from b.pprev when b.ctl[1]
   int write_w;    // mode3: W_k = G3_k pinv3 (else write G3 into Wout)
+  int write_l;    // mode3: emit L_k rows for the metric GEMM
   int64_t* status;
 };
 
@@ -214,28 +243,34 @@ DP2_DEV void load_cta_common(const SliceArgs& a, const AlsBufs& b, CtaShared& s,
   __syncthreads();
 }
 
-// accumulate an R x R block into this warp's global slot (first visit writes)
-DP2_DEV void slot_add(double* slot, int e, double v, bool first) { slot[e] = first ? v : slot[e] + v; }
-
 __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
   if (b.ctl[0]) return;
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, ldt = ldt_for(R), lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
-  double* wbase = sm + cta_shared_doubles(R) + (size_t)wib * warp_smem_doubles(R);
-  double* Ts = wbase;
+  const size_t wstride = warp_smem_doubles(R);
+  double* wbase = sm + cta_shared_doubles(R);
+  double* Ts = wbase + (size_t)wib * wstride;
   double* Vr = Ts + R * ldt;
   double* Fs = Vr + R * ldt;
   double* Th = Fs + R * R;
   double* Pi = Th + R * R;
-  double* tmp = Pi + R * R;  // 4R
+  double* acc1 = Pi + R * R;
+  double* acc2 = acc1 + R * R;
+  double* tmp = acc2 + R * R;  // 4R
   load_cta_common(a, b, cs, true, false);
+  const bool warm = a.warm && b.ctl[1];
+  for (int e = lane; e < R * R; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const int gw = blockIdx.x * b.wpb + wib;
-  bool first = true;
   for (int64_t k = gw; k < a.K; k += b.nwt) {
     const double* Fk = a.F + k * R * R;
     const double* wk = a.W + k * R;
     for (int e = lane; e < R * R; e += 32) Fs[e] = Fk[e];
+    // warm start: Vr = P_prev (column-major), else identity
+    for (int e = lane; e < R * R; e += 32) {
+      const int i = e / R, d = e % R;  // Vr[col i][row d]
+      Vr[i * ldt + d] = warm ? b.pprev[k * R * R + e] : (i == d ? 1.0 : 0.0);
+    }
     __syncwarp();
     // Th <- (F_k cc) * w_k   (reference: (core_block(k) @ core_cols) * w[k])
     for (int e = lane; e < R * R; e += 32) {
@@ -245,15 +280,29 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
       Th[e] = s * wk[c];
     }
     __syncwarp();
-    // T = Th H^T, stored column-major in Ts
+    // Pi <- T = Th H^T (row-major scratch), then Ts = T Vr (column-major)
     for (int e = lane; e < R * R; e += 32) {
       const int i = e / R, d = e % R;
       double s = 0.0;
       for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], cs.H[d * R + c], s);
-      Ts[d * ldt + i] = s;
+      Pi[e] = s;
+    }
+    __syncwarp();
+    for (int e = lane; e < R * R; e += 32) {
+      const int c = e / R, i = e % R;  // Ts[col c][row i] = sum_d T[i][d] Vr[col c][row d]
+      double s = 0.0;
+      if (warm)
+        for (int d = 0; d < R; ++d) s = fma(Pi[i * R + d], Vr[c * ldt + d], s);
+      else
+        s = Pi[i * R + c];
+      Ts[c * ldt + i] = s;
     }
     __syncwarp();
     warp_polar(Ts, Vr, ldt, R, Pi, tmp, a.status, k);
+    for (int e = lane; e < R * R; e += 32) {  // keep P_k for the next warm start
+      const int i = e / R, d = e % R;
+      b.pprev[k * R * R + e] = Vr[i * ldt + d];
+    }
     // Theta = Pi^T F
     for (int e = lane; e < R * R; e += 32) {
       const int i = e / R, c = e % R;
@@ -266,24 +315,20 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
     __syncwarp();
     if (a.mode1) {
       // g1[i][r] += w[k][r] * (Theta cc)[i][r];  wtw[i][r] += w[k][i] w[k][r]
-      double* sg = b.p_g1 + (size_t)gw * R * R;
-      double* sw = b.p_wtw + (size_t)gw * R * R;
       for (int e = lane; e < R * R; e += 32) {
         const int i = e / R, r = e % R;
         double s = 0.0;
         for (int q = 0; q < R; ++q) s = fma(Th[i * R + q], cs.cc[q * R + r], s);
-        slot_add(sg, e, wk[r] * s, first);
-        slot_add(sw, e, wk[i] * wk[r], first);
+        acc1[e] += wk[r] * s;
+        acc2[e] += wk[i] * wk[r];
       }
     }
-    first = false;
     __syncwarp();
   }
-  if (a.mode1 && first) {  // warp had no slice: zero its slots
-    for (int e = lane; e < R * R; e += 32) {
-      b.p_g1[(size_t)gw * R * R + e] = 0.0;
-      b.p_wtw[(size_t)gw * R * R + e] = 0.0;
-    }
+  if (a.mode1) {
+    __syncthreads();
+    combine_warps(wbase + (acc1 - Ts), wstride, b.wpb, R * R, b.s_g1 + (size_t)blockIdx.x * R * R);
+    combine_warps(wbase + (acc2 - Ts), wstride, b.wpb, R * R, b.s_wtw + (size_t)blockIdx.x * R * R);
   }
 }
 
@@ -292,11 +337,13 @@ __global__ void als_mode1_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
+  const size_t wstride = 2 * (size_t)R * R;
+  double* wbase = sm + cta_shared_doubles(R);
+  double* acc1 = wbase + wib * wstride;
+  double* acc2 = acc1 + R * R;
   load_cta_common(a, b, cs, false, false);
+  for (int e = lane; e < R * R; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const int gw = blockIdx.x * b.wpb + wib;
-  double* sg = b.p_g1 + (size_t)gw * R * R;
-  double* sw = b.p_wtw + (size_t)gw * R * R;
-  for (int e = lane; e < R * R; e += 32) { sg[e] = 0.0; sw[e] = 0.0; }
   for (int64_t k = gw; k < a.K; k += b.nwt) {
     const double* Th = a.theta + k * R * R;
     const double* wk = a.W + k * R;
@@ -304,10 +351,13 @@ __global__ void als_mode1_kernel(SliceArgs a, AlsBufs b) {
       const int i = e / R, r = e % R;
       double s = 0.0;
       for (int q = 0; q < R; ++q) s = fma(Th[i * R + q], cs.cc[q * R + r], s);
-      sg[e] += wk[r] * s;
-      sw[e] += wk[i] * wk[r];
+      acc1[e] += wk[r] * s;
+      acc2[e] += wk[i] * wk[r];
     }
   }
+  __syncthreads();
+  combine_warps(wbase, wstride, b.wpb, R * R, b.s_g1 + (size_t)blockIdx.x * R * R);
+  combine_warps(wbase + R * R, wstride, b.wpb, R * R, b.s_wtw + (size_t)blockIdx.x * R * R);
 }
 
 __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
@@ -315,11 +365,13 @@ __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
+  const size_t wstride = 2 * (size_t)R * R;
+  double* wbase = sm + cta_shared_doubles(R);
+  double* acc1 = wbase + wib * wstride;
+  double* acc2 = acc1 + R * R;
   load_cta_common(a, b, cs, true, false);
+  for (int e = lane; e < R * R; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const int gw = blockIdx.x * b.wpb + wib;
-  double* sm2 = b.p_m2 + (size_t)gw * R * R;
-  double* sw2 = b.p_wtw2 + (size_t)gw * R * R;
-  for (int e = lane; e < R * R; e += 32) { sm2[e] = 0.0; sw2[e] = 0.0; }
   for (int64_t k = gw; k < a.K; k += b.nwt) {
     const double* Th = a.theta + k * R * R;
     const double* wk = a.W + k * R;
@@ -328,27 +380,29 @@ __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
       double s = 0.0;  // (Theta^T H)[ai][r]
       for (int q = 0; q < R; ++q) s = fma(Th[q * R + ai], cs.H[q * R + r], s);
       const double wr = wk[r] * cs.vec[r], wa = wk[ai] * cs.vec[ai];
-      sm2[e] += wr * s;
-      sw2[e] += wa * wr;
+      acc1[e] += wr * s;
+      acc2[e] += wa * wr;
     }
   }
+  __syncthreads();
+  combine_warps(wbase, wstride, b.wpb, R * R, b.s_m2 + (size_t)blockIdx.x * R * R);
+  combine_warps(wbase + R * R, wstride, b.wpb, R * R, b.s_wtw2 + (size_t)blockIdx.x * R * R);
 }
 
-template <int RT>
+// G3 row, new W row, and the metric operator rows L_k = [Theta_k E | -H W_k]
 __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
   if (b.ctl[0]) return;
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
-  load_cta_common(a, b, cs, true, a.write_w != 0);
-  double* L = sm + cta_shared_doubles(R) + (size_t)wib * (2 * (size_t)R * R + 2 * R);  // R x 2R
-  double* g3 = L + 2 * R * R;
+  double* g3 = sm + cta_shared_doubles(R) + (size_t)wib * 2 * R;
   double* wn = g3 + R;
+  load_cta_common(a, b, cs, true, a.write_w != 0);
   const int gw = blockIdx.x * b.wpb + wib;
-  double esum = 0.0;
+  const int ldl = 2 * R;
   for (int64_t k = gw; k < a.K; k += b.nwt) {
     const double* Th = a.theta + k * R * R;
-    // G3[r] = sum_i H[i][r] sum_j Theta[i][j] cc[j][r]
+    // G3[r] = sum_i H[i][r] sum_j Theta[i][j] cc[j][r]   (P/solver.py:109-111)
     for (int r = lane; r < R; r += 32) {
       double s = 0.0;
       for (int i = 0; i < R; ++i) {
@@ -368,55 +422,82 @@ __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
         s = g3[c];
       }
       wn[c] = s;
-      a.Wout[k * R + c] = s;
+      if (a.Wout) a.Wout[k * R + c] = s;
     }
     __syncwarp();
-    if (a.metric) {
-      // L = [Theta * E | -(H * w_k)];  e_k = sum_j sum_i (L [D_j; V_j])_i^2
+    if (a.write_l) {
       const double* wk = a.write_w ? wn : a.W + k * R;
-      for (int e = lane; e < 2 * R * R; e += 32) {
-        const int i = e / (2 * R), c = e % (2 * R);
-        L[e] = c < R ? Th[i * R + c] * cs.E[c] : -(cs.H[i * R + (c - R)] * wk[c - R]);
+      for (int e = lane; e < R * ldl; e += 32) {
+        const int i = e / ldl, c = e % ldl;
+        b.L[(k * R + i) * ldl + c] = c < R ? Th[i * R + c] * cs.E[c] : -(cs.H[i * R + (c - R)] * wk[c - R]);
       }
-      __syncwarp();
-      for (int64_t j = lane; j < a.J; j += 32) {
-        double dv[2 * RT];
+    }
+    __syncwarp();
+  }
+}
+
+// e partials: ||L N^T||_F^2 over row tiles of L (rows = K*R, cols = 2R) with
+// N = [D V] (J x 2R).  Warp tile: 8 rows of L x all J in 8-column DMMA tiles;
+// A fragments (L rows) stay in registers, N streams through shared memory.
+template <int KS>  // k-steps of 4 covering 2R (padded)
+__global__ void __launch_bounds__(256) als_metric_kernel(AlsBufs b, const double* D, const double* V, int64_t J,
+                                                         int R, int64_t rowsL) {
+  if (b.ctl[0]) return;
+  constexpr int JC = KS <= 12 ? 64 : 32;
+  __shared__ double ns[JC][4 * KS + 1];
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ldl = 2 * R;
+  const int64_t mtiles = (rowsL + 7) / 8;
+  double acc = 0.0;
+  for (int64_t mt0 = (int64_t)blockIdx.x * 8; mt0 < mtiles; mt0 += (int64_t)gridDim.x * 8) {
+    const int64_t mt = mt0 + warp;
+    double af[KS];
+    const int64_t row = mt * 8 + (lane >> 2);
 #pragma unroll
-        for (int c = 0; c < RT; ++c) {
-          dv[c] = c < R ? a.D[j * R + c] : 0.0;
-          dv[RT + c] = c < R ? a.V[j * R + c] : 0.0;
-        }
-        for (int i = 0; i < R; ++i) {
-          double s = 0.0;
+    for (int ks = 0; ks < KS; ++ks) {
+      const int c = ks * 4 + (lane & 3);
+      af[ks] = (mt < mtiles && row < rowsL && c < ldl) ? b.L[row * ldl + c] : 0.0;
+    }
+    for (int64_t j0 = 0; j0 < J; j0 += JC) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < JC * 4 * KS; e += blockDim.x) {
+        const int jj = e / (4 * KS), c = e % (4 * KS);
+        const int64_t j = j0 + jj;
+        double v = 0.0;
+        if (j < J && c < ldl) v = c < R ? D[j * R + c] : V[j * R + (c - R)];
+        ns[jj][c] = v;
+      }
+      __syncthreads();
+      if (mt < mtiles) {
+        const int nj = (int)imin64(JC, J - j0);
+        for (int nt = 0; nt * 8 < nj; ++nt) {
+          double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-          for (int c = 0; c < RT; ++c)
-            if (c < R) s = fma(L[i * 2 * R + c], dv[c], s);
-#pragma unroll
-          for (int c = 0; c < RT; ++c)
-            if (c < R) s = fma(L[i * 2 * R + R + c], dv[RT + c], s);
-          esum = fma(s, s, esum);
+          for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(c0, c1, af[ks], ns[nt * 8 + (lane >> 2)][ks * 4 + (lane & 3)]);
+          acc = fma(c0, c0, acc);
+          acc = fma(c1, c1, acc);
         }
       }
-      __syncwarp();
     }
   }
-  if (a.metric) {
-    esum = warp_sum(esum);
-    if (lane == 0) b.p_e[gw] = esum;
-  }
+  const double tot = block_sum(acc, red);
+  if (threadIdx.x == 0) b.s_e[blockIdx.x] = tot;
 }
 
 // ------------------------------------------------------------ solves (1 CTA)
 // pinv of a symmetric R x R matrix (P/linalg.py:135-151 on a Hadamard of
-// Grams): eigen-decomposition, |lambda| <= R * max|lambda| * 1e-12 dropped.
-DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int* flag, int64_t* status) {
-  const int sw = jacobi_eig_block(A, R, U, R, R, cs, flag);
-  if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+// Grams): eigen-decomposition by warp 0, |lambda| <= R max|lambda| 1e-12 dropped.
+DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status) {
   __shared__ double lmax;
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int i = 0; i < R; ++i) m = fmax(m, fabs(A[i * R + i]));
-    lmax = m;
+  if (threadIdx.x < 32) {
+    const int sw = jacobi_eig_warp(A, R, U, R, R, cs);
+    if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int i = 0; i < R; ++i) m = fmax(m, fabs(A[i * R + i]));
+      lmax = m;
+    }
   }
   __syncthreads();
   const double tolr = R * lmax * 1e-12;
@@ -433,21 +514,12 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
   __syncthreads();
 }
 
-DP2_DEV void reduce_slots(const double* slots, int nslots, int n, double* out) {
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nslots; ++w) s += slots[(size_t)w * n + e];
-    out[e] = s;
-  }
-}
-
 struct SolveArgs {
   const double *D, *E;
   double *H, *V, *W;
   int64_t J;
   int R, normalize, nslots;
   int64_t* status;
-  double* G2;  // J x R scratch
 };
 
 __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
@@ -461,9 +533,9 @@ __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
   double* Pv = U + R * R;
   double* Hn = Pv + R * R;
   double* cs = Hn + R * R;  // 3*(R/2+1)
-  __shared__ int flag;
-  reduce_slots(b.p_g1, s.nslots, R * R, G1);
-  reduce_slots(b.p_wtw, s.nslots, R * R, WtW);
+  __shared__ double nrm[64];
+  reduce_slots_warp(b.s_g1, s.nslots, R * R, G1);
+  reduce_slots_warp(b.s_wtw, s.nslots, R * R, WtW);
   __syncthreads();
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     Mh[e] = WtW[e] * b.VtV[e];
@@ -471,7 +543,7 @@ __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
     b.WtW[e] = WtW[e];
   }
   __syncthreads();
-  block_pinv_sym(Mh, U, Pv, R, cs, &flag, s.status);
+  block_pinv_sym(Mh, U, Pv, R, cs, s.status);
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, c = e % R;
     double acc = 0.0;
@@ -479,7 +551,6 @@ __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
     Hn[e] = acc;
   }
   __syncthreads();
-  __shared__ double nrm[64];
   for (int c = threadIdx.x; c < R; c += blockDim.x) {
     double n2 = 0.0;
     for (int i = 0; i < R; ++i) n2 = fma(Hn[i * R + c], Hn[i * R + c], n2);
@@ -511,12 +582,11 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   double* Mv = WtW2 + R * R;
   double* U = Mv + R * R;
   double* Pv = U + R * R;
-  double* es = Pv + R * R;  // R*R: E * summed
+  double* es = Pv + R * R;  // E * summed
   double* cs = es + R * R;
-  __shared__ int flag;
   __shared__ double nrm[64];
-  reduce_slots(b.p_m2, s.nslots, R * R, summed);
-  reduce_slots(b.p_wtw2, s.nslots, R * R, WtW2);
+  reduce_slots_warp(b.s_m2, s.nslots, R * R, summed);
+  reduce_slots_warp(b.s_wtw2, s.nslots, R * R, WtW2);
   __syncthreads();
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     Mv[e] = WtW2[e] * b.HtH[e];
@@ -525,21 +595,22 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
     b.WtW2[e] = WtW2[e];
   }
   __syncthreads();
-  block_pinv_sym(Mv, U, Pv, R, cs, &flag, s.status);
-  // G2 = D (E * summed);  V = G2 pinv
+  block_pinv_sym(Mv, U, Pv, R, cs, s.status);
+  // G2 = D (E * summed) (P/solver.py:100) into b.G2
   for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
     const int64_t j = e / R;
     const int r = (int)(e % R);
-    double acc = 0.0;
-    for (int a = 0; a < R; ++a) acc = fma(s.D[j * R + a], es[a * R + r], acc);
-    s.G2[e] = acc;
+    double t = 0.0;
+    for (int q = 0; q < R; ++q) t = fma(s.D[j * R + q], es[q * R + r], t);
+    b.G2[e] = t;
   }
   __syncthreads();
+  // V = G2 pinv
   for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
     const int64_t j = e / R;
     const int r = (int)(e % R);
     double acc = 0.0;
-    for (int a = 0; a < R; ++a) acc = fma(s.G2[j * R + a], Pv[a * R + r], acc);
+    for (int a = 0; a < R; ++a) acc = fma(b.G2[j * R + a], Pv[a * R + r], acc);
     s.V[e] = acc;
   }
   __syncthreads();
@@ -557,14 +628,15 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   __syncthreads();
   gram_dv_warps(s.D, s.E, s.V, J, R, b.cc, b.VtV, Mv, b.HtH);
   __syncthreads();
-  block_pinv_sym(Mv, U, b.pinv3, R, cs, &flag, s.status);
+  block_pinv_sym(Mv, U, b.pinv3, R, cs, s.status);
 }
 
 // ------------------------------------------------------------ host side
 namespace {
 
 struct AlsLayout {
-  size_t theta, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, p_g1, p_wtw, p_m2, p_wtw2, p_e, G2, g3, ctl, total;
+  size_t theta, pprev, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, L, s_g1, s_wtw, s_m2, s_wtw2, s_e, G2, g3,
+      ctl, total;
 };
 
 int sm_count() {
@@ -586,12 +658,20 @@ int total_warps(int64_t K, int R) {
   return (int)(w < wpb ? wpb : w);
 }
 
+int metric_blocks(int64_t K, int R) {
+  const int64_t mtiles = (K * R + 7) / 8;
+  const int64_t b = (mtiles + 7) / 8;
+  const int64_t cap = (int64_t)sm_count() * 4;
+  return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
+}
+
 AlsLayout als_layout(int64_t K, int64_t J, int R) {
   AlsLayout L{};
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-  const size_t RR = (size_t)R * R * 8, nw = total_warps(K, R);
+  const size_t RR = (size_t)R * R * 8, nb = total_warps(K, R) / wpb_for(R), nbm = metric_blocks(K, R);
   L.theta = take(K * RR);
+  L.pprev = take(K * RR);
   L.cc = take(RR);
   L.nh = take(R * 8);
   L.HtH = take(RR);
@@ -601,11 +681,12 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.WtW = take(RR);
   L.summed = take(RR);
   L.WtW2 = take(RR);
-  L.p_g1 = take(nw * RR);
-  L.p_wtw = take(nw * RR);
-  L.p_m2 = take(nw * RR);
-  L.p_wtw2 = take(nw * RR);
-  L.p_e = take(nw * 8);
+  L.L = take(K * RR * 2);
+  L.s_g1 = take(nb * RR);
+  L.s_wtw = take(nb * RR);
+  L.s_m2 = take(nb * RR);
+  L.s_wtw2 = take(nb * RR);
+  L.s_e = take(nbm * 8);
   L.G2 = take(J * R * 8);
   L.g3 = take(K * R * 8);
   L.ctl = take(64);
@@ -613,11 +694,12 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   return L;
 }
 
-AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R, size_t* g2_off) {
+AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   const AlsLayout L = als_layout(K, J, R);
   AlsBufs b{};
   auto d = [&](size_t o) { return reinterpret_cast<double*>(ws + o); };
   b.theta = d(L.theta);
+  b.pprev = d(L.pprev);
   b.cc = d(L.cc);
   b.nh = d(L.nh);
   b.HtH = d(L.HtH);
@@ -627,24 +709,25 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R, size_t* g2_off) {
   b.WtW = d(L.WtW);
   b.summed = d(L.summed);
   b.WtW2 = d(L.WtW2);
-  b.p_g1 = d(L.p_g1);
-  b.p_wtw = d(L.p_wtw);
-  b.p_m2 = d(L.p_m2);
-  b.p_wtw2 = d(L.p_wtw2);
-  b.p_e = d(L.p_e);
-  b.scratch = d(L.G2);
+  b.L = d(L.L);
+  b.s_g1 = d(L.s_g1);
+  b.s_wtw = d(L.s_wtw);
+  b.s_m2 = d(L.s_m2);
+  b.s_wtw2 = d(L.s_wtw2);
+  b.s_e = d(L.s_e);
+  b.G2 = d(L.G2);
   b.g3 = d(L.g3);
   b.ctl = reinterpret_cast<int32_t*>(ws + L.ctl);
   b.nwt = total_warps(K, R);
   b.wpb = wpb_for(R);
-  if (g2_off) *g2_off = L.G2;
+  b.nb = b.nwt / b.wpb;
+  b.nbm = metric_blocks(K, R);
   return b;
 }
 
-size_t slice_smem(int R, int wpb, bool mode3) {
-  const size_t per = mode3 ? (2 * (size_t)R * R + 2 * R) : warp_smem_doubles(R);
-  return (cta_shared_doubles(R) + wpb * per) * 8;
-}
+size_t rotate_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * warp_smem_doubles(R)) * 8; }
+size_t acc2_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 2 * (size_t)R * R) * 8; }
+size_t mode3_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 2 * (size_t)R) * 8; }
 size_t solve_smem(int R) { return (7 * (size_t)R * R + 3 * (R / 2 + 1) + 8) * 8; }
 
 cudaError_t set_smem(const void* f, size_t bytes) {
@@ -652,49 +735,89 @@ cudaError_t set_smem(const void* f, size_t bytes) {
   return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <int RT>
-cudaError_t launch_mode3_t(const SliceArgs& a, const AlsBufs& b, cudaStream_t st) {
-  const size_t sm = slice_smem(a.R, b.wpb, true);
-  als_mode3_kernel<RT><<<b.nwt / b.wpb, 32 * b.wpb, sm, st>>>(a, b);
-  return cudaGetLastError();
-}
-cudaError_t launch_mode3(const SliceArgs& a, const AlsBufs& b, cudaStream_t st) {
-  if (a.R <= 16) return launch_mode3_t<16>(a, b, st);
-  if (a.R <= 32) return launch_mode3_t<32>(a, b, st);
-  return launch_mode3_t<64>(a, b, st);
+template <int KS>
+void metric_t(const AlsBufs& b, const double* D, const double* V, int64_t J, int R, int64_t K, cudaStream_t st) {
+  als_metric_kernel<KS><<<b.nbm, 256, 0, st>>>(b, D, V, J, R, K * R);
 }
 
-cudaError_t launch_iteration(const SliceArgs& base, SolveArgs sv, const AlsBufs& b, int it, double tol,
+cudaError_t launch_metric(const AlsBufs& b, const double* D, const double* V, int64_t J, int R, int64_t K,
+                          cudaStream_t st) {
+  const int ks = (2 * R + 3) / 4;
+  if (ks <= 1) metric_t<1>(b, D, V, J, R, K, st);
+  else if (ks <= 2) metric_t<2>(b, D, V, J, R, K, st);
+  else if (ks <= 3) metric_t<3>(b, D, V, J, R, K, st);
+  else if (ks <= 4) metric_t<4>(b, D, V, J, R, K, st);
+  else if (ks <= 5) metric_t<5>(b, D, V, J, R, K, st);
+  else if (ks <= 6) metric_t<6>(b, D, V, J, R, K, st);
+  else if (ks <= 8) metric_t<8>(b, D, V, J, R, K, st);
+  else if (ks <= 10) metric_t<10>(b, D, V, J, R, K, st);
+  else if (ks <= 12) metric_t<12>(b, D, V, J, R, K, st);
+  else if (ks <= 16) metric_t<16>(b, D, V, J, R, K, st);
+  else if (ks <= 24) metric_t<24>(b, D, V, J, R, K, st);
+  else metric_t<32>(b, D, V, J, R, K, st);
+  return cudaGetLastError();
+}
+
+cudaError_t prepare(int R, const AlsBufs& b) {
+  cudaError_t e = set_smem((const void*)als_rotate_kernel, rotate_smem(R, b.wpb));
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode2_kernel, acc2_smem(R, b.wpb));
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, acc2_smem(R, b.wpb));
+  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
+  if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
+  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, solve_smem(R));
+  return e;
+}
+
+cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const AlsBufs& b, int it, double tol,
                              double* trace, int64_t* tstamp, int32_t* iters, cudaStream_t st) {
-  const int R = base.R, nb = b.nwt / b.wpb, nt = 32 * b.wpb;
-  const size_t rs = slice_smem(R, b.wpb, false);
+  const int R = base.R, nt = 32 * b.wpb;
   SliceArgs a = base;
   a.mode1 = 1;
-  als_rotate_kernel<<<nb, nt, rs, st>>>(a, b);
+  a.warm = 1;
+  als_rotate_kernel<<<b.nb, nt, rotate_smem(R, b.wpb), st>>>(a, b);
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
-  als_mode2_kernel<<<nb, nt, rs, st>>>(a, b);
+  als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
-  a.metric = 1;
   a.write_w = 1;
+  a.write_l = 1;
   a.Wout = sv.W;
-  cudaError_t e = launch_mode3(a, b, st);
+  als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
+  cudaError_t e = launch_metric(b, a.D, sv.V, a.J, R, a.K, st);
   if (e != cudaSuccess) return e;
   als_finish_kernel<<<1, 32, 0, st>>>(b, it, tol, trace, tstamp, iters);
   return cudaGetLastError();
 }
 
-cudaError_t prepare(const SliceArgs& a, const AlsBufs& b, int R) {
-  cudaError_t e = set_smem((const void*)als_rotate_kernel, slice_smem(R, b.wpb, false));
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode2_kernel, slice_smem(R, b.wpb, false));
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, slice_smem(R, b.wpb, false));
-  if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
-  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, solve_smem(R));
-  const size_t m3 = slice_smem(R, b.wpb, true);
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<16>, m3);
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<32>, m3);
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel<64>, m3);
-  (void)a;
-  return e;
+SliceArgs slice_args(const double* F, const double* D, const double* E, const double* H, const double* V,
+                     const double* W, int64_t K, int64_t J, int R, int64_t* status) {
+  SliceArgs a{};
+  a.F = F;
+  a.D = D;
+  a.E = E;
+  a.H = H;
+  a.V = V;
+  a.W = W;
+  a.K = K;
+  a.J = J;
+  a.R = R;
+  a.status = status;
+  return a;
+}
+
+SolveArgs solve_args(const double* D, const double* E, double* H, double* V, double* W, int64_t J, int R,
+                     int normalize, const AlsBufs& b, int64_t* status) {
+  SolveArgs sv{};
+  sv.D = D;
+  sv.E = E;
+  sv.H = H;
+  sv.V = V;
+  sv.W = W;
+  sv.J = J;
+  sv.R = R;
+  sv.normalize = normalize;
+  sv.nslots = b.nb;
+  sv.status = status;
+  return sv;
 }
 
 }  // namespace
@@ -705,34 +828,12 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
                     int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
                     char* ws, int64_t* status, cudaStream_t st) {
-  size_t g2off = 0;
-  AlsBufs b = make_bufs(ws, K, J, R, &g2off);
-  SliceArgs a{};
-  a.F = F;
-  a.D = D;
-  a.E = E;
-  a.H = H;
-  a.V = V;
-  a.W = W;
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(F, D, E, H, V, W, K, J, R, status);
   a.polar = polar;
   a.theta = b.theta;
-  a.K = K;
-  a.J = J;
-  a.R = R;
-  a.status = status;
-  SolveArgs sv{};
-  sv.D = D;
-  sv.E = E;
-  sv.H = H;
-  sv.V = V;
-  sv.W = W;
-  sv.J = J;
-  sv.R = R;
-  sv.normalize = normalize;
-  sv.nslots = b.nwt;
-  sv.status = status;
-  sv.G2 = b.scratch;
-  cudaError_t e = prepare(a, b, R);
+  SolveArgs sv = solve_args(D, E, H, V, W, J, R, normalize, b, status);
+  cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, tstamp, 1);
   if (!use_graph) {
@@ -770,42 +871,38 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
 cudaError_t als_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                           const double* H, const double* V, const double* W, double* polar,
                           double* theta, char* ws, int64_t* status, cudaStream_t st) {
-  AlsBufs b = make_bufs(ws, K, J, R, nullptr);
-  SliceArgs a{};
-  a.F = F; a.D = D; a.E = E; a.H = H; a.V = V; a.W = W;
-  a.polar = polar; a.theta = const_cast<double*>(theta); a.K = K; a.J = J; a.R = R; a.status = status;
-  cudaError_t e = prepare(a, b, R);
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(F, D, E, H, V, W, K, J, R, status);
+  a.polar = polar;
+  a.theta = theta;
+  cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
-  als_rotate_kernel<<<b.nwt / b.wpb, 32 * b.wpb, slice_smem(R, b.wpb, false), st>>>(a, b);
+  als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(R, b.wpb), st>>>(a, b);
   return cudaGetLastError();
 }
 
 cudaError_t als_mttkrp(int mode, const double* theta, const double* D, const double* E, int64_t K,
                        int64_t J, int R, const double* H, const double* V, const double* W, double* out,
                        char* ws, cudaStream_t st) {
-  AlsBufs b = make_bufs(ws, K, J, R, nullptr);
-  SliceArgs a{};
-  a.D = D; a.E = E; a.H = H; a.V = V; a.W = W; a.theta = const_cast<double*>(theta); a.K = K; a.J = J; a.R = R;
-  cudaError_t e = prepare(a, b, R);
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(nullptr, D, E, H, V, W, K, J, R, nullptr);
+  a.theta = const_cast<double*>(theta);
+  cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
-  const int nb = b.nwt / b.wpb, nt = 32 * b.wpb;
-  const size_t rs = slice_smem(R, b.wpb, false);
+  const int nt = 32 * b.wpb;
   if (mode == 1) {
-    als_mode1_kernel<<<nb, nt, rs, st>>>(a, b);
-    reduce_parts_dev<<<1, 256, 0, st>>>(b.p_g1, b.nwt, (int64_t)R * R, out);
+    als_mode1_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
+    reduce_parts_dev<<<1, 256, 0, st>>>(b.s_g1, b.nb, (int64_t)R * R, out);
   } else if (mode == 2) {
-    als_mode2_kernel<<<nb, nt, rs, st>>>(a, b);  // nh == 1 after prep
-    reduce_parts_dev<<<1, 256, 0, st>>>(b.p_m2, b.nwt, (int64_t)R * R, b.summed);
-    // out = D (E * summed)
+    als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);  // nh == 1 after prep
+    reduce_parts_dev<<<1, 256, 0, st>>>(b.s_m2, b.nb, (int64_t)R * R, b.summed);
     g2_kernel<<<(unsigned)((J * R + 255) / 256), 256, 0, st>>>(D, E, b.summed, J, R, out);
   } else {
     a.write_w = 0;
-    a.metric = 0;
     a.Wout = out;
-    e = launch_mode3(a, b, st);
-    if (e != cudaSuccess) return e;
+    als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
   }
   return cudaGetLastError();
 }
@@ -813,42 +910,40 @@ cudaError_t als_mttkrp(int mode, const double* theta, const double* D, const dou
 cudaError_t als_update_factors(const double* theta, const double* D, const double* E, int64_t K,
                                int64_t J, int R, double* H, double* V, double* W, int normalize,
                                char* ws, int64_t* status, cudaStream_t st) {
-  AlsBufs b = make_bufs(ws, K, J, R, nullptr);
-  SliceArgs a{};
-  a.D = D; a.E = E; a.H = H; a.V = V; a.W = W; a.theta = const_cast<double*>(theta); a.K = K; a.J = J; a.R = R; a.status = status;
-  SolveArgs sv{};
-  sv.D = D; sv.E = E; sv.H = H; sv.V = V; sv.W = W; sv.J = J; sv.R = R; sv.normalize = normalize;
-  sv.nslots = b.nwt; sv.status = status; sv.G2 = b.scratch;
-  cudaError_t e = prepare(a, b, R);
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(nullptr, D, E, H, V, W, K, J, R, status);
+  a.theta = const_cast<double*>(theta);
+  SolveArgs sv = solve_args(D, E, H, V, W, J, R, normalize, b, status);
+  cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
-  const int nb = b.nwt / b.wpb, nt = 32 * b.wpb;
-  const size_t rs = slice_smem(R, b.wpb, false);
+  const int nt = 32 * b.wpb;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
-  als_mode1_kernel<<<nb, nt, rs, st>>>(a, b);
+  als_mode1_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
-  als_mode2_kernel<<<nb, nt, rs, st>>>(a, b);
+  als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
   a.write_w = 1;
-  a.metric = 0;
   a.Wout = W;
-  return launch_mode3(a, b, st);
+  als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
+  return cudaGetLastError();
 }
 
 cudaError_t als_metric(const double* theta, const double* D, const double* E, int64_t K, int64_t J,
                        int R, const double* H, const double* V, const double* W, double* out, char* ws,
                        cudaStream_t st) {
-  AlsBufs b = make_bufs(ws, K, J, R, nullptr);
-  SliceArgs a{};
-  a.D = D; a.E = E; a.H = H; a.V = V; a.W = W; a.theta = const_cast<double*>(theta); a.K = K; a.J = J; a.R = R;
-  a.metric = 1;
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(nullptr, D, E, H, V, W, K, J, R, nullptr);
+  a.theta = const_cast<double*>(theta);
   a.write_w = 0;
-  a.Wout = b.g3;
-  cudaError_t e = prepare(a, b, R);
+  a.write_l = 1;
+  a.Wout = nullptr;
+  cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
-  e = launch_mode3(a, b, st);
+  als_mode3_kernel<<<b.nb, 32 * b.wpb, mode3_smem(R, b.wpb), st>>>(a, b);
+  e = launch_metric(b, D, V, J, R, K, st);
   if (e != cudaSuccess) return e;
-  reduce_parts_dev<<<1, 32, 0, st>>>(b.p_e, b.nwt, 1, out);
+  reduce_parts_dev<<<1, 32, 0, st>>>(b.s_e, b.nbm, 1, out);
   return cudaGetLastError();
 }
 

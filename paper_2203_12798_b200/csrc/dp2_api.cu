@@ -131,6 +131,19 @@ int dp2_plan_pieces(const int64_t* row_off, int64_t K, int32_t nseg, int32_t* pi
   return DP2_OK;
 }
 
+// ---------------------------------------------------------------- sketch matrices
+uint64_t dp2_derived_seed(uint64_t seed, uint64_t index) { return dp2::derived_seed_host(seed, index); }
+
+int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev, int32_t sp,
+                       const int64_t* slice_ids_dev, double* out, dp2_tail_record* recs, int32_t cap,
+                       int32_t* nrec_dev, int32_t* redo_dev, void* stream) {
+  static_assert(sizeof(dp2_tail_record) == 88, "record layout");
+  if (K < 1 || J < 1 || sp < 1 || cap < 0) return fail_arg("invalid omega shape");
+  if (dp2::tail_record_bytes() != sizeof(dp2_tail_record)) return fail_arg("record layout mismatch");
+  cudaError_t e = dp2::run_omega(seed, K, J, s_dev, sp, slice_ids_dev, out, recs, cap, nrec_dev, redo_dev, S(stream));
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_omega_generate");
+}
+
 // ---------------------------------------------------------------- device calls
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream) {
   if (!store_ok(st)) return fail_arg("invalid store");
@@ -179,7 +192,7 @@ int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, in
   if (ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("workspace too small");
   cudaError_t e = dp2::als_run(F, D, E, K, J, R, H, V, W, polar_out, max_iters, tol, normalize, trace_out,
                                tstamp_out, iters_out, use_graph, static_cast<char*>(ws), status_dev, S(stream));
-  return e == cudaSuccess ? ok(1 + 6 * (int64_t)max_iters) : fail(e, "dp2_als_run");
+  return e == cudaSuccess ? ok(1 + 7 * (int64_t)max_iters) : fail(e, "dp2_als_run");
 }
 
 int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
@@ -214,7 +227,7 @@ int dp2_convergence_metric(const double* theta, const double* D, const double* E
                            size_t ws_bytes, void* stream) {
   if (R < 1 || R > 64 || ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("invalid arguments");
   cudaError_t e = dp2::als_metric(theta, D, E, K, J, R, H, V, W, out, static_cast<char*>(ws), S(stream));
-  return e == cudaSuccess ? ok(3) : fail(e, "dp2_convergence_metric");
+  return e == cudaSuccess ? ok(4) : fail(e, "dp2_convergence_metric");
 }
 
 int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar, double* Q_out,

@@ -172,6 +172,78 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
   return sweep + 1;
 }
 
+// Single-warp version of jacobi_eig_block (same ordering, rotations and
+// thresholds; __syncwarp instead of __syncthreads).  For the R x R pinvs and
+// other n <= 64 problems where a whole block would mostly idle.
+DP2_DEV int jacobi_eig_warp(double* A, int lda, double* V, int ldv, int n, double* cs, int max_sweeps = 40) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n * n; i += 32) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
+  __syncwarp();
+  if (n < 2) return 0;
+  const int ne = n + (n & 1), np = ne / 2;
+  const double tol = n * kEps;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < ne - 1; ++r) {
+      for (int i = lane; i < np; i += 32) {
+        int p, q;
+        rr_pair(ne, r, i, p, q);
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = A[p * lda + q], app = A[p * lda + p], aqq = A[q * lda + q];
+          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
+            const double th = (aqq - app) / (2.0 * apq);
+            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            rotated = 1;
+          }
+        }
+        cs[3 * i] = c;
+        cs[3 * i + 1] = s;
+        cs[3 * i + 2] = (double)(p * 1024 + q);
+      }
+      __syncwarp();
+      for (int it = lane; it < n * np; it += 32) {
+        const int i = it / np, pr = it % np;
+        const double s = cs[3 * pr + 1];
+        if (s == 0.0) continue;
+        const double c = cs[3 * pr];
+        const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
+        double a = A[i * lda + p], b = A[i * lda + q];
+        A[i * lda + p] = c * a - s * b;
+        A[i * lda + q] = s * a + c * b;
+        a = V[i * ldv + p];
+        b = V[i * ldv + q];
+        V[i * ldv + p] = c * a - s * b;
+        V[i * ldv + q] = s * a + c * b;
+      }
+      __syncwarp();
+      for (int it = lane; it < n * np; it += 32) {
+        const int pr = it / n, j = it % n;
+        const double s = cs[3 * pr + 1];
+        if (s == 0.0) continue;
+        const double c = cs[3 * pr];
+        const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
+        const double a = A[p * lda + j], b = A[q * lda + j];
+        A[p * lda + j] = c * a - s * b;
+        A[q * lda + j] = s * a + c * b;
+      }
+      __syncwarp();
+      for (int i = lane; i < np; i += 32) {
+        if (cs[3 * i + 1] == 0.0) continue;
+        const int pq = (int)cs[3 * i + 2], p = pq >> 10, q = pq & 1023;
+        A[p * lda + q] = 0.0;
+        A[q * lda + p] = 0.0;
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  return sweep + 1;
+}
+
 // Sort eigenpairs by descending eigenvalue (stable on index): writes the
 // permutation into ``perm`` (n ints, shared).  Single-threaded; n is tiny.
 DP2_DEV void sort_desc_perm(const double* A, int lda, int n, int* perm) {

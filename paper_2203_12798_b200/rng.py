@@ -1,10 +1,15 @@
 """Sketch-matrix (Omega) generation.
 
 Omega_k must be bit-identical to the reference's draw (P/linalg.py:122-123):
-``Generator(PCG64(derived_seed(seed, k))).standard_normal((J, s_k))``.  This
-module produces them on the host with NumPy's own generator (the algorithm the
-reference specifies), packed as (K, J, sp) float64 with zero padding, in
-parallel over slices, and copies them to the device through pinned memory.
+``Generator(PCG64(derived_seed(seed, k))).standard_normal((J, s_k))``.
+
+``omega_device`` (the product path) runs the native generator
+(csrc/dp2_rng.cu: SeedSequence -> PCG64 -> 256-layer ziggurat, one thread per
+slice) and then replays the rare layer-0 tail draws on the host with NumPy's
+log1p -- the only step whose last bit depends on the libm -- patching those
+entries, so the result is byte-identical to NumPy.  ``omega_host`` draws the
+same matrices with NumPy itself (used for stage 2's single stream, overlapped
+with stage 1, and as the test reference).
 """
 from __future__ import annotations
 
@@ -48,9 +53,65 @@ def omega_host(seed, n, widths, sp, threads=None, slice_ids=None):
     return host
 
 
-def omega_device(seed, n, widths, sp, device, stream=None, slice_ids=None):
-    host = omega_host(seed, n, widths, sp, slice_ids=slice_ids)
-    return host.to(device, non_blocking=True), host
+_REC = np.dtype([("slice", "<i8"), ("index", "<i8"), ("attempts", "<i4"), ("negative", "<i4"),
+                 ("u", "<f8", (8,))])
+_ZIG_R = 3.6541528853610087963519472518
+_ZIG_INV_R = 0.27366123732975827203338247596
+
+
+def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
+    """Device tensor (K, n, sp) of the reference's Omega_k (byte-exact)."""
+    import ctypes as C
+
+    from . import _lib
+    K = len(widths)
+    out = torch.empty((K, n, sp), dtype=torch.float64, device=device)
+    s_dev = torch.tensor(list(widths), dtype=torch.int32).to(device)
+    ids = None if slice_ids is None else torch.tensor(list(slice_ids), dtype=torch.int64).to(device)
+    cap = max(4096, 8 * K + n * max(widths) * K // 1000)
+    recs = torch.empty((cap, _REC.itemsize), dtype=torch.uint8, device=device)
+    nrec = torch.zeros(1, dtype=torch.int32, device=device)
+    redo = torch.zeros(K, dtype=torch.int32, device=device)
+    vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
+    _lib.check(_lib.lib().dp2_omega_generate(C.c_uint64(seed & _MASK64), K, n, vp(s_dev), sp, vp(ids), vp(out),
+                                             vp(recs), cap, vp(nrec), vp(redo),
+                                             C.c_void_p(torch.cuda.current_stream().cuda_stream)), "omega")
+    count = int(nrec.item())
+    redo_h = redo.cpu().numpy()
+    if count > cap:
+        redo_h[:] = 1  # record overflow: regenerate everything on the host (never expected)
+    patched = 0
+    if count:
+        r = recs[:min(count, cap)].cpu().numpy().view(_REC).reshape(-1)
+        vals = np.empty(r.size)
+        ok = np.ones(r.size, dtype=bool)
+        done = np.zeros(r.size, dtype=bool)
+        for a in range(4):  # replay each attempt with NumPy's log1p (P/linalg.py:123's sampler)
+            xx = -_ZIG_INV_R * np.log1p(-r["u"][:, 2 * a])
+            yy = -np.log1p(-r["u"][:, 2 * a + 1])
+            acc = (yy + yy) > (xx * xx)
+            last = r["attempts"] == a + 1
+            live = ~done & (r["attempts"] >= a + 1)
+            ok &= ~(live & (acc != last))
+            hit = live & last
+            vals[hit] = np.where(r["negative"][hit] != 0, -(_ZIG_R + xx[hit]), _ZIG_R + xx[hit])
+            done |= hit
+        redo_h[r["slice"][~ok]] = 1
+        good = ok & (redo_h[r["slice"]] == 0)
+        if good.any():
+            w = np.asarray(widths)[r["slice"][good]]
+            flat = r["slice"][good] * (n * sp) + (r["index"][good] // w) * sp + r["index"][good] % w
+            idx = torch.from_numpy(flat).to(device)
+            out.view(-1).index_copy_(0, idx, torch.from_numpy(vals[good]).to(device))
+            patched = int(good.sum())
+    bad = np.nonzero(redo_h)[0]
+    if bad.size:
+        ids_h = list(range(K)) if slice_ids is None else list(slice_ids)
+        host = omega_host(seed, n, [widths[k] for k in bad], sp, slice_ids=[ids_h[k] for k in bad])
+        out[torch.from_numpy(bad).to(device)] = host.to(device)
+    if stats is not None:
+        stats.update(omega_tail_events=count, omega_patched=patched, omega_host_regenerated=int(bad.size))
+    return out
 
 
 def stage2_omega(seed, rows, width):
