@@ -486,10 +486,69 @@ __global__ void __launch_bounds__(256) als_metric_kernel(AlsBufs b, const double
 }
 
 // ------------------------------------------------------------ solves (1 CTA)
-// pinv of a symmetric R x R matrix (P/linalg.py:135-151 on a Hadamard of
-// Grams): eigen-decomposition by warp 0, |lambda| <= R max|lambda| 1e-12 dropped.
+// pinv of the symmetric PSD R x R Hadamard-of-Grams matrix (P/linalg.py:135-151).
+// Fast path (warp 0): Cholesky A = L L^T and the explicit inverse; it is
+// accepted when every pivot is positive and the Frobenius condition estimate
+// ||A||_F ||A^-1||_F < 1e10, i.e. far from the reference's drop threshold
+// (sigma <= R sigma_max 1e-12), where pinv(A) == inv(A) up to rounding.
+// Otherwise: Jacobi eigen-decomposition with the reference's threshold.
+DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out) {
+  const int lane = threadIdx.x & 31;
+  // factor: column k pivot by lane 0, then lanes fill column k below the diagonal
+  bool okay = true;
+  for (int k = 0; k < R; ++k) {
+    double d = 0.0;
+    if (lane == 0) {
+      double t = A[k * R + k];
+      for (int m = 0; m < k; ++m) t = fma(-Lw[k * R + m], Lw[k * R + m], t);
+      d = t;
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (!(d > 0.0)) { okay = false; break; }
+    const double l = sqrt(d);
+    for (int i = k + 1 + lane; i < R; i += 32) {
+      double t = A[i * R + k];
+      for (int m = 0; m < k; ++m) t = fma(-Lw[i * R + m], Lw[k * R + m], t);
+      Lw[i * R + k] = t / l;
+    }
+    if (lane == 0) Lw[k * R + k] = l;
+    __syncwarp();
+  }
+  if (!okay) return false;
+  // inverse: lane j solves L y = e_j then L^T x = y (column j of A^-1)
+  double an = 0.0, in = 0.0;
+  for (int j = lane; j < R; j += 32) {
+    double y[64];
+    for (int i = 0; i < R; ++i) {
+      double t = (i == j) ? 1.0 : 0.0;
+      for (int m = 0; m < i; ++m) t = fma(-Lw[i * R + m], y[m], t);
+      y[i] = t / Lw[i * R + i];
+    }
+    for (int i = R - 1; i >= 0; --i) {
+      double t = y[i];
+      for (int m = i + 1; m < R; ++m) t = fma(-Lw[m * R + i], out[m * R + j], t);
+      out[i * R + j] = t / Lw[i * R + i];
+    }
+    for (int i = 0; i < R; ++i) {
+      an = fma(A[i * R + j], A[i * R + j], an);
+      in = fma(out[i * R + j], out[i * R + j], in);
+    }
+  }
+  an = warp_sum(an);
+  in = warp_sum(in);
+  __syncwarp();
+  return sqrt(an) * sqrt(in) < 1e10;
+}
+
 DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status) {
   __shared__ double lmax;
+  __shared__ int fast;
+  if (threadIdx.x < 32) {
+    const bool okay = warp_chol_inverse(A, R, U, out);
+    if (threadIdx.x == 0) fast = okay ? 1 : 0;
+  }
+  __syncthreads();
+  if (fast) return;
   if (threadIdx.x < 32) {
     const int sw = jacobi_eig_warp(A, R, U, R, R, cs);
     if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);

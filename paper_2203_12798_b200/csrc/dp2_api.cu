@@ -148,7 +148,7 @@ int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream) {
   if (!store_ok(st)) return fail_arg("invalid store");
   cudaError_t e = dp2::run_slice_stats(st, sqnorm_dev, status_dev, S(stream));
-  return e == cudaSuccess ? ok(1) : fail(e, "dp2_slice_stats");
+  return e == cudaSuccess ? ok(3) : fail(e, "dp2_slice_stats");
 }
 
 size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
@@ -178,7 +178,7 @@ int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_
   if (ws_bytes < dp2::stage2_bytes(J, KR, s2, rank)) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
                                   static_cast<char*>(ws), status_dev, S(stream));
-  return e == cudaSuccess ? ok(12) : fail(e, "dp2_stage2");
+  return e == cudaSuccess ? ok(11) : fail(e, "dp2_stage2");
 }
 
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }

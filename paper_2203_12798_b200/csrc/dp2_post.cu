@@ -8,24 +8,55 @@
 
 namespace dp2 {
 
+// per (slice, row-chunk) CTA: flat sum over the chunk's rows (cols < J); the
+// chunk partials are summed per slice in chunk order (deterministic)
 template <typename T>
 __global__ void __launch_bounds__(256) slice_stats_kernel(const T* X, int64_t ldx, int64_t J,
-                                                          const int64_t* row_off, double* sqnorm,
+                                                          const int64_t* row_off, int64_t K, int chunk_rows,
+                                                          const int64_t* chunk_begin, double* part,
                                                           int64_t* status) {
   __shared__ double red[32];
-  const int64_t k = blockIdx.x;
-  const int64_t r0 = row_off[k], r1 = row_off[k + 1];
+  const int64_t c = blockIdx.x;
+  // find the slice of chunk c (chunk_begin[k] = first chunk of slice k)
+  int64_t lo = 0, hi = K;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (chunk_begin[mid] <= c) lo = mid; else hi = mid;
+  }
+  const int64_t k = lo;
+  const int64_t r0 = row_off[k] + (c - chunk_begin[k]) * chunk_rows;
+  const int64_t r1 = imin64(row_off[k + 1], r0 + chunk_rows);
   double s = 0.0;
   int bad = 0;
-  const int64_t n = (r1 - r0) * J;
-  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-    const double v = (double)X[(r0 + e / J) * ldx + e % J];
-    s = fma(v, v, s);
-    bad |= !isfinite(v);
+  for (int64_t r = r0; r < r1; ++r) {
+    const T* row = X + r * ldx;
+    for (int64_t j = threadIdx.x; j < J; j += blockDim.x) {
+      const double v = (double)row[j];
+      s = fma(v, v, s);
+      bad |= !isfinite(v);
+    }
   }
   s = block_sum(s, red);
-  if (threadIdx.x == 0) sqnorm[k] = s;
+  if (threadIdx.x == 0) part[c] = s;
   if (__syncthreads_or(bad) && threadIdx.x == 0) status_min(status, ST_NONFINITE, k);
+}
+
+__global__ void slice_stats_reduce(const int64_t* chunk_begin, int64_t K, const double* part, double* sqnorm) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double s = 0.0;
+  for (int64_t c = chunk_begin[k]; c < chunk_begin[k + 1]; ++c) s += part[c];
+  sqnorm[k] = s;
+}
+
+__global__ void chunk_begin_kernel(const int64_t* row_off, int64_t K, int chunk_rows, int64_t* chunk_begin) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int64_t c = 0;
+  for (int64_t k = 0; k < K; ++k) {
+    chunk_begin[k] = c;
+    c += (row_off[k + 1] - row_off[k] + chunk_rows - 1) / chunk_rows;
+  }
+  chunk_begin[K] = c;
 }
 
 __global__ void __launch_bounds__(256) assemble_q_kernel(const double* A, const int32_t* piece_slice,
@@ -106,12 +137,29 @@ __global__ void fitness_reduce_kernel(const double* part, int64_t np, double* ou
 }
 
 cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status, cudaStream_t stream) {
+  // chunks of >= 64 rows; total chunks <= total_rows / 64 + K
+  const int chunk_rows = 64;
+  const int64_t K = st->K;
+  const int64_t maxc = st->total_rows / chunk_rows + K + 1;
+  int64_t* chunk_begin = nullptr;
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&chunk_begin, (K + 1) * sizeof(int64_t), stream);
+  if (e == cudaSuccess) e = cudaMallocAsync(&part, maxc * sizeof(double), stream);
+  if (e != cudaSuccess) return e;
+  chunk_begin_kernel<<<1, 1, 0, stream>>>(st->row_off, K, chunk_rows, chunk_begin);
+  int64_t nchunks = 0;
+  e = cudaMemcpyAsync(&nchunks, chunk_begin + K, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return e;
   if (st->dtype == DP2_F64)
-    slice_stats_kernel<double><<<(unsigned)st->K, 256, 0, stream>>>(
-        static_cast<const double*>(st->X), st->ldx, st->J, st->row_off, sqnorm, status);
+    slice_stats_kernel<double><<<(unsigned)nchunks, 256, 0, stream>>>(
+        static_cast<const double*>(st->X), st->ldx, st->J, st->row_off, K, chunk_rows, chunk_begin, part, status);
   else
-    slice_stats_kernel<float><<<(unsigned)st->K, 256, 0, stream>>>(
-        static_cast<const float*>(st->X), st->ldx, st->J, st->row_off, sqnorm, status);
+    slice_stats_kernel<float><<<(unsigned)nchunks, 256, 0, stream>>>(
+        static_cast<const float*>(st->X), st->ldx, st->J, st->row_off, K, chunk_rows, chunk_begin, part, status);
+  slice_stats_reduce<<<(unsigned)((K + 255) / 256), 256, 0, stream>>>(chunk_begin, K, part, sqnorm);
+  cudaFreeAsync(part, stream);
+  cudaFreeAsync(chunk_begin, stream);
   return cudaGetLastError();
 }
 

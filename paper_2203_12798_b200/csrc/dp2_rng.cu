@@ -121,9 +121,19 @@ struct TailRec {          // one layer-0 tail event, replayed on the host
 };
 constexpr int kTailAttempts = 4;
 
-__global__ void __launch_bounds__(64) omega_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp,
+__global__ void __launch_bounds__(32) omega_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp,
                                                    const int64_t* slice_ids, double* out, TailRec* recs,
                                                    int cap, int32_t* nrec, int32_t* redo) {
+  // lanes index the tables with different layers: shared memory, not the
+  // (uniform-access) constant cache
+  __shared__ uint64_t ki_s[256];
+  __shared__ double wi_s[256], fi_s[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    ki_s[i] = kZigKi[i];
+    wi_s[i] = __longlong_as_double((long long)kZigWiBits[i]);
+    fi_s[i] = __longlong_as_double((long long)kZigFiBits[i]);
+  }
+  __syncthreads();
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
   const uint64_t gid = slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k;
@@ -142,9 +152,9 @@ __global__ void __launch_bounds__(64) omega_kernel(uint64_t seed, int64_t K, int
         r >>= 8;
         const int sign = (int)(r & 1);
         const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-        double x = __dmul_rn((double)rabs, __longlong_as_double((long long)kZigWiBits[idx]));
+        double x = __dmul_rn((double)rabs, wi_s[idx]);
         if (sign) x = -x;
-        if (rabs < kZigKi[idx]) { val = x; break; }
+        if (rabs < ki_s[idx]) { val = x; break; }
         if (idx == 0) {
           TailRec rec;
           rec.slice = k;
@@ -172,8 +182,8 @@ __global__ void __launch_bounds__(64) omega_kernel(uint64_t seed, int64_t K, int
           }
           break;
         }
-        const double f0 = __longlong_as_double((long long)kZigFiBits[idx - 1]);
-        const double f1 = __longlong_as_double((long long)kZigFiBits[idx]);
+        const double f0 = fi_s[idx - 1];
+        const double f1 = fi_s[idx];
         const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(f0, -f1), g.next_double()), f1);
         if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) { val = x; break; }
       }
@@ -188,7 +198,7 @@ cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int s
                       double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st) {
   cudaMemsetAsync(nrec, 0, sizeof(int32_t), st);
   cudaMemsetAsync(redo, 0, sizeof(int32_t) * K, st);
-  omega_kernel<<<(unsigned)((K + 63) / 64), 64, 0, st>>>(seed, K, J, s_k, sp, slice_ids, out,
+  omega_kernel<<<(unsigned)((K + 31) / 32), 32, 0, st>>>(seed, K, J, s_k, sp, slice_ids, out,
                                                           static_cast<TailRec*>(recs), cap, nrec, redo);
   return cudaGetLastError();
 }

@@ -2,8 +2,8 @@
 // M = [V_1 S_1 | ... | V_K S_K] (J x KR, P/compress.py:108-111), fp64.
 //
 //   Y  = M Omega2           (J x s2)     nn split-K partials + ordered reduce
-//   Z  = orth(M^T Y)        (KR x s2)    tn + CGS2 (range-preserving)
-//   Y2 = M Z                (J x s2)     = range of the reference's M (M^T M Omega2)
+//   Z  = M^T Y              (KR x s2)    tn
+//   Y2 = M Z                (J x s2)     = the reference's M (M^T M Omega2)
 //   Q2 = orth(Y2)                        CGS2 (the reference's np.linalg.qr)
 //   C  = M^T Q2             (KR x s2)    B2 = Q2^T M = C^T
 //   B2 B2^T = C^T C = U mu U^T           Jacobi; E = sqrt(mu_R)
@@ -232,7 +232,6 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   };
   nn(omega2, Y);
   tn(Y, Z);
-  cgs2_kernel<<<1, 256, 0, st>>>(Z, KR, s2, s2, 0);
   nn(Z, Y2);
   cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
   tn(Y2, C);

@@ -13,6 +13,7 @@ with stage 1, and as the test reference).
 """
 from __future__ import annotations
 
+import math
 import os
 from concurrent.futures import ThreadPoolExecutor
 
@@ -86,9 +87,13 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
         vals = np.empty(r.size)
         ok = np.ones(r.size, dtype=bool)
         done = np.zeros(r.size, dtype=bool)
-        for a in range(4):  # replay each attempt with NumPy's log1p (P/linalg.py:123's sampler)
-            xx = -_ZIG_INV_R * np.log1p(-r["u"][:, 2 * a])
-            yy = -np.log1p(-r["u"][:, 2 * a + 1])
+        # replay each attempt with the C library's log1p -- the function the
+        # reference sampler calls (npy_log1p); NumPy's np.log1p ufunc may use
+        # a SIMD implementation with different last-bit rounding
+        log1p = np.frompyfunc(math.log1p, 1, 1)
+        for a in range(4):
+            xx = -_ZIG_INV_R * log1p(-r["u"][:, 2 * a]).astype(np.float64)
+            yy = -log1p(-r["u"][:, 2 * a + 1]).astype(np.float64)
             acc = (yy + yy) > (xx * xx)
             last = r["attempts"] == a + 1
             live = ~done & (r["attempts"] >= a + 1)

@@ -17,6 +17,7 @@ of draws, including rejection and tail paths.  Run in the build container:
 from __future__ import annotations
 
 import glob
+import math
 import os
 import sys
 from decimal import Decimal, getcontext
@@ -104,13 +105,13 @@ def sampler(seed, n, ki, wi, fi):
                 break
             if idx == 0:
                 while True:
-                    xx = -INV_R * np.log1p(-nxt_double())
-                    yy = -np.log1p(-nxt_double())
+                    xx = -INV_R * math.log1p(-nxt_double())
+                    yy = -math.log1p(-nxt_double())
                     if yy + yy > xx * xx:
                         out[j] = -(R_TAIL + xx) if ((rabs >> 8) & 1) else R_TAIL + xx
                         break
                 break
-            if (fi[idx - 1] - fi[idx]) * nxt_double() + fi[idx] < np.exp(-0.5 * x * x):
+            if (fi[idx - 1] - fi[idx]) * nxt_double() + fi[idx] < math.exp(-0.5 * x * x):
                 out[j] = x
                 break
     return out
