@@ -16,6 +16,8 @@ Stage1Layout stage1_layout(const dp2_store* st, int sp, int R);
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
                        float* timing, cudaStream_t stream);
+cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                           double* xsq_part, int64_t* status, cudaStream_t stream);
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                        double* xsq_part, int64_t* status, cudaStream_t stream);
 

@@ -638,8 +638,9 @@ static constexpr size_t kXTileBudget = 150 * 1024;
 
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                        double* xsq_part, int64_t* status, cudaStream_t stream) {
+  if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream);
   const int J = (int)st->J;
-  const int elem = st->dtype == DP2_F64 ? 8 : 4;
+  const int elem = 8;
   SketchParams prm{};
   prm.X = st->X;
   prm.ldx = st->ldx;
@@ -664,11 +665,8 @@ cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out
   const int tm = (size_t)2 * 16 * prm.lds * elem <= kXTileBudget ? 16 : 8;
   if ((size_t)2 * tm * prm.lds * elem > 200 * 1024) return cudaErrorInvalidValue;
   const int nseg = st->nseg;
-  if (elem == 8)
-    return tm == 16 ? dispatch_mt<double, 16>(prm, mt, nt, nseg, ng, njs, stream)
-                    : dispatch_mt<double, 8>(prm, mt, nt, nseg, ng, njs, stream);
-  return tm == 16 ? dispatch_mt<float, 16>(prm, mt, nt, nseg, ng, njs, stream)
-                  : dispatch_mt<float, 8>(prm, mt, nt, nseg, ng, njs, stream);
+  return tm == 16 ? dispatch_mt<double, 16>(prm, mt, nt, nseg, ng, njs, stream)
+                  : dispatch_mt<double, 8>(prm, mt, nt, nseg, ng, njs, stream);
 }
 
 int sketch_njs(int J) {
