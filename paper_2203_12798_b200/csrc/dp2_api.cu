@@ -164,7 +164,7 @@ int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_de
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
                                   static_cast<char*>(ws), status_dev, timing_ms, S(stream));
-  return e == cudaSuccess ? ok(8) : fail(e, "dp2_stage1");
+  return e == cudaSuccess ? ok(sp <= 32 ? 9 : 8) : fail(e, "dp2_stage1");
 }
 
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {

@@ -10,16 +10,21 @@
 namespace dp2 {
 
 struct Stage1Layout {
-  size_t part, qz, y2, Pm, Sv, Vt, cand_abs, cand_row, cand_neg, xsq, scr, total;
+  size_t part, qz, y2, Pm, Sv, Vt, cand_abs, cand_row, cand_neg, xsq, scr, gpart, CCg, Gg, sgn, total;
 };
 Stage1Layout stage1_layout(const dp2_store* st, int sp, int R);
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
                        float* timing, cudaStream_t stream);
+cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, int R, const double* part1,
+                             const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
+                             double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
+                             int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
+                             int64_t* status, int phase, cudaStream_t stream);
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                           double* xsq_part, int64_t* status, cudaStream_t stream);
+                           double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                       double* xsq_part, int64_t* status, cudaStream_t stream);
+                       double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part = nullptr);
 
 size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R);
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,

@@ -28,6 +28,7 @@ struct Sketch32Params {
   double* out_part;
   double* y_out;
   double* xsq_part;
+  double* g_part;
   int64_t* status;
 };
 
@@ -81,6 +82,11 @@ __global__ void __launch_bounds__(256, 1) sketch32_kernel(Sketch32Params prm) {
     for (int c = 0; c < SG; ++c) zacc[a][c] = 0.0f;
   double sq = 0.0;
   int bad = 0;
+  constexpr int GPT = (SG * SG + 255) / 256;
+  double gacc[GPT];
+#pragma unroll
+  for (int q = 0; q < GPT; ++q) gacc[q] = 0.0;
+  const bool do_g = prm.g_part != nullptr && jsplit == 0;
   int p = pbeg, t = 0, buf = 0, bslice = -1;
   issue(0, p, 0);
   cp_async_commit();
@@ -147,6 +153,18 @@ __global__ void __launch_bounds__(256, 1) sketch32_kernel(Sketch32Params prm) {
         prm.y_out[(grow + r) * sp + col0 + c] = (double)ys[i];
       }
     }
+    if (do_g) {  // G += Y_t^T Y_t in fp64 (rows past the piece are zero)
+#pragma unroll
+      for (int q = 0; q < GPT; ++q) {
+        const int e = tid + q * 256;
+        if (e < SG * SG) {
+          const int a = e / SG, b = e % SG;
+          double acc = gacc[q];
+          for (int r = 0; r < TM; ++r) acc = fma((double)ys[r * SG + a], (double)ys[r * SG + b], acc);
+          gacc[q] = acc;
+        }
+      }
+    }
 
     // ---- phase B: thread owns j = jbase + tid*JT + a
     const int j0 = jbase + tid * JT;
@@ -187,6 +205,14 @@ __global__ void __launch_bounds__(256, 1) sketch32_kernel(Sketch32Params prm) {
     }
 
     if ((t + 1) * TM >= prm.piece_rows[p]) {  // piece complete: flush partial
+      if (do_g) {
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) {
+          const int e = tid + q * 256;
+          if (e < SG * SG) prm.g_part[(size_t)p * SG * SG + e] = gacc[q];
+          gacc[q] = 0.0;
+        }
+      }
       double* out = prm.out_part + (size_t)p * J * sp + col0;
 #pragma unroll
       for (int a = 0; a < JT; ++a) {
@@ -253,7 +279,7 @@ int lds32(int J) {
 int sketch32_njs(int J) { return (J + 1023) / 1024; }
 
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                           double* xsq_part, int64_t* status, cudaStream_t stream) {
+                           double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
   const int J = (int)st->J;
   Sketch32Params prm{};
   prm.X = static_cast<const float*>(st->X);
@@ -269,6 +295,7 @@ cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double*
   prm.out_part = out_part;
   prm.y_out = y_out;
   prm.xsq_part = xsq_part;
+  prm.g_part = sp <= 32 ? g_part : nullptr;
   prm.status = status;
   const int cpl = sp >= 32 ? 4 : sp / 8;
   const int ng = sp >= 32 ? sp / 32 : 1;

@@ -37,6 +37,7 @@ struct SketchParams {
   double* out_part;         // npieces x J x sp
   double* y_out;            // total_rows x sp or null
   double* xsq_part;         // npieces x njs or null
+  double* g_part;           // npieces x sp x sp (G = Y^T Y per piece) or null
   int64_t* status;
 };
 
@@ -90,6 +91,11 @@ __global__ void __launch_bounds__(256, 1) sketch_kernel(SketchParams prm) {
     for (int b = 0; b < NT; ++b) zacc[a][b][0] = zacc[a][b][1] = 0.0;
   double sq = 0.0;
   int bad = 0;
+  constexpr int GPT = (SG * SG + 255) / 256;
+  double gacc[GPT];
+#pragma unroll
+  for (int q = 0; q < GPT; ++q) gacc[q] = 0.0;
+  const bool do_g = prm.g_part != nullptr && jsplit == 0;
 
   while (true) {
     int np = p, ntl = t + 1;
@@ -147,6 +153,18 @@ __global__ void __launch_bounds__(256, 1) sketch_kernel(SketchParams prm) {
         prm.y_out[(grow + r) * sp + col0 + c] = ys[r * YS + c];
       }
     }
+    if (do_g) {  // G += Y_t^T Y_t (rows past the piece are zero)
+#pragma unroll
+      for (int q = 0; q < GPT; ++q) {
+        const int e = tid + q * 256;
+        if (e < SG * SG) {
+          const int a = e / SG, b = e % SG;
+          double acc = gacc[q];
+          for (int r = 0; r < TM; ++r) acc = fma(ys[r * YS + a], ys[r * YS + b], acc);
+          gacc[q] = acc;
+        }
+      }
+    }
 
     // ---- phase B: Z += X_t^T Y_t (each warp owns MT 8-row blocks of J)
 #pragma unroll
@@ -172,6 +190,14 @@ __global__ void __launch_bounds__(256, 1) sketch_kernel(SketchParams prm) {
     }
 
     if ((t + 1) * TM >= prm.piece_rows[p]) {  // piece complete: flush partial
+      if (do_g) {
+#pragma unroll
+        for (int q = 0; q < GPT; ++q) {
+          const int e = tid + q * 256;
+          if (e < SG * SG) prm.g_part[(size_t)p * SG * SG + e] = gacc[q];
+          gacc[q] = 0.0;
+        }
+      }
       double* out = prm.out_part + (size_t)p * J * sp + col0;
 #pragma unroll
       for (int a = 0; a < MT; ++a) {
@@ -637,8 +663,8 @@ cudaError_t dispatch_mt(const SketchParams& prm, int mt, int nt, int nseg, int n
 static constexpr size_t kXTileBudget = 150 * 1024;
 
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                       double* xsq_part, int64_t* status, cudaStream_t stream) {
-  if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream);
+                       double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
+  if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
   const int J = (int)st->J;
   const int elem = 8;
   SketchParams prm{};
@@ -655,6 +681,7 @@ cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out
   prm.out_part = out_part;
   prm.y_out = y_out;
   prm.xsq_part = xsq_part;
+  prm.g_part = sp <= 32 ? g_part : nullptr;
   prm.status = status;
   const int nt = sp >= 32 ? 4 : sp / 8;
   const int ng = sp >= 32 ? sp / 32 : 1;
@@ -694,6 +721,10 @@ Stage1Layout stage1_layout(const dp2_store* st, int sp, int R) {
   L.cand_row = take(P * R * 8);
   L.cand_neg = take(P * R * 4);
   L.xsq = take(P * sketch_njs((int)J) * 8);
+  L.gpart = take(P * sp * sp * 8);
+  L.CCg = take(K * sp * sp * 8);
+  L.Gg = take(K * sp * sp * 8);
+  L.sgn = take(K * R * 8);
   L.scr = take(K * (3 * (size_t)sp * (sp + 1) + 4 * sp) * 8);
   L.total = off;
   return L;
@@ -719,6 +750,45 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   cudaError_t e = run_sketch(st, omega, sp, part, nullptr, xsq, status, stream);
   if (e != cudaSuccess) return e;
   if (timing) cudaEventRecord(ev[1], stream);
+  if (sp <= 32) {
+    double* gpart = reinterpret_cast<double*>(ws + L.gpart);
+    double* CCg = reinterpret_cast<double*>(ws + L.CCg);
+    double* Gg = reinterpret_cast<double*>(ws + L.Gg);
+    double* sgn = reinterpret_cast<double*>(ws + L.sgn);
+    auto small = [&](int phase) {
+      return run_stage1_small(st, s_dev, sp, R, part, part, gpart, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
+                              reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),
+                              reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
+                              stream);
+    };
+    if ((size_t)J * sp * 8 <= 200 * 1024) {
+      e = small(0);
+      if (e != cudaSuccess) return e;
+    } else {
+      orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
+    }
+    if (timing) cudaEventRecord(ev[2], stream);
+    e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream, gpart);
+    if (e != cudaSuccess) return e;
+    if (timing) cudaEventRecord(ev[3], stream);
+    e = small(1);
+    if (e != cudaSuccess) return e;
+    if (timing) cudaEventRecord(ev[4], stream);
+    complete_kernel<<<K, 256, 0, stream>>>(st->row_off, rank_out, R, A_out);
+    e = cudaGetLastError();
+    if (timing) {
+      cudaEventRecord(ev[5], stream);
+      cudaEventSynchronize(ev[5]);
+      cudaEventElapsedTime(&timing[0], ev[0], ev[1]);
+      cudaEventElapsedTime(&timing[1], ev[1], ev[2]);
+      cudaEventElapsedTime(&timing[2], ev[2], ev[3]);
+      cudaEventElapsedTime(&timing[3], ev[3], ev[4]);
+      cudaEventElapsedTime(&timing[4], ev[4], ev[5]);
+      cudaEventElapsedTime(&timing[5], ev[0], ev[5]);
+      for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+    }
+    return e;
+  }
   orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
   if (timing) cudaEventRecord(ev[2], stream);
   e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream);

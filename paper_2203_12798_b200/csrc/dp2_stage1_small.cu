@@ -1,0 +1,425 @@
+// Stage-1 per-slice factorizations for sketch widths s <= 32 (every config
+// except the rank sweep's large R): the small-matrix steps between and after
+// the two streaming passes, restructured for parallelism (see dp2_stage1.cu
+// for the math; references P/linalg.py:124-131, P/compress.py:108).
+//
+//   orth_smem     Q_Z = CGS2(sum of pass-1 partials), slice matrix in smem
+//   gather        C^T = sum of pass-2 partials; CC = C C^T; G = sum of the
+//                 per-piece Y^T Y accumulated inside pass 2
+//   factor_warp   one warp per slice: G = L L^T (Cholesky; Jacobi-eig fallback
+//                 for rank deficiency), B B^T = L^-1 CC L^-T, Jacobi eig ->
+//                 P = L^-T U_R, S = sqrt(mu_R)
+//   argmax_a      per piece: A = Y P (unsigned) + per-column max |A| (first
+//                 index on ties) candidates
+//   signs_m       per slice: sign rule (P/linalg.py:62-70), P *= sign,
+//                 M block = C^T P (= V S of the reference, P/compress.py:108)
+//   flip_a        A columns *= sign
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+
+// ------------------------------------------------------------ orth (smem CGS2)
+__global__ void __launch_bounds__(256) orth_smem_kernel(const double* part, const int32_t* slice_piece,
+                                                         const int32_t* s_k, int J, int sp, double* Q) {
+  extern __shared__ __align__(16) double qs[];  // J x sp
+  __shared__ double h[32];
+  __shared__ double red[32];
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k];
+  const int n = J * sp;
+  for (int i = tid; i < n; i += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
+    qs[i] = acc;
+  }
+  __syncthreads();
+  for (int c = 0; c < s; ++c) {
+    for (int attempt = 0;; ++attempt) {
+      if (attempt > 0) {
+        const int e = (c + attempt - 1) % J;
+        for (int i = tid; i < J; i += nt) qs[i * sp + c] = (i == e) ? 1.0 : 0.0;
+        __syncthreads();
+      }
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int i = warp; i < c; i += nw) {
+          double acc = 0.0;
+          for (int r = lane; r < J; r += 32) acc = fma(qs[r * sp + i], qs[r * sp + c], acc);
+          acc = warp_sum(acc);
+          if (lane == 0) h[i] = acc;
+        }
+        __syncthreads();
+        for (int r = tid; r < J; r += nt) {
+          double acc = qs[r * sp + c];
+          for (int i = 0; i < c; ++i) acc = fma(-h[i], qs[r * sp + i], acc);
+          qs[r * sp + c] = acc;
+        }
+        __syncthreads();
+      }
+      double part2 = 0.0;
+      for (int r = tid; r < J; r += nt) part2 = fma(qs[r * sp + c], qs[r * sp + c], part2);
+      const double nrm2 = block_sum(part2, red);
+      const bool ok = attempt == 0 ? (nrm2 > 1e-300) : (nrm2 > 0.25);
+      if (ok || attempt > J + 1) {
+        const double inv = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
+        for (int r = tid; r < J; r += nt) qs[r * sp + c] *= inv;
+        __syncthreads();
+        break;
+      }
+    }
+  }
+  double* Qk = Q + (size_t)k * n;
+  for (int i = tid; i < n; i += nt) Qk[i] = qs[i];
+}
+
+// ------------------------------------------------------------ gather
+__global__ void __launch_bounds__(256) gather_kernel(const double* part, const double* gpart,
+                                                      const int32_t* slice_piece, int J, int sp, double* Ct,
+                                                      double* CCg, double* Gg) {
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int n = J * sp;
+  double* C = Ct + (size_t)k * n;
+  for (int i = tid; i < n; i += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
+    C[i] = acc;
+  }
+  for (int e = tid; e < sp * sp; e += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * sp * sp + e];
+    Gg[(size_t)k * sp * sp + e] = acc;
+  }
+  __syncthreads();
+  const int ntri = sp * (sp + 1) / 2;
+  for (int e = warp; e < ntri; e += nw) {
+    int a = 0, rem = e;
+    while (rem >= sp - a) { rem -= sp - a; ++a; }
+    const int b = a + rem;
+    double acc = 0.0;
+    for (int j = lane; j < J; j += 32) acc = fma(C[j * sp + a], C[j * sp + b], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      CCg[(size_t)k * sp * sp + a * sp + b] = acc;
+      CCg[(size_t)k * sp * sp + b * sp + a] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------ factor (warp / slice)
+__global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, const double* CCg, const int32_t* s_k,
+                                                           int K, int sp, int R, double* Pm, double* Sv,
+                                                           int32_t* rank_out, int64_t* status) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int k = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int ld = sp + 1;
+  const size_t per = 4 * (size_t)sp * ld + 4 * (size_t)sp;
+  double* G = sm + wib * per;   // L or T
+  double* CC = G + sp * ld;     // X / Bg
+  double* W = CC + sp * ld;
+  double* U = W + sp * ld;
+  double* lam = U + sp * ld;    // sp
+  double* cs = lam + sp;        // 3 * (sp/2 + 1) <= 3 sp
+  __shared__ int perm_s[4][64];
+  int* perm = perm_s[wib];
+  if (k >= K) return;
+  const int s = s_k[k];
+  for (int e = lane; e < s * s; e += 32) {
+    const int a = e / s, b = e % s;
+    G[a * ld + b] = Gg[(size_t)k * sp * sp + a * sp + b];
+    CC[a * ld + b] = CCg[(size_t)k * sp * sp + a * sp + b];
+  }
+  __syncwarp();
+  // ---- Cholesky of G with a relative pivot floor
+  double gmax = 0.0;
+  for (int i = 0; i < s; ++i) gmax = fmax(gmax, G[i * ld + i]);
+  bool chol = gmax > 0.0;
+  for (int c = 0; c < s && chol; ++c) {
+    double d = 0.0;
+    if (lane == 0) {
+      d = G[c * ld + c];
+      for (int m = 0; m < c; ++m) d = fma(-G[c * ld + m], G[c * ld + m], d);
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (!(d > 1e-13 * gmax)) { chol = false; break; }
+    const double l = sqrt(d);
+    for (int i = c + 1 + lane; i < s; i += 32) {
+      double t = G[i * ld + c];
+      for (int m = 0; m < c; ++m) t = fma(-G[i * ld + m], G[c * ld + m], t);
+      G[i * ld + c] = t / l;
+    }
+    if (lane == 0) G[c * ld + c] = l;
+    __syncwarp();
+  }
+  int rp = s;
+  if (chol) {
+    // X = L^-1 CC (lanes own columns), then Bg = X L^-T: Bg[r][:] = (L^-1 X[r][:]^T)^T
+    for (int c = lane; c < s; c += 32)
+      for (int i = 0; i < s; ++i) {
+        double t = CC[i * ld + c];
+        for (int m = 0; m < i; ++m) t = fma(-G[i * ld + m], CC[m * ld + c], t);
+        CC[i * ld + c] = t / G[i * ld + i];
+      }
+    __syncwarp();
+    for (int r = lane; r < s; r += 32)
+      for (int i = 0; i < s; ++i) {
+        double t = CC[r * ld + i];
+        for (int m = 0; m < i; ++m) t = fma(-G[i * ld + m], W[r * ld + m], t);
+        W[r * ld + i] = t / G[i * ld + i];
+      }
+    __syncwarp();
+    for (int e = lane; e < s * s; e += 32) {  // symmetrise into CC
+      const int a = e / s, b = e % s;
+      CC[a * ld + b] = 0.5 * (W[a * ld + b] + W[b * ld + a]);
+    }
+    __syncwarp();
+  } else {
+    // rank-deficient sketch: eigen basis of G, drop lambda <= 1e-13 lambda_max
+    for (int e = lane; e < s * s; e += 32) {
+      const int a = e / s, b = e % s;
+      G[a * ld + b] = Gg[(size_t)k * sp * sp + a * sp + b];
+    }
+    __syncwarp();
+    const int sw = jacobi_eig_warp(G, ld, W, ld, s, cs);
+    if (sw > 40 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+    if (lane == 0) {
+      for (int i = 0; i < s; ++i) perm[i] = i;
+      for (int i = 1; i < s; ++i) {
+        const int v = perm[i];
+        const double key = G[v * ld + v];
+        int j = i - 1;
+        while (j >= 0 && G[perm[j] * ld + perm[j]] < key) { perm[j + 1] = perm[j]; --j; }
+        perm[j + 1] = v;
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < s; i += 32) lam[i] = G[perm[i] * ld + perm[i]];
+    __syncwarp();
+    const double lmax = lam[0] > 0.0 ? lam[0] : 0.0;
+    rp = 0;
+    for (int i = 0; i < s; ++i) rp += (lam[i] > 1e-13 * lmax && lam[i] > 0.0) ? 1 : 0;
+    for (int e = lane; e < s * s; e += 32) {  // T = W[:, perm] / sqrt(lam) -> G
+      const int a = e / s, c = e % s;
+      G[a * ld + c] = c < rp ? W[a * ld + perm[c]] / sqrt(lam[c]) : 0.0;
+    }
+    __syncwarp();
+    for (int e = lane; e < s * rp; e += 32) {  // tmp = CC T -> W
+      const int a = e / rp, c = e % rp;
+      double acc = 0.0;
+      for (int b = 0; b < s; ++b) acc = fma(CC[a * ld + b], G[b * ld + c], acc);
+      W[a * ld + c] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < rp * rp; e += 32) {  // Bg = T^T tmp -> U (then CC)
+      const int a = e / rp, c = e % rp;
+      double acc = 0.0;
+      for (int b = 0; b < s; ++b) acc = fma(G[b * ld + a], W[b * ld + c], acc);
+      U[a * ld + c] = acc;
+    }
+    __syncwarp();
+    for (int e = lane; e < rp * rp; e += 32) {
+      const int a = e / rp, c = e % rp;
+      CC[a * ld + c] = 0.5 * (U[a * ld + c] + U[c * ld + a]);
+    }
+    __syncwarp();
+  }
+  // ---- eig(Bg) -> U, descending
+  const int sw = jacobi_eig_warp(CC, ld, U, ld, rp, cs);
+  if (sw > 40 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  if (lane == 0) {
+    for (int i = 0; i < rp; ++i) perm[i] = i;
+    for (int i = 1; i < rp; ++i) {
+      const int v = perm[i];
+      const double key = CC[v * ld + v];
+      int j = i - 1;
+      while (j >= 0 && CC[perm[j] * ld + perm[j]] < key) { perm[j + 1] = perm[j]; --j; }
+      perm[j + 1] = v;
+    }
+  }
+  __syncwarp();
+  double* Pk = Pm + (size_t)k * sp * R;
+  double* Sk = Sv + (size_t)k * R;
+  // P[:, r] = T U[:, perm[r]]:  Cholesky path solves L^T p = u (lanes over r)
+  for (int r = lane; r < R; r += 32) {
+    const double mu = r < rp ? CC[perm[r] * ld + perm[r]] : 0.0;
+    Sk[r] = mu > 0.0 ? sqrt(mu) : 0.0;
+    if (r >= rp) {
+      for (int a = 0; a < sp; ++a) Pk[a * R + r] = 0.0;
+      continue;
+    }
+    const int col = perm[r];
+    if (chol) {
+      for (int i = s - 1; i >= 0; --i) {
+        double t = U[i * ld + col];
+        for (int m = i + 1; m < s; ++m) t = fma(-G[m * ld + i], Pk[m * R + r], t);
+        Pk[i * R + r] = t / G[i * ld + i];
+      }
+    } else {
+      for (int a = 0; a < s; ++a) {
+        double acc = 0.0;
+        for (int b = 0; b < rp; ++b) acc = fma(G[a * ld + b], U[b * ld + col], acc);
+        Pk[a * R + r] = acc;
+      }
+    }
+    for (int a = s; a < sp; ++a) Pk[a * R + r] = 0.0;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int rk = 0;
+    for (int r = 0; r < R; ++r) rk += Sk[r] > 0.0 ? 1 : 0;
+    rank_out[k] = rk;
+    if (rk < R) status_min(status, ST_RANKDEF, k);
+  }
+}
+
+// ------------------------------------------------------------ A = Y P + argmax candidates
+__global__ void __launch_bounds__(256) argmax_a_kernel(const double* y2, const int64_t* row_off,
+                                                        const int32_t* piece_slice, const int64_t* piece_row0,
+                                                        const int32_t* piece_rows, const int32_t* s_k,
+                                                        const double* Pm, int sp, int R, double* A,
+                                                        double* cand_abs, int64_t* cand_row, int32_t* cand_neg) {
+  constexpr int TR = 128;
+  extern __shared__ __align__(16) double sm[];
+  double* Ps = sm;                  // sp x R
+  double* ytile = Ps + sp * R;      // TR x sp
+  double* atile = ytile + TR * sp;  // TR x (R+1)
+  __shared__ double babs[64];
+  __shared__ int64_t brow[64];
+  __shared__ int bneg[64];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = piece_slice[p], s = s_k[k];
+  const int64_t base = row_off[k], r0 = piece_row0[p], nr = piece_rows[p];
+  const int lda = R + 1;
+  for (int i = tid; i < sp * R; i += blockDim.x) Ps[i] = Pm[(size_t)k * sp * R + i];
+  for (int c = tid; c < R; c += blockDim.x) { babs[c] = -1.0; brow[c] = INT64_MAX; bneg[c] = 0; }
+  for (int64_t t0 = 0; t0 < nr; t0 += TR) {
+    const int rows = (int)imin64(TR, nr - t0);
+    __syncthreads();
+    for (int i = tid; i < rows * sp; i += blockDim.x) ytile[i] = y2[(r0 + t0) * sp + i];
+    __syncthreads();
+    for (int e = tid; e < rows * R; e += blockDim.x) {
+      const int i = e / R, c = e % R;
+      double acc = 0.0;
+      for (int a = 0; a < s; ++a) acc = fma(ytile[i * sp + a], Ps[a * R + c], acc);
+      atile[i * lda + c] = acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < rows * R; e += blockDim.x) A[(r0 + t0) * R + e] = atile[(e / R) * lda + e % R];
+    for (int c = warp; c < R; c += 8) {
+      double ba = -1.0;
+      int64_t br = INT64_MAX;
+      int bn = 0;
+      for (int i = lane; i < rows; i += 32) {
+        const double v = atile[i * lda + c], a = fabs(v);
+        if (a > ba) { ba = a; br = r0 + t0 + i - base; bn = v < 0.0; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
+        const int64_t orow = __shfl_xor_sync(0xffffffffu, br, o);
+        const int on = __shfl_xor_sync(0xffffffffu, bn, o);
+        if (oa > ba || (oa == ba && orow < br)) { ba = oa; br = orow; bn = on; }
+      }
+      if (lane == 0 && (ba > babs[c] || (ba == babs[c] && br < brow[c]))) {
+        babs[c] = ba;
+        brow[c] = br;
+        bneg[c] = bn;
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < R; c += blockDim.x) {
+    cand_abs[(size_t)p * R + c] = babs[c];
+    cand_row[(size_t)p * R + c] = brow[c];
+    cand_neg[(size_t)p * R + c] = bneg[c];
+  }
+}
+
+// ------------------------------------------------------------ signs + M
+__global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece, const double* cand_abs,
+                                                       const int64_t* cand_row, const int32_t* cand_neg,
+                                                       double* Pm, const double* Ct, int K, int J, int sp, int R,
+                                                       double* sgn_out, double* M) {
+  extern __shared__ __align__(16) double sm[];
+  double* Ps = sm;  // sp x R (signed)
+  __shared__ double sgn[64];
+  const int k = blockIdx.x, tid = threadIdx.x;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  for (int r = tid; r < R; r += blockDim.x) {
+    double ba = -1.0;
+    int64_t br = INT64_MAX;
+    int bn = 0;
+    for (int p = p0; p < p1; ++p) {
+      const double va = cand_abs[(size_t)p * R + r];
+      const int64_t ra = cand_row[(size_t)p * R + r];
+      if (va > ba || (va == ba && ra < br)) { ba = va; br = ra; bn = cand_neg[(size_t)p * R + r]; }
+    }
+    sgn[r] = bn ? -1.0 : 1.0;
+    sgn_out[(size_t)k * R + r] = sgn[r];
+  }
+  __syncthreads();
+  double* Pk = Pm + (size_t)k * sp * R;
+  for (int i = tid; i < sp * R; i += blockDim.x) {
+    const double v = Pk[i] * sgn[i % R];
+    Pk[i] = v;
+    Ps[i] = v;
+  }
+  __syncthreads();
+  const double* C = Ct + (size_t)k * J * sp;
+  const int64_t KR = (int64_t)K * R;
+  for (int64_t e = tid; e < (int64_t)J * R; e += blockDim.x) {
+    const int64_t j = e / R;
+    const int r = (int)(e % R);
+    double acc = 0.0;
+    for (int a = 0; a < sp; ++a) acc = fma(C[j * sp + a], Ps[a * R + r], acc);
+    M[j * KR + (int64_t)k * R + r] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) flip_a_kernel(const int32_t* piece_slice, const int64_t* piece_row0,
+                                                      const int32_t* piece_rows, const double* sgn, int R,
+                                                      double* A) {
+  const int p = blockIdx.x;
+  const int k = piece_slice[p];
+  const int64_t r0 = piece_row0[p], nr = piece_rows[p];
+  for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) A[r0 * R + e] *= sgn[(size_t)k * R + e % R];
+}
+
+// ------------------------------------------------------------ host
+size_t small_factor_smem(int sp) { return (4 * (size_t)sp * (sp + 1) + 4 * (size_t)sp) * 8; }
+
+cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, int R, const double* part1,
+                             const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
+                             double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
+                             int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
+                             int64_t* status, int phase, cudaStream_t stream) {
+  const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
+  cudaError_t e = cudaSuccess;
+  if (phase == 0) {  // between the passes
+    const size_t qb = (size_t)J * sp * 8;
+    e = cudaFuncSetAttribute(orth_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb);
+    if (e != cudaSuccess) return e;
+    orth_smem_kernel<<<K, 256, qb, stream>>>(part1, st->slice_piece, s_dev, J, sp, qz);
+    return cudaGetLastError();
+  }
+  gather_kernel<<<K, 256, 0, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
+  const int wpb = sp <= 24 ? 4 : 2;
+  const size_t fs = wpb * small_factor_smem(sp);
+  e = cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
+  if (e != cudaSuccess) return e;
+  factor_warp_kernel<<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, sp, R, Pm, Sv, rank_out,
+                                                                      status);
+  const size_t as = ((size_t)sp * R + 128 * (size_t)sp + 128 * (size_t)(R + 1)) * 8;
+  e = cudaFuncSetAttribute(argmax_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
+  if (e != cudaSuccess) return e;
+  argmax_a_kernel<<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows, s_dev,
+                                          Pm, sp, R, A, cand_abs, cand_row, cand_neg);
+  signs_m_kernel<<<K, 256, (size_t)sp * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+                                                          J, sp, R, sgn, M);
+  flip_a_kernel<<<P, 256, 0, stream>>>(st->piece_slice, st->piece_row0, st->piece_rows, sgn, R, A);
+  return cudaGetLastError();
+}
+
+}  // namespace dp2
