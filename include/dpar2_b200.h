@@ -164,6 +164,19 @@ int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, in
                 int32_t normalize, double* trace_out, int64_t* tstamp_out, int32_t* iters_out,
                 int32_t use_graph, void* ws, size_t ws_bytes, int64_t* status_dev, void* stream);
 
+/* The same iteration split at its reduction points for multi-GPU runs
+ * (DESIGN.md §7): phase 0 prep; 1 rotate -> red_out[2R^2] = [G1 | W^T W]
+ * partials; 2 solve_h(red_in = allreduced [G1 | W^T W]); 3 mode2 -> red_out =
+ * [summed | gram(W nh)]; 4 solve_v(red_in); 5 mode3 + metric -> red_out[0] =
+ * local e; 6 finish(red_in[0] = global e: trace, stop rule).  K, F, W, polar
+ * are the caller's local slices; D, E, H, V replicated.  The workspace
+ * (dp2_als_workspace(K, J, R)) carries state between phases. */
+int dp2_als_phase(int32_t phase, const double* F, const double* D, const double* E, int64_t K, int64_t J,
+                  int32_t R, double* H, double* V, double* W, double* polar, int32_t it, double tol,
+                  int32_t normalize, double* trace_out, int64_t* tstamp_out, int32_t* iters_out,
+                  const double* red_in, double* red_out, void* ws, size_t ws_bytes, int64_t* status_dev,
+                  void* stream);
+
 /* Kernel-granular entry points (the reference's test-level API,
  * P/solver.py:48-149).  theta (K x R x R) = (P_k Z_k^T) F_k. */
 int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J,

@@ -55,6 +55,8 @@ _SIGS = {
     "dp2_als_workspace": (c_sz, [c_i64, c_i64, c_i32]),
     "dp2_als_run": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_i32,
                             c_vp, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp, c_vp]),
+    "dp2_als_phase": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_f64,
+                              c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "dp2_update_rotations": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                      c_sz, c_vp, c_vp]),
     "dp2_mttkrp": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,

@@ -96,42 +96,41 @@ def check_status(status, what):
     return s
 
 
-def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
-             plan=None, threads=None, timings=None):
-    """Compress ``tensor`` at ``rank`` with two randomized-SVD stages."""
-    if not isinstance(tensor, IrregularTensor):
-        tensor = IrregularTensor(tensor)
+def check_rank(tensor: IrregularTensor, rank, slice_ids=None):
+    """Rank checks and messages of P/compress.py:84-90."""
     if rank < 1:
         raise RankTooLargeError(f"rank must be >= 1, got {rank}")
     if rank > tensor.num_cols:
         raise RankTooLargeError(f"rank {rank} exceeds column count {tensor.num_cols}")
-    for k, rows in enumerate(tensor.row_counts):
+    ids = range(tensor.num_slices) if slice_ids is None else slice_ids
+    for k, rows in zip(ids, tensor.row_counts):
         if rank > rows:
             raise RankTooLargeError(f"rank {rank} exceeds row count {rows} of slice {k}")
     if rank > 64:
         raise RankTooLargeError(f"rank {rank} exceeds the device limit of 64")
-    resolve_threads(threads)
-    base = rsvd if rsvd is not None else RsvdParams(rank=rank)
+
+
+def stage2_params(base: RsvdParams, stage2, rank, K, J):
+    second = stage2 if stage2 is not None else base
+    second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
+    if second.power_iters != 1:
+        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
+    return second, sketch_width(J, K * rank, rank, second.oversampling)
+
+
+def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, timings=None, status=None):
+    """Stage 1 on the device for the tensor's slices (global ids ``slice_ids``
+    select the per-slice seeds in a multi-GPU shard).  Returns A (sum I_k x R),
+    M (J x K_local R, local slice order) and the per-slice numerical ranks."""
     if base.power_iters != 1:
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
     widths = [sketch_width(m, J, rank, base.oversampling) for m in tensor.row_counts]
     sp = padded_width(max(widths))
     dev = tensor.X.device
-    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on a host
-    # thread while the device generates the stage-1 sketches and runs stage 1
-    second = stage2 if stage2 is not None else base
-    second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
-    if second.power_iters != 1:
-        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
-    KR = K * rank
-    s2 = sketch_width(J, KR, rank, second.oversampling)
-    om2_box = {}
-    om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, KR, s2)))
-    om2_thread.start()
     t0 = time.perf_counter()
     rstats = {}
-    omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
+    omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats)
     s_dev = torch.tensor(widths, dtype=torch.int32).to(dev, non_blocking=True)
     t_omega = time.perf_counter() - t0
     nseg = nseg_for(tensor)
@@ -140,15 +139,26 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
     A = torch.empty((int(tensor.row_off_host[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
-    status = new_status(dev)
+    status = new_status(dev) if status is None else status
     ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), dev)
     tm = (C.c_float * 8)() if timings is not None else None
     _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
                               _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
-    del ws
-    # stage 2 (P/compress.py:109-111)
-    om2_thread.join()
-    om2 = torch.from_numpy(om2_box["v"]).to(dev)
+    if timings is not None:
+        timings.update(rstats)
+        timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
+                       stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
+                       stage1_ms=tm[5], sp=sp, nseg=nseg, npieces=int(st.npieces))
+    del keep, ws
+    return A, M, rank_found, status
+
+
+def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None):
+    """Stage 2 (P/compress.py:109-111) on the device: D, E, F."""
+    dev = M.device
+    lib = _lib.lib()
+    om2 = om2 if isinstance(om2, torch.Tensor) else torch.from_numpy(om2)
+    om2 = om2.to(dev)
     D = torch.empty((J, rank), dtype=torch.float64, device=dev)
     E = torch.empty(rank, dtype=torch.float64, device=dev)
     F = torch.empty((KR, rank), dtype=torch.float64, device=dev)
@@ -160,15 +170,30 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
                               _vp(status), stream_ptr()), "stage2")
     if ev:
         ev[1].record()
-    check_status(status, "compress")
-    if timings is not None:
         torch.cuda.synchronize()
-        timings.update(rstats)
-        timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
-                       stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
-                       stage1_ms=tm[5], stage2_ms=ev[0].elapsed_time(ev[1]), sp=sp, s2=s2, nseg=nseg,
-                       npieces=int(st.npieces))
-    del keep
+        timings.update(stage2_ms=ev[0].elapsed_time(ev[1]), s2=s2)
+    return D, E, F
+
+
+def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
+             plan=None, threads=None, timings=None):
+    """Compress ``tensor`` at ``rank`` with two randomized-SVD stages."""
+    if not isinstance(tensor, IrregularTensor):
+        tensor = IrregularTensor(tensor)
+    check_rank(tensor, rank)
+    resolve_threads(threads)
+    base = rsvd if rsvd is not None else RsvdParams(rank=rank)
+    J, K = tensor.num_cols, tensor.num_slices
+    second, s2 = stage2_params(base, stage2, rank, K, J)
+    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on a host
+    # thread while the device generates the stage-1 sketches and runs stage 1
+    om2_box = {}
+    om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, K * rank, s2)))
+    om2_thread.start()
+    A, M, rank_found, status = run_stage1(tensor, rank, base, timings=timings)
+    om2_thread.join()
+    D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2_box["v"], status, timings=timings)
+    check_status(status, "compress")
     return CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
                             cores=F, rank_found=rank_found)
 

@@ -1007,3 +1007,75 @@ cudaError_t als_metric(const double* theta, const double* D, const double* E, in
 }
 
 }  // namespace dp2
+
+namespace dp2 {
+// ------------------------------------------------------------ phase API (multi-GPU)
+// One ALS iteration split at its three reduction points so that the caller can
+// allreduce the R x R partials across GPUs between phases:
+//   0 prep | 1 rotate -> red_out = [G1 | W'W] | 2 solve_h(red_in)
+//   3 mode2 -> red_out = [summed | W''W''] | 4 solve_v(red_in)
+//   5 mode3 + metric -> red_out[0] = e_local | 6 finish(red_in[0])
+cudaError_t als_phase(int phase, const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
+                      double* H, double* V, double* W, double* polar, int it, double tol, int normalize,
+                      double* trace, int64_t* tstamp, int32_t* iters, const double* red_in, double* red_out,
+                      char* ws, int64_t* status, cudaStream_t st) {
+  AlsBufs b = make_bufs(ws, K, J, R);
+  SliceArgs a = slice_args(F, D, E, H, V, W, K, J, R, status);
+  a.polar = polar;
+  a.theta = b.theta;
+  SolveArgs sv = solve_args(D, E, H, V, W, J, R, normalize, b, status);
+  const int nt = 32 * b.wpb;
+  const size_t RR = (size_t)R * R;
+  cudaError_t e = cudaSuccess;
+  switch (phase) {
+    case 0:
+      e = prepare(R, b);
+      if (e != cudaSuccess) return e;
+      als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, tstamp, 1);
+      break;
+    case 1:
+      a.mode1 = 1;
+      a.warm = 1;
+      als_rotate_kernel<<<b.nb, nt, rotate_smem(R, b.wpb), st>>>(a, b);
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_g1, b.nb, (int64_t)RR, red_out);
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_wtw, b.nb, (int64_t)RR, red_out + RR);
+      break;
+    case 2:
+      cudaMemcpyAsync(b.s_g1, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(b.s_wtw, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
+      sv.nslots = 1;
+      als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
+      break;
+    case 3:
+      als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_m2, b.nb, (int64_t)RR, red_out);
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_wtw2, b.nb, (int64_t)RR, red_out + RR);
+      break;
+    case 4:
+      cudaMemcpyAsync(b.s_m2, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(b.s_wtw2, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
+      sv.nslots = 1;
+      als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
+      break;
+    case 5:
+      a.write_w = 1;
+      a.write_l = 1;
+      a.Wout = W;
+      als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
+      e = launch_metric(b, D, V, J, R, K, st);
+      if (e != cudaSuccess) return e;
+      reduce_parts_dev<<<1, 32, 0, st>>>(b.s_e, b.nbm, 1, red_out);
+      break;
+    case 6: {
+      cudaMemcpyAsync(b.s_e, red_in, 8, cudaMemcpyDeviceToDevice, st);
+      AlsBufs b1 = b;
+      b1.nbm = 1;
+      als_finish_kernel<<<1, 32, 0, st>>>(b1, it, tol, trace, tstamp, iters);
+      break;
+    }
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+}  // namespace dp2

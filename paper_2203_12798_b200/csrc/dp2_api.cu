@@ -195,6 +195,22 @@ int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, in
   return e == cudaSuccess ? ok(1 + 7 * (int64_t)max_iters) : fail(e, "dp2_als_run");
 }
 
+int dp2_als_phase(int32_t phase, const double* F, const double* D, const double* E, int64_t K, int64_t J,
+                  int32_t R, double* H, double* V, double* W, double* polar, int32_t it, double tol,
+                  int32_t normalize, double* trace_out, int64_t* tstamp_out, int32_t* iters_out,
+                  const double* red_in, double* red_out, void* ws, size_t ws_bytes, int64_t* status_dev,
+                  void* stream) {
+  if (phase < 0 || phase > 6 || R < 1 || R > 64 || K < 1 || J < 1) return fail_arg("invalid ALS phase");
+  if (ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("workspace too small");
+  if ((phase == 2 || phase == 4 || phase == 6) && red_in == nullptr) return fail_arg("phase needs red_in");
+  if ((phase == 1 || phase == 3 || phase == 5) && red_out == nullptr) return fail_arg("phase needs red_out");
+  cudaError_t e = dp2::als_phase(phase, F, D, E, K, J, R, H, V, W, polar, it, tol, normalize, trace_out,
+                                 tstamp_out, iters_out, red_in, red_out, static_cast<char*>(ws), status_dev,
+                                 S(stream));
+  static const int kLaunches[7] = {1, 3, 1, 3, 1, 3, 1};
+  return e == cudaSuccess ? ok(kLaunches[phase]) : fail(e, "dp2_als_phase");
+}
+
 int dp2_update_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
                          const double* H, const double* V, const double* W, double* polar_out, double* theta_out,
                          void* ws, size_t ws_bytes, int64_t* status_dev, void* stream) {

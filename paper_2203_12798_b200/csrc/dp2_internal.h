@@ -36,6 +36,10 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
                     int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
                     char* ws, int64_t* status, cudaStream_t stream);
+cudaError_t als_phase(int phase, const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
+                      double* H, double* V, double* W, double* polar, int it, double tol, int normalize,
+                      double* trace, int64_t* tstamp, int32_t* iters, const double* red_in, double* red_out,
+                      char* ws, int64_t* status, cudaStream_t st);
 cudaError_t als_rotations(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                           const double* H, const double* V, const double* W, double* polar,
                           double* theta, char* ws, int64_t* status, cudaStream_t stream);

@@ -1,0 +1,174 @@
+"""Multi-GPU DPar2: slices sharded over ranks (one process per GPU).
+
+* Placement: ``greedy_partition(row_counts, world)`` -- the reference's Alg. 4
+  (P/scheduler.py:29-51), bit-exact -- assigns slices to ranks; each rank keeps
+  its slices in ascending global order.
+* Stage 1: local, no communication; the per-slice sketch seeds use the
+  GLOBAL slice index (derived_seed(seed, k), P/compress.py:96-103), so every
+  slice gets exactly the reference's Omega_k wherever it lives.
+* Stage 2: M (J x KR) must be in global slice order (P/compress.py:108).  Each
+  rank scatters its J x R blocks into a zero J x KR buffer and one allreduce
+  (sum) assembles M exactly -- every entry has a single nonzero contributor, so
+  the sum is exact -- then stage 2 runs replicated (identical inputs, identical
+  outputs on every rank).
+* ALS: D, E, H, V replicated; F rows, W rows, rotations and Q local.  Each
+  iteration allreduces three tiny buffers (2 R^2, 2 R^2, 1 doubles) between
+  the phases of ``dp2_als_phase``.
+
+The driver (``ShardedALS``) only sequences phases and collectives; the phase
+compute is a pluggable ``ops`` object (the C ABI on the GPU; the gloo tests on
+CPU substitute a NumPy emulation to check the sharded decomposition).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .scheduler import greedy_partition
+
+
+def shard_slices(row_counts, world):
+    """Per-rank global slice ids (LPT placement, ascending within a rank)."""
+    plan = greedy_partition(row_counts, world)
+    return [sorted(s) for s in plan.sets], plan.loads
+
+
+def assemble_m(M_local, local_ids, K, R, group=None):
+    """Exact J x KR M in global slice order from each rank's J x K_local R blocks."""
+    J = M_local.shape[0]
+    full = torch.zeros((J, K * R), dtype=M_local.dtype, device=M_local.device)
+    if len(local_ids):
+        cols = (torch.as_tensor(local_ids, device=M_local.device)[:, None] * R +
+                torch.arange(R, device=M_local.device)[None, :]).reshape(-1)
+        full[:, cols] = M_local
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(full, group=group)
+    return full
+
+
+def local_rows(F, local_ids, R):
+    """Rows of F (KR x R) belonging to the local slices, in local order."""
+    idx = (torch.as_tensor(local_ids, device=F.device)[:, None] * R +
+           torch.arange(R, device=F.device)[None, :]).reshape(-1)
+    return F.index_select(0, idx).contiguous()
+
+
+class ShardedALS:
+    """Phase sequencer: per iteration three allreduces of R x R sized partials."""
+
+    def __init__(self, ops, allreduce):
+        self.ops, self.allreduce = ops, allreduce
+
+    def run(self, max_iters):
+        self.ops.phase(0)
+        for it in range(max_iters):
+            red = self.allreduce(self.ops.phase(1, it=it))
+            self.ops.phase(2, it=it, red_in=red)
+            red = self.allreduce(self.ops.phase(3, it=it))
+            self.ops.phase(4, it=it, red_in=red)
+            red = self.allreduce(self.ops.phase(5, it=it))
+            self.ops.phase(6, it=it, red_in=red)
+
+
+class GpuAlsOps:
+    """``dp2_als_phase`` on the local slices."""
+
+    def __init__(self, F_local, D, E, H, V, W_local, J, R, max_iters, tol, normalize):
+        dev = D.device
+        self.F, self.D, self.E, self.H, self.V, self.W = F_local, D, E, H, V, W_local
+        self.K, self.J, self.R = W_local.shape[0], J, R
+        self.tol, self.normalize = float(tol), int(bool(normalize))
+        self.polar = torch.empty((self.K, R, R), dtype=torch.float64, device=dev)
+        self.trace = torch.zeros(max_iters, dtype=torch.float64, device=dev)
+        self.tstamp = torch.zeros(max_iters + 1, dtype=torch.int64, device=dev)
+        self.iters = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.red = torch.zeros(2 * R * R, dtype=torch.float64, device=dev)
+        self.ws = torch.empty(max(256, int(_lib.lib().dp2_als_workspace(self.K, J, R))), dtype=torch.uint8,
+                              device=dev)
+        from .tensor import new_status
+        self.status = new_status(dev)
+
+    def phase(self, ph, it=0, red_in=None):
+        vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
+        n = 2 * self.R * self.R if ph in (1, 3) else 1
+        out = self.red[:n] if ph in (1, 3, 5) else None
+        _lib.check(_lib.lib().dp2_als_phase(
+            ph, vp(self.F), vp(self.D), vp(self.E), self.K, self.J, self.R, vp(self.H), vp(self.V), vp(self.W),
+            vp(self.polar), it, self.tol, self.normalize, vp(self.trace), vp(self.tstamp), vp(self.iters),
+            vp(red_in), vp(out), vp(self.ws), self.ws.numel(), vp(self.status),
+            C.c_void_p(torch.cuda.current_stream().cuda_stream)), f"als_phase{ph}")
+        return out.clone() if out is not None else None
+
+
+def nccl_allreduce(group=None):
+    def f(t):
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(t, group=group)
+        return t
+    return f
+
+
+class DistributedFit:
+    """This rank's shard of a synthetic BASELINE-model tensor, fitted jointly
+    with the other ranks (bench.py's N > 1 path)."""
+
+    def __init__(self, cfg, seed, rank, world):
+        from . import synth
+        from .tensor import IrregularTensor
+        rows_all, _, _ = synth.shared_factors(cfg, seed)
+        shards, loads = shard_slices(rows_all, world)
+        self.local_ids = shards[rank]
+        self.rank, self.world, self.cfg, self.seed = rank, world, cfg, seed
+        X, rows, _, _ = synth.generate_device(cfg, seed, slices=self.local_ids)
+        self.tensor = IrregularTensor.from_packed(X, rows, cfg.cols)
+        self.local_rows = int(sum(rows))
+        self.total_rows = int(sum(rows_all))
+        self.total_entries = self.total_rows * cfg.cols
+        self.K = cfg.num_slices
+        self.loads = loads
+
+    def fit(self, R, opts, timings=None):
+        from .compress import check_status, run_stage1, run_stage2, stage2_params
+        from .factors import FitTrace, Parafac2Factors, initial_factors
+        from .linalg import RsvdParams
+        from .rng import stage2_omega
+        from .solver import assemble_q
+        t = self.tensor
+        J, K = t.num_cols, self.K
+        base = RsvdParams(rank=R, seed=opts.seed)
+        second, s2 = stage2_params(base, None, R, K, J)
+        om2 = stage2_omega(second.seed, K * R, s2)
+        started = time.perf_counter()
+        A, M_local, rank_found, status = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings)
+        M = assemble_m(M_local, self.local_ids, K, R)
+        D, E, F = run_stage2(M, J, K * R, R, second.seed, s2, om2, status, timings=timings)
+        check_status(status, "compress")
+        dev = D.device
+        h, v, w = initial_factors(J, len(self.local_ids), R, opts.seed)
+        H, V = torch.from_numpy(h).to(dev), torch.from_numpy(v).to(dev)
+        W = torch.from_numpy(w).to(dev)
+        normalize = bool(opts.normalize) if opts.normalize is not None else True
+        ops = GpuAlsOps(local_rows(F, self.local_ids, R), D, E, H, V, W, J, R, opts.max_iters, opts.tol, normalize)
+        torch.cuda.synchronize()
+        pre = time.perf_counter() - started
+        ShardedALS(ops, nccl_allreduce()).run(opts.max_iters)
+        check_status(ops.status, "fit_dpar2")
+        n = int(ops.iters.item())
+        tr = FitTrace(objective=ops.trace[:n].cpu().tolist(),
+                      seconds=list(np.diff(ops.tstamp[:n + 1].cpu().numpy()) * 1e-9), preprocess_seconds=pre,
+                      compressed_float_count=self.total_rows * R + K * R * R + J * R + R)
+        if n >= 2:
+            prev, e = tr.objective[-2], tr.objective[-1]
+            tr.converged = bool(prev == 0.0 or abs(prev - e) <= opts.tol * prev)
+        from .compress import CompressedTensor
+        comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
+        Q = assemble_q(t, comp, ops.polar)
+        bounds = t.row_off_host
+        factors = Parafac2Factors(H=ops.H, V=ops.V, W=ops.W, Q=[Q[a:b] for a, b in zip(bounds[:-1], bounds[1:])],
+                                  Q_packed=Q)
+        return factors, tr

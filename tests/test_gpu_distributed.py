@@ -1,0 +1,59 @@
+"""The multi-GPU phase API (dp2_als_phase) on one GPU with virtual ranks: the
+slices are split into LPT shards, each shard runs the phases on its own
+slices, and the R x R partials are summed in rank order between phases --
+exactly what the NCCL allreduce does on N GPUs.  Must agree with the
+single-GPU graph path (fit_dpar2) to rounding."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_virtual_ranks_match_single_gpu(world):
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import distributed as D_, synth
+    from paper_2203_12798_b200.factors import initial_factors
+    from paper_2203_12798_b200.solver import run_als
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=40)
+    xs = synth.generate(cfg, 3)
+    t = dp.IrregularTensor(xs)
+    comp = dp.compress(t, 10)
+    K, J, R = t.num_slices, t.num_cols, 10
+    h, v, w = initial_factors(J, K, R)
+    H1, V1, W1, _, tr1, _ = run_als(comp, h, v, w, 16, 0.0, True)
+    shards, _ = D_.shard_slices(t.row_counts, world)
+    dev = comp.cores.device
+    ops = []
+    for ids in shards:
+        H = torch.from_numpy(h).to(dev)
+        V = torch.from_numpy(v).to(dev)
+        W = torch.from_numpy(w[ids]).to(dev)
+        ops.append(D_.GpuAlsOps(D_.local_rows(comp.cores, ids, R), comp.col_basis, comp.weights, H, V, W, J, R,
+                                16, 0.0, True))
+
+    class Virtual:
+        def phase(self, ph, it=0, red_in=None):
+            outs = [o.phase(ph, it=it, red_in=red_in) for o in ops]
+            return outs[0] if outs[0] is None else sum(outs[1:], outs[0].clone())
+
+    class Driver:
+        def __init__(self):
+            self.pending = None
+
+        def run(self, iters):
+            v = Virtual()
+            v.phase(0)
+            for it in range(iters):
+                for a, b in ((1, 2), (3, 4), (5, 6)):
+                    v.phase(b, it=it, red_in=v.phase(a, it=it))
+
+    Driver().run(16)
+    tr = ops[0].trace.cpu().numpy()
+    assert np.allclose(tr, tr1, rtol=1e-10, atol=0)
+    assert torch.allclose(ops[0].H, H1, rtol=0, atol=1e-9 * float(H1.abs().max()))
+    assert torch.allclose(ops[0].V, V1, rtol=0, atol=1e-9 * float(V1.abs().max()))
+    for o, ids in zip(ops, shards):
+        assert torch.allclose(o.W, W1[ids], rtol=0, atol=1e-9 * float(W1.abs().max()))
+        assert torch.equal(o.trace, ops[0].trace)
