@@ -761,7 +761,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
                               stream);
     };
-    if ((size_t)J * sp * 8 <= 200 * 1024) {
+    if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) {
       e = small(0);
       if (e != cudaSuccess) return e;
     } else {

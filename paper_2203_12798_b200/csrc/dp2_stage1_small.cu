@@ -22,69 +22,71 @@ namespace dp2 {
 // ------------------------------------------------------------ orth (smem CGS2)
 __global__ void __launch_bounds__(256) orth_smem_kernel(const double* part, const int32_t* slice_piece,
                                                          const int32_t* s_k, int J, int sp, double* Q) {
-  extern __shared__ __align__(16) double qs[];  // J x sp
+  extern __shared__ __align__(16) double qs[];  // J x ld, ld = sp + 1 (odd: conflict-free column walks)
   __shared__ double h[32];
   __shared__ double red[32];
   const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
-  const int s = s_k[k];
+  const int s = s_k[k], ld = sp + 1;
   const int n = J * sp;
   for (int i = tid; i < n; i += nt) {
     double acc = 0.0;
     for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
-    qs[i] = acc;
+    qs[(i / sp) * ld + i % sp] = acc;
   }
   __syncthreads();
   for (int c = 0; c < s; ++c) {
     for (int attempt = 0;; ++attempt) {
       if (attempt > 0) {
         const int e = (c + attempt - 1) % J;
-        for (int i = tid; i < J; i += nt) qs[i * sp + c] = (i == e) ? 1.0 : 0.0;
+        for (int i = tid; i < J; i += nt) qs[i * ld + c] = (i == e) ? 1.0 : 0.0;
         __syncthreads();
       }
       for (int pass = 0; pass < 2; ++pass) {
         for (int i = warp; i < c; i += nw) {
           double acc = 0.0;
-          for (int r = lane; r < J; r += 32) acc = fma(qs[r * sp + i], qs[r * sp + c], acc);
+          for (int r = lane; r < J; r += 32) acc = fma(qs[r * ld + i], qs[r * ld + c], acc);
           acc = warp_sum(acc);
           if (lane == 0) h[i] = acc;
         }
         __syncthreads();
         for (int r = tid; r < J; r += nt) {
-          double acc = qs[r * sp + c];
-          for (int i = 0; i < c; ++i) acc = fma(-h[i], qs[r * sp + i], acc);
-          qs[r * sp + c] = acc;
+          double acc = qs[r * ld + c];
+          for (int i = 0; i < c; ++i) acc = fma(-h[i], qs[r * ld + i], acc);
+          qs[r * ld + c] = acc;
         }
         __syncthreads();
       }
       double part2 = 0.0;
-      for (int r = tid; r < J; r += nt) part2 = fma(qs[r * sp + c], qs[r * sp + c], part2);
+      for (int r = tid; r < J; r += nt) part2 = fma(qs[r * ld + c], qs[r * ld + c], part2);
       const double nrm2 = block_sum(part2, red);
       const bool ok = attempt == 0 ? (nrm2 > 1e-300) : (nrm2 > 0.25);
       if (ok || attempt > J + 1) {
         const double inv = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
-        for (int r = tid; r < J; r += nt) qs[r * sp + c] *= inv;
+        for (int r = tid; r < J; r += nt) qs[r * ld + c] *= inv;
         __syncthreads();
         break;
       }
     }
   }
   double* Qk = Q + (size_t)k * n;
-  for (int i = tid; i < n; i += nt) Qk[i] = qs[i];
+  for (int i = tid; i < n; i += nt) Qk[i] = qs[(i / sp) * ld + i % sp];
 }
 
 // ------------------------------------------------------------ gather
 __global__ void __launch_bounds__(256) gather_kernel(const double* part, const double* gpart,
                                                       const int32_t* slice_piece, int J, int sp, double* Ct,
                                                       double* CCg, double* Gg) {
+  extern __shared__ __align__(16) double cs_[];  // J x (sp + 1)
   const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
-  const int n = J * sp;
+  const int n = J * sp, ld = sp + 1;
   double* C = Ct + (size_t)k * n;
   for (int i = tid; i < n; i += nt) {
     double acc = 0.0;
     for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
     C[i] = acc;
+    cs_[(i / sp) * ld + i % sp] = acc;
   }
   for (int e = tid; e < sp * sp; e += nt) {
     double acc = 0.0;
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* part, const d
     while (rem >= sp - a) { rem -= sp - a; ++a; }
     const int b = a + rem;
     double acc = 0.0;
-    for (int j = lane; j < J; j += 32) acc = fma(C[j * sp + a], C[j * sp + b], acc);
+    for (int j = lane; j < J; j += 32) acc = fma(cs_[j * ld + a], cs_[j * ld + b], acc);
     acc = warp_sum(acc);
     if (lane == 0) {
       CCg[(size_t)k * sp * sp + a * sp + b] = acc;
@@ -398,13 +400,16 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
-    const size_t qb = (size_t)J * sp * 8;
+    const size_t qb = (size_t)J * (sp + 1) * 8;
     e = cudaFuncSetAttribute(orth_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb);
     if (e != cudaSuccess) return e;
     orth_smem_kernel<<<K, 256, qb, stream>>>(part1, st->slice_piece, s_dev, J, sp, qz);
     return cudaGetLastError();
   }
-  gather_kernel<<<K, 256, 0, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
+  const size_t gb = (size_t)J * (sp + 1) * 8;
+  e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+  if (e != cudaSuccess) return e;
+  gather_kernel<<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
   const int wpb = sp <= 24 ? 4 : 2;
   const size_t fs = wpb * small_factor_smem(sp);
   e = cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
