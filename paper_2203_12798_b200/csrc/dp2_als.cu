@@ -30,6 +30,7 @@ struct AlsBufs {
   int wpb;       // warps per block
   int nb;        // blocks == partial slots
   int nbm;       // metric kernel blocks (slots)
+  int nbr, wpbr; // rotate kernel blocks (slots of s_g1 / s_wtw) and warps per block
 };
 
 __host__ __device__ inline int wpb_for(int R) { return R <= 16 ? 8 : (R <= 32 ? 4 : 1); }
@@ -332,6 +333,226 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
   }
 }
 
+// Rotation kernel with compile-time R (R <= 16): lane groups of G = ceil(R/2)
+// lanes each own one slice, so a warp solves floor(32/G) slices at once (6 at
+// R = 10) and every lane of a group drives one Jacobi pair per round.  Same
+// math, ordering and thresholds as als_rotate_kernel.
+template <int R>
+__host__ __device__ constexpr int grp_lanes() { return (R + 1) / 2; }
+template <int R>
+__host__ __device__ constexpr int grp_per_warp() { return 32 / grp_lanes<R>(); }
+template <int R>
+__host__ __device__ constexpr int grp_doubles() { return 2 * R * (R | 1) + 5 * R * R + 5 * R; }
+
+template <int R>
+__global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsBufs b, int wpb_r) {
+  if (b.ctl[0]) return;
+  constexpr int G = grp_lanes<R>(), NG = grp_per_warp<R>(), LDT = R | 1, PER = grp_doubles<R>();
+  constexpr int NE = R + (R & 1);
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int g = lane / G, gl = lane % G;
+  const bool lane_on = g < NG;
+  double* cc = sm;
+  double* Hs = cc + R * R;
+  double* gbase = sm + 2 * R * R + (size_t)wib * NG * PER;
+  double* Ts = gbase + (size_t)(lane_on ? g : 0) * PER;
+  double* Vr = Ts + R * LDT;
+  double* Fs = Vr + R * LDT;
+  double* Th = Fs + R * R;
+  double* Pi = Th + R * R;
+  double* acc1 = Pi + R * R;
+  double* acc2 = acc1 + R * R;
+  double* nrm = acc2 + R * R;  // R (+ 4R scratch)
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    cc[e] = b.cc[e];
+    Hs[e] = a.H[e];
+  }
+  __syncthreads();
+  if (lane_on)
+    for (int e = gl; e < R * R; e += G) { acc1[e] = 0.0; acc2[e] = 0.0; }
+  const bool warm = a.warm && b.ctl[1];
+  const int64_t gw = (int64_t)blockIdx.x * wpb_r + wib, nwr = (int64_t)gridDim.x * wpb_r;
+  for (int64_t k0 = gw * NG; k0 < a.K; k0 += nwr * NG) {
+    const int64_t k = k0 + g;
+    const bool has = lane_on && k < a.K;
+    const double* wk = a.W + (has ? k : 0) * R;
+    if (has) {
+      for (int e = gl; e < R * R; e += G) {
+        Fs[e] = a.F[k * R * R + e];
+        const int i = e / R, d = e % R;
+        Vr[i * LDT + d] = warm ? b.pprev[k * R * R + e] : (i == d ? 1.0 : 0.0);
+      }
+    }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {  // Th = (F_k cc) * w_k
+        const int i = e / R, c = e % R;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < R; ++q) s = fma(Fs[i * R + q], cc[q * R + c], s);
+        Th[e] = s * wk[c];
+      }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {  // Pi = T = Th H^T
+        const int i = e / R, d = e % R;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], Hs[d * R + c], s);
+        Pi[e] = s;
+      }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {  // Ts = T Vr (column-major)
+        const int c = e / R, i = e % R;
+        double s;
+        if (warm) {
+          s = 0.0;
+#pragma unroll
+          for (int d = 0; d < R; ++d) s = fma(Pi[i * R + d], Vr[c * LDT + d], s);
+        } else {
+          s = Pi[i * R + c];
+        }
+        Ts[c * LDT + i] = s;
+      }
+    __syncwarp();
+    // one-sided Jacobi: lane gl owns pair gl of every round
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+      int rotated = 0;
+      for (int r = 0; r < NE - 1; ++r) {
+        if (has && R > 1) {
+          int p, q;
+          rr_pair(NE, r, gl, p, q);
+          if (q < R) {
+            double* tp = Ts + p * LDT;
+            double* tq = Ts + q * LDT;
+            double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+            for (int i = 0; i < R; ++i) {
+              const double x = tp[i], y = tq[i];
+              al = fma(x, x, al);
+              be = fma(y, y, be);
+              ga = fma(x, y, ga);
+            }
+            if (ga != 0.0 && fabs(ga) > (R * kEps) * sqrt(al * be)) {
+              const double ze = (be - al) / (2.0 * ga);
+              const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
+              const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
+              for (int i = 0; i < R; ++i) {
+                const double x = tp[i], y = tq[i];
+                tp[i] = c * x - s * y;
+                tq[i] = s * x + c * y;
+              }
+              double* vp = Vr + p * LDT;
+              double* vq = Vr + q * LDT;
+#pragma unroll
+              for (int i = 0; i < R; ++i) {
+                const double x = vp[i], y = vq[i];
+                vp[i] = c * x - s * y;
+                vq[i] = s * x + c * y;
+              }
+              rotated = 1;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (!__any_sync(0xffffffffu, rotated)) break;
+    }
+    if (sweep >= 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.status + ST_SWEEPCAP), 1ull);
+    if (has)
+      for (int i = gl; i < R; i += G) {
+        double s = 0.0;
+#pragma unroll
+        for (int x = 0; x < R; ++x) s = fma(Ts[i * LDT + x], Ts[i * LDT + x], s);
+        nrm[i] = sqrt(s);
+      }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {
+        const int i = e / R, x = e % R;
+        const double n = nrm[i];
+        Ts[i * LDT + x] = n > 1e-300 ? Ts[i * LDT + x] / n : 0.0;
+      }
+    __syncwarp();
+    if (has && gl == 0) {  // exact-zero singular directions: orthonormal completion
+      for (int i = 0; i < R; ++i) {
+        if (nrm[i] > 1e-300) continue;
+        for (int t = 0; t < R; ++t) {
+          double* z = Ts + i * LDT;
+          for (int x = 0; x < R; ++x) z[x] = (x == t) ? 1.0 : 0.0;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int c = 0; c < R; ++c) {
+              if (c == i || !(nrm[c] > 1e-300)) continue;
+              double d = 0.0;
+              for (int x = 0; x < R; ++x) d = fma(Ts[c * LDT + x], z[x], d);
+              for (int x = 0; x < R; ++x) z[x] = fma(-d, Ts[c * LDT + x], z[x]);
+            }
+          double n2 = 0.0;
+          for (int x = 0; x < R; ++x) n2 = fma(z[x], z[x], n2);
+          if (n2 > 0.25) {
+            const double inv = 1.0 / sqrt(n2);
+            for (int x = 0; x < R; ++x) z[x] *= inv;
+            nrm[i] = 1.0;
+            break;
+          }
+        }
+        if (!(nrm[i] > 1e-300)) status_min(a.status, ST_POLAR, k);
+      }
+    }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {  // Pi = Z P^T; keep P for the next warm start
+        const int x = e / R, d = e % R;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) s = fma(Ts[i * LDT + x], Vr[i * LDT + d], s);
+        Pi[e] = s;
+        b.pprev[k * R * R + e] = Vr[x * LDT + d];
+      }
+    __syncwarp();
+    if (has)
+      for (int e = gl; e < R * R; e += G) {  // Theta = Pi^T F
+        const int i = e / R, c = e % R;
+        double s = 0.0;
+#pragma unroll
+        for (int d = 0; d < R; ++d) s = fma(Pi[d * R + i], Fs[d * R + c], s);
+        Th[e] = s;
+        a.theta[k * R * R + e] = s;
+        if (a.polar) a.polar[k * R * R + e] = Pi[e];
+      }
+    __syncwarp();
+    if (has && a.mode1)
+      for (int e = gl; e < R * R; e += G) {
+        const int i = e / R, r = e % R;
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < R; ++q) s = fma(Th[i * R + q], cc[q * R + r], s);
+        acc1[e] += wk[r] * s;
+        acc2[e] += wk[i] * wk[r];
+      }
+    __syncwarp();
+  }
+  if (a.mode1) {
+    __syncthreads();
+    const double* g0 = sm + 2 * R * R;
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int w = 0; w < wpb_r; ++w)
+        for (int gg = 0; gg < NG; ++gg) {
+          const double* gb = g0 + ((size_t)w * NG + gg) * PER + 2 * R * LDT + 3 * R * R;
+          s1 += gb[e];
+          s2 += gb[R * R + e];
+        }
+      b.s_g1[(size_t)blockIdx.x * R * R + e] = s1;
+      b.s_wtw[(size_t)blockIdx.x * R * R + e] = s2;
+    }
+  }
+}
+
 // mode-1 partials from a given Theta stack (kernel-granular API)
 __global__ void als_mode1_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
@@ -577,7 +798,7 @@ struct SolveArgs {
   const double *D, *E;
   double *H, *V, *W;
   int64_t J;
-  int R, normalize, nslots;
+  int R, normalize, nslots, nslots_h;
   int64_t* status;
 };
 
@@ -593,8 +814,8 @@ __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
   double* Hn = Pv + R * R;
   double* cs = Hn + R * R;  // 3*(R/2+1)
   __shared__ double nrm[64];
-  reduce_slots_warp(b.s_g1, s.nslots, R * R, G1);
-  reduce_slots_warp(b.s_wtw, s.nslots, R * R, WtW);
+  reduce_slots_warp(b.s_g1, s.nslots_h, R * R, G1);
+  reduce_slots_warp(b.s_wtw, s.nslots_h, R * R, WtW);
   __syncthreads();
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     Mh[e] = WtW[e] * b.VtV[e];
@@ -724,6 +945,32 @@ int metric_blocks(int64_t K, int R) {
   return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
 }
 
+// compile-time-R rotation kernel configuration (R <= 16); nbr = 0 -> generic kernel
+template <int R>
+void rot_cfg_t(int64_t K, int& wpbr, int& nbr) {
+  constexpr int NG = grp_per_warp<R>();
+  const size_t per_warp = (size_t)NG * grp_doubles<R>() * 8;
+  wpbr = (int)(160 * 1024 / per_warp);
+  wpbr = wpbr < 1 ? 1 : (wpbr > 4 ? 4 : wpbr);
+  int64_t warps = (K + NG - 1) / NG;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  warps = warps < cap ? warps : cap;
+  nbr = (int)((warps + wpbr - 1) / wpbr);
+}
+void rot_cfg(int64_t K, int R, int& wpbr, int& nbr) {
+  wpbr = 0;
+  nbr = 0;
+  switch (R) {
+#define DP2_ROT_CASE(N) \
+  case N: rot_cfg_t<N>(K, wpbr, nbr); break;
+    DP2_ROT_CASE(1) DP2_ROT_CASE(2) DP2_ROT_CASE(3) DP2_ROT_CASE(4) DP2_ROT_CASE(5) DP2_ROT_CASE(6)
+    DP2_ROT_CASE(7) DP2_ROT_CASE(8) DP2_ROT_CASE(9) DP2_ROT_CASE(10) DP2_ROT_CASE(11) DP2_ROT_CASE(12)
+    DP2_ROT_CASE(13) DP2_ROT_CASE(14) DP2_ROT_CASE(15) DP2_ROT_CASE(16)
+#undef DP2_ROT_CASE
+    default: break;
+  }
+}
+
 AlsLayout als_layout(int64_t K, int64_t J, int R) {
   AlsLayout L{};
   size_t off = 0;
@@ -741,8 +988,11 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.summed = take(RR);
   L.WtW2 = take(RR);
   L.L = take(K * RR * 2);
-  L.s_g1 = take(nb * RR);
-  L.s_wtw = take(nb * RR);
+  int wr = 0, nr = 0;
+  rot_cfg(K, R, wr, nr);
+  const size_t ns = nr > (int)nb ? (size_t)nr : nb;
+  L.s_g1 = take(ns * RR);
+  L.s_wtw = take(ns * RR);
   L.s_m2 = take(nb * RR);
   L.s_wtw2 = take(nb * RR);
   L.s_e = take(nbm * 8);
@@ -781,6 +1031,8 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.wpb = wpb_for(R);
   b.nb = b.nwt / b.wpb;
   b.nbm = metric_blocks(K, R);
+  rot_cfg(K, R, b.wpbr, b.nbr);
+  if (b.nbr <= 0) { b.nbr = b.nb; b.wpbr = b.wpb; }
   return b;
 }
 
@@ -817,6 +1069,33 @@ cudaError_t launch_metric(const AlsBufs& b, const double* D, const double* V, in
   return cudaGetLastError();
 }
 
+template <int R>
+size_t rot_group_smem(int wpbr) { return ((size_t)2 * R * R + (size_t)wpbr * grp_per_warp<R>() * grp_doubles<R>()) * 8; }
+
+template <int R>
+cudaError_t rotate_t(const SliceArgs& a, const AlsBufs& b, cudaStream_t st, bool setattr) {
+  const size_t sm = rot_group_smem<R>(b.wpbr);
+  if (setattr) return set_smem((const void*)als_rotate_group_kernel<R>, sm);
+  als_rotate_group_kernel<R><<<b.nbr, 32 * b.wpbr, sm, st>>>(a, b, b.wpbr);
+  return cudaGetLastError();
+}
+
+// rotation step: compile-time-R lane-group kernel for R <= 16, else generic
+cudaError_t launch_rotate(const SliceArgs& a, const AlsBufs& b, cudaStream_t st, bool setattr = false) {
+  switch (a.R) {
+#define DP2_ROT_CASE(N) \
+  case N: return rotate_t<N>(a, b, st, setattr);
+    DP2_ROT_CASE(1) DP2_ROT_CASE(2) DP2_ROT_CASE(3) DP2_ROT_CASE(4) DP2_ROT_CASE(5) DP2_ROT_CASE(6)
+    DP2_ROT_CASE(7) DP2_ROT_CASE(8) DP2_ROT_CASE(9) DP2_ROT_CASE(10) DP2_ROT_CASE(11) DP2_ROT_CASE(12)
+    DP2_ROT_CASE(13) DP2_ROT_CASE(14) DP2_ROT_CASE(15) DP2_ROT_CASE(16)
+#undef DP2_ROT_CASE
+    default:
+      if (setattr) return set_smem((const void*)als_rotate_kernel, rotate_smem(a.R, b.wpb));
+      als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(a.R, b.wpb), st>>>(a, b);
+      return cudaGetLastError();
+  }
+}
+
 cudaError_t prepare(int R, const AlsBufs& b) {
   cudaError_t e = set_smem((const void*)als_rotate_kernel, rotate_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode2_kernel, acc2_smem(R, b.wpb));
@@ -824,6 +1103,11 @@ cudaError_t prepare(int R, const AlsBufs& b) {
   if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, solve_smem(R));
+  if (e == cudaSuccess) {
+    SliceArgs a{};
+    a.R = R;
+    e = launch_rotate(a, b, nullptr, true);
+  }
   return e;
 }
 
@@ -833,7 +1117,8 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   SliceArgs a = base;
   a.mode1 = 1;
   a.warm = 1;
-  als_rotate_kernel<<<b.nb, nt, rotate_smem(R, b.wpb), st>>>(a, b);
+  cudaError_t e0 = launch_rotate(a, b, st);
+  if (e0 != cudaSuccess) return e0;
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
@@ -875,6 +1160,7 @@ SolveArgs solve_args(const double* D, const double* E, double* H, double* V, dou
   sv.R = R;
   sv.normalize = normalize;
   sv.nslots = b.nb;
+  sv.nslots_h = b.nbr;
   sv.status = status;
   return sv;
 }
@@ -937,8 +1223,7 @@ cudaError_t als_rotations(const double* F, const double* D, const double* E, int
   cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
-  als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(R, b.wpb), st>>>(a, b);
-  return cudaGetLastError();
+  return launch_rotate(a, b, st);
 }
 
 cudaError_t als_mttkrp(int mode, const double* theta, const double* D, const double* E, int64_t K,
@@ -978,6 +1263,7 @@ cudaError_t als_update_factors(const double* theta, const double* D, const doubl
   const int nt = 32 * b.wpb;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
   als_mode1_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
+  sv.nslots_h = b.nb;
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
@@ -1036,14 +1322,15 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
     case 1:
       a.mode1 = 1;
       a.warm = 1;
-      als_rotate_kernel<<<b.nb, nt, rotate_smem(R, b.wpb), st>>>(a, b);
-      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_g1, b.nb, (int64_t)RR, red_out);
-      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_wtw, b.nb, (int64_t)RR, red_out + RR);
+      e = launch_rotate(a, b, st);
+      if (e != cudaSuccess) return e;
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_g1, b.nbr, (int64_t)RR, red_out);
+      reduce_parts_dev<<<1, 256, 0, st>>>(b.s_wtw, b.nbr, (int64_t)RR, red_out + RR);
       break;
     case 2:
       cudaMemcpyAsync(b.s_g1, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
-      sv.nslots = 1;
+      sv.nslots_h = 1;
       als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
       break;
     case 3:
