@@ -344,6 +344,12 @@ __host__ __device__ constexpr int grp_per_warp() { return 32 / grp_lanes<R>(); }
 template <int R>
 __host__ __device__ constexpr int grp_doubles() { return 2 * R * (R | 1) + 5 * R * R + 5 * R; }
 
+// lane gl of a G-lane group visits elements gl, gl+G, ... of an R x R block;
+// fully unrolled so the independent outputs overlap their smem latencies
+#define DP2_GROUP_LOOP(e) \
+  _Pragma("unroll") for (int e##_it = 0; e##_it < (R * R + G - 1) / G; ++e##_it) \
+    if (const int e = gl + e##_it * G; e < R * R)
+
 template <int R>
 __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsBufs b, int wpb_r) {
   if (b.ctl[0]) return;
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
   }
   __syncthreads();
   if (lane_on)
-    for (int e = gl; e < R * R; e += G) { acc1[e] = 0.0; acc2[e] = 0.0; }
+    DP2_GROUP_LOOP(e) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const bool warm = a.warm && b.ctl[1];
   const int64_t gw = (int64_t)blockIdx.x * wpb_r + wib, nwr = (int64_t)gridDim.x * wpb_r;
   for (int64_t k0 = gw * NG; k0 < a.K; k0 += nwr * NG) {
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
     const bool has = lane_on && k < a.K;
     const double* wk = a.W + (has ? k : 0) * R;
     if (has) {
-      for (int e = gl; e < R * R; e += G) {
+      DP2_GROUP_LOOP(e) {
         Fs[e] = a.F[k * R * R + e];
         const int i = e / R, d = e % R;
         Vr[i * LDT + d] = warm ? b.pprev[k * R * R + e] : (i == d ? 1.0 : 0.0);
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
     }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {  // Th = (F_k cc) * w_k
+      DP2_GROUP_LOOP(e) {  // Th = (F_k cc) * w_k
         const int i = e / R, c = e % R;
         double s = 0.0;
 #pragma unroll
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
       }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {  // Pi = T = Th H^T
+      DP2_GROUP_LOOP(e) {  // Pi = T = Th H^T
         const int i = e / R, d = e % R;
         double s = 0.0;
 #pragma unroll
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
       }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {  // Ts = T Vr (column-major)
+      DP2_GROUP_LOOP(e) {  // Ts = T Vr (column-major)
         const int c = e / R, i = e % R;
         double s;
         if (warm) {
@@ -436,10 +442,9 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
               be = fma(y, y, be);
               ga = fma(x, y, ga);
             }
-            if (ga != 0.0 && fabs(ga) > (R * kEps) * sqrt(al * be)) {
-              const double ze = (be - al) / (2.0 * ga);
-              const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
-              const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+            if (ga != 0.0 && ga * ga > (R * kEps) * (R * kEps) * (al * be)) {
+              double c, s;
+              rot_params(be - al, ga, c, s);
 #pragma unroll
               for (int i = 0; i < R; ++i) {
                 const double x = tp[i], y = tq[i];
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
       }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {
+      DP2_GROUP_LOOP(e) {
         const int i = e / R, x = e % R;
         const double n = nrm[i];
         Ts[i * LDT + x] = n > 1e-300 ? Ts[i * LDT + x] / n : 0.0;
@@ -505,7 +510,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
     }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {  // Pi = Z P^T; keep P for the next warm start
+      DP2_GROUP_LOOP(e) {  // Pi = Z P^T; keep P for the next warm start
         const int x = e / R, d = e % R;
         double s = 0.0;
 #pragma unroll
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
       }
     __syncwarp();
     if (has)
-      for (int e = gl; e < R * R; e += G) {  // Theta = Pi^T F
+      DP2_GROUP_LOOP(e) {  // Theta = Pi^T F
         const int i = e / R, c = e % R;
         double s = 0.0;
 #pragma unroll
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
       }
     __syncwarp();
     if (has && a.mode1)
-      for (int e = gl; e < R * R; e += G) {
+      DP2_GROUP_LOOP(e) {
         const int i = e / R, r = e % R;
         double s = 0.0;
 #pragma unroll
@@ -558,7 +563,7 @@ __global__ void als_mode1_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
-  const size_t wstride = 2 * (size_t)R * R;
+  const size_t wstride = 3 * (size_t)R * R;
   double* wbase = sm + cta_shared_doubles(R);
   double* acc1 = wbase + wib * wstride;
   double* acc2 = acc1 + R * R;
@@ -586,15 +591,17 @@ __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
-  const size_t wstride = 2 * (size_t)R * R;
+  const size_t wstride = 3 * (size_t)R * R;
   double* wbase = sm + cta_shared_doubles(R);
   double* acc1 = wbase + wib * wstride;
   double* acc2 = acc1 + R * R;
+  double* Th = acc2 + R * R;  // Theta_k staged in smem
   load_cta_common(a, b, cs, true, false);
   for (int e = lane; e < R * R; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const int gw = blockIdx.x * b.wpb + wib;
   for (int64_t k = gw; k < a.K; k += b.nwt) {
-    const double* Th = a.theta + k * R * R;
+    for (int e = lane; e < R * R; e += 32) Th[e] = a.theta[k * R * R + e];
+    __syncwarp();
     const double* wk = a.W + k * R;
     for (int e = lane; e < R * R; e += 32) {
       const int ai = e / R, r = e % R;
@@ -604,6 +611,7 @@ __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
       acc1[e] += wr * s;
       acc2[e] += wa * wr;
     }
+    __syncwarp();
   }
   __syncthreads();
   combine_warps(wbase, wstride, b.wpb, R * R, b.s_m2 + (size_t)blockIdx.x * R * R);
@@ -616,13 +624,15 @@ __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
   extern __shared__ __align__(16) double sm[];
   const int R = a.R, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   CtaShared cs = carve_cta(sm, R);
-  double* g3 = sm + cta_shared_doubles(R) + (size_t)wib * 2 * R;
+  double* g3 = sm + cta_shared_doubles(R) + (size_t)wib * ((size_t)R * R + 2 * R);
   double* wn = g3 + R;
+  double* Th = wn + R;  // Theta_k staged in smem
   load_cta_common(a, b, cs, true, a.write_w != 0);
   const int gw = blockIdx.x * b.wpb + wib;
   const int ldl = 2 * R;
   for (int64_t k = gw; k < a.K; k += b.nwt) {
-    const double* Th = a.theta + k * R * R;
+    for (int e = lane; e < R * R; e += 32) Th[e] = a.theta[k * R * R + e];
+    __syncwarp();
     // G3[r] = sum_i H[i][r] sum_j Theta[i][j] cc[j][r]   (P/solver.py:109-111)
     for (int r = lane; r < R; r += 32) {
       double s = 0.0;
@@ -798,7 +808,7 @@ struct SolveArgs {
   const double *D, *E;
   double *H, *V, *W;
   int64_t J;
-  int R, normalize, nslots, nslots_h;
+  int R, normalize, nslots, nslots_h, dsm;
   int64_t* status;
 };
 
@@ -876,37 +886,46 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   }
   __syncthreads();
   block_pinv_sym(Mv, U, Pv, R, cs, s.status);
-  // G2 = D (E * summed) (P/solver.py:100) into b.G2
-  for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
-    const int64_t j = e / R;
-    const int r = (int)(e % R);
-    double t = 0.0;
-    for (int q = 0; q < R; ++q) t = fma(s.D[j * R + q], es[q * R + r], t);
-    b.G2[e] = t;
+  // V = D (E * summed) pinv = D EP with EP = (E * summed) pinv (R x R), so the
+  // J-sized work is one product; D and V stay in smem when they fit
+  double* EP = cs + 3 * (R / 2 + 1) + 8;
+  double* Ds = EP + R * R;
+  double* Vs = s.dsm ? Ds + J * R : b.G2;
+  const double* Dp = s.dsm ? Ds : s.D;
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int q = e / R, r = e % R;
+    double acc = 0.0;
+    for (int a2 = 0; a2 < R; ++a2) acc = fma(es[q * R + a2], Pv[a2 * R + r], acc);
+    EP[e] = acc;
   }
+  if (s.dsm)
+    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) Ds[e] = s.D[e];
   __syncthreads();
-  // V = G2 pinv
   for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
     const int64_t j = e / R;
     const int r = (int)(e % R);
     double acc = 0.0;
-    for (int a = 0; a < R; ++a) acc = fma(b.G2[j * R + a], Pv[a * R + r], acc);
-    s.V[e] = acc;
+    for (int q = 0; q < R; ++q) acc = fma(Dp[j * R + q], EP[q * R + r], acc);
+    Vs[e] = acc;
   }
   __syncthreads();
   {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int c = warp; c < R; c += nw) {
       double part = 0.0;
-      for (int64_t j = lane; j < J; j += 32) part = fma(s.V[j * R + c], s.V[j * R + c], part);
+      for (int64_t j = lane; j < J; j += 32) part = fma(Vs[j * R + c], Vs[j * R + c], part);
       const double n = sqrt(warp_sum(part));
       if (lane == 0) nrm[c] = (s.normalize && !(n < 1e-300)) ? n : 1.0;
     }
   }
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) s.V[e] = s.V[e] / nrm[e % R];
+  for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
+    const double v = Vs[e] / nrm[e % R];
+    Vs[e] = v;
+    s.V[e] = v;
+  }
   __syncthreads();
-  gram_dv_warps(s.D, s.E, s.V, J, R, b.cc, b.VtV, Mv, b.HtH);
+  gram_dv_warps(Dp, s.E, Vs, J, R, b.cc, b.VtV, Mv, b.HtH);
   __syncthreads();
   block_pinv_sym(Mv, U, b.pinv3, R, cs, s.status);
 }
@@ -1037,9 +1056,14 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
 }
 
 size_t rotate_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * warp_smem_doubles(R)) * 8; }
-size_t acc2_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 2 * (size_t)R * R) * 8; }
-size_t mode3_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 2 * (size_t)R) * 8; }
+size_t acc2_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 3 * (size_t)R * R) * 8; }
+size_t mode3_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * ((size_t)R * R + 2 * (size_t)R)) * 8; }
 size_t solve_smem(int R) { return (7 * (size_t)R * R + 3 * (R / 2 + 1) + 8) * 8; }
+// solve_v: + EP (R x R) + D, V (J x R each) when they fit in shared memory
+bool solve_v_dsm(int64_t J, int R) { return (solve_smem(R) + ((size_t)R * R + 2 * (size_t)J * R) * 8) <= 200 * 1024; }
+size_t solve_v_smem(int64_t J, int R) {
+  return solve_smem(R) + ((size_t)R * R + (solve_v_dsm(J, R) ? 2 * (size_t)J * R : 0)) * 8;
+}
 
 cudaError_t set_smem(const void* f, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
@@ -1102,7 +1126,7 @@ cudaError_t prepare(int R, const AlsBufs& b) {
   if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, acc2_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
-  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, solve_smem(R));
+  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, 227 * 1024);
   if (e == cudaSuccess) {
     SliceArgs a{};
     a.R = R;
@@ -1121,7 +1145,7 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   if (e0 != cudaSuccess) return e0;
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.write_l = 1;
   a.Wout = sv.W;
@@ -1161,6 +1185,7 @@ SolveArgs solve_args(const double* D, const double* E, double* H, double* V, dou
   sv.normalize = normalize;
   sv.nslots = b.nb;
   sv.nslots_h = b.nbr;
+  sv.dsm = solve_v_dsm(J, R);
   sv.status = status;
   return sv;
 }
@@ -1266,7 +1291,7 @@ cudaError_t als_update_factors(const double* theta, const double* D, const doubl
   sv.nslots_h = b.nb;
   als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.Wout = W;
   als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
@@ -1342,7 +1367,7 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
       cudaMemcpyAsync(b.s_m2, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw2, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
       sv.nslots = 1;
-      als_solve_v_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
+      als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
       break;
     case 5:
       a.write_w = 1;

@@ -90,6 +90,35 @@ DP2_DEV void rr_pair(int n_even, int r, int i, int& p, int& q) {
   if (p > q) { int t = p; p = q; q = t; }
 }
 
+// ---------------------------------------------------------------- rotations
+// Jacobi rotation (c, s) annihilating g for the 2x2 symmetric problem with
+// diagonal difference d (= b - a): t = sgn(d) 2g / (|d| + sqrt(d^2 + 4g^2)).
+// The angle is estimated in fp32 on the scaled pair (any angle that shrinks g
+// keeps the sweep converging); (c, s) are then made orthonormal to fp64
+// precision: c = (1 + t^2)^(-1/2) by two Newton steps, s = c t.  This keeps the
+// accumulated rotations exactly orthogonal while avoiding the fp64 div/sqrt
+// sequences on the latency-critical path.
+DP2_DEV void rot_params(double d, double g, double& c, double& s) {
+  const float df = (float)d, gf = (float)(2.0 * g);
+  const float m = fmaxf(fabsf(df), fabsf(gf));
+  double t;
+  if (m > 1e-30f && m < 1e30f) {
+    const float inv = __frcp_rn(m);
+    const float dn = df * inv, gn = gf * inv;
+    const float tf = (dn >= 0.0f ? gn : -gn) * __frcp_rn(fabsf(dn) + sqrtf(fmaf(dn, dn, gn * gn)));
+    t = (double)tf;
+  } else {  // out of fp32 range: exact fp64 formula
+    const double ze = d / (2.0 * g);
+    t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
+  }
+  const double x = fma(t, t, 1.0);
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  c = r;
+  s = r * t;
+}
+
 // ---------------------------------------------------------------- Jacobi eig
 // Block-cooperative cyclic Jacobi for a symmetric n x n matrix A (row-major,
 // leading dim lda, shared memory).  On return diag(A) holds the eigenvalues and
@@ -116,11 +145,8 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
         double c = 1.0, s = 0.0;
         if (q < n) {
           const double apq = A[p * lda + q], app = A[p * lda + p], aqq = A[q * lda + q];
-          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
-            const double th = (aqq - app) / (2.0 * apq);
-            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
+          if (apq != 0.0 && apq * apq > (tol * tol) * fabs(app * aqq)) {
+            rot_params(aqq - app, apq, c, s);
             *flag = 1;
           }
         }
@@ -192,11 +218,8 @@ DP2_DEV int jacobi_eig_warp(double* A, int lda, double* V, int ldv, int n, doubl
         double c = 1.0, s = 0.0;
         if (q < n) {
           const double apq = A[p * lda + q], app = A[p * lda + p], aqq = A[q * lda + q];
-          if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app * aqq))) {
-            const double th = (aqq - app) / (2.0 * apq);
-            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
+          if (apq != 0.0 && apq * apq > (tol * tol) * fabs(app * aqq)) {
+            rot_params(aqq - app, apq, c, s);
             rotated = 1;
           }
         }
@@ -289,10 +312,9 @@ DP2_DEV int jacobi_onesided_warp(double* T, int ldt, double* Vr, int ldv, int n,
           be = fma(y, y, be);
           ga = fma(x, y, ga);
         }
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-          const double ze = (be - al) / (2.0 * ga);
-          const double t = (ze >= 0.0 ? 1.0 : -1.0) / (fabs(ze) + sqrt(ze * ze + 1.0));
-          const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        if (ga != 0.0 && ga * ga > (tol * tol) * (al * be)) {
+          double c, s;
+          rot_params(be - al, ga, c, s);
           for (int k = 0; k < n; ++k) {
             const double x = tp[k], y = tq[k];
             tp[k] = c * x - s * y;
