@@ -1126,7 +1126,7 @@ cudaError_t prepare(int R, const AlsBufs& b) {
   if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, acc2_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
-  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, 227 * 1024);
+  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, 200 * 1024);
   if (e == cudaSuccess) {
     SliceArgs a{};
     a.R = R;
