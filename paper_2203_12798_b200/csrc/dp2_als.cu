@@ -19,6 +19,7 @@
 // is one CUDA graph (P/solver.py:180-184 evaluated on the device).
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
+#include <cstdio>
 
 namespace dp2 {
 
@@ -1067,7 +1068,13 @@ size_t solve_v_smem(int64_t J, int R) {
 
 cudaError_t set_smem(const void* f, size_t bytes) {
   if (bytes <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), "dynamic smem attribute %zu bytes", bytes);
+    note_error(buf);
+  }
+  return e;
 }
 
 template <int KS>

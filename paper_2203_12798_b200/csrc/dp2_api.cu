@@ -11,6 +11,7 @@
 
 namespace {
 thread_local std::string g_last_error;
+thread_local std::string g_note;
 std::atomic<int64_t> g_launches{0};
 int ok(int64_t n) {
   g_launches += n;
@@ -18,7 +19,8 @@ int ok(int64_t n) {
 }
 
 int fail(cudaError_t e, const char* where) {
-  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e) + (g_note.empty() ? "" : " [" + g_note + "]");
+  g_note.clear();
   return DP2_ERR_CUDA;
 }
 int fail_arg(const char* msg) {
@@ -32,6 +34,10 @@ bool store_ok(const dp2_store* st) {
 }
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 }  // namespace
+
+namespace dp2 {
+void note_error(const char* what) { g_note = what; }
+}  // namespace dp2
 
 extern "C" {
 

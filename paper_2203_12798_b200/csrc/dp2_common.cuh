@@ -183,13 +183,6 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
         A[q * lda + j] = s * a + c * b;
       }
       __syncthreads();
-      for (int i = tid; i < np; i += nt) {
-        if (cs[3 * i + 1] == 0.0) continue;
-        const int pq = (int)cs[3 * i + 2], p = pq >> 10, q = pq & 1023;
-        A[p * lda + q] = 0.0;
-        A[q * lda + p] = 0.0;
-      }
-      __syncthreads();
     }
     const int any = *flag;
     __syncthreads();
@@ -252,13 +245,6 @@ DP2_DEV int jacobi_eig_warp(double* A, int lda, double* V, int ldv, int n, doubl
         const double a = A[p * lda + j], b = A[q * lda + j];
         A[p * lda + j] = c * a - s * b;
         A[q * lda + j] = s * a + c * b;
-      }
-      __syncwarp();
-      for (int i = lane; i < np; i += 32) {
-        if (cs[3 * i + 1] == 0.0) continue;
-        const int pq = (int)cs[3 * i + 2], p = pq >> 10, q = pq & 1023;
-        A[p * lda + q] = 0.0;
-        A[q * lda + p] = 0.0;
       }
       __syncwarp();
     }

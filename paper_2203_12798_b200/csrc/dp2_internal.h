@@ -9,6 +9,9 @@
 
 namespace dp2 {
 
+// detail appended to the next dp2_last_error() message
+void note_error(const char* what);
+
 struct Stage1Layout {
   size_t part, qz, y2, Pm, Sv, Vt, cand_abs, cand_row, cand_neg, xsq, scr, gpart, CCg, Gg, sgn, total;
 };
