@@ -334,205 +334,175 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
   }
 }
 
-// Rotation kernel with compile-time R (R <= 16): lane groups of G = ceil(R/2)
-// lanes each own one slice, so a warp solves floor(32/G) slices at once (6 at
-// R = 10) and every lane of a group drives one Jacobi pair per round.  Same
-// math, ordering and thresholds as als_rotate_kernel.
+// Rotation kernel with compile-time R (R <= 16), one warp per slice.
+// Warm iterations solve the polar factor by Newton-Schulz from the previous
+// iteration's Pi_prev:  M = Pi_prev^T T, X0 = M sym(M)^-1 (close to
+// orthogonal when T moved little), X <- X (3I - X^T X) / 2 until the update
+// is < 3e-8 (quadratic: the last iterate is converged to rounding), then
+// Pi = Pi_prev X -- the unique orthogonal polar factor of the nonsingular T,
+// i.e. the reference's Z_k P_k^T (P/solver.py:59).  Iteration 0, a singular
+// sym(M) or a non-converging start fall back to one-sided Jacobi (warp_polar).
 template <int R>
-__host__ __device__ constexpr int grp_lanes() { return (R + 1) / 2; }
+__host__ __device__ constexpr int grp_doubles() { return 13 * R * R + 2 * R * (R | 1) + 8 * R; }
 template <int R>
-__host__ __device__ constexpr int grp_per_warp() { return 32 / grp_lanes<R>(); }
-template <int R>
-__host__ __device__ constexpr int grp_doubles() { return 2 * R * (R | 1) + 5 * R * R + 5 * R; }
+__host__ __device__ constexpr int grp_per_warp() { return 1; }
 
-// lane gl of a G-lane group visits elements gl, gl+G, ... of an R x R block;
-// fully unrolled so the independent outputs overlap their smem latencies
-#define DP2_GROUP_LOOP(e) \
-  _Pragma("unroll") for (int e##_it = 0; e##_it < (R * R + G - 1) / G; ++e##_it) \
-    if (const int e = gl + e##_it * G; e < R * R)
+// C = op(A) op(B) for R x R row-major smem matrices; lanes over outputs
+template <int R, bool TA, bool TB>
+DP2_DEV void wmm(const double* A, const double* B, double* C) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int it = 0; it < (R * R + 31) / 32; ++it) {
+    const int e = lane + 32 * it;
+    if (e < R * R) {
+      const int i = e / R, j = e % R;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) s = fma(TA ? A[q * R + i] : A[i * R + q], TB ? B[j * R + q] : B[q * R + j], s);
+      C[e] = s;
+    }
+  }
+  __syncwarp();
+}
+
+// Gauss-Jordan inverse with partial pivoting of the R x R matrix in aug[:, :R]
+// (aug is R x 2R); result in aug[:, R:].  Returns false on a zero pivot.
+template <int R>
+DP2_DEV bool wgj_inverse(double* aug, double* fac) {
+  const int lane = threadIdx.x & 31;
+  constexpr int W = 2 * R;
+#pragma unroll
+  for (int it = 0; it < (R * R + 31) / 32; ++it) {
+    const int e = lane + 32 * it;
+    if (e < R * R) aug[(e / R) * W + R + e % R] = (e / R == e % R) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  for (int c = 0; c < R; ++c) {
+    double best = lane >= c && lane < R ? fabs(aug[lane * W + c]) : -1.0;
+    int bi = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (!(best > 0.0)) return false;
+    if (bi != c)
+      for (int j = lane; j < W; j += 32) {
+        const double t = aug[c * W + j];
+        aug[c * W + j] = aug[bi * W + j];
+        aug[bi * W + j] = t;
+      }
+    __syncwarp();
+    const double inv = 1.0 / aug[c * W + c];
+    if (lane < R) fac[lane] = aug[lane * W + c];
+    __syncwarp();
+    for (int j = lane; j < W; j += 32) aug[c * W + j] *= inv;
+    __syncwarp();
+    for (int e = lane; e < R * W; e += 32) {
+      const int i = e / W, j = e % W;
+      if (i != c) aug[e] = fma(-fac[i], aug[c * W + j], aug[e]);
+    }
+    __syncwarp();
+  }
+  return true;
+}
 
 template <int R>
 __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsBufs b, int wpb_r) {
   if (b.ctl[0]) return;
-  constexpr int G = grp_lanes<R>(), NG = grp_per_warp<R>(), LDT = R | 1, PER = grp_doubles<R>();
-  constexpr int NE = R + (R & 1);
+  constexpr int LDT = R | 1, PER = grp_doubles<R>(), RR = R * R;
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int g = lane / G, gl = lane % G;
-  const bool lane_on = g < NG;
   double* cc = sm;
-  double* Hs = cc + R * R;
-  double* gbase = sm + 2 * R * R + (size_t)wib * NG * PER;
-  double* Ts = gbase + (size_t)(lane_on ? g : 0) * PER;
+  double* Hs = cc + RR;
+  double* base = sm + 2 * RR + (size_t)wib * PER;
+  double* Fs = base;
+  double* Th = Fs + RR;
+  double* T = Th + RR;
+  double* Pp = T + RR;
+  double* X = Pp + RR;
+  double* Y = X + RR;
+  double* Pi = Y + RR;
+  double* aug = Pi + RR;      // R x 2R
+  double* acc1 = aug + 2 * RR;
+  double* acc2 = acc1 + RR;
+  double* Ts = acc2 + RR;     // Jacobi fallback: R x LDT each
   double* Vr = Ts + R * LDT;
-  double* Fs = Vr + R * LDT;
-  double* Th = Fs + R * R;
-  double* Pi = Th + R * R;
-  double* acc1 = Pi + R * R;
-  double* acc2 = acc1 + R * R;
-  double* nrm = acc2 + R * R;  // R (+ 4R scratch)
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+  double* tmp = Vr + R * LDT;  // 8R
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
     cc[e] = b.cc[e];
     Hs[e] = a.H[e];
   }
   __syncthreads();
-  if (lane_on)
-    DP2_GROUP_LOOP(e) { acc1[e] = 0.0; acc2[e] = 0.0; }
+  for (int e = lane; e < RR; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
   const bool warm = a.warm && b.ctl[1];
   const int64_t gw = (int64_t)blockIdx.x * wpb_r + wib, nwr = (int64_t)gridDim.x * wpb_r;
-  for (int64_t k0 = gw * NG; k0 < a.K; k0 += nwr * NG) {
-    const int64_t k = k0 + g;
-    const bool has = lane_on && k < a.K;
-    const double* wk = a.W + (has ? k : 0) * R;
-    if (has) {
-      DP2_GROUP_LOOP(e) {
-        Fs[e] = a.F[k * R * R + e];
-        const int i = e / R, d = e % R;
-        Vr[i * LDT + d] = warm ? b.pprev[k * R * R + e] : (i == d ? 1.0 : 0.0);
-      }
+  for (int64_t k = gw; k < a.K; k += nwr) {
+    const double* wk = a.W + k * R;
+    for (int e = lane; e < RR; e += 32) {
+      Fs[e] = a.F[k * RR + e];
+      if (warm) Pp[e] = b.pprev[k * RR + e];
     }
     __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {  // Th = (F_k cc) * w_k
-        const int i = e / R, c = e % R;
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) s = fma(Fs[i * R + q], cc[q * R + c], s);
-        Th[e] = s * wk[c];
-      }
+    wmm<R, false, false>(Fs, cc, Th);  // Th = F_k cc
+    for (int e = lane; e < RR; e += 32) Th[e] *= wk[e % R];
     __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {  // Pi = T = Th H^T
-        const int i = e / R, d = e % R;
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], Hs[d * R + c], s);
-        Pi[e] = s;
+    wmm<R, false, true>(Th, Hs, T);  // T = Th H^T
+    bool done = false;
+    if (warm) {
+      wmm<R, true, false>(Pp, T, X);  // M = Pi_prev^T T
+      for (int e = lane; e < RR; e += 32) {
+        const int i = e / R, j = e % R;
+        aug[i * 2 * R + j] = 0.5 * (X[i * R + j] + X[j * R + i]);
       }
-    __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {  // Ts = T Vr (column-major)
-        const int c = e / R, i = e % R;
-        double s;
-        if (warm) {
-          s = 0.0;
-#pragma unroll
-          for (int d = 0; d < R; ++d) s = fma(Pi[i * R + d], Vr[c * LDT + d], s);
-        } else {
-          s = Pi[i * R + c];
-        }
-        Ts[c * LDT + i] = s;
-      }
-    __syncwarp();
-    // one-sided Jacobi: lane gl owns pair gl of every round
-    int sweep = 0;
-    for (; sweep < 60; ++sweep) {
-      int rotated = 0;
-      for (int r = 0; r < NE - 1; ++r) {
-        if (has && R > 1) {
-          int p, q;
-          rr_pair(NE, r, gl, p, q);
-          if (q < R) {
-            double* tp = Ts + p * LDT;
-            double* tq = Ts + q * LDT;
-            double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-            for (int i = 0; i < R; ++i) {
-              const double x = tp[i], y = tq[i];
-              al = fma(x, x, al);
-              be = fma(y, y, be);
-              ga = fma(x, y, ga);
-            }
-            if (ga != 0.0 && ga * ga > (R * kEps) * (R * kEps) * (al * be)) {
-              double c, s;
-              rot_params(be - al, ga, c, s);
-#pragma unroll
-              for (int i = 0; i < R; ++i) {
-                const double x = tp[i], y = tq[i];
-                tp[i] = c * x - s * y;
-                tq[i] = s * x + c * y;
-              }
-              double* vp = Vr + p * LDT;
-              double* vq = Vr + q * LDT;
-#pragma unroll
-              for (int i = 0; i < R; ++i) {
-                const double x = vp[i], y = vq[i];
-                vp[i] = c * x - s * y;
-                vq[i] = s * x + c * y;
-              }
-              rotated = 1;
-            }
-          }
-        }
+      __syncwarp();
+      if (wgj_inverse<R>(aug, tmp)) {
+        for (int e = lane; e < RR; e += 32) Y[e] = aug[(e / R) * 2 * R + R + e % R];
         __syncwarp();
-      }
-      if (!__any_sync(0xffffffffu, rotated)) break;
-    }
-    if (sweep >= 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.status + ST_SWEEPCAP), 1ull);
-    if (has)
-      for (int i = gl; i < R; i += G) {
-        double s = 0.0;
-#pragma unroll
-        for (int x = 0; x < R; ++x) s = fma(Ts[i * LDT + x], Ts[i * LDT + x], s);
-        nrm[i] = sqrt(s);
-      }
-    __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {
-        const int i = e / R, x = e % R;
-        const double n = nrm[i];
-        Ts[i * LDT + x] = n > 1e-300 ? Ts[i * LDT + x] / n : 0.0;
-      }
-    __syncwarp();
-    if (has && gl == 0) {  // exact-zero singular directions: orthonormal completion
-      for (int i = 0; i < R; ++i) {
-        if (nrm[i] > 1e-300) continue;
-        for (int t = 0; t < R; ++t) {
-          double* z = Ts + i * LDT;
-          for (int x = 0; x < R; ++x) z[x] = (x == t) ? 1.0 : 0.0;
-          for (int pass = 0; pass < 2; ++pass)
-            for (int c = 0; c < R; ++c) {
-              if (c == i || !(nrm[c] > 1e-300)) continue;
-              double d = 0.0;
-              for (int x = 0; x < R; ++x) d = fma(Ts[c * LDT + x], z[x], d);
-              for (int x = 0; x < R; ++x) z[x] = fma(-d, Ts[c * LDT + x], z[x]);
-            }
-          double n2 = 0.0;
-          for (int x = 0; x < R; ++x) n2 = fma(z[x], z[x], n2);
-          if (n2 > 0.25) {
-            const double inv = 1.0 / sqrt(n2);
-            for (int x = 0; x < R; ++x) z[x] *= inv;
-            nrm[i] = 1.0;
-            break;
+        wmm<R, false, false>(X, Y, Pi);  // X0 = M sym(M)^-1 (into Pi)
+        double* Xc = Pi;
+        double* Xn = X;
+        for (int it = 0; it < 10; ++it) {
+          wmm<R, true, false>(Xc, Xc, Y);  // Y = X^T X
+          for (int e = lane; e < RR; e += 32) Y[e] = ((e / R == e % R) ? 1.5 : 0.0) - 0.5 * Y[e];
+          __syncwarp();
+          wmm<R, false, false>(Xc, Y, Xn);  // Xn = X (3I - X^T X) / 2
+          double d = 0.0;
+          for (int e = lane; e < RR; e += 32) {
+            const double t = Xn[e] - Xc[e];
+            d = fma(t, t, d);
           }
+          d = warp_sum(d);
+          double* t = Xc;
+          Xc = Xn;
+          Xn = t;
+          if (d < 9e-16) { done = true; break; }
         }
-        if (!(nrm[i] > 1e-300)) status_min(a.status, ST_POLAR, k);
+        if (done) {
+          wmm<R, false, false>(Pp, Xc, Y);  // Pi = Pi_prev X
+          for (int e = lane; e < RR; e += 32) Pi[e] = Y[e];
+          __syncwarp();
+        }
       }
     }
-    __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {  // Pi = Z P^T; keep P for the next warm start
-        const int x = e / R, d = e % R;
-        double s = 0.0;
-#pragma unroll
-        for (int i = 0; i < R; ++i) s = fma(Ts[i * LDT + x], Vr[i * LDT + d], s);
-        Pi[e] = s;
-        b.pprev[k * R * R + e] = Vr[x * LDT + d];
-      }
-    __syncwarp();
-    if (has)
-      DP2_GROUP_LOOP(e) {  // Theta = Pi^T F
+    if (!done) {  // cold start / fallback: one-sided Jacobi on T
+      for (int e = lane; e < RR; e += 32) {
         const int i = e / R, c = e % R;
-        double s = 0.0;
-#pragma unroll
-        for (int d = 0; d < R; ++d) s = fma(Pi[d * R + i], Fs[d * R + c], s);
-        Th[e] = s;
-        a.theta[k * R * R + e] = s;
-        if (a.polar) a.polar[k * R * R + e] = Pi[e];
+        Ts[c * LDT + i] = T[e];
+        Vr[c * LDT + i] = (i == c) ? 1.0 : 0.0;
       }
-    __syncwarp();
-    if (has && a.mode1)
-      DP2_GROUP_LOOP(e) {
+      __syncwarp();
+      warp_polar(Ts, Vr, LDT, R, Pi, tmp, a.status, k);
+    }
+    for (int e = lane; e < RR; e += 32) {
+      b.pprev[k * RR + e] = Pi[e];
+      if (a.polar) a.polar[k * RR + e] = Pi[e];
+    }
+    wmm<R, true, false>(Pi, Fs, Th);  // Theta = Pi^T F
+    for (int e = lane; e < RR; e += 32) a.theta[k * RR + e] = Th[e];
+    if (a.mode1)
+      for (int e = lane; e < RR; e += 32) {
         const int i = e / R, r = e % R;
         double s = 0.0;
 #pragma unroll
@@ -544,17 +514,16 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
   }
   if (a.mode1) {
     __syncthreads();
-    const double* g0 = sm + 2 * R * R;
-    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const double* g0 = sm + 2 * RR;
+    for (int e = threadIdx.x; e < RR; e += blockDim.x) {
       double s1 = 0.0, s2 = 0.0;
-      for (int w = 0; w < wpb_r; ++w)
-        for (int gg = 0; gg < NG; ++gg) {
-          const double* gb = g0 + ((size_t)w * NG + gg) * PER + 2 * R * LDT + 3 * R * R;
-          s1 += gb[e];
-          s2 += gb[R * R + e];
-        }
-      b.s_g1[(size_t)blockIdx.x * R * R + e] = s1;
-      b.s_wtw[(size_t)blockIdx.x * R * R + e] = s2;
+      for (int w = 0; w < wpb_r; ++w) {
+        const double* gb = g0 + (size_t)w * PER + 9 * RR;  // acc1 (acc2 follows)
+        s1 += gb[e];
+        s2 += gb[RR + e];
+      }
+      b.s_g1[(size_t)blockIdx.x * RR + e] = s1;
+      b.s_wtw[(size_t)blockIdx.x * RR + e] = s2;
     }
   }
 }
@@ -969,7 +938,7 @@ int metric_blocks(int64_t K, int R) {
 template <int R>
 void rot_cfg_t(int64_t K, int& wpbr, int& nbr) {
   constexpr int NG = grp_per_warp<R>();
-  const size_t per_warp = (size_t)NG * grp_doubles<R>() * 8;
+  const size_t per_warp = (size_t)NG * grp_doubles<R>() * 8 + 2 * R * R * 8;
   wpbr = (int)(160 * 1024 / per_warp);
   wpbr = wpbr < 1 ? 1 : (wpbr > 4 ? 4 : wpbr);
   int64_t warps = (K + NG - 1) / NG;
