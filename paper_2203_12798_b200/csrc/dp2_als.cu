@@ -334,14 +334,12 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
   }
 }
 
-// Rotation kernel with compile-time R (R <= 16), one warp per slice.
-// Warm iterations solve the polar factor by Newton-Schulz from the previous
-// iteration's Pi_prev:  M = Pi_prev^T T, X0 = M sym(M)^-1 (close to
-// orthogonal when T moved little), X <- X (3I - X^T X) / 2 until the update
-// is < 3e-8 (quadratic: the last iterate is converged to rounding), then
-// Pi = Pi_prev X -- the unique orthogonal polar factor of the nonsingular T,
-// i.e. the reference's Z_k P_k^T (P/solver.py:59).  Iteration 0, a singular
-// sym(M) or a non-converging start fall back to one-sided Jacobi (warp_polar).
+// Rotation kernel with compile-time R (R <= 16), one warp per slice: the polar
+// factor of T_k by the scaled Newton iteration (warp-parallel Gauss-Jordan
+// inverse per step, ~7 steps) -- the unique orthogonal polar factor of the
+// nonsingular T_k, i.e. the reference's Z_k P_k^T (P/solver.py:59).  A
+// singular T_k (zero pivot) falls back to one-sided Jacobi with orthonormal
+// completion (warp_polar).
 template <int R>
 __host__ __device__ constexpr int grp_doubles() { return 13 * R * R + 2 * R * (R | 1) + 8 * R; }
 template <int R>
@@ -449,41 +447,50 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
     for (int e = lane; e < RR; e += 32) Th[e] *= wk[e % R];
     __syncwarp();
     wmm<R, false, true>(Th, Hs, T);  // T = Th H^T
+    // scaled Newton iteration for the polar factor (Higham):
+    //   X <- (zeta X + X^-T / zeta) / 2,  zeta = sqrt(||X^-1||_F / ||X||_F)
+    // (scaling off once the update is < 1e-2); stop when the update is < 1e-8
+    // (quadratic convergence: the last iterate is at rounding level).
     bool done = false;
-    if (warm) {
-      wmm<R, true, false>(Pp, T, X);  // M = Pi_prev^T T
-      for (int e = lane; e < RR; e += 32) {
-        const int i = e / R, j = e % R;
-        aug[i * 2 * R + j] = 0.5 * (X[i * R + j] + X[j * R + i]);
-      }
+    {
+      double* Xc = X;
+      for (int e = lane; e < RR; e += 32) Xc[e] = T[e];
       __syncwarp();
-      if (wgj_inverse<R>(aug, tmp)) {
-        for (int e = lane; e < RR; e += 32) Y[e] = aug[(e / R) * 2 * R + R + e % R];
+      double delta = 1.0;
+      for (int it = 0; it < 16; ++it) {
+        for (int e = lane; e < RR; e += 32) aug[(e / R) * 2 * R + e % R] = Xc[e];
         __syncwarp();
-        wmm<R, false, false>(X, Y, Pi);  // X0 = M sym(M)^-1 (into Pi)
-        double* Xc = Pi;
-        double* Xn = X;
-        for (int it = 0; it < 10; ++it) {
-          wmm<R, true, false>(Xc, Xc, Y);  // Y = X^T X
-          for (int e = lane; e < RR; e += 32) Y[e] = ((e / R == e % R) ? 1.5 : 0.0) - 0.5 * Y[e];
-          __syncwarp();
-          wmm<R, false, false>(Xc, Y, Xn);  // Xn = X (3I - X^T X) / 2
-          double d = 0.0;
-          for (int e = lane; e < RR; e += 32) {
-            const double t = Xn[e] - Xc[e];
-            d = fma(t, t, d);
-          }
-          d = warp_sum(d);
-          double* t = Xc;
-          Xc = Xn;
-          Xn = t;
-          if (d < 9e-16) { done = true; break; }
+        if (!wgj_inverse<R>(aug, tmp)) break;
+        double nx = 0.0, ni = 0.0;
+        for (int e = lane; e < RR; e += 32) {
+          const double xv = Xc[e], iv = aug[(e / R) * 2 * R + R + e % R];
+          nx = fma(xv, xv, nx);
+          ni = fma(iv, iv, ni);
         }
-        if (done) {
-          wmm<R, false, false>(Pp, Xc, Y);  // Pi = Pi_prev X
-          for (int e = lane; e < RR; e += 32) Pi[e] = Y[e];
-          __syncwarp();
+        nx = warp_sum(nx);
+        ni = warp_sum(ni);
+        const double zeta = delta < 1e-2 ? 1.0 : sqrt(sqrt(ni / nx));
+        const double hz = 0.5 * zeta, hiz = 0.5 / zeta;
+        double d = 0.0, nn = 0.0;
+        for (int e = lane; e < RR; e += 32) {
+          const int i = e / R, j = e % R;
+          const double xn = fma(hz, Xc[e], hiz * aug[j * 2 * R + R + i]);  // X^-T[i][j] = X^-1[j][i]
+          const double t = xn - Xc[e];
+          d = fma(t, t, d);
+          nn = fma(xn, xn, nn);
+          Y[e] = xn;
         }
+        d = warp_sum(d);
+        nn = warp_sum(nn);
+        __syncwarp();
+        for (int e = lane; e < RR; e += 32) Xc[e] = Y[e];
+        __syncwarp();
+        delta = sqrt(d / nn);
+        if (delta < 1e-8) { done = true; break; }
+      }
+      if (done) {
+        for (int e = lane; e < RR; e += 32) Pi[e] = Xc[e];
+        __syncwarp();
       }
     }
     if (!done) {  // cold start / fallback: one-sided Jacobi on T
