@@ -143,13 +143,21 @@ __global__ void g2_kernel(const double* D, const double* E, const double* summed
   out[e] = acc;
 }
 
-// Ordered reduction of per-CTA slots: warp w handles entries w, w+nw, ...;
-// lanes stride over slots, fixed xor tree.  Deterministic for a given nslots.
+// Ordered reduction of per-CTA slots, latency-first: warp w handles entries
+// w, w+nw, ...; each lane issues its (up to 8) slot loads before summing, the
+// 32 lane partials combine by a fixed xor tree.  Deterministic for a given
+// nslots.
 DP2_DEV void reduce_slots_warp(const double* slots, int nslots, int n, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int e = warp; e < n; e += nw) {
-    double s = 0.0;
-    for (int w = lane; w < nslots; w += 32) s += slots[(size_t)w * n + e];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int w = lane + 32 * u;
+      v[u] = w < nslots ? slots[(size_t)w * n + e] : 0.0;
+    }
+    double s = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+    for (int w = lane + 256; w < nslots; w += 32) s += slots[(size_t)w * n + e];
     s = warp_sum(s);
     if (lane == 0) out[e] = s;
   }
@@ -335,11 +343,11 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
 }
 
 // Rotation kernel with compile-time R (R <= 16), one warp per slice: the polar
-// factor of T_k by the scaled Newton iteration (warp-parallel Gauss-Jordan
-// inverse per step, ~7 steps) -- the unique orthogonal polar factor of the
-// nonsingular T_k, i.e. the reference's Z_k P_k^T (P/solver.py:59).  A
-// singular T_k (zero pivot) falls back to one-sided Jacobi with orthonormal
-// completion (warp_polar).
+// factor of T_k by the Newton-Schulz iteration (R x R warp matmuls only) --
+// the unique orthogonal polar factor of the nonsingular T_k, i.e. the
+// reference's Z_k P_k^T (P/solver.py:59).  A singular or extremely
+// ill-conditioned T_k (no convergence in 80 steps) falls back to one-sided
+// Jacobi with orthonormal completion (warp_polar).
 template <int R>
 __host__ __device__ constexpr int grp_doubles() { return 13 * R * R + 2 * R * (R | 1) + 8 * R; }
 template <int R>
@@ -447,50 +455,43 @@ __global__ void __launch_bounds__(128) als_rotate_group_kernel(SliceArgs a, AlsB
     for (int e = lane; e < RR; e += 32) Th[e] *= wk[e % R];
     __syncwarp();
     wmm<R, false, true>(Th, Hs, T);  // T = Th H^T
-    // scaled Newton iteration for the polar factor (Higham):
-    //   X <- (zeta X + X^-T / zeta) / 2,  zeta = sqrt(||X^-1||_F / ||X||_F)
-    // (scaling off once the update is < 1e-2); stop when the update is < 1e-8
-    // (quadratic convergence: the last iterate is at rounding level).
+    // Newton-Schulz iteration for the polar factor: X0 = T / ||T||_F (all
+    // singular values in (0, 1]), X <- X (3I - X^T X) / 2; converges to the
+    // orthogonal polar factor of any nonsingular T (quadratically once the
+    // singular values approach 1).  Stop when the update is < 3e-8 (the next
+    // step's error is ~ the square of that).  Only R x R matmuls: no inverse,
+    // no divisions on the critical path.
     bool done = false;
     {
-      double* Xc = X;
-      for (int e = lane; e < RR; e += 32) Xc[e] = T[e];
-      __syncwarp();
-      double delta = 1.0;
-      for (int it = 0; it < 16; ++it) {
-        for (int e = lane; e < RR; e += 32) aug[(e / R) * 2 * R + e % R] = Xc[e];
+      double nt = 0.0;
+      for (int e = lane; e < RR; e += 32) nt = fma(T[e], T[e], nt);
+      nt = warp_sum(nt);
+      if (nt > 0.0 && isfinite(nt)) {
+        const double inv = 1.0 / sqrt(nt);
+        for (int e = lane; e < RR; e += 32) X[e] = T[e] * inv;
         __syncwarp();
-        if (!wgj_inverse<R>(aug, tmp)) break;
-        double nx = 0.0, ni = 0.0;
-        for (int e = lane; e < RR; e += 32) {
-          const double xv = Xc[e], iv = aug[(e / R) * 2 * R + R + e % R];
-          nx = fma(xv, xv, nx);
-          ni = fma(iv, iv, ni);
+        double* Xc = X;
+        double* Xn = Pi;
+        for (int it = 0; it < 80; ++it) {
+          wmm<R, true, false>(Xc, Xc, Y);  // Y = X^T X
+          for (int e = lane; e < RR; e += 32) Y[e] = ((e / R == e % R) ? 1.5 : 0.0) - 0.5 * Y[e];
+          __syncwarp();
+          wmm<R, false, false>(Xc, Y, Xn);  // Xn = X (3I - X^T X) / 2
+          double d = 0.0;
+          for (int e = lane; e < RR; e += 32) {
+            const double t = Xn[e] - Xc[e];
+            d = fma(t, t, d);
+          }
+          d = warp_sum(d);
+          double* t = Xc;
+          Xc = Xn;
+          Xn = t;
+          if (d < 9e-16) { done = true; break; }
         }
-        nx = warp_sum(nx);
-        ni = warp_sum(ni);
-        const double zeta = delta < 1e-2 ? 1.0 : sqrt(sqrt(ni / nx));
-        const double hz = 0.5 * zeta, hiz = 0.5 / zeta;
-        double d = 0.0, nn = 0.0;
-        for (int e = lane; e < RR; e += 32) {
-          const int i = e / R, j = e % R;
-          const double xn = fma(hz, Xc[e], hiz * aug[j * 2 * R + R + i]);  // X^-T[i][j] = X^-1[j][i]
-          const double t = xn - Xc[e];
-          d = fma(t, t, d);
-          nn = fma(xn, xn, nn);
-          Y[e] = xn;
+        if (done && Xc != Pi) {
+          for (int e = lane; e < RR; e += 32) Pi[e] = Xc[e];
+          __syncwarp();
         }
-        d = warp_sum(d);
-        nn = warp_sum(nn);
-        __syncwarp();
-        for (int e = lane; e < RR; e += 32) Xc[e] = Y[e];
-        __syncwarp();
-        delta = sqrt(d / nn);
-        if (delta < 1e-8) { done = true; break; }
-      }
-      if (done) {
-        for (int e = lane; e < RR; e += 32) Pi[e] = Xc[e];
-        __syncwarp();
       }
     }
     if (!done) {  // cold start / fallback: one-sided Jacobi on T
@@ -1126,9 +1127,9 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   a.warm = 1;
   cudaError_t e0 = launch_rotate(a, b, st);
   if (e0 != cudaSuccess) return e0;
-  als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
+  als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.write_l = 1;
   a.Wout = sv.W;
@@ -1272,9 +1273,9 @@ cudaError_t als_update_factors(const double* theta, const double* D, const doubl
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
   als_mode1_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   sv.nslots_h = b.nb;
-  als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
+  als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.Wout = W;
   als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
@@ -1339,7 +1340,7 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
       cudaMemcpyAsync(b.s_g1, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
       sv.nslots_h = 1;
-      als_solve_h_kernel<<<1, 256, solve_smem(R), st>>>(sv, b);
+      als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
       break;
     case 3:
       als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
@@ -1350,7 +1351,7 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
       cudaMemcpyAsync(b.s_m2, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw2, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
       sv.nslots = 1;
-      als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
+      als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
       break;
     case 5:
       a.write_w = 1;
