@@ -74,6 +74,14 @@ int dp2_device_sm_count(void);
 /* Kernels enqueued by this library so far (every launch, including the
  * kernels inside the ALS graph); reset != 0 returns the count and zeroes it. */
 int64_t dp2_launch_count(int32_t reset);
+/* Persistent segments (CTAs) of the stage-1 streaming passes for a store of
+ * this dtype / column count on a device with `sms` SMs: one per SM for fp64
+ * (DMMA) and for fp32 with J <= 512 (tcgen05 tf32 pass), two per SM for the
+ * fp32 FFMA pass.  Planning aid for dp2_plan_pieces(nseg). */
+int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms);
+/* fp32 streaming-pass engine: 0 = tcgen05 tf32 tensor cores where eligible
+ * (default), 1 = FFMA kernel everywhere.  Returns the previous setting. */
+int32_t dp2_set_sketch_engine(int32_t engine);
 /* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
 int dp2_status_init(int64_t* status_dev, void* stream);
 
@@ -140,6 +148,16 @@ size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank);
 int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
                int32_t rank, double* A_out, double* M_out, int32_t* rank_out, void* ws,
                size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
+
+/* One streaming pass of stage 1 (the two sketch products of
+ * P/linalg.py:124-127 fused per piece): for every piece p (segment x slice)
+ *   out_part[p] (J x sp)  = X_p^T (X_p B_k),  B = b_dev[k] (K x J x sp, fp64)
+ * and, when non-null: y_out (total_rows x sp) = X_k B_k rows, g_part[p]
+ * (sp x sp) = Y_p^T Y_p, xsq_part[p] = sum of squares of X_p (non-finite
+ * values set status word 0).  Pieces follow dp2_plan_pieces for st->nseg.
+ * fp32 stores use the tcgen05 tf32 pass when eligible (dp2_set_sketch_engine). */
+int dp2_stream_pass(const dp2_store* st, const double* b_dev, int32_t sp, double* out_part, double* y_out,
+                    double* g_part, double* xsq_part, int64_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------ stage 2
  * Randomized SVD of M (J x KR) (P/compress.py:109-111): D (J x rank), E (rank),

@@ -39,6 +39,8 @@ _SIGS = {
     "dp2_device_sm_count": (c_i32, []),
     "dp2_launch_count": (c_i64, [c_i32]),
     "dp2_status_init": (c_i32, [c_vp, c_vp]),
+    "dp2_stream_segments": (c_i32, [c_i32, c_i64, c_i32]),
+    "dp2_set_sketch_engine": (c_i32, [c_i32]),
     "dp2_greedy_partition": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i64), P(c_i32), P(c_i64)]),
     "dp2_piece_capacity": (c_i64, [c_i64, c_i32]),
     "dp2_plan_pieces": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i32), P(c_i64), P(c_i32), P(c_i32), P(c_i32),
@@ -47,6 +49,7 @@ _SIGS = {
     "dp2_omega_generate": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_vp]),
     "dp2_slice_stats": (c_i32, [P(Store), c_vp, c_vp, c_vp]),
+    "dp2_stream_pass": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dp2_stage1_workspace": (c_sz, [P(Store), c_i32, c_i32]),
     "dp2_stage1": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
                            P(c_f32), c_vp]),

@@ -81,9 +81,10 @@ class CompressedTensor:
 
 
 def nseg_for(tensor: IrregularTensor):
-    """Persistent segments of the streaming passes: 1 CTA/SM for f64 tiles,
-    2 for f32 (smem-limited)."""
-    return sm_count() * (1 if tensor.dtype == "f64" else 2)
+    """Persistent segments of the streaming passes (dp2_stream_segments): one
+    CTA per SM for the f64 DMMA and f32 tensor-core passes, two for the f32
+    FFMA pass."""
+    return int(_lib.lib().dp2_stream_segments(0 if tensor.dtype == "f64" else 1, tensor.num_cols, sm_count()))
 
 
 def check_status(status, what):

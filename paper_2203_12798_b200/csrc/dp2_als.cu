@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256) als_metric_kernel(AlsBufs b, const double
 // ||A||_F ||A^-1||_F < 1e10, i.e. far from the reference's drop threshold
 // (sigma <= R sigma_max 1e-12), where pinv(A) == inv(A) up to rounding.
 // Otherwise: Jacobi eigen-decomposition with the reference's threshold.
-DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out) {
+DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out, double* dinv) {
   const int lane = threadIdx.x & 31;
   // factor: column k pivot by lane 0, then lanes fill column k below the diagonal
   bool okay = true;
@@ -724,19 +724,21 @@ DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out) 
     __syncwarp();
   }
   if (!okay) return false;
-  // inverse: lane j solves L y = e_j then L^T x = y (column j of A^-1)
+  // inverse: lane j solves L y = e_j then L^T x = y (column j of A^-1), in
+  // place in ``out`` (shared) with reciprocal pivots -- no local arrays
+  for (int i = lane; i < R; i += 32) dinv[i] = 1.0 / Lw[i * R + i];
+  __syncwarp();
   double an = 0.0, in = 0.0;
   for (int j = lane; j < R; j += 32) {
-    double y[64];
     for (int i = 0; i < R; ++i) {
       double t = (i == j) ? 1.0 : 0.0;
-      for (int m = 0; m < i; ++m) t = fma(-Lw[i * R + m], y[m], t);
-      y[i] = t / Lw[i * R + i];
+      for (int m = j; m < i; ++m) t = fma(-Lw[i * R + m], out[m * R + j], t);
+      out[i * R + j] = i < j ? 0.0 : t * dinv[i];
     }
     for (int i = R - 1; i >= 0; --i) {
-      double t = y[i];
+      double t = out[i * R + j];
       for (int m = i + 1; m < R; ++m) t = fma(-Lw[m * R + i], out[m * R + j], t);
-      out[i * R + j] = t / Lw[i * R + i];
+      out[i * R + j] = t * dinv[i];
     }
     for (int i = 0; i < R; ++i) {
       an = fma(A[i * R + j], A[i * R + j], an);
@@ -753,7 +755,7 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
   __shared__ double lmax;
   __shared__ int fast;
   if (threadIdx.x < 32) {
-    const bool okay = warp_chol_inverse(A, R, U, out);
+    const bool okay = warp_chol_inverse(A, R, U, out, cs);
     if (threadIdx.x == 0) fast = okay ? 1 : 0;
   }
   __syncthreads();
@@ -853,6 +855,13 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   double* es = Pv + R * R;  // E * summed
   double* cs = es + R * R;
   __shared__ double nrm[64];
+  double* EP = cs + 3 * (R / 2 + 1) + 8;
+  double* Ds = EP + R * R;
+  double* Vs = s.dsm ? Ds + J * R : b.G2;
+  const double* Dp = s.dsm ? Ds : s.D;
+  // stage D first: its load overlaps the slot reductions and warp 0's pinv
+  if (s.dsm)
+    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) Ds[e] = s.D[e];
   reduce_slots_warp(b.s_m2, s.nslots, R * R, summed);
   reduce_slots_warp(b.s_wtw2, s.nslots, R * R, WtW2);
   __syncthreads();
@@ -866,18 +875,12 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   block_pinv_sym(Mv, U, Pv, R, cs, s.status);
   // V = D (E * summed) pinv = D EP with EP = (E * summed) pinv (R x R), so the
   // J-sized work is one product; D and V stay in smem when they fit
-  double* EP = cs + 3 * (R / 2 + 1) + 8;
-  double* Ds = EP + R * R;
-  double* Vs = s.dsm ? Ds + J * R : b.G2;
-  const double* Dp = s.dsm ? Ds : s.D;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int q = e / R, r = e % R;
     double acc = 0.0;
     for (int a2 = 0; a2 < R; ++a2) acc = fma(es[q * R + a2], Pv[a2 * R + r], acc);
     EP[e] = acc;
   }
-  if (s.dsm)
-    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) Ds[e] = s.D[e];
   __syncthreads();
   for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
     const int64_t j = e / R;
@@ -905,7 +908,8 @@ __global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   __syncthreads();
   gram_dv_warps(Dp, s.E, Vs, J, R, b.cc, b.VtV, Mv, b.HtH);
   __syncthreads();
-  block_pinv_sym(Mv, U, b.pinv3, R, cs, s.status);
+  block_pinv_sym(Mv, U, Pv, R, cs, s.status);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) b.pinv3[e] = Pv[e];
 }
 
 // ------------------------------------------------------------ host side

@@ -68,6 +68,17 @@ int dp2_device_sm_count(void) {
   return n;
 }
 
+int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms) {
+  if (sms < 1) return 1;
+  return (dtype == DP2_F64 || J <= 512) ? sms : 2 * sms;
+}
+
+int32_t dp2_set_sketch_engine(int32_t engine) {
+  const int prev = dp2::sketch_engine();
+  dp2::set_sketch_engine(engine);
+  return prev;
+}
+
 int dp2_status_init(int64_t* status_dev, void* stream) {
   int64_t init[DP2_STATUS_WORDS] = {INT64_MAX, 0, INT64_MAX, INT64_MAX, 0, 0, 0, 0};
   cudaError_t e = cudaMemcpyAsync(status_dev, init, sizeof(init), cudaMemcpyHostToDevice, S(stream));
@@ -155,6 +166,14 @@ int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev
   if (!store_ok(st)) return fail_arg("invalid store");
   cudaError_t e = dp2::run_slice_stats(st, sqnorm_dev, status_dev, S(stream));
   return e == cudaSuccess ? ok(3) : fail(e, "dp2_slice_stats");
+}
+
+int dp2_stream_pass(const dp2_store* st, const double* b_dev, int32_t sp, double* out_part, double* y_out,
+                    double* g_part, double* xsq_part, int64_t* status_dev, void* stream) {
+  if (!store_ok(st) || sp < 1 || !b_dev || !out_part) return fail_arg("invalid stream-pass arguments");
+  if (g_part && sp > 32) return fail_arg("g_part needs sp <= 32");
+  cudaError_t e = dp2::run_sketch(st, b_dev, sp, out_part, y_out, xsq_part, status_dev, S(stream), g_part);
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_stream_pass");
 }
 
 size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {

@@ -26,6 +26,11 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
                              int64_t* status, int phase, cudaStream_t stream);
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                            double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
+bool sketch_tc_eligible(const dp2_store* st, int sp);
+cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                          double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
+void set_sketch_engine(int e);
+int sketch_engine();
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                        double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part = nullptr);
 

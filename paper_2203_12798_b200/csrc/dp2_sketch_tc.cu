@@ -1,0 +1,638 @@
+// Stage-1 streaming sketch pass for fp32 slice storage on the 5th-gen tensor
+// cores (tcgen05.mma kind::tf32, accumulators in TMEM).
+//
+// Same contract as run_sketch_f32 (dp2_sketch32.cu) and the fp64 DMMA pass:
+// per persistent segment, walk the pieces (segment x slice) tile by tile and
+//   Y_t = X_t B            (P1: M = 64 rows, N = sp, K = J)
+//   Z  += X_t^T Y_t        (P2: M = 128 columns of X, N = sp (padded to 16), K = 64 rows)
+// writing one fp64 partial Z (J x sp) per piece, plus (pass 1) the per-piece
+// sum of squares / non-finite flag and (pass 2) Y rows and G = Y^T Y.
+// P/compress.py:64-103 (randomized_svd per slice) is what this computes the
+// sketches of; the algebra is DESIGN.md §3.
+//
+// Data movement (one CTA per SM, 13 warps):
+//   warps 0-7   producers: warp-wide LDG of 128 B row segments of X (one
+//               "unit" = 64 rows x 128 columns, 32 KB; thread = one column,
+//               32 rows) -> statistics -> round to tf32 (cvt.rna) -> two
+//               on-chip copies:
+//                 * STS into a ring of 8 KB chunk slots in the SWIZZLE_128B
+//                   row-major layout: P1's K-major A operand;
+//                 * tcgen05.st into TMEM (lane = column of X, TMEM column =
+//                   row): P2's A operand X^T, which must be K-major.  (tf32
+//                   MN-major shared-memory operands only exist in the
+//                   128B-base-32B swizzle, which no K-major layout shares, so
+//                   one shared-memory copy cannot feed both products --
+//                   tools/umma_probe.cu measures this.)
+//   warp 8      TMEM allocation + a single elected thread issuing tcgen05.mma
+//               and tcgen05.commit (mbarrier arrive on completion).
+//   warps 9-12  epilogue: tcgen05.ld of Y (TMEM lanes = rows) -> rounded Y^T
+//               into shared memory as P2's K-major B operand; Y rows / G in
+//               pass 2; the per-piece Z flush (TMEM lanes = columns of X).
+// B (Omega_k or Q_Z,k, fp64 in HBM) is converted per piece to a K-major tf32
+// copy in shared memory.  TMEM: X^T blocks in columns [0, 256), Z in
+// [256, 384), Y in [384, 416).  Ring slots are released right after P1, the
+// X^T blocks after P2, so HBM streaming overlaps both products.
+//
+// Precision: products in tf32 (10-bit mantissa, round-to-nearest on both
+// operands), fp32 accumulation within a piece, fp64 partials across pieces --
+// the fp32-mode budget (BASELINE.json north_star: factors and fitness within
+// 1e-3).  fp64 storage keeps the DMMA path.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+namespace tcs {
+
+constexpr int TM = 64;             // rows per tile
+constexpr int CHUNK = TM * 128;    // bytes of one 32-column chunk (64 rows x 128 B)
+constexpr int NXT = 128;           // X^T producers + statistics (warps 0-3)
+constexpr int B0 = 128, NB = 128;  // B (Omega / Q_Z) converters (warps 4-7)
+constexpr int MMA_WARP = 8;
+constexpr int EPI0 = 9 * 32;       // first epilogue thread (warps 9-12)
+constexpr int NEPI = 128;
+constexpr int TMA_WARP = 13;
+constexpr int NTHREADS = 14 * 32;
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Params {
+  const float* X;
+  int64_t ldx;
+  int J, Jp, sp, n2, nslot, nsup;
+  const double* B;
+  const int32_t* piece_slice;
+  const int64_t* piece_row0;
+  const int32_t* piece_rows;
+  const int32_t* seg_begin;
+  double* out_part;
+  double* y_out;
+  double* xsq_part;
+  double* g_part;
+  int64_t* status;
+  uint32_t off_b, off_y, off_yrow, off_bar;
+};
+
+// ------------------------------------------------------------ PTX helpers
+DP2_DEV uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+DP2_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+DP2_DEV void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+DP2_DEV bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a protocol error traps (kernel error) instead of hanging the GPU
+DP2_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(bar, parity)) return;
+    if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
+  }
+}
+DP2_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+DP2_DEV void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+DP2_DEV void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+DP2_DEV void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+DP2_DEV void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+DP2_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+DP2_DEV float tf32r(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+DP2_DEV void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// shared-memory matrix descriptor, SWIZZLE_128B (sm_100 version 1)
+DP2_DEV uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
+}
+// instruction descriptor: f32 accumulate, tf32 A/B, majors, N, M
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// byte offset of element (row, col) inside a 128 B-row swizzled block (col < 32)
+DP2_DEV uint32_t swz(int row, int col) {
+  return (uint32_t)row * 128u + ((uint32_t)(((col >> 2) ^ row) & 7) << 4) + (uint32_t)(col & 3) * 4u;
+}
+
+// barrier slots (uint64 each) after off_bar
+enum : int {
+  BAR_BFULL = 0, BAR_BFREE, BAR_YFULL, BAR_YSFULL, BAR_ZFULL, BAR_ZFREE,
+  BAR_XT = 8,    // 4 x (full, free) for the TMEM X^T blocks
+  BAR_RING = 16  // nss x full, nss x empty
+};
+
+struct Unit {  // 64 rows x 128 columns of one tile
+  int p, t, jb, rows;
+  int64_t row0;
+};
+
+DP2_DEV void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// A operand from TMEM (K-major: lanes = M, columns = K)
+DP2_DEV void tc_mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+DP2_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+DP2_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// TMEM columns: X^T blocks [0, 64 nsup), Z [XT_END, +32 nsup), Y [YCOL2, +32)
+constexpr int ZCOL = 256, YCOL2 = 384;
+
+__global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, const __grid_constant__ CUtensorMap xmap) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  __shared__ double red[32];
+  const int seg = blockIdx.x;
+  const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
+  if (pbeg >= pend) return;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t base = (su32(smem_raw) + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (base - su32(smem_raw));
+  const int J = prm.J, Jp = prm.Jp, sp = prm.sp, n2 = prm.n2, nslot = prm.nslot, nsup = prm.nsup;
+  const int nss = nslot / 4;  // superslots (4 chunks = one 128-column unit)
+  const uint32_t ring = base, bsm = base + prm.off_b, ysm = base + prm.off_y;
+  float* yrow = reinterpret_cast<float*>(gbase + prm.off_yrow);
+  const uint32_t bars = base + prm.off_bar;
+  auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
+
+  if (tid == 0) {
+    mbar_init(bar(BAR_BFULL), 1);
+    mbar_init(bar(BAR_BFREE), 1);
+    mbar_init(bar(BAR_YFULL), 1);
+    mbar_init(bar(BAR_YSFULL), NEPI);
+    mbar_init(bar(BAR_ZFULL), 1);
+    mbar_init(bar(BAR_ZFREE), NEPI);
+    for (int jb = 0; jb < 4; ++jb) {
+      mbar_init(bar(BAR_XT + 2 * jb), NXT);
+      mbar_init(bar(BAR_XT + 2 * jb + 1), 1);
+    }
+    for (int s = 0; s < nss; ++s) {
+      mbar_init(bar(BAR_RING + s), 1);  // TMA thread's arrive.expect_tx
+      mbar_init(bar(BAR_RING + nss + s), 1 + NXT);  // P1 commit + X^T copies
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // Y^T rows >= sp stay zero (P2's N is sp rounded up to 16)
+  {
+    float* ys = reinterpret_cast<float*>(gbase + prm.off_y);
+    for (int i = tid; i < 2 * n2 * 32; i += NTHREADS) ys[i] = 0.0f;
+    fence_async_smem();
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = tmem_slot;
+
+  // unit iteration shared by both producer groups
+  auto first_unit = [&](int p) {
+    Unit u;
+    u.p = p;
+    u.t = 0;
+    u.jb = 0;
+    u.rows = min(TM, prm.piece_rows[p]);
+    u.row0 = prm.piece_row0[p];
+    return u;
+  };
+  auto next_unit = [&](Unit u) {
+    if (++u.jb < nsup) return u;
+    u.jb = 0;
+    const int pr = prm.piece_rows[u.p];
+    if ((u.t + 1) * TM < pr) {
+      ++u.t;
+      u.rows = min(TM, pr - u.t * TM);
+      return u;
+    }
+    if (u.p + 1 >= pend) {
+      u.p = pend;
+      return u;
+    }
+    return first_unit(u.p + 1);
+  };
+
+  if (warp == TMA_WARP) {
+    // ===================================================== TMA issuer
+    // unit = 4 boxes of 64 rows x 32 columns (128 B inner, SWIZZLE_128B: the
+    // UMMA K-major SW128 layout); rows past the piece or the store are other
+    // slices' rows or TMA zero fill -- masked downstream (Y^T rows, X^T rows).
+    if (lane == 0) {
+      Unit cur = first_unit(pbeg);
+      uint32_t ucount = 0;
+      while (cur.p < pend) {
+        const int ss = (int)(ucount % (uint32_t)nss);
+        const uint32_t fill = ucount / (uint32_t)nss;
+        if (fill > 0) mbar_wait(bar(BAR_RING + nss + ss), (fill - 1) & 1u);
+        mbar_expect_tx(bar(BAR_RING + ss), 4 * CHUNK);
+        const int row = (int)(cur.row0 + (int64_t)cur.t * TM);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch)
+          tma_load_2d(ring + (uint32_t)(ss * 4 + ch) * CHUNK, &xmap, cur.jb * 128 + ch * 32, row,
+                      bar(BAR_RING + ss));
+        ++ucount;
+        cur = next_unit(cur);
+      }
+    }
+    __syncwarp();
+  } else if (tid >= B0 && tid < B0 + NB) {
+    // ===================================================== B converters
+    // per piece: Omega_k / Q_Z,k (fp64, J x sp) -> tf32 K-major SW128 smem,
+    // once P1 of the previous piece has released the buffer
+    const int bt = tid - B0;
+    int pidx = 0;
+    for (int p = pbeg; p < pend; ++p, ++pidx) {
+      if (pidx > 0) mbar_wait(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u);
+      const double* Bm = prm.B + (size_t)prm.piece_slice[p] * J * sp;
+      unsigned char* bb = gbase + prm.off_b;
+      for (int e = bt; e < Jp * sp; e += NB) {
+        const int j = e / sp, c = e - j * sp;
+        const float v = j < J ? tf32r((float)Bm[(size_t)j * sp + c]) : 0.0f;
+        *reinterpret_cast<float*>(bb + (size_t)(j >> 5) * sp * 128 + swz(c, j & 31)) = v;
+      }
+      fence_async_smem();
+      named_sync(3, NB);
+      if (bt == 0) mbar_arrive(bar(BAR_BFULL));
+    }
+  } else if (tid < NXT) {
+    // ===================================================== X^T producers
+    // thread (q = warp, lane) owns column 32 q + lane of every unit: it reads
+    // that column's 64 rows from ring chunk q (one 128 B swizzled row per
+    // warp-wide LDS, conflict-free), releases the slot, zeroes rows past the
+    // piece, accumulates the piece statistics, rounds to tf32 (rna) and stores
+    // the column to TMEM lane 32 q + lane, columns jb*64 .. +63 once P2 of the
+    // previous tile has consumed that block.
+    const int q = warp;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool stats = prm.xsq_part != nullptr;
+    double sq = 0.0;
+    float probe = 0.0f;
+    Unit cur = first_unit(pbeg);
+    uint32_t ucount = 0, tcount = 0;
+    while (cur.p < pend) {
+      const int ss = (int)(ucount % (uint32_t)nss);
+      mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
+      const unsigned char* srcb = gbase + (size_t)(ss * 4 + q) * CHUNK;
+      float v0[32], v1[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v0[i] = *reinterpret_cast<const float*>(srcb + swz(i, lane));
+        v1[i] = *reinterpret_cast<const float*>(srcb + swz(i + 32, lane));
+      }
+      mbar_arrive(bar(BAR_RING + nss + ss));  // release orders the loads above before it
+      float s = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v0[i] = i < cur.rows ? v0[i] : 0.0f;
+        v1[i] = i + 32 < cur.rows ? v1[i] : 0.0f;
+        s = fmaf(v0[i], v0[i], s);
+        s = fmaf(v1[i], v1[i], s);
+        probe = fmaf(v0[i], 0.0f, probe);
+        probe = fmaf(v1[i], 0.0f, probe);
+        v0[i] = tf32r(v0[i]);
+        v1[i] = tf32r(v1[i]);
+      }
+      sq += (double)s;
+      if (tcount > 0) mbar_wait(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u);
+      tc_after();
+      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64), v0);
+      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32), v1);
+      tc_before();
+      mbar_arrive(bar(BAR_XT + 2 * cur.jb));
+      ++ucount;
+      const Unit nx = next_unit(cur);
+      if (nx.jb == 0) ++tcount;
+      if (nx.p != cur.p && stats) {  // piece complete: sum of squares, non-finite flag
+        const double tot = warp_sum(sq);
+        const int anybad = __any_sync(0xffffffffu, !isfinite(probe));
+        if (lane == 0) {
+          red[warp] = tot;
+          red[16 + warp] = anybad ? 1.0 : 0.0;
+        }
+        named_sync(1, NXT);
+        if (tid == 0) {
+          double t = 0.0;
+          int b = 0;
+          for (int w = 0; w < NXT / 32; ++w) {
+            t += red[w];
+            b |= red[16 + w] != 0.0;
+          }
+          prm.xsq_part[cur.p] = t;
+          if (b) status_min(prm.status, ST_NONFINITE, prm.piece_slice[cur.p]);
+        }
+        named_sync(1, NXT);
+        sq = 0.0;
+        probe = 0.0f;
+      }
+      cur = nx;
+    }
+  } else if (warp == MMA_WARP) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      const uint32_t id1 = idesc_tf32(64, sp, 0, 0);   // X (smem, K-major) x B^T (K-major)
+      const uint32_t id2 = idesc_tf32(128, n2, 0, 0);  // X^T (TMEM) x Y^T (K-major)
+      uint32_t ucount = 0, tcount = 0;
+      int pidx = 0;
+      for (int p = pbeg; p < pend; ++p, ++pidx) {
+        const int ntiles = (prm.piece_rows[p] + TM - 1) / TM;
+        mbar_wait(bar(BAR_BFULL), (uint32_t)pidx & 1u);
+        tc_after();
+        for (int t = 0; t < ntiles; ++t, ++tcount) {
+          for (int jb = 0; jb < nsup; ++jb, ++ucount) {  // P1: Y = X B
+            const int ss = (int)(ucount % (uint32_t)nss);
+            mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
+            tc_after();
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t a = sdesc(ring + (uint32_t)(ss * 4 + ch) * CHUNK + kk * 32, 16, 1024);
+                const uint64_t b = sdesc(bsm + (uint32_t)(jb * 4 + ch) * sp * 128 + kk * 32, 16, 1024);
+                tc_mma(tmem + YCOL2, a, b, id1, (jb | ch | kk) != 0);
+              }
+            tc_commit(bar(BAR_RING + nss + ss));
+          }
+          if (t == ntiles - 1) tc_commit(bar(BAR_BFREE));
+          tc_commit(bar(BAR_YFULL));
+          mbar_wait(bar(BAR_YSFULL), tcount & 1u);
+          if (t == 0 && pidx > 0) mbar_wait(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u);
+          tc_after();
+          for (int jb = 0; jb < nsup; ++jb) {  // P2: Z += X^T Y
+            mbar_wait(bar(BAR_XT + 2 * jb), tcount & 1u);
+            tc_after();
+#pragma unroll
+            for (int k = 0; k < TM / 8; ++k) {
+              const uint64_t b = sdesc(ysm + (uint32_t)(k >> 2) * n2 * 128 + (k & 3) * 32, 16, 1024);
+              tc_mma_ts(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, b, id2, (t > 0 || k > 0) ? 1u : 0u);
+            }
+            tc_commit(bar(BAR_XT + 2 * jb + 1));
+          }
+        }
+        tc_commit(bar(BAR_ZFULL));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================================================== epilogue
+    const int q = warp & 3, et = tid - EPI0;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    unsigned char* yb = gbase + prm.off_y;
+    const bool pass2 = prm.y_out != nullptr;
+    const bool do_g = prm.g_part != nullptr;
+    const int ng = sp * sp;
+    double gacc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    uint32_t tcount = 0;
+    int pidx = 0;
+    for (int p = pbeg; p < pend; ++p, ++pidx) {
+      const int prows = prm.piece_rows[p];
+      const int ntiles = (prows + TM - 1) / TM;
+      for (int t = 0; t < ntiles; ++t, ++tcount) {
+        mbar_wait(bar(BAR_YFULL), tcount & 1u);
+        tc_after();
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + YCOL2, v);
+        // M = 64 accumulator: row 16 q + l lives in TMEM lane 32 q + l (l < 16)
+        const int r = 16 * q + lane;
+        const int rows = min(TM, prows - t * TM);
+        const bool valid = lane < 16 && r < rows;
+        if (lane < 16) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            if (c >= sp) break;
+            const float y = valid ? __uint_as_float(v[c]) : 0.0f;
+            *reinterpret_cast<float*>(yb + (size_t)(r >> 5) * n2 * 128 + swz(c, r & 31)) = tf32r(y);
+          }
+        }
+        fence_async_smem();
+        tc_before();
+        mbar_arrive(bar(BAR_YSFULL));
+        if (pass2) {
+          if (valid) {
+            double* yo = prm.y_out + (prm.piece_row0[p] + (int64_t)t * TM + r) * sp;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c < sp) yo[c] = (double)__uint_as_float(v[c]);
+          }
+          if (do_g) {  // G += Y_t^T Y_t: fp64 DMMA m8n8k4 over 8x8 blocks of G
+            if (lane < 16)
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (c < sp) yrow[r * (sp + 1) + c] = valid ? __uint_as_float(v[c]) : 0.0f;
+            named_sync(2, NEPI);
+            const int nb = sp / 8, ew = et >> 5;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const int blk = ew + 4 * s;
+              if (blk < nb * nb) {
+                const int bi = blk / nb, bj = blk - bi * nb;
+                double c0 = gacc[2 * s], c1 = gacc[2 * s + 1];
+#pragma unroll 4
+                for (int kk = 0; kk < TM / 4; ++kk) {
+                  const float* yr = yrow + (4 * kk + (lane & 3)) * (sp + 1);
+                  dmma_8x8x4(c0, c1, (double)yr[8 * bi + (lane >> 2)], (double)yr[8 * bj + (lane >> 2)]);
+                }
+                gacc[2 * s] = c0;
+                gacc[2 * s + 1] = c1;
+              }
+            }
+            named_sync(2, NEPI);
+          }
+        }
+      }
+      // piece complete: Z (TMEM lanes = columns of X) -> fp64 partial
+      mbar_wait(bar(BAR_ZFULL), (uint32_t)pidx & 1u);
+      tc_after();
+      double* out = prm.out_part + (size_t)p * J * sp;
+      for (int jb = 0; jb < nsup; ++jb) {
+        uint32_t z[32];
+        tmem_ld32(tmem + lane_off + ZCOL + jb * 32, z);
+        const int j = jb * 128 + q * 32 + lane;
+        if (j < J)
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c < sp) out[(size_t)j * sp + c] = (double)__uint_as_float(z[c]);
+      }
+      tc_before();
+      mbar_arrive(bar(BAR_ZFREE));
+      if (do_g) {
+        const int nb = sp / 8, ew = et >> 5;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int blk = ew + 4 * s;
+          if (blk < nb * nb) {
+            const int bi = blk / nb, bj = blk - bi * nb;
+            double* g = prm.g_part + (size_t)p * ng + (size_t)(8 * bi + (lane >> 2)) * sp + 8 * bj + 2 * (lane & 3);
+            g[0] = gacc[2 * s];
+            g[1] = gacc[2 * s + 1];
+          }
+          gacc[2 * s] = 0.0;
+          gacc[2 * s + 1] = 0.0;
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace tcs
+
+namespace {
+int g_engine = 0;  // 0: tensor cores when eligible, 1: FFMA kernel
+}
+
+void set_sketch_engine(int e) { g_engine = e; }
+int sketch_engine() { return g_engine; }
+
+// shared-memory plan; 0 when the shape is not eligible for the tensor-core pass
+static size_t tc_plan(int J, int sp, tcs::Params* prm) {
+  if (J < 1 || J > 512 || sp < 8 || sp > 32 || sp % 8) return 0;
+  const int Jp = (J + 127) / 128 * 128, nch = Jp / 32, n2 = (sp + 15) / 16 * 16;
+  const size_t fixed = (size_t)sp * Jp * 4 + (size_t)2 * n2 * 128 + (size_t)tcs::TM * (sp + 1) * 4;
+  const size_t cap = 227 * 1024 - 1024 - fixed;
+  int nslot = (int)(cap / tcs::CHUNK) / 4 * 4;
+  nslot = nslot > 24 ? 24 : nslot;
+  (void)nch;
+  if (nslot < 8) return 0;
+  const int nss = nslot / 4;
+  prm->J = J;
+  prm->Jp = Jp;
+  prm->sp = sp;
+  prm->n2 = n2;
+  prm->nslot = nslot;
+  prm->nsup = Jp / 128;
+  prm->off_b = (uint32_t)nslot * tcs::CHUNK;
+  prm->off_y = prm->off_b + (uint32_t)sp * Jp * 4;
+  prm->off_yrow = prm->off_y + 2u * n2 * 128;
+  prm->off_bar = (prm->off_yrow + (uint32_t)tcs::TM * (sp + 1) * 4 + 7u) & ~7u;
+  return prm->off_bar + 8u * (tcs::BAR_RING + 2 * nss) + 1024;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+bool sketch_tc_eligible(const dp2_store* st, int sp) {
+  tcs::Params prm{};
+  return g_engine == 0 && st->dtype == DP2_F32 && st->ldx % 4 == 0 &&
+         reinterpret_cast<uintptr_t>(st->X) % 16 == 0 && st->total_rows < (1ll << 31) &&
+         tc_plan((int)st->J, sp, &prm) != 0 && encode_fn() != nullptr;
+}
+
+cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                          double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
+  tcs::Params prm{};
+  const size_t smem = tc_plan((int)st->J, sp, &prm);
+  if (smem == 0 || encode_fn() == nullptr) return cudaErrorInvalidValue;
+  // X as a 2-D tensor (J columns, total_rows rows, row pitch ldx*4 B); boxes
+  // of 32 columns x 64 rows land in shared memory with the 128 B swizzle
+  CUtensorMap xmap;
+  const cuuint64_t dims[2] = {(cuuint64_t)st->J, (cuuint64_t)st->total_rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)st->ldx * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)tcs::TM};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult cr = encode_fn()(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(st->X), dims, strides,
+                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) {
+    note_error("cuTensorMapEncodeTiled failed for the fp32 store");
+    return cudaErrorInvalidValue;
+  }
+  prm.X = static_cast<const float*>(st->X);
+  prm.ldx = st->ldx;
+  prm.B = B;
+  prm.piece_slice = st->piece_slice;
+  prm.piece_row0 = st->piece_row0;
+  prm.piece_rows = st->piece_rows;
+  prm.seg_begin = st->seg_begin;
+  prm.out_part = out_part;
+  prm.y_out = y_out;
+  prm.xsq_part = xsq_part;
+  prm.g_part = g_part;
+  prm.status = status;
+  cudaError_t e = cudaFuncSetAttribute(tcs::sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tcs::sketch_tc_kernel<<<st->nseg, tcs::NTHREADS, smem, stream>>>(prm, xmap);
+  return cudaGetLastError();
+}
+
+}  // namespace dp2
