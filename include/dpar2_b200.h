@@ -123,6 +123,12 @@ typedef struct dp2_tail_record {
 int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev, int32_t sp,
                        const int64_t* slice_ids_dev, double* out, dp2_tail_record* recs, int32_t cap,
                        int32_t* nrec_dev, int32_t* redo_dev, void* stream);
+/* Host-side replay of tail records (host pointers): for each record, re-run
+ * its attempts with this process's libm log1p -- the function NumPy's
+ * ziggurat calls (npy_log1p) -- giving the reference's output value in
+ * vals[i] and ok[i] = 1, or ok[i] = 0 when the device's acceptance decision
+ * differed (the slice must then be regenerated on the host). */
+int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok);
 
 /* ------------------------------------------------------------------ tensor checks
  * Per-slice squared Frobenius norms (sqnorm_dev[K]) and the lowest slice with

@@ -48,6 +48,7 @@ _SIGS = {
     "dp2_derived_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "dp2_omega_generate": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_vp]),
+    "dp2_omega_replay": (c_i32, [c_vp, c_i64, P(c_f64), P(c_i32)]),
     "dp2_slice_stats": (c_i32, [P(Store), c_vp, c_vp, c_vp]),
     "dp2_stream_pass": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dp2_stage1_workspace": (c_sz, [P(Store), c_i32, c_i32]),

@@ -1,5 +1,6 @@
 // extern "C" entry points of libdpar2_b200.so (declared in include/dpar2_b200.h).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -159,6 +160,28 @@ int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev
   if (dp2::tail_record_bytes() != sizeof(dp2_tail_record)) return fail_arg("record layout mismatch");
   cudaError_t e = dp2::run_omega(seed, K, J, s_dev, sp, slice_ids_dev, out, recs, cap, nrec_dev, redo_dev, S(stream));
   return e == cudaSuccess ? ok(1) : fail(e, "dp2_omega_generate");
+}
+
+int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok_out) {
+  if (count < 0 || (count && (!recs || !vals || !ok_out))) return fail_arg("invalid replay arguments");
+  constexpr double kR = 3.6541528853610087963519472518, kInvR = 0.27366123732975827203338247596;
+  for (int64_t n = 0; n < count; ++n) {
+    const dp2_tail_record& r = recs[n];
+    int good = r.attempts >= 1 && r.attempts <= 4;
+    double v = 0.0;
+    for (int a = 0; good && a < r.attempts; ++a) {
+      // P/linalg.py:122 -> numpy random_standard_normal, layer-0 tail branch
+      const double xx = -kInvR * std::log1p(-r.u[2 * a]);
+      const double yy = -std::log1p(-r.u[2 * a + 1]);
+      const bool acc = (yy + yy) > (xx * xx);
+      const bool last = a + 1 == r.attempts;
+      if (acc != last) good = 0;
+      if (last) v = r.negative ? -(kR + xx) : kR + xx;
+    }
+    vals[n] = v;
+    ok_out[n] = good;
+  }
+  return DP2_OK;
 }
 
 // ---------------------------------------------------------------- device calls

@@ -6,8 +6,9 @@
 //   SeedSequence(derived)   -> 4 uint64 -> PCG64 state/inc (pcg setseq srandom)
 //   PCG64 XSL-RR 128/64 stream -> 256-layer ziggurat (tables: dp2_ziggurat_tables.h)
 //
-// One thread per slice walks that slice's stream.  The fast path (>99% of
-// draws: one 64-bit output, one multiply) is exact IEEE arithmetic.  The rare
+// One warp per slice walks that slice's stream (32 draws in flight via
+// jump-ahead, see omega_kernel).  The fast path (>99% of draws: one 64-bit
+// output, one multiply) is exact IEEE arithmetic.  The rare
 // tail branch (layer 0, about 2.6e-4 of draws) needs log1p, whose last bit
 // differs between libm implementations, so every tail event is recorded
 // (output index, the uniforms it consumed) and the host replays it with
@@ -121,11 +122,36 @@ struct TailRec {          // one layer-0 tail event, replayed on the host
 };
 constexpr int kTailAttempts = 4;
 
-__global__ void __launch_bounds__(32) omega_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp,
-                                                   const int64_t* slice_ids, double* out, TailRec* recs,
-                                                   int cap, int32_t* nrec, int32_t* redo) {
-  // lanes index the tables with different layers: shared memory, not the
-  // (uniform-access) constant cache
+// 128-bit LCG arithmetic (mod 2^128) for PCG64 jump-ahead
+struct U128 {
+  uint64_t lo, hi;
+};
+__device__ inline U128 mul128(U128 a, U128 b) {
+  return {a.lo * b.lo, __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo};
+}
+__device__ inline U128 add128(U128 a, U128 b) {
+  const uint64_t lo = a.lo + b.lo;
+  return {lo, a.hi + b.hi + (lo < a.lo ? 1ull : 0ull)};
+}
+__device__ inline uint64_t pcg_out(U128 s) {
+  const uint64_t x = s.hi ^ s.lo;
+  const unsigned rot = (unsigned)(s.hi >> 58);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// One warp per slice.  Lane l holds the generator state of draw base + l
+// (state_{p+l} = A^l state_p + inc * (1 + A + ... + A^(l-1))), so a batch of
+// 32 consecutive 64-bit draws is produced in parallel.  The ziggurat parse of
+// the draw stream is inherently sequential but almost always one draw per
+// normal: every round, the lanes from the current normal start up to the
+// first draw that misses the fast rectangle emit their normals at once
+// (ballot + prefix count); that one wedge/tail draw is resolved by its lane
+// with its own sequential generator, which then broadcasts its state so the
+// warp re-bases behind the consumed draws.  The output is the reference's
+// stream exactly.
+__global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp,
+                                                    const int64_t* slice_ids, double* out, TailRec* recs,
+                                                    int cap, int32_t* nrec, int32_t* redo) {
   __shared__ uint64_t ki_s[256];
   __shared__ double wi_s[256], fi_s[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -134,72 +160,135 @@ __global__ void __launch_bounds__(32) omega_kernel(uint64_t seed, int64_t K, int
     fi_s[i] = __longlong_as_double((long long)kZigFiBits[i]);
   }
   __syncthreads();
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= K) return;
+  // jump constants: A^lane, S_lane = sum_{i<lane} A^i, and the same for 32
+  const U128 A{kPcgMulLo, kPcgMulHi};
+  U128 Al{1, 0}, Sl{0, 0}, P{1, 0}, S{0, 0};
+  for (int i = 0; i < 32; ++i) {
+    if (i == lane) {
+      Al = P;
+      Sl = S;
+    }
+    S = add128(S, P);
+    P = mul128(P, A);
+  }
+  const U128 A32 = P, S32 = S;
   const uint64_t gid = slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k;
   Pcg g;
   g.seed(derived_seed_u64(seed, gid));
+  const U128 inc{g.ilo, g.ihi};
+  const U128 Cl = mul128(inc, Sl), C32 = mul128(inc, S32);
+  // state of draw 0 (Pcg::next steps, then outputs)
+  U128 b = add128(mul128(U128{g.slo, g.shi}, A), inc);
+  U128 st = add128(mul128(b, Al), Cl);
   const int s = s_k[k];
   double* o = out + (size_t)k * J * sp;
   const int64_t total = (int64_t)J * s;
-  int64_t i = 0;
-  for (int j = 0; j < J; ++j) {
-    for (int c = 0; c < s; ++c, ++i) {
-      double val;
-      for (;;) {
-        uint64_t r = g.next();
-        const int idx = (int)(r & 0xff);
-        r >>= 8;
-        const int sign = (int)(r & 1);
-        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-        double x = __dmul_rn((double)rabs, wi_s[idx]);
-        if (sign) x = -x;
-        if (rabs < ki_s[idx]) { val = x; break; }
-        if (idx == 0) {
-          TailRec rec;
-          rec.slice = k;
-          rec.index = i;
-          rec.negative = (int)((rabs >> 8) & 1);
-          int a = 0;
-          for (;;) {
-            const double u1 = g.next_double(), u2 = g.next_double();
-            if (a < kTailAttempts) { rec.u[2 * a] = u1; rec.u[2 * a + 1] = u2; }
-            ++a;
-            const double xx = __dmul_rn(-kZigInvR, log1p(-u1));
-            const double yy = -log1p(-u2);
-            if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
-              val = rec.negative ? -(kZigR + xx) : kZigR + xx;
-              break;
-            }
+  for (int64_t e = lane; e < (int64_t)J * (sp - s); e += 32)  // zero padding columns
+    o[(e / (sp - s)) * sp + s + e % (sp - s)] = 0.0;
+  int64_t i = 0;  // normals emitted
+  int start = 0;  // lane of the next normal start in this batch
+  while (i < total) {
+    uint64_t r = pcg_out(st);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = __dmul_rn((double)rabs, wi_s[idx]);
+    if (sign) x = -x;
+    const bool fast = rabs < ki_s[idx];
+    const unsigned slow = __ballot_sync(0xffffffffu, !fast) & (0xffffffffu << start);
+    const int f = slow ? __ffs(slow) - 1 : 32;
+    // lanes start .. f-1 are one-draw normals
+    if (lane >= start && lane < f) {
+      const int64_t oi = i + (lane - start);
+      if (oi < total) o[(oi / s) * sp + oi % s] = x;
+    }
+    i += f - start;
+    if (f == 32) {  // batch exhausted: advance every lane by 32 draws
+      st = add128(mul128(st, A32), C32);
+      start = 0;
+      continue;
+    }
+    if (i >= total) break;
+    // draw f misses the rectangle: its lane resolves the wedge / tail
+    int produced = 0, consumed = 1;
+    U128 last{0, 0};
+    if (lane == f) {
+      Pcg h;
+      h.slo = st.lo;
+      h.shi = st.hi;
+      h.ilo = inc.lo;
+      h.ihi = inc.hi;
+      if (idx == 0) {
+        TailRec rec;
+        rec.slice = k;
+        rec.index = i;
+        rec.negative = (int)((rabs >> 8) & 1);
+        int a = 0;
+        double val = 0.0;
+        for (;;) {
+          const double u1 = h.next_double(), u2 = h.next_double();
+          if (a < kTailAttempts) {
+            rec.u[2 * a] = u1;
+            rec.u[2 * a + 1] = u2;
           }
-          rec.attempts = a;
-          if (a > kTailAttempts) {
-            redo[k] = 1;
-          } else {
-            const int slot = atomicAdd(nrec, 1);
-            if (slot < cap) recs[slot] = rec;
-            else redo[k] = 1;
+          ++a;
+          const double xx = __dmul_rn(-kZigInvR, log1p(-u1));
+          const double yy = -log1p(-u2);
+          if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+            val = rec.negative ? -(kZigR + xx) : kZigR + xx;
+            break;
           }
-          break;
         }
+        rec.attempts = a;
+        consumed = 1 + 2 * a;
+        if (a > kTailAttempts) {
+          redo[k] = 1;
+        } else {
+          const int slot = atomicAdd(nrec, 1);
+          if (slot < cap) recs[slot] = rec;
+          else redo[k] = 1;
+        }
+        o[(i / s) * sp + i % s] = val;
+        produced = 1;
+      } else {
         const double f0 = fi_s[idx - 1];
         const double f1 = fi_s[idx];
-        const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(f0, -f1), g.next_double()), f1);
-        if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) { val = x; break; }
+        const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(f0, -f1), h.next_double()), f1);
+        consumed = 2;
+        if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
+          o[(i / s) * sp + i % s] = x;
+          produced = 1;
+        }
       }
-      o[(size_t)j * sp + c] = val;
+      last = U128{h.slo, h.shi};  // state of the last consumed draw
     }
-    for (int c = s; c < sp; ++c) o[(size_t)j * sp + c] = 0.0;
+    produced = __shfl_sync(0xffffffffu, produced, f);
+    consumed = __shfl_sync(0xffffffffu, consumed, f);
+    i += produced;
+    const int nstart = f + consumed;
+    if (nstart < 32) {
+      start = nstart;  // lanes still hold the draws behind the consumed ones
+      continue;
+    }
+    // re-base: draw (base + nstart) = A * last + inc, then lane offsets
+    last.lo = __shfl_sync(0xffffffffu, last.lo, f);
+    last.hi = __shfl_sync(0xffffffffu, last.hi, f);
+    b = add128(mul128(last, A), inc);
+    st = add128(mul128(b, Al), Cl);
+    start = 0;
   }
-  (void)total;
 }
 
 cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp, const int64_t* slice_ids,
                       double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st) {
   cudaMemsetAsync(nrec, 0, sizeof(int32_t), st);
   cudaMemsetAsync(redo, 0, sizeof(int32_t) * K, st);
-  omega_kernel<<<(unsigned)((K + 31) / 32), 32, 0, st>>>(seed, K, J, s_k, sp, slice_ids, out,
-                                                          static_cast<TailRec*>(recs), cap, nrec, redo);
+  omega_kernel<<<(unsigned)((K + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, sp, slice_ids, out,
+                                                        static_cast<TailRec*>(recs), cap, nrec, redo);
   return cudaGetLastError();
 }
 

@@ -38,6 +38,9 @@
 // the fp32-mode budget (BASELINE.json north_star: factors and fitness within
 // 1e-3).  fp64 storage keeps the DMMA path.
 #include <cuda.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include <cudaTypedefs.h>
 
 #include "dp2_common.cuh"
@@ -72,6 +75,7 @@ struct Params {
   double* g_part;
   int64_t* status;
   uint32_t off_b, off_y, off_yrow, off_bar;
+  unsigned long long* dbg;  // per-CTA wait-time counters (DP2_TC_DEBUG), or null
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -103,6 +107,22 @@ DP2_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
     if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
   }
 }
+DP2_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// wait with optional accounting into dbg slot k of this CTA
+#define TWAIT(barexpr, par, k)                                           \
+  do {                                                                   \
+    if (prm.dbg) {                                                       \
+      const unsigned long long t0_ = gtime();                            \
+      mbar_wait(barexpr, par);                                           \
+      dacc[k] += gtime() - t0_;                                          \
+    } else {                                                             \
+      mbar_wait(barexpr, par);                                           \
+    }                                                                    \
+  } while (0)
 DP2_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 DP2_DEV void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 DP2_DEV void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -185,6 +205,33 @@ DP2_DEV void tc_mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, 
       : "memory");
 }
 
+// elect.sync-predicated issue (whole warp executes; one lane issues)
+DP2_DEV void tc_mma_ss_e(uint32_t d, uint32_t alo, uint32_t blo, uint32_t hi, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %3};\n\tmov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %4, p;\n\t}" ::"r"(d),
+      "r"(alo), "r"(blo), "r"(hi), "r"(idesc), "r"(acc)
+      : "memory");
+}
+DP2_DEV void tc_mma_ts_e(uint32_t d, uint32_t a_tmem, uint32_t blo, uint32_t hi, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], db, %4, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "r"(blo), "r"(hi), "r"(idesc), "r"(acc)
+      : "memory");
+}
+DP2_DEV void tc_commit_e(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
 DP2_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -250,6 +297,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   __syncthreads();
   tc_after();
   const uint32_t tmem = tmem_slot;
+  const unsigned long long t_start = prm.dbg ? gtime() : 0ull;
+  unsigned long long dacc[16] = {};  // wait-time accounting (DP2_TC_DEBUG)
 
   // unit iteration shared by both producer groups
   auto first_unit = [&](int p) {
@@ -288,7 +337,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       while (cur.p < pend) {
         const int ss = (int)(ucount % (uint32_t)nss);
         const uint32_t fill = ucount / (uint32_t)nss;
-        if (fill > 0) mbar_wait(bar(BAR_RING + nss + ss), (fill - 1) & 1u);
+        if (fill > 0) TWAIT(bar(BAR_RING + nss + ss), (fill - 1) & 1u, 0);
         mbar_expect_tx(bar(BAR_RING + ss), 4 * CHUNK);
         const int row = (int)(cur.row0 + (int64_t)cur.t * TM);
 #pragma unroll
@@ -307,7 +356,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     const int bt = tid - B0;
     int pidx = 0;
     for (int p = pbeg; p < pend; ++p, ++pidx) {
-      if (pidx > 0) mbar_wait(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u);
+      if (pidx > 0) {
+        if (bt == 0) TWAIT(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u, 1);
+        else mbar_wait(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u);
+      }
       const double* Bm = prm.B + (size_t)prm.piece_slice[p] * J * sp;
       unsigned char* bb = gbase + prm.off_b;
       for (int e = bt; e < Jp * sp; e += NB) {
@@ -336,7 +388,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     uint32_t ucount = 0, tcount = 0;
     while (cur.p < pend) {
       const int ss = (int)(ucount % (uint32_t)nss);
-      mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
+      if (tid == 0) TWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 2);
+      else mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
       const unsigned char* srcb = gbase + (size_t)(ss * 4 + q) * CHUNK;
       float v0[32], v1[32];
 #pragma unroll
@@ -358,7 +411,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         v1[i] = tf32r(v1[i]);
       }
       sq += (double)s;
-      if (tcount > 0) mbar_wait(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u);
+      if (tcount > 0) {
+        if (tid == 0) TWAIT(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u, 3);
+        else mbar_wait(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u);
+      }
       tc_after();
       tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64), v0);
       tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32), v1);
@@ -393,50 +449,68 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     }
   } else if (warp == MMA_WARP) {
     // ===================================================== MMA issuer
-    if (lane == 0) {
-      const uint32_t id1 = idesc_tf32(64, sp, 0, 0);   // X (smem, K-major) x B^T (K-major)
-      const uint32_t id2 = idesc_tf32(128, n2, 0, 0);  // X^T (TMEM) x Y^T (K-major)
-      uint32_t ucount = 0, tcount = 0;
-      int pidx = 0;
-      for (int p = pbeg; p < pend; ++p, ++pidx) {
-        const int ntiles = (prm.piece_rows[p] + TM - 1) / TM;
-        mbar_wait(bar(BAR_BFULL), (uint32_t)pidx & 1u);
-        tc_after();
-        for (int t = 0; t < ntiles; ++t, ++tcount) {
-          for (int jb = 0; jb < nsup; ++jb, ++ucount) {  // P1: Y = X B
-            const int ss = (int)(ucount % (uint32_t)nss);
-            mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
-            tc_after();
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch)
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t a = sdesc(ring + (uint32_t)(ss * 4 + ch) * CHUNK + kk * 32, 16, 1024);
-                const uint64_t b = sdesc(bsm + (uint32_t)(jb * 4 + ch) * sp * 128 + kk * 32, 16, 1024);
-                tc_mma(tmem + YCOL2, a, b, id1, (jb | ch | kk) != 0);
-              }
-            tc_commit(bar(BAR_RING + nss + ss));
-          }
-          if (t == ntiles - 1) tc_commit(bar(BAR_BFREE));
-          tc_commit(bar(BAR_YFULL));
-          mbar_wait(bar(BAR_YSFULL), tcount & 1u);
-          if (t == 0 && pidx > 0) mbar_wait(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u);
+    // The whole warp runs the loop (warp-uniform descriptor arithmetic on the
+    // uniform datapath: one add per MMA); elect.sync picks the issuing lane.
+    // Descriptor words: lo = start>>4 | LBO(16 B)>>4 << 16, hi = SBO(1024)>>4 |
+    // version 1 | SWIZZLE_128B; every operand address below is a compile-time
+    // offset from a per-unit base.
+    const uint32_t id1 = idesc_tf32(64, sp, 0, 0);   // X (smem, K-major) x B^T (K-major)
+    const uint32_t id2 = idesc_tf32(128, n2, 0, 0);  // X^T (TMEM) x Y^T (K-major)
+    const uint32_t dhi = (1024u >> 4) | (1u << 14) | (2u << 29);
+    const uint32_t lbo = 1u << 16;
+    const uint32_t ring_lo = (ring >> 4) | lbo, b_lo = (bsm >> 4) | lbo, y_lo = (ysm >> 4) | lbo;
+    const uint32_t bch = (uint32_t)sp * 8;  // one 32-column chunk of B^T, in 16 B units
+    uint32_t ucount = 0, tcount = 0;
+    int pidx = 0;
+#define MWAIT(barexpr, par, k)        \
+  do {                                \
+    if (lane == 0)                    \
+      TWAIT(barexpr, par, k);         \
+    else                              \
+      mbar_wait(barexpr, par);        \
+    __syncwarp();                     \
+  } while (0)
+    for (int p = pbeg; p < pend; ++p, ++pidx) {
+      const int ntiles = (prm.piece_rows[p] + TM - 1) / TM;
+      MWAIT(bar(BAR_BFULL), (uint32_t)pidx & 1u, 4);
+      tc_after();
+      for (int t = 0; t < ntiles; ++t, ++tcount) {
+        for (int jb = 0; jb < nsup; ++jb, ++ucount) {  // P1: Y = X B
+          const int ss = (int)(ucount % (uint32_t)nss);
+          MWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 5);
           tc_after();
-          for (int jb = 0; jb < nsup; ++jb) {  // P2: Z += X^T Y
-            mbar_wait(bar(BAR_XT + 2 * jb), tcount & 1u);
-            tc_after();
+          const uint32_t a0 = ring_lo + (uint32_t)ss * (4 * CHUNK / 16);
+          const uint32_t b0 = b_lo + (uint32_t)jb * 4 * bch;
+          const unsigned long long tp1 = prm.dbg ? gtime() : 0ull;
 #pragma unroll
-            for (int k = 0; k < TM / 8; ++k) {
-              const uint64_t b = sdesc(ysm + (uint32_t)(k >> 2) * n2 * 128 + (k & 3) * 32, 16, 1024);
-              tc_mma_ts(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, b, id2, (t > 0 || k > 0) ? 1u : 0u);
-            }
-            tc_commit(bar(BAR_XT + 2 * jb + 1));
-          }
+          for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_ss_e(tmem + YCOL2, a0 + ch * (CHUNK / 16) + kk * 2, b0 + ch * bch + kk * 2, dhi, id1,
+                          (jb | ch | kk) != 0);
+          tc_commit_e(bar(BAR_RING + nss + ss));
+          if (prm.dbg && lane == 0) dacc[11] += gtime() - tp1;
         }
-        tc_commit(bar(BAR_ZFULL));
+        if (t == ntiles - 1) tc_commit_e(bar(BAR_BFREE));
+        tc_commit_e(bar(BAR_YFULL));
+        MWAIT(bar(BAR_YSFULL), tcount & 1u, 6);
+        if (t == 0 && pidx > 0) MWAIT(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u, 7);
+        tc_after();
+        for (int jb = 0; jb < nsup; ++jb) {  // P2: Z += X^T Y
+          MWAIT(bar(BAR_XT + 2 * jb), tcount & 1u, 8);
+          tc_after();
+          const unsigned long long tp2 = prm.dbg ? gtime() : 0ull;
+#pragma unroll
+          for (int k = 0; k < TM / 8; ++k)
+            tc_mma_ts_e(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, y_lo + (k >> 2) * (n2 * 8) + (k & 3) * 2, dhi,
+                        id2, (t > 0 || k > 0) ? 1u : 0u);
+          tc_commit_e(bar(BAR_XT + 2 * jb + 1));
+          if (prm.dbg && lane == 0) dacc[12] += gtime() - tp2;
+        }
       }
+      tc_commit_e(bar(BAR_ZFULL));
     }
-    __syncwarp();
+#undef MWAIT
   } else {
     // ===================================================== epilogue
     const int q = warp & 3, et = tid - EPI0;
@@ -452,7 +526,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       const int prows = prm.piece_rows[p];
       const int ntiles = (prows + TM - 1) / TM;
       for (int t = 0; t < ntiles; ++t, ++tcount) {
-        mbar_wait(bar(BAR_YFULL), tcount & 1u);
+        if (et == 0) TWAIT(bar(BAR_YFULL), tcount & 1u, 9);
+        else mbar_wait(bar(BAR_YFULL), tcount & 1u);
         tc_after();
         uint32_t v[32];
         tmem_ld32(tmem + lane_off + YCOL2, v);
@@ -505,7 +580,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         }
       }
       // piece complete: Z (TMEM lanes = columns of X) -> fp64 partial
-      mbar_wait(bar(BAR_ZFULL), (uint32_t)pidx & 1u);
+      if (et == 0) TWAIT(bar(BAR_ZFULL), (uint32_t)pidx & 1u, 10);
+      else mbar_wait(bar(BAR_ZFULL), (uint32_t)pidx & 1u);
       tc_after();
       double* out = prm.out_part + (size_t)p * J * sp;
       for (int jb = 0; jb < nsup; ++jb) {
@@ -535,6 +611,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         }
       }
     }
+  }
+  if (prm.dbg) {
+    // each slot is accounted by exactly one thread; the others add zeros
+    if (tid == 0) dacc[15] = gtime() - t_start;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (dacc[k]) atomicAdd(prm.dbg + blockIdx.x * 16 + k, dacc[k]);
   }
   tc_before();
   __syncthreads();
@@ -631,8 +714,30 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
   prm.status = status;
   cudaError_t e = cudaFuncSetAttribute(tcs::sketch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  static const bool debug = getenv("DP2_TC_DEBUG") != nullptr;
+  if (debug) {
+    cudaMalloc(&prm.dbg, (size_t)st->nseg * 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prm.dbg, 0, (size_t)st->nseg * 16 * sizeof(unsigned long long), stream);
+  }
   tcs::sketch_tc_kernel<<<st->nseg, tcs::NTHREADS, smem, stream>>>(prm, xmap);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (debug && e == cudaSuccess) {
+    std::vector<unsigned long long> h((size_t)st->nseg * 16);
+    cudaMemcpyAsync(h.data(), prm.dbg, h.size() * 8, cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    const char* names[16] = {"tma.empty", "b.bfree", "xt.full", "xt.xtfree", "mma.bfull", "mma.full", "mma.ysfull",
+                             "mma.zfree", "mma.xtfull", "epi.yfull", "epi.zfull", "mma.p1issue", "mma.p2issue", "", "", "total"};
+    fprintf(stderr, "[dp2 tc] pass (%s) mean us per CTA:", y_out ? "2" : "1");
+    for (int k = 0; k < 16; ++k) {
+      if (!names[k][0]) continue;
+      double m = 0;
+      for (int c = 0; c < st->nseg; ++c) m += h[(size_t)c * 16 + k];
+      fprintf(stderr, " %s=%.1f", names[k], m / st->nseg / 1e3);
+    }
+    fprintf(stderr, "\n");
+    cudaFree(prm.dbg);
+  }
+  return e;
 }
 
 }  // namespace dp2

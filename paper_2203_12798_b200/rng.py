@@ -13,7 +13,6 @@ with stage 1, and as the test reference).
 """
 from __future__ import annotations
 
-import math
 import os
 from concurrent.futures import ThreadPoolExecutor
 
@@ -85,22 +84,14 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
     if count:
         r = recs[:min(count, cap)].cpu().numpy().view(_REC).reshape(-1)
         vals = np.empty(r.size)
-        ok = np.ones(r.size, dtype=bool)
-        done = np.zeros(r.size, dtype=bool)
-        # replay each attempt with the C library's log1p -- the function the
-        # reference sampler calls (npy_log1p); NumPy's np.log1p ufunc may use
-        # a SIMD implementation with different last-bit rounding
-        log1p = np.frompyfunc(math.log1p, 1, 1)
-        for a in range(4):
-            xx = -_ZIG_INV_R * log1p(-r["u"][:, 2 * a]).astype(np.float64)
-            yy = -log1p(-r["u"][:, 2 * a + 1]).astype(np.float64)
-            acc = (yy + yy) > (xx * xx)
-            last = r["attempts"] == a + 1
-            live = ~done & (r["attempts"] >= a + 1)
-            ok &= ~(live & (acc != last))
-            hit = live & last
-            vals[hit] = np.where(r["negative"][hit] != 0, -(_ZIG_R + xx[hit]), _ZIG_R + xx[hit])
-            done |= hit
+        okv = np.empty(r.size, dtype=np.int32)
+        # replay each attempt with the C library's log1p (dp2_omega_replay) --
+        # the function the reference sampler calls (npy_log1p); NumPy's
+        # np.log1p ufunc may use a SIMD implementation with different rounding
+        _lib.check(_lib.lib().dp2_omega_replay(C.c_void_p(r.ctypes.data), r.size,
+                                               vals.ctypes.data_as(C.POINTER(C.c_double)),
+                                               okv.ctypes.data_as(C.POINTER(C.c_int32))), "omega_replay")
+        ok = okv != 0
         redo_h[r["slice"][~ok]] = 1
         good = ok & (redo_h[r["slice"]] == 0)
         if good.any():

@@ -84,3 +84,54 @@ def test_piece_plan_invariants(seed):
     for k in range(len(rows)):
         assert all(ps[p] == k for p in range(sl[k], sl[k + 1]))
         assert sum(int(prs[p]) for p in range(sl[k], sl[k + 1])) == rows[k]
+
+
+def test_omega_tail_replay_matches_python_log1p():
+    """dp2_omega_replay (host C, libm log1p) == the Python restatement of the
+    reference's layer-0 tail branch (math.log1p is libm's log1p too)."""
+    import ctypes as C
+    import math
+
+    from paper_2203_12798_b200 import _lib
+    from paper_2203_12798_b200.rng import _REC, _ZIG_INV_R, _ZIG_R
+
+    rng = np.random.default_rng(11)
+    n = 4000
+    r = np.zeros(n, dtype=_REC)
+    r["slice"] = rng.integers(0, 50, n)
+    r["index"] = rng.integers(0, 10000, n)
+    r["negative"] = rng.integers(0, 2, n)
+    r["u"] = rng.random((n, 8))
+    want_v, want_ok = np.zeros(n), np.zeros(n, dtype=np.int32)
+    for i in range(n):
+        # the acceptance sequence decides the attempt count the device saw
+        a_acc = None
+        for a in range(4):
+            xx = -_ZIG_INV_R * math.log1p(-r["u"][i, 2 * a])
+            yy = -math.log1p(-r["u"][i, 2 * a + 1])
+            if yy + yy > xx * xx:
+                a_acc = a
+                break
+        r["attempts"][i] = (a_acc + 1) if a_acc is not None else 4
+        if i % 7 == 0:  # a device that disagreed: claims a different attempt
+            r["attempts"][i] = 1 + (r["attempts"][i] % 4)
+        ok = 1
+        v = 0.0
+        for a in range(r["attempts"][i]):
+            xx = -_ZIG_INV_R * math.log1p(-r["u"][i, 2 * a])
+            yy = -math.log1p(-r["u"][i, 2 * a + 1])
+            acc = (yy + yy) > (xx * xx)
+            last = a + 1 == r["attempts"][i]
+            if acc != last:
+                ok = 0
+            if last:
+                v = -(_ZIG_R + xx) if r["negative"][i] else _ZIG_R + xx
+        want_v[i], want_ok[i] = v, ok
+    vals = np.empty(n)
+    okv = np.empty(n, dtype=np.int32)
+    assert _lib.lib().dp2_omega_replay(C.c_void_p(r.ctypes.data), n, vals.ctypes.data_as(C.POINTER(C.c_double)),
+                                       okv.ctypes.data_as(C.POINTER(C.c_int32))) == 0
+    assert np.array_equal(okv, want_ok)
+    good = want_ok == 1  # values of rejected records are never used
+    assert np.array_equal(vals[good].view(np.uint64), want_v[good].view(np.uint64))
+    assert 0 < want_ok.sum() < n
