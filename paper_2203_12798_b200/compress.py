@@ -159,7 +159,9 @@ def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None):
     dev = M.device
     lib = _lib.lib()
     om2 = om2 if isinstance(om2, torch.Tensor) else torch.from_numpy(om2)
-    om2 = om2.to(dev)
+    if om2.device.type == "cpu" and not om2.is_pinned():
+        om2 = om2.pin_memory()
+    om2 = om2.to(dev, non_blocking=True)
     D = torch.empty((J, rank), dtype=torch.float64, device=dev)
     E = torch.empty(rank, dtype=torch.float64, device=dev)
     F = torch.empty((KR, rank), dtype=torch.float64, device=dev)
@@ -179,6 +181,16 @@ def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None):
 def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
              plan=None, threads=None, timings=None):
     """Compress ``tensor`` at ``rank`` with two randomized-SVD stages."""
+    comp, status = compress_async(tensor, rank, rsvd, stage2, plan, threads, timings)
+    check_status(status, "compress")
+    return comp
+
+
+def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
+                   plan=None, threads=None, timings=None):
+    """``compress`` without the host synchronisation of its status check:
+    returns (CompressedTensor, device status block); the caller checks the
+    status (check_status) once its later work is enqueued."""
     if not isinstance(tensor, IrregularTensor):
         tensor = IrregularTensor(tensor)
     check_rank(tensor, rank)
@@ -194,9 +206,8 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
     A, M, rank_found, status = run_stage1(tensor, rank, base, timings=timings)
     om2_thread.join()
     D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2_box["v"], status, timings=timings)
-    check_status(status, "compress")
     return CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
-                            cores=F, rank_found=rank_found)
+                            cores=F, rank_found=rank_found), status
 
 
 def reconstruct_slice(comp: CompressedTensor, k):

@@ -71,10 +71,57 @@ class Parafac2Factors:
         """Host copy (NumPy) of device factors."""
         if isinstance(self.H, np.ndarray):
             return self
-        qp = self.Q_packed.cpu().numpy()
+        qp = device_to_numpy(self.Q_packed)
+        H, V, W = (t.cpu().numpy() for t in (self.H, self.V, self.W))
         bounds = np.cumsum([0] + [q.shape[0] for q in self.Q])
-        return Parafac2Factors(H=self.H.cpu().numpy(), V=self.V.cpu().numpy(), W=self.W.cpu().numpy(),
-                               Q=[qp[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=qp)
+        return Parafac2Factors(H=H, V=V, W=W, Q=[qp[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=qp)
+
+
+_STAGE = {}
+
+
+def device_to_numpy(t, chunk_bytes=32 << 20, threads=8):
+    """Large device tensor -> new NumPy array at PCIe speed: chunked async D2H
+    into a reused pair of pinned staging buffers, each chunk copied out on
+    host threads while the next one is in flight.  (A pageable destination
+    would go through the driver's slow staging path; a fresh pinned
+    allocation per call costs more than the copy.)"""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    n = t.numel() * t.element_size()
+    if n <= chunk_bytes:
+        return t.cpu().numpy()
+    dev = t.device
+    if "buf" not in _STAGE:
+        _STAGE["buf"] = [torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        _STAGE["ev"] = [torch.cuda.Event() for _ in range(2)]
+        _STAGE["pool"] = ThreadPoolExecutor(threads)
+    bufs, evs, pool = _STAGE["buf"], _STAGE["ev"], _STAGE["pool"]
+    src = t.contiguous().view(-1).view(torch.uint8)
+    out = np.empty(tuple(t.shape), dtype=t.cpu().numpy().dtype if t.numel() == 0 else
+                   {torch.float64: np.float64, torch.float32: np.float32, torch.int64: np.int64,
+                    torch.int32: np.int32}[t.dtype])
+    dst = out.reshape(-1).view(np.uint8)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream()
+        chunks = [(o, min(chunk_bytes, n - o)) for o in range(0, n, chunk_bytes)]
+
+        def host_copy(i):
+            o, nb = chunks[i]
+            b = bufs[i % 2].numpy()
+            evs[i % 2].synchronize()
+            step = -(-nb // threads)
+            spans = [(a, min(nb, a + step)) for a in range(0, nb, step)]
+            list(pool.map(lambda ab: np.copyto(dst[o + ab[0]:o + ab[1]], b[ab[0]:ab[1]]), spans))
+
+        for i, (o, nb) in enumerate(chunks):
+            if i >= 2:
+                host_copy(i - 2)  # frees buffer i % 2 before reuse
+            bufs[i % 2][:nb].copy_(src[o:o + nb], non_blocking=True)
+            evs[i % 2].record(stream)
+        for i in range(max(0, len(chunks) - 2), len(chunks)):
+            host_copy(i)
+    return out
 
 
 def initial_factors(num_cols, num_slices, rank, seed=0):

@@ -76,13 +76,21 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
     _lib.check(_lib.lib().dp2_omega_generate(C.c_uint64(seed & _MASK64), K, n, vp(s_dev), sp, vp(ids), vp(out),
                                              vp(recs), cap, vp(nrec), vp(redo),
                                              C.c_void_p(torch.cuda.current_stream().cuda_stream)), "omega")
-    count = int(nrec.item())
-    redo_h = redo.cpu().numpy()
+    # one readback: record count, per-slice redo flags and the records
+    nrec_h = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    redo_h_t = torch.empty(K, dtype=torch.int32, pin_memory=True)
+    recs_h = torch.empty(tuple(recs.shape), dtype=torch.uint8, pin_memory=True)
+    nrec_h.copy_(nrec, non_blocking=True)
+    redo_h_t.copy_(redo, non_blocking=True)
+    recs_h.copy_(recs, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    count = int(nrec_h[0])
+    redo_h = redo_h_t.numpy().copy()
     if count > cap:
         redo_h[:] = 1  # record overflow: regenerate everything on the host (never expected)
     patched = 0
     if count:
-        r = recs[:min(count, cap)].cpu().numpy().view(_REC).reshape(-1)
+        r = recs_h[:min(count, cap)].numpy().view(_REC).reshape(-1)
         vals = np.empty(r.size)
         okv = np.empty(r.size, dtype=np.int32)
         # replay each attempt with the C library's log1p (dp2_omega_replay) --

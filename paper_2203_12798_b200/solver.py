@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressedTensor, _vp, check_status, compress, nseg_for, workspace
+from .compress import CompressedTensor, _vp, check_status, compress, compress_async, nseg_for, workspace
 from .factors import FitTrace, Parafac2Factors, SolverOptions, initial_factors
 from .linalg import RsvdParams
 from .scheduler import resolve_threads
@@ -136,6 +136,13 @@ def convergence_metric(comp, rotations, h, v, w, threads=None):
 
 def run_als(comp: CompressedTensor, h, v, w, max_iters, tol, normalize, use_graph=True):
     """Device iteration loop; returns (H, V, W, polar, trace list, seconds list)."""
+    launched = _als_launch(comp, h, v, w, max_iters, tol, normalize, use_graph)
+    return _als_collect(launched)
+
+
+def _als_launch(comp: CompressedTensor, h, v, w, max_iters, tol, normalize, use_graph=True):
+    """Enqueue the ALS loop; returns device outputs plus pinned readback slots
+    filled by non-blocking copies (read them after a stream synchronise)."""
     dev = comp.cores.device
     K, J, R = comp.num_slices, comp.num_cols, comp.rank
     F, D, E = _comp_args(comp)
@@ -150,10 +157,21 @@ def run_als(comp: CompressedTensor, h, v, w, max_iters, tol, normalize, use_grap
     _lib.check(lib.dp2_als_run(_vp(F), _vp(D), _vp(E), K, J, R, _vp(H), _vp(V), _vp(W), _vp(polar), max_iters,
                                float(tol), int(bool(normalize)), _vp(trace), _vp(tstamp), _vp(iters),
                                int(bool(use_graph)), _vp(ws), ws.numel(), _vp(status), stream_ptr()), "als_run")
-    n = int(iters.item())
-    check_status(status, "fit_dpar2")
-    tr = trace[:n].cpu().tolist()
-    ts = tstamp[:n + 1].cpu().numpy()
+    host = {}
+    for name, t in (("iters", iters), ("trace", trace), ("tstamp", tstamp), ("status", status)):
+        host[name] = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        host[name].copy_(t, non_blocking=True)
+    return H, V, W, polar, host
+
+
+def _als_collect(launched, synced=False):
+    H, V, W, polar, host = launched
+    if not synced:
+        torch.cuda.current_stream().synchronize()
+    check_status(host["status"], "fit_dpar2")
+    n = int(host["iters"][0])
+    tr = host["trace"][:n].tolist()
+    ts = host["tstamp"][:n + 1].numpy()
     secs = list(np.diff(ts) * 1e-9)
     return H, V, W, polar, tr, secs
 
@@ -184,18 +202,30 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     normalize = bool(opts.normalize) if opts.normalize is not None else True
     if not isinstance(tensor, IrregularTensor):
         tensor = IrregularTensor(tensor)
+    # one host synchronisation per fit (besides the Omega tail readback): the
+    # compression status, ALS outputs and Q assembly are all enqueued first
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
     started = time.perf_counter()
-    comp = compress(tensor, rank, rsvd=RsvdParams(rank=rank, seed=opts.seed), timings=timings)
-    torch.cuda.synchronize()
-    trace = FitTrace(preprocess_seconds=time.perf_counter() - started, compressed_float_count=comp.float_count())
+    ev0.record()
+    comp, cstatus = compress_async(tensor, rank, rsvd=RsvdParams(rank=rank, seed=opts.seed), timings=timings)
+    ev1.record()
+    cstatus_h = torch.empty(tuple(cstatus.shape), dtype=cstatus.dtype, pin_memory=True)
+    cstatus_h.copy_(cstatus, non_blocking=True)
+    host_pre = time.perf_counter() - started
     h, v, w = initial_factors(tensor.num_cols, tensor.num_slices, rank, opts.seed)
-    H, V, W, polar, tr, secs = run_als(comp, h, v, w, opts.max_iters, opts.tol, normalize, use_graph=use_graph)
+    launched = _als_launch(comp, h, v, w, opts.max_iters, opts.tol, normalize, use_graph=use_graph)
+    Q = assemble_q(tensor, comp, launched[3])
+    torch.cuda.current_stream().synchronize()
+    check_status(cstatus_h, "compress")
+    H, V, W, polar, tr, secs = _als_collect(launched, synced=True)
+    trace = FitTrace(preprocess_seconds=max(host_pre, ev0.elapsed_time(ev1) * 1e-3),
+                     compressed_float_count=comp.float_count())
     trace.objective = tr
     trace.seconds = secs
     if len(tr) >= 2:
         prev, e = tr[-2], tr[-1]
         trace.converged = bool(prev == 0.0 or abs(prev - e) <= opts.tol * prev)
-    Q = assemble_q(tensor, comp, polar)
     bounds = tensor.row_off_host
     factors = Parafac2Factors(H=H, V=V, W=W, Q=[Q[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=Q)
     if output == "numpy":

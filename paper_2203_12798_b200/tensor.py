@@ -43,6 +43,32 @@ def sm_count():
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
+def _coalesce_pinned(arrs, J, tdt):
+    """Merge runs of row-adjacent, contiguous pinned host tensors that view one
+    storage (e.g. slices cut from one pinned buffer) into single tensors, so
+    the upload is one large async copy per run instead of one per slice."""
+    out, run, run_rows, end = [], None, 0, None
+    for a in arrs:
+        ok = (isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dtype == tdt and a.is_contiguous()
+              and a.shape[1] == J and a.is_pinned())
+        if ok and run is not None and a.untyped_storage().data_ptr() == run.untyped_storage().data_ptr() \
+                and a.data_ptr() == end:
+            run_rows += a.shape[0]
+            end = a.data_ptr() + a.numel() * a.element_size()
+            continue
+        if run is not None:
+            out.append(torch.empty(0, dtype=tdt).set_(run.untyped_storage(), run.storage_offset(), (run_rows, J),
+                                                      (J, 1)))
+            run = None
+        if ok:
+            run, run_rows, end = a, a.shape[0], a.data_ptr() + a.numel() * a.element_size()
+        else:
+            out.append(a)
+    if run is not None:
+        out.append(torch.empty(0, dtype=tdt).set_(run.untyped_storage(), run.storage_offset(), (run_rows, J), (J, 1)))
+    return out
+
+
 class IrregularTensor:
     """K dense slices (I_k x J) sharing the column count J, packed on the GPU."""
 
@@ -110,7 +136,7 @@ class IrregularTensor:
         self.X = torch.zeros((total, self.ldx), dtype=tdt, device=dev) if self.ldx != J else \
             torch.empty((total, J), dtype=tdt, device=dev)
         r = 0
-        for a in arrs:
+        for a in _coalesce_pinned(arrs, J, tdt):
             n = a.shape[0]
             if isinstance(a, torch.Tensor):
                 # pinned host tensors go straight into the packed buffer (async H2D)
