@@ -196,7 +196,7 @@ int dp2_stream_pass(const dp2_store* st, const double* b_dev, int32_t sp, double
   if (!store_ok(st) || sp < 1 || !b_dev || !out_part) return fail_arg("invalid stream-pass arguments");
   if (g_part && sp > 32) return fail_arg("g_part needs sp <= 32");
   cudaError_t e = dp2::run_sketch(st, b_dev, sp, out_part, y_out, xsq_part, status_dev, S(stream), g_part);
-  return e == cudaSuccess ? ok(1) : fail(e, "dp2_stream_pass");
+  return e == cudaSuccess ? ok(dp2::sketch_tc_eligible(st, sp) ? 2 : 1) : fail(e, "dp2_stream_pass");
 }
 
 size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
@@ -212,7 +212,9 @@ int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_de
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
                                   static_cast<char*>(ws), status_dev, timing_ms, S(stream));
-  return e == cudaSuccess ? ok(sp <= 32 ? 9 : 8) : fail(e, "dp2_stage1");
+  // + the B-image kernel of each tensor-core streaming pass and gram_y_kernel
+  const int tc = dp2::sketch_tc_eligible(st, sp) ? 3 : 0;
+  return e == cudaSuccess ? ok((sp <= 32 ? 9 : 8) + tc) : fail(e, "dp2_stage1");
 }
 
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {

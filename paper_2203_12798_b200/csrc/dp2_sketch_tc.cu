@@ -51,13 +51,15 @@ namespace tcs {
 
 constexpr int TM = 64;             // rows per tile
 constexpr int CHUNK = TM * 128;    // bytes of one 32-column chunk (64 rows x 128 B)
-constexpr int NXT = 128;           // X^T producers + statistics (warps 0-3)
-constexpr int B0 = 128, NB = 128;  // B (Omega / Q_Z) converters (warps 4-7)
+constexpr int NXT = 256;           // X^T producers + statistics (warps 0-7)
 constexpr int MMA_WARP = 8;
 constexpr int EPI0 = 9 * 32;       // first epilogue thread (warps 9-12)
 constexpr int NEPI = 128;
-constexpr int TMA_WARP = 13;
-constexpr int NTHREADS = 14 * 32;
+constexpr int TMA_WARP = 13;       // lane 0: X boxes into the ring; lane 1: B image per piece
+constexpr int P2_WARP = 14;        // P2 issuer (P1 is issued by MMA_WARP)
+constexpr int AUX0 = 15 * 32;      // first aux epilogue thread (warps 15-18): Y rows + G in pass 2
+constexpr int NAUX = 128;
+constexpr int NTHREADS = 19 * 32;
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
@@ -65,6 +67,8 @@ struct Params {
   int64_t ldx;
   int J, Jp, sp, n2, nslot, nsup;
   const double* B;
+  const float* btile;  // B pre-tiled per slice in the shared-memory image (tf32, K-major SW128)
+  uint32_t bbytes;     // bytes of one slice's image
   const int32_t* piece_slice;
   const int64_t* piece_row0;
   const int32_t* piece_rows;
@@ -123,6 +127,12 @@ DP2_DEV unsigned long long gtime() {
       mbar_wait(barexpr, par);                                           \
     }                                                                    \
   } while (0)
+// one arrival per warp (barrier counts in warps): __syncwarp orders the
+// lanes' prior accesses before lane 0's release-arrive
+DP2_DEV void warp_arrive(uint32_t bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 DP2_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 DP2_DEV void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 DP2_DEV void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -138,7 +148,10 @@ DP2_DEV void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// tcgen05.ld/st are .sync.aligned: call sites that follow lane-divergent code
+// (single-lane barrier waits, statistics) must reconverge first
 DP2_DEV void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  __syncwarp();
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
       "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -174,9 +187,12 @@ DP2_DEV uint32_t swz(int row, int col) {
 
 // barrier slots (uint64 each) after off_bar
 enum : int {
-  BAR_BFULL = 0, BAR_BFREE, BAR_YFULL, BAR_YSFULL, BAR_ZFULL, BAR_ZFREE,
-  BAR_XT = 8,    // 4 x (full, free) for the TMEM X^T blocks
-  BAR_RING = 16  // nss x full, nss x empty
+  BAR_BFULL = 0, BAR_BFREE, BAR_YSFULL = 3, BAR_ZFULL, BAR_ZFREE,
+  BAR_XT = 8,       // 4 x (full, free) for the TMEM X^T blocks
+  BAR_YFULL = 16,   // [2] Y accumulator b holds tile t (P1 commit)
+  BAR_YFREE = 18,   // [2] epilogue has read Y accumulator b
+  BAR_YSTFREE = 20, // P2 has consumed the Y^T staging buffer
+  BAR_RING = 24     // nss x full, nss x empty
 };
 
 struct Unit {  // 64 rows x 128 columns of one tile
@@ -185,6 +201,7 @@ struct Unit {  // 64 rows x 128 columns of one tile
 };
 
 DP2_DEV void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  __syncwarp();
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
       "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
@@ -235,6 +252,11 @@ DP2_DEV void tc_commit_e(uint32_t bar) {
 DP2_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+DP2_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 DP2_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -267,17 +289,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   if (tid == 0) {
     mbar_init(bar(BAR_BFULL), 1);
     mbar_init(bar(BAR_BFREE), 1);
-    mbar_init(bar(BAR_YFULL), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(BAR_YFULL + b), 1);
+      mbar_init(bar(BAR_YFREE + b), (prm.y_out || prm.g_part) ? NEPI + NAUX : NEPI);
+    }
+    mbar_init(bar(BAR_YSTFREE), 1);
     mbar_init(bar(BAR_YSFULL), NEPI);
     mbar_init(bar(BAR_ZFULL), 1);
     mbar_init(bar(BAR_ZFREE), NEPI);
     for (int jb = 0; jb < 4; ++jb) {
-      mbar_init(bar(BAR_XT + 2 * jb), NXT);
+      mbar_init(bar(BAR_XT + 2 * jb), NXT / 32);
       mbar_init(bar(BAR_XT + 2 * jb + 1), 1);
     }
     for (int s = 0; s < nss; ++s) {
       mbar_init(bar(BAR_RING + s), 1);  // TMA thread's arrive.expect_tx
-      mbar_init(bar(BAR_RING + nss + s), 1 + NXT);  // P1 commit + X^T copies
+      mbar_init(bar(BAR_RING + nss + s), 1 + NXT / 32);  // P1 commit + one per X^T warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -331,6 +357,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     // unit = 4 boxes of 64 rows x 32 columns (128 B inner, SWIZZLE_128B: the
     // UMMA K-major SW128 layout); rows past the piece or the store are other
     // slices' rows or TMA zero fill -- masked downstream (Y^T rows, X^T rows).
+    if (lane == 1) {  // B image of each piece's slice, once P1 of the previous piece released it
+      int pidx = 0;
+      for (int p = pbeg; p < pend; ++p, ++pidx) {
+        if (pidx > 0) TWAIT(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u, 1);
+        mbar_expect_tx(bar(BAR_BFULL), prm.bbytes);
+        bulk_load(bsm, prm.btile + (size_t)prm.piece_slice[p] * (prm.bbytes / 4), prm.bbytes, bar(BAR_BFULL));
+      }
+    }
     if (lane == 0) {
       Unit cur = first_unit(pbeg);
       uint32_t ucount = 0;
@@ -349,41 +383,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       }
     }
     __syncwarp();
-  } else if (tid >= B0 && tid < B0 + NB) {
-    // ===================================================== B converters
-    // per piece: Omega_k / Q_Z,k (fp64, J x sp) -> tf32 K-major SW128 smem,
-    // once P1 of the previous piece has released the buffer
-    const int bt = tid - B0;
-    int pidx = 0;
-    for (int p = pbeg; p < pend; ++p, ++pidx) {
-      if (pidx > 0) {
-        if (bt == 0) TWAIT(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u, 1);
-        else mbar_wait(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u);
-      }
-      const double* Bm = prm.B + (size_t)prm.piece_slice[p] * J * sp;
-      unsigned char* bb = gbase + prm.off_b;
-      for (int e = bt; e < Jp * sp; e += NB) {
-        const int j = e / sp, c = e - j * sp;
-        const float v = j < J ? tf32r((float)Bm[(size_t)j * sp + c]) : 0.0f;
-        *reinterpret_cast<float*>(bb + (size_t)(j >> 5) * sp * 128 + swz(c, j & 31)) = v;
-      }
-      fence_async_smem();
-      named_sync(3, NB);
-      if (bt == 0) mbar_arrive(bar(BAR_BFULL));
-    }
   } else if (tid < NXT) {
     // ===================================================== X^T producers
-    // thread (q = warp, lane) owns column 32 q + lane of every unit: it reads
-    // that column's 64 rows from ring chunk q (one 128 B swizzled row per
-    // warp-wide LDS, conflict-free), releases the slot, zeroes rows past the
-    // piece, accumulates the piece statistics, rounds to tf32 (rna) and stores
-    // the column to TMEM lane 32 q + lane, columns jb*64 .. +63 once P2 of the
-    // previous tile has consumed that block.
-    const int q = warp;
+    // thread (q = warp % 4, h = warp / 4, lane) owns column 32 q + lane of
+    // every unit, rows 32 h .. 32 h + 31: one 128 B swizzled ring row per
+    // warp-wide LDS (conflict-free), rows past the piece zeroed, statistics,
+    // rna rounding, one tcgen05.st.32x32b.x32 to TMEM lane 32 q + lane,
+    // columns jb*64 + 32 h, once P2 of the previous tile consumed block jb.
+    const int q = warp & 3, h = warp >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool stats = prm.xsq_part != nullptr;
     double sq = 0.0;
-    float probe = 0.0f;
+    int bad = 0;
     Unit cur = first_unit(pbeg);
     uint32_t ucount = 0, tcount = 0;
     while (cur.p < pend) {
@@ -391,41 +402,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       if (tid == 0) TWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 2);
       else mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
       const unsigned char* srcb = gbase + (size_t)(ss * 4 + q) * CHUNK;
-      float v0[32], v1[32];
+      float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        v0[i] = *reinterpret_cast<const float*>(srcb + swz(i, lane));
-        v1[i] = *reinterpret_cast<const float*>(srcb + swz(i + 32, lane));
-      }
-      mbar_arrive(bar(BAR_RING + nss + ss));  // release orders the loads above before it
-      float s = 0.0f;
+      for (int i = 0; i < 32; ++i) v[i] = *reinterpret_cast<const float*>(srcb + swz(h * 32 + i, lane));
+      warp_arrive(bar(BAR_RING + nss + ss));  // the loads above are ordered before it
+      const int rows_h = cur.rows - 32 * h;
+      if (rows_h < 32)  // rows past the piece (other slices' rows / TMA zero fill)
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        v0[i] = i < cur.rows ? v0[i] : 0.0f;
-        v1[i] = i + 32 < cur.rows ? v1[i] : 0.0f;
-        s = fmaf(v0[i], v0[i], s);
-        s = fmaf(v1[i], v1[i], s);
-        probe = fmaf(v0[i], 0.0f, probe);
-        probe = fmaf(v1[i], 0.0f, probe);
-        v0[i] = tf32r(v0[i]);
-        v1[i] = tf32r(v1[i]);
+        for (int i = 0; i < 32; ++i) v[i] = i < rows_h ? v[i] : 0.0f;
+      if (stats) {
+        float s = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s = fmaf(v[i], v[i], s);
+        if (!isfinite(s)) {  // Inf/NaN -- or an fp32 overflow of the squares: exact check
+          double sd = 0.0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            bad |= !isfinite(v[i]);
+            sd = fma((double)v[i], (double)v[i], sd);
+          }
+          sq += sd;
+        } else {
+          sq += (double)s;
+        }
       }
-      sq += (double)s;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = tf32r(v[i]);
       if (tcount > 0) {
         if (tid == 0) TWAIT(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u, 3);
         else mbar_wait(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u);
       }
       tc_after();
-      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64), v0);
-      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32), v1);
+      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32 * h), v);
       tc_before();
-      mbar_arrive(bar(BAR_XT + 2 * cur.jb));
+      warp_arrive(bar(BAR_XT + 2 * cur.jb));
       ++ucount;
       const Unit nx = next_unit(cur);
       if (nx.jb == 0) ++tcount;
       if (nx.p != cur.p && stats) {  // piece complete: sum of squares, non-finite flag
         const double tot = warp_sum(sq);
-        const int anybad = __any_sync(0xffffffffu, !isfinite(probe));
+        const int anybad = __any_sync(0xffffffffu, bad);
         if (lane == 0) {
           red[warp] = tot;
           red[16 + warp] = anybad ? 1.0 : 0.0;
@@ -443,12 +459,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         }
         named_sync(1, NXT);
         sq = 0.0;
-        probe = 0.0f;
+        bad = 0;
       }
       cur = nx;
     }
-  } else if (warp == MMA_WARP) {
-    // ===================================================== MMA issuer
+  } else if (warp == MMA_WARP || warp == P2_WARP) {
+    // ===================================================== MMA issuers (P1: MMA_WARP, P2: P2_WARP)
     // The whole warp runs the loop (warp-uniform descriptor arithmetic on the
     // uniform datapath: one add per MMA); elect.sync picks the issuing lane.
     // Descriptor words: lo = start>>4 | LBO(16 B)>>4 << 16, hi = SBO(1024)>>4 |
@@ -472,93 +488,121 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   } while (0)
     for (int p = pbeg; p < pend; ++p, ++pidx) {
       const int ntiles = (prm.piece_rows[p] + TM - 1) / TM;
-      MWAIT(bar(BAR_BFULL), (uint32_t)pidx & 1u, 4);
-      tc_after();
-      for (int t = 0; t < ntiles; ++t, ++tcount) {
-        for (int jb = 0; jb < nsup; ++jb, ++ucount) {  // P1: Y = X B
-          const int ss = (int)(ucount % (uint32_t)nss);
-          MWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 5);
-          tc_after();
-          const uint32_t a0 = ring_lo + (uint32_t)ss * (4 * CHUNK / 16);
-          const uint32_t b0 = b_lo + (uint32_t)jb * 4 * bch;
-          const unsigned long long tp1 = prm.dbg ? gtime() : 0ull;
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch)
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tc_mma_ss_e(tmem + YCOL2, a0 + ch * (CHUNK / 16) + kk * 2, b0 + ch * bch + kk * 2, dhi, id1,
-                          (jb | ch | kk) != 0);
-          tc_commit_e(bar(BAR_RING + nss + ss));
-          if (prm.dbg && lane == 0) dacc[11] += gtime() - tp1;
-        }
-        if (t == ntiles - 1) tc_commit_e(bar(BAR_BFREE));
-        tc_commit_e(bar(BAR_YFULL));
-        MWAIT(bar(BAR_YSFULL), tcount & 1u, 6);
-        if (t == 0 && pidx > 0) MWAIT(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u, 7);
+      if (warp == MMA_WARP) {  // P1: Y(t) = X(t) B into accumulator t % 2
+        MWAIT(bar(BAR_BFULL), (uint32_t)pidx & 1u, 4);
         tc_after();
-        for (int jb = 0; jb < nsup; ++jb) {  // P2: Z += X^T Y
-          MWAIT(bar(BAR_XT + 2 * jb), tcount & 1u, 8);
+        for (int t = 0; t < ntiles; ++t, ++tcount) {
+          const uint32_t b = tcount & 1u;
+          if (tcount >= 2) MWAIT(bar(BAR_YFREE + b), ((tcount >> 1) - 1) & 1u, 13);
           tc_after();
-          const unsigned long long tp2 = prm.dbg ? gtime() : 0ull;
+          for (int jb = 0; jb < nsup; ++jb, ++ucount) {
+            const int ss = (int)(ucount % (uint32_t)nss);
+            MWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 5);
+            tc_after();
+            const uint32_t a0 = ring_lo + (uint32_t)ss * (4 * CHUNK / 16);
+            const uint32_t b0 = b_lo + (uint32_t)jb * 4 * bch;
+            const unsigned long long tp1 = prm.dbg ? gtime() : 0ull;
 #pragma unroll
-          for (int k = 0; k < TM / 8; ++k)
-            tc_mma_ts_e(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, y_lo + (k >> 2) * (n2 * 8) + (k & 3) * 2, dhi,
-                        id2, (t > 0 || k > 0) ? 1u : 0u);
-          tc_commit_e(bar(BAR_XT + 2 * jb + 1));
-          if (prm.dbg && lane == 0) dacc[12] += gtime() - tp2;
+            for (int ch = 0; ch < 4; ++ch)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                tc_mma_ss_e(tmem + YCOL2 + 32 * b, a0 + ch * (CHUNK / 16) + kk * 2, b0 + ch * bch + kk * 2, dhi,
+                            id1, (jb | ch | kk) != 0);
+            tc_commit_e(bar(BAR_RING + nss + ss));
+            if (prm.dbg && lane == 0) dacc[11] += gtime() - tp1;
+          }
+          if (t == ntiles - 1) tc_commit_e(bar(BAR_BFREE));
+          tc_commit_e(bar(BAR_YFULL + b));
         }
+      } else {  // P2: Z += X^T(t) Y(t)
+        for (int t = 0; t < ntiles; ++t, ++tcount) {
+          MWAIT(bar(BAR_YSFULL), tcount & 1u, 6);
+          if (t == 0 && pidx > 0) MWAIT(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u, 7);
+          tc_after();
+          for (int jb = 0; jb < nsup; ++jb) {
+            MWAIT(bar(BAR_XT + 2 * jb), tcount & 1u, 8);
+            tc_after();
+            const unsigned long long tp2 = prm.dbg ? gtime() : 0ull;
+#pragma unroll
+            for (int k = 0; k < TM / 8; ++k)
+              tc_mma_ts_e(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, y_lo + (k >> 2) * (n2 * 8) + (k & 3) * 2,
+                          dhi, id2, (t > 0 || k > 0) ? 1u : 0u);
+            tc_commit_e(bar(BAR_XT + 2 * jb + 1));
+            if (prm.dbg && lane == 0) dacc[12] += gtime() - tp2;
+          }
+          tc_commit_e(bar(BAR_YSTFREE));
+        }
+        tc_commit_e(bar(BAR_ZFULL));
       }
-      tc_commit_e(bar(BAR_ZFULL));
     }
 #undef MWAIT
   } else {
     // ===================================================== epilogue
-    const int q = warp & 3, et = tid - EPI0;
+    // main group (warps 9-12): Y -> rounded Y^T staging for P2, non-finite
+    // flags (pass 1), the per-piece Z flush.  aux group (warps 15-18, pass 2
+    // only): Y rows (coalesced through smem) and G = Y^T Y (fp64 DMMA), off
+    // the staging -> P2 critical path.  Both read the Y accumulator.
+    const bool aux = warp >= AUX0 / 32;
+    const int q = warp & 3, et = aux ? tid - AUX0 : tid - EPI0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     unsigned char* yb = gbase + prm.off_y;
-    const bool pass2 = prm.y_out != nullptr;
+    const bool pass2 = prm.y_out != nullptr || prm.g_part != nullptr;  // Y rows and/or G wanted
     const bool do_g = prm.g_part != nullptr;
     const int ng = sp * sp;
     double gacc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     uint32_t tcount = 0;
     int pidx = 0;
-    for (int p = pbeg; p < pend; ++p, ++pidx) {
+    const int r = 16 * q + lane;  // M = 64 accumulator: row 16 q + l lives in TMEM lane 32 q + l (l < 16)
+    for (int p = pbeg; p < pend && (!aux || pass2); ++p, ++pidx) {
       const int prows = prm.piece_rows[p];
       const int ntiles = (prows + TM - 1) / TM;
       for (int t = 0; t < ntiles; ++t, ++tcount) {
-        if (et == 0) TWAIT(bar(BAR_YFULL), tcount & 1u, 9);
-        else mbar_wait(bar(BAR_YFULL), tcount & 1u);
+        const uint32_t b = tcount & 1u;
+        if (et == 0 && !aux) TWAIT(bar(BAR_YFULL + b), (tcount >> 1) & 1u, 9);
+        else mbar_wait(bar(BAR_YFULL + b), (tcount >> 1) & 1u);
         tc_after();
         uint32_t v[32];
-        tmem_ld32(tmem + lane_off + YCOL2, v);
-        // M = 64 accumulator: row 16 q + l lives in TMEM lane 32 q + l (l < 16)
-        const int r = 16 * q + lane;
+        tmem_ld32(tmem + lane_off + YCOL2 + 32 * b, v);
+        tc_before();
+        mbar_arrive(bar(BAR_YFREE + b));  // P1 may refill accumulator b once both groups read it
         const int rows = min(TM, prows - t * TM);
         const bool valid = lane < 16 && r < rows;
-        if (lane < 16) {
+        if (!aux) {
+          if (tcount > 0) mbar_wait(bar(BAR_YSTFREE), (tcount - 1) & 1u);  // P2 of the previous tile done with Y^T
+          if (lane < 16) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            if (c >= sp) break;
-            const float y = valid ? __uint_as_float(v[c]) : 0.0f;
-            *reinterpret_cast<float*>(yb + (size_t)(r >> 5) * n2 * 128 + swz(c, r & 31)) = tf32r(y);
+            for (int c = 0; c < 32; ++c) {
+              if (c >= sp) break;
+              const float y = valid ? __uint_as_float(v[c]) : 0.0f;
+              *reinterpret_cast<float*>(yb + (size_t)(r >> 5) * n2 * 128 + swz(c, r & 31)) = tf32r(y);
+            }
           }
-        }
-        fence_async_smem();
-        tc_before();
-        mbar_arrive(bar(BAR_YSFULL));
-        if (pass2) {
-          if (valid) {
-            double* yo = prm.y_out + (prm.piece_row0[p] + (int64_t)t * TM + r) * sp;
+          fence_async_smem();
+          tc_before();
+          mbar_arrive(bar(BAR_YSFULL));
+          if (!pass2 && valid) {  // Inf/NaN in X reach Y (B is dense Gaussian / Q_Z)
+            bool nf = false;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              if (c < sp) yo[c] = (double)__uint_as_float(v[c]);
+              if (c < sp) nf |= !isfinite(__uint_as_float(v[c]));
+            if (nf) status_min(prm.status, ST_NONFINITE, prm.piece_slice[p]);
+          }
+        } else {
+          // Y rows through the shared row buffer: coalesced fp64 stores of the
+          // tile's rows * sp contiguous values
+          if (lane < 16)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c < sp) yrow[r * (sp + 1) + c] = valid ? __uint_as_float(v[c]) : 0.0f;
+          named_sync(4, NAUX);
+          if (prm.y_out) {
+            double* yo = prm.y_out + (prm.piece_row0[p] + (int64_t)t * TM) * sp;
+            for (int e = et; e < rows * sp; e += NAUX) {
+              const int rr = e / sp, c = e - rr * sp;
+              yo[e] = (double)yrow[rr * (sp + 1) + c];
+            }
           }
           if (do_g) {  // G += Y_t^T Y_t: fp64 DMMA m8n8k4 over 8x8 blocks of G
-            if (lane < 16)
-#pragma unroll
-              for (int c = 0; c < 32; ++c)
-                if (c < sp) yrow[r * (sp + 1) + c] = valid ? __uint_as_float(v[c]) : 0.0f;
-            named_sync(2, NEPI);
             const int nb = sp / 8, ew = et >> 5;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
@@ -575,27 +619,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
                 gacc[2 * s + 1] = c1;
               }
             }
-            named_sync(2, NEPI);
           }
+          named_sync(4, NAUX);  // yrow is rewritten for the next tile
         }
       }
-      // piece complete: Z (TMEM lanes = columns of X) -> fp64 partial
-      if (et == 0) TWAIT(bar(BAR_ZFULL), (uint32_t)pidx & 1u, 10);
-      else mbar_wait(bar(BAR_ZFULL), (uint32_t)pidx & 1u);
-      tc_after();
-      double* out = prm.out_part + (size_t)p * J * sp;
-      for (int jb = 0; jb < nsup; ++jb) {
-        uint32_t z[32];
-        tmem_ld32(tmem + lane_off + ZCOL + jb * 32, z);
-        const int j = jb * 128 + q * 32 + lane;
-        if (j < J)
+      if (!aux) {  // piece complete: Z (TMEM lanes = columns of X) -> fp64 partial
+        if (et == 0) TWAIT(bar(BAR_ZFULL), (uint32_t)pidx & 1u, 10);
+        else mbar_wait(bar(BAR_ZFULL), (uint32_t)pidx & 1u);
+        tc_after();
+        double* out = prm.out_part + (size_t)p * J * sp;
+        for (int jb = 0; jb < nsup; ++jb) {
+          uint32_t z[32];
+          tmem_ld32(tmem + lane_off + ZCOL + jb * 32, z);
+          const int j = jb * 128 + q * 32 + lane;
+          if (j < J)
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (c < sp) out[(size_t)j * sp + c] = (double)__uint_as_float(z[c]);
-      }
-      tc_before();
-      mbar_arrive(bar(BAR_ZFREE));
-      if (do_g) {
+            for (int c = 0; c < 32; ++c)
+              if (c < sp) out[(size_t)j * sp + c] = (double)__uint_as_float(z[c]);
+        }
+        tc_before();
+        mbar_arrive(bar(BAR_ZFREE));
+      } else if (do_g) {
         const int nb = sp / 8, ew = et >> 5;
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
@@ -624,6 +668,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   if (warp == MMA_WARP) {
     tc_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// B (K x J x sp, fp64) -> per-slice images of the kernel's B shared memory:
+// tf32 (rna), K-major SW128: 32-column chunk j/32, row c, swizzled granule
+__global__ void b_tile_kernel(const double* B, int64_t K, int J, int Jp, int sp, float* out) {
+  const int64_t per = (int64_t)Jp * sp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * per; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / per;
+    const int r = (int)(e - k * per), j = r / sp, c = r - j * sp;
+    const float v = j < J ? tf32r((float)B[(k * J + j) * sp + c]) : 0.0f;
+    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(out + k * per) + (size_t)(j >> 5) * sp * 128 +
+                              swz(c, j & 31)) = v;
   }
 }
 
@@ -681,11 +738,40 @@ bool sketch_tc_eligible(const dp2_store* st, int sp) {
          tc_plan((int)st->J, sp, &prm) != 0 && encode_fn() != nullptr;
 }
 
+// per-device scratch for the pre-tiled B images (grown on demand, kept)
+static float* btile_scratch(size_t bytes, cudaError_t* err) {
+  static float* buf[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) {
+    *err = cudaErrorInvalidDevice;
+    return nullptr;
+  }
+  if (cap[dev] < bytes) {
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    *err = cudaMalloc(&buf[dev], bytes);
+    if (*err != cudaSuccess) return nullptr;
+    cap[dev] = bytes;
+  }
+  *err = cudaSuccess;
+  return buf[dev];
+}
+
 cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                           double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
   tcs::Params prm{};
   const size_t smem = tc_plan((int)st->J, sp, &prm);
   if (smem == 0 || encode_fn() == nullptr) return cudaErrorInvalidValue;
+  // B images: one bulk copy per piece replaces per-element conversion in the kernel
+  prm.bbytes = (uint32_t)prm.Jp * sp * 4;
+  cudaError_t be;
+  float* bt = btile_scratch((size_t)st->K * prm.bbytes, &be);
+  if (!bt) return be;
+  tcs::b_tile_kernel<<<592, 256, 0, stream>>>(B, st->K, prm.J, prm.Jp, sp, bt);
+  prm.btile = bt;
   // X as a 2-D tensor (J columns, total_rows rows, row pitch ldx*4 B); boxes
   // of 32 columns x 64 rows land in shared memory with the 128 B swizzle
   CUtensorMap xmap;
@@ -726,7 +812,7 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
     cudaMemcpyAsync(h.data(), prm.dbg, h.size() * 8, cudaMemcpyDeviceToHost, stream);
     cudaStreamSynchronize(stream);
     const char* names[16] = {"tma.empty", "b.bfree", "xt.full", "xt.xtfree", "mma.bfull", "mma.full", "mma.ysfull",
-                             "mma.zfree", "mma.xtfull", "epi.yfull", "epi.zfull", "mma.p1issue", "mma.p2issue", "", "", "total"};
+                             "mma.zfree", "mma.xtfull", "epi.yfull", "epi.zfull", "mma.p1issue", "mma.p2issue", "mma.yfree", "", "total"};
     fprintf(stderr, "[dp2 tc] pass (%s) mean us per CTA:", y_out ? "2" : "1");
     for (int k = 0; k < 16; ++k) {
       if (!names[k][0]) continue;

@@ -747,7 +747,9 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
     for (int i = 0; i < 7; ++i) cudaEventCreate(&ev[i]);
     cudaEventRecord(ev[0], stream);
   }
-  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, xsq, status, stream);
+  // the per-piece sums of squares are not consumed by stage 1 (the fitness
+  // uses dp2_slice_stats); the tensor-core pass flags non-finite input from Y
+  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, sketch_tc_eligible(st, sp) ? nullptr : xsq, status, stream);
   if (e != cudaSuccess) return e;
   if (timing) cudaEventRecord(ev[1], stream);
   if (sp <= 32) {
@@ -755,8 +757,11 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
     double* CCg = reinterpret_cast<double*>(ws + L.CCg);
     double* Gg = reinterpret_cast<double*>(ws + L.Gg);
     double* sgn = reinterpret_cast<double*>(ws + L.sgn);
+    // the tensor-core pass leaves G to gram_y_kernel (run_stage1_small)
+    const bool tc = sketch_tc_eligible(st, sp);
+    double* gp = tc ? nullptr : gpart;
     auto small = [&](int phase) {
-      return run_stage1_small(st, s_dev, sp, R, part, part, gpart, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
+      return run_stage1_small(st, s_dev, sp, R, part, part, gp, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
                               reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
                               stream);
@@ -768,7 +773,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
       orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
     }
     if (timing) cudaEventRecord(ev[2], stream);
-    e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream, gpart);
+    e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream, gp);
     if (e != cudaSuccess) return e;
     if (timing) cudaEventRecord(ev[3], stream);
     e = small(1);

@@ -88,11 +88,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* part, const d
     C[i] = acc;
     cs_[(i / sp) * ld + i % sp] = acc;
   }
-  for (int e = tid; e < sp * sp; e += nt) {
-    double acc = 0.0;
-    for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * sp * sp + e];
-    Gg[(size_t)k * sp * sp + e] = acc;
-  }
+  if (gpart)  // else G comes from gram_y_kernel
+    for (int e = tid; e < sp * sp; e += nt) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * sp * sp + e];
+      Gg[(size_t)k * sp * sp + e] = acc;
+    }
   __syncthreads();
   const int ntri = sp * (sp + 1) / 2;
   for (int e = warp; e < ntri; e += nw) {
@@ -105,6 +106,64 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* part, const d
     if (lane == 0) {
       CCg[(size_t)k * sp * sp + a * sp + b] = acc;
       CCg[(size_t)k * sp * sp + b * sp + a] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------ G from Y rows
+// G_k = Y_k^T Y_k (sp x sp, fp64) for slice k from its pass-2 rows y2[row_off[k]
+// .. row_off[k+1]) -- used when the streaming pass does not accumulate G
+// (tensor-core pass: fp64 DMMA inside it would share the tensor pipe with the
+// tcgen05 products).  64-row tiles staged in smem, 8x8 blocks of G on fp64
+// DMMA m8n8k4, one CTA (8 warps) per slice.
+__global__ void __launch_bounds__(256) gram_y_kernel(const double* y2, const int64_t* row_off, int sp, double* Gg) {
+  constexpr int TR = 64, LD = 34;  // rows per tile; row stride (doubles): 16 B aligned, conflict-light for DMMA
+  __shared__ __align__(16) double ys[2][TR * LD];
+  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = row_off[k], r1 = row_off[k + 1];
+  const int nb = sp / 8, c16 = sp / 2;  // 16 B chunks per row
+  const int ntile = (int)((r1 - r0 + TR - 1) / TR);
+  auto issue = [&](int t, int buf) {
+    const int64_t base = r0 + (int64_t)t * TR;
+    const int rows = (int)min((int64_t)TR, r1 - base);
+    for (int e = tid; e < TR * c16; e += 256) {
+      const int r = e / c16, c = e - r * c16;
+      double* dst = &ys[buf][r * LD + 2 * c];
+      if (r < rows) cp_async16(dst, y2 + (base + r) * sp + 2 * c, 16);
+      else cp_async16(dst, y2, 0);  // zero fill
+    }
+  };
+  double acc[4][2] = {};
+  if (ntile > 0) issue(0, 0);
+  cp_async_commit();
+  for (int t = 0; t < ntile; ++t) {
+    if (t + 1 < ntile) issue(t + 1, (t + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* yt = ys[t & 1];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int blk = warp + 8 * s;
+      if (blk < nb * nb) {
+        const int bi = blk / nb, bj = blk - bi * nb;
+#pragma unroll 4
+        for (int kk = 0; kk < TR / 4; ++kk) {
+          const double* yr = yt + (4 * kk + (lane & 3)) * LD;
+          dmma_8x8x4(acc[s][0], acc[s][1], yr[8 * bi + (lane >> 2)], yr[8 * bj + (lane >> 2)]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int blk = warp + 8 * s;
+    if (blk < nb * nb) {
+      const int bi = blk / nb, bj = blk - bi * nb;
+      double* g = Gg + (size_t)k * sp * sp + (size_t)(8 * bi + (lane >> 2)) * sp + 8 * bj + 2 * (lane & 3);
+      g[0] = acc[s][0];
+      g[1] = acc[s][1];
     }
   }
 }
@@ -410,6 +469,7 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
   e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
   if (e != cudaSuccess) return e;
   gather_kernel<<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
+  if (!gpart) gram_y_kernel<<<K, 256, 0, stream>>>(y2, st->row_off, sp, Gg);
   const int wpb = sp <= 24 ? 4 : 2;
   const size_t fs = wpb * small_factor_smem(sp);
   e = cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
