@@ -132,7 +132,8 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     t0 = time.perf_counter()
     rstats = {}
     omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats)
-    s_dev = torch.tensor(widths, dtype=torch.int32).to(dev, non_blocking=True)
+    from .tensor import to_device_async
+    s_dev = to_device_async(widths, torch.int32, dev)
     t_omega = time.perf_counter() - t0
     nseg = nseg_for(tensor)
     st, keep = tensor.store(nseg)

@@ -66,8 +66,9 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
     from . import _lib
     K = len(widths)
     out = torch.empty((K, n, sp), dtype=torch.float64, device=device)
-    s_dev = torch.tensor(list(widths), dtype=torch.int32).to(device)
-    ids = None if slice_ids is None else torch.tensor(list(slice_ids), dtype=torch.int64).to(device)
+    from .tensor import to_device_async
+    s_dev = to_device_async(list(widths), torch.int32, device)
+    ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
     cap = max(4096, 8 * K + n * max(widths) * K // 1000)
     recs = torch.empty((cap, _REC.itemsize), dtype=torch.uint8, device=device)
     nrec = torch.zeros(1, dtype=torch.int32, device=device)
@@ -105,8 +106,8 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
         if good.any():
             w = np.asarray(widths)[r["slice"][good]]
             flat = r["slice"][good] * (n * sp) + (r["index"][good] // w) * sp + r["index"][good] % w
-            idx = torch.from_numpy(flat).to(device)
-            out.view(-1).index_copy_(0, idx, torch.from_numpy(vals[good]).to(device))
+            idx = to_device_async(flat, torch.int64, device)
+            out.view(-1).index_copy_(0, idx, to_device_async(vals[good], torch.float64, device))
             patched = int(good.sum())
     bad = np.nonzero(redo_h)[0]
     if bad.size:

@@ -31,7 +31,8 @@ from .tensor import IrregularTensor, new_status, stream_ptr
 def _dev(x, dev):
     if isinstance(x, torch.Tensor):
         return x.to(device=dev, dtype=torch.float64).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    # pinned staging: a pageable host copy would wait for the whole stream
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory().to(dev, non_blocking=True)
 
 
 @dataclass
@@ -188,7 +189,7 @@ def assemble_q(tensor: IrregularTensor, comp: CompressedTensor, polar, nseg=None
     return Q
 
 
-def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", timings=None, use_graph=True):
+def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", timings=None, use_graph=False):
     """Compress once, then alternate rotations and factor sweeps in R x R space.
 
     Returns ``(factors, trace)`` like P/solver.py:152-190.  ``output="device"``

@@ -237,5 +237,14 @@ class IrregularTensor:
 
 
 def new_status(dev):
-    init = torch.tensor([_lib.INT64_MAX, 0, _lib.INT64_MAX, _lib.INT64_MAX, 0, 0, 0, 0], dtype=torch.int64)
-    return init.to(dev)
+    # device-side fills: no host copy, so no implicit stream synchronisation
+    st = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int64, device=dev)
+    st[0:1].fill_(_lib.INT64_MAX)
+    st[2:4].fill_(_lib.INT64_MAX)
+    return st
+
+
+def to_device_async(values, dtype, dev):
+    """Small host list/array -> device without an implicit synchronisation
+    (pageable host copies wait for the stream; pinned ones are async)."""
+    return torch.as_tensor(np.asarray(values), dtype=dtype).pin_memory().to(dev, non_blocking=True)
