@@ -8,10 +8,66 @@
 //   C  = M^T Q2             (KR x s2)    B2 = Q2^T M = C^T
 //   B2 B2^T = C^T C = U mu U^T           Jacobi; E = sqrt(mu_R)
 //   D = Q2 U_R (sign rule, P/linalg.py:62-70), F = C U_R / E (same flips)
+#include <dlfcn.h>
+
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
 namespace dp2 {
+
+// ---------------------------------------------------------------- cuBLAS
+// The four products with M and the Gram C^T C are plain dense fp64 GEMMs
+// (M is J x KR, e.g. 512 x 10^4): cuBLAS DGEMM (fp64 tensor cores) when the
+// library can be opened at run time, else the kernels below.  Loaded with
+// dlopen so libdpar2 has no link-time dependency on it; cuBLAS results are
+// bitwise reproducible on a given GPU.
+namespace {
+typedef int (*blas_create_t)(void**);
+typedef int (*blas_stream_t)(void*, cudaStream_t);
+typedef int (*blas_dgemm_t)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
+                            const double*, double*, int);
+struct Blas {
+  bool tried = false;
+  blas_create_t create = nullptr;
+  blas_stream_t stream = nullptr;
+  blas_dgemm_t dgemm = nullptr;
+  void* handle[64] = {};
+};
+Blas& blas() {
+  static Blas b;
+  if (!b.tried) {
+    b.tried = true;
+    const char* names[] = {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12", "libcublas.so"};
+    void* lib = nullptr;
+    for (const char* n : names)
+      if ((lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (lib) {
+      b.create = reinterpret_cast<blas_create_t>(dlsym(lib, "cublasCreate_v2"));
+      b.stream = reinterpret_cast<blas_stream_t>(dlsym(lib, "cublasSetStream_v2"));
+      b.dgemm = reinterpret_cast<blas_dgemm_t>(dlsym(lib, "cublasDgemm_v2"));
+      if (!b.create || !b.stream || !b.dgemm) b.create = nullptr;
+    }
+  }
+  return b;
+}
+// column-major C (m x n) = op(A) op(B); false when cuBLAS is unavailable
+bool dgemm_cm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, const double* A, int lda, const double* B,
+              int ldb, double* C, int ldc) {
+  Blas& b = blas();
+  if (!b.create) return false;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+  if (!b.handle[dev] && b.create(&b.handle[dev]) != 0) {
+    b.handle[dev] = nullptr;
+    return false;
+  }
+  if (b.stream(b.handle[dev], st) != 0) return false;
+  const double one = 1.0, zero = 0.0;
+  return b.dgemm(b.handle[dev], ta ? 1 : 0, tb ? 1 : 0, m, n, k, &one, A, lda, B, ldb, &zero, C, ldc) == 0;
+}
+}  // namespace
+
+bool stage2_uses_blas() { return blas().create != nullptr; }
 
 constexpr int kChunk = 1024;  // split-K chunk of the KR dimension
 
@@ -223,11 +279,16 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   double* Ubuf = reinterpret_cast<double*>(ws + L.Ubuf);
   const int nch = (int)((KR + kChunk - 1) / kChunk);
   const int ng = (s2 + 31) / 32;
+  // row-major M (J x KR) is column-major (KR x J); row-major B (KR x s2) is
+  // column-major (s2 x KR): Y = M B  <=>  Y_cm (s2 x J) = B_cm M_cm
   auto nn = [&](const double* B, double* out) {
+    if (dgemm_cm(st, false, false, s2, (int)J, (int)KR, B, s2, M, (int)KR, out, s2)) return;
     nn_partial_kernel<<<dim3((unsigned)J, nch, ng), 256, 0, st>>>(M, KR, KR, B, s2, s2, parts, J);
     reduce_parts_kernel<<<(unsigned)((J * s2 + 255) / 256), 256, 0, st>>>(parts, nch, J * s2, out);
   };
+  // Z = M^T Y  <=>  Z_cm (s2 x KR) = Y_cm M_cm^T
   auto tn = [&](const double* B, double* out) {
+    if (dgemm_cm(st, false, true, s2, (int)KR, (int)J, B, s2, M, (int)KR, out, s2)) return;
     tn_kernel<<<dim3((unsigned)((KR + 255) / 256), ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, out, s2);
   };
   nn(omega2, Y);
@@ -235,8 +296,11 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   nn(Z, Y2);
   cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
   tn(Y2, C);
-  gram_partial_kernel<<<nch, 256, 0, st>>>(C, KR, s2, s2, bbp);
-  reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(bbp, nch, (int64_t)s2 * s2, BB);
+  // BB = C^T C  <=>  C_cm C_cm^T (symmetric, so layout-neutral)
+  if (!dgemm_cm(st, false, true, s2, s2, (int)KR, C, s2, C, s2, BB, s2)) {
+    gram_partial_kernel<<<nch, 256, 0, st>>>(C, KR, s2, s2, bbp);
+    reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(bbp, nch, (int64_t)s2 * s2, BB);
+  }
   stage2_final_kernel<<<1, 256, 0, st>>>(BB, s2, Y2, J, R, D, E, Uf, Ubuf, status);
   f_kernel<<<(unsigned)imin64((KR * R + 255) / 256, 4096), 256, 0, st>>>(C, KR, s2, Uf, R, F);
   return cudaGetLastError();
