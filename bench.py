@@ -235,15 +235,25 @@ def main():
     N_rows = int(tensor.row_off_host[-1]) if world == 1 else runner.local_rows
     K_loc = tensor.num_slices
     x_bytes = N_rows * cfg.cols * elem
-    b_bytes = K_loc * cfg.cols * sp * 8
-    alg_pass1 = x_bytes + b_bytes
-    alg_pass2 = x_bytes + b_bytes + N_rows * sp * 8
+    # algorithmic bytes of one streaming pass (X once per pass
+    # plus the per-slice B and the pass outputs).  The fp32 tensor-core pass
+    # (J <= 512) reads B as a pre-tiled tf32 image and stores Y rows in fp32;
+    # the fp64 DMMA / FFMA passes read B and write Y in fp64.
+    tc = cfg.dtype == "f32" and cfg.cols <= 512 and sp <= 32
+    jp = -(-cfg.cols // 128) * 128
+    b_bytes = K_loc * (jp if tc else cfg.cols) * sp * (4 if tc else 8)
+    part_bytes = int(tms[0].get("npieces", K_loc)) * cfg.cols * sp * 8  # fp64 per-piece partials
+    alg_pass1 = x_bytes + b_bytes + part_bytes
+    alg_pass2 = alg_pass1 + N_rows * sp * (4 if tc else 8)
     avg_launch_ms = (s1 + s2) / 2
     achieved = (alg_pass1 + alg_pass2) / 2 / (avg_launch_ms * 1e-3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
         else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     flops_launch = 4.0 * N_rows * cfg.cols * sp  # two skinny GEMMs per pass over the padded sketch width
+    kernel_name = ("tcs::sketch_tc_kernel (stage-1 streaming pass: tcgen05 kind::tf32, TMA ring, X^T in TMEM)"
+                   if tc else "sketch_kernel (stage-1 streaming pass, %s)" % ("fp64 DMMA m8n8k4" if cfg.dtype == "f64"
+                                                                               else "fp32 FFMA"))
     traffic = None
     prof = ROOT / "profiles" / "sketch_traffic.json"
     if prof.exists():
@@ -259,17 +269,22 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
-        "dtype": f"{cfg.dtype} X, f64 compute (stage-1 DMMA m8n8k4), f64 stage 2 / ALS",
+        "dtype": (f"{cfg.dtype} X; stage-1 sketch products tf32 on tcgen05 (fp32 accumulate, fp64 partials); "
+                  "f64 factorizations, stage 2, ALS" if tc else
+                  f"{cfg.dtype} X; f64 compute (stage-1 DMMA m8n8k4), f64 stage 2 / ALS"),
         "data": "synthetic (BASELINE.json model, generated on device)",
         "config": {"workload": workload_desc(cfg, args.iters), "entries": total_entries,
                    "parallelism": f"slice-sharded dp{world} (LPT)" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (X %.1f GB >> 126 MB)" % (x_bytes / 1e9)},
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": {"bound": "hbm", "kernel": "sketch_kernel (stage-1 streaming pass)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": kernel_name, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": (alg_pass1 + alg_pass2) / 2, "avg_launch_ms": avg_launch_ms,
-                     "fp64_tflops_achieved": flops_launch / (avg_launch_ms * 1e-3) / 1e12,
+                     "pass_frac": [alg_pass1 / (s1 * 1e-3) / 1e9 / peak, alg_pass2 / (s2 * 1e-3) / 1e9 / peak],
+                     ("tf32_tflops_achieved" if tc else "fp64_tflops_achieved"):
+                         flops_launch / (avg_launch_ms * 1e-3) / 1e12,
+                     "traffic_source": "profiles/sketch_traffic.json (ncu dram__bytes_read+write per launch)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
         "breakdown_ms": {"stage1": stage1_ms, "sketch_pass1": s1, "sketch_pass2": s2,
                          "orth": float(np.mean([t["stage1_orth_ms"] for t in tms])),

@@ -80,6 +80,7 @@ struct Params {
   int64_t* status;
   uint32_t off_b, off_y, off_yrow, off_bar;
   unsigned long long* dbg;  // per-CTA wait-time counters (DP2_TC_DEBUG), or null
+  int y32;                  // y_out holds fp32 rows (the accumulator's own precision) instead of fp64
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -596,10 +597,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
               if (c < sp) yrow[r * (sp + 1) + c] = valid ? __uint_as_float(v[c]) : 0.0f;
           named_sync(4, NAUX);
           if (prm.y_out) {
-            double* yo = prm.y_out + (prm.piece_row0[p] + (int64_t)t * TM) * sp;
+            const int64_t o = (prm.piece_row0[p] + (int64_t)t * TM) * sp;
+            float* yo32 = reinterpret_cast<float*>(prm.y_out) + o;
+            double* yo = prm.y_out + o;
             for (int e = et; e < rows * sp; e += NAUX) {
               const int rr = e / sp, c = e - rr * sp;
-              yo[e] = (double)yrow[rr * (sp + 1) + c];
+              if (prm.y32) yo32[e] = yrow[rr * (sp + 1) + c];
+              else yo[e] = (double)yrow[rr * (sp + 1) + c];
             }
           }
           if (do_g) {  // G += Y_t^T Y_t: fp64 DMMA m8n8k4 over 8x8 blocks of G
@@ -761,8 +765,9 @@ static float* btile_scratch(size_t bytes, cudaError_t* err) {
 }
 
 cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                          double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
+                          double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part, bool y32) {
   tcs::Params prm{};
+  prm.y32 = y32 ? 1 : 0;
   const size_t smem = tc_plan((int)st->J, sp, &prm);
   if (smem == 0 || encode_fn() == nullptr) return cudaErrorInvalidValue;
   // B images: one bulk copy per piece replaces per-element conversion in the kernel

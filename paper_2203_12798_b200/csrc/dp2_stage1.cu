@@ -764,7 +764,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
       return run_stage1_small(st, s_dev, sp, R, part, part, gp, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
                               reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
-                              stream);
+                              stream, tc);
     };
     if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) {
       e = small(0);
@@ -773,7 +773,9 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
       orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
     }
     if (timing) cudaEventRecord(ev[2], stream);
-    e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream, gp);
+    // the tensor-core pass stores Y in fp32: its accumulator precision, half the bytes
+    e = tc ? run_sketch_tc(st, qz, sp, part, y2, nullptr, status, stream, nullptr, true)
+           : run_sketch(st, qz, sp, part, y2, nullptr, status, stream, gp);
     if (e != cudaSuccess) return e;
     if (timing) cudaEventRecord(ev[3], stream);
     e = small(1);

@@ -116,20 +116,22 @@ __global__ void __launch_bounds__(256) gather_kernel(const double* part, const d
 // (tensor-core pass: fp64 DMMA inside it would share the tensor pipe with the
 // tcgen05 products).  64-row tiles staged in smem, 8x8 blocks of G on fp64
 // DMMA m8n8k4, one CTA (8 warps) per slice.
-__global__ void __launch_bounds__(256) gram_y_kernel(const double* y2, const int64_t* row_off, int sp, double* Gg) {
-  constexpr int TR = 64, LD = 34;  // rows per tile; row stride (doubles): 16 B aligned, conflict-light for DMMA
-  __shared__ __align__(16) double ys[2][TR * LD];
+template <typename Y>  // Y rows stored as fp64, or as fp32 by the tensor-core pass
+__global__ void __launch_bounds__(256) gram_y_kernel(const Y* y2, const int64_t* row_off, int sp, double* Gg) {
+  constexpr int TR = 64, LD = sizeof(Y) == 8 ? 34 : 36;  // row stride (elements): 16 B aligned, conflict-light
+  __shared__ __align__(16) Y ys[2][TR * LD];
   const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r0 = row_off[k], r1 = row_off[k + 1];
-  const int nb = sp / 8, c16 = sp / 2;  // 16 B chunks per row
+  constexpr int EPC = 16 / (int)sizeof(Y);  // elements per 16 B chunk
+  const int nb = sp / 8, c16 = sp / EPC;     // 16 B chunks per row
   const int ntile = (int)((r1 - r0 + TR - 1) / TR);
   auto issue = [&](int t, int buf) {
     const int64_t base = r0 + (int64_t)t * TR;
     const int rows = (int)min((int64_t)TR, r1 - base);
     for (int e = tid; e < TR * c16; e += 256) {
       const int r = e / c16, c = e - r * c16;
-      double* dst = &ys[buf][r * LD + 2 * c];
-      if (r < rows) cp_async16(dst, y2 + (base + r) * sp + 2 * c, 16);
+      Y* dst = &ys[buf][r * LD + EPC * c];
+      if (r < rows) cp_async16(dst, y2 + (base + r) * sp + EPC * c, 16);
       else cp_async16(dst, y2, 0);  // zero fill
     }
   };
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(256) gram_y_kernel(const double* y2, const int
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* yt = ys[t & 1];
+    const Y* yt = ys[t & 1];
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int blk = warp + 8 * s;
@@ -149,8 +151,8 @@ __global__ void __launch_bounds__(256) gram_y_kernel(const double* y2, const int
         const int bi = blk / nb, bj = blk - bi * nb;
 #pragma unroll 4
         for (int kk = 0; kk < TR / 4; ++kk) {
-          const double* yr = yt + (4 * kk + (lane & 3)) * LD;
-          dmma_8x8x4(acc[s][0], acc[s][1], yr[8 * bi + (lane >> 2)], yr[8 * bj + (lane >> 2)]);
+          const Y* yr = yt + (4 * kk + (lane & 3)) * LD;
+          dmma_8x8x4(acc[s][0], acc[s][1], (double)yr[8 * bi + (lane >> 2)], (double)yr[8 * bj + (lane >> 2)]);
         }
       }
     }
@@ -336,7 +338,8 @@ __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, cons
 }
 
 // ------------------------------------------------------------ A = Y P + argmax candidates
-__global__ void __launch_bounds__(256) argmax_a_kernel(const double* y2, const int64_t* row_off,
+template <typename Y>
+__global__ void __launch_bounds__(256) argmax_a_kernel(const Y* y2, const int64_t* row_off,
                                                         const int32_t* piece_slice, const int64_t* piece_row0,
                                                         const int32_t* piece_rows, const int32_t* s_k,
                                                         const double* Pm, int sp, int R, double* A,
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(256) argmax_a_kernel(const double* y2, const i
   for (int64_t t0 = 0; t0 < nr; t0 += TR) {
     const int rows = (int)imin64(TR, nr - t0);
     __syncthreads();
-    for (int i = tid; i < rows * sp; i += blockDim.x) ytile[i] = y2[(r0 + t0) * sp + i];
+    for (int i = tid; i < rows * sp; i += blockDim.x) ytile[i] = (double)y2[(r0 + t0) * sp + i];
     __syncthreads();
     for (int e = tid; e < rows * R; e += blockDim.x) {
       const int i = e / R, c = e % R;
@@ -455,8 +458,9 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                             int64_t* status, int phase, cudaStream_t stream) {
+                             int64_t* status, int phase, cudaStream_t stream, bool y32) {
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
+  const float* y2f = reinterpret_cast<const float*>(y2);
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
     const size_t qb = (size_t)J * (sp + 1) * 8;
@@ -469,7 +473,10 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
   e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
   if (e != cudaSuccess) return e;
   gather_kernel<<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
-  if (!gpart) gram_y_kernel<<<K, 256, 0, stream>>>(y2, st->row_off, sp, Gg);
+  if (!gpart) {
+    if (y32) gram_y_kernel<float><<<K, 256, 0, stream>>>(y2f, st->row_off, sp, Gg);
+    else gram_y_kernel<double><<<K, 256, 0, stream>>>(y2, st->row_off, sp, Gg);
+  }
   const int wpb = sp <= 24 ? 4 : 2;
   const size_t fs = wpb * small_factor_smem(sp);
   e = cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
@@ -477,10 +484,17 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
   factor_warp_kernel<<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, sp, R, Pm, Sv, rank_out,
                                                                       status);
   const size_t as = ((size_t)sp * R + 128 * (size_t)sp + 128 * (size_t)(R + 1)) * 8;
-  e = cudaFuncSetAttribute(argmax_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
-  if (e != cudaSuccess) return e;
-  argmax_a_kernel<<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows, s_dev,
-                                          Pm, sp, R, A, cand_abs, cand_row, cand_neg);
+  if (y32) {
+    e = cudaFuncSetAttribute(argmax_a_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
+    if (e != cudaSuccess) return e;
+    argmax_a_kernel<float><<<P, 256, as, stream>>>(y2f, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows,
+                                                   s_dev, Pm, sp, R, A, cand_abs, cand_row, cand_neg);
+  } else {
+    e = cudaFuncSetAttribute(argmax_a_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
+    if (e != cudaSuccess) return e;
+    argmax_a_kernel<double><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows,
+                                                    s_dev, Pm, sp, R, A, cand_abs, cand_row, cand_neg);
+  }
   signs_m_kernel<<<K, 256, (size_t)sp * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
                                                           J, sp, R, sgn, M);
   flip_a_kernel<<<P, 256, 0, stream>>>(st->piece_slice, st->piece_row0, st->piece_rows, sgn, R, A);
