@@ -751,11 +751,63 @@ DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out, 
   return sqrt(an) * sqrt(in) < 1e10;
 }
 
+// Register Gauss-Jordan inverse, R known at compile time: lane c < 2R owns
+// column c of [A | I] in registers; per pivot k the row factors come from
+// lane k by shuffle, so a step is one reciprocal and R independent
+// shuffle+FMA pairs (a runtime R would predicate every shuffle; measured 3.75x
+// slower -- tools/inv_probe.cu).  No pivoting: only the SPD fast path, accepted
+// under the Cholesky path's tests (positive pivots, ||A||_F ||A^-1||_F < 1e10).
+template <int R>
+DP2_DEV bool warp_gj_inverse(const double* A, double* out) {
+  const int lane = threadIdx.x & 31;
+  double col[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) col[i] = lane < R ? A[i * R + lane] : (lane < 2 * R && i == lane - R ? 1.0 : 0.0);
+  bool okay = true;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    const double piv = __shfl_sync(0xffffffffu, col[k], k);
+    okay &= piv > 0.0;
+    const double rk = col[k] * (1.0 / piv);
+    double f[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) f[i] = __shfl_sync(0xffffffffu, col[i], k);
+#pragma unroll
+    for (int i = 0; i < R; ++i) col[i] = (i == k) ? rk : fma(-f[i], rk, col[i]);
+  }
+  double an = 0.0, in = 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    if (lane < R) an = fma(A[i * R + lane], A[i * R + lane], an);
+    if (lane >= R && lane < 2 * R) {
+      out[i * R + (lane - R)] = col[i];
+      in = fma(col[i], col[i], in);
+    }
+  }
+  an = warp_sum(an);
+  in = warp_sum(in);
+  __syncwarp();
+  return okay && sqrt(an) * sqrt(in) < 1e10;
+}
+
+DP2_DEV bool warp_fast_inverse(const double* A, int R, double* Lw, double* out, double* dinv) {
+  switch (R) {
+#define DP2_GJ(n) \
+  case n:         \
+    return warp_gj_inverse<n>(A, out);
+    DP2_GJ(2) DP2_GJ(3) DP2_GJ(4) DP2_GJ(5) DP2_GJ(6) DP2_GJ(7) DP2_GJ(8) DP2_GJ(9) DP2_GJ(10) DP2_GJ(11) DP2_GJ(12)
+    DP2_GJ(13) DP2_GJ(14) DP2_GJ(15) DP2_GJ(16)
+#undef DP2_GJ
+    default:
+      return warp_chol_inverse(A, R, Lw, out, dinv);
+  }
+}
+
 DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status) {
   __shared__ double lmax;
   __shared__ int fast;
   if (threadIdx.x < 32) {
-    const bool okay = warp_chol_inverse(A, R, U, out, cs);
+    const bool okay = warp_fast_inverse(A, R, U, out, cs);
     if (threadIdx.x == 0) fast = okay ? 1 : 0;
   }
   __syncthreads();
@@ -792,7 +844,7 @@ struct SolveArgs {
   int64_t* status;
 };
 
-__global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
+__global__ void __launch_bounds__(512) als_solve_h_kernel(SolveArgs s, AlsBufs b) {
   if (b.ctl[0]) return;
   extern __shared__ __align__(16) double sm[];
   const int R = s.R;
@@ -842,7 +894,7 @@ __global__ void als_solve_h_kernel(SolveArgs s, AlsBufs b) {
   }
 }
 
-__global__ void als_solve_v_kernel(SolveArgs s, AlsBufs b) {
+__global__ void __launch_bounds__(512) als_solve_v_kernel(SolveArgs s, AlsBufs b) {
   if (b.ctl[0]) return;
   extern __shared__ __align__(16) double sm[];
   const int R = s.R;
@@ -1131,9 +1183,9 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   a.warm = 1;
   cudaError_t e0 = launch_rotate(a, b, st);
   if (e0 != cudaSuccess) return e0;
-  als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
+  als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.write_l = 1;
   a.Wout = sv.W;
@@ -1277,9 +1329,9 @@ cudaError_t als_update_factors(const double* theta, const double* D, const doubl
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, nullptr, 1);
   als_mode1_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
   sv.nslots_h = b.nb;
-  als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
+  als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
+  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
   a.write_w = 1;
   a.Wout = W;
   als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
@@ -1344,7 +1396,7 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
       cudaMemcpyAsync(b.s_g1, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
       sv.nslots_h = 1;
-      als_solve_h_kernel<<<1, 1024, solve_smem(R), st>>>(sv, b);
+      als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
       break;
     case 3:
       als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
@@ -1355,7 +1407,7 @@ cudaError_t als_phase(int phase, const double* F, const double* D, const double*
       cudaMemcpyAsync(b.s_m2, red_in, RR * 8, cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(b.s_wtw2, red_in + RR, RR * 8, cudaMemcpyDeviceToDevice, st);
       sv.nslots = 1;
-      als_solve_v_kernel<<<1, 1024, solve_v_smem(sv.J, R), st>>>(sv, b);
+      als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
       break;
     case 5:
       a.write_w = 1;

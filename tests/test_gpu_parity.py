@@ -177,6 +177,23 @@ def test_random_instances_vs_live_oracle(seed):
         assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
 
 
+@pytest.mark.parametrize("R", [12, 16, 17, 24])
+def test_larger_ranks_vs_live_oracle(R):
+    """Ranks either side of the solves' register inverse (R <= 16) and its
+    Cholesky fallback (dp2_als.cu block_pinv_sym)."""
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    rng = np.random.default_rng(2000 + R)
+    J, K = R + 6, 9
+    xs = [rng.random((int(c), J)) for c in rng.integers(R, R + 30, size=K)]
+    o = orc.fit_dpar2(xs, R, 6, 0.0, 0)
+    f, tr = dp.fit_dpar2(dp.IrregularTensor(xs), R, dp.SolverOptions(max_iters=6, tol=0.0))
+    assert abs(dp.fitness(dp.IrregularTensor(xs), f) - orc.fitness(xs, o["H"], o["V"], o["W"], o["Q"])) <= FIT_TOL
+    check_trace(tr, o["objective"], o["converged"], xs)
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
+
+
 def test_errors_mirror_reference():
     import paper_2203_12798_b200 as dp
     rng = np.random.default_rng(0)
