@@ -9,7 +9,7 @@ kernel-level functions.  See DESIGN.md.
 """
 from .errors import (DecompositionError, DegenerateInputError, NonFiniteInputError, NumericFailure,
                      RankTooLargeError, ShapeMismatchError)
-from .factors import FitTrace, Parafac2Factors, SolverOptions, initial_factors, push_col_norms
+from .factors import FitTrace, Parafac2Factors, SliceViews, SolverOptions, initial_factors, push_col_norms
 from .linalg import RsvdParams, derived_seed
 from .scheduler import PartitionPlan, greedy_partition, resolve_threads
 
@@ -27,5 +27,5 @@ _LAZY = ["IrregularTensor", "CompressedTensor", "compress", "reconstruct_slice",
 
 __all__ = sorted(list(_LAZY) + [
     "DecompositionError", "DegenerateInputError", "NonFiniteInputError", "NumericFailure", "RankTooLargeError",
-    "ShapeMismatchError", "FitTrace", "Parafac2Factors", "SolverOptions", "initial_factors", "push_col_norms",
+    "ShapeMismatchError", "FitTrace", "Parafac2Factors", "SliceViews", "SolverOptions", "initial_factors", "push_col_norms",
     "RsvdParams", "derived_seed", "PartitionPlan", "greedy_partition", "resolve_threads"])

@@ -134,7 +134,7 @@ class DistributedFit:
 
     def fit(self, R, opts, timings=None):
         from .compress import check_status, run_stage1, run_stage2, stage2_params
-        from .factors import FitTrace, Parafac2Factors, initial_factors
+        from .factors import FitTrace, Parafac2Factors, SliceViews, initial_factors
         from .linalg import RsvdParams
         from .rng import stage2_omega
         from .solver import assemble_q
@@ -169,6 +169,5 @@ class DistributedFit:
         comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
         Q = assemble_q(t, comp, ops.polar)
         bounds = t.row_off_host
-        factors = Parafac2Factors(H=ops.H, V=ops.V, W=ops.W, Q=[Q[a:b] for a, b in zip(bounds[:-1], bounds[1:])],
-                                  Q_packed=Q)
+        factors = Parafac2Factors(H=ops.H, V=ops.V, W=ops.W, Q=SliceViews(Q, bounds), Q_packed=Q)
         return factors, tr

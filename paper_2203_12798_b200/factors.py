@@ -2,10 +2,11 @@
 
 Same fields and semantics as the reference.  Arrays are NumPy by default
 (drop-in); with ``output="device"`` the solver returns CUDA tensors and Q is a
-list of views into one packed (sum I_k x R) device tensor.
+sequence of views into one packed (sum I_k x R) device tensor.
 """
 from __future__ import annotations
 
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -41,6 +42,37 @@ class FitTrace:
         return len(self.objective)
 
 
+class SliceViews(Sequence):
+    """Read-only sequence of the per-slice row blocks of one packed array,
+    built on access: Q_k = packed[row_off[k]:row_off[k+1]].  Making K views
+    eagerly costs ~1 us each on the host (1 ms at K = 1000, 7% of a c2 fit)."""
+
+    __slots__ = ("packed", "row_off")
+
+    def __init__(self, packed, row_off):
+        self.packed = packed
+        self.row_off = np.asarray(row_off, dtype=np.int64)
+
+    def __len__(self):
+        return len(self.row_off) - 1
+
+    def __getitem__(self, k):
+        if isinstance(k, slice):
+            return [self[i] for i in range(*k.indices(len(self)))]
+        n = len(self)
+        if k < -n or k >= n:
+            raise IndexError("slice index out of range")
+        k %= n
+        return self.packed[int(self.row_off[k]):int(self.row_off[k + 1])]
+
+    def __iter__(self):
+        b = self.row_off.tolist()
+        return (self.packed[a:z] for a, z in zip(b[:-1], b[1:]))
+
+    def __repr__(self):
+        return f"SliceViews({len(self)} slices of {tuple(self.packed.shape)})"
+
+
 @dataclass
 class Parafac2Factors:
     """H (R x R), V (J x R), W (K x R), per-slice Q_k (I_k x R)."""
@@ -73,7 +105,7 @@ class Parafac2Factors:
             return self
         qp = device_to_numpy(self.Q_packed)
         H, V, W = (t.cpu().numpy() for t in (self.H, self.V, self.W))
-        bounds = np.cumsum([0] + [q.shape[0] for q in self.Q])
+        bounds = self.Q.row_off if isinstance(self.Q, SliceViews) else np.cumsum([0] + [q.shape[0] for q in self.Q])
         return Parafac2Factors(H=H, V=V, W=W, Q=[qp[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=qp)
 
 

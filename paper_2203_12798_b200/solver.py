@@ -22,7 +22,7 @@ import torch
 
 from . import _lib
 from .compress import CompressedTensor, _vp, check_status, compress, compress_async, nseg_for, workspace
-from .factors import FitTrace, Parafac2Factors, SolverOptions, initial_factors
+from .factors import FitTrace, Parafac2Factors, SliceViews, SolverOptions, initial_factors
 from .linalg import RsvdParams
 from .scheduler import resolve_threads
 from .tensor import IrregularTensor, new_status, stream_ptr
@@ -228,7 +228,7 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
         prev, e = tr[-2], tr[-1]
         trace.converged = bool(prev == 0.0 or abs(prev - e) <= opts.tol * prev)
     bounds = tensor.row_off_host
-    factors = Parafac2Factors(H=H, V=V, W=W, Q=[Q[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=Q)
+    factors = Parafac2Factors(H=H, V=V, W=W, Q=SliceViews(Q, bounds), Q_packed=Q)
     if output == "numpy":
         factors = factors.numpy()
     return factors, trace
