@@ -20,13 +20,15 @@
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 #include <cstdio>
+#include <cstdlib>
 
 namespace dp2 {
 
 struct AlsBufs {
   double *theta, *pprev, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2, *L;
   double *s_g1, *s_wtw, *s_m2, *s_wtw2, *s_e, *G2, *g3;
-  int32_t* ctl;  // [0] stop flag, [1] warm-start valid
+  double *GD, *ps_slots, *ps_e, *ps_C;  // persistent loop: D^T D, per-CTA partial slots, V = D C
+  int32_t* ctl;  // [0] stop flag, [1] warm-start valid, [8] persistent-loop grid barrier counter
   int nwt;       // total warps in the per-slice kernels
   int wpb;       // warps per block
   int nb;        // blocks == partial slots
@@ -198,7 +200,18 @@ DP2_DEV void combine_warps(const double* wbase, size_t wstride, int nwarps, int 
 __global__ void als_prep_kernel(const double* D, const double* E, const double* V, int64_t J, int R,
                                 AlsBufs b, int64_t* tstamp, int reset) {
   gram_dv_warps(D, E, V, J, R, b.cc, b.VtV, nullptr, nullptr);
+  if (b.GD) {  // G_D = D^T D for the persistent loop's implicit V = D C
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int e = warp; e < R * R; e += nw) {
+      const int a = e / R, c = e % R;
+      double s = 0.0;
+      for (int64_t j = lane; j < J; j += 32) s = fma(D[j * R + a], D[j * R + c], s);
+      s = warp_sum(s);
+      if (lane == 0) b.GD[e] = s;
+    }
+  }
   if (threadIdx.x == 0) {
+    b.ctl[8] = 0;
     for (int r = 0; r < R; ++r) b.nh[r] = 1.0;
     if (reset) {
       b.ctl[0] = 0;
@@ -964,12 +977,14 @@ __global__ void __launch_bounds__(512) als_solve_v_kernel(SolveArgs s, AlsBufs b
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) b.pinv3[e] = Pv[e];
 }
 
+#include "dp2_als_persist.cuh"
+
 // ------------------------------------------------------------ host side
 namespace {
 
 struct AlsLayout {
   size_t theta, pprev, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, L, s_g1, s_wtw, s_m2, s_wtw2, s_e, G2, g3,
-      ctl, total;
+      GD, ps_slots, ps_e, ps_C, ctl, total;
 };
 
 int sm_count() {
@@ -1051,6 +1066,11 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.s_e = take(nbm * 8);
   L.G2 = take(J * R * 8);
   L.g3 = take(K * R * 8);
+  const size_t ps_cap = (size_t)sm_count() * PS_CAP_PER_SM;
+  L.GD = take(RR);
+  L.ps_slots = take(ps_cap * 2 * RR);
+  L.ps_e = take(ps_cap * 8);
+  L.ps_C = take(RR);
   L.ctl = take(64);
   L.total = off;
   return L;
@@ -1079,6 +1099,10 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.s_e = d(L.s_e);
   b.G2 = d(L.G2);
   b.g3 = d(L.g3);
+  b.GD = d(L.GD);
+  b.ps_slots = d(L.ps_slots);
+  b.ps_e = d(L.ps_e);
+  b.ps_C = d(L.ps_C);
   b.ctl = reinterpret_cast<int32_t*>(ws + L.ctl);
   b.nwt = total_warps(K, R);
   b.wpb = wpb_for(R);
@@ -1230,6 +1254,47 @@ SolveArgs solve_args(const double* D, const double* E, double* H, double* V, dou
   return sv;
 }
 
+bool persist_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("DP2_ALS_PERSIST");
+    v = (s && s[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int R>
+cudaError_t launch_persist_t(const PsArgs& p, const AlsBufs& b, cudaStream_t st) {
+  using Cf = PsCfg<R>;
+  const size_t smem = Cf::smem_bytes();
+  const void* fn = (const void*)als_persist_kernel<R>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, Cf::WPB * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+  const int64_t cap = (int64_t)sm_count() * (occ < PS_CAP_PER_SM ? occ : PS_CAP_PER_SM);
+  int64_t grid = (p.K + Cf::WPB - 1) / Cf::WPB;
+  grid = grid < cap ? grid : cap;
+  PsArgs pa = p;
+  AlsBufs ba = b;
+  void* args[] = {&pa, &ba};
+  return cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(Cf::WPB * 32), args, smem, st);
+}
+
+cudaError_t launch_persist(int R, const PsArgs& p, const AlsBufs& b, cudaStream_t st) {
+  switch (R) {
+#define DP2_PS_CASE(N) \
+  case N: return launch_persist_t<N>(p, b, st);
+    DP2_PS_CASE(1) DP2_PS_CASE(2) DP2_PS_CASE(3) DP2_PS_CASE(4) DP2_PS_CASE(5) DP2_PS_CASE(6)
+    DP2_PS_CASE(7) DP2_PS_CASE(8) DP2_PS_CASE(9) DP2_PS_CASE(10) DP2_PS_CASE(11) DP2_PS_CASE(12)
+    DP2_PS_CASE(13) DP2_PS_CASE(14) DP2_PS_CASE(15) DP2_PS_CASE(16)
+#undef DP2_PS_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
 
 size_t als_bytes(int64_t K, int64_t J, int R) { return als_layout(K, J, R).total; }
@@ -1237,12 +1302,45 @@ size_t als_bytes(int64_t K, int64_t J, int R) { return als_layout(K, J, R).total
 cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
                     int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
-                    char* ws, int64_t* status, cudaStream_t st) {
+                    char* ws, int64_t* status, cudaStream_t st, int64_t* launches) {
+  if (launches) *launches = 1 + 7 * (int64_t)max_iters;
   AlsBufs b = make_bufs(ws, K, J, R);
   SliceArgs a = slice_args(F, D, E, H, V, W, K, J, R, status);
   a.polar = polar;
   a.theta = b.theta;
   SolveArgs sv = solve_args(D, E, H, V, W, J, R, normalize, b, status);
+  if (persist_enabled() && R <= 16) {
+    PsArgs p{};
+    p.F = F;
+    p.D = D;
+    p.E = E;
+    p.H = H;
+    p.V = V;
+    p.W = W;
+    p.polar = polar;
+    p.trace = trace;
+    p.tstamp = tstamp;
+    p.iters = iters;
+    p.K = K;
+    p.J = J;
+    p.max_iters = max_iters;
+    p.normalize = normalize;
+    p.tol = tol;
+    p.slots = b.ps_slots;
+    p.eslots = b.ps_e;
+    p.C = b.ps_C;
+    p.GD = b.GD;
+    p.bar = reinterpret_cast<unsigned*>(b.ctl + 8);
+    p.status = status;
+    als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, tstamp, 1);
+    const cudaError_t pe = launch_persist(R, p, b, st);
+    if (pe == cudaSuccess) {
+      if (launches) *launches = 2;
+      return cudaSuccess;
+    }
+    (void)cudaGetLastError();  // not co-resident here: the multi-kernel loop below
+  }
+  b.GD = nullptr;
   cudaError_t e = prepare(R, b);
   if (e != cudaSuccess) return e;
   als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, tstamp, 1);

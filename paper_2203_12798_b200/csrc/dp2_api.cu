@@ -241,9 +241,11 @@ int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, in
   if (max_iters < 1) return fail_arg("max_iters must be >= 1");
   if (R < 1 || R > 64 || K < 1 || J < 1) return fail_arg("invalid ALS shape");
   if (ws_bytes < dp2::als_bytes(K, J, R)) return fail_arg("workspace too small");
+  int64_t launches = 0;
   cudaError_t e = dp2::als_run(F, D, E, K, J, R, H, V, W, polar_out, max_iters, tol, normalize, trace_out,
-                               tstamp_out, iters_out, use_graph, static_cast<char*>(ws), status_dev, S(stream));
-  return e == cudaSuccess ? ok(1 + 7 * (int64_t)max_iters) : fail(e, "dp2_als_run");
+                               tstamp_out, iters_out, use_graph, static_cast<char*>(ws), status_dev, S(stream),
+                               &launches);
+  return e == cudaSuccess ? ok(launches) : fail(e, "dp2_als_run");
 }
 
 int dp2_als_phase(int32_t phase, const double* F, const double* D, const double* E, int64_t K, int64_t J,

@@ -44,7 +44,7 @@ struct AlsCtx;  // defined in dp2_als.cu
 cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
                     int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
-                    char* ws, int64_t* status, cudaStream_t stream);
+                    char* ws, int64_t* status, cudaStream_t stream, int64_t* launches = nullptr);
 cudaError_t als_phase(int phase, const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                       double* H, double* V, double* W, double* polar, int it, double tol, int normalize,
                       double* trace, int64_t* tstamp, int32_t* iters, const double* red_in, double* red_out,
