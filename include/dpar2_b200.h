@@ -181,8 +181,13 @@ int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_
  * (``prev == 0 || |prev - e| <= tol * prev``, P/solver.py:180-184); writes the
  * objective trace, globaltimer stamps (ns, max_iters+1) and the executed
  * iteration count; polar_out (K x R x R) holds Z_k P_k^T of the last executed
- * iteration.  use_graph != 0 captures the loop in a CUDA graph. */
+ * iteration.  use_graph != 0 captures the loop in a CUDA graph (multi-kernel
+ * path only).  For R <= 16 the loop is one cooperative launch; with the
+ * environment variable DP2_ALS_STAMPS set it also records 16 globaltimer
+ * slots per iteration (first 64 iterations) at byte offset
+ * dp2_als_stamp_offset(K, J, R) of the workspace (profiling aid). */
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R);
+size_t dp2_als_stamp_offset(int64_t K, int64_t J, int32_t R);
 int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R,
                 double* H, double* V, double* W, double* polar_out, int32_t max_iters, double tol,
                 int32_t normalize, double* trace_out, int64_t* tstamp_out, int32_t* iters_out,

@@ -57,6 +57,7 @@ _SIGS = {
     "dp2_stage2_workspace": (c_sz, [c_i64, c_i64, c_i32, c_i32]),
     "dp2_stage2": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "dp2_als_workspace": (c_sz, [c_i64, c_i64, c_i32]),
+    "dp2_als_stamp_offset": (c_sz, [c_i64, c_i64, c_i32]),
     "dp2_als_run": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_f64, c_i32,
                             c_vp, c_vp, c_vp, c_i32, c_vp, c_sz, c_vp, c_vp]),
     "dp2_als_phase": (c_i32, [c_i32, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_f64,

@@ -19,110 +19,11 @@
 // is one CUDA graph (P/solver.py:180-184 evaluated on the device).
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
+#include "dp2_als_persist.cuh"
 #include <cstdio>
 #include <cstdlib>
 
 namespace dp2 {
-
-struct AlsBufs {
-  double *theta, *pprev, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2, *L;
-  double *s_g1, *s_wtw, *s_m2, *s_wtw2, *s_e, *G2, *g3;
-  double *GD, *ps_slots, *ps_e, *ps_C;  // persistent loop: D^T D, per-CTA partial slots, V = D C
-  int32_t* ctl;  // [0] stop flag, [1] warm-start valid, [8] persistent-loop grid barrier counter
-  int nwt;       // total warps in the per-slice kernels
-  int wpb;       // warps per block
-  int nb;        // blocks == partial slots
-  int nbm;       // metric kernel blocks (slots)
-  int nbr, wpbr; // rotate kernel blocks (slots of s_g1 / s_wtw) and warps per block
-};
-
-__host__ __device__ inline int wpb_for(int R) { return R <= 16 ? 8 : (R <= 32 ? 4 : 1); }
-__host__ __device__ inline int ldt_for(int R) { return R | 1; }
-// per-warp smem: Ts, Vr (R x ldt), Fs, Th, Pi (R x R), two partial accumulators (R x R), tmp (4R)
-__host__ __device__ inline size_t warp_smem_doubles(int R) {
-  const int ldt = ldt_for(R);
-  return (size_t)2 * R * ldt + 5 * (size_t)R * R + 4 * R;
-}
-__host__ __device__ inline size_t cta_shared_doubles(int R) { return 3 * (size_t)R * R + 2 * R; }
-
-DP2_DEV uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-struct CtaShared {
-  double *cc, *H, *E, *aux, *vec;
-};
-DP2_DEV CtaShared carve_cta(double* base, int R) {
-  CtaShared s;
-  s.cc = base;
-  s.H = s.cc + R * R;
-  s.E = s.H + R * R;
-  s.aux = s.E + R;
-  s.vec = s.aux + R * R;
-  return s;
-}
-
-// ------------------------------------------------------------ polar factor
-// Pi = Z P^T of T (column-major in Ts, already multiplied by the warm start
-// Vr = P_prev) via one-sided Jacobi; exact-zero singular directions are
-// completed to an orthonormal set (LAPACK likewise returns some completion).
-DP2_DEV void warp_polar(double* Ts, double* Vr, int ldt, int R, double* pi, double* nrm, int64_t* status,
-                        int64_t k) {
-  const int lane = threadIdx.x & 31;
-  const int sw = jacobi_onesided_warp(Ts, ldt, Vr, ldt, R);
-  if (sw > 60 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
-  for (int i = lane; i < R; i += 32) {
-    double s = 0.0;
-    for (int a = 0; a < R; ++a) s = fma(Ts[i * ldt + a], Ts[i * ldt + a], s);
-    nrm[i] = sqrt(s);
-  }
-  __syncwarp();
-  for (int e = lane; e < R * R; e += 32) {
-    const int i = e / R, a = e % R;
-    const double n = nrm[i];
-    Ts[i * ldt + a] = n > 1e-300 ? Ts[i * ldt + a] / n : 0.0;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    bool def = false;
-    for (int i = 0; i < R; ++i) def |= !(nrm[i] > 1e-300);
-    if (def) {
-      for (int i = 0; i < R; ++i) {
-        if (nrm[i] > 1e-300) continue;
-        for (int t = 0; t < R; ++t) {
-          double* z = Ts + i * ldt;
-          for (int a = 0; a < R; ++a) z[a] = (a == t) ? 1.0 : 0.0;
-          for (int pass = 0; pass < 2; ++pass)
-            for (int c = 0; c < R; ++c) {
-              if (c == i || !(nrm[c] > 1e-300)) continue;
-              double d = 0.0;
-              for (int a = 0; a < R; ++a) d = fma(Ts[c * ldt + a], z[a], d);
-              for (int a = 0; a < R; ++a) z[a] = fma(-d, Ts[c * ldt + a], z[a]);
-            }
-          double n2 = 0.0;
-          for (int a = 0; a < R; ++a) n2 = fma(z[a], z[a], n2);
-          if (n2 > 0.25) {
-            const double inv = 1.0 / sqrt(n2);
-            for (int a = 0; a < R; ++a) z[a] *= inv;
-            nrm[i] = 1.0;
-            break;
-          }
-        }
-        if (!(nrm[i] > 1e-300)) status_min(status, ST_POLAR, k);
-      }
-    }
-  }
-  __syncwarp();
-  for (int e = lane; e < R * R; e += 32) {  // Pi[a][d] = sum_i Z[a][i] P[d][i]
-    const int a = e / R, d = e % R;
-    double s = 0.0;
-    for (int i = 0; i < R; ++i) s = fma(Ts[i * ldt + a], Vr[i * ldt + d], s);
-    pi[e] = s;
-  }
-  __syncwarp();
-}
 
 // ------------------------------------------------------------ helpers
 __global__ void reduce_parts_dev(const double* part, int nparts, int64_t size, double* out) {
@@ -210,6 +111,7 @@ __global__ void als_prep_kernel(const double* D, const double* E, const double* 
       if (lane == 0) b.GD[e] = s;
     }
   }
+  if (b.ps_gcnt && threadIdx.x < 64) b.ps_gcnt[threadIdx.x] = 0u;
   if (threadIdx.x == 0) {
     b.ctl[8] = 0;
     for (int r = 0; r < R; ++r) b.nh[r] = 1.0;
@@ -365,24 +267,6 @@ template <int R>
 __host__ __device__ constexpr int grp_doubles() { return 13 * R * R + 2 * R * (R | 1) + 8 * R; }
 template <int R>
 __host__ __device__ constexpr int grp_per_warp() { return 1; }
-
-// C = op(A) op(B) for R x R row-major smem matrices; lanes over outputs
-template <int R, bool TA, bool TB>
-DP2_DEV void wmm(const double* A, const double* B, double* C) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int it = 0; it < (R * R + 31) / 32; ++it) {
-    const int e = lane + 32 * it;
-    if (e < R * R) {
-      const int i = e / R, j = e % R;
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < R; ++q) s = fma(TA ? A[q * R + i] : A[i * R + q], TB ? B[j * R + q] : B[q * R + j], s);
-      C[e] = s;
-    }
-  }
-  __syncwarp();
-}
 
 // Gauss-Jordan inverse with partial pivoting of the R x R matrix in aug[:, :R]
 // (aug is R x 2R); result in aug[:, R:].  Returns false on a zero pivot.
@@ -707,148 +591,6 @@ __global__ void __launch_bounds__(256) als_metric_kernel(AlsBufs b, const double
   if (threadIdx.x == 0) b.s_e[blockIdx.x] = tot;
 }
 
-// ------------------------------------------------------------ solves (1 CTA)
-// pinv of the symmetric PSD R x R Hadamard-of-Grams matrix (P/linalg.py:135-151).
-// Fast path (warp 0): Cholesky A = L L^T and the explicit inverse; it is
-// accepted when every pivot is positive and the Frobenius condition estimate
-// ||A||_F ||A^-1||_F < 1e10, i.e. far from the reference's drop threshold
-// (sigma <= R sigma_max 1e-12), where pinv(A) == inv(A) up to rounding.
-// Otherwise: Jacobi eigen-decomposition with the reference's threshold.
-DP2_DEV bool warp_chol_inverse(const double* A, int R, double* Lw, double* out, double* dinv) {
-  const int lane = threadIdx.x & 31;
-  // factor: column k pivot by lane 0, then lanes fill column k below the diagonal
-  bool okay = true;
-  for (int k = 0; k < R; ++k) {
-    double d = 0.0;
-    if (lane == 0) {
-      double t = A[k * R + k];
-      for (int m = 0; m < k; ++m) t = fma(-Lw[k * R + m], Lw[k * R + m], t);
-      d = t;
-    }
-    d = __shfl_sync(0xffffffffu, d, 0);
-    if (!(d > 0.0)) { okay = false; break; }
-    const double l = sqrt(d);
-    for (int i = k + 1 + lane; i < R; i += 32) {
-      double t = A[i * R + k];
-      for (int m = 0; m < k; ++m) t = fma(-Lw[i * R + m], Lw[k * R + m], t);
-      Lw[i * R + k] = t / l;
-    }
-    if (lane == 0) Lw[k * R + k] = l;
-    __syncwarp();
-  }
-  if (!okay) return false;
-  // inverse: lane j solves L y = e_j then L^T x = y (column j of A^-1), in
-  // place in ``out`` (shared) with reciprocal pivots -- no local arrays
-  for (int i = lane; i < R; i += 32) dinv[i] = 1.0 / Lw[i * R + i];
-  __syncwarp();
-  double an = 0.0, in = 0.0;
-  for (int j = lane; j < R; j += 32) {
-    for (int i = 0; i < R; ++i) {
-      double t = (i == j) ? 1.0 : 0.0;
-      for (int m = j; m < i; ++m) t = fma(-Lw[i * R + m], out[m * R + j], t);
-      out[i * R + j] = i < j ? 0.0 : t * dinv[i];
-    }
-    for (int i = R - 1; i >= 0; --i) {
-      double t = out[i * R + j];
-      for (int m = i + 1; m < R; ++m) t = fma(-Lw[m * R + i], out[m * R + j], t);
-      out[i * R + j] = t * dinv[i];
-    }
-    for (int i = 0; i < R; ++i) {
-      an = fma(A[i * R + j], A[i * R + j], an);
-      in = fma(out[i * R + j], out[i * R + j], in);
-    }
-  }
-  an = warp_sum(an);
-  in = warp_sum(in);
-  __syncwarp();
-  return sqrt(an) * sqrt(in) < 1e10;
-}
-
-// Register Gauss-Jordan inverse, R known at compile time: lane c < 2R owns
-// column c of [A | I] in registers; per pivot k the row factors come from
-// lane k by shuffle, so a step is one reciprocal and R independent
-// shuffle+FMA pairs (a runtime R would predicate every shuffle; measured 3.75x
-// slower -- tools/inv_probe.cu).  No pivoting: only the SPD fast path, accepted
-// under the Cholesky path's tests (positive pivots, ||A||_F ||A^-1||_F < 1e10).
-template <int R>
-DP2_DEV bool warp_gj_inverse(const double* A, double* out) {
-  const int lane = threadIdx.x & 31;
-  double col[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) col[i] = lane < R ? A[i * R + lane] : (lane < 2 * R && i == lane - R ? 1.0 : 0.0);
-  bool okay = true;
-#pragma unroll
-  for (int k = 0; k < R; ++k) {
-    const double piv = __shfl_sync(0xffffffffu, col[k], k);
-    okay &= piv > 0.0;
-    const double rk = col[k] * (1.0 / piv);
-    double f[R];
-#pragma unroll
-    for (int i = 0; i < R; ++i) f[i] = __shfl_sync(0xffffffffu, col[i], k);
-#pragma unroll
-    for (int i = 0; i < R; ++i) col[i] = (i == k) ? rk : fma(-f[i], rk, col[i]);
-  }
-  double an = 0.0, in = 0.0;
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    if (lane < R) an = fma(A[i * R + lane], A[i * R + lane], an);
-    if (lane >= R && lane < 2 * R) {
-      out[i * R + (lane - R)] = col[i];
-      in = fma(col[i], col[i], in);
-    }
-  }
-  an = warp_sum(an);
-  in = warp_sum(in);
-  __syncwarp();
-  return okay && sqrt(an) * sqrt(in) < 1e10;
-}
-
-DP2_DEV bool warp_fast_inverse(const double* A, int R, double* Lw, double* out, double* dinv) {
-  switch (R) {
-#define DP2_GJ(n) \
-  case n:         \
-    return warp_gj_inverse<n>(A, out);
-    DP2_GJ(2) DP2_GJ(3) DP2_GJ(4) DP2_GJ(5) DP2_GJ(6) DP2_GJ(7) DP2_GJ(8) DP2_GJ(9) DP2_GJ(10) DP2_GJ(11) DP2_GJ(12)
-    DP2_GJ(13) DP2_GJ(14) DP2_GJ(15) DP2_GJ(16)
-#undef DP2_GJ
-    default:
-      return warp_chol_inverse(A, R, Lw, out, dinv);
-  }
-}
-
-DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status) {
-  __shared__ double lmax;
-  __shared__ int fast;
-  if (threadIdx.x < 32) {
-    const bool okay = warp_fast_inverse(A, R, U, out, cs);
-    if (threadIdx.x == 0) fast = okay ? 1 : 0;
-  }
-  __syncthreads();
-  if (fast) return;
-  if (threadIdx.x < 32) {
-    const int sw = jacobi_eig_warp(A, R, U, R, R, cs);
-    if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
-    if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int i = 0; i < R; ++i) m = fmax(m, fabs(A[i * R + i]));
-      lmax = m;
-    }
-  }
-  __syncthreads();
-  const double tolr = R * lmax * 1e-12;
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    const int i = e / R, j = e % R;
-    double s = 0.0;
-    if (lmax > 0.0)
-      for (int q = 0; q < R; ++q) {
-        const double l = A[q * R + q];
-        if (fabs(l) > tolr) s += U[i * R + q] * (1.0 / l) * U[j * R + q];
-      }
-    out[e] = s;
-  }
-  __syncthreads();
-}
-
 struct SolveArgs {
   const double *D, *E;
   double *H, *V, *W;
@@ -977,14 +719,13 @@ __global__ void __launch_bounds__(512) als_solve_v_kernel(SolveArgs s, AlsBufs b
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) b.pinv3[e] = Pv[e];
 }
 
-#include "dp2_als_persist.cuh"
 
 // ------------------------------------------------------------ host side
 namespace {
 
 struct AlsLayout {
   size_t theta, pprev, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, L, s_g1, s_wtw, s_m2, s_wtw2, s_e, G2, g3,
-      GD, ps_slots, ps_e, ps_C, ctl, total;
+      GD, ps_slots, ps_e, ps_C, ps_stamps, ps_gslots, ps_gcnt, ctl, total;
 };
 
 int sm_count() {
@@ -1071,6 +812,9 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.ps_slots = take(ps_cap * 2 * RR);
   L.ps_e = take(ps_cap * 8);
   L.ps_C = take(RR);
+  L.ps_stamps = take(64 * 16 * 8);
+  L.ps_gslots = take(64 * 2 * RR);
+  L.ps_gcnt = take(64 * 4);
   L.ctl = take(64);
   L.total = off;
   return L;
@@ -1103,6 +847,9 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.ps_slots = d(L.ps_slots);
   b.ps_e = d(L.ps_e);
   b.ps_C = d(L.ps_C);
+  b.ps_stamps = reinterpret_cast<int64_t*>(ws + L.ps_stamps);
+  b.ps_gslots = d(L.ps_gslots);
+  b.ps_gcnt = reinterpret_cast<unsigned*>(ws + L.ps_gcnt);
   b.ctl = reinterpret_cast<int32_t*>(ws + L.ctl);
   b.nwt = total_warps(K, R);
   b.wpb = wpb_for(R);
@@ -1263,41 +1010,20 @@ bool persist_enabled() {
   return v == 1;
 }
 
-template <int R>
-cudaError_t launch_persist_t(const PsArgs& p, const AlsBufs& b, cudaStream_t st) {
-  using Cf = PsCfg<R>;
-  const size_t smem = Cf::smem_bytes();
-  const void* fn = (const void*)als_persist_kernel<R>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, Cf::WPB * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
-  const int64_t cap = (int64_t)sm_count() * (occ < PS_CAP_PER_SM ? occ : PS_CAP_PER_SM);
-  int64_t grid = (p.K + Cf::WPB - 1) / Cf::WPB;
-  grid = grid < cap ? grid : cap;
-  PsArgs pa = p;
-  AlsBufs ba = b;
-  void* args[] = {&pa, &ba};
-  return cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(Cf::WPB * 32), args, smem, st);
-}
-
 cudaError_t launch_persist(int R, const PsArgs& p, const AlsBufs& b, cudaStream_t st) {
-  switch (R) {
-#define DP2_PS_CASE(N) \
-  case N: return launch_persist_t<N>(p, b, st);
-    DP2_PS_CASE(1) DP2_PS_CASE(2) DP2_PS_CASE(3) DP2_PS_CASE(4) DP2_PS_CASE(5) DP2_PS_CASE(6)
-    DP2_PS_CASE(7) DP2_PS_CASE(8) DP2_PS_CASE(9) DP2_PS_CASE(10) DP2_PS_CASE(11) DP2_PS_CASE(12)
-    DP2_PS_CASE(13) DP2_PS_CASE(14) DP2_PS_CASE(15) DP2_PS_CASE(16)
-#undef DP2_PS_CASE
-    default: return cudaErrorInvalidValue;
-  }
+  const int sms = sm_count();
+  if (R >= 1 && R <= 4) return launch_persist_a(R, p, b, sms, st);
+  if (R <= 8) return launch_persist_b(R, p, b, sms, st);
+  if (R <= 12) return launch_persist_c(R, p, b, sms, st);
+  if (R <= 16) return launch_persist_d(R, p, b, sms, st);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 size_t als_bytes(int64_t K, int64_t J, int R) { return als_layout(K, J, R).total; }
+// byte offset of the persistent loop's phase stamps inside the workspace (profiling)
+size_t als_stamp_offset(int64_t K, int64_t J, int R) { return als_layout(K, J, R).ps_stamps; }
 
 cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
@@ -1332,6 +1058,9 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
     p.GD = b.GD;
     p.bar = reinterpret_cast<unsigned*>(b.ctl + 8);
     p.status = status;
+    p.gslots = b.ps_gslots;
+    p.gcnt = b.ps_gcnt;
+    p.stamps = getenv("DP2_ALS_STAMPS") ? reinterpret_cast<int64_t*>(b.ps_stamps) : nullptr;
     als_prep_kernel<<<1, 256, 0, st>>>(D, E, V, J, R, b, tstamp, 1);
     const cudaError_t pe = launch_persist(R, p, b, st);
     if (pe == cudaSuccess) {

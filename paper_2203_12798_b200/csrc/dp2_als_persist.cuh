@@ -1,4 +1,5 @@
-// Persistent ALS loop (included by dp2_als.cu inside namespace dp2).
+// Persistent ALS loop: kernel template and launcher (instantiated for R = 1..16
+// in dp2_als_ps{a,b,c,d}.cu, dispatched from dp2_als.cu).
 //
 // The whole iteration loop of P/solver.py:152-184 in ONE cooperative launch:
 // every CTA is resident, slices are owned by warps (warp w of the grid handles
@@ -25,21 +26,28 @@
 // held in registers (lane j owns column j), warm-started from the previous
 // iteration's right singular vectors of the same slice.
 
+#pragma once
+#include "dp2_als_dev.cuh"
+#include <cstdlib>
+
+namespace dp2 {
+
 constexpr int PS_CAP_PER_SM = 2;  // grid cap (partial slots are sized for it)
 
 template <int R>
 struct PsCfg {
   static constexpr int RR = R * R, LDT = R | 1;
-  static constexpr int WPB = R <= 12 ? 16 : 8;  // warps per CTA
+  static constexpr int N = R + (R & 1);  // Jacobi columns (a zero column pads odd R)
+  static constexpr int MAXW = 8;         // warps per CTA (upper bound; 255 registers)
   // per-warp shared layout (doubles)
-  static constexpr int FS = 0, TH = RR, T = 2 * RR, US = 3 * RR, VS = 4 * RR, PI = 5 * RR, ACC1 = 6 * RR,
+  static constexpr int FS = 0, T = RR, US = 2 * RR, VS = 3 * RR, TH = 4 * RR, PI = 5 * RR, ACC1 = 6 * RR,
                        ACC2 = 7 * RR, TS = 8 * RR, VR = TS + R * LDT, TMP = VR + R * LDT, WTOT = TMP + 8 * R;
   // per-CTA shared layout (doubles)
   static constexpr int CC = 0, H = RR, VTV = 2 * RR, HTH = 3 * RR, C = 4 * RR, P3 = 5 * RR, GD = 6 * RR,
                        RED = 7 * RR /* 2 RR */, M = 9 * RR, U = 10 * RR, PV = 11 * RR, X = 12 * RR, Y = 13 * RR,
                        E = 14 * RR, NH = E + R, NRM = NH + R, CS = NRM + R, WE = CS + 3 * (R / 2 + 1) + 8,
                        CTOT = WE + 32;
-  static constexpr size_t smem_bytes() { return ((size_t)CTOT + (size_t)WPB * WTOT) * 8; }
+  static constexpr size_t smem_bytes(int wpb) { return ((size_t)CTOT + (size_t)wpb * WTOT) * 8; }
 };
 
 struct PsArgs {
@@ -54,7 +62,32 @@ struct PsArgs {
   double *slots, *eslots, *C, *GD;
   unsigned* bar;
   int64_t* status;
+  double* gslots;    // per-group partial slots (<= 64 groups)
+  unsigned* gcnt;    // per-group arrival counters (zeroed by the prep kernel)
+  int64_t* stamps;  // optional (DP2_ALS_STAMPS=1): CTA 0's globaltimer at phase boundaries, 16 per iteration
 };
+
+#define PS_STAMP(slot)                                                                    \
+  do {                                                                                    \
+    if (p.stamps && blockIdx.x == 0 && threadIdx.x == 0 && it < 64)                       \
+      p.stamps[it * 16 + (slot)] = (int64_t)globaltimer_ns();                              \
+  } while (0)
+
+DP2_DEV float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+DP2_DEV float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+DP2_DEV float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 DP2_DEV unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -81,10 +114,10 @@ DP2_DEV void ps_grid_barrier(unsigned* bar, unsigned& target) {
 // by every CTA: warp w sums a fixed contiguous block range for all entries
 // (L2 loads, the slots were written by other SMs), then the warps' partials
 // combine in warp order.  Deterministic for a given grid size.
-template <int N, int WPB>
+template <int N>
 DP2_DEV void ps_reduce_slots(const double* slots, int nblk, double* wscr, int wstride, double* out) {
   constexpr int NE = (N + 31) / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, WPB = blockDim.x >> 5;
   const int per = (nblk + WPB - 1) / WPB, b0 = warp * per, b1 = min(nblk, b0 + per);
   double v[NE];
 #pragma unroll
@@ -104,11 +137,37 @@ DP2_DEV void ps_reduce_slots(const double* slots, int nblk, double* wscr, int ws
   __syncthreads();
   for (int e = threadIdx.x; e < N; e += blockDim.x) {
     double s = 0.0;
-#pragma unroll
     for (int w = 0; w < WPB; ++w) s += wscr[w * wstride + e];
     out[e] = s;
   }
   __syncthreads();
+}
+
+// Two-level ordered reduction, level 1: CTAs form groups of ~sqrt(nblk);
+// after writing its slot each CTA arrives on its group's counter and the
+// group's last arrival folds the group's slots (in CTA order) into the group
+// slot before entering the grid barrier.  Level 2 (after the barrier) is then
+// a reduction over <= ~sqrt(nblk) group slots instead of nblk CTA slots.
+DP2_DEV int ps_group_size(int nblk) {
+  int g = 1;
+  while (g * g < nblk) ++g;
+  return g;
+}
+
+template <int N>
+DP2_DEV void ps_group_fold(const double* slots, double* gslots, unsigned* gcnt, double* wscr, int wstride) {
+  __shared__ int last;
+  const int nblk = gridDim.x, GS = ps_group_size(nblk), grp = blockIdx.x / GS;
+  const int gsz = min(GS, nblk - grp * GS);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(gcnt + grp, 1u);
+    last = ((old + 1) % (unsigned)gsz) == 0;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  if (last) ps_reduce_slots<N>(slots + (size_t)grp * GS * N, gsz, wscr, wstride, gslots + (size_t)grp * N);
 }
 
 // C = op(A) op(B) for R x R row-major matrices, all threads of the CTA
@@ -124,122 +183,95 @@ DP2_DEV void cta_mm(const double* A, const double* B, double* C) {
   __syncthreads();
 }
 
-// One-sided Jacobi (Hestenes) on the columns held by lanes 0..R-1: a = column
-// of A = T V, v = column of V.  Round-robin pairing (R-1 or R rounds per
-// sweep); both lanes of a pair compute bitwise-identical (alpha, beta, gamma)
-// -- fma(x, y, z) is symmetric in x, y -- so they apply the same rotation.
-// Returns the sweeps used (cap + 1 when not converged).
+// One-sided Jacobi (Hestenes): lane j < R holds column j of A = T V (a) and
+// of V (v); a zero column pads odd R.  Round-robin pairing, N - 1 rounds per
+// sweep.  Both lanes of a pair compute bitwise-identical (alpha, beta, gamma)
+// -- fma(x, y, z) is symmetric in x, y -- hence the same rotation.  The
+// rotation angle only has to be accurate enough to converge: t comes from
+// fp32 arithmetic on the power-of-two-scaled (beta - alpha, 2 gamma), while
+// c = (1 + t^2)^-1/2 and s = c t are fp64, so every applied rotation is
+// orthogonal to fp64 rounding.  Stops after a sweep whose largest relative
+// off-diagonal |gamma| / sqrt(alpha beta) was below 1e-6 (quadratic
+// convergence leaves ~1e-12 after it).  Returns the sweeps used (cap + 1
+// when not converged).  Measured on B200 (tools/fp64_probe.cu): ~630 cycles
+// per round at R = 10, about half of it the angle's dependent chain.
 template <int R>
 DP2_DEV int jacobi_reg(double (&a)[R], double (&v)[R]) {
-  constexpr int N = R + (R & 1);
-  constexpr int CAP = 40;
-  constexpr double TOL = 4.0 * R * 2.220446049250313e-16;
+  constexpr int N = PsCfg<R>::N, CAP = 40;
+  constexpr double TOL = 4.0 * R * 2.220446049250313e-16, TOL2 = TOL * TOL;
   const int lane = threadIdx.x & 31;
   for (int sw = 0; sw < CAP; ++sw) {
-    bool rot = false;
+    bool big = false;
+#pragma unroll 1
     for (int r = 0; r < N - 1; ++r) {
-      int p;
-      if (lane >= N) p = lane;
-      else if (lane == N - 1) p = r;
-      else if (lane == r) p = N - 1;
-      else p = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+      int pj = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+      pj = (lane == r) ? N - 1 : pj;
+      pj = (lane == N - 1) ? r : pj;
+      const int p = lane < N ? pj : lane;
       double pa[R], pv[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         pa[i] = __shfl_sync(0xffffffffu, a[i], p);
         pv[i] = __shfl_sync(0xffffffffu, v[i], p);
       }
-      double al = 0.0, be = 0.0, ga = 0.0;
+      double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < R; ++i) {
-        al = fma(a[i], a[i], al);
-        be = fma(pa[i], pa[i], be);
-        ga = fma(a[i], pa[i], ga);
+      for (int i = 0; i < R; i += 2) {
+        al0 = fma(a[i], a[i], al0);
+        be0 = fma(pa[i], pa[i], be0);
+        ga0 = fma(a[i], pa[i], ga0);
+        if (i + 1 < R) {
+          al1 = fma(a[i + 1], a[i + 1], al1);
+          be1 = fma(pa[i + 1], pa[i + 1], be1);
+          ga1 = fma(a[i + 1], pa[i + 1], ga1);
+        }
       }
+      const double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
       const bool lower = lane < p;
       const double alpha = lower ? al : be, beta = lower ? be : al;
-      if (p != lane && fabs(ga) > TOL * sqrt(alpha * beta)) {
-        const double zeta = (beta - alpha) / (2.0 * ga);
-        const double az = fabs(zeta);
-        const double t = az > 1e100 ? 0.5 / zeta : copysign(1.0, zeta) / (az + sqrt(fma(zeta, zeta, 1.0)));
-        const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = c * t;
-        const double so = lower ? -s : s;
+      const double g2ab = ga * ga, ab = alpha * beta;
+      double c = 1.0, s = 0.0;
+      if (p != lane && g2ab > TOL2 * ab) {
+        const double d = beta - alpha, g2 = 2.0 * ga;
+        const int hi = max(__double2hiint(alpha), __double2hiint(beta));  // both > 0
+        const int ex = min(max(((hi >> 20) & 0x7ff) - 1023, -1000), 1000);
+        const double sc = __hiloint2double((1023 - ex) << 20, 0);  // 2^-ex: max(alpha, beta) sc in [1, 2)
+        const float df = (float)(d * sc), gf = (float)(g2 * sc);
+        const float af = (float)(alpha * sc), bf = (float)(beta * sc);
+        big |= 0.25f * gf * gf > 1e-12f * (af * bf);  // relative off-diagonal above 1e-6
+        float tf = (df >= 0.f ? gf : -gf) * rcp_approx(fabsf(df) + sqrt_approx(fmaf(df, df, gf * gf)));
+        double t = (double)tf;
+        if (fabsf(tf) <= 1e-30f) t = g2 / (2.0 * d);  // |zeta| beyond fp32 range: t ~ 1 / (2 zeta)
+        // c = (1 + t^2)^-1/2 to fp64 accuracy: fp32 estimate + two Newton steps
+        const double x = fma(t, t, 1.0);
+        double y = (double)rsqrt_approx((float)x);
+        y = y * fma(-0.5 * x, y * y, 1.5);
+        y = y * fma(-0.5 * x, y * y, 1.5);
+        c = y;
+        s = c * t;
+      }
+      const double so = lower ? -s : s;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-          a[i] = fma(c, a[i], so * pa[i]);
-          v[i] = fma(c, v[i], so * pv[i]);
-        }
-        rot = true;
+      for (int i = 0; i < R; ++i) {
+        a[i] = fma(c, a[i], so * pa[i]);
+        v[i] = fma(c, v[i], so * pv[i]);
       }
     }
-    if (!__any_sync(0xffffffffu, rot)) return sw + 1;
+    if (!__any_sync(0xffffffffu, big)) return sw + 1;
   }
   return CAP + 1;
 }
 
-// polar factor of T (row-major, per-warp smem) -> Pi; V of T's SVD -> Vs
-// (warm start in: Vs holds the previous V or I).  Singular T (an exactly zero
-// singular value) or a non-converged sweep falls back to warp_polar's
-// orthonormal completion.
 template <int R>
-DP2_DEV void ps_polar(double* w, int64_t k, int64_t* status) {
+__global__ void __launch_bounds__(PsCfg<R>::MAXW * 32, 1) als_persist_kernel(PsArgs p, AlsBufs b) {
   using Cf = PsCfg<R>;
   constexpr int RR = R * R, LDT = Cf::LDT;
-  const int lane = threadIdx.x & 31;
-  double* T = w + Cf::T;
-  double* Us = w + Cf::US;
-  double* Vs = w + Cf::VS;
-  double* Pi = w + Cf::PI;
-  wmm<R, false, false>(T, Vs, Us);  // A = T V_warm
-  double a[R], v[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) {
-    a[i] = lane < R ? Us[i * R + lane] : 0.0;
-    v[i] = lane < R ? Vs[i * R + lane] : 0.0;
-  }
-  const int sw = jacobi_reg<R>(a, v);
-  double s2 = 0.0;
-#pragma unroll
-  for (int i = 0; i < R; ++i) s2 = fma(a[i], a[i], s2);
-  const double sig = sqrt(s2);
-  const bool bad = lane < R && !(sig > 1e-300 && sig < 1e300);
-  __syncwarp();
-  if (__any_sync(0xffffffffu, bad) || sw > 40) {
-    double* Ts = w + Cf::TS;
-    double* Vr = w + Cf::VR;
-    for (int e = lane; e < RR; e += 32) {
-      const int i = e / R, c = e % R;
-      Ts[c * LDT + i] = T[e];
-      Vr[c * LDT + i] = (i == c) ? 1.0 : 0.0;
-    }
-    __syncwarp();
-    warp_polar(Ts, Vr, LDT, R, Pi, w + Cf::TMP, status, k);
-    for (int e = lane; e < RR; e += 32) Vs[e] = (e / R == e % R) ? 1.0 : 0.0;  // next warm start: cold
-    __syncwarp();
-    return;
-  }
-  const double inv = 1.0 / sig;
-  if (lane < R) {
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      Us[i * R + lane] = a[i] * inv;
-      Vs[i * R + lane] = v[i];
-    }
-  }
-  __syncwarp();
-  wmm<R, false, true>(Us, Vs, Pi);  // Pi = U V^T
-}
-
-template <int R>
-__global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsArgs p, AlsBufs b) {
-  using Cf = PsCfg<R>;
-  constexpr int RR = R * R, WPB = Cf::WPB;
   extern __shared__ __align__(16) double sm[];
   double* cs = sm;
   double* w = sm + Cf::CTOT + (size_t)(threadIdx.x >> 5) * Cf::WTOT;
   double* wscr = sm + Cf::CTOT + Cf::ACC1;  // per-warp 2RR scratch (acc1|acc2) for the slot reductions
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int nblk = gridDim.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, WPB = blockDim.x >> 5;
+  const int nblk = gridDim.x, ngrp = (nblk + ps_group_size(nblk) - 1) / ps_group_size(nblk);
   const int64_t gw = (int64_t)blockIdx.x * WPB + wib, nw = (int64_t)nblk * WPB;
   unsigned bar_target = 0;
   double* cc = cs + Cf::CC;
@@ -274,24 +306,26 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
   double prev_e = 0.0;
   int it = 0;
   for (; it < p.max_iters; ++it) {
-    // ---------------- rotate + mode-1 partials
+    PS_STAMP(0);
+    // ---------------- rotate + mode-1 partials: G slices of this warp per Jacobi
     double* acc1 = w + Cf::ACC1;
     double* acc2 = w + Cf::ACC2;
+    double* Th = w + Cf::TH;
+    double* Pi = w + Cf::PI;
     for (int e = lane; e < RR; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
     for (int64_t k = gw; k < p.K; k += nw) {
+      const long long dq0 = clock64();  // profiling (stamps only)
       double* Fs = w + Cf::FS;
-      double* Th = w + Cf::TH;
       double* T = w + Cf::T;
+      double* Us = w + Cf::US;
       double* Vs = w + Cf::VS;
-      double* Pi = w + Cf::PI;
-      const double* wk = p.W + k * R;
       for (int e = lane; e < RR; e += 32) {
         Fs[e] = __ldg(p.F + k * RR + e);
         Vs[e] = it > 0 ? __ldcg(b.pprev + k * RR + e) : ((e / R == e % R) ? 1.0 : 0.0);
       }
       double wr[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) wr[r] = __ldcg(wk + r);
+      for (int r = 0; r < R; ++r) wr[r] = __ldcg(p.W + k * R + r);
       __syncwarp();
       wmm<R, false, false>(Fs, cc, Th);  // Th = F_k cc
       for (int e = lane; e < RR; e += 32) {
@@ -301,8 +335,49 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
         Th[e] = s;
       }
       __syncwarp();
-      wmm<R, false, true>(Th, Hs, T);  // T = Th H^T
-      ps_polar<R>(w, k, p.status);
+      wmm<R, false, true>(Th, Hs, T);   // T = Th H^T
+      wmm<R, false, false>(T, Vs, Us);  // A = T V_warm
+      // polar factor: one-sided Jacobi SVD of A in registers
+      double a[R], v[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        a[i] = lane < R ? Us[i * R + lane] : 0.0;
+        v[i] = lane < R ? Vs[i * R + lane] : 0.0;
+      }
+      const long long dq1 = clock64();
+      const int sw = jacobi_reg<R>(a, v);
+      const long long dq2 = clock64();
+      double s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i) s2 = fma(a[i], a[i], s2);
+      const double sig = sqrt(s2);
+      const bool bad = lane < R && !(sig > 1e-300 && sig < 1e300);
+      __syncwarp();
+      if (__any_sync(0xffffffffu, bad) || sw > 40) {
+        // singular T (or no convergence): one-sided Jacobi with orthonormal completion
+        double* Ts = w + Cf::TS;
+        double* Vr = w + Cf::VR;
+        for (int e = lane; e < RR; e += 32) {
+          const int i = e / R, c = e % R;
+          Ts[c * LDT + i] = T[e];
+          Vr[c * LDT + i] = (i == c) ? 1.0 : 0.0;
+        }
+        __syncwarp();
+        warp_polar(Ts, Vr, LDT, R, Pi, w + Cf::TMP, p.status, k);
+        for (int e = lane; e < RR; e += 32) Vs[e] = (e / R == e % R) ? 1.0 : 0.0;  // next warm start: cold
+        __syncwarp();
+      } else {
+        if (lane < R) {
+          const double inv = 1.0 / sig;
+#pragma unroll
+          for (int i = 0; i < R; ++i) {
+            Us[i * R + lane] = a[i] * inv;
+            Vs[i * R + lane] = v[i];
+          }
+        }
+        __syncwarp();
+        wmm<R, false, true>(Us, Vs, Pi);  // Pi = U V^T
+      }
       for (int e = lane; e < RR; e += 32) {
         b.pprev[k * RR + e] = Vs[e];
         p.polar[k * RR + e] = Pi[e];
@@ -324,6 +399,15 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
         acc2[e] += wi * wrr;
       }
       __syncwarp();
+      if (p.stamps && lane == 0 && it < 64) {  // per-warp maxima: setup, Jacobi, epilogue cycles, sweeps, total
+        unsigned long long* q = reinterpret_cast<unsigned long long*>(p.stamps + it * 16);
+        const long long dq3 = clock64();
+        atomicMax(q + 11, (unsigned long long)(dq1 - dq0));
+        atomicMax(q + 12, (unsigned long long)(dq2 - dq1));
+        atomicMax(q + 13, (unsigned long long)(dq3 - dq2));
+        atomicMax(q + 14, (unsigned long long)sw);
+        atomicMax(q + 15, (unsigned long long)(dq3 - dq0));
+      }
     }
     __syncthreads();
     for (int e = threadIdx.x; e < 2 * RR; e += blockDim.x) {
@@ -331,12 +415,17 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
       for (int q = 0; q < WPB; ++q) s += sm[Cf::CTOT + (size_t)q * Cf::WTOT + Cf::ACC1 + e];
       p.slots[(size_t)blockIdx.x * 2 * RR + e] = s;
     }
+    ps_group_fold<2 * RR>(p.slots, p.gslots, p.gcnt, wscr, Cf::WTOT);
+    PS_STAMP(1);
     ps_grid_barrier(p.bar, bar_target);
+    PS_STAMP(2);
     // ---------------- solve_h (every CTA)
-    ps_reduce_slots<2 * RR, WPB>(p.slots, nblk, wscr, Cf::WTOT, red);  // red = [G1 | W'W]
+    ps_reduce_slots<2 * RR>(p.gslots, ngrp, wscr, Cf::WTOT, red);  // red = [G1 | W'W]
+    PS_STAMP(8);
     for (int e = threadIdx.x; e < RR; e += blockDim.x) M[e] = red[RR + e] * VtV[e];
     __syncthreads();
-    block_pinv_sym(M, U, Pv, R, csc, p.status);
+    block_pinv_sym<R>(M, U, Pv, R, csc, p.status);
+    PS_STAMP(9);
     cta_mm<R, false, false>(red, Pv, X);  // Hn = G1 pinv
     for (int c = threadIdx.x; c < R; c += blockDim.x) {
       double n2 = 0.0;
@@ -352,6 +441,7 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
     }
     __syncthreads();
     cta_mm<R, true, false>(Hs, Hs, HtH);
+    PS_STAMP(3);
     // ---------------- mode-2 partials
     for (int e = lane; e < RR; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
     for (int64_t k = gw; k < p.K; k += nw) {
@@ -383,15 +473,19 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
       for (int q = 0; q < WPB; ++q) s += sm[Cf::CTOT + (size_t)q * Cf::WTOT + Cf::ACC1 + e];
       p.slots[(size_t)blockIdx.x * 2 * RR + e] = s;
     }
+    ps_group_fold<2 * RR>(p.slots, p.gslots, p.gcnt, wscr, Cf::WTOT);
+    PS_STAMP(4);
     ps_grid_barrier(p.bar, bar_target);
+    PS_STAMP(5);
     // ---------------- solve_v (every CTA), V = D C implicit
-    ps_reduce_slots<2 * RR, WPB>(p.slots, nblk, wscr, Cf::WTOT, red);  // red = [summed | W''W'']
+    ps_reduce_slots<2 * RR>(p.gslots, ngrp, wscr, Cf::WTOT, red);  // red = [summed | W''W'']
+    PS_STAMP(10);
     for (int e = threadIdx.x; e < RR; e += blockDim.x) {
       M[e] = red[RR + e] * HtH[e];
       Y[e] = Es[e / R] * red[e];  // E * summed
     }
     __syncthreads();
-    block_pinv_sym(M, U, Pv, R, csc, p.status);
+    block_pinv_sym<R>(M, U, Pv, R, csc, p.status);
     cta_mm<R, false, false>(Y, Pv, X);   // EP = (E * summed) pinv
     cta_mm<R, false, false>(GD, X, Y);   // G_D EP
     for (int c = threadIdx.x; c < R; c += blockDim.x) {
@@ -412,7 +506,8 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
     cta_mm<R, true, false>(Cm, Y, VtV);   // V^T V = C^T G_D C
     for (int e = threadIdx.x; e < RR; e += blockDim.x) M[e] = VtV[e] * HtH[e];
     __syncthreads();
-    block_pinv_sym(M, U, P3, R, csc, p.status);
+    block_pinv_sym<R>(M, U, P3, R, csc, p.status);
+    PS_STAMP(6);
     // ---------------- mode-3: W_k and the residual
     double eacc = 0.0;
     for (int64_t k = gw; k < p.K; k += nw) {
@@ -470,6 +565,7 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
       for (int q = 0; q < WPB; ++q) s += we[q];
       p.eslots[blockIdx.x] = s;
     }
+    PS_STAMP(7);
     ps_grid_barrier(p.bar, bar_target);
     // ---------------- e, trace, stop rule (every CTA, identical decision)
     if (threadIdx.x < 32) {
@@ -501,3 +597,40 @@ __global__ void __launch_bounds__(PsCfg<R>::WPB * 32, 1) als_persist_kernel(PsAr
     p.V[idx] = s;
   }
 }
+
+// Grid shape: one slice per warp (the rotation is latency-bound per warp),
+// the K warps spread over all SMs, at most MAXW warps and the smem budget per
+// CTA; larger K loops each warp over several slices.
+template <int R>
+cudaError_t launch_persist_t(const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st) {
+  using Cf = PsCfg<R>;
+  const void* fn = (const void*)als_persist_kernel<R>;
+  int maxw = Cf::MAXW;
+  while (maxw > 1 && Cf::smem_bytes(maxw) > 220 * 1024) --maxw;
+  const int64_t warps = p.K;
+  int wpb = (int)((warps + sms - 1) / sms);
+  if (const char* env = getenv("DP2_ALS_WPB")) wpb = atoi(env);
+  wpb = wpb < 1 ? 1 : (wpb > maxw ? maxw : wpb);
+  const size_t smem = Cf::smem_bytes(wpb);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, wpb * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+  const int64_t cap = (int64_t)sms * (occ < PS_CAP_PER_SM ? occ : PS_CAP_PER_SM);
+  int64_t grid = (warps + wpb - 1) / wpb;
+  grid = grid < cap ? grid : cap;
+  PsArgs pa = p;
+  AlsBufs ba = b;
+  void* args[] = {&pa, &ba};
+  return cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(wpb * 32), args, smem, st);
+}
+
+// one per translation unit (R ranges 1-4, 5-8, 9-12, 13-16)
+cudaError_t launch_persist_a(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+cudaError_t launch_persist_b(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+cudaError_t launch_persist_c(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+cudaError_t launch_persist_d(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+
+}  // namespace dp2

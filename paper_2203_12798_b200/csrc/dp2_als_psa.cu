@@ -1,0 +1,14 @@
+// Persistent ALS loop instances for R = 1..4 (see dp2_als_persist.cuh).
+#include "dp2_als_persist.cuh"
+
+namespace dp2 {
+cudaError_t launch_persist_a(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st) {
+  switch (R) {
+#define DP2_PS_CASE(N) \
+  case N: return launch_persist_t<N>(p, b, sms, st);
+    DP2_PS_CASE(1) DP2_PS_CASE(2) DP2_PS_CASE(3) DP2_PS_CASE(4)
+#undef DP2_PS_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+}  // namespace dp2

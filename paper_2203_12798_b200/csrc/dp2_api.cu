@@ -233,6 +233,7 @@ int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_
 }
 
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }
+size_t dp2_als_stamp_offset(int64_t K, int64_t J, int32_t R) { return dp2::als_stamp_offset(K, J, R); }
 
 int dp2_als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int32_t R, double* H,
                 double* V, double* W, double* polar_out, int32_t max_iters, double tol, int32_t normalize,

@@ -40,6 +40,7 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
                        double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t stream);
 
 size_t als_bytes(int64_t K, int64_t J, int R);
+size_t als_stamp_offset(int64_t K, int64_t J, int R);
 struct AlsCtx;  // defined in dp2_als.cu
 cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K, int64_t J, int R,
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
