@@ -324,6 +324,105 @@ DP2_DEV int jacobi_onesided_warp(double* T, int ldt, double* Vr, int ldv, int n,
   return sweep + 1;
 }
 
+// ---------------------------------------------------------------- register Jacobi
+DP2_DEV float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+DP2_DEV float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+DP2_DEV float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One-sided Jacobi (Hestenes) on an R x R matrix held column-wise in
+// registers: lane j < R holds column j (a) and, with WITHV, column j of the
+// accumulated right rotations V (v); a zero column pads odd R.  For a
+// symmetric PSD input the converged columns are lambda_j u_j (eigenpairs) and
+// V is not needed.  Round-robin pairing, N - 1 rounds per
+// sweep.  Both lanes of a pair compute bitwise-identical (alpha, beta, gamma)
+// -- fma(x, y, z) is symmetric in x, y -- hence the same rotation.  The
+// rotation angle only has to be accurate enough to converge: t comes from
+// fp32 arithmetic on the power-of-two-scaled (beta - alpha, 2 gamma), while
+// c = (1 + t^2)^-1/2 and s = c t are fp64, so every applied rotation is
+// orthogonal to fp64 rounding.  Stops after a sweep whose largest relative
+// off-diagonal |gamma| / sqrt(alpha beta) was below 1e-6 (quadratic
+// convergence leaves ~1e-12 after it).  Returns the sweeps used (cap + 1
+// when not converged).  Measured on B200 (tools/fp64_probe.cu): ~630 cycles
+// per round at R = 10, about half of it the angle's dependent chain.
+template <int R, bool WITHV>
+DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
+  constexpr int N = R + (R & 1), CAP = 40;
+  constexpr double TOL = 4.0 * R * 2.220446049250313e-16, TOL2 = TOL * TOL;
+  const int lane = threadIdx.x & 31;
+  for (int sw = 0; sw < CAP; ++sw) {
+    bool big = false;
+#pragma unroll 1
+    for (int r = 0; r < N - 1; ++r) {
+      int pj = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+      pj = (lane == r) ? N - 1 : pj;
+      pj = (lane == N - 1) ? r : pj;
+      const int p = lane < N ? pj : lane;
+      double pa[R], pv[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        pa[i] = __shfl_sync(0xffffffffu, a[i], p);
+        if (WITHV) pv[i] = __shfl_sync(0xffffffffu, v[i], p);
+      }
+      double al0 = 0.0, be0 = 0.0, ga0 = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; i += 2) {
+        al0 = fma(a[i], a[i], al0);
+        be0 = fma(pa[i], pa[i], be0);
+        ga0 = fma(a[i], pa[i], ga0);
+        if (i + 1 < R) {
+          al1 = fma(a[i + 1], a[i + 1], al1);
+          be1 = fma(pa[i + 1], pa[i + 1], be1);
+          ga1 = fma(a[i + 1], pa[i + 1], ga1);
+        }
+      }
+      const double al = al0 + al1, be = be0 + be1, ga = ga0 + ga1;
+      const bool lower = lane < p;
+      const double alpha = lower ? al : be, beta = lower ? be : al;
+      const double g2ab = ga * ga, ab = alpha * beta;
+      double c = 1.0, s = 0.0;
+      if (p != lane && g2ab > TOL2 * ab) {
+        const double d = beta - alpha, g2 = 2.0 * ga;
+        const int hi = max(__double2hiint(alpha), __double2hiint(beta));  // both > 0
+        const int ex = min(max(((hi >> 20) & 0x7ff) - 1023, -1000), 1000);
+        const double sc = __hiloint2double((1023 - ex) << 20, 0);  // 2^-ex: max(alpha, beta) sc in [1, 2)
+        const float df = (float)(d * sc), gf = (float)(g2 * sc);
+        const float af = (float)(alpha * sc), bf = (float)(beta * sc);
+        big |= 0.25f * gf * gf > 1e-12f * (af * bf);  // relative off-diagonal above 1e-6
+        float tf = (df >= 0.f ? gf : -gf) * rcp_approx(fabsf(df) + sqrt_approx(fmaf(df, df, gf * gf)));
+        double t = (double)tf;
+        if (fabsf(tf) <= 1e-30f) t = g2 / (2.0 * d);  // |zeta| beyond fp32 range: t ~ 1 / (2 zeta)
+        // c = (1 + t^2)^-1/2 to fp64 accuracy: fp32 estimate + two Newton steps
+        const double x = fma(t, t, 1.0);
+        double y = (double)rsqrt_approx((float)x);
+        y = y * fma(-0.5 * x, y * y, 1.5);
+        y = y * fma(-0.5 * x, y * y, 1.5);
+        c = y;
+        s = c * t;
+      }
+      const double so = lower ? -s : s;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        a[i] = fma(c, a[i], so * pa[i]);
+        if (WITHV) v[i] = fma(c, v[i], so * pv[i]);
+      }
+    }
+    if (!__any_sync(0xffffffffu, big)) return sw + 1;
+  }
+  return CAP + 1;
+}
+
 DP2_DEV int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 

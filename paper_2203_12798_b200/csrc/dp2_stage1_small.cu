@@ -7,13 +7,13 @@
 //   gather        C^T = sum of pass-2 partials; CC = C C^T; G = sum of the
 //                 per-piece Y^T Y accumulated inside pass 2
 //   factor_warp   one warp per slice: G = L L^T (Cholesky; Jacobi-eig fallback
-//                 for rank deficiency), B B^T = L^-1 CC L^-T, Jacobi eig ->
-//                 P = L^-T U_R, S = sqrt(mu_R)
-//   argmax_a      per piece: A = Y P (unsigned) + per-column max |A| (first
-//                 index on ties) candidates
+//                 for rank deficiency), B B^T = L^-1 CC L^-T, register Jacobi
+//                 eig -> P = L^-T U_R, S = sqrt(mu_R)
+//   argmax_cand   per piece: per-column max |A| (first index on ties)
+//                 candidates of A = Y P, A not stored
 //   signs_m       per slice: sign rule (P/linalg.py:62-70), P *= sign,
 //                 M block = C^T P (= V S of the reference, P/compress.py:108)
-//   flip_a        A columns *= sign
+//   write_a       A = Y P (signed P), one pass
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
@@ -171,6 +171,39 @@ __global__ void __launch_bounds__(256) gram_y_kernel(const Y* y2, const int64_t*
 }
 
 // ------------------------------------------------------------ factor (warp / slice)
+// Symmetric PSD eigenproblem (n <= SP) by register one-sided Jacobi: lane j
+// holds column j; converged columns are lambda_j u_j, so the eigenvalues are
+// the column norms (written to A's diagonal) and the eigenvectors the
+// normalised columns (into U's columns).  Returns false (caller falls back to
+// the shared-memory two-sided Jacobi) on an exactly zero or non-finite column
+// norm or no convergence.
+template <int SP>
+DP2_DEV bool eig_sym_reg(double* A, int lda, double* U, int ldu, int n) {
+  const int lane = threadIdx.x & 31;
+  double a[SP], dummy[SP];
+#pragma unroll
+  for (int i = 0; i < SP; ++i) a[i] = (lane < n && i < n) ? A[i * lda + lane] : 0.0;
+  const int sw = jacobi_cols<SP, false>(a, dummy);
+  double s2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < SP; ++i) s2 = fma(a[i], a[i], s2);
+  const double lam = sqrt(s2);
+  const bool bad = lane < n && !(lam > 0.0 && lam < 1e300);
+  __syncwarp();
+  if (__any_sync(0xffffffffu, bad) || sw > 40) return false;
+  if (lane < n) {
+    const double inv = 1.0 / lam;
+#pragma unroll
+    for (int i = 0; i < SP; ++i)
+      if (i < n) U[i * ldu + lane] = a[i] * inv;
+  }
+  __syncwarp();
+  if (lane < n) A[lane * lda + lane] = lam;
+  __syncwarp();
+  return true;
+}
+
+template <int SP>
 __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, const double* CCg, const int32_t* s_k,
                                                            int K, int sp, int R, double* Pm, double* Sv,
                                                            int32_t* rank_out, int64_t* status) {
@@ -289,8 +322,10 @@ __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, cons
     __syncwarp();
   }
   // ---- eig(Bg) -> U, descending
-  const int sw = jacobi_eig_warp(CC, ld, U, ld, rp, cs);
-  if (sw > 40 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  if (!eig_sym_reg<SP>(CC, ld, U, ld, rp)) {
+    const int sw = jacobi_eig_warp(CC, ld, U, ld, rp, cs);
+    if (sw > 40 && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  }
   if (lane == 0) {
     for (int i = 0; i < rp; ++i) perm[i] = i;
     for (int i = 1; i < rp; ++i) {
@@ -337,67 +372,163 @@ __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, cons
   }
 }
 
-// ------------------------------------------------------------ A = Y P + argmax candidates
-template <typename Y>
-__global__ void __launch_bounds__(256) argmax_a_kernel(const Y* y2, const int64_t* row_off,
-                                                        const int32_t* piece_slice, const int64_t* piece_row0,
-                                                        const int32_t* piece_rows, const int32_t* s_k,
-                                                        const double* Pm, int sp, int R, double* A,
-                                                        double* cand_abs, int64_t* cand_row, int32_t* cand_neg) {
-  constexpr int TR = 128;
+// One row of Y (SP entries, fp32 or fp64 storage) into fp64 registers, entries
+// >= s zeroed (16 B loads).
+template <typename Y, int SP>
+DP2_DEV void load_y_row(const Y* yr, int s, double (&y)[SP]) {
+  if constexpr (sizeof(Y) == 4) {
+#pragma unroll
+    for (int q = 0; q < SP / 4; ++q) {
+      const float4 f = reinterpret_cast<const float4*>(yr)[q];
+      y[4 * q] = f.x; y[4 * q + 1] = f.y; y[4 * q + 2] = f.z; y[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SP / 2; ++q) {
+      const double2 f = reinterpret_cast<const double2*>(yr)[q];
+      y[2 * q] = f.x; y[2 * q + 1] = f.y;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < SP; ++a) y[a] = a < s ? y[a] : 0.0;
+}
+
+// (y0 P[:, c], y1 P[:, c]) with P stored transposed in shared memory (Pt =
+// R x SP, rows >= s of P zero): fma over a = 0..SP-1 in order, so padded
+// entries add exact zeros.
+template <int SP>
+DP2_DEV void dot_pcol(const double (&y0)[SP], const double (&y1)[SP], const double* Pt, int c, double& a0,
+                      double& a1) {
+  const double2* pc = reinterpret_cast<const double2*>(Pt + c * SP);
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int q = 0; q < SP / 2; ++q) {
+    const double2 pp = pc[q];
+    s0 = fma(y0[2 * q], pp.x, s0);
+    s1 = fma(y1[2 * q], pp.x, s1);
+    s0 = fma(y0[2 * q + 1], pp.y, s0);
+    s1 = fma(y1[2 * q + 1], pp.y, s1);
+  }
+  a0 = s0;
+  a1 = s1;
+}
+
+// ------------------------------------------------------------ argmax candidates of A = Y P
+// Per piece: the column-wise max |A| entry (first row on ties) of A = Y P,
+// without storing A (the signed A is written once the slice's signs are known,
+// write_a_kernel).  One thread per row: the row of Y in registers (16 B
+// loads), R dot products against P in shared memory (broadcast), running
+// per-column best in registers; rows of a thread increase, so strict '>' keeps
+// the first index, and the block merge orders ties by row.
+template <typename Y, int SP>
+__global__ void __launch_bounds__(256) argmax_cand_kernel(const Y* y2, const int64_t* row_off,
+                                                          const int32_t* piece_slice, const int64_t* piece_row0,
+                                                          const int32_t* piece_rows, const int32_t* s_k,
+                                                          const double* Pm, int R, double* cand_abs,
+                                                          int64_t* cand_row, int32_t* cand_neg) {
   extern __shared__ __align__(16) double sm[];
-  double* Ps = sm;                  // sp x R
-  double* ytile = Ps + sp * R;      // TR x sp
-  double* atile = ytile + TR * sp;  // TR x (R+1)
-  __shared__ double babs[64];
-  __shared__ int64_t brow[64];
-  __shared__ int bneg[64];
+  double* Pt = sm;                                   // R x SP (P transposed), entries a >= s zero
+  double* bval = Pt + SP * R;                        // R x 256 signed best values
+  int* brow = reinterpret_cast<int*>(bval + R * 256);  // R x 256 row within the piece
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = piece_slice[p], s = s_k[k];
-  const int64_t base = row_off[k], r0 = piece_row0[p], nr = piece_rows[p];
-  const int lda = R + 1;
-  for (int i = tid; i < sp * R; i += blockDim.x) Ps[i] = Pm[(size_t)k * sp * R + i];
-  for (int c = tid; c < R; c += blockDim.x) { babs[c] = -1.0; brow[c] = INT64_MAX; bneg[c] = 0; }
-  for (int64_t t0 = 0; t0 < nr; t0 += TR) {
-    const int rows = (int)imin64(TR, nr - t0);
-    __syncthreads();
-    for (int i = tid; i < rows * sp; i += blockDim.x) ytile[i] = (double)y2[(r0 + t0) * sp + i];
-    __syncthreads();
-    for (int e = tid; e < rows * R; e += blockDim.x) {
-      const int i = e / R, c = e % R;
-      double acc = 0.0;
-      for (int a = 0; a < s; ++a) acc = fma(ytile[i * sp + a], Ps[a * R + c], acc);
-      atile[i * lda + c] = acc;
-    }
-    __syncthreads();
-    for (int e = tid; e < rows * R; e += blockDim.x) A[(r0 + t0) * R + e] = atile[(e / R) * lda + e % R];
-    for (int c = warp; c < R; c += 8) {
-      double ba = -1.0;
-      int64_t br = INT64_MAX;
-      int bn = 0;
-      for (int i = lane; i < rows; i += 32) {
-        const double v = atile[i * lda + c], a = fabs(v);
-        if (a > ba) { ba = a; br = r0 + t0 + i - base; bn = v < 0.0; }
-      }
+  const int64_t base = row_off[k], r0 = piece_row0[p];
+  const int nr = piece_rows[p];
+  for (int i = tid; i < SP * R; i += 256) {
+    const int c = i / SP, a = i - c * SP;
+    Pt[i] = a < s ? Pm[(size_t)k * SP * R + a * R + c] : 0.0;
+  }
+  for (int c = 0; c < R; ++c) brow[c * 256 + tid] = -1;  // own slots
+  __syncthreads();
+  // rows i and i + 256 per step: a thread's rows still increase
+  for (int i = tid; i < nr; i += 512) {
+    const bool two = i + 256 < nr;
+    double y0[SP], y1[SP];
+    load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
+    if (two) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
+    else {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
-        const int64_t orow = __shfl_xor_sync(0xffffffffu, br, o);
-        const int on = __shfl_xor_sync(0xffffffffu, bn, o);
-        if (oa > ba || (oa == ba && orow < br)) { ba = oa; br = orow; bn = on; }
-      }
-      if (lane == 0 && (ba > babs[c] || (ba == babs[c] && br < brow[c]))) {
-        babs[c] = ba;
-        brow[c] = br;
-        bneg[c] = bn;
-      }
+      for (int a = 0; a < SP; ++a) y1[a] = 0.0;
+    }
+#pragma unroll 1
+    for (int c = 0; c < R; ++c) {
+      double a0, a1;
+      dot_pcol<SP>(y0, y1, Pt, c, a0, a1);
+      double bv = bval[c * 256 + tid];
+      int rw = brow[c * 256 + tid];
+      if (rw < 0 || fabs(a0) > fabs(bv)) { bv = a0; rw = i; }
+      if (two && fabs(a1) > fabs(bv)) { bv = a1; rw = i + 256; }
+      bval[c * 256 + tid] = bv;
+      brow[c * 256 + tid] = rw;
     }
   }
   __syncthreads();
-  for (int c = tid; c < R; c += blockDim.x) {
-    cand_abs[(size_t)p * R + c] = babs[c];
-    cand_row[(size_t)p * R + c] = brow[c];
-    cand_neg[(size_t)p * R + c] = bneg[c];
+  for (int c = warp; c < R; c += 8) {
+    double ba = -1.0, bv = 0.0;
+    int br = INT32_MAX;
+    for (int t = lane; t < 256; t += 32) {
+      const int rw = brow[c * 256 + t];
+      if (rw < 0) continue;
+      const double v = bval[c * 256 + t], a = fabs(v);
+      if (a > ba || (a == ba && rw < br)) { ba = a; br = rw; bv = v; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int orw = __shfl_xor_sync(0xffffffffu, br, o);
+      if (oa > ba || (oa == ba && orw < br)) { ba = oa; br = orw; bv = ov; }
+    }
+    if (lane == 0) {
+      cand_abs[(size_t)p * R + c] = ba;
+      cand_row[(size_t)p * R + c] = br == INT32_MAX ? INT64_MAX : r0 + br - base;
+      cand_neg[(size_t)p * R + c] = bv < 0.0;
+    }
+  }
+}
+
+// A = Y (P * sign) for the rows of a piece (P already signed by signs_m);
+// the same fma order as the candidate pass, so |A| there and here agree.
+// Rows staged through shared memory for coalesced stores.
+template <typename Y, int SP>
+__global__ void __launch_bounds__(256) write_a_kernel(const Y* y2, const int32_t* piece_slice,
+                                                      const int64_t* piece_row0, const int32_t* piece_rows,
+                                                      const int32_t* s_k, const double* Pm, int R, double* A) {
+  extern __shared__ __align__(16) double sm[];
+  double* Pt = sm;            // R x SP (P transposed)
+  double* at = Pt + SP * R;   // 512 x R output tile
+  const int p = blockIdx.x, tid = threadIdx.x;
+  const int k = piece_slice[p], s = s_k[k];
+  const int64_t r0 = piece_row0[p];
+  const int nr = piece_rows[p];
+  for (int i = tid; i < SP * R; i += 256) {
+    const int c = i / SP, a = i - c * SP;
+    Pt[i] = a < s ? Pm[(size_t)k * SP * R + a * R + c] : 0.0;
+  }
+  __syncthreads();
+  for (int t0 = 0; t0 < nr; t0 += 512) {
+    const int i = t0 + tid;
+    if (i < nr) {
+      double y0[SP], y1[SP];
+      load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
+      if (i + 256 < nr) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
+      else {
+#pragma unroll
+        for (int a = 0; a < SP; ++a) y1[a] = 0.0;
+      }
+#pragma unroll 1
+      for (int c = 0; c < R; ++c) {
+        double a0, a1;
+        dot_pcol<SP>(y0, y1, Pt, c, a0, a1);
+        at[tid * R + c] = a0;
+        at[(tid + 256) * R + c] = a1;
+      }
+    }
+    __syncthreads();
+    const int rows = min(512, nr - t0);
+    double* dst = A + (r0 + t0) * R;
+    for (int e = tid; e < rows * R; e += 256) dst[e] = at[e];
+    __syncthreads();
   }
 }
 
@@ -433,33 +564,65 @@ __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece
   __syncthreads();
   const double* C = Ct + (size_t)k * J * sp;
   const int64_t KR = (int64_t)K * R;
-  for (int64_t e = tid; e < (int64_t)J * R; e += blockDim.x) {
-    const int64_t j = e / R;
-    const int r = (int)(e % R);
+  for (int e = tid; e < J * R; e += blockDim.x) {
+    const int j = e / R, r = e - j * R;
     double acc = 0.0;
-    for (int a = 0; a < sp; ++a) acc = fma(C[j * sp + a], Ps[a * R + r], acc);
+    for (int a = 0; a < sp; ++a) acc = fma(C[(size_t)j * sp + a], Ps[a * R + r], acc);
     M[j * KR + (int64_t)k * R + r] = acc;
   }
 }
 
-__global__ void __launch_bounds__(256) flip_a_kernel(const int32_t* piece_slice, const int64_t* piece_row0,
-                                                      const int32_t* piece_rows, const double* sgn, int R,
-                                                      double* A) {
-  const int p = blockIdx.x;
-  const int k = piece_slice[p];
-  const int64_t r0 = piece_row0[p], nr = piece_rows[p];
-  for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) A[r0 * R + e] *= sgn[(size_t)k * R + e % R];
-}
-
 // ------------------------------------------------------------ host
 size_t small_factor_smem(int sp) { return (4 * (size_t)sp * (sp + 1) + 4 * (size_t)sp) * 8; }
+
+// factor -> argmax candidates -> signs + M -> signed A, for padded width SP
+template <int SP>
+cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const double* Gg, const double* CCg,
+                   const double* Ct, const double* y2, bool y32, double* Pm, double* Sv, double* sgn,
+                   double* cand_abs, int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
+                   int64_t* status, cudaStream_t stream) {
+  const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
+  const int wpb = SP <= 24 ? 4 : 2;
+  const size_t fs = wpb * small_factor_smem(SP);
+  cudaError_t e = cudaFuncSetAttribute(factor_warp_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
+  if (e != cudaSuccess) return e;
+  factor_warp_kernel<SP><<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, SP, R, Pm, Sv, rank_out,
+                                                                          status);
+  const size_t as = ((size_t)SP * R + (size_t)R * 256) * 8 + (size_t)R * 256 * 4;
+  const size_t ws = ((size_t)SP * R + 512 * (size_t)R) * 8;
+  if (y32) {
+    const float* y = reinterpret_cast<const float*>(y2);
+    e = cudaFuncSetAttribute(argmax_cand_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(write_a_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+    if (e != cudaSuccess) return e;
+    argmax_cand_kernel<float, SP><<<P, 256, as, stream>>>(y, st->row_off, st->piece_slice, st->piece_row0,
+                                                         st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
+    signs_m_kernel<<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+                                                            J, SP, R, sgn, M);
+    write_a_kernel<float, SP><<<P, 256, ws, stream>>>(y, st->piece_slice, st->piece_row0, st->piece_rows, s_dev, Pm,
+                                                     R, A);
+  } else {
+    e = cudaFuncSetAttribute(argmax_cand_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(write_a_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+    if (e != cudaSuccess) return e;
+    argmax_cand_kernel<double, SP><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0,
+                                                          st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
+    signs_m_kernel<<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+                                                            J, SP, R, sgn, M);
+    write_a_kernel<double, SP><<<P, 256, ws, stream>>>(y2, st->piece_slice, st->piece_row0, st->piece_rows, s_dev,
+                                                      Pm, R, A);
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, int R, const double* part1,
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
                              int64_t* status, int phase, cudaStream_t stream, bool y32) {
-  const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
+  const int K = (int)st->K, J = (int)st->J;
   const float* y2f = reinterpret_cast<const float*>(y2);
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
@@ -477,28 +640,13 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
     if (y32) gram_y_kernel<float><<<K, 256, 0, stream>>>(y2f, st->row_off, sp, Gg);
     else gram_y_kernel<double><<<K, 256, 0, stream>>>(y2, st->row_off, sp, Gg);
   }
-  const int wpb = sp <= 24 ? 4 : 2;
-  const size_t fs = wpb * small_factor_smem(sp);
-  e = cudaFuncSetAttribute(factor_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
-  if (e != cudaSuccess) return e;
-  factor_warp_kernel<<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, sp, R, Pm, Sv, rank_out,
-                                                                      status);
-  const size_t as = ((size_t)sp * R + 128 * (size_t)sp + 128 * (size_t)(R + 1)) * 8;
-  if (y32) {
-    e = cudaFuncSetAttribute(argmax_a_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
-    if (e != cudaSuccess) return e;
-    argmax_a_kernel<float><<<P, 256, as, stream>>>(y2f, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows,
-                                                   s_dev, Pm, sp, R, A, cand_abs, cand_row, cand_neg);
-  } else {
-    e = cudaFuncSetAttribute(argmax_a_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
-    if (e != cudaSuccess) return e;
-    argmax_a_kernel<double><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0, st->piece_rows,
-                                                    s_dev, Pm, sp, R, A, cand_abs, cand_row, cand_neg);
+  switch (sp) {
+    case 8: return post_t<8>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 16: return post_t<16>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 24: return post_t<24>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 32: return post_t<32>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    default: return cudaErrorInvalidValue;
   }
-  signs_m_kernel<<<K, 256, (size_t)sp * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
-                                                          J, sp, R, sgn, M);
-  flip_a_kernel<<<P, 256, 0, stream>>>(st->piece_slice, st->piece_row0, st->piece_rows, sgn, R, A);
-  return cudaGetLastError();
 }
 
 }  // namespace dp2
