@@ -84,6 +84,11 @@ int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms);
 int32_t dp2_set_sketch_engine(int32_t engine);
 /* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
 int dp2_status_init(int64_t* status_dev, void* stream);
+/* Stream-ordered upload of a small PINNED host buffer by a kernel reading it
+ * through the UVA mapping (no copy engine: it cannot queue behind bulk
+ * uploads submitted earlier on another stream).  The host buffer must stay
+ * valid until the stream reaches the copy. */
+int dp2_copy_h2d_small(void* dst_dev, const void* src_pinned, size_t nbytes, void* stream);
 
 /* ------------------------------------------------------------------ host planning
  * Alg. 4 LPT partition, bit-exact with P/scheduler.py:29-51 (greedy_partition):
@@ -135,6 +140,12 @@ int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, i
  * a NaN/Inf (status[0]); mirrors IrregularTensor's isfinite check
  * (P/tensor.py:61) and total_sq_norm (P/tensor.py:79-80). */
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream);
+/* The same isfinite check on HOST slices (ptrs[k]: rows[k] x J, row stride
+ * ld[k] elements, dtype DP2_F32/DP2_F64), multithreaded (threads <= 0: all
+ * hardware threads), so it runs while the upload of the same slices is in
+ * flight; *first_bad = lowest non-finite slice or INT64_MAX. */
+int dp2_host_first_nonfinite(const void* const* ptrs, const int64_t* rows, const int64_t* ld, int64_t K, int64_t J,
+                             int32_t dtype, int32_t threads, int64_t* first_bad);
 
 /* ------------------------------------------------------------------ stage 1
  * Per-slice randomized SVD (P/linalg.py:97-132 with power_iters = 1, as called

@@ -135,23 +135,85 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     from .tensor import to_device_async
     s_dev = to_device_async(widths, torch.int32, dev)
     t_omega = time.perf_counter() - t0
-    nseg = nseg_for(tensor)
-    st, keep = tensor.store(nseg)
-    lib = _lib.lib()
     A = torch.empty((int(tensor.row_off_host[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
     status = new_status(dev) if status is None else status
-    ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), dev)
-    tm = (C.c_float * 8)() if timings is not None else None
-    _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
-                              _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
+    tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None)
     if timings is not None:
         timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
                        stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
-                       stage1_ms=tm[5], sp=sp, nseg=nseg, npieces=int(st.npieces))
+                       stage1_ms=tm[5], sp=sp, nseg=nseg_for(tensor), npieces=int(tensor.store(nseg_for(tensor))[0].npieces))
+    return A, M, rank_found, status
+
+
+def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False):
+    """One dp2_stage1 call over ``tensor``'s slices (omega / s_dev / outputs
+    already sliced to them); returns the phase timings when ``timed``."""
+    nseg = nseg_for(tensor)
+    st, keep = tensor.store(nseg)
+    lib = _lib.lib()
+    ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), tensor.X.device)
+    tm = (C.c_float * 8)() if timed else None
+    _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
+                              _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
     del keep, ws
+    return tm
+
+
+# status words holding a (min) slice index (INT64_MAX = none) and counters;
+# slices, not index lists (a list index would copy from pageable memory,
+# which synchronises the stream)
+_ST_INDEX = (slice(0, 1), slice(2, 4))
+_ST_COUNT = (slice(1, 2), slice(4, 8))
+
+
+def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None):
+    """Stage 1 overlapped with the tensor's chunked upload: Omega for all
+    slices first (independent of X), then per upload chunk of whole slices the
+    compute stream waits for that chunk's copy event (device-side) and runs
+    stage 1 on a view of its slices with their global seeds, writing straight
+    into the full A / rank buffers (M block copied into place).  Per-chunk
+    status words merge with the slice offset."""
+    if base.power_iters != 1:
+        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
+    J, K = tensor.num_cols, tensor.num_slices
+    rows = tensor.row_counts
+    widths = [sketch_width(m, J, rank, base.oversampling) for m in rows]
+    sp = padded_width(max(widths))
+    dev = tensor.X.device
+    t0 = time.perf_counter()
+    rstats = {}
+    omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
+    from .tensor import to_device_async
+    s_dev = to_device_async(widths, torch.int32, dev)
+    t_omega = time.perf_counter() - t0
+    off = tensor.row_off_host
+    A = torch.empty((int(off[-1]), rank), dtype=torch.float64, device=dev)
+    M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
+    rank_found = torch.empty(K, dtype=torch.int32, device=dev)
+    status = new_status(dev)
+    bounds = [k1 for k1, _ in tensor._upload_events]
+    k0 = 0
+    for k1 in bounds:
+        tensor.wait_upload(k1)
+        r0, r1 = int(off[k0]), int(off[k1])
+        sub = IrregularTensor.from_packed(tensor.X[r0:r1], rows[k0:k1], J, dtype=tensor.dtype, check=False)
+        Mc = torch.empty((J, (k1 - k0) * rank), dtype=torch.float64, device=dev)
+        st_c = new_status(dev)
+        _stage1_call(sub, rank, omega[k0:k1], s_dev[k0:k1], sp, A[r0:r1], Mc, rank_found[k0:k1], st_c)
+        M[:, k0 * rank:k1 * rank].copy_(Mc)
+        for sl in _ST_INDEX:
+            idx = st_c[sl]
+            torch.minimum(status[sl], torch.where(idx == _lib.INT64_MAX, idx, idx + k0), out=status[sl])
+        for sl in _ST_COUNT:
+            status[sl] += st_c[sl]
+        k0 = k1
+    tensor.wait_upload()
+    if timings is not None:
+        timings.update(rstats)
+        timings.update(omega_host_s=t_omega, stage1_chunks=len(bounds), sp=sp)
     return A, M, rank_found, status
 
 
@@ -204,7 +266,10 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     om2_box = {}
     om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, K * rank, s2)))
     om2_thread.start()
-    A, M, rank_found, status = run_stage1(tensor, rank, base, timings=timings)
+    if len(tensor._upload_events) > 1:
+        A, M, rank_found, status = run_stage1_chunked(tensor, rank, base, timings=timings)
+    else:
+        A, M, rank_found, status = run_stage1(tensor, rank, base, timings=timings)
     om2_thread.join()
     D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2_box["v"], status, timings=timings)
     return CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,

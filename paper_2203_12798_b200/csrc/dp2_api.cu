@@ -9,6 +9,7 @@
 #include "dp2_internal.h"
 
 #include <atomic>
+#include <thread>
 
 namespace {
 thread_local std::string g_last_error;
@@ -85,6 +86,31 @@ int dp2_status_init(int64_t* status_dev, void* stream) {
   cudaError_t e = cudaMemcpyAsync(status_dev, init, sizeof(init), cudaMemcpyHostToDevice, S(stream));
   if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
   return e == cudaSuccess ? DP2_OK : fail(e, "dp2_status_init");
+}
+
+// ---------------------------------------------------------------- small uploads
+// Copies read pinned (UVA-mapped) host memory directly from a kernel: no copy
+// engine, so a few-KB upload on the compute stream never queues behind bulk
+// slice uploads already submitted on another stream.
+static __global__ void h2d_small_kernel(unsigned char* dst, const unsigned char* src, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((((uintptr_t)dst | (uintptr_t)src | n) & 7) == 0) {
+    for (size_t w = i; w < n / 8; w += (size_t)gridDim.x * blockDim.x)
+      reinterpret_cast<uint64_t*>(dst)[w] = reinterpret_cast<const volatile uint64_t*>(src)[w];
+  } else {
+    for (size_t b = i; b < n; b += (size_t)gridDim.x * blockDim.x) dst[b] = reinterpret_cast<const volatile unsigned char*>(src)[b];
+  }
+}
+
+int dp2_copy_h2d_small(void* dst_dev, const void* src_pinned, size_t nbytes, void* stream) {
+  if (nbytes == 0) return DP2_OK;
+  if (!dst_dev || !src_pinned) return fail_arg("null pointer");
+  const size_t words = (nbytes + 7) / 8;
+  const unsigned blocks = (unsigned)std::min<size_t>(64, (words + 255) / 256);
+  h2d_small_kernel<<<blocks, 256, 0, S(stream)>>>(static_cast<unsigned char*>(dst_dev),
+                                                  static_cast<const unsigned char*>(src_pinned), nbytes);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_copy_h2d_small");
 }
 
 // ---------------------------------------------------------------- planning
@@ -181,6 +207,55 @@ int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, i
     vals[n] = v;
     ok_out[n] = good;
   }
+  return DP2_OK;
+}
+
+// ---------------------------------------------------------------- host checks
+// all-ones exponent <=> NaN/Inf; integer tests, so the inner loops vectorise
+static bool rows_finite_f(const float* p, int64_t rows, int64_t ld, int64_t J) {
+  for (int64_t r = 0; r < rows; ++r) {
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(p + r * ld);
+    uint32_t bad = 0;
+    for (int64_t j = 0; j < J; ++j) bad |= ((row[j] & 0x7f800000u) == 0x7f800000u);
+    if (bad) return false;
+  }
+  return true;
+}
+static bool rows_finite_d(const double* p, int64_t rows, int64_t ld, int64_t J) {
+  for (int64_t r = 0; r < rows; ++r) {
+    const uint64_t* row = reinterpret_cast<const uint64_t*>(p + r * ld);
+    uint64_t bad = 0;
+    for (int64_t j = 0; j < J; ++j) bad |= ((row[j] & 0x7ff0000000000000ull) == 0x7ff0000000000000ull);
+    if (bad) return false;
+  }
+  return true;
+}
+
+int dp2_host_first_nonfinite(const void* const* ptrs, const int64_t* rows, const int64_t* ld, int64_t K, int64_t J,
+                             int32_t dtype, int32_t threads, int64_t* first_bad) {
+  if (K < 0 || J < 1 || !first_bad || (K && (!ptrs || !rows || !ld))) return fail_arg("invalid check arguments");
+  if (dtype != DP2_F32 && dtype != DP2_F64) return fail_arg("dtype must be DP2_F32 or DP2_F64");
+  std::atomic<int64_t> next{0}, bad{INT64_MAX};
+  auto work = [&]() {
+    for (int64_t k; (k = next.fetch_add(1)) < K;) {
+      if (k > bad.load(std::memory_order_relaxed)) continue;
+      const bool okk = dtype == DP2_F32 ? rows_finite_f(static_cast<const float*>(ptrs[k]), rows[k], ld[k], J)
+                                        : rows_finite_d(static_cast<const double*>(ptrs[k]), rows[k], ld[k], J);
+      if (!okk) {
+        int64_t cur = bad.load();
+        while (k < cur && !bad.compare_exchange_weak(cur, k)) {
+        }
+      }
+    }
+  };
+  int nt = threads > 0 ? threads : (int)std::thread::hardware_concurrency();
+  nt = std::max(1, std::min<int>(nt, 64));
+  if (K < 2 * nt) nt = std::max<int64_t>(1, K / 2);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  *first_bad = bad.load();
   return DP2_OK;
 }
 

@@ -4,8 +4,11 @@ All K slices (I_k x J) live in ONE device buffer of shape (sum I_k, ldx):
 slice k is rows [row_off[k], row_off[k+1]).  ``ldx`` pads rows to 16 bytes
 (padding columns are zero) so every row is a whole number of 16-byte
 ``cp.async`` chunks.  Construction mirrors the reference's validation order and
-messages (2-D, non-empty, consistent J, finite) -- the finiteness scan and the
-per-slice squared norms run on the device in one pass.
+messages (2-D, non-empty, consistent J, finite).  Host slices upload
+asynchronously in chunks of whole slices on a copy stream (one event per
+chunk, so stage 1 can start on the first chunks while the rest is in flight)
+and the finiteness scan runs on host threads over the same memory meanwhile;
+device inputs are scanned on the device.  Squared norms are computed lazily.
 
 ``dtype='f64'`` is the reference's float64 container; ``dtype='f32'`` is the
 optional fp32 mode (the reference sees the same values upcast exactly).
@@ -37,6 +40,19 @@ def device():
 
 def stream_ptr():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+_COPY_STREAMS = {}
+UPLOAD_CHUNKS = 6          # upload chunks of whole slices (stage 1 overlaps all but the last)
+UPLOAD_MIN_CHUNK = 64 << 20
+
+
+def copy_stream(dev):
+    """Per-device stream for host->device uploads."""
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _COPY_STREAMS[key]
 
 
 def sm_count():
@@ -99,8 +115,13 @@ class IrregularTensor:
         self._J = int(cols)
         self._rows = [int(a.shape[0]) for a in arrs]
         self._host = None if any(isinstance(a, torch.Tensor) for a in arrs) else arrs
-        self._upload(arrs)
-        self._stats()
+        self._upload_events = []
+        self._upload_keep = None
+        if all(not (isinstance(a, torch.Tensor) and a.device.type != "cpu") for a in arrs):
+            self._upload_host(arrs)
+        else:
+            self._upload(arrs)
+            self._stats()
 
     # ------------------------------------------------------------ construction
     @classmethod
@@ -113,6 +134,8 @@ class IrregularTensor:
         self._host = None
         self.X = packed
         self.ldx = packed.shape[1]
+        self._upload_events = []
+        self._upload_keep = None
         self._finish_layout()
         if check:
             self._stats()
@@ -123,7 +146,7 @@ class IrregularTensor:
         off = np.zeros(len(self._rows) + 1, np.int64)
         np.cumsum(self._rows, out=off[1:])
         self.row_off_host = off
-        self.row_off = torch.from_numpy(off).to(dev)
+        self.row_off = to_device_async(off, torch.int64, dev)
         self._plans = {}
         self._sqnorm = None
 
@@ -150,7 +173,102 @@ class IrregularTensor:
             r += n
         self._finish_layout()
 
+    def _upload_host(self, arrs):
+        """Host slices: chunked async H2D on the copy stream (pinned sources
+        are DMA'd directly; pageable ones are staged by the driver) with an
+        event per chunk of whole slices, and the reference's isfinite check
+        (P/tensor.py:61) on host threads while the copies are in flight."""
+        dev = device()
+        J = self._J
+        self.ldx = _ldx_for(J, self.dtype)
+        tdt, ndt = _TORCH[self.dtype], _NP[self.dtype]
+        srcs = []
+        for a in arrs:
+            if isinstance(a, torch.Tensor):
+                t = a if a.dtype == tdt else a.to(tdt)
+            else:
+                t = torch.from_numpy(np.asarray(a, dtype=ndt))
+            if t.stride(1) != 1:
+                t = t.contiguous()
+            srcs.append(t)
+        total = int(sum(self._rows))
+        self.X = torch.zeros((total, self.ldx), dtype=tdt, device=dev) if self.ldx != J else \
+            torch.empty((total, J), dtype=tdt, device=dev)
+        self._finish_layout()
+        cs = copy_stream(dev)
+        cs.wait_stream(torch.cuda.current_stream())  # the allocation / zero fill above
+        off = self.row_off_host
+        esz = torch.empty(0, dtype=tdt).element_size()
+        K = len(srcs)
+        events = []
+        target = max(UPLOAD_MIN_CHUNK, -(-total * J * esz // UPLOAD_CHUNKS))
+        with torch.cuda.stream(cs):
+            k0 = 0
+            while k0 < K:
+                k1, nbytes = k0, 0
+                while k1 < K and (k1 == k0 or nbytes < target):
+                    nbytes += self._rows[k1] * J * esz
+                    k1 += 1
+                self._copy_run(srcs, k0, k1, off, J)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                events.append((k1, ev))
+                k0 = k1
+        self._upload_events = events
+        self._upload_keep = srcs
+        # host isfinite scan over the same memory, concurrent with the DMA
+        ptrs = np.fromiter((t.data_ptr() for t in srcs), dtype=np.uint64, count=K)
+        rows = np.asarray(self._rows, dtype=np.int64)
+        lds = np.fromiter((t.stride(0) for t in srcs), dtype=np.int64, count=K)
+        bad = C.c_int64(0)
+        _lib.check(_lib.lib().dp2_host_first_nonfinite(
+            C.c_void_p(ptrs.ctypes.data), C.c_void_p(rows.ctypes.data), C.c_void_p(lds.ctypes.data), K, J,
+            _lib.DP2_F64 if self.dtype == "f64" else _lib.DP2_F32, 0, C.byref(bad)), "host_first_nonfinite")
+        if bad.value != _lib.INT64_MAX:
+            cs.synchronize()
+            raise NonFiniteInputError(f"slice {bad.value} contains non-finite values")
+
+    def _copy_run(self, srcs, k0, k1, off, J):
+        """Copy slices [k0, k1) into X: one copy per run of slices that are
+        row-contiguous views of one storage, else one per slice."""
+        k = k0
+        while k < k1:
+            t = srcs[k]
+            e = k + 1
+            if t.is_contiguous():
+                end = t.data_ptr() + t.numel() * t.element_size()
+                base = t.untyped_storage().data_ptr()
+                while e < k1 and srcs[e].is_contiguous() and srcs[e].data_ptr() == end and \
+                        srcs[e].untyped_storage().data_ptr() == base:
+                    end = srcs[e].data_ptr() + srcs[e].numel() * srcs[e].element_size()
+                    e += 1
+            r0, r1 = int(off[k]), int(off[e])
+            if e - k > 1:
+                src = torch.empty(0, dtype=t.dtype).set_(t.untyped_storage(), t.storage_offset(), (r1 - r0, J),
+                                                        (J, 1))
+            else:
+                src = t
+            dst = self.X[r0:r1] if self.ldx == J else self.X[r0:r1, :J]
+            dst.copy_(src, non_blocking=True)
+            k = e
+
+    def wait_upload(self, k_end=None):
+        """Make the current stream wait (device-side, no host sync) for the
+        upload of slices [0, k_end) -- all of it by default."""
+        if not self._upload_events:
+            return
+        cur = torch.cuda.current_stream()
+        if k_end is None:
+            cur.wait_event(self._upload_events[-1][1])
+            self._upload_events = []
+            return
+        for k1, ev in self._upload_events:
+            if k1 >= k_end:
+                cur.wait_event(ev)
+                return
+
     def _stats(self):
+        self.wait_upload()
         dev = self.X.device
         sq = torch.empty(self.num_slices, dtype=torch.float64, device=dev)
         status = new_status(dev)
@@ -183,12 +301,14 @@ class IrregularTensor:
                 sb.ctypes.data_as(P(C.c_int32)), sl.ctypes.data_as(P(C.c_int32)), C.byref(npc)), "plan_pieces")
             n = npc.value
             dev = self.X.device
-            arrays = dict(piece_slice=torch.from_numpy(ps[:n].copy()).to(dev),
-                          piece_row0=torch.from_numpy(pr0[:n].copy()).to(dev),
-                          piece_rows=torch.from_numpy(prs[:n].copy()).to(dev),
-                          seg_begin=torch.from_numpy(sb).to(dev), slice_piece=torch.from_numpy(sl).to(dev))
+            arrays = dict(piece_slice=to_device_async(ps[:n], torch.int32, dev),
+                          piece_row0=to_device_async(pr0[:n], torch.int64, dev),
+                          piece_rows=to_device_async(prs[:n], torch.int32, dev),
+                          seg_begin=to_device_async(sb, torch.int32, dev),
+                          slice_piece=to_device_async(sl, torch.int32, dev))
             self._plans[nseg] = (n, arrays, dict(piece_slice=ps[:n].copy(), slice_piece=sl.copy()))
         n, arrays, _ = self._plans[nseg]
+        self.wait_upload()
         st = _lib.Store()
         st.X = self.X.data_ptr()
         st.dtype = _lib.DP2_F64 if self.dtype == "f64" else _lib.DP2_F32
@@ -224,15 +344,17 @@ class IrregularTensor:
     def slices(self):
         """Host float64 views of the slices (the reference's ``slices``)."""
         if self._host is None:
+            self.wait_upload()
             x = self.X[:, :self._J].double().cpu().numpy()
             self._host = [x[a:b] for a, b in zip(self.row_off_host[:-1], self.row_off_host[1:])]
         return [np.asarray(a, dtype=np.float64) for a in self._host]
 
     def total_sq_norm(self):
-        return float(self._sqnorm.sum().item()) if self._sqnorm is not None else float(
-            (self.X.double() ** 2).sum().item())
+        return float(self.slice_sq_norms().sum().item())
 
     def slice_sq_norms(self):
+        if self._sqnorm is None:
+            self._stats()
         return self._sqnorm
 
 
@@ -244,7 +366,27 @@ def new_status(dev):
     return st
 
 
+_SMALL_KEEP = []          # (pinned source, completion event) of small uploads
+_SMALL_KEEP_MAX = 256
+
+
 def to_device_async(values, dtype, dev):
-    """Small host list/array -> device without an implicit synchronisation
-    (pageable host copies wait for the stream; pinned ones are async)."""
-    return torch.as_tensor(np.asarray(values), dtype=dtype).pin_memory().to(dev, non_blocking=True)
+    """Small host list/array -> device without an implicit synchronisation:
+    staged in pinned memory and copied by a kernel that reads it through the
+    UVA mapping (dp2_copy_h2d_small), so the upload neither synchronises the
+    stream (pageable copies do) nor waits behind bulk uploads queued on a copy
+    engine.  The pinned source is kept alive until an event recorded after the
+    copy has completed."""
+    src = torch.as_tensor(np.asarray(values), dtype=dtype).pin_memory()
+    out = torch.empty(tuple(src.shape), dtype=dtype, device=dev)
+    nbytes = src.numel() * src.element_size()
+    if nbytes:
+        _lib.check(_lib.lib().dp2_copy_h2d_small(C.c_void_p(out.data_ptr()), C.c_void_p(src.data_ptr()), nbytes,
+                                                  C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)),
+                   "copy_h2d_small")
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dev))
+        _SMALL_KEEP.append((src, ev))
+        if len(_SMALL_KEEP) > _SMALL_KEEP_MAX:
+            _SMALL_KEEP[:] = [(t, e) for t, e in _SMALL_KEEP if not e.query()]
+    return out

