@@ -140,6 +140,9 @@ int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, i
  * a NaN/Inf (status[0]); mirrors IrregularTensor's isfinite check
  * (P/tensor.py:61) and total_sq_norm (P/tensor.py:79-80). */
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream);
+/* 1 when the streaming sketch of this store at padded width sp runs on the
+ * tf32 tensor-core pass (fp32 storage, J <= 512, sp <= 32), else 0. */
+int dp2_sketch_uses_tc(const dp2_store* st, int32_t sp);
 /* The same isfinite check on HOST slices (ptrs[k]: rows[k] x J, row stride
  * ld[k] elements, dtype DP2_F32/DP2_F64), multithreaded (threads <= 0: all
  * hardware threads), so it runs while the upload of the same slices is in

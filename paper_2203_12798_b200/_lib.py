@@ -51,6 +51,7 @@ _SIGS = {
     "dp2_omega_replay": (c_i32, [c_vp, c_i64, P(c_f64), P(c_i32)]),
     "dp2_slice_stats": (c_i32, [P(Store), c_vp, c_vp, c_vp]),
     "dp2_copy_h2d_small": (c_i32, [c_vp, c_vp, c_sz, c_vp]),
+    "dp2_sketch_uses_tc": (c_i32, [P(Store), c_i32]),
     "dp2_host_first_nonfinite": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_i32, P(c_i64)]),
     "dp2_stream_pass": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "dp2_stage1_workspace": (c_sz, [P(Store), c_i32, c_i32]),

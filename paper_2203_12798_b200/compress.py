@@ -103,10 +103,12 @@ def check_rank(tensor: IrregularTensor, rank, slice_ids=None):
         raise RankTooLargeError(f"rank must be >= 1, got {rank}")
     if rank > tensor.num_cols:
         raise RankTooLargeError(f"rank {rank} exceeds column count {tensor.num_cols}")
-    ids = range(tensor.num_slices) if slice_ids is None else slice_ids
-    for k, rows in zip(ids, tensor.row_counts):
-        if rank > rows:
-            raise RankTooLargeError(f"rank {rank} exceeds row count {rows} of slice {k}")
+    rows = np.asarray(tensor.row_counts)
+    short = np.nonzero(rows < rank)[0]
+    if short.size:
+        k = int(short[0])
+        ids = range(tensor.num_slices) if slice_ids is None else slice_ids
+        raise RankTooLargeError(f"rank {rank} exceeds row count {int(rows[k])} of slice {list(ids)[k]}")
     if rank > 64:
         raise RankTooLargeError(f"rank {rank} exceeds the device limit of 64")
 
@@ -119,19 +121,43 @@ def stage2_params(base: RsvdParams, stage2, rank, K, J):
     return second, sketch_width(J, K * rank, rank, second.oversampling)
 
 
-def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, timings=None, status=None):
+def sketch_widths(row_counts, J, rank, oversampling):
+    """linalg.sketch_width for every slice at once (list of ints)."""
+    m = np.minimum(np.asarray(row_counts, dtype=np.int64), J)
+    if oversampling is None:
+        over = np.minimum(10, m - rank)
+    else:
+        over = np.full(m.shape, oversampling)
+    if (over < 0).any():
+        raise ValueError("oversampling must be >= 0")
+    return (rank + over).tolist()
+
+
+def _uses_tc(sub, sp):
+    st, keep = sub.store(nseg_for(sub))
+    return bool(_lib.lib().dp2_sketch_uses_tc(C.byref(st), sp))
+
+
+def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, timings=None, status=None,
+               speculative=False):
     """Stage 1 on the device for the tensor's slices (global ids ``slice_ids``
     select the per-slice seeds in a multi-GPU shard).  Returns A (sum I_k x R),
-    M (J x K_local R, local slice order) and the per-slice numerical ranks."""
+    M (J x K_local R, local slice order) and the per-slice numerical ranks
+    (plus, with ``speculative``, the Omega replay check future or None --
+    rng.omega_device)."""
     if base.power_iters != 1:
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
-    widths = [sketch_width(m, J, rank, base.oversampling) for m in tensor.row_counts]
+    widths = sketch_widths(tensor.row_counts, J, rank, base.oversampling)
     sp = padded_width(max(widths))
     dev = tensor.X.device
     t0 = time.perf_counter()
     rstats = {}
-    omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats)
+    check = None
+    if speculative and _uses_tc(tensor, sp):
+        omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True)
+    else:
+        omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats)
     from .tensor import to_device_async
     s_dev = to_device_async(widths, torch.int32, dev)
     t_omega = time.perf_counter() - t0
@@ -145,6 +171,8 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
                        stage1_sketch2_ms=tm[2], stage1_factor_ms=tm[3], stage1_signs_ms=tm[4],
                        stage1_ms=tm[5], sp=sp, nseg=nseg_for(tensor), npieces=int(tensor.store(nseg_for(tensor))[0].npieces))
+    if speculative:
+        return A, M, rank_found, status, check
     return A, M, rank_found, status
 
 
@@ -169,7 +197,7 @@ _ST_INDEX = (slice(0, 1), slice(2, 4))
 _ST_COUNT = (slice(1, 2), slice(4, 8))
 
 
-def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None):
+def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None, speculative=False):
     """Stage 1 overlapped with the tensor's chunked upload: Omega for all
     slices first (independent of X), then per upload chunk of whole slices the
     compute stream waits for that chunk's copy event (device-side) and runs
@@ -180,26 +208,34 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
     rows = tensor.row_counts
-    widths = [sketch_width(m, J, rank, base.oversampling) for m in rows]
+    widths = sketch_widths(rows, J, rank, base.oversampling)
     sp = padded_width(max(widths))
     dev = tensor.X.device
+    off = tensor.row_off_host
+    bounds = [k1 for k1, _ in tensor._upload_events]
+    subs, k0 = [], 0
+    for k1 in bounds:  # chunk views (host-side plans only; no device waits yet)
+        r0, r1 = int(off[k0]), int(off[k1])
+        subs.append((k0, k1, IrregularTensor.from_packed(tensor.X[r0:r1], rows[k0:k1], J, dtype=tensor.dtype,
+                                                         check=False)))
+        k0 = k1
     t0 = time.perf_counter()
     rstats = {}
-    omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
+    check = None
+    if speculative and _uses_tc(subs[0][2], sp):
+        omega, check = omega_device(base.seed, J, widths, sp, dev, speculative=True)
+    else:
+        omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
     from .tensor import to_device_async
     s_dev = to_device_async(widths, torch.int32, dev)
     t_omega = time.perf_counter() - t0
-    off = tensor.row_off_host
     A = torch.empty((int(off[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
     status = new_status(dev)
-    bounds = [k1 for k1, _ in tensor._upload_events]
-    k0 = 0
-    for k1 in bounds:
+    for k0, k1, sub in subs:
         tensor.wait_upload(k1)
         r0, r1 = int(off[k0]), int(off[k1])
-        sub = IrregularTensor.from_packed(tensor.X[r0:r1], rows[k0:k1], J, dtype=tensor.dtype, check=False)
         Mc = torch.empty((J, (k1 - k0) * rank), dtype=torch.float64, device=dev)
         st_c = new_status(dev)
         _stage1_call(sub, rank, omega[k0:k1], s_dev[k0:k1], sp, A[r0:r1], Mc, rank_found[k0:k1], st_c)
@@ -209,11 +245,12 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
             torch.minimum(status[sl], torch.where(idx == _lib.INT64_MAX, idx, idx + k0), out=status[sl])
         for sl in _ST_COUNT:
             status[sl] += st_c[sl]
-        k0 = k1
     tensor.wait_upload()
     if timings is not None:
         timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_chunks=len(bounds), sp=sp)
+    if speculative:
+        return A, M, rank_found, status, check
     return A, M, rank_found, status
 
 
@@ -246,11 +283,22 @@ def compress(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stag
     """Compress ``tensor`` at ``rank`` with two randomized-SVD stages."""
     comp, status = compress_async(tensor, rank, rsvd, stage2, plan, threads, timings)
     check_status(status, "compress")
+    if omega_mismatch(comp):
+        comp, status = compress_async(tensor, rank, rsvd, stage2, plan, threads, timings, exact_omega=True)
+        check_status(status, "compress")
     return comp
 
 
+def omega_mismatch(comp):
+    """True when the speculative (tensor-core path) Omega of ``comp`` turned
+    out to differ from the reference's (an acceptance decision of the
+    ziggurat tail, practically never): the caller recomputes exactly."""
+    chk = getattr(comp, "_omega_check", None)
+    return chk is not None and bool(chk.result()["omega_mismatch"])
+
+
 def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
-                   plan=None, threads=None, timings=None):
+                   plan=None, threads=None, timings=None, exact_omega=False):
     """``compress`` without the host synchronisation of its status check:
     returns (CompressedTensor, device status block); the caller checks the
     status (check_status) once its later work is enqueued."""
@@ -266,14 +314,19 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     om2_box = {}
     om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, K * rank, s2)))
     om2_thread.start()
+    spec = not exact_omega
     if len(tensor._upload_events) > 1:
-        A, M, rank_found, status = run_stage1_chunked(tensor, rank, base, timings=timings)
+        res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec)
     else:
-        A, M, rank_found, status = run_stage1(tensor, rank, base, timings=timings)
+        res = run_stage1(tensor, rank, base, timings=timings, speculative=spec)
+    A, M, rank_found, status = res[:4]
+    check = res[4] if len(res) > 4 else None
     om2_thread.join()
     D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2_box["v"], status, timings=timings)
-    return CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
-                            cores=F, rank_found=rank_found), status
+    comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
+                            cores=F, rank_found=rank_found)
+    comp._omega_check = check
+    return comp, status
 
 
 def reconstruct_slice(comp: CompressedTensor, k):

@@ -259,6 +259,11 @@ int dp2_host_first_nonfinite(const void* const* ptrs, const int64_t* rows, const
   return DP2_OK;
 }
 
+int dp2_sketch_uses_tc(const dp2_store* st, int32_t sp) {
+  if (!store_ok(st)) return 0;
+  return dp2::sketch_tc_eligible(st, sp) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------- device calls
 int dp2_slice_stats(const dp2_store* st, double* sqnorm_dev, int64_t* status_dev, void* stream) {
   if (!store_ok(st)) return fail_arg("invalid store");

@@ -59,8 +59,40 @@ _ZIG_R = 3.6541528853610087963519472518
 _ZIG_INV_R = 0.27366123732975827203338247596
 
 
-def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
-    """Device tensor (K, n, sp) of the reference's Omega_k (byte-exact)."""
+_REPLAY_POOL = None
+
+
+def _replay_check(ev, nrec_h, redo_h_t, recs_h, cap):
+    """Background half of a speculative omega_device: wait for the records,
+    replay them with libm's log1p and report whether any acceptance decision
+    (or a record overflow / device redo flag) differs from the reference's."""
+    import ctypes as C
+
+    from . import _lib
+    ev.synchronize()
+    count = int(nrec_h[0])
+    mismatch = count > cap or bool(redo_h_t.numpy().any())
+    if count and not mismatch:
+        r = recs_h[:count].numpy().view(_REC).reshape(-1)
+        vals = np.empty(r.size)
+        okv = np.empty(r.size, dtype=np.int32)
+        _lib.check(_lib.lib().dp2_omega_replay(C.c_void_p(r.ctypes.data), r.size,
+                                               vals.ctypes.data_as(C.POINTER(C.c_double)),
+                                               okv.ctypes.data_as(C.POINTER(C.c_int32))), "omega_replay")
+        mismatch = not bool(okv.all())
+    return {"omega_tail_events": count, "omega_mismatch": mismatch}
+
+
+def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, speculative=False):
+    """Device tensor (K, n, sp) of the reference's Omega_k (byte-exact).
+
+    ``speculative=True`` (for consumers that round Omega to tf32, the fp32
+    tensor-core sketch): no host synchronisation -- the device's own tail
+    values (its log1p may differ from libm's in the last bit, which tf32
+    rounding absorbs) are used as they are, and the libm replay runs on a
+    background thread; returns ``(omega, future)`` whose result reports
+    ``omega_mismatch`` (an acceptance decision differing from the reference's,
+    practically never: the caller then recomputes with the exact path)."""
     import ctypes as C
 
     from . import _lib
@@ -84,6 +116,16 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None):
     nrec_h.copy_(nrec, non_blocking=True)
     redo_h_t.copy_(redo, non_blocking=True)
     recs_h.copy_(recs, non_blocking=True)
+    if speculative:
+        global _REPLAY_POOL
+        if _REPLAY_POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _REPLAY_POOL = ThreadPoolExecutor(1)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        keep = (recs, nrec, redo)  # device buffers live until the copies ran
+        fut = _REPLAY_POOL.submit(lambda: (_replay_check(ev, nrec_h, redo_h_t, recs_h, cap), keep)[0])
+        return out, fut
     torch.cuda.current_stream().synchronize()
     count = int(nrec_h[0])
     redo_h = redo_h_t.numpy().copy()

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressedTensor, _vp, check_status, compress, compress_async, nseg_for, workspace
+from .compress import CompressedTensor, _vp, check_status, compress, compress_async, nseg_for, omega_mismatch, workspace
 from .factors import FitTrace, Parafac2Factors, SliceViews, SolverOptions, initial_factors, prefaulted_empty
 from .linalg import RsvdParams
 from .scheduler import resolve_threads
@@ -189,7 +189,8 @@ def assemble_q(tensor: IrregularTensor, comp: CompressedTensor, polar, nseg=None
     return Q
 
 
-def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", timings=None, use_graph=False):
+def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", timings=None, use_graph=False,
+              _exact_omega=False):
     """Compress once, then alternate rotations and factor sweeps in R x R space.
 
     Returns ``(factors, trace)`` like P/solver.py:152-190.  ``output="device"``
@@ -209,7 +210,8 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     ev1 = torch.cuda.Event(enable_timing=True)
     started = time.perf_counter()
     ev0.record()
-    comp, cstatus = compress_async(tensor, rank, rsvd=RsvdParams(rank=rank, seed=opts.seed), timings=timings)
+    comp, cstatus = compress_async(tensor, rank, rsvd=RsvdParams(rank=rank, seed=opts.seed), timings=timings,
+                                   exact_omega=_exact_omega)
     ev1.record()
     cstatus_h = torch.empty(tuple(cstatus.shape), dtype=cstatus.dtype, pin_memory=True)
     cstatus_h.copy_(cstatus, non_blocking=True)
@@ -225,6 +227,8 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     torch.cuda.current_stream().synchronize()
     tensor._upload_keep = None  # the stream waited for the whole upload before stage 1 finished
     check_status(cstatus_h, "compress")
+    if omega_mismatch(comp):  # speculative Omega differed from the reference's: redo exactly
+        return fit_dpar2(tensor, rank, opts, output, timings, use_graph, _exact_omega=True)
     H, V, W, polar, tr, secs = _als_collect(launched, synced=True)
     trace = FitTrace(preprocess_seconds=max(host_pre, ev0.elapsed_time(ev1) * 1e-3),
                      compressed_float_count=comp.float_count())

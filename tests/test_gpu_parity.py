@@ -270,3 +270,28 @@ def test_chunked_upload_overlap_matches_resident(monkeypatch):
     bad[17][3, 5] = np.inf
     with pytest.raises(dp.NonFiniteInputError, match="slice 17"):
         dp.IrregularTensor(bad)
+
+
+def test_speculative_omega_redo_path(monkeypatch):
+    """fp32 tensor-core path: Omega is used before the libm tail replay
+    finishes (rng.omega_device speculative); a reported mismatch makes
+    fit_dpar2 recompute with the exact, patched Omega -- the two agree."""
+    import importlib
+    import paper_2203_12798_b200 as dp
+    solver = importlib.import_module("paper_2203_12798_b200.solver")
+    rng = np.random.default_rng(5)
+    xs = [rng.standard_normal((int(m), 64)).astype(np.float32) for m in rng.integers(40, 120, size=9)]
+    t = dp.IrregularTensor(xs, dtype="f32")
+    f, tr = dp.fit_dpar2(t, 5, dp.SolverOptions(max_iters=5, tol=0.0))
+    calls = []
+    real = solver.omega_mismatch
+
+    def once(comp):
+        calls.append(getattr(comp, "_omega_check", None) is not None)
+        return len(calls) == 1 or real(comp)
+
+    monkeypatch.setattr(solver, "omega_mismatch", once)
+    g, tr2 = dp.fit_dpar2(t, 5, dp.SolverOptions(max_iters=5, tol=0.0))
+    assert calls == [True, False]  # speculative first, exact (no check) on the redo
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(g, key), getattr(f, key)) <= 1e-6, key
