@@ -292,7 +292,7 @@ int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_de
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
                                   static_cast<char*>(ws), status_dev, timing_ms, S(stream));
-  // + the B-image kernel of each tensor-core streaming pass and gram_y_kernel
+  // + the B-image kernel of each tensor-core streaming pass and gram_y_piece_kernel
   const int tc = dp2::sketch_tc_eligible(st, sp) ? 3 : 0;
   return e == cudaSuccess ? ok((sp <= 32 ? 9 : 8) + tc) : fail(e, "dp2_stage1");
 }

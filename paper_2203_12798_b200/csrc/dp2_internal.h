@@ -23,7 +23,7 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                             int64_t* status, int phase, cudaStream_t stream, bool y32 = false);
+                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch);
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                            double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
 bool sketch_tc_eligible(const dp2_store* st, int sp);

@@ -757,14 +757,14 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
     double* CCg = reinterpret_cast<double*>(ws + L.CCg);
     double* Gg = reinterpret_cast<double*>(ws + L.Gg);
     double* sgn = reinterpret_cast<double*>(ws + L.sgn);
-    // the tensor-core pass leaves G to gram_y_kernel (run_stage1_small)
+    // the tensor-core pass leaves G to gram_y_piece_kernel (run_stage1_small; partials into gpart)
     const bool tc = sketch_tc_eligible(st, sp);
     double* gp = tc ? nullptr : gpart;
     auto small = [&](int phase) {
       return run_stage1_small(st, s_dev, sp, R, part, part, gp, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
                               reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
-                              stream, tc);
+                              stream, tc, gpart);
     };
     if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) {
       e = small(0);

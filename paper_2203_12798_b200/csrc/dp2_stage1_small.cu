@@ -4,8 +4,9 @@
 // for the math; references P/linalg.py:124-131, P/compress.py:108).
 //
 //   orth_smem     Q_Z = CGS2(sum of pass-1 partials), slice matrix in smem
-//   gather        C^T = sum of pass-2 partials; CC = C C^T; G = sum of the
-//                 per-piece Y^T Y accumulated inside pass 2
+//   gram_y_piece  (tensor-core pass) per piece G partial = Y_p^T Y_p, DMMA
+//   gather_dmma   C = sum of pass-2 partials; CC = C^T C (DMMA); G = sum of
+//                 the per-piece Y^T Y partials
 //   factor_warp   one warp per slice: G = L L^T (Cholesky; Jacobi-eig fallback
 //                 for rank deficiency), B B^T = L^-1 CC L^-T, register Jacobi
 //                 eig -> P = L^-T U_R, S = sqrt(mu_R)
@@ -20,21 +21,10 @@
 namespace dp2 {
 
 // ------------------------------------------------------------ orth (smem CGS2)
-__global__ void __launch_bounds__(256) orth_smem_kernel(const double* part, const int32_t* slice_piece,
-                                                         const int32_t* s_k, int J, int sp, double* Q) {
-  extern __shared__ __align__(16) double qs[];  // J x ld, ld = sp + 1 (odd: conflict-free column walks)
-  __shared__ double h[32];
-  __shared__ double red[32];
-  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
-  const int s = s_k[k], ld = sp + 1;
-  const int n = J * sp;
-  for (int i = tid; i < n; i += nt) {
-    double acc = 0.0;
-    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
-    qs[(i / sp) * ld + i % sp] = acc;
-  }
-  __syncthreads();
+// CGS2 with re-randomisation of (numerically) dependent columns on the
+// columns c < s of the J x ld shared-memory block qs (whole CTA).
+DP2_DEV void cgs2_smem(double* qs, int J, int ld, int s, double* h, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int c = 0; c < s; ++c) {
     for (int attempt = 0;; ++attempt) {
       if (attempt > 0) {
@@ -69,105 +59,343 @@ __global__ void __launch_bounds__(256) orth_smem_kernel(const double* part, cons
       }
     }
   }
+}
+
+__global__ void __launch_bounds__(256) orth_smem_kernel(const double* part, const int32_t* slice_piece,
+                                                         const int32_t* s_k, int J, int sp, double* Q) {
+  extern __shared__ __align__(16) double qs[];  // J x ld, ld = sp + 1 (odd: conflict-free column walks)
+  __shared__ double h[32];
+  __shared__ double red[32];
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k], ld = sp + 1;
+  const int n = J * sp;
+  for (int i = tid; i < n; i += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
+    qs[(i / sp) * ld + i % sp] = acc;
+  }
+  __syncthreads();
+  cgs2_smem(qs, J, ld, s, h, red);
   double* Qk = Q + (size_t)k * n;
   for (int i = tid; i < n; i += nt) Qk[i] = qs[(i / sp) * ld + i % sp];
 }
 
-// ------------------------------------------------------------ gather
-__global__ void __launch_bounds__(256) gather_kernel(const double* part, const double* gpart,
-                                                      const int32_t* slice_piece, int J, int sp, double* Ct,
-                                                      double* CCg, double* Gg) {
-  extern __shared__ __align__(16) double cs_[];  // J x (sp + 1)
-  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
-  const int n = J * sp, ld = sp + 1;
-  double* C = Ct + (size_t)k * n;
-  for (int i = tid; i < n; i += nt) {
-    double acc = 0.0;
-    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
-    C[i] = acc;
-    cs_[(i / sp) * ld + i % sp] = acc;
-  }
-  if (gpart)  // else G comes from gram_y_kernel
-    for (int e = tid; e < sp * sp; e += nt) {
-      double acc = 0.0;
-      for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * sp * sp + e];
-      Gg[(size_t)k * sp * sp + e] = acc;
-    }
-  __syncthreads();
-  const int ntri = sp * (sp + 1) / 2;
-  for (int e = warp; e < ntri; e += nw) {
-    int a = 0, rem = e;
-    while (rem >= sp - a) { rem -= sp - a; ++a; }
-    const int b = a + rem;
-    double acc = 0.0;
-    for (int j = lane; j < J; j += 32) acc = fma(cs_[j * ld + a], cs_[j * ld + b], acc);
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      CCg[(size_t)k * sp * sp + a * sp + b] = acc;
-      CCg[(size_t)k * sp * sp + b * sp + a] = acc;
-    }
+// ------------------------------------------------------------ DMMA Gram tiles
+// Upper-triangular 8x8 blocks (bi <= bj) of T^T T for a 32-row tile T held in
+// warp-private shared memory (row stride LD): 8 k-steps of m8n8k4 per block.
+template <int SP>
+struct GramBlocks {
+  static constexpr int NB = SP / 8, NBLK = NB * (NB + 1) / 2;
+};
+
+template <int SP, typename T, int LD>
+DP2_DEV void gram_tile_dmma(const T* tile, double (&acc)[GramBlocks<SP>::NBLK][2]) {
+  constexpr int NB = SP / 8;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const T* tr = tile + (4 * kk + (lane & 3)) * LD + (lane >> 2);
+    double f[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) f[b] = (double)tr[8 * b];
+    int blk = 0;
+#pragma unroll
+    for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+      for (int bj = bi; bj < NB; ++bj, ++blk) dmma_8x8x4(acc[blk][0], acc[blk][1], f[bi], f[bj]);
   }
 }
 
-// ------------------------------------------------------------ G from Y rows
-// G_k = Y_k^T Y_k (sp x sp, fp64) for slice k from its pass-2 rows y2[row_off[k]
-// .. row_off[k+1]) -- used when the streaming pass does not accumulate G
-// (tensor-core pass: fp64 DMMA inside it would share the tensor pipe with the
-// tcgen05 products).  64-row tiles staged in smem, 8x8 blocks of G on fp64
-// DMMA m8n8k4, one CTA (8 warps) per slice.
-template <typename Y>  // Y rows stored as fp64, or as fp32 by the tensor-core pass
-__global__ void __launch_bounds__(256) gram_y_kernel(const Y* y2, const int64_t* row_off, int sp, double* Gg) {
-  constexpr int TR = 64, LD = sizeof(Y) == 8 ? 34 : 36;  // row stride (elements): 16 B aligned, conflict-light
-  __shared__ __align__(16) Y ys[2][TR * LD];
-  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r0 = row_off[k], r1 = row_off[k + 1];
-  constexpr int EPC = 16 / (int)sizeof(Y);  // elements per 16 B chunk
-  const int nb = sp / 8, c16 = sp / EPC;     // 16 B chunks per row
-  const int ntile = (int)((r1 - r0 + TR - 1) / TR);
-  auto issue = [&](int t, int buf) {
-    const int64_t base = r0 + (int64_t)t * TR;
-    const int rows = (int)min((int64_t)TR, r1 - base);
-    for (int e = tid; e < TR * c16; e += 256) {
-      const int r = e / c16, c = e - r * c16;
-      Y* dst = &ys[buf][r * LD + EPC * c];
-      if (r < rows) cp_async16(dst, y2 + (base + r) * sp + EPC * c, 16);
-      else cp_async16(dst, y2, 0);  // zero fill
-    }
-  };
-  double acc[4][2] = {};
-  if (ntile > 0) issue(0, 0);
-  cp_async_commit();
-  for (int t = 0; t < ntile; ++t) {
-    if (t + 1 < ntile) issue(t + 1, (t + 1) & 1);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const Y* yt = ys[t & 1];
+// Block partials of every warp -> full symmetric SP x SP matrix (warp order)
+template <int SP>
+DP2_DEV void gram_store(double (&acc)[GramBlocks<SP>::NBLK][2], double* wpart, double* out) {
+  constexpr int NB = SP / 8, NBLK = GramBlocks<SP>::NBLK;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const int blk = warp + 8 * s;
-      if (blk < nb * nb) {
-        const int bi = blk / nb, bj = blk - bi * nb;
-#pragma unroll 4
-        for (int kk = 0; kk < TR / 4; ++kk) {
-          const Y* yr = yt + (4 * kk + (lane & 3)) * LD;
-          dmma_8x8x4(acc[s][0], acc[s][1], (double)yr[8 * bi + (lane >> 2)], (double)yr[8 * bj + (lane >> 2)]);
-        }
+  for (int blk = 0; blk < NBLK; ++blk) {
+    wpart[(warp * NBLK + blk) * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[blk][0];
+    wpart[(warp * NBLK + blk) * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[blk][1];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < SP * SP; e += blockDim.x) {
+    int a = e / SP, b = e - a * SP;
+    if (a / 8 > b / 8) { const int t = a; a = b; b = t; }
+    const int bi = a / 8, bj = b / 8;
+    const int blk = bi * NB - bi * (bi - 1) / 2 + (bj - bi);
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += wpart[(w * NBLK + blk) * 64 + (a % 8) * 8 + (b % 8)];
+    out[e] = v;
+  }
+}
+
+// G partial of one piece from its pass-2 Y rows (tensor-core pass: Y fp32):
+// each warp streams 32-row tiles through its own shared-memory slab (16 B
+// loads) and accumulates the Gram blocks on fp64 DMMA.
+template <typename Y, int SP>
+__global__ void __launch_bounds__(256) gram_y_piece_kernel(const Y* y2, const int64_t* piece_row0,
+                                                           const int32_t* piece_rows, double* gpart) {
+  constexpr int EPC = 16 / (int)sizeof(Y), LD = SP + EPC, NBLK = GramBlocks<SP>::NBLK;
+  extern __shared__ __align__(16) double sm[];
+  const int p = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Y* tile = reinterpret_cast<Y*>(sm) + warp * 32 * LD;
+  double* wpart = sm + (8 * 32 * LD * sizeof(Y)) / 8;
+  const int64_t r0 = piece_row0[p];
+  const int nr = piece_rows[p];
+  double acc[NBLK][2];
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+  for (int t = warp * 32; t < nr; t += 256) {
+    const int rows = min(32, nr - t);
+    constexpr int NQ = SP / EPC;  // 16 B chunks per row; lane q-th chunk of the tile: all loads first
+    float4 v[NQ];
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int q = lane + 32 * u, r = q / NQ, c = q - r * NQ;
+      v[u] = r < rows ? __ldg(reinterpret_cast<const float4*>(y2 + (r0 + t + r) * SP + EPC * c))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      const int q = lane + 32 * u, r = q / NQ, c = q - r * NQ;
+      *reinterpret_cast<float4*>(tile + r * LD + EPC * c) = v[u];
+    }
+    __syncwarp();
+    gram_tile_dmma<SP, Y, LD>(tile, acc);
+    __syncwarp();
+  }
+  gram_store<SP>(acc, wpart, gpart + (size_t)p * SP * SP);
+}
+
+// Per slice: C = sum of the pass-2 partials (J x SP, written out), CC = C^T C
+// on DMMA over warp-private 32-row tiles, G = sum of the per-piece Gram
+// partials.
+template <int SP>
+__global__ void __launch_bounds__(256) gather_dmma_kernel(const double* part, const double* gpart,
+                                                          const int32_t* slice_piece, int J, double* Ct,
+                                                          double* CCg, double* Gg) {
+  constexpr int LD = SP + 2, NBLK = GramBlocks<SP>::NBLK;
+  extern __shared__ __align__(16) double sm[];
+  const int k = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* tile = sm + warp * 32 * LD;
+  double* wpart = sm + 8 * 32 * LD;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const size_t n = (size_t)J * SP;
+  for (int e = threadIdx.x; e < SP * SP; e += blockDim.x) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * SP * SP + e];
+    Gg[(size_t)k * SP * SP + e] = acc;
+  }
+  double acc[NBLK][2];
+#pragma unroll
+  for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+  double* C = Ct + (size_t)k * n;
+  for (int t = warp * 32; t < J; t += 256) {
+    const int rows = min(32, J - t);
+    double v[SP];  // lane's SP entries of the tile (q = lane + 32 u): all loads issued before any store
+#pragma unroll
+    for (int u = 0; u < SP; ++u) v[u] = 0.0;
+    for (int p = p0; p < p1; ++p) {
+      const double* src = part + (size_t)p * n + (size_t)t * SP;
+#pragma unroll
+      for (int u = 0; u < SP; ++u) {
+        const int q = lane + 32 * u;
+        if (q / SP < rows) v[u] += __ldg(src + q);
       }
     }
-    __syncthreads();
-  }
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int blk = warp + 8 * s;
-    if (blk < nb * nb) {
-      const int bi = blk / nb, bj = blk - bi * nb;
-      double* g = Gg + (size_t)k * sp * sp + (size_t)(8 * bi + (lane >> 2)) * sp + 8 * bj + 2 * (lane & 3);
-      g[0] = acc[s][0];
-      g[1] = acc[s][1];
+    for (int u = 0; u < SP; ++u) {
+      const int q = lane + 32 * u, r = q / SP, c = q - r * SP;
+      if (r < rows) C[(size_t)t * SP + q] = v[u];
+      tile[r * LD + c] = v[u];
+    }
+    __syncwarp();
+    gram_tile_dmma<SP, double, LD>(tile, acc);
+    __syncwarp();
+  }
+  gram_store<SP>(acc, wpart, CCg + (size_t)k * SP * SP);
+}
+
+// ------------------------------------------------------------ orth (CholQR2)
+// Cholesky of the s x s Gram G (shared, row stride ldg) by one warp into L
+// (lower, row-major, stride SP) and 1/diag; false when a pivot falls to
+// rel_floor * max diag(G) (the caller then falls back to CGS2).
+DP2_DEV bool chol_warp_smem(const double* G, int ldg, double* L, int ldl, double* dinv, int s, double rel_floor) {
+  const int lane = threadIdx.x & 31;
+  double gmax = 0.0;
+  for (int i = 0; i < s; ++i) gmax = fmax(gmax, G[i * ldg + i]);
+  if (!(gmax > 0.0)) return false;
+  for (int c = 0; c < s; ++c) {
+    double d = 0.0;
+    if (lane == 0) {
+      d = G[c * ldg + c];
+      for (int m = 0; m < c; ++m) d = fma(-L[c * ldl + m], L[c * ldl + m], d);
+    }
+    d = __shfl_sync(0xffffffffu, d, 0);
+    if (!(d > rel_floor * gmax)) return false;
+    const double l = sqrt(d), il = 1.0 / l;
+    for (int i = c + 1 + lane; i < s; i += 32) {
+      double t = G[i * ldg + c];
+      for (int m = 0; m < c; ++m) t = fma(-L[i * ldl + m], L[c * ldl + m], t);
+      L[i * ldl + c] = t * il;
+    }
+    if (lane == 0) {
+      L[c * ldl + c] = l;
+      dinv[c] = il;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// Register Cholesky of the s x s SPD matrix G (s <= SP <= 32), one warp:
+// lane j holds column j; step k broadcasts the scaled pivot column by
+// shuffles (entries below the diagonal only) and every lane updates its own
+// column.  Writes L (lower, row-major) and 1/diag; false when a pivot falls to
+// rel_floor * max diag(G).
+template <int SP>
+DP2_DEV bool chol_reg(const double* G, int ldg, double* L, int ldl, double* dinv, int s, double rel_floor) {
+  const int lane = threadIdx.x & 31;
+  double g[SP];
+#pragma unroll
+  for (int i = 0; i < SP; ++i) g[i] = (lane < s && i < s) ? G[i * ldg + lane] : 0.0;
+  double dg = 0.0;
+#pragma unroll
+  for (int i = 0; i < SP; ++i) dg = (i == lane) ? g[i] : dg;
+  double gmax = dg;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+  if (!(gmax > 0.0)) return false;
+#pragma unroll
+  for (int k = 0; k < SP; ++k) {
+    if (k >= s) break;
+    const double d = __shfl_sync(0xffffffffu, g[k], k);
+    if (!(d > rel_floor * gmax)) return false;
+    const double l = sqrt(d), il = 1.0 / l;
+    double lk[SP];
+#pragma unroll
+    for (int i = k + 1; i < SP; ++i) lk[i] = __shfl_sync(0xffffffffu, g[i], k) * il;
+    double ljk = 0.0;
+#pragma unroll
+    for (int i = k + 1; i < SP; ++i) ljk = (i == lane) ? lk[i] : ljk;
+    if (lane > k && lane < s) {
+#pragma unroll
+      for (int i = k + 1; i < SP; ++i) g[i] = fma(-lk[i], ljk, g[i]);
+    }
+    if (lane == k) {
+      L[k * ldl + k] = l;
+      dinv[k] = il;
+#pragma unroll
+      for (int i = k + 1; i < SP; ++i)
+        if (i < s) L[i * ldl + k] = lk[i];
     }
   }
+  __syncwarp();
+  return true;
+}
+
+// Q_Z = orth(Z), Z = sum of the slice's pass-1 partials (P/linalg.py:124-126):
+// CholQR -- G = Z^T Z on DMMA over the shared-memory slab, G = L L^T,
+// Z <- Z L^-T (row-wise substitution in registers); in exact arithmetic the
+// Gram-Schmidt / positive-diagonal-QR Q.  One pass suffices here: Q_Z only
+// seeds the second streaming pass, and everything downstream depends on
+// span(Q_Z) alone, which a nonsingular right factor preserves up to the
+// product's rounding; with the pivot guard below, kappa(Q_Z) <= 1 + ~1e-4.  A
+// pivot below 1e-12 of the largest (kappa(Z) beyond ~1e6, or a dependent
+// column) sends the slice to CGS2 with re-randomisation (cgs2_smem).
+template <int SP>
+__global__ void __launch_bounds__(256) orth_cholqr_kernel(const double* part, const int32_t* slice_piece,
+                                                          const int32_t* s_k, int J, double* Q) {
+  constexpr int LD = SP + 1, NBLK = GramBlocks<SP>::NBLK;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double h[32];
+  __shared__ double red[32];
+  __shared__ int ok_s;
+  const int JP = (J + 31) & ~31;
+  double* Z = sm;                          // JP x LD
+  double* wpart = Z + (size_t)JP * LD;     // 8 x NBLK x 64
+  double* G = wpart + 8 * NBLK * 64;       // SP x SP
+  double* L = G + SP * SP;                 // SP x SP (lower)
+  double* dinv = L + SP * SP;              // SP
+  const int k = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k];
+  const size_t n = (size_t)J * SP;
+  // Z = sum of partials: 8 independent loads per thread in flight per piece
+  for (int i0 = tid; i0 < JP * SP; i0 += 256 * 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = 0.0;
+    for (int p = p0; p < p1; ++p) {
+      const double* src = part + (size_t)p * n;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + 256 * u;
+        if (i < J * SP) v[u] += __ldg(src + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + 256 * u;
+      if (i < JP * SP) Z[(i / SP) * LD + i % SP] = v[u];
+    }
+  }
+  __syncthreads();
+  bool chol = true;
+  for (int pass = 0; pass < 1; ++pass) {
+    double acc[NBLK][2];
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int t = warp * 32; t < JP; t += 256) gram_tile_dmma<SP, double, LD>(Z + t * LD, acc);
+    gram_store<SP>(acc, wpart, G);
+    __syncthreads();
+    if (warp == 0) {
+      const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, 1e-12);
+      if (tid == 0) ok_s = okk;
+    }
+    __syncthreads();
+    chol = ok_s != 0;
+    if (!chol) break;
+    for (int r = tid; r < J; r += 256) {  // row r of Z L^-T: L q^T = z^T
+      double q[SP];
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        if (i < s) {
+          double t = Z[r * LD + i];
+#pragma unroll
+          for (int m = 0; m < i; ++m) t = fma(-L[i * SP + m], q[m], t);
+          q[i] = t * dinv[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < SP; ++i)
+        if (i < s) Z[r * LD + i] = q[i];
+    }
+    __syncthreads();
+  }
+  if (!chol) {  // reload Z, then CGS2
+    for (int i = tid; i < J * SP; i += 256) {
+      double v = 0.0;
+      for (int p = p0; p < p1; ++p) v += part[(size_t)p * n + i];
+      Z[(i / SP) * LD + i % SP] = v;
+    }
+    __syncthreads();
+    cgs2_smem(Z, J, LD, s, h, red);
+  }
+  double* Qk = Q + (size_t)k * n;
+  for (int i = tid; i < J * SP; i += 256) Qk[i] = Z[(i / SP) * LD + i % SP];
+}
+
+template <int SP>
+cudaError_t orth_t(const dp2_store* st, const int32_t* s_dev, const double* part1, double* qz, cudaStream_t stream) {
+  constexpr int NBLK = GramBlocks<SP>::NBLK;
+  const int K = (int)st->K, J = (int)st->J, JP = (J + 31) & ~31;
+  const size_t bytes = ((size_t)JP * (SP + 1) + 8 * NBLK * 64 + 2 * SP * SP + SP) * 8;
+  if (bytes > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(orth_cholqr_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  orth_cholqr_kernel<SP><<<K, 256, bytes, stream>>>(part1, st->slice_piece, s_dev, J, qz);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ factor (warp / slice)
@@ -577,14 +805,27 @@ size_t small_factor_smem(int sp) { return (4 * (size_t)sp * (sp + 1) + 4 * (size
 
 // factor -> argmax candidates -> signs + M -> signed A, for padded width SP
 template <int SP>
-cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const double* Gg, const double* CCg,
-                   const double* Ct, const double* y2, bool y32, double* Pm, double* Sv, double* sgn,
-                   double* cand_abs, int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                   int64_t* status, cudaStream_t stream) {
+cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const double* part2, const double* gpart,
+                   double* gscratch, double* Gg, double* CCg, double* Ct, const double* y2, bool y32, double* Pm,
+                   double* Sv, double* sgn, double* cand_abs, int64_t* cand_row, int32_t* cand_neg, double* A,
+                   double* M, int32_t* rank_out, int64_t* status, cudaStream_t stream) {
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
+  cudaError_t e = cudaSuccess;
+  if (!gpart) {  // tensor-core pass: G partials per piece from its fp32 Y rows
+    const size_t gs = (size_t)8 * 32 * (SP + 4) * 4 + (size_t)8 * GramBlocks<SP>::NBLK * 64 * 8;
+    e = cudaFuncSetAttribute(gram_y_piece_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs);
+    if (e != cudaSuccess) return e;
+    gram_y_piece_kernel<float, SP><<<P, 256, gs, stream>>>(reinterpret_cast<const float*>(y2), st->piece_row0,
+                                                           st->piece_rows, gscratch);
+    gpart = gscratch;
+  }
+  const size_t gb = ((size_t)8 * 32 * (SP + 2) + (size_t)8 * GramBlocks<SP>::NBLK * 64) * 8;
+  e = cudaFuncSetAttribute(gather_dmma_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+  if (e != cudaSuccess) return e;
+  gather_dmma_kernel<SP><<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, Ct, CCg, Gg);
   const int wpb = SP <= 24 ? 4 : 2;
   const size_t fs = wpb * small_factor_smem(SP);
-  cudaError_t e = cudaFuncSetAttribute(factor_warp_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
+  e = cudaFuncSetAttribute(factor_warp_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
   if (e != cudaSuccess) return e;
   factor_warp_kernel<SP><<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, SP, R, Pm, Sv, rank_out,
                                                                           status);
@@ -621,30 +862,31 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                             int64_t* status, int phase, cudaStream_t stream, bool y32) {
+                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch) {
   const int K = (int)st->K, J = (int)st->J;
-  const float* y2f = reinterpret_cast<const float*>(y2);
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
+    cudaError_t eo = cudaErrorInvalidValue;
+    switch (sp) {
+      case 8: eo = orth_t<8>(st, s_dev, part1, qz, stream); break;
+      case 16: eo = orth_t<16>(st, s_dev, part1, qz, stream); break;
+      case 24: eo = orth_t<24>(st, s_dev, part1, qz, stream); break;
+      case 32: eo = orth_t<32>(st, s_dev, part1, qz, stream); break;
+      default: break;
+    }
+    if (eo == cudaSuccess) return eo;
+    (void)cudaGetLastError();  // slab does not fit: shared-memory CGS2
     const size_t qb = (size_t)J * (sp + 1) * 8;
     e = cudaFuncSetAttribute(orth_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb);
     if (e != cudaSuccess) return e;
     orth_smem_kernel<<<K, 256, qb, stream>>>(part1, st->slice_piece, s_dev, J, sp, qz);
     return cudaGetLastError();
   }
-  const size_t gb = (size_t)J * (sp + 1) * 8;
-  e = cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
-  if (e != cudaSuccess) return e;
-  gather_kernel<<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, sp, Ct, CCg, Gg);
-  if (!gpart) {
-    if (y32) gram_y_kernel<float><<<K, 256, 0, stream>>>(y2f, st->row_off, sp, Gg);
-    else gram_y_kernel<double><<<K, 256, 0, stream>>>(y2, st->row_off, sp, Gg);
-  }
   switch (sp) {
-    case 8: return post_t<8>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 16: return post_t<16>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 24: return post_t<24>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 32: return post_t<32>(st, s_dev, R, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 8: return post_t<8>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 16: return post_t<16>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 24: return post_t<24>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 32: return post_t<32>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
     default: return cudaErrorInvalidValue;
   }
 }
