@@ -8,7 +8,6 @@ accepted (they never change values in the reference either).
 from __future__ import annotations
 
 import ctypes as C
-import threading
 import time
 from dataclasses import dataclass, replace
 
@@ -133,6 +132,20 @@ def sketch_widths(row_counts, J, rank, oversampling):
     return (rank + over).tolist()
 
 
+def _stage1_setup(tensor, rank, oversampling, dev):
+    """(widths, sp, device widths) for ``tensor`` at ``rank`` -- cached on the
+    tensor (its row counts are immutable), so repeated fits skip the host work
+    before the first launch."""
+    cache = tensor.__dict__.setdefault("_s1_setup", {})
+    key = (rank, oversampling)
+    if key not in cache:
+        from .tensor import to_device_async
+        widths = sketch_widths(tensor.row_counts, tensor.num_cols, rank, oversampling)
+        sp = padded_width(max(widths))
+        cache[key] = (widths, sp, to_device_async(widths, torch.int32, dev))
+    return cache[key]
+
+
 def _uses_tc(sub, sp):
     st, keep = sub.store(nseg_for(sub))
     return bool(_lib.lib().dp2_sketch_uses_tc(C.byref(st), sp))
@@ -148,18 +161,16 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     if base.power_iters != 1:
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
-    widths = sketch_widths(tensor.row_counts, J, rank, base.oversampling)
-    sp = padded_width(max(widths))
     dev = tensor.X.device
+    widths, sp, s_dev = _stage1_setup(tensor, rank, base.oversampling, dev)
     t0 = time.perf_counter()
     rstats = {}
     check = None
     if speculative and _uses_tc(tensor, sp):
-        omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True)
+        omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True,
+                                    s_dev=s_dev)
     else:
-        omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats)
-    from .tensor import to_device_async
-    s_dev = to_device_async(widths, torch.int32, dev)
+        omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats, s_dev=s_dev)
     t_omega = time.perf_counter() - t0
     A = torch.empty((int(tensor.row_off_host[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
@@ -208,9 +219,8 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
     rows = tensor.row_counts
-    widths = sketch_widths(rows, J, rank, base.oversampling)
-    sp = padded_width(max(widths))
     dev = tensor.X.device
+    widths, sp, s_dev = _stage1_setup(tensor, rank, base.oversampling, dev)
     off = tensor.row_off_host
     bounds = [k1 for k1, _ in tensor._upload_events]
     subs, k0 = [], 0
@@ -223,11 +233,9 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
     rstats = {}
     check = None
     if speculative and _uses_tc(subs[0][2], sp):
-        omega, check = omega_device(base.seed, J, widths, sp, dev, speculative=True)
+        omega, check = omega_device(base.seed, J, widths, sp, dev, speculative=True, s_dev=s_dev)
     else:
-        omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats)
-    from .tensor import to_device_async
-    s_dev = to_device_async(widths, torch.int32, dev)
+        omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats, s_dev=s_dev)
     t_omega = time.perf_counter() - t0
     A = torch.empty((int(off[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
@@ -304,16 +312,14 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     status (check_status) once its later work is enqueued."""
     if not isinstance(tensor, IrregularTensor):
         tensor = IrregularTensor(tensor)
-    check_rank(tensor, rank)
+    checked = tensor.__dict__.setdefault("_rank_ok", set())
+    if rank not in checked:
+        check_rank(tensor, rank)
+        checked.add(rank)
     resolve_threads(threads)
     base = rsvd if rsvd is not None else RsvdParams(rank=rank)
     J, K = tensor.num_cols, tensor.num_slices
     second, s2 = stage2_params(base, stage2, rank, K, J)
-    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on a host
-    # thread while the device generates the stage-1 sketches and runs stage 1
-    om2_box = {}
-    om2_thread = threading.Thread(target=lambda: om2_box.update(v=stage2_omega(second.seed, K * rank, s2)))
-    om2_thread.start()
     spec = not exact_omega
     if len(tensor._upload_events) > 1:
         res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec)
@@ -321,8 +327,10 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
         res = run_stage1(tensor, rank, base, timings=timings, speculative=spec)
     A, M, rank_found, status = res[:4]
     check = res[4] if len(res) > 4 else None
-    om2_thread.join()
-    D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2_box["v"], status, timings=timings)
+    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on the
+    # host once stage 1 is enqueued -- the device is busy with it meanwhile
+    om2 = stage2_omega(second.seed, K * rank, s2)
+    D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2, status, timings=timings)
     comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
                             cores=F, rank_found=rank_found)
     comp._omega_check = check

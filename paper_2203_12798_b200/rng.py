@@ -83,7 +83,7 @@ def _replay_check(ev, nrec_h, redo_h_t, recs_h, cap):
     return {"omega_tail_events": count, "omega_mismatch": mismatch}
 
 
-def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, speculative=False):
+def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, speculative=False, s_dev=None):
     """Device tensor (K, n, sp) of the reference's Omega_k (byte-exact).
 
     ``speculative=True`` (for consumers that round Omega to tf32, the fp32
@@ -99,7 +99,8 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     K = len(widths)
     out = torch.empty((K, n, sp), dtype=torch.float64, device=device)
     from .tensor import to_device_async
-    s_dev = to_device_async(list(widths), torch.int32, device)
+    if s_dev is None:
+        s_dev = to_device_async(list(widths), torch.int32, device)
     ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
     cap = max(4096, 8 * K + n * max(widths) * K // 1000)
     recs = torch.empty((cap, _REC.itemsize), dtype=torch.uint8, device=device)
