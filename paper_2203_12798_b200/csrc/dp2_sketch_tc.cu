@@ -368,10 +368,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     }
     if (lane == 0) {
       Unit cur = first_unit(pbeg);
-      uint32_t ucount = 0;
+      int ss = 0;          // ring slot = ucount % nss, fill = ucount / nss (tracked incrementally)
+      uint32_t fill = 0;
       while (cur.p < pend) {
-        const int ss = (int)(ucount % (uint32_t)nss);
-        const uint32_t fill = ucount / (uint32_t)nss;
         if (fill > 0) TWAIT(bar(BAR_RING + nss + ss), (fill - 1) & 1u, 0);
         mbar_expect_tx(bar(BAR_RING + ss), 4 * CHUNK);
         const int row = (int)(cur.row0 + (int64_t)cur.t * TM);
@@ -379,7 +378,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         for (int ch = 0; ch < 4; ++ch)
           tma_load_2d(ring + (uint32_t)(ss * 4 + ch) * CHUNK, &xmap, cur.jb * 128 + ch * 32, row,
                       bar(BAR_RING + ss));
-        ++ucount;
+        if (++ss == nss) { ss = 0; ++fill; }
         cur = next_unit(cur);
       }
     }
@@ -397,11 +396,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     double sq = 0.0;
     int bad = 0;
     Unit cur = first_unit(pbeg);
-    uint32_t ucount = 0, tcount = 0;
+    uint32_t tcount = 0, rph = 0;  // ring slot ss = ucount % nss with parity rph = (ucount / nss) & 1
+    int ss = 0;
     while (cur.p < pend) {
-      const int ss = (int)(ucount % (uint32_t)nss);
-      if (tid == 0) TWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 2);
-      else mbar_wait(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u);
+      if (tid == 0) TWAIT(bar(BAR_RING + ss), rph, 2);
+      else mbar_wait(bar(BAR_RING + ss), rph);
       const unsigned char* srcb = gbase + (size_t)(ss * 4 + q) * CHUNK;
       float v[32];
 #pragma unroll
@@ -437,7 +436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32 * h), v);
       tc_before();
       warp_arrive(bar(BAR_XT + 2 * cur.jb));
-      ++ucount;
+      if (++ss == nss) { ss = 0; rph ^= 1u; }
       const Unit nx = next_unit(cur);
       if (nx.jb == 0) ++tcount;
       if (nx.p != cur.p && stats) {  // piece complete: sum of squares, non-finite flag
@@ -477,8 +476,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     const uint32_t lbo = 1u << 16;
     const uint32_t ring_lo = (ring >> 4) | lbo, b_lo = (bsm >> 4) | lbo, y_lo = (ysm >> 4) | lbo;
     const uint32_t bch = (uint32_t)sp * 8;  // one 32-column chunk of B^T, in 16 B units
-    uint32_t ucount = 0, tcount = 0;
-    int pidx = 0;
+    uint32_t tcount = 0, rph = 0;
+    int ss = 0, pidx = 0;
 #define MWAIT(barexpr, par, k)        \
   do {                                \
     if (lane == 0)                    \
@@ -496,9 +495,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
           const uint32_t b = tcount & 1u;
           if (tcount >= 2) MWAIT(bar(BAR_YFREE + b), ((tcount >> 1) - 1) & 1u, 13);
           tc_after();
-          for (int jb = 0; jb < nsup; ++jb, ++ucount) {
-            const int ss = (int)(ucount % (uint32_t)nss);
-            MWAIT(bar(BAR_RING + ss), (ucount / (uint32_t)nss) & 1u, 5);
+          for (int jb = 0; jb < nsup; ++jb) {
+            MWAIT(bar(BAR_RING + ss), rph, 5);
             tc_after();
             const uint32_t a0 = ring_lo + (uint32_t)ss * (4 * CHUNK / 16);
             const uint32_t b0 = b_lo + (uint32_t)jb * 4 * bch;
@@ -511,6 +509,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
                             id1, (jb | ch | kk) != 0);
             tc_commit_e(bar(BAR_RING + nss + ss));
             if (prm.dbg && lane == 0) dacc[11] += gtime() - tp1;
+            if (++ss == nss) { ss = 0; rph ^= 1u; }
           }
           if (t == ntiles - 1) tc_commit_e(bar(BAR_BFREE));
           tc_commit_e(bar(BAR_YFULL + b));

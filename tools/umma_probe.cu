@@ -36,6 +36,11 @@ __device__ uint32_t a_off(int cs, int m, int k) {
       return (m / 4) * 128 + (k % 8) * 16 + (m % 4) * 4;
     case 5:  // MN-major BASE32B, same bytes as 1, LBO/SBO swapped in the descriptor
       return (m / 32) * 1024 + (k / 4) * 512 + (k % 4) * 128 + ((((m % 32) / 8) ^ (k % 4)) << 5) + (m % 8) * 4;
+    case 6:  // K-major SWIZZLE_128B_BASE32B: 128 B rows of k, 32 B granule ^ m%4 (SBO 512)
+    case 7:  // same bytes, SBO 1024
+      return m * 128 + ((((k % 32) / 8) ^ (m % 4)) << 5) + (k % 8) * 4;
+    case 8:  // K-major BASE32B, the K=8 slice at k = 8..15 of the row (descriptor start + 32 B)
+      return m * 128 + ((((k + 8) / 8) ^ (m % 4)) << 5) + (k % 8) * 4;
     default:
       return 0;
   }
@@ -81,7 +86,10 @@ __global__ void probe(int cs, const float* A, const float* B, float* D) {
       case 2: ad = sdesc(su32(As), 4096, 128, 0); break;  // LBO: k-core stride (unused, K=8), SBO: m-core stride
       case 3: ad = sdesc(su32(As), 128, 256, 0); amn = 0; break;  // LBO: k-core stride, SBO: m-core stride
       case 4: ad = sdesc(su32(As), 128, 4096, 0); break;  // swapped
-      default: ad = sdesc(su32(As), 512, 1024, 1); break;  // swapped
+      case 5: ad = sdesc(su32(As), 512, 1024, 1); break;  // swapped
+      case 6: ad = sdesc(su32(As), 16, 512, 1); amn = 0; break;
+      case 7: ad = sdesc(su32(As), 16, 1024, 1); amn = 0; break;
+      default: ad = sdesc(su32(As) + 32, 16, 512, 1); amn = 0; break;
     }
     const uint64_t bd = sdesc(su32(Bs), 16, 1024, 2);
     const uint32_t id = idesc_tf32(128, 32, amn, 0);
@@ -132,9 +140,10 @@ int main(int argc, char** argv) {
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   const char* names[] = {"MN-major SW128", "MN-major SW128_BASE32B", "MN-major INTERLEAVE (LBO=k,SBO=m)",
                          "K-major INTERLEAVE", "MN-major INTERLEAVE (LBO=m,SBO=k)",
-                         "MN-major BASE32B (LBO=512,SBO=1024)"};
+                         "MN-major BASE32B (LBO=512,SBO=1024)", "K-major BASE32B (SBO=512)",
+                         "K-major BASE32B (SBO=1024)", "K-major BASE32B k=8..15 (+32 B)"};
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
-  for (int cs = 0; cs < 6; ++cs) {
+  for (int cs = 0; cs < 9; ++cs) {
     if (only >= 0 && cs != only) continue;
     cudaMemset(dD, 0, D.size() * 4);
     probe<<<1, 128, 32768>>>(cs, dA, dB, dD);
