@@ -77,6 +77,36 @@ __global__ void __launch_bounds__(256) assemble_q_kernel(const double* A, const 
   }
 }
 
+// Q rows = A rows Pi_k for R known at compile time: one thread per row, the
+// row of A in registers, Pi_k in shared memory (broadcast reads), the same
+// fma order as assemble_q_kernel (so results are bit-identical to it).
+template <int R>
+__global__ void __launch_bounds__(256) assemble_q_rows_kernel(const double* A, const int32_t* piece_slice,
+                                                              const int64_t* piece_row0, const int32_t* piece_rows,
+                                                              const double* polar, double* Q) {
+  __shared__ double pis[R * R];
+  const int p = blockIdx.x;
+  const int64_t k = piece_slice[p];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) pis[e] = polar[k * R * R + e];
+  __syncthreads();
+  const int64_t r0 = piece_row0[p];
+  const int nr = piece_rows[p];
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+    const double* a = A + (r0 + i) * R;
+    double x[R];
+#pragma unroll
+    for (int d = 0; d < R; ++d) x[d] = __ldg(a + d);
+    double* q = Q + (r0 + i) * R;
+#pragma unroll
+    for (int c = 0; c < R; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int d = 0; d < R; ++d) acc = fma(x[d], pis[d * R + c], acc);
+      q[c] = acc;
+    }
+  }
+}
+
 // one warp per row: u = q H * w_k (R), recon_j = sum_a u_a V[j][a]
 template <typename T>
 __global__ void __launch_bounds__(256) fitness_kernel(const T* X, int64_t ldx, int64_t J,
@@ -165,6 +195,17 @@ cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status
 
 cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const double* polar, double* Q,
                            cudaStream_t stream) {
+  const unsigned P = (unsigned)st->npieces;
+  switch (R) {
+#define DP2_AQ(N)                                                                                             \
+  case N:                                                                                                     \
+    assemble_q_rows_kernel<N><<<P, 256, 0, stream>>>(A, st->piece_slice, st->piece_row0, st->piece_rows, polar, Q); \
+    return cudaGetLastError();
+    DP2_AQ(1) DP2_AQ(2) DP2_AQ(3) DP2_AQ(4) DP2_AQ(5) DP2_AQ(6) DP2_AQ(7) DP2_AQ(8) DP2_AQ(9) DP2_AQ(10)
+    DP2_AQ(11) DP2_AQ(12) DP2_AQ(13) DP2_AQ(14) DP2_AQ(15) DP2_AQ(16)
+#undef DP2_AQ
+    default: break;
+  }
   assemble_q_kernel<<<(unsigned)st->npieces, 256, (size_t)R * R * 8, stream>>>(
       A, st->piece_slice, st->piece_row0, st->piece_rows, R, polar, Q);
   return cudaGetLastError();

@@ -4,14 +4,15 @@
 //   Y  = M Omega2           (J x s2)     nn split-K partials + ordered reduce
 //   Z  = M^T Y              (KR x s2)    tn
 //   Y2 = M Z                (J x s2)     = the reference's M (M^T M Omega2)
-//   Q2 = orth(Y2)                        CGS2 (the reference's np.linalg.qr)
+//   Q2 = orth(Y2)                        CholQR2 in one CTA (CGS2 fallback; the reference's np.linalg.qr)
 //   C  = M^T Q2             (KR x s2)    B2 = Q2^T M = C^T
-//   B2 B2^T = C^T C = U mu U^T           Jacobi; E = sqrt(mu_R)
+//   B2 B2^T = C^T C = U mu U^T           register Jacobi (block Jacobi fallback); E = sqrt(mu_R)
 //   D = Q2 U_R (sign rule, P/linalg.py:62-70), F = C U_R / E (same flips)
 #include <dlfcn.h>
 
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
+#include "dp2_small_linalg.cuh"
 
 namespace dp2 {
 
@@ -168,6 +169,105 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* C, int6
 }
 
 // single block: eig(BB) -> E, D = Q2 U_R with the sign rule, Uf = U_R * sign / E
+// Q2 = orth(Y2) (J x s, row-major, in place), one CTA: the J x SP slab in
+// shared memory, CholQR twice (G = Y^T Y on DMMA, register Cholesky, row
+// substitution) -- orthonormal to rounding for kappa(Y2) below ~1e6 (first
+// pivot floor 1e-12); otherwise CGS2 with re-randomisation, like cgs2_kernel.
+template <int SP>
+__global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, int s) {
+  constexpr int LD = SP + 1, NBLK = GramBlocks<SP>::NBLK;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double h[32];
+  __shared__ double red[32];
+  __shared__ int ok_s;
+  const int JP = (J + 31) & ~31;
+  double* Z = sm;
+  double* wpart = Z + (size_t)JP * LD;
+  double* G = wpart + 8 * NBLK * 64;
+  double* L = G + SP * SP;
+  double* dinv = L + SP * SP;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < JP * SP; i += 256) {
+    const int r = i / SP, c = i - r * SP;
+    Z[r * LD + c] = (r < J && c < s) ? Y2[(size_t)r * s + c] : 0.0;
+  }
+  __syncthreads();
+  bool chol = true;
+  for (int pass = 0; pass < 2 && chol; ++pass) {
+    double acc[NBLK][2];
+#pragma unroll
+    for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int t = warp * 32; t < JP; t += 256) gram_tile_dmma<SP, double, LD>(Z + t * LD, acc);
+    gram_store<SP>(acc, wpart, G);
+    __syncthreads();
+    if (warp == 0) {
+      const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, pass == 0 ? 1e-12 : 1e-3);
+      if (tid == 0) ok_s = okk;
+    }
+    __syncthreads();
+    chol = ok_s != 0;
+    if (!chol) break;
+    for (int r = tid; r < J; r += 256) {
+      double q[SP];
+#pragma unroll
+      for (int i = 0; i < SP; ++i) {
+        if (i < s) {
+          double t = Z[r * LD + i];
+#pragma unroll
+          for (int m = 0; m < i; ++m) t = fma(-L[i * SP + m], q[m], t);
+          q[i] = t * dinv[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < SP; ++i)
+        if (i < s) Z[r * LD + i] = q[i];
+    }
+    __syncthreads();
+  }
+  if (!chol) {
+    for (int i = tid; i < J * SP; i += 256) {
+      const int r = i / SP, c = i - r * SP;
+      Z[r * LD + c] = c < s ? Y2[(size_t)r * s + c] : 0.0;
+    }
+    __syncthreads();
+    cgs2_smem(Z, J, LD, s, h, red);
+  }
+  for (int i = tid; i < J * s; i += 256) Y2[i] = Z[(i / s) * LD + i % s];
+}
+
+template <int SP>
+bool orth2_t(double* Y2, int64_t J, int s, cudaStream_t st) {
+  constexpr int NBLK = GramBlocks<SP>::NBLK;
+  const int JP = (int)((J + 31) & ~31);
+  const size_t bytes = ((size_t)JP * (SP + 1) + 8 * NBLK * 64 + 2 * SP * SP + SP) * 8;
+  if (bytes > 200 * 1024) return false;
+  if (cudaFuncSetAttribute(orth2_cholqr_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  orth2_cholqr_kernel<SP><<<1, 256, bytes, st>>>(Y2, (int)J, s);
+  return true;
+}
+
+bool run_orth2(double* Y2, int64_t J, int s, cudaStream_t st) {
+  if (s <= 8) return orth2_t<8>(Y2, J, s, st);
+  if (s <= 16) return orth2_t<16>(Y2, J, s, st);
+  if (s <= 24) return orth2_t<24>(Y2, J, s, st);
+  if (s <= 32) return orth2_t<32>(Y2, J, s, st);
+  return false;
+}
+
+// eig of the s x s Gram BB by warp 0 in registers (s <= 32); the block
+// Jacobi below only when it declines (a zero eigenvalue / no convergence)
+DP2_DEV bool eig_reg_any(double* A, int s, double* U) {
+  if (s <= 8) return eig_sym_reg<8>(A, s, U, s, s);
+  if (s <= 16) return eig_sym_reg<16>(A, s, U, s, s);
+  if (s <= 24) return eig_sym_reg<24>(A, s, U, s, s);
+  if (s <= 32) return eig_sym_reg<32>(A, s, U, s, s);
+  return false;
+}
+
 __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, const double* Q2, int64_t J,
                                                             int R, double* D, double* E, double* Uf,
                                                             double* Ubuf, int64_t* status) {
@@ -180,8 +280,16 @@ __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, co
   __shared__ double sgn[64];
   __shared__ double ev[64];
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int sw = jacobi_eig_block(BB, s, Ubuf, s, s, cs, &flag);
-  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  __shared__ int reg_ok;
+  if (tid < 32) {
+    const bool okk = eig_reg_any(BB, s, Ubuf);
+    if (tid == 0) reg_ok = okk;
+  }
+  __syncthreads();
+  if (!reg_ok) {
+    const int sw = jacobi_eig_block(BB, s, Ubuf, s, s, cs, &flag);
+    if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  }
   sort_desc_perm(BB, s, s, perm);
   for (int r = tid; r < R; r += nt) {
     const double mu = BB[perm[r] * s + perm[r]];
@@ -294,7 +402,7 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   nn(omega2, Y);
   tn(Y, Z);
   nn(Z, Y2);
-  cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
+  if (!run_orth2(Y2, J, s2, st)) cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
   tn(Y2, C);
   // BB = C^T C  <=>  C_cm C_cm^T (symmetric, so layout-neutral)
   if (!dgemm_cm(st, false, true, s2, s2, (int)KR, C, s2, C, s2, BB, s2)) {
