@@ -260,27 +260,9 @@ __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, cons
     CC[a * ld + b] = CCg[(size_t)k * sp * sp + a * sp + b];
   }
   __syncwarp();
-  // ---- Cholesky of G with a relative pivot floor
-  double gmax = 0.0;
-  for (int i = 0; i < s; ++i) gmax = fmax(gmax, G[i * ld + i]);
-  bool chol = gmax > 0.0;
-  for (int c = 0; c < s && chol; ++c) {
-    double d = 0.0;
-    if (lane == 0) {
-      d = G[c * ld + c];
-      for (int m = 0; m < c; ++m) d = fma(-G[c * ld + m], G[c * ld + m], d);
-    }
-    d = __shfl_sync(0xffffffffu, d, 0);
-    if (!(d > 1e-13 * gmax)) { chol = false; break; }
-    const double l = sqrt(d);
-    for (int i = c + 1 + lane; i < s; i += 32) {
-      double t = G[i * ld + c];
-      for (int m = 0; m < c; ++m) t = fma(-G[i * ld + m], G[c * ld + m], t);
-      G[i * ld + c] = t / l;
-    }
-    if (lane == 0) G[c * ld + c] = l;
-    __syncwarp();
-  }
+  // ---- Cholesky of G with a relative pivot floor (registers; L overwrites G's
+  // lower triangle, the upper triangle is not read afterwards)
+  const bool chol = chol_reg<SP>(G, ld, G, ld, lam, s, 1e-13);
   int rp = s;
   if (chol) {
     // X = L^-1 CC (lanes own columns), then Bg = X L^-T: Bg[r][:] = (L^-1 X[r][:]^T)^T
