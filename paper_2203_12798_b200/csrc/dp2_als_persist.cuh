@@ -167,10 +167,13 @@ DP2_DEV void cta_mm(const double* A, const double* B, double* C) {
   __syncthreads();
 }
 
-// Polar factor Jacobi: jacobi_cols (dp2_common.cuh) with V accumulated.
+// Polar factor Jacobi: jacobi_cols (dp2_common.cuh) with V accumulated and
+// the loose stop (largest relative off-diagonal of the last sweep < 1e-4, so
+// ~1e-8 remains: the polar factor enters the next ALS update, whose own
+// rounding and the 1e-5 / 1e-6 parity bounds are far above that).
 template <int R>
 DP2_DEV int jacobi_reg(double (&a)[R], double (&v)[R]) {
-  return jacobi_cols<R, true>(a, v);
+  return jacobi_cols<R, true, true>(a, v);
 }
 
 template <int R>

@@ -356,8 +356,11 @@ DP2_DEV float rsqrt_approx(float x) {
 // convergence leaves ~1e-12 after it).  Returns the sweeps used (cap + 1
 // when not converged).  Measured on B200 (tools/fp64_probe.cu): ~630 cycles
 // per round at R = 10, about half of it the angle's dependent chain.
-template <int R, bool WITHV>
+template <int R, bool WITHV, bool LOOSE = false>
 DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
+  // stop threshold on the largest relative off-diagonal seen in a sweep
+  // (squared): 1e-6 -> ~1e-12 left after it; LOOSE: 1e-4 -> ~1e-8
+  constexpr float STOP2 = LOOSE ? 1e-8f : 1e-12f;
   constexpr int N = R + (R & 1), CAP = 40;
   constexpr double TOL = 4.0 * R * 2.220446049250313e-16, TOL2 = TOL * TOL;
   const int lane = threadIdx.x & 31;
@@ -399,7 +402,7 @@ DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
         const double sc = __hiloint2double((1023 - ex) << 20, 0);  // 2^-ex: max(alpha, beta) sc in [1, 2)
         const float df = (float)(d * sc), gf = (float)(g2 * sc);
         const float af = (float)(alpha * sc), bf = (float)(beta * sc);
-        big |= 0.25f * gf * gf > 1e-12f * (af * bf);  // relative off-diagonal above 1e-6
+        big |= 0.25f * gf * gf > STOP2 * (af * bf);  // relative off-diagonal above the stop threshold
         float tf = (df >= 0.f ? gf : -gf) * rcp_approx(fabsf(df) + sqrt_approx(fmaf(df, df, gf * gf)));
         double t = (double)tf;
         if (fabsf(tf) <= 1e-30f) t = g2 / (2.0 * d);  // |zeta| beyond fp32 range: t ~ 1 / (2 zeta)
