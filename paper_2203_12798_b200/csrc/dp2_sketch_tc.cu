@@ -677,14 +677,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
 
 // B (K x J x sp, fp64) -> per-slice images of the kernel's B shared memory:
 // tf32 (rna), K-major SW128: 32-column chunk j/32, row c, swizzled granule
-__global__ void b_tile_kernel(const double* B, int64_t K, int J, int Jp, int sp, float* out) {
+__global__ void __launch_bounds__(256) b_tile_kernel(const double* B, int64_t K, int J, int Jp, int sp, float* out) {
+  // one block per slice (grid-stride over slices); thread = (row j, 4
+  // consecutive columns c): 32-bit index math, 16-byte loads of B's row
   const int64_t per = (int64_t)Jp * sp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * per; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = e / per;
-    const int r = (int)(e - k * per), j = r / sp, c = r - j * sp;
-    const float v = j < J ? tf32r((float)B[(k * J + j) * sp + c]) : 0.0f;
-    *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(out + k * per) + (size_t)(j >> 5) * sp * 128 +
-                              swz(c, j & 31)) = v;
+  const int q4 = sp / 4;  // sp % 8 == 0
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const double* bk = B + k * (int64_t)J * sp;
+    unsigned char* ok = reinterpret_cast<unsigned char*>(out + k * per);
+    for (int e = threadIdx.x; e < Jp * q4; e += blockDim.x) {
+      const int j = e / q4, c0 = (e - j * q4) * 4;
+      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+      if (j < J) {
+        const double2 a = *reinterpret_cast<const double2*>(bk + (size_t)j * sp + c0);
+        const double2 b = *reinterpret_cast<const double2*>(bk + (size_t)j * sp + c0 + 2);
+        v = make_double4(a.x, a.y, b.x, b.y);
+      }
+      unsigned char* row = ok + (size_t)(j >> 5) * sp * 128;
+      *reinterpret_cast<float*>(row + swz(c0, j & 31)) = tf32r((float)v.x);
+      *reinterpret_cast<float*>(row + swz(c0 + 1, j & 31)) = tf32r((float)v.y);
+      *reinterpret_cast<float*>(row + swz(c0 + 2, j & 31)) = tf32r((float)v.z);
+      *reinterpret_cast<float*>(row + swz(c0 + 3, j & 31)) = tf32r((float)v.w);
+    }
   }
 }
 
@@ -775,7 +789,7 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
   cudaError_t be;
   float* bt = btile_scratch((size_t)st->K * prm.bbytes, &be);
   if (!bt) return be;
-  tcs::b_tile_kernel<<<592, 256, 0, stream>>>(B, st->K, prm.J, prm.Jp, sp, bt);
+  tcs::b_tile_kernel<<<(unsigned)(st->K < 2048 ? st->K : 2048), 256, 0, stream>>>(B, st->K, prm.J, prm.Jp, sp, bt);
   prm.btile = bt;
   // X as a 2-D tensor (J columns, total_rows rows, row pitch ldx*4 B); boxes
   // of 32 columns x 64 rows land in shared memory with the 128 B swizzle
