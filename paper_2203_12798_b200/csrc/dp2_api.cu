@@ -292,9 +292,11 @@ int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_de
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
                                   static_cast<char*>(ws), status_dev, timing_ms, S(stream));
-  // + the B-image kernel of each tensor-core streaming pass and gram_y_piece_kernel
+  // sp <= 32: 2 streaming passes + orth (Gram, Cholesky, substitution, CGS2
+  // fallback) + gather, factor, argmax, signs, write_a, complete; the
+  // tensor-core pass adds its two B-image kernels and gram_y_piece_kernel
   const int tc = dp2::sketch_tc_eligible(st, sp) ? 3 : 0;
-  return e == cudaSuccess ? ok((sp <= 32 ? 9 : 8) + tc) : fail(e, "dp2_stage1");
+  return e == cudaSuccess ? ok((sp <= 32 ? 12 : 8) + tc) : fail(e, "dp2_stage1");
 }
 
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {

@@ -131,107 +131,167 @@ __global__ void __launch_bounds__(256) gather_dmma_kernel(const double* part, co
 
 // ------------------------------------------------------------ orth (CholQR2)
 // Q_Z = orth(Z), Z = sum of the slice's pass-1 partials (P/linalg.py:124-126):
-// CholQR -- G = Z^T Z on DMMA over the shared-memory slab, G = L L^T,
-// Z <- Z L^-T (row-wise substitution in registers); in exact arithmetic the
-// Gram-Schmidt / positive-diagonal-QR Q.  One pass suffices here: Q_Z only
-// seeds the second streaming pass, and everything downstream depends on
-// span(Q_Z) alone, which a nonsingular right factor preserves up to the
-// product's rounding; with the pivot guard below, kappa(Q_Z) <= 1 + ~1e-4.  A
-// pivot below 1e-12 of the largest (kappa(Z) beyond ~1e6, or a dependent
-// column) sends the slice to CGS2 with re-randomisation (cgs2_smem).
-template <int SP>
-__global__ void __launch_bounds__(256) orth_cholqr_kernel(const double* part, const int32_t* slice_piece,
-                                                          const int32_t* s_k, int J, double* Q) {
+// CholQR -- G = Z^T Z on DMMA, G = L L^T, Z <- Z L^-T (row-wise substitution
+// in registers); in exact arithmetic the Gram-Schmidt / positive-diagonal-QR
+// Q.  One pass suffices here: Q_Z only seeds the second streaming pass, and
+// everything downstream depends on span(Q_Z) alone, which a nonsingular right
+// factor preserves up to the product's rounding; with the pivot guard below,
+// kappa(Q_Z) <= 1 + ~1e-4.  A pivot below 1e-12 of the largest (kappa(Z)
+// beyond ~1e6, or a dependent column) flags the slice for CGS2 with
+// re-randomisation (orth_fallback_kernel).  Each lane keeps its rows of Z in
+// registers (rows r, r + 256, ... of the slice); warp-private 32-row tiles in
+// shared memory feed the DMMA Gram only, so two CTAs fit per SM.
+// Three kernels so that no SM idles behind a serial Cholesky: the Gram of
+// each slice (DMMA over warp tiles of Z rows), one warp per slice for the
+// Cholesky (all slices at once), then the row-parallel substitution.  G and
+// L are staged in the slice's own output slot (Q_k, J x SP), which the last
+// kernel reads into shared memory before writing Q rows over it.
+template <int SP, int RPT>  // RPT: rows per thread (J <= 256 RPT)
+__global__ void __launch_bounds__(256) orth_gram_kernel(const double* part, const int32_t* slice_piece, int J,
+                                                        double* Q) {
   constexpr int LD = SP + 1, NBLK = GramBlocks<SP>::NBLK;
   extern __shared__ __align__(16) double sm[];
-  __shared__ double h[32];
-  __shared__ double red[32];
-  __shared__ int ok_s;
-  const int JP = (J + 31) & ~31;
-  double* Z = sm;                          // JP x LD
-  double* wpart = Z + (size_t)JP * LD;     // 8 x NBLK x 64
-  double* G = wpart + 8 * NBLK * 64;       // SP x SP
-  double* L = G + SP * SP;                 // SP x SP (lower)
-  double* dinv = L + SP * SP;              // SP
-  const int k = blockIdx.x, tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* tile = sm + warp * 32 * LD;
+  double* wpart = sm + 8 * 32 * LD;
+  const int k = blockIdx.x;
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
-  const int s = s_k[k];
   const size_t n = (size_t)J * SP;
-  // Z = sum of partials: 8 independent loads per thread in flight per piece
-  for (int i0 = tid; i0 < JP * SP; i0 += 256 * 8) {
-    double v[8];
+  double acc[NBLK][2];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = 0.0;
-    for (int p = p0; p < p1; ++p) {
-      const double* src = part + (size_t)p * n;
+  for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll 1
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + 256 * u;
+    double z[SP];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + 256 * u;
-        if (i < J * SP) v[u] += __ldg(src + i);
-      }
-    }
+    for (int c = 0; c < SP; ++c) z[c] = 0.0;
+    if (r < J)
+      for (int p = p0; p < p1; ++p) {
+        const double2* src = reinterpret_cast<const double2*>(part + (size_t)p * n + (size_t)r * SP);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + 256 * u;
-      if (i < JP * SP) Z[(i / SP) * LD + i % SP] = v[u];
-    }
-  }
-  __syncthreads();
-  bool chol = true;
-  for (int pass = 0; pass < 1; ++pass) {
-    double acc[NBLK][2];
-#pragma unroll
-    for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
-    for (int t = warp * 32; t < JP; t += 256) gram_tile_dmma<SP, double, LD>(Z + t * LD, acc);
-    gram_store<SP>(acc, wpart, G);
-    __syncthreads();
-    if (warp == 0) {
-      const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, 1e-12);
-      if (tid == 0) ok_s = okk;
-    }
-    __syncthreads();
-    chol = ok_s != 0;
-    if (!chol) break;
-    for (int r = tid; r < J; r += 256) {  // row r of Z L^-T: L q^T = z^T
-      double q[SP];
-#pragma unroll
-      for (int i = 0; i < SP; ++i) {
-        if (i < s) {
-          double t = Z[r * LD + i];
-#pragma unroll
-          for (int m = 0; m < i; ++m) t = fma(-L[i * SP + m], q[m], t);
-          q[i] = t * dinv[i];
+        for (int c = 0; c < SP / 2; ++c) {
+          const double2 v = __ldg(src + c);
+          z[2 * c] += v.x;
+          z[2 * c + 1] += v.y;
         }
       }
 #pragma unroll
-      for (int i = 0; i < SP; ++i)
-        if (i < s) Z[r * LD + i] = q[i];
-    }
-    __syncthreads();
+    for (int c = 0; c < SP; ++c) tile[lane * LD + c] = z[c];
+    __syncwarp();
+    gram_tile_dmma<SP, double, LD>(tile, acc);
+    __syncwarp();
   }
-  if (!chol) {  // reload Z, then CGS2
-    for (int i = tid; i < J * SP; i += 256) {
-      double v = 0.0;
-      for (int p = p0; p < p1; ++p) v += part[(size_t)p * n + i];
-      Z[(i / SP) * LD + i % SP] = v;
-    }
-    __syncthreads();
-    cgs2_smem(Z, J, LD, s, h, red);
-  }
-  double* Qk = Q + (size_t)k * n;
-  for (int i = tid; i < J * SP; i += 256) Qk[i] = Z[(i / SP) * LD + i % SP];
+  gram_store<SP>(acc, wpart, Q + (size_t)k * n);  // G into Q_k[0 : SP*SP]
 }
 
 template <int SP>
-cudaError_t orth_t(const dp2_store* st, const int32_t* s_dev, const double* part1, double* qz, cudaStream_t stream) {
+__global__ void __launch_bounds__(128) orth_chol_kernel(const int32_t* s_k, int K, int J, double* Q, int32_t* flag) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= K) return;
+  double* slot = Q + (size_t)k * J * SP;
+  // G at slot[0 : SP^2], L to slot[SP^2 : 2 SP^2], 1/diag to slot[2 SP^2 : + SP]
+  const bool ok = chol_reg<SP>(slot, SP, slot + SP * SP, SP, slot + 2 * SP * SP, s_k[k], 1e-12);
+  if (lane == 0) flag[k] = ok ? 0 : 1;
+}
+
+template <int SP, int RPT>
+__global__ void __launch_bounds__(256) orth_apply_kernel(const double* part, const int32_t* slice_piece,
+                                                         const int32_t* s_k, int J, double* Q, const int32_t* flag) {
+  __shared__ double L[SP * SP];
+  __shared__ double dinv[SP];
+  const int k = blockIdx.x, tid = threadIdx.x;
+  if (flag[k]) return;  // orth_fallback_kernel
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k];
+  const size_t n = (size_t)J * SP;
+  double* Qk = Q + (size_t)k * n;
+  for (int e = tid; e < SP * SP; e += 256) L[e] = Qk[SP * SP + e];
+  if (tid < SP) dinv[tid] = Qk[2 * SP * SP + tid];
+  __syncthreads();
+#pragma unroll 1
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + 256 * u;
+    if (r >= J) break;
+    double q[SP];
+#pragma unroll
+    for (int c = 0; c < SP; ++c) q[c] = 0.0;
+    for (int p = p0; p < p1; ++p) {
+      const double2* src = reinterpret_cast<const double2*>(part + (size_t)p * n + (size_t)r * SP);
+#pragma unroll
+      for (int c = 0; c < SP / 2; ++c) {
+        const double2 v = __ldg(src + c);
+        q[2 * c] += v.x;
+        q[2 * c + 1] += v.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < SP; ++i) {
+      if (i < s) {
+        double t = q[i];
+#pragma unroll
+        for (int m = 0; m < i; ++m) t = fma(-L[i * SP + m], q[m], t);
+        q[i] = t * dinv[i];
+      }
+    }
+    double2* dst = reinterpret_cast<double2*>(Qk + (size_t)r * SP);
+#pragma unroll
+    for (int c = 0; c < SP / 2; ++c) dst[c] = make_double2(q[2 * c], q[2 * c + 1]);
+  }
+}
+
+// the slices orth_cholqr flagged: CGS2 with re-randomisation on the shared-memory slab
+__global__ void __launch_bounds__(256) orth_fallback_kernel(const double* part, const int32_t* slice_piece,
+                                                            const int32_t* s_k, int J, int sp, double* Q,
+                                                            const int32_t* flag) {
+  extern __shared__ __align__(16) double qs[];
+  __shared__ double h[32];
+  __shared__ double red[32];
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  if (!flag[k]) return;
+  const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k], ld = sp + 1;
+  const int n = J * sp;
+  for (int i = tid; i < n; i += nt) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * n + i];
+    qs[(i / sp) * ld + i % sp] = acc;
+  }
+  __syncthreads();
+  cgs2_smem(qs, J, ld, s, h, red);
+  double* Qk = Q + (size_t)k * n;
+  for (int i = tid; i < n; i += nt) Qk[i] = qs[(i / sp) * ld + i % sp];
+}
+
+template <int SP, int RPT>
+cudaError_t orth_rt(const dp2_store* st, const int32_t* s_dev, const double* part1, double* qz, int32_t* flag,
+                    cudaStream_t stream) {
   constexpr int NBLK = GramBlocks<SP>::NBLK;
-  const int K = (int)st->K, J = (int)st->J, JP = (J + 31) & ~31;
-  const size_t bytes = ((size_t)JP * (SP + 1) + 8 * NBLK * 64 + 2 * SP * SP + SP) * 8;
-  if (bytes > 220 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(orth_cholqr_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  const int K = (int)st->K, J = (int)st->J;
+  if ((size_t)J * SP < (size_t)2 * SP * SP + SP) return cudaErrorInvalidValue;  // staging needs the slot
+  const size_t bytes = ((size_t)8 * 32 * (SP + 1) + 8 * NBLK * 64) * 8;
+  cudaError_t e = cudaFuncSetAttribute(orth_gram_kernel<SP, RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bytes);
   if (e != cudaSuccess) return e;
-  orth_cholqr_kernel<SP><<<K, 256, bytes, stream>>>(part1, st->slice_piece, s_dev, J, qz);
+  orth_gram_kernel<SP, RPT><<<K, 256, bytes, stream>>>(part1, st->slice_piece, J, qz);
+  orth_chol_kernel<SP><<<(K + 3) / 4, 128, 0, stream>>>(s_dev, K, J, qz, flag);
+  orth_apply_kernel<SP, RPT><<<K, 256, 0, stream>>>(part1, st->slice_piece, s_dev, J, qz, flag);
+  const size_t qb = (size_t)J * (SP + 1) * 8;
+  e = cudaFuncSetAttribute(orth_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qb);
+  if (e != cudaSuccess) return e;
+  orth_fallback_kernel<<<K, 256, qb, stream>>>(part1, st->slice_piece, s_dev, J, SP, qz, flag);
   return cudaGetLastError();
+}
+
+template <int SP>
+cudaError_t orth_t(const dp2_store* st, const int32_t* s_dev, const double* part1, double* qz, int32_t* flag,
+                   cudaStream_t stream) {
+  const int J = (int)st->J;
+  if ((size_t)J * (SP + 1) * 8 > 200 * 1024) return cudaErrorInvalidValue;  // no fallback slab
+  if (J <= 256) return orth_rt<SP, 1>(st, s_dev, part1, qz, flag, stream);
+  if (J <= 512) return orth_rt<SP, 2>(st, s_dev, part1, qz, flag, stream);
+  return cudaErrorInvalidValue;
 }
 
 // ------------------------------------------------------------ factor (warp / slice)
@@ -653,11 +713,12 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
     cudaError_t eo = cudaErrorInvalidValue;
+    int32_t* flag = reinterpret_cast<int32_t*>(gscratch);  // free until pass 2's Gram partials
     switch (sp) {
-      case 8: eo = orth_t<8>(st, s_dev, part1, qz, stream); break;
-      case 16: eo = orth_t<16>(st, s_dev, part1, qz, stream); break;
-      case 24: eo = orth_t<24>(st, s_dev, part1, qz, stream); break;
-      case 32: eo = orth_t<32>(st, s_dev, part1, qz, stream); break;
+      case 8: eo = orth_t<8>(st, s_dev, part1, qz, flag, stream); break;
+      case 16: eo = orth_t<16>(st, s_dev, part1, qz, flag, stream); break;
+      case 24: eo = orth_t<24>(st, s_dev, part1, qz, flag, stream); break;
+      case 32: eo = orth_t<32>(st, s_dev, part1, qz, flag, stream); break;
       default: break;
     }
     if (eo == cudaSuccess) return eo;
