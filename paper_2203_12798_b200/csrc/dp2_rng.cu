@@ -190,6 +190,26 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
     o[(e / (sp - s)) * sp + s + e % (sp - s)] = 0.0;
   int64_t i = 0;  // normals emitted
   int start = 0;  // lane of the next normal start in this batch
+  // (row, column) of normal i, advanced incrementally (no 64-bit division per
+  // normal): advance by d <= 33 with s >= 1
+  int64_t row0 = 0;
+  int col0 = 0;
+  auto advance = [&](int d) {
+    col0 += d;
+    while (col0 >= s) {
+      col0 -= s;
+      ++row0;
+    }
+  };
+  auto at = [&](int off) -> double* {  // element of normal i + off (0 <= off < 32)
+    int c = col0 + off;
+    int64_t r = row0;
+    while (c >= s) {
+      c -= s;
+      ++r;
+    }
+    return o + r * sp + c;
+  };
   while (i < total) {
     uint64_t r = pcg_out(st);
     const int idx = (int)(r & 0xff);
@@ -204,9 +224,10 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
     // lanes start .. f-1 are one-draw normals
     if (lane >= start && lane < f) {
       const int64_t oi = i + (lane - start);
-      if (oi < total) o[(oi / s) * sp + oi % s] = x;
+      if (oi < total) *at(lane - start) = x;
     }
     i += f - start;
+    advance(f - start);
     if (f == 32) {  // batch exhausted: advance every lane by 32 draws
       st = add128(mul128(st, A32), C32);
       start = 0;
@@ -252,7 +273,7 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
           if (slot < cap) recs[slot] = rec;
           else redo[k] = 1;
         }
-        o[(i / s) * sp + i % s] = val;
+        *at(0) = val;
         produced = 1;
       } else {
         const double f0 = fi_s[idx - 1];
@@ -260,7 +281,7 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
         const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(f0, -f1), h.next_double()), f1);
         consumed = 2;
         if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
-          o[(i / s) * sp + i % s] = x;
+          *at(0) = x;
           produced = 1;
         }
       }
@@ -269,6 +290,7 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
     produced = __shfl_sync(0xffffffffu, produced, f);
     consumed = __shfl_sync(0xffffffffu, consumed, f);
     i += produced;
+    advance(produced);
     const int nstart = f + consumed;
     if (nstart < 32) {
       start = nstart;  // lanes still hold the draws behind the consumed ones

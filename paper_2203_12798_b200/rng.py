@@ -60,6 +60,31 @@ _ZIG_INV_R = 0.27366123732975827203338247596
 
 
 _REPLAY_POOL = None
+_SCRATCH = {}
+
+
+def _scratch(device, K, cap):
+    """Device tail-record buffers and their pinned readback copies, reused
+    across calls (two alternating sets per shape, so a speculative replay
+    still reading one set is never overwritten)."""
+    key = (str(device), K, cap)
+    sets = _SCRATCH.get(key)
+    if sets is None:
+        def one():
+            return {"recs": torch.empty((cap, _REC.itemsize), dtype=torch.uint8, device=device),
+                    "nrec": torch.zeros(1, dtype=torch.int32, device=device),
+                    "redo": torch.zeros(K, dtype=torch.int32, device=device),
+                    "nrec_h": torch.empty(1, dtype=torch.int32, pin_memory=True),
+                    "redo_h": torch.empty(K, dtype=torch.int32, pin_memory=True),
+                    "recs_h": torch.empty((cap, _REC.itemsize), dtype=torch.uint8, pin_memory=True),
+                    "busy": None}
+        sets = _SCRATCH[key] = [one(), one(), 0]
+    sets[2] ^= 1
+    cur = sets[sets[2]]
+    if cur["busy"] is not None:
+        cur["busy"].result()  # its replay must be done reading the pinned copies
+        cur["busy"] = None
+    return cur
 
 
 def _replay_check(ev, nrec_h, redo_h_t, recs_h, cap):
@@ -103,17 +128,16 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
         s_dev = to_device_async(list(widths), torch.int32, device)
     ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
     cap = max(4096, 8 * K + n * max(widths) * K // 1000)
-    recs = torch.empty((cap, _REC.itemsize), dtype=torch.uint8, device=device)
-    nrec = torch.zeros(1, dtype=torch.int32, device=device)
-    redo = torch.zeros(K, dtype=torch.int32, device=device)
+    bufs = _scratch(device, K, cap)
+    recs, nrec, redo = bufs["recs"], bufs["nrec"], bufs["redo"]
+    nrec.zero_()
+    redo.zero_()
     vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
     _lib.check(_lib.lib().dp2_omega_generate(C.c_uint64(seed & _MASK64), K, n, vp(s_dev), sp, vp(ids), vp(out),
                                              vp(recs), cap, vp(nrec), vp(redo),
                                              C.c_void_p(torch.cuda.current_stream().cuda_stream)), "omega")
     # one readback: record count, per-slice redo flags and the records
-    nrec_h = torch.empty(1, dtype=torch.int32, pin_memory=True)
-    redo_h_t = torch.empty(K, dtype=torch.int32, pin_memory=True)
-    recs_h = torch.empty(tuple(recs.shape), dtype=torch.uint8, pin_memory=True)
+    nrec_h, redo_h_t, recs_h = bufs["nrec_h"], bufs["redo_h"], bufs["recs_h"]
     nrec_h.copy_(nrec, non_blocking=True)
     redo_h_t.copy_(redo, non_blocking=True)
     recs_h.copy_(recs, non_blocking=True)
@@ -124,8 +148,8 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
             _REPLAY_POOL = ThreadPoolExecutor(1)
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream())
-        keep = (recs, nrec, redo)  # device buffers live until the copies ran
-        fut = _REPLAY_POOL.submit(lambda: (_replay_check(ev, nrec_h, redo_h_t, recs_h, cap), keep)[0])
+        fut = _REPLAY_POOL.submit(_replay_check, ev, nrec_h, redo_h_t, recs_h, cap)
+        bufs["busy"] = fut
         return out, fut
     torch.cuda.current_stream().synchronize()
     count = int(nrec_h[0])
