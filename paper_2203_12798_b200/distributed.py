@@ -11,9 +11,14 @@
   (sum) assembles M exactly -- every entry has a single nonzero contributor, so
   the sum is exact -- then stage 2 runs replicated (identical inputs, identical
   outputs on every rank).
-* ALS: D, E, H, V replicated; F rows, W rows, rotations and Q local.  Each
-  iteration allreduces three tiny buffers (2 R^2, 2 R^2, 1 doubles) between
-  the phases of ``dp2_als_phase``.
+* ALS (default ``als="replicated"``): after stage 2 every rank holds the full
+  compressed tensor (D, E and all K R x R cores F_k -- K R^2 doubles, tiny),
+  so each rank runs the single-GPU persistent ALS loop on all of it: no
+  per-iteration communication at all; Q is then assembled for the local
+  slices only (their A_k and polar factors).  ``als="sharded"`` keeps the
+  phase-split variant: D, E, H, V replicated, F rows / W rows / rotations
+  local, three allreduces of tiny buffers (2 R^2, 2 R^2, 1 doubles) per
+  iteration between the phases of ``dp2_als_phase``.
 
 The driver (``ShardedALS``) only sequences phases and collectives; the phase
 compute is a pluggable ``ops`` object (the C ABI on the GPU; the gloo tests on
@@ -56,6 +61,29 @@ def local_rows(F, local_ids, R):
     idx = (torch.as_tensor(local_ids, device=F.device)[:, None] * R +
            torch.arange(R, device=F.device)[None, :]).reshape(-1)
     return F.index_select(0, idx).contiguous()
+
+
+def replicated_als(F, D, E, K, J, R, h, v, w, max_iters, tol, normalize):
+    """The single-GPU ALS loop (``dp2_als_run``: one cooperative launch for
+    R <= 16) on the FULL compressed tensor (global K); returns device H, V, W
+    (K x R), polar (K x R x R), trace, tstamp, iters, status."""
+    from .tensor import new_status
+    dev = D.device
+    lib = _lib.lib()
+    H = torch.from_numpy(np.ascontiguousarray(h)).to(dev)
+    V = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    W = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
+    polar = torch.empty((K, R, R), dtype=torch.float64, device=dev)
+    trace = torch.zeros(max_iters, dtype=torch.float64, device=dev)
+    tstamp = torch.zeros(max_iters + 1, dtype=torch.int64, device=dev)
+    iters = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(max(256, int(lib.dp2_als_workspace(K, J, R))), dtype=torch.uint8, device=dev)
+    status = new_status(dev)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(lib.dp2_als_run(vp(F), vp(D), vp(E), K, J, R, vp(H), vp(V), vp(W), vp(polar), max_iters, float(tol),
+                               int(bool(normalize)), vp(trace), vp(tstamp), vp(iters), 0, vp(ws), ws.numel(),
+                               vp(status), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "als_run")
+    return H, V, W, polar, trace, tstamp, iters, status
 
 
 class ShardedALS:
@@ -132,7 +160,7 @@ class DistributedFit:
         self.K = cfg.num_slices
         self.loads = loads
 
-    def fit(self, R, opts, timings=None):
+    def fit(self, R, opts, timings=None, als="replicated"):
         from .compress import check_status, run_stage1, run_stage2, stage2_params
         from .factors import FitTrace, Parafac2Factors, SliceViews, initial_factors
         from .linalg import RsvdParams
@@ -147,27 +175,41 @@ class DistributedFit:
         A, M_local, rank_found, status = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings)
         M = assemble_m(M_local, self.local_ids, K, R)
         D, E, F = run_stage2(M, J, K * R, R, second.seed, s2, om2, status, timings=timings)
-        check_status(status, "compress")
         dev = D.device
-        h, v, w = initial_factors(J, len(self.local_ids), R, opts.seed)
-        H, V = torch.from_numpy(h).to(dev), torch.from_numpy(v).to(dev)
-        W = torch.from_numpy(w).to(dev)
         normalize = bool(opts.normalize) if opts.normalize is not None else True
-        ops = GpuAlsOps(local_rows(F, self.local_ids, R), D, E, H, V, W, J, R, opts.max_iters, opts.tol, normalize)
-        torch.cuda.synchronize()
+        ids = torch.as_tensor(self.local_ids, device=dev)
+        if als == "replicated":
+            h, v, w = initial_factors(J, K, R, opts.seed)
+            H, V, W, polar, trace, tstamp, iters, st_als = replicated_als(
+                F, D, E, K, J, R, h, v, w, opts.max_iters, opts.tol, normalize)
+            torch.cuda.synchronize()
+            check_status(status, "compress")
+            check_status(st_als, "fit_dpar2")
+            polar_local = polar.index_select(0, ids)
+            W_out = W.index_select(0, ids)
+        else:
+            check_status(status, "compress")
+            h, v, w = initial_factors(J, len(self.local_ids), R, opts.seed)
+            H, V = torch.from_numpy(h).to(dev), torch.from_numpy(v).to(dev)
+            W = torch.from_numpy(w).to(dev)
+            ops = GpuAlsOps(local_rows(F, self.local_ids, R), D, E, H, V, W, J, R, opts.max_iters, opts.tol,
+                            normalize)
+            torch.cuda.synchronize()
+            ShardedALS(ops, nccl_allreduce()).run(opts.max_iters)
+            check_status(ops.status, "fit_dpar2")
+            H, V, W_out, polar_local = ops.H, ops.V, ops.W, ops.polar
+            trace, tstamp, iters = ops.trace, ops.tstamp, ops.iters
         pre = time.perf_counter() - started
-        ShardedALS(ops, nccl_allreduce()).run(opts.max_iters)
-        check_status(ops.status, "fit_dpar2")
-        n = int(ops.iters.item())
-        tr = FitTrace(objective=ops.trace[:n].cpu().tolist(),
-                      seconds=list(np.diff(ops.tstamp[:n + 1].cpu().numpy()) * 1e-9), preprocess_seconds=pre,
+        n = int(iters.item())
+        tr = FitTrace(objective=trace[:n].cpu().tolist(),
+                      seconds=list(np.diff(tstamp[:n + 1].cpu().numpy()) * 1e-9), preprocess_seconds=pre,
                       compressed_float_count=self.total_rows * R + K * R * R + J * R + R)
         if n >= 2:
             prev, e = tr.objective[-2], tr.objective[-1]
             tr.converged = bool(prev == 0.0 or abs(prev - e) <= opts.tol * prev)
         from .compress import CompressedTensor
         comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
-        Q = assemble_q(t, comp, ops.polar)
+        Q = assemble_q(t, comp, polar_local.contiguous())
         bounds = t.row_off_host
-        factors = Parafac2Factors(H=ops.H, V=ops.V, W=ops.W, Q=SliceViews(Q, bounds), Q_packed=Q)
+        factors = Parafac2Factors(H=H, V=V, W=W_out, Q=SliceViews(Q, bounds), Q_packed=Q)
         return factors, tr

@@ -57,3 +57,22 @@ def test_virtual_ranks_match_single_gpu(world):
     for o, ids in zip(ops, shards):
         assert torch.allclose(o.W, W1[ids], rtol=0, atol=1e-9 * float(W1.abs().max()))
         assert torch.equal(o.trace, ops[0].trace)
+
+
+def test_distributed_fit_replicated_als_world1_matches_fit():
+    """bench.py's N > 1 path (DistributedFit: sharded stage 1, M assembled,
+    stage 2 + the persistent ALS replicated, Q for the local slices) at world
+    size 1 must reproduce fit_dpar2 on the same tensor."""
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import distributed as D_, synth
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=30)
+    runner = D_.DistributedFit(cfg, 4, 0, 1)
+    opts = dp.SolverOptions(max_iters=12, tol=0.0, seed=0)
+    f, tr = runner.fit(cfg.rank, opts)
+    g, tr2 = dp.fit_dpar2(runner.tensor, cfg.rank, opts, output="device")
+    for key in ("H", "V", "W"):
+        a, b = getattr(f, key).cpu().numpy(), getattr(g, key).cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-10 * max(np.abs(b).max(), 1.0), key
+    assert np.allclose(tr.objective, tr2.objective, rtol=1e-12, atol=0)
+    q1, q2 = f.Q_packed.cpu().numpy(), g.Q_packed.cpu().numpy()
+    assert np.abs(q1 - q2).max() <= 1e-10
