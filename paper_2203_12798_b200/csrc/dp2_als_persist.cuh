@@ -251,14 +251,45 @@ __global__ void __launch_bounds__(PsCfg<R>::MAXW * 32, 1) als_persist_kernel(PsA
       __syncwarp();
       wmm<R, false, true>(Th, Hs, T);   // T = Th H^T
       wmm<R, false, false>(T, Vs, Us);  // A = T V_warm
-      // polar factor: one-sided Jacobi SVD of A in registers
+      const long long dq1 = clock64();
+      int sw32 = 0;
+      // polar factor: one-sided Jacobi SVD of A in registers, mixed precision:
+      // fp32 sweeps to ~1e-5, V re-orthonormalised in fp64 (one Newton-Schulz
+      // step, V <- V (3I - V^T V) / 2), then fp64 sweeps from there (their
+      // first sweep sees off-diagonals near fp32's floor, so the loose stop
+      // ends it after one sweep with ~1e-12 left)
+      {
+        float af[R], vf[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          af[i] = lane < R ? (float)Us[i * R + lane] : 0.f;
+          vf[i] = lane < R ? (float)Vs[i * R + lane] : 0.f;
+        }
+        sw32 = jacobi_cols_f32<R>(af, vf, 12);
+        bool fin = true;
+#pragma unroll
+        for (int i = 0; i < R; ++i) fin &= isfinite(vf[i]);
+        if (__all_sync(0xffffffffu, fin)) {  // else: keep V_warm
+          __syncwarp();
+          if (lane < R)
+#pragma unroll
+            for (int i = 0; i < R; ++i) Vs[i * R + lane] = (double)vf[i];
+          __syncwarp();
+          wmm<R, true, false>(Vs, Vs, Us);  // V^T V
+          for (int e = lane; e < RR; e += 32) Us[e] = ((e / R == e % R) ? 1.5 : 0.0) - 0.5 * Us[e];
+          __syncwarp();
+          wmm<R, false, false>(Vs, Us, Pi);  // V (3I - V^T V) / 2
+          for (int e = lane; e < RR; e += 32) Vs[e] = Pi[e];
+          __syncwarp();
+          wmm<R, false, false>(T, Vs, Us);  // A = T V
+        }
+      }
       double a[R], v[R];
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         a[i] = lane < R ? Us[i * R + lane] : 0.0;
         v[i] = lane < R ? Vs[i * R + lane] : 0.0;
       }
-      const long long dq1 = clock64();
       const int sw = jacobi_reg<R>(a, v);
       const long long dq2 = clock64();
       double s2 = 0.0;
@@ -319,7 +350,7 @@ __global__ void __launch_bounds__(PsCfg<R>::MAXW * 32, 1) als_persist_kernel(PsA
         atomicMax(q + 11, (unsigned long long)(dq1 - dq0));
         atomicMax(q + 12, (unsigned long long)(dq2 - dq1));
         atomicMax(q + 13, (unsigned long long)(dq3 - dq2));
-        atomicMax(q + 14, (unsigned long long)sw);
+        atomicMax(q + 14, (unsigned long long)(sw32 * 100 + sw));
         atomicMax(q + 15, (unsigned long long)(dq3 - dq0));
       }
     }

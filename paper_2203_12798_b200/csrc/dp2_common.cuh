@@ -426,6 +426,58 @@ DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
   return CAP + 1;
 }
 
+// fp32 one-sided Jacobi (same pairing as jacobi_cols): the cheap first phase
+// of a mixed-precision SVD -- rounds are shorter (half the shuffles, fp32
+// latencies); it stops as below or after ``cap`` sweeps.  The caller
+// re-orthonormalises V in fp64 and finishes with jacobi_cols.
+template <int R>
+DP2_DEV int jacobi_cols_f32(float (&a)[R], float (&v)[R], int cap) {
+  constexpr int N = R + (R & 1);
+  constexpr float TOL2 = 1e-11f, STOP2 = 1e-6f;  // rotate above fp32 noise; stop after a sweep with max ratio < 1e-3
+  const int lane = threadIdx.x & 31;
+  for (int sw = 0; sw < cap; ++sw) {
+    bool big = false;
+#pragma unroll 1
+    for (int r = 0; r < N - 1; ++r) {
+      int pj = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+      pj = (lane == r) ? N - 1 : pj;
+      pj = (lane == N - 1) ? r : pj;
+      const int p = lane < N ? pj : lane;
+      float pa[R], pv[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        pa[i] = __shfl_sync(0xffffffffu, a[i], p);
+        pv[i] = __shfl_sync(0xffffffffu, v[i], p);
+      }
+      float al = 0.f, be = 0.f, ga = 0.f;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        al = fmaf(a[i], a[i], al);
+        be = fmaf(pa[i], pa[i], be);
+        ga = fmaf(a[i], pa[i], ga);
+      }
+      const bool lower = lane < p;
+      const float alpha = lower ? al : be, beta = lower ? be : al;
+      float c = 1.f, s = 0.f;
+      if (p != lane && ga * ga > TOL2 * (alpha * beta)) {
+        big |= ga * ga > STOP2 * (alpha * beta);
+        const float d = beta - alpha, g2 = 2.f * ga;
+        const float t = (d >= 0.f ? g2 : -g2) * rcp_approx(fabsf(d) + sqrt_approx(fmaf(d, d, g2 * g2)));
+        c = rsqrt_approx(fmaf(t, t, 1.f));
+        s = c * t;
+      }
+      const float so = lower ? -s : s;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        a[i] = fmaf(c, a[i], so * pa[i]);
+        v[i] = fmaf(c, v[i], so * pv[i]);
+      }
+    }
+    if (!__any_sync(0xffffffffu, big)) return sw + 1;
+  }
+  return cap;
+}
+
 DP2_DEV int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
