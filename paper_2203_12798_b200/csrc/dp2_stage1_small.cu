@@ -81,20 +81,20 @@ __global__ void __launch_bounds__(256) gram_y_piece_kernel(const Y* y2, const in
 }
 
 // Per slice: C = sum of the pass-2 partials (J x SP, written out), CC = C^T C
-// on DMMA over warp-private 32-row tiles, G = sum of the per-piece Gram
-// partials.
-template <int SP>
+// on DMMA over warp tiles (lane = row, rows r, r + 256 of the slice: 16-byte
+// loads of each piece's row), G = sum of the per-piece Y^T Y partials.
+template <int SP, int RPT>
 __global__ void __launch_bounds__(256) gather_dmma_kernel(const double* part, const double* gpart,
                                                           const int32_t* slice_piece, int J, double* Ct,
                                                           double* CCg, double* Gg) {
-  constexpr int LD = SP + 2, NBLK = GramBlocks<SP>::NBLK;
+  constexpr int LD = SP + 1, NBLK = GramBlocks<SP>::NBLK;
   extern __shared__ __align__(16) double sm[];
-  const int k = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* tile = sm + warp * 32 * LD;
   double* wpart = sm + 8 * 32 * LD;
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
   const size_t n = (size_t)J * SP;
-  for (int e = threadIdx.x; e < SP * SP; e += blockDim.x) {
+  for (int e = tid; e < SP * SP; e += 256) {
     double acc = 0.0;
     for (int p = p0; p < p1; ++p) acc += gpart[(size_t)p * SP * SP + e];
     Gg[(size_t)k * SP * SP + e] = acc;
@@ -103,25 +103,28 @@ __global__ void __launch_bounds__(256) gather_dmma_kernel(const double* part, co
 #pragma unroll
   for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
   double* C = Ct + (size_t)k * n;
-  for (int t = warp * 32; t < J; t += 256) {
-    const int rows = min(32, J - t);
-    double v[SP];  // lane's SP entries of the tile (q = lane + 32 u): all loads issued before any store
+#pragma unroll 1
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + 256 * u;
+    double z[SP];
 #pragma unroll
-    for (int u = 0; u < SP; ++u) v[u] = 0.0;
-    for (int p = p0; p < p1; ++p) {
-      const double* src = part + (size_t)p * n + (size_t)t * SP;
+    for (int c = 0; c < SP; ++c) z[c] = 0.0;
+    if (r < J) {
+      for (int p = p0; p < p1; ++p) {
+        const double2* src = reinterpret_cast<const double2*>(part + (size_t)p * n + (size_t)r * SP);
 #pragma unroll
-      for (int u = 0; u < SP; ++u) {
-        const int q = lane + 32 * u;
-        if (q / SP < rows) v[u] += __ldg(src + q);
+        for (int c = 0; c < SP / 2; ++c) {
+          const double2 v = __ldg(src + c);
+          z[2 * c] += v.x;
+          z[2 * c + 1] += v.y;
+        }
       }
+      double2* dst = reinterpret_cast<double2*>(C + (size_t)r * SP);
+#pragma unroll
+      for (int c = 0; c < SP / 2; ++c) dst[c] = make_double2(z[2 * c], z[2 * c + 1]);
     }
 #pragma unroll
-    for (int u = 0; u < SP; ++u) {
-      const int q = lane + 32 * u, r = q / SP, c = q - r * SP;
-      if (r < rows) C[(size_t)t * SP + q] = v[u];
-      tile[r * LD + c] = v[u];
-    }
+    for (int c = 0; c < SP; ++c) tile[lane * LD + c] = z[c];
     __syncwarp();
     gram_tile_dmma<SP, double, LD>(tile, acc);
     __syncwarp();
@@ -665,10 +668,20 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
                                                            st->piece_rows, gscratch);
     gpart = gscratch;
   }
-  const size_t gb = ((size_t)8 * 32 * (SP + 2) + (size_t)8 * GramBlocks<SP>::NBLK * 64) * 8;
-  e = cudaFuncSetAttribute(gather_dmma_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
-  if (e != cudaSuccess) return e;
-  gather_dmma_kernel<SP><<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, Ct, CCg, Gg);
+  const size_t gb = ((size_t)8 * 32 * (SP + 1) + (size_t)8 * GramBlocks<SP>::NBLK * 64) * 8;
+  if (J <= 256) {
+    e = cudaFuncSetAttribute(gather_dmma_kernel<SP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+    if (e != cudaSuccess) return e;
+    gather_dmma_kernel<SP, 1><<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, Ct, CCg, Gg);
+  } else if (J <= 512) {
+    e = cudaFuncSetAttribute(gather_dmma_kernel<SP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+    if (e != cudaSuccess) return e;
+    gather_dmma_kernel<SP, 2><<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, Ct, CCg, Gg);
+  } else {
+    e = cudaFuncSetAttribute(gather_dmma_kernel<SP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gb);
+    if (e != cudaSuccess) return e;
+    gather_dmma_kernel<SP, 8><<<K, 256, gb, stream>>>(part2, gpart, st->slice_piece, J, Ct, CCg, Gg);
+  }
   const int wpb = SP <= 24 ? 4 : 2;
   const size_t fs = wpb * small_factor_smem(SP);
   e = cudaFuncSetAttribute(factor_warp_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
