@@ -451,40 +451,42 @@ __global__ void __launch_bounds__(128) factor_warp_kernel(const double* Gg, cons
 
 // One row of Y (SP entries, fp32 or fp64 storage) into fp64 registers, entries
 // >= s zeroed (16 B loads).
+// One row of Y (SP entries) into registers in its storage type (fp32 rows
+// stay fp32: half the registers; the products convert exactly), entries >= s
+// zeroed (16 B loads).
 template <typename Y, int SP>
-DP2_DEV void load_y_row(const Y* yr, int s, double (&y)[SP]) {
+DP2_DEV void load_y_row(const Y* yr, int s, Y (&y)[SP]) {
   if constexpr (sizeof(Y) == 4) {
 #pragma unroll
     for (int q = 0; q < SP / 4; ++q) {
-      const float4 f = reinterpret_cast<const float4*>(yr)[q];
+      const float4 f = __ldg(reinterpret_cast<const float4*>(yr) + q);
       y[4 * q] = f.x; y[4 * q + 1] = f.y; y[4 * q + 2] = f.z; y[4 * q + 3] = f.w;
     }
   } else {
 #pragma unroll
     for (int q = 0; q < SP / 2; ++q) {
-      const double2 f = reinterpret_cast<const double2*>(yr)[q];
+      const double2 f = __ldg(reinterpret_cast<const double2*>(yr) + q);
       y[2 * q] = f.x; y[2 * q + 1] = f.y;
     }
   }
 #pragma unroll
-  for (int a = 0; a < SP; ++a) y[a] = a < s ? y[a] : 0.0;
+  for (int a = 0; a < SP; ++a) y[a] = a < s ? y[a] : (Y)0;
 }
 
-// (y0 P[:, c], y1 P[:, c]) with P stored transposed in shared memory (Pt =
-// R x SP, rows >= s of P zero): fma over a = 0..SP-1 in order, so padded
+// (y0 P[:, c], y1 P[:, c]) in fp64 with P stored transposed in shared memory
+// (Pt = R x SP, rows >= s of P zero): fma over a = 0..SP-1 in order, so padded
 // entries add exact zeros.
-template <int SP>
-DP2_DEV void dot_pcol(const double (&y0)[SP], const double (&y1)[SP], const double* Pt, int c, double& a0,
-                      double& a1) {
+template <int SP, typename Y>
+DP2_DEV void dot_pcol(const Y (&y0)[SP], const Y (&y1)[SP], const double* Pt, int c, double& a0, double& a1) {
   const double2* pc = reinterpret_cast<const double2*>(Pt + c * SP);
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int q = 0; q < SP / 2; ++q) {
     const double2 pp = pc[q];
-    s0 = fma(y0[2 * q], pp.x, s0);
-    s1 = fma(y1[2 * q], pp.x, s1);
-    s0 = fma(y0[2 * q + 1], pp.y, s0);
-    s1 = fma(y1[2 * q + 1], pp.y, s1);
+    s0 = fma((double)y0[2 * q], pp.x, s0);
+    s1 = fma((double)y1[2 * q], pp.x, s1);
+    s0 = fma((double)y0[2 * q + 1], pp.y, s0);
+    s1 = fma((double)y1[2 * q + 1], pp.y, s1);
   }
   a0 = s0;
   a1 = s1;
@@ -520,17 +522,17 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const Y* y2, const int
   // rows i and i + 256 per step: a thread's rows still increase
   for (int i = tid; i < nr; i += 512) {
     const bool two = i + 256 < nr;
-    double y0[SP], y1[SP];
+    Y y0[SP], y1[SP];
     load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
     if (two) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
     else {
 #pragma unroll
-      for (int a = 0; a < SP; ++a) y1[a] = 0.0;
+      for (int a = 0; a < SP; ++a) y1[a] = (Y)0;
     }
 #pragma unroll 1
     for (int c = 0; c < R; ++c) {
       double a0, a1;
-      dot_pcol<SP>(y0, y1, Pt, c, a0, a1);
+      dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
       double bv = bval[c * 256 + tid];
       int rw = brow[c * 256 + tid];
       if (rw < 0 || fabs(a0) > fabs(bv)) { bv = a0; rw = i; }
@@ -586,17 +588,17 @@ __global__ void __launch_bounds__(256) write_a_kernel(const Y* y2, const int32_t
   for (int t0 = 0; t0 < nr; t0 += 512) {
     const int i = t0 + tid;
     if (i < nr) {
-      double y0[SP], y1[SP];
+      Y y0[SP], y1[SP];
       load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
       if (i + 256 < nr) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
       else {
 #pragma unroll
-        for (int a = 0; a < SP; ++a) y1[a] = 0.0;
+        for (int a = 0; a < SP; ++a) y1[a] = (Y)0;
       }
 #pragma unroll 1
       for (int c = 0; c < R; ++c) {
         double a0, a1;
-        dot_pcol<SP>(y0, y1, Pt, c, a0, a1);
+        dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
         at[tid * R + c] = a0;
         at[(tid + 256) * R + c] = a1;
       }
