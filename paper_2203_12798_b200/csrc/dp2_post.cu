@@ -93,16 +93,32 @@ __global__ void __launch_bounds__(256) assemble_q_rows_kernel(const double* A, c
   const int nr = piece_rows[p];
   for (int i = threadIdx.x; i < nr; i += blockDim.x) {
     const double* a = A + (r0 + i) * R;
-    double x[R];
+    double x[R], y[R];
+    if constexpr (R % 2 == 0) {  // rows are 16-byte aligned: paired loads / stores
 #pragma unroll
-    for (int d = 0; d < R; ++d) x[d] = __ldg(a + d);
-    double* q = Q + (r0 + i) * R;
+      for (int d = 0; d < R / 2; ++d) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(a) + d);
+        x[2 * d] = v.x;
+        x[2 * d + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < R; ++d) x[d] = __ldg(a + d);
+    }
 #pragma unroll
     for (int c = 0; c < R; ++c) {
       double acc = 0.0;
 #pragma unroll
       for (int d = 0; d < R; ++d) acc = fma(x[d], pis[d * R + c], acc);
-      q[c] = acc;
+      y[c] = acc;
+    }
+    double* q = Q + (r0 + i) * R;
+    if constexpr (R % 2 == 0) {
+#pragma unroll
+      for (int c = 0; c < R / 2; ++c) reinterpret_cast<double2*>(q)[c] = make_double2(y[2 * c], y[2 * c + 1]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < R; ++c) q[c] = y[c];
     }
   }
 }

@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(256) write_a_kernel(const Y* y2, const int32_t
 }
 
 // ------------------------------------------------------------ signs + M
+template <int SP>
 __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece, const double* cand_abs,
                                                        const int64_t* cand_row, const int32_t* cand_neg,
                                                        double* Pm, const double* Ct, int K, int J, int sp, int R,
@@ -643,11 +644,24 @@ __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece
   __syncthreads();
   const double* C = Ct + (size_t)k * J * sp;
   const int64_t KR = (int64_t)K * R;
-  for (int e = tid; e < J * R; e += blockDim.x) {
-    const int j = e / R, r = e - j * R;
-    double acc = 0.0;
-    for (int a = 0; a < sp; ++a) acc = fma(C[(size_t)j * sp + a], Ps[a * R + r], acc);
-    M[j * KR + (int64_t)k * R + r] = acc;
+  // thread = row j of C (16 B loads), the slice's R outputs of M's row j
+  for (int j = tid; j < J; j += blockDim.x) {
+    double cr[SP];
+    const double2* src = reinterpret_cast<const double2*>(C + (size_t)j * SP);
+#pragma unroll
+    for (int q = 0; q < SP / 2; ++q) {
+      const double2 v = __ldg(src + q);
+      cr[2 * q] = v.x;
+      cr[2 * q + 1] = v.y;
+    }
+    double* mrow = M + j * KR + (int64_t)k * R;
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < SP; ++a) acc = fma(cr[a], Ps[a * R + r], acc);
+      mrow[r] = acc;
+    }
   }
 }
 
@@ -700,7 +714,7 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
     if (e != cudaSuccess) return e;
     argmax_cand_kernel<float, SP><<<P, 256, as, stream>>>(y, st->row_off, st->piece_slice, st->piece_row0,
                                                          st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
-    signs_m_kernel<<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+    signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
                                                             J, SP, R, sgn, M);
     write_a_kernel<float, SP><<<P, 256, ws, stream>>>(y, st->piece_slice, st->piece_row0, st->piece_rows, s_dev, Pm,
                                                      R, A);
@@ -711,7 +725,7 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
     if (e != cudaSuccess) return e;
     argmax_cand_kernel<double, SP><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0,
                                                           st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
-    signs_m_kernel<<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+    signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
                                                             J, SP, R, sgn, M);
     write_a_kernel<double, SP><<<P, 256, ws, stream>>>(y2, st->piece_slice, st->piece_row0, st->piece_rows, s_dev,
                                                       Pm, R, A);
