@@ -606,7 +606,13 @@ __global__ void __launch_bounds__(256) write_a_kernel(const Y* y2, const int32_t
     __syncthreads();
     const int rows = min(512, nr - t0);
     double* dst = A + (r0 + t0) * R;
-    for (int e = tid; e < rows * R; e += 256) dst[e] = at[e];
+    if ((R & 1) == 0) {  // the block's rows are one contiguous, 16-byte aligned run
+      const int n2 = rows * R / 2;
+      for (int e = tid; e < n2; e += 256)
+        reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(at)[e];
+    } else {
+      for (int e = tid; e < rows * R; e += 256) dst[e] = at[e];
+    }
     __syncthreads();
   }
 }
