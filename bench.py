@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--also-f64", action="store_true", help="add a c2 fp64 sub-measurement")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="use the multi-rank (sharded stage 1 + NCCL) path even at world size 1")
     return ap.parse_args()
 
 
@@ -156,7 +158,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- our arm
@@ -171,7 +173,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.dist_path
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2203_12798_b200 as dp
     from paper_2203_12798_b200 import _lib, synth
@@ -179,7 +186,7 @@ def main():
 
     cfg = workload(args)
     opts = dp.SolverOptions(max_iters=args.iters, tol=0.0, seed=args.seed)
-    if world > 1:
+    if sharded:
         from paper_2203_12798_b200.distributed import DistributedFit
         runner = DistributedFit(cfg, args.seed, rank, world)
         tensor = runner.tensor
@@ -196,7 +203,7 @@ def main():
             return fit_dpar2(tensor, cfg.rank, opts, output="device", timings=timings)
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -224,7 +231,7 @@ def main():
     phase.append((tm, tr))
     barrier()
     ms = start.elapsed_time(stop) / args.steps
-    if world > 1:
+    if sharded:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -236,7 +243,7 @@ def main():
     s2 = float(np.mean([t["stage1_sketch2_ms"] for t in tms]))
     sp = tms[0]["sp"]
     elem = 4 if cfg.dtype == "f32" else 8
-    N_rows = int(tensor.row_off_host[-1]) if world == 1 else runner.local_rows
+    N_rows = runner.local_rows if sharded else int(tensor.row_off_host[-1])
     K_loc = tensor.num_slices
     x_bytes = N_rows * cfg.cols * elem
     # algorithmic bytes of one streaming pass (X once per pass
@@ -278,7 +285,7 @@ def main():
                   f"{cfg.dtype} X; f64 compute (stage-1 DMMA m8n8k4), f64 stage 2 / ALS"),
         "data": "synthetic (BASELINE.json model, generated on device)",
         "config": {"workload": workload_desc(cfg, args.iters), "entries": total_entries,
-                   "parallelism": f"slice-sharded dp{world} (LPT)" if world > 1 else "single GPU",
+                   "parallelism": f"slice-sharded dp{world} (LPT)" if sharded else "single GPU",
                    "l2": "inputs larger than L2 (X %.1f GB >> 126 MB)" % (x_bytes / 1e9)},
         "gpu_launches": launches,
         "clocks": clk,
@@ -299,15 +306,15 @@ def main():
                          "omega_host": float(np.mean([t["omega_host_s"] for t in tms])) * 1e3},
     }
     # ---- end-to-end through the public API from pinned host buffers
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e(tensor, cfg, opts, args)
+    if not args.no_e2e:
+        line["e2e"] = e2e_sharded(runner, cfg, opts, args) if sharded else e2e(tensor, cfg, opts, args)
     if not args.no_cpu and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline(tensor, cfg, args)
     if args.also_f64 and world == 1:
         line["f64"] = f64_sub(args, opts)
     if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if sharded:
         dist.destroy_process_group()
 
 
@@ -340,6 +347,48 @@ def e2e(tensor, cfg, opts, args):
     return {"value": N * cfg.cols / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "seconds_per_step": sec, "steps": steps,
             "timing": "wall clock around IrregularTensor(pinned host slices) + fit_dpar2 -> NumPy, synced"}
+
+
+def e2e_sharded(runner, cfg, opts, args):
+    """End to end at N ranks: every rank builds an IrregularTensor over its own
+    pinned host slices, fits jointly (stage-1 upload inside the timed region),
+    and copies its factors (its Q slices, H, V, its W rows) back to NumPy.
+    The step time is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2203_12798_b200 as dp
+    tensor = runner.tensor
+    host = torch.empty(tuple(tensor.X.shape), dtype=tensor.X.dtype, pin_memory=True)
+    host.copy_(tensor.X)
+    views = [host[a:b, :cfg.cols] for a, b in zip(tensor.row_off_host[:-1], tensor.row_off_host[1:])]
+    R = cfg.rank
+    steps = max(1, min(args.steps, 3))
+    times = []
+    for i in range(steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        t = dp.IrregularTensor(views, dtype=cfg.dtype)
+        f, tr = runner.fit(R, opts, tensor=t)
+        f.numpy()
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        if i > 0:
+            times.append(float(dt.item()))
+        del t
+    N = runner.local_rows
+    K = runner.K
+    elem = 4 if cfg.dtype == "f32" else 8
+    from paper_2203_12798_b200.linalg import padded_width
+    sp = padded_width(cfg.rank + 10)
+    # per rank: its X slices + Omega for them; replicated stage-2 Omega
+    h2d = N * cfg.cols * elem + len(runner.local_ids) * cfg.cols * sp * 8 + K * 10 * R * 8
+    d2h = (N * R + R * R + cfg.cols * R + len(runner.local_ids) * R + args.iters * 2) * 8
+    sec = float(np.mean(times))
+    return {"value": runner.total_entries / sec, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "seconds_per_step": sec, "steps": steps, "per_rank_bytes": True,
+            "timing": "wall clock, max over ranks, around IrregularTensor(pinned host shard) + joint fit -> NumPy"}
 
 
 def cpu_baseline(tensor, cfg, args):
@@ -381,5 +430,19 @@ def f64_sub(args, opts):
             "sketch_pass_ms": float(np.mean([(t["stage1_sketch1_ms"] + t["stage1_sketch2_ms"]) / 2 for t in tms]))}
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the real stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 if __name__ == "__main__":
+    # stdout carries exactly one JSON line: anything else written to fd 1 by
+    # libraries (NCCL's version banner, warnings) goes to stderr instead
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     main()

@@ -208,7 +208,8 @@ _ST_INDEX = (slice(0, 1), slice(2, 4))
 _ST_COUNT = (slice(1, 2), slice(4, 8))
 
 
-def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None, speculative=False):
+def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None, speculative=False,
+                       slice_ids=None):
     """Stage 1 overlapped with the tensor's chunked upload: Omega for all
     slices first (independent of X), then per upload chunk of whole slices the
     compute stream waits for that chunk's copy event (device-side) and runs
@@ -233,9 +234,10 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
     rstats = {}
     check = None
     if speculative and _uses_tc(subs[0][2], sp):
-        omega, check = omega_device(base.seed, J, widths, sp, dev, speculative=True, s_dev=s_dev)
+        omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True,
+                                    s_dev=s_dev)
     else:
-        omega = omega_device(base.seed, J, widths, sp, dev, stats=rstats, s_dev=s_dev)
+        omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats, s_dev=s_dev)
     t_omega = time.perf_counter() - t0
     A = torch.empty((int(off[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)

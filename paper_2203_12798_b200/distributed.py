@@ -43,17 +43,29 @@ def shard_slices(row_counts, world):
     return [sorted(s) for s in plan.sets], plan.loads
 
 
-def assemble_m(M_local, local_ids, K, R, group=None):
-    """Exact J x KR M in global slice order from each rank's J x K_local R blocks."""
+def assemble_m(M_local, local_ids, K, R, group=None, cols=None):
+    """Exact J x KR M in global slice order from each rank's J x K_local R blocks
+    (``cols``: the device column index of the local blocks, see ``m_columns``)."""
     J = M_local.shape[0]
     full = torch.zeros((J, K * R), dtype=M_local.dtype, device=M_local.device)
     if len(local_ids):
-        cols = (torch.as_tensor(local_ids, device=M_local.device)[:, None] * R +
-                torch.arange(R, device=M_local.device)[None, :]).reshape(-1)
+        if cols is None:
+            cols = m_columns(local_ids, R, M_local.device)
         full[:, cols] = M_local
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(full, group=group)
     return full
+
+
+def m_columns(local_ids, R, device):
+    """Device index of the local slices' columns of M (rows of F): k R + r.
+    Built from pinned memory (a pageable copy would synchronise the stream)."""
+    from .tensor import to_device_async
+    ids = np.asarray(local_ids, dtype=np.int64)
+    cols = (ids[:, None] * R + np.arange(R, dtype=np.int64)[None, :]).reshape(-1)
+    if torch.device(device).type != "cuda":
+        return torch.from_numpy(cols)
+    return to_device_async(cols, torch.int64, device)
 
 
 def local_rows(F, local_ids, R):
@@ -67,12 +79,12 @@ def replicated_als(F, D, E, K, J, R, h, v, w, max_iters, tol, normalize):
     """The single-GPU ALS loop (``dp2_als_run``: one cooperative launch for
     R <= 16) on the FULL compressed tensor (global K); returns device H, V, W
     (K x R), polar (K x R x R), trace, tstamp, iters, status."""
-    from .tensor import new_status
+    from .tensor import new_status, to_device_async
     dev = D.device
     lib = _lib.lib()
-    H = torch.from_numpy(np.ascontiguousarray(h)).to(dev)
-    V = torch.from_numpy(np.ascontiguousarray(v)).to(dev)
-    W = torch.from_numpy(np.ascontiguousarray(w)).to(dev)
+    H = to_device_async(np.ascontiguousarray(h), torch.float64, dev)
+    V = to_device_async(np.ascontiguousarray(v), torch.float64, dev)
+    W = to_device_async(np.ascontiguousarray(w), torch.float64, dev)
     polar = torch.empty((K, R, R), dtype=torch.float64, device=dev)
     trace = torch.zeros(max_iters, dtype=torch.float64, device=dev)
     tstamp = torch.zeros(max_iters + 1, dtype=torch.int64, device=dev)
@@ -160,45 +172,71 @@ class DistributedFit:
         self.K = cfg.num_slices
         self.loads = loads
 
-    def fit(self, R, opts, timings=None, als="replicated"):
-        from .compress import check_status, run_stage1, run_stage2, stage2_params
+    def fit(self, R, opts, timings=None, als="replicated", tensor=None, _exact_omega=False):
+        """Fit the whole tensor with this rank's slices from ``tensor`` (default:
+        the device-resident shard; a host-backed ``IrregularTensor`` of the same
+        slices is uploaded in chunks overlapped with stage 1, as in
+        ``fit_dpar2``).  Like ``fit_dpar2`` the fit is enqueued without host
+        synchronisation (speculative stage-1 Omega, index tensors from pinned
+        memory) and synchronises once at the end; a speculative-Omega mismatch
+        on ANY rank (agreed by one allreduce) makes every rank redo exactly."""
+        from .compress import check_status, run_stage1, run_stage1_chunked, run_stage2, stage2_params
         from .factors import FitTrace, Parafac2Factors, SliceViews, initial_factors
         from .linalg import RsvdParams
         from .rng import stage2_omega
         from .solver import assemble_q
-        t = self.tensor
+        from .tensor import to_device_async
+        t = self.tensor if tensor is None else tensor
         J, K = t.num_cols, self.K
+        dev = t.X.device
+        if getattr(self, "_dev_index", None) is None or self._dev_index[0] != (R, dev):
+            self._dev_index = ((R, dev), m_columns(self.local_ids, R, dev),
+                               to_device_async(np.asarray(self.local_ids, dtype=np.int64), torch.int64, dev))
+        _, cols, ids = self._dev_index
         base = RsvdParams(rank=R, seed=opts.seed)
         second, s2 = stage2_params(base, None, R, K, J)
-        om2 = stage2_omega(second.seed, K * R, s2)
         started = time.perf_counter()
-        A, M_local, rank_found, status = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings)
-        M = assemble_m(M_local, self.local_ids, K, R)
+        spec = not _exact_omega
+        if len(t._upload_events) > 1:
+            res = run_stage1_chunked(t, R, base, timings=timings, speculative=spec, slice_ids=self.local_ids)
+        else:
+            res = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings, speculative=spec)
+        A, M_local, rank_found, status = res[:4]
+        check = res[4] if len(res) > 4 else None
+        om2 = stage2_omega(second.seed, K * R, s2)  # host, while stage 1 runs
+        M = assemble_m(M_local, self.local_ids, K, R, cols=cols)
         D, E, F = run_stage2(M, J, K * R, R, second.seed, s2, om2, status, timings=timings)
-        dev = D.device
         normalize = bool(opts.normalize) if opts.normalize is not None else True
-        ids = torch.as_tensor(self.local_ids, device=dev)
         if als == "replicated":
             h, v, w = initial_factors(J, K, R, opts.seed)
             H, V, W, polar, trace, tstamp, iters, st_als = replicated_als(
                 F, D, E, K, J, R, h, v, w, opts.max_iters, opts.tol, normalize)
-            torch.cuda.synchronize()
-            check_status(status, "compress")
-            check_status(st_als, "fit_dpar2")
             polar_local = polar.index_select(0, ids)
             W_out = W.index_select(0, ids)
         else:
-            check_status(status, "compress")
             h, v, w = initial_factors(J, len(self.local_ids), R, opts.seed)
             H, V = torch.from_numpy(h).to(dev), torch.from_numpy(v).to(dev)
             W = torch.from_numpy(w).to(dev)
             ops = GpuAlsOps(local_rows(F, self.local_ids, R), D, E, H, V, W, J, R, opts.max_iters, opts.tol,
                             normalize)
-            torch.cuda.synchronize()
             ShardedALS(ops, nccl_allreduce()).run(opts.max_iters)
-            check_status(ops.status, "fit_dpar2")
+            st_als = ops.status
             H, V, W_out, polar_local = ops.H, ops.V, ops.W, ops.polar
             trace, tstamp, iters = ops.trace, ops.tstamp, ops.iters
+        from .compress import CompressedTensor
+        comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
+        Q = assemble_q(t, comp, polar_local.contiguous())
+        torch.cuda.current_stream().synchronize()
+        t._upload_keep = None
+        mismatch = bool(check.result()["omega_mismatch"]) if check is not None else False
+        if dist.is_initialized() and dist.get_world_size() > 1:
+            flag = torch.tensor([int(mismatch)], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            mismatch = bool(flag.item())
+        if mismatch:
+            return self.fit(R, opts, timings, als, tensor, _exact_omega=True)
+        check_status(status, "compress")
+        check_status(st_als, "fit_dpar2")
         pre = time.perf_counter() - started
         n = int(iters.item())
         tr = FitTrace(objective=trace[:n].cpu().tolist(),
@@ -207,9 +245,6 @@ class DistributedFit:
         if n >= 2:
             prev, e = tr.objective[-2], tr.objective[-1]
             tr.converged = bool(prev == 0.0 or abs(prev - e) <= opts.tol * prev)
-        from .compress import CompressedTensor
-        comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
-        Q = assemble_q(t, comp, polar_local.contiguous())
         bounds = t.row_off_host
         factors = Parafac2Factors(H=H, V=V, W=W_out, Q=SliceViews(Q, bounds), Q_packed=Q)
         return factors, tr
