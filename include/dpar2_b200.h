@@ -168,6 +168,15 @@ size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank);
 int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
                int32_t rank, double* A_out, double* M_out, int32_t* rank_out, void* ws,
                size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
+/* dp2_stage1 with the column signs of A (P/linalg.py:42-49 sign rule)
+ * deferred: A_out holds A_k up to column signs and a_signs_out (K x rank)
+ * the signs, A_k(reference) = A_out_k diag(a_signs_out[k]) exactly (+1 for
+ * completed columns of rank-deficient slices).  M_out is identical to
+ * dp2_stage1's.  Saves the sign pass over A when the consumer can fold the
+ * signs (dp2_assemble_q_signed). */
+int dp2_stage1_signs(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
+                     int32_t rank, double* A_out, double* M_out, int32_t* rank_out, double* a_signs_out,
+                     void* ws, size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
 
 /* One streaming pass of stage 1 (the two sketch products of
  * P/linalg.py:124-127 fused per piece): for every piece p (segment x slice)
@@ -245,6 +254,10 @@ int dp2_convergence_metric(const double* theta, const double* D, const double* E
  * Q_k = A_k (Z_k P_k^T) for every slice (P/solver.py:186-189). */
 int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar,
                    double* Q_out, void* stream);
+/* dp2_assemble_q for an A from dp2_stage1_signs: Q_k = A_k diag(a_signs[k]) Pi_k
+ * (bit-identical to dp2_assemble_q on the signed A). */
+int dp2_assemble_q_signed(const dp2_store* st, const double* A, int32_t R, const double* a_signs,
+                          const double* polar, double* Q_out, void* stream);
 /* fitness terms (P/analysis.py:23-45): out2_dev[0] = sum ||X_k||^2,
  * out2_dev[1] = sum ||X_k - Q_k (H * w_k) V^T||^2, fixed-order reductions. */
 size_t dp2_fitness_workspace(const dp2_store* st);

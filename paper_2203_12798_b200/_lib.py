@@ -57,6 +57,8 @@ _SIGS = {
     "dp2_stage1_workspace": (c_sz, [P(Store), c_i32, c_i32]),
     "dp2_stage1": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
                            P(c_f32), c_vp]),
+    "dp2_stage1_signs": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
+                                 P(c_f32), c_vp]),
     "dp2_stage2_workspace": (c_sz, [c_i64, c_i64, c_i32, c_i32]),
     "dp2_stage2": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "dp2_als_workspace": (c_sz, [c_i64, c_i64, c_i32]),
@@ -74,6 +76,7 @@ _SIGS = {
     "dp2_convergence_metric": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_sz, c_vp]),
     "dp2_assemble_q": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "dp2_assemble_q_signed": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "dp2_fitness_workspace": (c_sz, [P(Store)]),
     "dp2_fitness": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
 }

@@ -44,6 +44,10 @@ class CompressedTensor:
     weights: torch.Tensor      # E
     cores: torch.Tensor        # F
     rank_found: torch.Tensor | None = None
+    # fit-internal compressions (compress_async(defer_signs=True)): A is held
+    # up to column signs, A_k(reference) = A_k diag(a_signs[k]); assemble_q
+    # folds them into the polar factors.  None: A is the reference's A.
+    a_signs: torch.Tensor | None = None
 
     @property
     def num_slices(self):
@@ -152,12 +156,13 @@ def _uses_tc(sub, sp):
 
 
 def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, timings=None, status=None,
-               speculative=False):
+               speculative=False, a_signs=None):
     """Stage 1 on the device for the tensor's slices (global ids ``slice_ids``
     select the per-slice seeds in a multi-GPU shard).  Returns A (sum I_k x R),
     M (J x K_local R, local slice order) and the per-slice numerical ranks
     (plus, with ``speculative``, the Omega replay check future or None --
-    rng.omega_device)."""
+    rng.omega_device).  With ``a_signs`` (device K x rank) A is returned up to
+    its column signs, which go to ``a_signs`` (dp2_stage1_signs)."""
     if base.power_iters != 1:
         raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
@@ -176,7 +181,7 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
     status = new_status(dev) if status is None else status
-    tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None)
+    tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None, a_signs)
     if timings is not None:
         timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
@@ -187,7 +192,7 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     return A, M, rank_found, status
 
 
-def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False):
+def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False, a_signs=None):
     """One dp2_stage1 call over ``tensor``'s slices (omega / s_dev / outputs
     already sliced to them); returns the phase timings when ``timed``."""
     nseg = nseg_for(tensor)
@@ -195,8 +200,13 @@ def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed
     lib = _lib.lib()
     ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), tensor.X.device)
     tm = (C.c_float * 8)() if timed else None
-    _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
-                              _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
+    if a_signs is None:
+        _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
+                                  _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
+    else:
+        _lib.check(lib.dp2_stage1_signs(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M),
+                                        _vp(rank_found), _vp(a_signs), _vp(ws), ws.numel(), _vp(status), tm,
+                                        stream_ptr()), "stage1")
     del keep, ws
     return tm
 
@@ -209,7 +219,7 @@ _ST_COUNT = (slice(1, 2), slice(4, 8))
 
 
 def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=None, speculative=False,
-                       slice_ids=None):
+                       slice_ids=None, a_signs=None):
     """Stage 1 overlapped with the tensor's chunked upload: Omega for all
     slices first (independent of X), then per upload chunk of whole slices the
     compute stream waits for that chunk's copy event (device-side) and runs
@@ -248,7 +258,8 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
         r0, r1 = int(off[k0]), int(off[k1])
         Mc = torch.empty((J, (k1 - k0) * rank), dtype=torch.float64, device=dev)
         st_c = new_status(dev)
-        _stage1_call(sub, rank, omega[k0:k1], s_dev[k0:k1], sp, A[r0:r1], Mc, rank_found[k0:k1], st_c)
+        _stage1_call(sub, rank, omega[k0:k1], s_dev[k0:k1], sp, A[r0:r1], Mc, rank_found[k0:k1], st_c,
+                     a_signs=None if a_signs is None else a_signs[k0:k1])
         M[:, k0 * rank:k1 * rank].copy_(Mc)
         for sl in _ST_INDEX:
             idx = st_c[sl]
@@ -308,10 +319,11 @@ def omega_mismatch(comp):
 
 
 def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
-                   plan=None, threads=None, timings=None, exact_omega=False):
+                   plan=None, threads=None, timings=None, exact_omega=False, defer_signs=False):
     """``compress`` without the host synchronisation of its status check:
     returns (CompressedTensor, device status block); the caller checks the
-    status (check_status) once its later work is enqueued."""
+    status (check_status) once its later work is enqueued.  ``defer_signs``
+    (fit-internal): A is left up to its column signs (``comp.a_signs``)."""
     if not isinstance(tensor, IrregularTensor):
         tensor = IrregularTensor(tensor)
     checked = tensor.__dict__.setdefault("_rank_ok", set())
@@ -323,10 +335,11 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     J, K = tensor.num_cols, tensor.num_slices
     second, s2 = stage2_params(base, stage2, rank, K, J)
     spec = not exact_omega
+    a_signs = torch.empty((K, rank), dtype=torch.float64, device=tensor.X.device) if defer_signs else None
     if len(tensor._upload_events) > 1:
-        res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec)
+        res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
     else:
-        res = run_stage1(tensor, rank, base, timings=timings, speculative=spec)
+        res = run_stage1(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
     A, M, rank_found, status = res[:4]
     check = res[4] if len(res) > 4 else None
     # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on the
@@ -334,7 +347,7 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     om2 = stage2_omega(second.seed, K * rank, s2)
     D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2, status, timings=timings)
     comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
-                            cores=F, rank_found=rank_found)
+                            cores=F, rank_found=rank_found, a_signs=a_signs)
     comp._omega_check = check
     return comp, status
 

@@ -283,20 +283,37 @@ size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
   return dp2::stage1_layout(st, sp, rank).total;
 }
 
-int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
-               double* A_out, double* M_out, int32_t* rank_out, void* ws, size_t ws_bytes,
-               int64_t* status_dev, float* timing_ms, void* stream) {
+static int stage1_impl(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
+                       int32_t rank, double* A_out, double* M_out, int32_t* rank_out, void* ws, size_t ws_bytes,
+                       int64_t* status_dev, float* timing_ms, void* stream, double* a_signs) {
   if (!store_ok(st)) return fail_arg("invalid store");
   if (rank < 1 || rank > 64 || sp < rank || sp % 8 != 0 || (sp > 32 && sp % 32 != 0) || sp > 256)
     return fail_arg("invalid rank / sketch width");
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
-                                  static_cast<char*>(ws), status_dev, timing_ms, S(stream));
+                                  static_cast<char*>(ws), status_dev, timing_ms, S(stream), a_signs);
   // sp <= 32: 2 streaming passes + orth (Gram, Cholesky, substitution, CGS2
-  // fallback) + gather, factor, argmax, signs, write_a, complete; the
-  // tensor-core pass adds its two B-image kernels and gram_y_piece_kernel
+  // fallback) + gather, factor, A + candidates, signs, [apply signs],
+  // complete; the tensor-core pass adds its two B-image kernels and
+  // gram_y_piece_kernel.  sp > 32: 8 kernels [+ the sign fill].
   const int tc = dp2::sketch_tc_eligible(st, sp) ? 3 : 0;
-  return e == cudaSuccess ? ok((sp <= 32 ? 12 : 8) + tc) : fail(e, "dp2_stage1");
+  const int n = sp <= 32 ? (a_signs ? 11 : 12) + tc : (a_signs ? 9 : 8);
+  return e == cudaSuccess ? ok(n) : fail(e, "dp2_stage1");
+}
+
+int dp2_stage1(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
+               double* A_out, double* M_out, int32_t* rank_out, void* ws, size_t ws_bytes,
+               int64_t* status_dev, float* timing_ms, void* stream) {
+  return stage1_impl(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out, ws, ws_bytes, status_dev, timing_ms,
+                     stream, nullptr);
+}
+
+int dp2_stage1_signs(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
+                     double* A_out, double* M_out, int32_t* rank_out, double* a_signs_out, void* ws,
+                     size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream) {
+  if (!a_signs_out) return fail_arg("a_signs_out is null");
+  return stage1_impl(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out, ws, ws_bytes, status_dev, timing_ms,
+                     stream, a_signs_out);
 }
 
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {
@@ -385,8 +402,15 @@ int dp2_convergence_metric(const double* theta, const double* D, const double* E
 int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar, double* Q_out,
                    void* stream) {
   if (!store_ok(st) || R < 1 || R > 64) return fail_arg("invalid arguments");
-  cudaError_t e = dp2::run_assemble_q(st, A, R, polar, Q_out, S(stream));
+  cudaError_t e = dp2::run_assemble_q(st, A, R, polar, Q_out, S(stream), nullptr);
   return e == cudaSuccess ? ok(1) : fail(e, "dp2_assemble_q");
+}
+
+int dp2_assemble_q_signed(const dp2_store* st, const double* A, int32_t R, const double* a_signs,
+                          const double* polar, double* Q_out, void* stream) {
+  if (!store_ok(st) || R < 1 || R > 64 || !a_signs) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::run_assemble_q(st, A, R, polar, Q_out, S(stream), a_signs);
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_assemble_q_signed");
 }
 
 size_t dp2_fitness_workspace(const dp2_store* st) { return dp2::fitness_bytes(st); }

@@ -18,12 +18,13 @@ struct Stage1Layout {
 Stage1Layout stage1_layout(const dp2_store* st, int sp, int R);
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
-                       float* timing, cudaStream_t stream);
+                       float* timing, cudaStream_t stream, double* a_signs = nullptr);
 cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, int R, const double* part1,
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch);
+                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch,
+                             double* a_signs);
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                            double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
 bool sketch_tc_eligible(const dp2_store* st, int sp);
@@ -64,7 +65,7 @@ cudaError_t als_metric(const double* theta, const double* D, const double* E, in
                        cudaStream_t stream);
 
 cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const double* polar, double* Q,
-                           cudaStream_t stream);
+                           cudaStream_t stream, const double* a_signs);
 size_t fitness_bytes(const dp2_store* st);
 cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const double* H, const double* V,
                         const double* W, double* out2, char* ws, cudaStream_t stream);

@@ -61,11 +61,13 @@ __global__ void chunk_begin_kernel(const int64_t* row_off, int64_t K, int chunk_
 
 __global__ void __launch_bounds__(256) assemble_q_kernel(const double* A, const int32_t* piece_slice,
                                                           const int64_t* piece_row0, const int32_t* piece_rows,
-                                                          int R, const double* polar, double* Q) {
+                                                          int R, const double* polar, const double* sgn,
+                                                          double* Q) {
   extern __shared__ double pis[];
   const int p = blockIdx.x;
   const int64_t k = piece_slice[p];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) pis[e] = polar[k * R * R + e];
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x)
+    pis[e] = sgn ? sgn[k * R + e / R] * polar[k * R * R + e] : polar[k * R * R + e];
   __syncthreads();
   const int64_t r0 = piece_row0[p], nr = piece_rows[p];
   for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) {
@@ -83,11 +85,14 @@ __global__ void __launch_bounds__(256) assemble_q_kernel(const double* A, const 
 template <int R>
 __global__ void __launch_bounds__(256) assemble_q_rows_kernel(const double* A, const int32_t* piece_slice,
                                                               const int64_t* piece_row0, const int32_t* piece_rows,
-                                                              const double* polar, double* Q) {
+                                                              const double* polar, const double* sgn, double* Q) {
   __shared__ double pis[R * R];
   const int p = blockIdx.x;
   const int64_t k = piece_slice[p];
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) pis[e] = polar[k * R * R + e];
+  // with sgn (the deferred column signs of A, dp2_stage1_signs): row d of
+  // Pi_k times sign d, so unsigned A rows give the signed A's Q exactly
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x)
+    pis[e] = sgn ? sgn[k * R + e / R] * polar[k * R * R + e] : polar[k * R * R + e];
   __syncthreads();
   const int64_t r0 = piece_row0[p];
   const int nr = piece_rows[p];
@@ -210,12 +215,12 @@ cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status
 }
 
 cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const double* polar, double* Q,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, const double* sgn) {
   const unsigned P = (unsigned)st->npieces;
   switch (R) {
 #define DP2_AQ(N)                                                                                             \
   case N:                                                                                                     \
-    assemble_q_rows_kernel<N><<<P, 256, 0, stream>>>(A, st->piece_slice, st->piece_row0, st->piece_rows, polar, Q); \
+    assemble_q_rows_kernel<N><<<P, 256, 0, stream>>>(A, st->piece_slice, st->piece_row0, st->piece_rows, polar, sgn, Q); \
     return cudaGetLastError();
     DP2_AQ(1) DP2_AQ(2) DP2_AQ(3) DP2_AQ(4) DP2_AQ(5) DP2_AQ(6) DP2_AQ(7) DP2_AQ(8) DP2_AQ(9) DP2_AQ(10)
     DP2_AQ(11) DP2_AQ(12) DP2_AQ(13) DP2_AQ(14) DP2_AQ(15) DP2_AQ(16)
@@ -223,7 +228,7 @@ cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const do
     default: break;
   }
   assemble_q_kernel<<<(unsigned)st->npieces, 256, (size_t)R * R * 8, stream>>>(
-      A, st->piece_slice, st->piece_row0, st->piece_rows, R, polar, Q);
+      A, st->piece_slice, st->piece_row0, st->piece_rows, R, polar, sgn, Q);
   return cudaGetLastError();
 }
 

@@ -568,6 +568,11 @@ __global__ void __launch_bounds__(256) assemble_a_kernel(RowsParams prm) {
   }
 }
 
+__global__ void fill_kernel(double* x, int64_t n, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
 // Rank-deficient slices: complete A_k's trailing columns to an orthonormal set.
 __global__ void __launch_bounds__(256) complete_kernel(const int64_t* row_off, const int32_t* rank_out,
                                                         int R, double* A) {
@@ -732,7 +737,7 @@ Stage1Layout stage1_layout(const dp2_store* st, int sp, int R) {
 
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
-                       float* timing, cudaStream_t stream) {
+                       float* timing, cudaStream_t stream, double* a_signs) {
   const Stage1Layout L = stage1_layout(st, sp, R);
   double* part = reinterpret_cast<double*>(ws + L.part);
   double* qz = reinterpret_cast<double*>(ws + L.qz);
@@ -764,7 +769,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
       return run_stage1_small(st, s_dev, sp, R, part, part, gp, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
                               reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
-                              stream, tc, gpart);
+                              stream, tc, gpart, a_signs);
     };
     if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) {
       e = small(0);
@@ -845,6 +850,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
                                       K, J, sp, R, M_out);
   assemble_a_kernel<<<P, 256, 0, stream>>>(rp);
   complete_kernel<<<K, 256, 0, stream>>>(st->row_off, rank_out, R, A_out);
+  if (a_signs) fill_kernel<<<(K * R + 255) / 256, 256, 0, stream>>>(a_signs, (int64_t)K * R, 1.0);  // A is signed
   e = cudaGetLastError();
   if (timing) {
     cudaEventRecord(ev[5], stream);

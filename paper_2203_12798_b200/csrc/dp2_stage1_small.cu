@@ -492,22 +492,28 @@ DP2_DEV void dot_pcol(const Y (&y0)[SP], const Y (&y1)[SP], const double* Pt, in
   a1 = s1;
 }
 
-// ------------------------------------------------------------ argmax candidates of A = Y P
-// Per piece: the column-wise max |A| entry (first row on ties) of A = Y P,
-// without storing A (the signed A is written once the slice's signs are known,
-// write_a_kernel).  One thread per row: the row of Y in registers (16 B
-// loads), R dot products against P in shared memory (broadcast), running
-// per-column best in registers; rows of a thread increase, so strict '>' keeps
-// the first index, and the block merge orders ties by row.
+// ------------------------------------------------------------ A = Y P and its argmax candidates
+// Per piece: A = Y P for its rows, written UNSIGNED (the column signs are
+// applied afterwards by apply_signs_kernel, or deferred to the caller), and
+// the column-wise max |A| entry (first row on ties) as the piece's candidate
+// for the sign rule.  One thread per row pair (rows i, i + 256 of a 512-row
+// tile): the rows of Y in registers (16 B loads), R dot products against P in
+// shared memory (broadcast), each A value both staged for a coalesced store
+// and compared with the thread's running best (shared memory, per column);
+// a thread's rows increase, so strict '>' keeps the first index, and the
+// block merge orders ties by row.  The values written and the values
+// compared are the same doubles, so the sign chosen from a candidate is the
+// sign of the stored entry.
 template <typename Y, int SP>
-__global__ void __launch_bounds__(256) argmax_cand_kernel(const Y* y2, const int64_t* row_off,
-                                                          const int32_t* piece_slice, const int64_t* piece_row0,
-                                                          const int32_t* piece_rows, const int32_t* s_k,
-                                                          const double* Pm, int R, double* cand_abs,
-                                                          int64_t* cand_row, int32_t* cand_neg) {
+__global__ void __launch_bounds__(256) a_cand_kernel(const Y* y2, const int64_t* row_off,
+                                                     const int32_t* piece_slice, const int64_t* piece_row0,
+                                                     const int32_t* piece_rows, const int32_t* s_k,
+                                                     const double* Pm, int R, double* A, double* cand_abs,
+                                                     int64_t* cand_row, int32_t* cand_neg) {
   extern __shared__ __align__(16) double sm[];
   double* Pt = sm;                                   // R x SP (P transposed), entries a >= s zero
-  double* bval = Pt + SP * R;                        // R x 256 signed best values
+  double* at = Pt + SP * R;                          // 512 x R output tile
+  double* bval = at + 512 * R;                       // R x 256 signed best values
   int* brow = reinterpret_cast<int*>(bval + R * 256);  // R x 256 row within the piece
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = piece_slice[p], s = s_k[k];
@@ -519,29 +525,43 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const Y* y2, const int
   }
   for (int c = 0; c < R; ++c) brow[c * 256 + tid] = -1;  // own slots
   __syncthreads();
-  // rows i and i + 256 per step: a thread's rows still increase
-  for (int i = tid; i < nr; i += 512) {
-    const bool two = i + 256 < nr;
-    Y y0[SP], y1[SP];
-    load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
-    if (two) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
-    else {
+  for (int t0 = 0; t0 < nr; t0 += 512) {
+    const int i = t0 + tid;
+    if (i < nr) {
+      const bool two = i + 256 < nr;
+      Y y0[SP], y1[SP];
+      load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
+      if (two) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
+      else {
 #pragma unroll
-      for (int a = 0; a < SP; ++a) y1[a] = (Y)0;
-    }
+        for (int a = 0; a < SP; ++a) y1[a] = (Y)0;
+      }
 #pragma unroll 1
-    for (int c = 0; c < R; ++c) {
-      double a0, a1;
-      dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
-      double bv = bval[c * 256 + tid];
-      int rw = brow[c * 256 + tid];
-      if (rw < 0 || fabs(a0) > fabs(bv)) { bv = a0; rw = i; }
-      if (two && fabs(a1) > fabs(bv)) { bv = a1; rw = i + 256; }
-      bval[c * 256 + tid] = bv;
-      brow[c * 256 + tid] = rw;
+      for (int c = 0; c < R; ++c) {
+        double a0, a1;
+        dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
+        at[tid * R + c] = a0;
+        at[(tid + 256) * R + c] = a1;
+        double bv = bval[c * 256 + tid];
+        int rw = brow[c * 256 + tid];
+        if (rw < 0 || fabs(a0) > fabs(bv)) { bv = a0; rw = i; }
+        if (two && fabs(a1) > fabs(bv)) { bv = a1; rw = i + 256; }
+        bval[c * 256 + tid] = bv;
+        brow[c * 256 + tid] = rw;
+      }
     }
+    __syncthreads();
+    const int rows = min(512, nr - t0);
+    double* dst = A + (r0 + t0) * R;
+    if ((R & 1) == 0) {  // the tile's rows are one contiguous, 16-byte aligned run
+      const int n2 = rows * R / 2;
+      for (int e = tid; e < n2; e += 256)
+        reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(at)[e];
+    } else {
+      for (int e = tid; e < rows * R; e += 256) dst[e] = at[e];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   for (int c = warp; c < R; c += 8) {
     double ba = -1.0, bv = 0.0;
     int br = INT32_MAX;
@@ -566,63 +586,40 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const Y* y2, const int
   }
 }
 
-// A = Y (P * sign) for the rows of a piece (P already signed by signs_m);
-// the same fma order as the candidate pass, so |A| there and here agree.
-// Rows staged through shared memory for coalesced stores.
-template <typename Y, int SP>
-__global__ void __launch_bounds__(256) write_a_kernel(const Y* y2, const int32_t* piece_slice,
-                                                      const int64_t* piece_row0, const int32_t* piece_rows,
-                                                      const int32_t* s_k, const double* Pm, int R, double* A) {
-  extern __shared__ __align__(16) double sm[];
-  double* Pt = sm;            // R x SP (P transposed)
-  double* at = Pt + SP * R;   // 512 x R output tile
+// A rows of a piece *= the slice's column signs (in place, 16 B when R is even).
+__global__ void __launch_bounds__(256) apply_signs_kernel(const int32_t* piece_slice, const int64_t* piece_row0,
+                                                          const int32_t* piece_rows, const double* sgn, int R,
+                                                          double* A) {
+  __shared__ double sg[64];
   const int p = blockIdx.x, tid = threadIdx.x;
-  const int k = piece_slice[p], s = s_k[k];
-  const int64_t r0 = piece_row0[p];
-  const int nr = piece_rows[p];
-  for (int i = tid; i < SP * R; i += 256) {
-    const int c = i / SP, a = i - c * SP;
-    Pt[i] = a < s ? Pm[(size_t)k * SP * R + a * R + c] : 0.0;
-  }
+  const int k = piece_slice[p];
+  if (tid < R) sg[tid] = sgn[(size_t)k * R + tid];
   __syncthreads();
-  for (int t0 = 0; t0 < nr; t0 += 512) {
-    const int i = t0 + tid;
-    if (i < nr) {
-      Y y0[SP], y1[SP];
-      load_y_row<Y, SP>(y2 + (r0 + i) * SP, s, y0);
-      if (i + 256 < nr) load_y_row<Y, SP>(y2 + (r0 + i + 256) * SP, s, y1);
-      else {
-#pragma unroll
-        for (int a = 0; a < SP; ++a) y1[a] = (Y)0;
-      }
-#pragma unroll 1
-      for (int c = 0; c < R; ++c) {
-        double a0, a1;
-        dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
-        at[tid * R + c] = a0;
-        at[(tid + 256) * R + c] = a1;
-      }
+  double* a = A + piece_row0[p] * R;
+  const int64_t n = (int64_t)piece_rows[p] * R;
+  if ((R & 1) == 0) {
+    double2* a2 = reinterpret_cast<double2*>(a);
+    for (int64_t e = tid; e < n / 2; e += 256) {
+      const int c = (int)((2 * e) % R);
+      double2 v = a2[e];
+      v.x *= sg[c];
+      v.y *= sg[c + 1];
+      a2[e] = v;
     }
-    __syncthreads();
-    const int rows = min(512, nr - t0);
-    double* dst = A + (r0 + t0) * R;
-    if ((R & 1) == 0) {  // the block's rows are one contiguous, 16-byte aligned run
-      const int n2 = rows * R / 2;
-      for (int e = tid; e < n2; e += 256)
-        reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(at)[e];
-    } else {
-      for (int e = tid; e < rows * R; e += 256) dst[e] = at[e];
-    }
-    __syncthreads();
+  } else {
+    for (int64_t e = tid; e < n; e += 256) a[e] *= sg[e % R];
   }
 }
 
 // ------------------------------------------------------------ signs + M
 template <int SP>
+// sgn_out[k][r]: the sign A's column r takes (the candidate's sign for r below
+// the slice's numerical rank, +1 for the columns complete_kernel replaces);
+// P and M take the candidate's sign for every column.
 __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece, const double* cand_abs,
                                                        const int64_t* cand_row, const int32_t* cand_neg,
                                                        double* Pm, const double* Ct, int K, int J, int sp, int R,
-                                                       double* sgn_out, double* M) {
+                                                       const int32_t* rank_found, double* sgn_out, double* M) {
   extern __shared__ __align__(16) double sm[];
   double* Ps = sm;  // sp x R (signed)
   __shared__ double sgn[64];
@@ -638,7 +635,7 @@ __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece
       if (va > ba || (va == ba && ra < br)) { ba = va; br = ra; bn = cand_neg[(size_t)p * R + r]; }
     }
     sgn[r] = bn ? -1.0 : 1.0;
-    sgn_out[(size_t)k * R + r] = sgn[r];
+    sgn_out[(size_t)k * R + r] = r < rank_found[k] ? sgn[r] : 1.0;
   }
   __syncthreads();
   double* Pk = Pm + (size_t)k * sp * R;
@@ -679,7 +676,7 @@ template <int SP>
 cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const double* part2, const double* gpart,
                    double* gscratch, double* Gg, double* CCg, double* Ct, const double* y2, bool y32, double* Pm,
                    double* Sv, double* sgn, double* cand_abs, int64_t* cand_row, int32_t* cand_neg, double* A,
-                   double* M, int32_t* rank_out, int64_t* status, cudaStream_t stream) {
+                   double* M, int32_t* rank_out, int64_t* status, cudaStream_t stream, double* a_signs) {
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
   cudaError_t e = cudaSuccess;
   if (!gpart) {  // tensor-core pass: G partials per piece from its fp32 Y rows
@@ -710,32 +707,26 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
   if (e != cudaSuccess) return e;
   factor_warp_kernel<SP><<<(K + wpb - 1) / wpb, 32 * wpb, fs, stream>>>(Gg, CCg, s_dev, K, SP, R, Pm, Sv, rank_out,
                                                                           status);
-  const size_t as = ((size_t)SP * R + (size_t)R * 256) * 8 + (size_t)R * 256 * 4;
-  const size_t ws = ((size_t)SP * R + 512 * (size_t)R) * 8;
+  // A unsigned + candidates -> signs (and signed P, M) -> A signs applied,
+  // unless the caller takes them (a_signs: A stays unsigned)
+  const size_t as = ((size_t)SP * R + 512 * (size_t)R + (size_t)R * 256) * 8 + (size_t)R * 256 * 4;
+  double* sA = a_signs ? a_signs : sgn;
   if (y32) {
-    const float* y = reinterpret_cast<const float*>(y2);
-    e = cudaFuncSetAttribute(argmax_cand_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(write_a_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+    e = cudaFuncSetAttribute(a_cand_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
     if (e != cudaSuccess) return e;
-    argmax_cand_kernel<float, SP><<<P, 256, as, stream>>>(y, st->row_off, st->piece_slice, st->piece_row0,
-                                                         st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
-    signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
-                                                            J, SP, R, sgn, M);
-    write_a_kernel<float, SP><<<P, 256, ws, stream>>>(y, st->piece_slice, st->piece_row0, st->piece_rows, s_dev, Pm,
-                                                     R, A);
+    a_cand_kernel<float, SP><<<P, 256, as, stream>>>(reinterpret_cast<const float*>(y2), st->row_off,
+                                                     st->piece_slice, st->piece_row0, st->piece_rows, s_dev, Pm, R,
+                                                     A, cand_abs, cand_row, cand_neg);
   } else {
-    e = cudaFuncSetAttribute(argmax_cand_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(write_a_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ws);
+    e = cudaFuncSetAttribute(a_cand_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
     if (e != cudaSuccess) return e;
-    argmax_cand_kernel<double, SP><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0,
-                                                          st->piece_rows, s_dev, Pm, R, cand_abs, cand_row, cand_neg);
-    signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
-                                                            J, SP, R, sgn, M);
-    write_a_kernel<double, SP><<<P, 256, ws, stream>>>(y2, st->piece_slice, st->piece_row0, st->piece_rows, s_dev,
-                                                      Pm, R, A);
+    a_cand_kernel<double, SP><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0,
+                                                      st->piece_rows, s_dev, Pm, R, A, cand_abs, cand_row, cand_neg);
   }
+  signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
+                                                          J, SP, R, rank_out, sA, M);
+  if (!a_signs)
+    apply_signs_kernel<<<P, 256, 0, stream>>>(st->piece_slice, st->piece_row0, st->piece_rows, sA, R, A);
   return cudaGetLastError();
 }
 
@@ -743,7 +734,8 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
                              int64_t* cand_row, int32_t* cand_neg, double* A, double* M, int32_t* rank_out,
-                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch) {
+                             int64_t* status, int phase, cudaStream_t stream, bool y32, double* gscratch,
+                             double* a_signs) {
   const int K = (int)st->K, J = (int)st->J;
   cudaError_t e = cudaSuccess;
   if (phase == 0) {  // between the passes
@@ -765,10 +757,10 @@ cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, 
     return cudaGetLastError();
   }
   switch (sp) {
-    case 8: return post_t<8>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 16: return post_t<16>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 24: return post_t<24>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
-    case 32: return post_t<32>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream);
+    case 8: return post_t<8>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream, a_signs);
+    case 16: return post_t<16>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream, a_signs);
+    case 24: return post_t<24>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream, a_signs);
+    case 32: return post_t<32>(st, s_dev, R, part2, gpart, gscratch, Gg, CCg, Ct, y2, y32, Pm, Sv, sgn, cand_abs, cand_row, cand_neg, A, M, rank_out, status, stream, a_signs);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -197,10 +197,13 @@ class DistributedFit:
         second, s2 = stage2_params(base, None, R, K, J)
         started = time.perf_counter()
         spec = not _exact_omega
+        a_signs = torch.empty((t.num_slices, R), dtype=torch.float64, device=dev)  # folded into Q's Pi_k
         if len(t._upload_events) > 1:
-            res = run_stage1_chunked(t, R, base, timings=timings, speculative=spec, slice_ids=self.local_ids)
+            res = run_stage1_chunked(t, R, base, timings=timings, speculative=spec, slice_ids=self.local_ids,
+                                     a_signs=a_signs)
         else:
-            res = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings, speculative=spec)
+            res = run_stage1(t, R, base, slice_ids=self.local_ids, timings=timings, speculative=spec,
+                             a_signs=a_signs)
         A, M_local, rank_found, status = res[:4]
         check = res[4] if len(res) > 4 else None
         om2 = stage2_omega(second.seed, K * R, s2)  # host, while stage 1 runs
@@ -224,7 +227,8 @@ class DistributedFit:
             H, V, W_out, polar_local = ops.H, ops.V, ops.W, ops.polar
             trace, tstamp, iters = ops.trace, ops.tstamp, ops.iters
         from .compress import CompressedTensor
-        comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F)
+        comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F,
+                                a_signs=a_signs)
         Q = assemble_q(t, comp, polar_local.contiguous())
         torch.cuda.current_stream().synchronize()
         t._upload_keep = None

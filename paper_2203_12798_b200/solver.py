@@ -183,8 +183,12 @@ def assemble_q(tensor: IrregularTensor, comp: CompressedTensor, polar, nseg=None
     nseg = nseg or nseg_for(tensor)
     st, keep = tensor.store(nseg)
     Q = torch.empty_like(comp.A)
-    _lib.check(_lib.lib().dp2_assemble_q(C.byref(st), _vp(comp.A), comp.rank, _vp(polar), _vp(Q), stream_ptr()),
-               "assemble_q")
+    if comp.a_signs is None:
+        _lib.check(_lib.lib().dp2_assemble_q(C.byref(st), _vp(comp.A), comp.rank, _vp(polar), _vp(Q), stream_ptr()),
+                   "assemble_q")
+    else:  # A held up to column signs (compress_async(defer_signs=True)): folded into Pi_k
+        _lib.check(_lib.lib().dp2_assemble_q_signed(C.byref(st), _vp(comp.A), comp.rank, _vp(comp.a_signs),
+                                                    _vp(polar), _vp(Q), stream_ptr()), "assemble_q")
     del keep
     return Q
 
@@ -211,7 +215,7 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     started = time.perf_counter()
     ev0.record()
     comp, cstatus = compress_async(tensor, rank, rsvd=RsvdParams(rank=rank, seed=opts.seed), timings=timings,
-                                   exact_omega=_exact_omega)
+                                   exact_omega=_exact_omega, defer_signs=True)
     ev1.record()
     cstatus_h = torch.empty(tuple(cstatus.shape), dtype=cstatus.dtype, pin_memory=True)
     cstatus_h.copy_(cstatus, non_blocking=True)

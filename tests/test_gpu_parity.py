@@ -295,3 +295,40 @@ def test_speculative_omega_redo_path(monkeypatch):
     assert calls == [True, False]  # speculative first, exact (no check) on the redo
     for key in ("H", "V", "W"):
         assert rel_signed(getattr(g, key), getattr(f, key)) <= 1e-6, key
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_deferred_signs_bit_identical(dtype):
+    """dp2_stage1_signs (the fit path) leaves A up to its column signs; the
+    signs applied to it reproduce dp2_stage1's A bit for bit (including a
+    rank-deficient slice whose completed columns keep sign +1), M is the same,
+    and dp2_assemble_q_signed gives dp2_assemble_q's Q on the signed A."""
+    import torch
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200.compress import run_stage1
+    from paper_2203_12798_b200.linalg import RsvdParams
+    from paper_2203_12798_b200.solver import assemble_q
+    rng = np.random.default_rng(11)
+    xs = [rng.standard_normal((int(m), 40)) for m in rng.integers(30, 700, size=12)]
+    xs[4] = np.outer(rng.standard_normal(50), rng.standard_normal(40))  # rank 1 < R
+    xs = [x.astype(np.float32) for x in xs] if dtype == "f32" else xs
+    t = dp.IrregularTensor(xs, dtype=dtype)
+    R, K = 6, len(xs)
+    base = RsvdParams(rank=R, seed=3)
+    A, M, rk, st = run_stage1(t, R, base)
+    sg = torch.empty((K, R), dtype=torch.float64, device="cuda")
+    A2, M2, rk2, st2 = run_stage1(t, R, base, a_signs=sg)
+    torch.cuda.synchronize()
+    if dtype == "f64":  # in fp32 the rank-1 slice's rounding noise counts as rank
+        assert int(rk[4]) < R
+    assert torch.equal(M, M2) and torch.equal(rk, rk2)
+    rows = torch.as_tensor([x.shape[0] for x in xs], device="cuda")
+    s_rows = sg.repeat_interleave(rows, dim=0)
+    assert torch.equal(A2 * s_rows, A)
+    assert bool((sg.abs() == 1).all()) and bool((sg[4, int(rk[4]):] == 1).all())
+    polar = torch.linalg.qr(torch.randn((K, R, R), dtype=torch.float64, device="cuda"))[0].contiguous()
+    comp = dp.compress(t, R, rsvd=base)
+    comp2 = type(comp)(rank=R, A=A2, row_off=comp.row_off, col_basis=comp.col_basis, weights=comp.weights,
+                       cores=comp.cores, a_signs=sg)
+    assert torch.equal(comp.A, A)
+    assert torch.equal(assemble_q(t, comp2, polar), assemble_q(t, comp, polar))
