@@ -184,8 +184,10 @@ int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev
   static_assert(sizeof(dp2_tail_record) == 88, "record layout");
   if (K < 1 || J < 1 || sp < 1 || cap < 0) return fail_arg("invalid omega shape");
   if (dp2::tail_record_bytes() != sizeof(dp2_tail_record)) return fail_arg("record layout mismatch");
-  cudaError_t e = dp2::run_omega(seed, K, J, s_dev, sp, slice_ids_dev, out, recs, cap, nrec_dev, redo_dev, S(stream));
-  return e == cudaSuccess ? ok(1) : fail(e, "dp2_omega_generate");
+  int launches = 0;
+  cudaError_t e = dp2::run_omega(seed, K, J, s_dev, sp, slice_ids_dev, out, recs, cap, nrec_dev, redo_dev, S(stream),
+                                 &launches);
+  return e == cudaSuccess ? ok(launches) : fail(e, "dp2_omega_generate");
 }
 
 int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok_out) {

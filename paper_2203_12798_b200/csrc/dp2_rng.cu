@@ -6,8 +6,8 @@
 //   SeedSequence(derived)   -> 4 uint64 -> PCG64 state/inc (pcg setseq srandom)
 //   PCG64 XSL-RR 128/64 stream -> 256-layer ziggurat (tables: dp2_ziggurat_tables.h)
 //
-// One warp per slice walks that slice's stream (32 draws in flight via
-// jump-ahead, see omega_kernel).  The fast path (>99% of draws: one 64-bit
+// Warps walk segments of each slice's stream (32 draws in flight via
+// jump-ahead, segments stitched exactly, see omega_emit_kernel).  The fast path (>99% of draws: one 64-bit
 // output, one multiply) is exact IEEE arithmetic.  The rare
 // tail branch (layer 0, about 2.6e-4 of draws) needs log1p, whose last bit
 // differs between libm implementations, so every tail event is recorded
@@ -18,6 +18,9 @@
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 #include "dp2_ziggurat_tables.h"
+
+#include <algorithm>
+#include <cstdlib>
 
 namespace dp2 {
 
@@ -139,97 +142,159 @@ __device__ inline uint64_t pcg_out(U128 s) {
   return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
-// One warp per slice.  Lane l holds the generator state of draw base + l
-// (state_{p+l} = A^l state_p + inc * (1 + A + ... + A^(l-1))), so a batch of
-// 32 consecutive 64-bit draws is produced in parallel.  The ziggurat parse of
-// the draw stream is inherently sequential but almost always one draw per
-// normal: every round, the lanes from the current normal start up to the
-// first draw that misses the fast rectangle emit their normals at once
-// (ballot + prefix count); that one wedge/tail draw is resolved by its lane
-// with its own sequential generator, which then broadcasts its state so the
-// warp re-bases behind the consumed draws.  The output is the reference's
-// stream exactly.
-__global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp,
-                                                    const int64_t* slice_ids, double* out, TailRec* recs,
-                                                    int cap, int32_t* nrec, int32_t* redo) {
-  __shared__ uint64_t ki_s[256];
-  __shared__ double wi_s[256], fi_s[256];
+// (A^p, S_p = sum_{i<p} A^i) of the PCG64 LCG (pcg_advance_lcg_128 with a
+// unit increment): the state p steps after x is A^p x + S_p inc.
+__device__ inline void lcg_coeffs(uint64_t p, U128& am, U128& as) {
+  am = U128{1, 0};
+  as = U128{0, 0};
+  U128 cm{kPcgMulLo, kPcgMulHi}, cs{1, 0};
+  while (p) {
+    if (p & 1) {
+      am = mul128(am, cm);
+      as = add128(mul128(as, cm), cs);
+    }
+    cs = mul128(add128(cm, U128{1, 0}), cs);
+    cm = mul128(cm, cm);
+    p >>= 1;
+  }
+}
+__device__ inline U128 lcg_jump(U128 x, U128 inc, uint64_t p) {
+  U128 am, as;
+  lcg_coeffs(p, am, as);
+  return add128(mul128(am, x), mul128(as, inc));
+}
+
+struct ZigTabs {
+  uint64_t ki[256];
+  double wi[256], fi[256];
+};
+__device__ inline void load_zig(ZigTabs& T) {
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    ki_s[i] = kZigKi[i];
-    wi_s[i] = __longlong_as_double((long long)kZigWiBits[i]);
-    fi_s[i] = __longlong_as_double((long long)kZigFiBits[i]);
+    T.ki[i] = kZigKi[i];
+    T.wi[i] = __longlong_as_double((long long)kZigWiBits[i]);
+    T.fi[i] = __longlong_as_double((long long)kZigFiBits[i]);
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (k >= K) return;
-  // jump constants: A^lane, S_lane = sum_{i<lane} A^i, and the same for 32
-  const U128 A{kPcgMulLo, kPcgMulHi};
-  U128 Al{1, 0}, Sl{0, 0}, P{1, 0}, S{0, 0};
-  for (int i = 0; i < 32; ++i) {
-    if (i == lane) {
-      Al = P;
-      Sl = S;
-    }
-    S = add128(S, P);
-    P = mul128(P, A);
-  }
-  const U128 A32 = P, S32 = S;
-  const uint64_t gid = slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k;
+}
+
+// Per-slice stream: inc and the state of draw 0 (Pcg::next steps, then outputs).
+struct SliceStream {
+  U128 b, inc;
+};
+__device__ inline SliceStream slice_stream(uint64_t seed, uint64_t gid) {
   Pcg g;
   g.seed(derived_seed_u64(seed, gid));
   const U128 inc{g.ilo, g.ihi};
-  const U128 Cl = mul128(inc, Sl), C32 = mul128(inc, S32);
-  // state of draw 0 (Pcg::next steps, then outputs)
-  U128 b = add128(mul128(U128{g.slo, g.shi}, A), inc);
-  U128 st = add128(mul128(b, Al), Cl);
-  const int s = s_k[k];
-  double* o = out + (size_t)k * J * sp;
-  const int64_t total = (int64_t)J * s;
-  for (int64_t e = lane; e < (int64_t)J * (sp - s); e += 32)  // zero padding columns
-    o[(e / (sp - s)) * sp + s + e % (sp - s)] = 0.0;
-  int64_t i = 0;  // normals emitted
-  int start = 0;  // lane of the next normal start in this batch
-  // (row, column) of normal i, advanced incrementally (no 64-bit division per
-  // normal): advance by d <= 33 with s >= 1
-  int64_t row0 = 0;
-  int col0 = 0;
-  auto advance = [&](int d) {
-    col0 += d;
-    while (col0 >= s) {
-      col0 -= s;
-      ++row0;
+  return SliceStream{add128(mul128(U128{g.slo, g.shi}, U128{kPcgMulLo, kPcgMulHi}), inc), inc};
+}
+
+// Sequential ziggurat attempt starting at draw p (one thread): advances p past
+// the draws it consumes, returns the number of normals produced (0 or 1).
+__device__ int zig_attempt_seq(const ZigTabs& T, const SliceStream& S, int64_t& p) {
+  const U128 sp = lcg_jump(S.b, S.inc, (uint64_t)p);
+  uint64_t r = pcg_out(sp);
+  const int idx = (int)(r & 0xff);
+  r >>= 8;
+  const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+  if (rabs < T.ki[idx]) {
+    p += 1;
+    return 1;
+  }
+  Pcg h;
+  h.slo = sp.lo;
+  h.shi = sp.hi;
+  h.ilo = S.inc.lo;
+  h.ihi = S.inc.hi;
+  if (idx == 0) {
+    int a = 0;
+    for (;;) {
+      const double u1 = h.next_double(), u2 = h.next_double();
+      ++a;
+      const double xx = __dmul_rn(-kZigInvR, log1p(-u1));
+      const double yy = -log1p(-u2);
+      if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) break;
     }
+    p += 1 + 2 * a;
+    return 1;
+  }
+  const double x = __dmul_rn((double)rabs, T.wi[idx]);
+  const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(T.fi[idx - 1], -T.fi[idx]), h.next_double()), T.fi[idx]);
+  p += 2;
+  return lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x)) ? 1 : 0;
+}
+
+// Warp parse of one slice's stream from draw p0 (an attempt start) over the
+// attempts starting before p_end, normals numbered from i0 (stops at total).
+// Lane l holds the generator state of draw base + l (state_{p+l} = A^l
+// state_p + inc S_l), so a batch of 32 consecutive draws is produced in
+// parallel.  The ziggurat parse of the draw stream is sequential but almost
+// always one draw per normal: every round, the lanes from the current
+// attempt start up to the first draw that misses the fast rectangle are
+// normals at once (ballot + prefix count); that wedge/tail draw is resolved
+// by its lane with its own sequential generator, which then broadcasts its
+// state so the warp re-bases behind the consumed draws.  Returns the normals
+// produced (n_out) and the first attempt start >= p_end (p_out).  EMIT writes
+// the normals (row-major J x s_k in an sp-wide row) and records tail events.
+struct LaneJump {
+  U128 Al, Cl, A32, C32;
+};
+template <bool EMIT>
+__device__ void zig_parse(const ZigTabs& T, const SliceStream& S, const LaneJump& LJ, int lane, int64_t p0,
+                          int64_t p_end, int64_t i0, int64_t total, double* o, int s, int sp, int64_t k,
+                          TailRec* recs, int cap, int32_t* nrec, int32_t* redo, int64_t& n_out, int64_t& p_out) {
+  const U128 A{kPcgMulLo, kPcgMulHi};
+  if (p0 >= p_end) {
+    n_out = 0;
+    p_out = p0;
+    return;
+  }
+  U128 st = add128(mul128(lcg_jump(S.b, S.inc, (uint64_t)p0), LJ.Al), LJ.Cl);
+  int64_t base = p0, i = i0;
+  int start = 0;
+  p_out = p_end;
+  // (row, column) of normal i, advanced incrementally (advance by d <= 33)
+  int64_t row0 = EMIT ? i0 / s : 0;
+  int col0 = EMIT ? (int)(i0 - row0 * s) : 0;
+  // c / s by a 32-bit reciprocal: floor(c ceil(2^32/s) / 2^32) = floor(c/s)
+  // exactly for c < 2^32 / s (here c < s + 64); s = 1 separately
+  const uint32_t rcp_s = s > 1 ? (uint32_t)((0x100000000ull + (uint64_t)s - 1) / (uint64_t)s) : 0u;
+  auto divs = [&](int c) { return s > 1 ? (int)__umulhi((uint32_t)c, rcp_s) : c; };
+  auto advance = [&](int d) {
+    if (!EMIT) return;
+    col0 += d;
+    const int q = divs(col0);
+    col0 -= q * s;
+    row0 += q;
   };
   auto at = [&](int off) -> double* {  // element of normal i + off (0 <= off < 32)
-    int c = col0 + off;
-    int64_t r = row0;
-    while (c >= s) {
-      c -= s;
-      ++r;
-    }
-    return o + r * sp + c;
+    const int c = col0 + off;
+    const int q = divs(c);
+    return o + (row0 + q) * sp + (c - q * s);
   };
   while (i < total) {
+    const int64_t remp = p_end - base;
+    const int lim = remp < 32 ? (int)remp : 32;
     uint64_t r = pcg_out(st);
     const int idx = (int)(r & 0xff);
     r >>= 8;
     const int sign = (int)(r & 1);
     const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
-    double x = __dmul_rn((double)rabs, wi_s[idx]);
+    double x = __dmul_rn((double)rabs, T.wi[idx]);
     if (sign) x = -x;
-    const bool fast = rabs < ki_s[idx];
-    const unsigned slow = __ballot_sync(0xffffffffu, !fast) & (0xffffffffu << start);
-    const int f = slow ? __ffs(slow) - 1 : 32;
+    const bool fast = rabs < T.ki[idx];
+    unsigned slow = __ballot_sync(0xffffffffu, !fast) & (0xffffffffu << start);
+    if (lim < 32) slow &= (1u << lim) - 1u;
+    const int f = slow ? __ffs(slow) - 1 : lim;
     // lanes start .. f-1 are one-draw normals
-    if (lane >= start && lane < f) {
-      const int64_t oi = i + (lane - start);
-      if (oi < total) *at(lane - start) = x;
+    if (EMIT && lane >= start && lane < f) {
+      if (i + (lane - start) < total) *at(lane - start) = x;
     }
     i += f - start;
     advance(f - start);
-    if (f == 32) {  // batch exhausted: advance every lane by 32 draws
-      st = add128(mul128(st, A32), C32);
+    if (f == lim) {
+      if (lim < 32) break;  // reached p_end exactly
+      st = add128(mul128(st, LJ.A32), LJ.C32);  // batch exhausted: every lane 32 draws on
+      base += 32;
       start = 0;
       continue;
     }
@@ -241,8 +306,8 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
       Pcg h;
       h.slo = st.lo;
       h.shi = st.hi;
-      h.ilo = inc.lo;
-      h.ihi = inc.hi;
+      h.ilo = S.inc.lo;
+      h.ihi = S.inc.hi;
       if (idx == 0) {
         TailRec rec;
         rec.slice = k;
@@ -266,22 +331,24 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
         }
         rec.attempts = a;
         consumed = 1 + 2 * a;
-        if (a > kTailAttempts) {
-          redo[k] = 1;
-        } else {
-          const int slot = atomicAdd(nrec, 1);
-          if (slot < cap) recs[slot] = rec;
-          else redo[k] = 1;
+        if (EMIT) {
+          if (a > kTailAttempts) {
+            redo[k] = 1;
+          } else {
+            const int slot = atomicAdd(nrec, 1);
+            if (slot < cap) recs[slot] = rec;
+            else redo[k] = 1;
+          }
+          *at(0) = val;
         }
-        *at(0) = val;
         produced = 1;
       } else {
-        const double f0 = fi_s[idx - 1];
-        const double f1 = fi_s[idx];
+        const double f0 = T.fi[idx - 1];
+        const double f1 = T.fi[idx];
         const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(f0, -f1), h.next_double()), f1);
         consumed = 2;
         if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
-          *at(0) = x;
+          if (EMIT) *at(0) = x;
           produced = 1;
         }
       }
@@ -292,6 +359,10 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
     i += produced;
     advance(produced);
     const int nstart = f + consumed;
+    if (base + nstart >= p_end) {
+      p_out = base + nstart;
+      break;
+    }
     if (nstart < 32) {
       start = nstart;  // lanes still hold the draws behind the consumed ones
       continue;
@@ -299,18 +370,139 @@ __global__ void __launch_bounds__(128) omega_kernel(uint64_t seed, int64_t K, in
     // re-base: draw (base + nstart) = A * last + inc, then lane offsets
     last.lo = __shfl_sync(0xffffffffu, last.lo, f);
     last.hi = __shfl_sync(0xffffffffu, last.hi, f);
-    b = add128(mul128(last, A), inc);
-    st = add128(mul128(b, Al), Cl);
+    st = add128(mul128(add128(mul128(last, A), S.inc), LJ.Al), LJ.Cl);
+    base += nstart;
     start = 0;
+  }
+  n_out = i - i0;
+}
+
+__device__ inline LaneJump lane_jump(int lane, U128 inc) {
+  LaneJump L;
+  U128 sl, s32;
+  lcg_coeffs((uint64_t)lane, L.Al, sl);
+  lcg_coeffs(32, L.A32, s32);
+  L.Cl = mul128(inc, sl);
+  L.C32 = mul128(inc, s32);
+  return L;
+}
+
+// Segment-parallel Omega: slice k's draw stream is cut into G segments of L_k
+// = ceil(J s_k / G) draws.  omega_count_kernel parses segment g < G-1
+// speculatively from its first draw gL (assuming it starts an attempt) and
+// records (normals, first attempt start >= (g+1)L).  omega_emit_kernel
+// recovers, for its segment, the true start and output offset by scanning
+// the earlier segments' records: a segment whose true start t differs from hL
+// (the previous attempt ran over the boundary, ~1% of segments) is repaired
+// by stepping the true and the speculative parse one attempt at a time until
+// they meet -- from there they coincide -- or the true one leaves the
+// segment.  It then parses from its true start and writes.  The result is the
+// sequential stream exactly.
+__global__ void __launch_bounds__(128) omega_count_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k,
+                                                          int G, const int64_t* slice_ids, int64_t* seg_n,
+                                                          int64_t* seg_end) {
+  __shared__ ZigTabs T;
+  load_zig(T);
+  const int lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= K * (G - 1)) return;
+  const int64_t k = w / (G - 1);
+  const int g = (int)(w - k * (G - 1));
+  const int s = s_k[k];
+  const int64_t total = (int64_t)J * s, L = (total + G - 1) / G;
+  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k);
+  const LaneJump LJ = lane_jump(lane, S.inc);
+  int64_t n, e;
+  zig_parse<false>(T, S, LJ, lane, g * L, (g + 1) * L, 0, INT64_MAX, nullptr, s, 0, k, nullptr, 0, nullptr,
+                   nullptr, n, e);
+  if (lane == 0) {
+    seg_n[k * G + g] = n;
+    seg_end[k * G + g] = e;
   }
 }
 
+__global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k,
+                                                         int sp, int G, const int64_t* slice_ids,
+                                                         const int64_t* seg_n, const int64_t* seg_end, double* out,
+                                                         TailRec* recs, int cap, int32_t* nrec, int32_t* redo) {
+  __shared__ ZigTabs T;
+  load_zig(T);
+  const int lane = threadIdx.x & 31;
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= K * G) return;
+  const int64_t k = w / G;
+  const int g = (int)(w - k * G);
+  const int s = s_k[k];
+  const int64_t total = (int64_t)J * s, L = (total + G - 1) / G;
+  double* o = out + (size_t)k * J * sp;
+  if (s < sp) {  // zero padding columns: the slice's J x (sp - s) block, flat over its G warps
+    const int pw = sp - s;
+    for (int e = g * 32 + lane; e < J * pw; e += 32 * G) {
+      const int j = e / pw;
+      o[(int64_t)j * sp + s + (e - j * pw)] = 0.0;
+    }
+  }
+  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k);
+  // true start t and output offset O of segment g (every lane alike)
+  int64_t t = 0, O = 0;
+  for (int h = 0; h < g; ++h) {
+    const int64_t end_h = (h + 1) * L;
+    int64_t n = seg_n[k * G + h], e = seg_end[k * G + h];
+    if (t != h * L) {  // misaligned: walk the true (pt) and speculative (ps) attempts until they meet
+      int64_t pt = t, ps = h * L, ct = 0, cs = 0;
+      for (;;) {
+        if (pt >= end_h) {
+          n = ct;
+          e = pt;
+          break;
+        }
+        if (pt == ps) {
+          n = n - cs + ct;
+          break;
+        }
+        if (ps < pt) cs += zig_attempt_seq(T, S, ps);
+        else ct += zig_attempt_seq(T, S, pt);
+      }
+    }
+    O += n;
+    t = e;
+  }
+  if (O >= total) return;
+  const LaneJump LJ = lane_jump(lane, S.inc);
+  int64_t n, e;
+  zig_parse<true>(T, S, LJ, lane, t, g == G - 1 ? INT64_MAX : (g + 1) * L, O, total, o, s, sp, k, recs, cap, nrec,
+                  redo, n, e);
+}
+
 cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp, const int64_t* slice_ids,
-                      double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st) {
+                      double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st,
+                      int* launches) {
   cudaMemsetAsync(nrec, 0, sizeof(int32_t), st);
   cudaMemsetAsync(redo, 0, sizeof(int32_t) * K, st);
-  omega_kernel<<<(unsigned)((K + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, sp, slice_ids, out,
-                                                        static_cast<TailRec*>(recs), cap, nrec, redo);
+  // segments per slice: about 48 warps per SM in flight, segments >= 512 draws
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // (a count pass over all draws costs more than the latency it hides:
+  // DP2_OMEGA_SEGMENTS > 1 enables the segment-parallel path)
+  const char* env = getenv("DP2_OMEGA_SEGMENTS");
+  const int64_t want = env ? std::max(1, atoi(env)) : 1;
+  (void)sms;
+  const int64_t cap_len = std::max<int64_t>(1, (int64_t)J * sp / 512);
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>({want, cap_len, 64}));
+  int64_t* seg = nullptr;
+  if (G > 1) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&seg), sizeof(int64_t) * 2 * K * G, st);
+    if (e != cudaSuccess) return e;
+    const int64_t wc = K * (G - 1);
+    omega_count_kernel<<<(unsigned)((wc + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, G, slice_ids, seg, seg + K * G);
+  }
+  const int64_t we = K * G;
+  omega_emit_kernel<<<(unsigned)((we + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, sp, G, slice_ids, seg,
+                                                              seg ? seg + K * G : nullptr, out,
+                                                              static_cast<TailRec*>(recs), cap, nrec, redo);
+  if (seg) cudaFreeAsync(seg, st);
+  if (launches) *launches = G > 1 ? 2 : 1;
   return cudaGetLastError();
 }
 

@@ -19,6 +19,9 @@
 #include "dp2_internal.h"
 #include "dp2_small_linalg.cuh"
 
+#include <cstdlib>
+#include <utility>
+
 namespace dp2 {
 
 // ------------------------------------------------------------ orth (smem CGS2)
@@ -78,6 +81,134 @@ __global__ void __launch_bounds__(256) gram_y_piece_kernel(const Y* y2, const in
     __syncwarp();
   }
   gram_store<SP>(acc, wpart, gpart + (size_t)p * SP * SP);
+}
+
+// G partials of the fp32 Y rows (the tensor-core pass) on the FMA pipes.
+// Per piece (one block of 4 warps): 128-row tiles of Y are double-buffered
+// into shared memory with cp.async (row stride SP + 4 floats: conflict-free
+// 16 B reads); warp h owns a quarter of the upper-triangle (a <= b) pairs and
+// runs over all rows of a tile, 4 per lane (lane = row, the row in
+// registers), accumulating in fp32 (Y carries the tf32-product error ~1e-4
+// already; the <= nr / 32 term fp32 sums add ~1e-6).  The lanes are summed
+// in fp64 in a fixed order -> gpart[p] (full symmetric SP x SP).  Replaces
+// the DMMA Gram (the fp64 tensor pipe does 4x fewer FMAs per cycle).
+template <int SP>
+struct GramFfma {
+  static constexpr int NP = SP * (SP + 1) / 2;
+  static constexpr int NH = 4;                      // warps = pair groups
+  static constexpr int NPH = (NP + NH - 1) / NH;
+  static constexpr int TR = 128, LD = SP + 4;        // tile rows, row stride (floats)
+  static constexpr size_t RING = (size_t)2 * TR * LD * 4;
+  static constexpr size_t STAGE = (size_t)NH * NPH * 33 * 4;
+  static constexpr size_t SMEM = RING > STAGE ? RING : STAGE;
+};
+
+// upper-triangle pair j -> (a, b), row-major over a (b >= a)
+template <int SP>
+DP2_DEV constexpr int pair_a(int j) {
+  int a = 0;
+  while (j >= SP - a) {
+    j -= SP - a;
+    ++a;
+  }
+  return a;
+}
+template <int SP>
+DP2_DEV constexpr int pair_b(int j) {
+  int a = 0;
+  while (j >= SP - a) {
+    j -= SP - a;
+    ++a;
+  }
+  return a + j;
+}
+template <int SP, int PJ>
+DP2_DEV void pair_fma(const float (&v)[SP], float& acc) {
+  if constexpr (PJ < GramFfma<SP>::NP) {
+    constexpr int a = pair_a<SP>(PJ), b = pair_b<SP>(PJ);
+    acc = fmaf(v[a], v[b], acc);
+  }
+}
+template <int SP, int H, int... J>
+DP2_DEV void pairs_fma(const float (&v)[SP], float (&acc)[GramFfma<SP>::NPH], std::integer_sequence<int, J...>) {
+  (pair_fma<SP, H * GramFfma<SP>::NPH + J>(v, acc[J]), ...);
+}
+
+template <int SP>
+DP2_DEV void gram_tile_load(const float* y, int64_t r0, int nr, int t0, float* buf) {
+  constexpr int Q = SP / 4, TR = GramFfma<SP>::TR, LD = GramFfma<SP>::LD;
+  for (int e = threadIdx.x; e < TR * Q; e += blockDim.x) {
+    const int r = e / Q, q = e - r * Q;
+    const bool in = t0 + r < nr;
+    cp_async16(buf + r * LD + 4 * q, y + (r0 + (in ? t0 + r : 0)) * SP + 4 * q, in ? 16 : 0);
+  }
+}
+
+template <int SP, int H>
+DP2_DEV void gram_ffma_piece(const float* y, int64_t r0, int nr, int lane, float* sm, double* red) {
+  using GF = GramFfma<SP>;
+  constexpr int NPH = GF::NPH, TR = GF::TR, LD = GF::LD;
+  float acc[NPH];
+#pragma unroll
+  for (int j = 0; j < NPH; ++j) acc[j] = 0.f;
+  const int ntile = (nr + TR - 1) / TR;
+  gram_tile_load<SP>(y, r0, nr, 0, sm);
+  cp_async_commit();
+  for (int it = 0; it < ntile; ++it) {
+    float* cur = sm + (it & 1) * TR * LD;
+    if (it + 1 < ntile) gram_tile_load<SP>(y, r0, nr, (it + 1) * TR, sm + ((it + 1) & 1) * TR * LD);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll 1
+    for (int u = 0; u < TR / 32; ++u) {  // rows past the piece end are zero-filled
+      const float4* row = reinterpret_cast<const float4*>(cur + (lane + 32 * u) * LD);
+      float v[SP];
+#pragma unroll
+      for (int q = 0; q < SP / 4; ++q) {
+        const float4 f = row[q];
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+      }
+      pairs_fma<SP, H>(v, acc, std::make_integer_sequence<int, NPH>{});
+    }
+    __syncthreads();
+  }
+  // lane sums in fp64 through a (pair x lane) staging tile (row stride 33),
+  // aliasing the (drained) tile ring
+  float* stage = sm + H * NPH * 33;
+#pragma unroll
+  for (int j = 0; j < NPH; ++j) stage[j * 33 + lane] = acc[j];
+  __syncwarp();
+  for (int j = lane; j < NPH; j += 32) {
+    double d = 0.0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) d += (double)stage[j * 33 + l];
+    if (H * NPH + j < GF::NP) red[H * NPH + j] = d;
+  }
+}
+
+template <int SP>
+__global__ void __launch_bounds__(128) gram_y_ffma_kernel(const float* y2, const int64_t* piece_row0,
+                                                          const int32_t* piece_rows, double* gpart) {
+  using GF = GramFfma<SP>;
+  __shared__ double red[GF::NH * GF::NPH];
+  extern __shared__ __align__(16) float gsm[];
+  const int p = blockIdx.x, lane = threadIdx.x & 31, h = threadIdx.x >> 5;
+  const int64_t r0 = piece_row0[p];
+  const int nr = piece_rows[p];
+  switch (h) {
+    case 0: gram_ffma_piece<SP, 0>(y2, r0, nr, lane, gsm, red); break;
+    case 1: gram_ffma_piece<SP, 1>(y2, r0, nr, lane, gsm, red); break;
+    case 2: gram_ffma_piece<SP, 2>(y2, r0, nr, lane, gsm, red); break;
+    default: gram_ffma_piece<SP, 3>(y2, r0, nr, lane, gsm, red); break;
+  }
+  __syncthreads();
+  double* out = gpart + (size_t)p * SP * SP;
+  for (int e = threadIdx.x; e < SP * SP; e += blockDim.x) {
+    int a = e / SP, b = e - a * SP;
+    if (a > b) { const int t = a; a = b; b = t; }
+    out[e] = red[a * SP - a * (a - 1) / 2 + (b - a)];  // upper-triangle pair index
+  }
 }
 
 // Per slice: C = sum of the pass-2 partials (J x SP, written out), CC = C^T C
@@ -680,11 +811,20 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
   cudaError_t e = cudaSuccess;
   if (!gpart) {  // tensor-core pass: G partials per piece from its fp32 Y rows
-    const size_t gs = (size_t)8 * 32 * (SP + 4) * 4 + (size_t)8 * GramBlocks<SP>::NBLK * 64 * 8;
-    e = cudaFuncSetAttribute(gram_y_piece_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs);
-    if (e != cudaSuccess) return e;
-    gram_y_piece_kernel<float, SP><<<P, 256, gs, stream>>>(reinterpret_cast<const float*>(y2), st->piece_row0,
-                                                           st->piece_rows, gscratch);
+    static const bool dmma = getenv("DP2_GRAM_DMMA") && atoi(getenv("DP2_GRAM_DMMA")) != 0;
+    if (dmma) {
+      const size_t gs = (size_t)8 * 32 * (SP + 4) * 4 + (size_t)8 * GramBlocks<SP>::NBLK * 64 * 8;
+      e = cudaFuncSetAttribute(gram_y_piece_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs);
+      if (e != cudaSuccess) return e;
+      gram_y_piece_kernel<float, SP><<<P, 256, gs, stream>>>(reinterpret_cast<const float*>(y2), st->piece_row0,
+                                                             st->piece_rows, gscratch);
+    } else {
+      const size_t fs = GramFfma<SP>::SMEM;
+      e = cudaFuncSetAttribute(gram_y_ffma_kernel<SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs);
+      if (e != cudaSuccess) return e;
+      gram_y_ffma_kernel<SP><<<P, 128, fs, stream>>>(reinterpret_cast<const float*>(y2), st->piece_row0,
+                                                     st->piece_rows, gscratch);
+    }
     gpart = gscratch;
   }
   const size_t gb = ((size_t)8 * 32 * (SP + 1) + (size_t)8 * GramBlocks<SP>::NBLK * 64) * 8;

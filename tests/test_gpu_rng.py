@@ -21,7 +21,7 @@ def test_golden_omega_digests(golden):
 
 
 @pytest.mark.parametrize("seed,K,J,smax", [(0, 1000, 512, 20), (7, 300, 100, 20), ((1 << 64) - 1, 64, 37, 13),
-                                           (2**63 + 5, 200, 256, 32), (12345, 50, 1000, 20)])
+                                           (2**63 + 5, 200, 256, 32), (12345, 50, 1000, 20), (99, 2, 4000, 16)])
 def test_device_omega_matches_numpy_bytes(seed, K, J, smax):
     import torch
     from paper_2203_12798_b200.linalg import padded_width
