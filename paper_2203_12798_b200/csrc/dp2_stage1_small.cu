@@ -623,6 +623,42 @@ DP2_DEV void dot_pcol(const Y (&y0)[SP], const Y (&y1)[SP], const double* Pt, in
   a1 = s1;
 }
 
+// (y0 P[:, c], y1 P[:, c]) in the rows' own type T (fp32 rows: fp32 products
+// -- Y carries tf32-product error ~1e-4, the 1e-7 of an fp32 dot is below
+// it; fp64 rows: fp64), P transposed in shared memory as T (rows >= s zero),
+// fma over a = 0..SP-1 in order.
+template <int SP, typename T>
+DP2_DEV void dot_pcol_t(const T (&y0)[SP], const T (&y1)[SP], const T* Pt, int c, T& a0, T& a1) {
+  T s0 = 0, s1 = 0;
+  if constexpr (sizeof(T) == 4) {
+    const float4* pc = reinterpret_cast<const float4*>(Pt + c * SP);
+#pragma unroll
+    for (int q = 0; q < SP / 4; ++q) {
+      const float4 pp = pc[q];
+      s0 = fmaf(y0[4 * q], pp.x, s0);
+      s1 = fmaf(y1[4 * q], pp.x, s1);
+      s0 = fmaf(y0[4 * q + 1], pp.y, s0);
+      s1 = fmaf(y1[4 * q + 1], pp.y, s1);
+      s0 = fmaf(y0[4 * q + 2], pp.z, s0);
+      s1 = fmaf(y1[4 * q + 2], pp.z, s1);
+      s0 = fmaf(y0[4 * q + 3], pp.w, s0);
+      s1 = fmaf(y1[4 * q + 3], pp.w, s1);
+    }
+  } else {
+    const double2* pc = reinterpret_cast<const double2*>(Pt + c * SP);
+#pragma unroll
+    for (int q = 0; q < SP / 2; ++q) {
+      const double2 pp = pc[q];
+      s0 = fma(y0[2 * q], pp.x, s0);
+      s1 = fma(y1[2 * q], pp.x, s1);
+      s0 = fma(y0[2 * q + 1], pp.y, s0);
+      s1 = fma(y1[2 * q + 1], pp.y, s1);
+    }
+  }
+  a0 = s0;
+  a1 = s1;
+}
+
 // ------------------------------------------------------------ A = Y P and its argmax candidates
 // Per piece: A = Y P for its rows, written UNSIGNED (the column signs are
 // applied afterwards by apply_signs_kernel, or deferred to the caller), and
@@ -642,17 +678,17 @@ __global__ void __launch_bounds__(256) a_cand_kernel(const Y* y2, const int64_t*
                                                      const double* Pm, int R, double* A, double* cand_abs,
                                                      int64_t* cand_row, int32_t* cand_neg) {
   extern __shared__ __align__(16) double sm[];
-  double* Pt = sm;                                   // R x SP (P transposed), entries a >= s zero
-  double* at = Pt + SP * R;                          // 512 x R output tile
+  double* at = sm;                                   // 512 x R output tile
   double* bval = at + 512 * R;                       // R x 256 signed best values
   int* brow = reinterpret_cast<int*>(bval + R * 256);  // R x 256 row within the piece
+  Y* Pt = reinterpret_cast<Y*>(brow + R * 256);      // R x SP (P transposed, as Y), entries a >= s zero
   const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int k = piece_slice[p], s = s_k[k];
   const int64_t base = row_off[k], r0 = piece_row0[p];
   const int nr = piece_rows[p];
   for (int i = tid; i < SP * R; i += 256) {
     const int c = i / SP, a = i - c * SP;
-    Pt[i] = a < s ? Pm[(size_t)k * SP * R + a * R + c] : 0.0;
+    Pt[i] = a < s ? (Y)Pm[(size_t)k * SP * R + a * R + c] : (Y)0;
   }
   for (int c = 0; c < R; ++c) brow[c * 256 + tid] = -1;  // own slots
   __syncthreads();
@@ -669,8 +705,9 @@ __global__ void __launch_bounds__(256) a_cand_kernel(const Y* y2, const int64_t*
       }
 #pragma unroll 1
       for (int c = 0; c < R; ++c) {
-        double a0, a1;
-        dot_pcol<SP, Y>(y0, y1, Pt, c, a0, a1);
+        Y a0y, a1y;
+        dot_pcol_t<SP, Y>(y0, y1, Pt, c, a0y, a1y);
+        const double a0 = (double)a0y, a1 = (double)a1y;  // exact widening: stored = compared
         at[tid * R + c] = a0;
         at[(tid + 256) * R + c] = a1;
         double bv = bval[c * 256 + tid];
@@ -849,7 +886,7 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
                                                                           status);
   // A unsigned + candidates -> signs (and signed P, M) -> A signs applied,
   // unless the caller takes them (a_signs: A stays unsigned)
-  const size_t as = ((size_t)SP * R + 512 * (size_t)R + (size_t)R * 256) * 8 + (size_t)R * 256 * 4;
+  const size_t as = (512 * (size_t)R + (size_t)R * 256) * 8 + (size_t)R * 256 * 4 + (size_t)SP * R * (y32 ? 4 : 8);
   double* sA = a_signs ? a_signs : sgn;
   if (y32) {
     e = cudaFuncSetAttribute(a_cand_kernel<float, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)as);
