@@ -7,8 +7,8 @@ The public surface mirrors the reference package's hot-path API
 ``SolverOptions``, ``FitTrace``, ``Parafac2Factors``, ``fitness`` and the
 kernel-level functions.  See DESIGN.md.
 """
-from .errors import (DecompositionError, DegenerateInputError, NonFiniteInputError, NumericFailure,
-                     RankTooLargeError, ShapeMismatchError)
+from .errors import (ArchiveFormatError, DecompositionError, DegenerateInputError, NonFiniteInputError,
+                     NumericFailure, RankTooLargeError, ShapeMismatchError)
 from .factors import FitTrace, Parafac2Factors, SliceViews, SolverOptions, initial_factors, push_col_norms
 from .linalg import RsvdParams, derived_seed
 from .scheduler import PartitionPlan, greedy_partition, resolve_threads
@@ -20,12 +20,14 @@ from .compress import CompressedTensor, compress, reconstruct_slice  # noqa: E40
 from .solver import (Rotations, convergence_metric, fit_dpar2, mttkrp_mode1, mttkrp_mode2,  # noqa: E402
                      mttkrp_mode3, rotated_cores, update_factors, update_rotations)
 from .analysis import fitness  # noqa: E402
+from .archive import fit_compressed, load_archive, load_compressed, save_archive, save_compressed  # noqa: E402
 
 _LAZY = ["IrregularTensor", "CompressedTensor", "compress", "reconstruct_slice", "fit_dpar2", "update_rotations",
          "rotated_cores", "mttkrp_mode1", "mttkrp_mode2", "mttkrp_mode3", "update_factors", "convergence_metric",
-         "fitness", "Rotations"]
+         "fitness", "Rotations", "load_archive", "save_archive", "load_compressed", "save_compressed",
+         "fit_compressed"]
 
 __all__ = sorted(list(_LAZY) + [
-    "DecompositionError", "DegenerateInputError", "NonFiniteInputError", "NumericFailure", "RankTooLargeError",
+    "ArchiveFormatError", "DecompositionError", "DegenerateInputError", "NonFiniteInputError", "NumericFailure", "RankTooLargeError",
     "ShapeMismatchError", "FitTrace", "Parafac2Factors", "SliceViews", "SolverOptions", "initial_factors", "push_col_norms",
     "RsvdParams", "derived_seed", "PartitionPlan", "greedy_partition", "resolve_threads"])

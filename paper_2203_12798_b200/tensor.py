@@ -141,6 +141,15 @@ class IrregularTensor:
             self._stats()
         return self
 
+    @classmethod
+    def plan_only(cls, row_counts, dev):
+        """Row layout and piece plans of a tensor whose values are absent (e.g.
+        the slice bases of a loaded compressed tensor): consumers that only
+        walk rows by pieces (assemble_q) take its store; X is a one-row
+        16-byte placeholder broadcast over the rows and never read."""
+        X = torch.zeros((1, 2), dtype=torch.float64, device=dev).expand(int(sum(row_counts)), 2)
+        return cls.from_packed(X, row_counts, 1, dtype="f64", check=False)
+
     def _finish_layout(self):
         dev = self.X.device
         off = np.zeros(len(self._rows) + 1, np.int64)
