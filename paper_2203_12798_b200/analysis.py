@@ -2,6 +2,19 @@
 
 One streaming pass over the packed store computes both sum ||X_k||^2 and
 sum ||X_k - Q_k (H * w_k) V^T||^2 (fixed-order reductions).
+
+Zero-pass form for factors fresh from ``fit_dpar2`` on an
+fp64 tensor: with G_k = H diag(w_k) and Q_k orthonormal,
+
+    ||X_k - Q_k G_k V^T||^2 = ||X_k||^2 - 2 <Q_k^T X_k, G_k V^T> + ||G_k V^T||^2
+
+and stage 1 already holds Q_k^T X_k: Q_k = A_k Pi_k with A_k = Y_k P_k and
+C_k = X_k^T Y_k from the second pass, so Q_k^T X_k = Pi_k^T (C_k P_k)^T =
+Pi_k^T M_k^T, M_k the slice's (signed) block of the stage-1 matrix M.  The fit
+keeps V^T M (R x KR); the fitness is then R x R work per slice, no pass over X
+(||X_k||^2 comes from the tensor's stored slice norms).  Rank-deficient slices
+(completed A_k columns are not Y_k P_k) and fp32 stores (M from tf32
+products) use the streaming pass.
 """
 from __future__ import annotations
 
@@ -17,8 +30,31 @@ from .factors import Parafac2Factors
 from .tensor import IrregularTensor, stream_ptr
 
 
-def fitness(tensor: IrregularTensor, factors: Parafac2Factors, threads=None):
-    """1 - sum_k ||X_k - Xhat_k||_F^2 / sum_k ||X_k||_F^2."""
+def _zero_pass_terms(tensor, factors, d):
+    """(sum ||X_k||^2, sum residual) from the fit's V^T M, or None when the
+    factors do not carry it for this tensor (or it does not apply)."""
+    zp = getattr(factors, "_zero_pass", None)
+    if not zp or zp["tensor"]() is not tensor:
+        return None
+    R = factors.H.shape[1]
+    if int(zp["rank_found"].min().item()) < R:
+        return None
+    V = d(factors.V)
+    if not torch.equal(V, zp["V"]):  # V^T M was formed with the fit's V
+        return None
+    H, W = d(factors.H), d(factors.W)
+    K = W.shape[0]
+    G = H[None, :, :] * W[:, None, :]                               # G_k = H diag(w_k)
+    B = zp["VtM"].reshape(R, K, R).permute(1, 0, 2)                 # B_k = V^T M_k
+    cross = (zp["polar"] * torch.bmm(G, B).transpose(1, 2)).sum(dim=(1, 2))   # tr(Pi_k G_k B_k)
+    norm = (torch.matmul(G, V.t() @ V) * G).sum(dim=(1, 2))         # ||G_k V^T||^2
+    sq = tensor.slice_sq_norms()
+    return float(sq.sum().item()), float((sq - 2.0 * cross + norm).sum().item())
+
+
+def fitness(tensor: IrregularTensor, factors: Parafac2Factors, threads=None, zero_pass=True):
+    """1 - sum_k ||X_k - Xhat_k||_F^2 / sum_k ||X_k||_F^2 (``zero_pass``: use
+    the fit's stage-1 data when it applies, see the module docstring)."""
     if factors.num_slices != tensor.num_slices:
         raise ShapeMismatchError(
             f"factors cover {factors.num_slices} slices, tensor has {tensor.num_slices}")
@@ -29,6 +65,13 @@ def fitness(tensor: IrregularTensor, factors: Parafac2Factors, threads=None):
         if isinstance(x, torch.Tensor):
             return x.to(device=dev, dtype=torch.float64).contiguous()
         return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+
+    terms = _zero_pass_terms(tensor, factors, d) if zero_pass else None
+    if terms is not None:
+        total, resid = terms
+        if total == 0.0:
+            raise DegenerateInputError("fitness undefined for an all-zero tensor")
+        return 1.0 - resid / total
 
     if factors.Q_packed is not None:
         Q = d(factors.Q_packed)

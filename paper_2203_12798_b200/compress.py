@@ -349,6 +349,8 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
                             cores=F, rank_found=rank_found, a_signs=a_signs)
     comp._omega_check = check
+    if defer_signs:  # fit-internal: fit_dpar2 takes V^T M for the zero-pass fitness
+        comp._stage1_M = M
     return comp, status
 
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -223,6 +224,11 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     h, v, w = initial_factors(tensor.num_cols, tensor.num_slices, rank, opts.seed)
     launched = _als_launch(comp, h, v, w, opts.max_iters, opts.tol, normalize, use_graph=use_graph)
     Q = assemble_q(tensor, comp, launched[3])
+    zero_pass = None
+    if tensor.dtype == "f64":  # V^T M (R x KR) for fitness without a pass over X (analysis.py)
+        zero_pass = dict(VtM=torch.mm(launched[1].t(), comp._stage1_M), V=launched[1], polar=launched[3],
+                         rank_found=comp.rank_found, tensor=weakref.ref(tensor))
+    comp._stage1_M = None
     q_host = None
     if output == "numpy":
         # while the GPU finishes: allocate + pre-touch Q's NumPy destination
@@ -247,4 +253,5 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
         # staged D2H (device_to_numpy): a fresh pinned destination per fit
         # costs ~0.5 ms/MB to pin, far more than the copy
         factors = factors.numpy(q_out=q_host.result())
+    factors._zero_pass = zero_pass
     return factors, trace
