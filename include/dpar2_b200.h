@@ -128,6 +128,15 @@ typedef struct dp2_tail_record {
 int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev, int32_t sp,
                        const int64_t* slice_ids_dev, double* out, dp2_tail_record* recs, int32_t cap,
                        int32_t* nrec_dev, int32_t* redo_dev, void* stream);
+/* One stream: out (rows x width, row-major) = Generator(PCG64(seed))
+ * .standard_normal((rows, width)) byte-exact -- the stage-2 sketch matrix
+ * (P/compress.py:109-111, seed = derived_seed(seed, K) computed by the
+ * caller).  The stream is cut into segments parsed in parallel and stitched
+ * exactly; tail records as for dp2_omega_generate (slice 0).  width_dev:
+ * device int32 holding width. */
+int dp2_omega_generate_stream(uint64_t seed, int64_t rows, int32_t width, const int32_t* width_dev, double* out,
+                              dp2_tail_record* recs, int32_t cap, int32_t* nrec_dev, int32_t* redo_dev,
+                              void* stream);
 /* Host-side replay of tail records (host pointers): for each record, re-run
  * its attempts with this process's libm log1p -- the function NumPy's
  * ziggurat calls (npy_log1p) -- giving the reference's output value in

@@ -8,6 +8,7 @@ accepted (they never change values in the reference either).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, replace
 
@@ -17,7 +18,7 @@ import torch
 from . import _lib
 from .errors import NumericFailure, RankTooLargeError
 from .linalg import RsvdParams, derived_seed, padded_width, sketch_width
-from .rng import omega_device, stage2_omega
+from .rng import omega_device, stage2_omega, stage2_omega_finish, stage2_omega_launch  # noqa: F401
 from .scheduler import resolve_threads
 from .tensor import IrregularTensor, new_status, sm_count, stream_ptr
 
@@ -318,6 +319,9 @@ def omega_mismatch(comp):
     return chk is not None and bool(chk.result()["omega_mismatch"])
 
 
+_OMEGA2_HOST = os.environ.get("DP2_OMEGA2_HOST", "0") not in ("", "0")
+
+
 def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None, stage2: RsvdParams | None = None,
                    plan=None, threads=None, timings=None, exact_omega=False, defer_signs=False):
     """``compress`` without the host synchronisation of its status check:
@@ -335,6 +339,8 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     J, K = tensor.num_cols, tensor.num_slices
     second, s2 = stage2_params(base, stage2, rank, K, J)
     spec = not exact_omega
+    # DP2_OMEGA2_HOST=1: draw Omega_2 with NumPy while stage 1 runs (A/B knob)
+    om2h = None if _OMEGA2_HOST else stage2_omega_launch(second.seed, K * rank, s2, tensor.X.device)
     a_signs = torch.empty((K, rank), dtype=torch.float64, device=tensor.X.device) if defer_signs else None
     if len(tensor._upload_events) > 1:
         res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
@@ -342,9 +348,10 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
         res = run_stage1(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
     A, M, rank_found, status = res[:4]
     check = res[4] if len(res) > 4 else None
-    # stage-2 Omega (one NumPy stream, P/compress.py:109-111) is drawn on the
-    # host once stage 1 is enqueued -- the device is busy with it meanwhile
-    om2 = stage2_omega(second.seed, K * rank, s2)
+    # stage-2 Omega (one stream, P/compress.py:109-111): generated on the
+    # device ahead of stage 1; its few tail draws are replayed and patched
+    # now, while stage 1 runs
+    om2 = stage2_omega(second.seed, K * rank, s2) if om2h is None else stage2_omega_finish(om2h)
     D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2, status, timings=timings)
     comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
                             cores=F, rank_found=rank_found, a_signs=a_signs)

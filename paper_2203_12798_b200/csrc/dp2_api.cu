@@ -190,6 +190,17 @@ int dp2_omega_generate(uint64_t seed, int64_t K, int32_t J, const int32_t* s_dev
   return e == cudaSuccess ? ok(launches) : fail(e, "dp2_omega_generate");
 }
 
+int dp2_omega_generate_stream(uint64_t seed, int64_t rows, int32_t width, const int32_t* width_dev, double* out,
+                              dp2_tail_record* recs, int32_t cap, int32_t* nrec_dev, int32_t* redo_dev,
+                              void* stream) {
+  if (rows < 1 || width < 1 || rows * width > INT32_MAX || cap < 0 || !width_dev)
+    return fail_arg("invalid omega stream shape");
+  int launches = 0;
+  cudaError_t e = dp2::run_omega(seed, 1, (int)rows, width_dev, width, nullptr, out, recs, cap, nrec_dev, redo_dev,
+                                 S(stream), &launches, true);
+  return e == cudaSuccess ? ok(launches) : fail(e, "dp2_omega_generate_stream");
+}
+
 int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok_out) {
   if (count < 0 || (count && (!recs || !vals || !ok_out))) return fail_arg("invalid replay arguments");
   constexpr double kR = 3.6541528853610087963519472518, kInvR = 0.27366123732975827203338247596;

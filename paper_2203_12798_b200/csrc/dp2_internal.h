@@ -72,7 +72,8 @@ cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const doubl
 cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status, cudaStream_t stream);
 
 cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp, const int64_t* slice_ids,
-                      double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st, int* launches = nullptr);
+                      double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st, int* launches = nullptr,
+                      bool raw = false);
 size_t tail_record_bytes();
 uint64_t derived_seed_host(uint64_t seed, uint64_t index);
 

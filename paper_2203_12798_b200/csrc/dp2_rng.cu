@@ -181,9 +181,11 @@ __device__ inline void load_zig(ZigTabs& T) {
 struct SliceStream {
   U128 b, inc;
 };
-__device__ inline SliceStream slice_stream(uint64_t seed, uint64_t gid) {
+// raw: PCG64(seed) itself (one stream, e.g. the stage-2 Omega); else
+// PCG64(derived_seed(seed, gid)) (the per-slice streams, P/linalg.py:187-194)
+__device__ inline SliceStream slice_stream(uint64_t seed, uint64_t gid, bool raw = false) {
   Pcg g;
-  g.seed(derived_seed_u64(seed, gid));
+  g.seed(raw ? seed : derived_seed_u64(seed, gid));
   const U128 inc{g.ilo, g.ihi};
   return SliceStream{add128(mul128(U128{g.slo, g.shi}, U128{kPcgMulLo, kPcgMulHi}), inc), inc};
 }
@@ -377,6 +379,14 @@ __device__ void zig_parse(const ZigTabs& T, const SliceStream& S, const LaneJump
   n_out = i - i0;
 }
 
+// Segment length in draws: a normal takes ~1.013 draws on average (wedge
+// uniforms, rejections, tails), so segments sized on 1.03 x the normal count
+// leave the last one (which runs until the stream's normals are complete)
+// without a long overhang; trailing segments past the end exit at once.
+__device__ inline int64_t seg_len(int64_t total, int G) {
+  return G == 1 ? total : (total * 103 + 100 * (int64_t)G - 1) / (100 * (int64_t)G);
+}
+
 __device__ inline LaneJump lane_jump(int lane, U128 inc) {
   LaneJump L;
   U128 sl, s32;
@@ -400,7 +410,7 @@ __device__ inline LaneJump lane_jump(int lane, U128 inc) {
 // sequential stream exactly.
 __global__ void __launch_bounds__(128) omega_count_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k,
                                                           int G, const int64_t* slice_ids, int64_t* seg_n,
-                                                          int64_t* seg_end) {
+                                                          int64_t* seg_end, int raw) {
   __shared__ ZigTabs T;
   load_zig(T);
   const int lane = threadIdx.x & 31;
@@ -409,8 +419,8 @@ __global__ void __launch_bounds__(128) omega_count_kernel(uint64_t seed, int64_t
   const int64_t k = w / (G - 1);
   const int g = (int)(w - k * (G - 1));
   const int s = s_k[k];
-  const int64_t total = (int64_t)J * s, L = (total + G - 1) / G;
-  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k);
+  const int64_t total = (int64_t)J * s, L = seg_len(total, G);
+  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k, raw != 0);
   const LaneJump LJ = lane_jump(lane, S.inc);
   int64_t n, e;
   zig_parse<false>(T, S, LJ, lane, g * L, (g + 1) * L, 0, INT64_MAX, nullptr, s, 0, k, nullptr, 0, nullptr,
@@ -424,7 +434,8 @@ __global__ void __launch_bounds__(128) omega_count_kernel(uint64_t seed, int64_t
 __global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t K, int J, const int32_t* s_k,
                                                          int sp, int G, const int64_t* slice_ids,
                                                          const int64_t* seg_n, const int64_t* seg_end, double* out,
-                                                         TailRec* recs, int cap, int32_t* nrec, int32_t* redo) {
+                                                         TailRec* recs, int cap, int32_t* nrec, int32_t* redo,
+                                                         int raw) {
   __shared__ ZigTabs T;
   load_zig(T);
   const int lane = threadIdx.x & 31;
@@ -433,7 +444,7 @@ __global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t 
   const int64_t k = w / G;
   const int g = (int)(w - k * G);
   const int s = s_k[k];
-  const int64_t total = (int64_t)J * s, L = (total + G - 1) / G;
+  const int64_t total = (int64_t)J * s, L = seg_len(total, G);
   double* o = out + (size_t)k * J * sp;
   if (s < sp) {  // zero padding columns: the slice's J x (sp - s) block, flat over its G warps
     const int pw = sp - s;
@@ -442,18 +453,25 @@ __global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t 
       o[(int64_t)j * sp + s + (e - j * pw)] = 0.0;
     }
   }
-  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k);
-  // true start t and output offset O of segment g (every lane alike)
-  int64_t t = 0, O = 0;
-  for (int h = 0; h < g; ++h) {
-    const int64_t end_h = (h + 1) * L;
-    int64_t n = seg_n[k * G + h], e = seg_end[k * G + h];
-    if (t != h * L) {  // misaligned: walk the true (pt) and speculative (ps) attempts until they meet
+  const SliceStream S = slice_stream(seed, slice_ids ? (uint64_t)slice_ids[k] : (uint64_t)k, raw != 0);
+  // true start t and output offset O of segment g.  Warp-parallel: lane
+  // sums the counts of segments h = lane, lane + 32, ... < g; a segment whose
+  // predecessor ended past its first draw (misaligned) is repaired by its
+  // lane, walking the true and the speculative attempts until they meet --
+  // from there they coincide, so its end and every later start are
+  // unchanged.  If a walk leaves the segment first (its end moves; never
+  // observed), the starts are rebuilt by the sequential scan.
+  int64_t part = 0;
+  int lost = 0;
+  for (int h = lane; h < g; h += 32) {
+    int64_t n = seg_n[k * G + h];
+    const int64_t t = h == 0 ? 0 : seg_end[k * G + h - 1];
+    if (t != h * L) {
+      const int64_t end_h = (h + 1) * L;
       int64_t pt = t, ps = h * L, ct = 0, cs = 0;
       for (;;) {
         if (pt >= end_h) {
-          n = ct;
-          e = pt;
+          lost = 1;
           break;
         }
         if (pt == ps) {
@@ -464,8 +482,35 @@ __global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t 
         else ct += zig_attempt_seq(T, S, pt);
       }
     }
-    O += n;
-    t = e;
+    part += n;
+  }
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  int64_t O = part, t = g == 0 ? 0 : seg_end[k * G + g - 1];
+  if (__any_sync(0xffffffffu, lost)) {  // sequential scan (every lane alike)
+    t = 0;
+    O = 0;
+    for (int h = 0; h < g; ++h) {
+      const int64_t end_h = (h + 1) * L;
+      int64_t n = seg_n[k * G + h], e = seg_end[k * G + h];
+      if (t != h * L) {
+        int64_t pt = t, ps = h * L, ct = 0, cs = 0;
+        for (;;) {
+          if (pt >= end_h) {
+            n = ct;
+            e = pt;
+            break;
+          }
+          if (pt == ps) {
+            n = n - cs + ct;
+            break;
+          }
+          if (ps < pt) cs += zig_attempt_seq(T, S, ps);
+          else ct += zig_attempt_seq(T, S, pt);
+        }
+      }
+      O += n;
+      t = e;
+    }
   }
   if (O >= total) return;
   const LaneJump LJ = lane_jump(lane, S.inc);
@@ -476,32 +521,49 @@ __global__ void __launch_bounds__(128) omega_emit_kernel(uint64_t seed, int64_t 
 
 cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp, const int64_t* slice_ids,
                       double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st,
-                      int* launches) {
+                      int* launches, bool raw) {
   cudaMemsetAsync(nrec, 0, sizeof(int32_t), st);
   cudaMemsetAsync(redo, 0, sizeof(int32_t) * K, st);
   // segments per slice: about 48 warps per SM in flight, segments >= 512 draws
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // (a count pass over all draws costs more than the latency it hides:
-  // DP2_OMEGA_SEGMENTS > 1 enables the segment-parallel path)
+  // Segments per stream: with >= 4 streams per SM one warp per stream keeps
+  // the GPU busy (a count pass over all draws costs more than the latency it
+  // hides); fewer streams (the stage-2 Omega is one) split into segments of
+  // >= 512 draws, ~48 warps per SM.  DP2_OMEGA_SEGMENTS overrides.
   const char* env = getenv("DP2_OMEGA_SEGMENTS");
-  const int64_t want = env ? std::max(1, atoi(env)) : 1;
-  (void)sms;
+  const int64_t want = env ? std::max(1, atoi(env))
+                           : (K >= (int64_t)sms * 4 ? 1 : ((int64_t)sms * 48 + K - 1) / K);
   const int64_t cap_len = std::max<int64_t>(1, (int64_t)J * sp / 512);
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>({want, cap_len, 64}));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>({want, cap_len, 1024}));
   int64_t* seg = nullptr;
   if (G > 1) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&seg), sizeof(int64_t) * 2 * K * G, st);
-    if (e != cudaSuccess) return e;
+    // grow-only per-device scratch (a stream-ordered pool allocation is
+    // returned to the driver at every synchronisation and re-mapped next call)
+    static int64_t* cache[64] = {};
+    static size_t cache_bytes[64] = {};
+    const size_t need = sizeof(int64_t) * 2 * K * G;
+    if (dev < 64 && cache_bytes[dev] < need) {
+      cudaStreamSynchronize(st);  // the old buffer may still be in use
+      if (cache[dev]) cudaFree(cache[dev]);
+      cache[dev] = nullptr;
+      cache_bytes[dev] = 0;
+      cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&cache[dev]), std::max<size_t>(need, 1 << 16));
+      if (e != cudaSuccess) return e;
+      cache_bytes[dev] = std::max<size_t>(need, 1 << 16);
+    }
+    if (dev >= 64) return cudaErrorInvalidDevice;
+    seg = cache[dev];
     const int64_t wc = K * (G - 1);
-    omega_count_kernel<<<(unsigned)((wc + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, G, slice_ids, seg, seg + K * G);
+    omega_count_kernel<<<(unsigned)((wc + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, G, slice_ids, seg, seg + K * G,
+                                                                 raw ? 1 : 0);
   }
   const int64_t we = K * G;
   omega_emit_kernel<<<(unsigned)((we + 3) / 4), 128, 0, st>>>(seed, K, J, s_k, sp, G, slice_ids, seg,
                                                               seg ? seg + K * G : nullptr, out,
-                                                              static_cast<TailRec*>(recs), cap, nrec, redo);
-  if (seg) cudaFreeAsync(seg, st);
+                                                              static_cast<TailRec*>(recs), cap, nrec, redo,
+                                                              raw ? 1 : 0);
   if (launches) *launches = G > 1 ? 2 : 1;
   return cudaGetLastError();
 }

@@ -183,7 +183,7 @@ class DistributedFit:
         from .compress import check_status, run_stage1, run_stage1_chunked, run_stage2, stage2_params
         from .factors import FitTrace, Parafac2Factors, SliceViews, initial_factors
         from .linalg import RsvdParams
-        from .rng import stage2_omega
+        from .rng import stage2_omega_finish, stage2_omega_launch
         from .solver import assemble_q
         from .tensor import to_device_async
         t = self.tensor if tensor is None else tensor
@@ -196,6 +196,7 @@ class DistributedFit:
         base = RsvdParams(rank=R, seed=opts.seed)
         second, s2 = stage2_params(base, None, R, K, J)
         started = time.perf_counter()
+        om2h = stage2_omega_launch(second.seed, K * R, s2, dev)  # replicated on every rank, ahead of stage 1
         spec = not _exact_omega
         a_signs = torch.empty((t.num_slices, R), dtype=torch.float64, device=dev)  # folded into Q's Pi_k
         if len(t._upload_events) > 1:
@@ -206,7 +207,7 @@ class DistributedFit:
                              a_signs=a_signs)
         A, M_local, rank_found, status = res[:4]
         check = res[4] if len(res) > 4 else None
-        om2 = stage2_omega(second.seed, K * R, s2)  # host, while stage 1 runs
+        om2 = stage2_omega_finish(om2h)  # tail replay + patch, while stage 1 runs
         M = assemble_m(M_local, self.local_ids, K, R, cols=cols)
         D, E, F = run_stage2(M, J, K * R, R, second.seed, s2, om2, status, timings=timings)
         normalize = bool(opts.normalize) if opts.normalize is not None else True

@@ -129,9 +129,7 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
     cap = max(4096, 8 * K + n * max(widths) * K // 1000)
     bufs = _scratch(device, K, cap)
-    recs, nrec, redo = bufs["recs"], bufs["nrec"], bufs["redo"]
-    nrec.zero_()
-    redo.zero_()
+    recs, nrec, redo = bufs["recs"], bufs["nrec"], bufs["redo"]  # zeroed by dp2_omega_generate
     vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
     _lib.check(_lib.lib().dp2_omega_generate(C.c_uint64(seed & _MASK64), K, n, vp(s_dev), sp, vp(ids), vp(out),
                                              vp(recs), cap, vp(nrec), vp(redo),
@@ -190,3 +188,66 @@ def stage2_omega(seed, rows, width):
     """Omega_2 (rows x width), one stream seeded ``seed`` (P/compress.py:109-111)."""
     g = np.random.Generator(np.random.PCG64(seed & _MASK64))
     return g.standard_normal((rows, width))
+
+
+def stage2_omega_launch(seed, rows, width, device):
+    """Enqueue Omega_2 on the device (``dp2_omega_generate_stream``: the one
+    stream split into segments parsed in parallel, stitched exactly) and the
+    readback of its tail records; ``stage2_omega_finish`` completes it.
+    Launched ahead of stage 1, it leaves the host free while stage 1 runs."""
+    return _stage2_omega_enqueue(seed, rows, width, device, torch.cuda.current_stream(device))
+
+
+def _stage2_omega_enqueue(seed, rows, width, device, main):
+    import ctypes as C
+
+    from . import _lib
+    from .tensor import to_device_async
+    out = torch.empty((rows, width), dtype=torch.float64, device=device)
+    w_dev = to_device_async(np.array([width], np.int32), torch.int32, device)
+    cap = max(4096, rows * width // 1000)
+    bufs = _scratch(device, 1, cap)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(_lib.lib().dp2_omega_generate_stream(C.c_uint64(seed & _MASK64), rows, width, vp(w_dev), vp(out),
+                                                    vp(bufs["recs"]), cap, vp(bufs["nrec"]), vp(bufs["redo"]),
+                                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+               "omega_stream")
+    bufs["nrec_h"].copy_(bufs["nrec"], non_blocking=True)
+    bufs["redo_h"].copy_(bufs["redo"], non_blocking=True)
+    bufs["recs_h"].copy_(bufs["recs"], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream())
+    return dict(out=out, ev=ev, bufs=bufs, cap=cap, seed=seed, rows=rows, width=width, keep=w_dev, main=main)
+
+
+def stage2_omega_finish(h, stats=None):
+    """Wait for Omega_2's records only (its event, not the stream), replay
+    the tail draws with libm log1p (dp2_omega_replay) and patch the device
+    matrix in place (stream-ordered): byte-exact with ``stage2_omega``.  A
+    record overflow or a differing acceptance decision regenerates it with
+    NumPy (never expected)."""
+    import ctypes as C
+
+    from . import _lib
+    from .tensor import to_device_async
+    h["ev"].synchronize()
+    bufs, out, cap = h["bufs"], h["out"], h["cap"]
+    count = int(bufs["nrec_h"].numpy()[0])
+    redo = count > cap or bool(bufs["redo_h"].numpy()[0])
+    if count and not redo:
+        r = bufs["recs_h"][:count].numpy().view(_REC).reshape(-1)
+        vals = np.empty(r.size)
+        okv = np.empty(r.size, dtype=np.int32)
+        _lib.check(_lib.lib().dp2_omega_replay(C.c_void_p(r.ctypes.data), r.size,
+                                               vals.ctypes.data_as(C.POINTER(C.c_double)),
+                                               okv.ctypes.data_as(C.POINTER(C.c_int32))), "omega_replay")
+        if okv.all():
+            idx = to_device_async(np.ascontiguousarray(r["index"]), torch.int64, out.device)
+            out.view(-1).index_copy_(0, idx, to_device_async(vals, torch.float64, out.device))
+        else:
+            redo = True
+    if redo:
+        out.copy_(torch.from_numpy(stage2_omega(h["seed"], h["rows"], h["width"])))
+    if stats is not None:
+        stats.update(omega2_tail_events=count, omega2_host_regenerated=int(redo))
+    return out

@@ -171,10 +171,9 @@ def _als_collect(launched, synced=False):
     if not synced:
         torch.cuda.current_stream().synchronize()
     check_status(host["status"], "fit_dpar2")
-    n = int(host["iters"][0])
-    tr = host["trace"][:n].tolist()
-    ts = host["tstamp"][:n + 1].numpy()
-    secs = list(np.diff(ts) * 1e-9)
+    n = int(host["iters"].numpy()[0])
+    tr = host["trace"].numpy()[:n].tolist()
+    secs = (np.diff(host["tstamp"].numpy()[:n + 1]) * 1e-9).tolist()
     return H, V, W, polar, tr, secs
 
 

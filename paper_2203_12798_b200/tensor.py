@@ -367,12 +367,21 @@ class IrregularTensor:
         return self._sqnorm
 
 
+_STATUS_TEMPLATE = {}
+
+
 def new_status(dev):
-    # device-side fills: no host copy, so no implicit stream synchronisation
-    st = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int64, device=dev)
-    st[0:1].fill_(_lib.INT64_MAX)
-    st[2:4].fill_(_lib.INT64_MAX)
-    return st
+    """Fresh device status block (index words INT64_MAX, counters 0): one
+    device-to-device clone of a cached template (no host copy, so no implicit
+    stream synchronisation)."""
+    key = str(dev)
+    tpl = _STATUS_TEMPLATE.get(key)
+    if tpl is None:
+        tpl = torch.zeros(_lib.STATUS_WORDS, dtype=torch.int64, device=dev)
+        tpl[0:1].fill_(_lib.INT64_MAX)
+        tpl[2:4].fill_(_lib.INT64_MAX)
+        _STATUS_TEMPLATE[key] = tpl
+    return tpl.clone()
 
 
 _SMALL_KEEP = []          # (pinned source, completion event) of small uploads

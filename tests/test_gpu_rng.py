@@ -44,3 +44,18 @@ def test_device_omega_slice_ids():
     dev = omega_device(3, 40, [12] * 4, 16, torch.device("cuda"), slice_ids=ids).cpu().numpy()
     host = omega_host(3, 40, [12] * 4, 16, slice_ids=ids).numpy()
     assert dev.tobytes() == host.tobytes()
+
+
+@pytest.mark.parametrize("seed,rows,width", [(0, 10000, 20), (2**64 - 3, 333, 7), (77, 50000, 40), (5, 1, 1),
+                                             (123456789, 4096, 13)])
+def test_device_stage2_omega_matches_numpy_bytes(seed, rows, width):
+    """The stage-2 sketch matrix (one stream, P/compress.py:109-111) generated
+    by segments on the device, tail draws replayed and patched: byte-exact."""
+    import torch
+    from paper_2203_12798_b200.rng import stage2_omega, stage2_omega_finish, stage2_omega_launch
+    stats = {}
+    h = stage2_omega_launch(seed, rows, width, torch.device("cuda"))
+    dev = stage2_omega_finish(h, stats).cpu().numpy()
+    assert dev.tobytes() == stage2_omega(seed, rows, width).tobytes(), stats
+    if rows * width >= 1e6:
+        assert stats["omega2_tail_events"] > 50 and stats["omega2_host_regenerated"] == 0
