@@ -356,19 +356,25 @@ DP2_DEV float rsqrt_approx(float x) {
 // convergence leaves ~1e-12 after it).  Returns the sweeps used (cap + 1
 // when not converged).  Measured on B200 (tools/fp64_probe.cu): ~630 cycles
 // per round at R = 10, about half of it the angle's dependent chain.
+// ``n`` (<= R): the live columns -- the tournament pairs only those (a
+// padded register width R with zero columns n.. needs no rotations).
 template <int R, bool WITHV, bool LOOSE = false>
-DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
+DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R], int n = R) {
   // stop threshold on the largest relative off-diagonal seen in a sweep
   // (squared): 1e-6 -> ~1e-12 left after it; LOOSE: 1e-4 -> ~1e-8
   constexpr float STOP2 = LOOSE ? 1e-8f : 1e-12f;
-  constexpr int N = R + (R & 1), CAP = 40;
+  constexpr int CAP = 40;
+  const int N = n + (n & 1);
   constexpr double TOL = 4.0 * R * 2.220446049250313e-16, TOL2 = TOL * TOL;
   const int lane = threadIdx.x & 31;
+  // round-robin partner (2 r - lane) mod (N - 1), advanced by 2 per round
+  const int base0 = N > 1 ? (2 * (N - 1) - lane % (N - 1)) % (N - 1) : 0;
   for (int sw = 0; sw < CAP; ++sw) {
     bool big = false;
+    int pr = base0;
 #pragma unroll 1
-    for (int r = 0; r < N - 1; ++r) {
-      int pj = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+    for (int r = 0; r < N - 1; ++r, pr = (pr + 2 >= N - 1) ? pr + 2 - (N - 1) : pr + 2) {
+      int pj = pr;
       pj = (lane == r) ? N - 1 : pj;
       pj = (lane == N - 1) ? r : pj;
       const int p = lane < N ? pj : lane;
@@ -431,15 +437,17 @@ DP2_DEV int jacobi_cols(double (&a)[R], double (&v)[R]) {
 // latencies); it stops as below or after ``cap`` sweeps.  The caller
 // re-orthonormalises V in fp64 and finishes with jacobi_cols.
 template <int R>
-DP2_DEV int jacobi_cols_f32(float (&a)[R], float (&v)[R], int cap) {
-  constexpr int N = R + (R & 1);
+DP2_DEV int jacobi_cols_f32(float (&a)[R], float (&v)[R], int cap, int n = R) {
+  const int N = n + (n & 1);
   constexpr float TOL2 = 1e-11f, STOP2 = 1e-6f;  // rotate above fp32 noise; stop after a sweep with max ratio < 1e-3
   const int lane = threadIdx.x & 31;
+  const int base0 = N > 1 ? (2 * (N - 1) - lane % (N - 1)) % (N - 1) : 0;
   for (int sw = 0; sw < cap; ++sw) {
     bool big = false;
+    int pr = base0;
 #pragma unroll 1
-    for (int r = 0; r < N - 1; ++r) {
-      int pj = (2 * r - lane + 2 * (N - 1)) % (N - 1);
+    for (int r = 0; r < N - 1; ++r, pr = (pr + 2 >= N - 1) ? pr + 2 - (N - 1) : pr + 2) {
+      int pj = pr;
       pj = (lane == r) ? N - 1 : pj;
       pj = (lane == N - 1) ? r : pj;
       const int p = lane < N ? pj : lane;

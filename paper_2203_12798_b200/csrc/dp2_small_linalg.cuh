@@ -181,9 +181,12 @@ template <int SP>
 DP2_DEV bool eig_sym_reg(double* A, int lda, double* U, int ldu, int n) {
   const int lane = threadIdx.x & 31;
   double a[SP], dummy[SP];
+  // (fp64 throughout: these are Gram-type matrices whose condition number is
+  // squared -- fp32 sweeps cannot resolve the small eigenvalues, measured
+  // slower than fp64 alone)
 #pragma unroll
   for (int i = 0; i < SP; ++i) a[i] = (lane < n && i < n) ? A[i * lda + lane] : 0.0;
-  const int sw = jacobi_cols<SP, false>(a, dummy);
+  const int sw = jacobi_cols<SP, false>(a, dummy, n);
   double s2 = 0.0;
 #pragma unroll
   for (int i = 0; i < SP; ++i) s2 = fma(a[i], a[i], s2);
