@@ -259,6 +259,12 @@ int dp2_convergence_metric(const double* theta, const double* D, const double* E
                            int64_t J, int32_t R, const double* H, const double* V, const double* W,
                            double* out, void* ws, size_t ws_bytes, void* stream);
 
+/* Device -> pageable host copy at link speed (the NumPy readback of Q,
+ * P/solver.py:186-189 returns host arrays): chunks through a persistent
+ * pinned staging ring, copied out by a persistent host thread team while the
+ * next chunks are in flight.  Returns after the data is in dst_host. */
+int dp2_d2h_staged(void* dst_host, const void* src_dev, size_t nbytes, void* stream);
+
 /* ------------------------------------------------------------------ outputs
  * Q_k = A_k (Z_k P_k^T) for every slice (P/solver.py:186-189). */
 int dp2_assemble_q(const dp2_store* st, const double* A, int32_t R, const double* polar,

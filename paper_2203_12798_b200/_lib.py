@@ -47,6 +47,7 @@ _SIGS = {
                                 P(c_i64)]),
     "dp2_derived_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "dp2_omega_generate_stream": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
+    "dp2_d2h_staged": (c_i32, [c_vp, c_vp, c_sz, c_vp]),
     "dp2_omega_generate": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_vp]),
     "dp2_omega_replay": (c_i32, [c_vp, c_i64, P(c_f64), P(c_i32)]),

@@ -201,6 +201,12 @@ int dp2_omega_generate_stream(uint64_t seed, int64_t rows, int32_t width, const 
   return e == cudaSuccess ? ok(launches) : fail(e, "dp2_omega_generate_stream");
 }
 
+int dp2_d2h_staged(void* dst_host, const void* src_dev, size_t nbytes, void* stream) {
+  if ((!dst_host || !src_dev) && nbytes) return fail_arg("null buffer");
+  cudaError_t e = dp2::d2h_staged(dst_host, src_dev, nbytes, S(stream));
+  return e == cudaSuccess ? ok(0) : fail(e, "dp2_d2h_staged");
+}
+
 int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok_out) {
   if (count < 0 || (count && (!recs || !vals || !ok_out))) return fail_arg("invalid replay arguments");
   constexpr double kR = 3.6541528853610087963519472518, kInvR = 0.27366123732975827203338247596;

@@ -75,6 +75,7 @@ cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int s
                       double* out, void* recs, int cap, int32_t* nrec, int32_t* redo, cudaStream_t st, int* launches = nullptr,
                       bool raw = false);
 size_t tail_record_bytes();
+cudaError_t d2h_staged(void* dst, const void* src, size_t n, cudaStream_t st);
 uint64_t derived_seed_host(uint64_t seed, uint64_t index);
 
 // shared small kernels (stage 1 / stage 2)

@@ -110,9 +110,6 @@ class Parafac2Factors:
         return Parafac2Factors(H=H, V=V, W=W, Q=[qp[a:b] for a, b in zip(bounds[:-1], bounds[1:])], Q_packed=qp)
 
 
-_STAGE = {}
-
-
 def prefaulted_empty(shape, dtype, threads=None):
     """np.empty whose pages are already touched (parallel zero fill): run in
     the background while the GPU finishes, it takes the first-touch page
@@ -128,52 +125,29 @@ def prefaulted_empty(shape, dtype, threads=None):
     return out
 
 
-def device_to_numpy(t, chunk_bytes=32 << 20, nbuf=4, threads=None, out=None):
-    """Large device tensor -> new NumPy array at PCIe speed: chunked async D2H
-    into a ring of ``nbuf`` reused pinned staging buffers, every chunk copied
-    out by all host threads while the following chunks are in flight.  (A
-    pageable destination would go through the driver's slow staging path; a
-    fresh pinned allocation per call costs ~0.5 ms/MB to pin -- far more than
-    the copy.)"""
-    import os
+def device_to_numpy(t, out=None):
+    """Large device tensor -> NumPy array at link speed (``dp2_d2h_staged``:
+    chunked async D2H through a persistent pinned staging ring, each landed
+    chunk copied out by a persistent host thread team while the next ones are
+    in flight).  A pageable destination would go through the driver's slow
+    staging path; a fresh pinned allocation costs ~0.5 ms/MB to pin -- far
+    more than the copy.  ``out``: preallocated (ideally pre-faulted)
+    destination."""
+    import ctypes as C
 
     import torch
-    from concurrent.futures import ThreadPoolExecutor
-    n = t.numel() * t.element_size()
-    if n <= chunk_bytes:
-        return t.cpu().numpy()
-    threads = threads or min(16, os.cpu_count() or 1)
-    dev = t.device
-    if _STAGE.get("key") != (chunk_bytes, nbuf, threads):
-        _STAGE["buf"] = [torch.empty(chunk_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(nbuf)]
-        _STAGE["ev"] = [torch.cuda.Event() for _ in range(nbuf)]
-        _STAGE["pool"] = ThreadPoolExecutor(threads)
-        _STAGE["key"] = (chunk_bytes, nbuf, threads)
-    bufs, evs, pool = _STAGE["buf"], _STAGE["ev"], _STAGE["pool"]
-    src = t.contiguous().view(-1).view(torch.uint8)
+
+    from . import _lib
+    src = t.contiguous()
     if out is None:
         out = np.empty(tuple(t.shape), dtype={torch.float64: np.float64, torch.float32: np.float32,
                                               torch.int64: np.int64, torch.int32: np.int32}[t.dtype])
-    dst = out.reshape(-1).view(np.uint8)
-    chunks = [(o, min(chunk_bytes, n - o)) for o in range(0, n, chunk_bytes)]
-    with torch.cuda.device(dev):
-        stream = torch.cuda.current_stream()
-
-        def issue(i):
-            o, nb = chunks[i]
-            bufs[i % nbuf][:nb].copy_(src[o:o + nb], non_blocking=True)
-            evs[i % nbuf].record(stream)
-
-        for i in range(min(nbuf, len(chunks))):
-            issue(i)
-        for i, (o, nb) in enumerate(chunks):
-            b = bufs[i % nbuf].numpy()
-            evs[i % nbuf].synchronize()
-            step = -(-nb // threads)
-            list(pool.map(lambda a: np.copyto(dst[o + a:o + min(nb, a + step)], b[a:min(nb, a + step)]),
-                          range(0, nb, step)))
-            if i + nbuf < len(chunks):
-                issue(i + nbuf)
+    if not out.flags.c_contiguous or out.nbytes != src.numel() * src.element_size():
+        raise ValueError("out must be a C-contiguous array of the tensor's size")
+    with torch.cuda.device(src.device):
+        _lib.check(_lib.lib().dp2_d2h_staged(C.c_void_p(out.ctypes.data), C.c_void_p(src.data_ptr()),
+                                             src.numel() * src.element_size(),
+                                             C.c_void_p(torch.cuda.current_stream().cuda_stream)), "d2h_staged")
     return out
 
 
