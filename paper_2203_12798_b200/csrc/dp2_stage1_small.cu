@@ -19,6 +19,7 @@
 #include "dp2_internal.h"
 #include "dp2_small_linalg.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -784,10 +785,15 @@ template <int SP>
 // sgn_out[k][r]: the sign A's column r takes (the candidate's sign for r below
 // the slice's numerical rank, +1 for the columns complete_kernel replaces);
 // P and M take the candidate's sign for every column.
-__global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece, const double* cand_abs,
+// grid (K, row blocks): every block of slice k derives the slice's signs from
+// the candidates (a few reads), the first one records them; each block forms
+// M's rows for its share of j with P signed in shared memory (P itself is not
+// needed signed afterwards).
+__global__ void __launch_bounds__(128) signs_m_kernel(const int32_t* slice_piece, const double* cand_abs,
                                                        const int64_t* cand_row, const int32_t* cand_neg,
-                                                       double* Pm, const double* Ct, int K, int J, int sp, int R,
-                                                       const int32_t* rank_found, double* sgn_out, double* M) {
+                                                       const double* Pm, const double* Ct, int K, int J, int sp,
+                                                       int R, const int32_t* rank_found, double* sgn_out,
+                                                       double* M) {
   extern __shared__ __align__(16) double sm[];
   double* Ps = sm;  // sp x R (signed)
   __shared__ double sgn[64];
@@ -803,20 +809,16 @@ __global__ void __launch_bounds__(256) signs_m_kernel(const int32_t* slice_piece
       if (va > ba || (va == ba && ra < br)) { ba = va; br = ra; bn = cand_neg[(size_t)p * R + r]; }
     }
     sgn[r] = bn ? -1.0 : 1.0;
-    sgn_out[(size_t)k * R + r] = r < rank_found[k] ? sgn[r] : 1.0;
+    if (blockIdx.y == 0) sgn_out[(size_t)k * R + r] = r < rank_found[k] ? sgn[r] : 1.0;
   }
   __syncthreads();
-  double* Pk = Pm + (size_t)k * sp * R;
-  for (int i = tid; i < sp * R; i += blockDim.x) {
-    const double v = Pk[i] * sgn[i % R];
-    Pk[i] = v;
-    Ps[i] = v;
-  }
+  const double* Pk = Pm + (size_t)k * sp * R;
+  for (int i = tid; i < sp * R; i += blockDim.x) Ps[i] = Pk[i] * sgn[i % R];
   __syncthreads();
   const double* C = Ct + (size_t)k * J * sp;
   const int64_t KR = (int64_t)K * R;
   // thread = row j of C (16 B loads), the slice's R outputs of M's row j
-  for (int j = tid; j < J; j += blockDim.x) {
+  for (int j = blockIdx.y * blockDim.x + tid; j < J; j += gridDim.y * blockDim.x) {
     double cr[SP];
     const double2* src = reinterpret_cast<const double2*>(C + (size_t)j * SP);
 #pragma unroll
@@ -900,8 +902,8 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
     a_cand_kernel<double, SP><<<P, 256, as, stream>>>(y2, st->row_off, st->piece_slice, st->piece_row0,
                                                       st->piece_rows, s_dev, Pm, R, A, cand_abs, cand_row, cand_neg);
   }
-  signs_m_kernel<SP><<<K, 256, (size_t)SP * R * 8, stream>>>(st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K,
-                                                          J, SP, R, rank_out, sA, M);
+  signs_m_kernel<SP><<<dim3(K, std::min(16, (J + 127) / 128)), 128, (size_t)SP * R * 8, stream>>>(
+      st->slice_piece, cand_abs, cand_row, cand_neg, Pm, Ct, K, J, SP, R, rank_out, sA, M);
   if (!a_signs)
     apply_signs_kernel<<<P, 256, 0, stream>>>(st->piece_slice, st->piece_row0, st->piece_rows, sA, R, A);
   return cudaGetLastError();
