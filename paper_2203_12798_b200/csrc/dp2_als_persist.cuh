@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(PsCfg<R>::MAXW * 32, 1) als_persist_kernel(PsA
     nh[e] = 1.0;
   }
   __syncthreads();
+  __shared__ int vfast;  // the V solve's pinv was done during barrier 2
+  if (threadIdx.x == 0) vfast = 0;
   double prev_e = 0.0;
   int it = 0;
   for (; it < p.max_iters; ++it) {
@@ -420,17 +422,41 @@ __global__ void __launch_bounds__(PsCfg<R>::MAXW * 32, 1) als_persist_kernel(PsA
     }
     ps_group_fold<2 * RR>(p.slots, p.gslots, p.gcnt, wscr, Cf::WTOT);
     PS_STAMP(4);
-    ps_grid_barrier(p.bar, bar_target);
+    // grid barrier 2, with the V solve's pinv computed while thread 0 waits:
+    // its matrix (W''^T W'') o (H^T H) is known before the barrier -- W'' =
+    // W diag(nh), and W^T W came with solve_h's reduction (red[RR..], intact
+    // until this barrier's reduction).  Warp 1 (warp 0 with one warp) runs
+    // the register Gauss-Jordan; if it declines, solve_v takes the usual path.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bar_target += gridDim.x;
+      __threadfence();
+      atomicAdd(p.bar, 1u);
+    }
+    if constexpr (R >= 2 && R <= 16) {
+      if (wib == (WPB > 1 ? 1 : 0)) {
+        for (int e = lane; e < RR; e += 32) M[e] = (red[RR + e] * nh[e / R]) * nh[e % R] * HtH[e];
+        __syncwarp();
+        const bool okk = warp_gj_inverse<R>(M, Pv);
+        if (lane == 0) vfast = okk ? 1 : 0;
+      }
+    }
+    if (threadIdx.x == 0) {
+      while ((int)(ld_acquire_u32(p.bar) - bar_target) < 0) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
     PS_STAMP(5);
     // ---------------- solve_v (every CTA), V = D C implicit
     ps_reduce_slots<2 * RR>(p.gslots, ngrp, wscr, Cf::WTOT, red);  // red = [summed | W''W'']
     PS_STAMP(10);
     for (int e = threadIdx.x; e < RR; e += blockDim.x) {
-      M[e] = red[RR + e] * HtH[e];
+      if (!vfast) M[e] = red[RR + e] * HtH[e];
       Y[e] = Es[e / R] * red[e];  // E * summed
     }
     __syncthreads();
-    block_pinv_sym<R>(M, U, Pv, R, csc, p.status);
+    if (!vfast) block_pinv_sym<R>(M, U, Pv, R, csc, p.status);
     cta_mm<R, false, false>(Y, Pv, X);   // EP = (E * summed) pinv
     cta_mm<R, false, false>(GD, X, Y);   // G_D EP
     for (int c = threadIdx.x; c < R; c += blockDim.x) {
