@@ -192,8 +192,17 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
     Z[r * LD + c] = (r < J && c < s) ? Y2[(size_t)r * s + c] : 0.0;
   }
   __syncthreads();
+  // Shifted CholeskyQR3: the power iteration makes Y2 = M M^T M Omega
+  // ill-conditioned (plain CholQR fails its pivot floor on such inputs), so
+  // the first pass factors G + 11 (J s + s (s + 1)) u ||Y||_F^2 I -- always
+  // positive definite, leaving kappa ~ u^-1/2 -- and two plain passes then
+  // orthonormalise to rounding.  A failure past that takes CGS2.  (Q2 enters
+  // stage 2 only through its range.)
+  // mode: 1 shifted, 2 plain, 3 last plain (pivot floor 1e-3), 4 done
+  // (mode 0, a plain first attempt falling back to 1, is kept for reference)
   bool chol = true;
-  for (int pass = 0; pass < 2 && chol; ++pass) {
+  int mode = 1;
+  while (mode < 4) {
     double acc[NBLK][2];
 #pragma unroll
     for (int b = 0; b < NBLK; ++b) acc[b][0] = acc[b][1] = 0.0;
@@ -201,12 +210,26 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
     gram_store<SP>(acc, wpart, G);
     __syncthreads();
     if (warp == 0) {
-      const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, pass == 0 ? 1e-12 : 1e-3);
+      if (mode == 1) {
+        double tr = (tid < s) ? G[tid * SP + tid] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+        const double shift = 11.0 * ((double)J * s + (double)s * (s + 1)) * 1.1102230246251565e-16 * tr;
+        if (tid < s) G[tid * SP + tid] += shift;
+        __syncwarp();
+      }
+      const double floor_rel = mode == 0 ? 1e-12 : (mode == 3 ? 1e-3 : 0.0);
+      const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, floor_rel);
       if (tid == 0) ok_s = okk;
     }
     __syncthreads();
-    chol = ok_s != 0;
-    if (!chol) break;
+    if (!ok_s) {
+      if (mode == 0) {  // Z untouched: retry shifted
+        mode = 1;
+        continue;
+      }
+      chol = false;
+      break;
+    }
     for (int r = tid; r < J; r += 256) {
       double q[SP];
 #pragma unroll
@@ -223,6 +246,7 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
         if (i < s) Z[r * LD + i] = q[i];
     }
     __syncthreads();
+    mode = mode == 0 ? 3 : mode + 1;
   }
   if (!chol) {
     for (int i = tid; i < J * SP; i += 256) {
