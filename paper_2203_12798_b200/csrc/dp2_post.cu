@@ -86,7 +86,7 @@ template <int R>
 __global__ void __launch_bounds__(256) assemble_q_rows_kernel(const double* A, const int32_t* piece_slice,
                                                               const int64_t* piece_row0, const int32_t* piece_rows,
                                                               const double* polar, const double* sgn, double* Q) {
-  __shared__ double pis[R * R];
+  __shared__ __align__(16) double pis[R * R];
   const int p = blockIdx.x;
   const int64_t k = piece_slice[p];
   // with sgn (the deferred column signs of A, dp2_stage1_signs): row d of
@@ -110,12 +110,24 @@ __global__ void __launch_bounds__(256) assemble_q_rows_kernel(const double* A, c
 #pragma unroll
       for (int d = 0; d < R; ++d) x[d] = __ldg(a + d);
     }
+    // y[c] = sum_d x[d] Pi[d][c], accumulated over d in order for every c
+    // (the same fma chain per c as assemble_q_kernel); Pi's row d is read as
+    // 16-byte pairs (half the shared-memory reads of a column-wise loop)
 #pragma unroll
-    for (int c = 0; c < R; ++c) {
-      double acc = 0.0;
+    for (int c = 0; c < R; ++c) y[c] = 0.0;
 #pragma unroll
-      for (int d = 0; d < R; ++d) acc = fma(x[d], pis[d * R + c], acc);
-      y[c] = acc;
+    for (int d = 0; d < R; ++d) {
+      if constexpr (R % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < R / 2; ++c) {
+          const double2 pp = reinterpret_cast<const double2*>(pis + d * R)[c];
+          y[2 * c] = fma(x[d], pp.x, y[2 * c]);
+          y[2 * c + 1] = fma(x[d], pp.y, y[2 * c + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < R; ++c) y[c] = fma(x[d], pis[d * R + c], y[c]);
+      }
     }
     double* q = Q + (r0 + i) * R;
     if constexpr (R % 2 == 0) {
