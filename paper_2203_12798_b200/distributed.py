@@ -79,7 +79,7 @@ def replicated_als(F, D, E, K, J, R, h, v, w, max_iters, tol, normalize):
     """The single-GPU ALS loop (``dp2_als_run``: one cooperative launch for
     R <= 16) on the FULL compressed tensor (global K); returns device H, V, W
     (K x R), polar (K x R x R), trace, tstamp, iters, status."""
-    from .tensor import new_status, to_device_async
+    from .tensor import new_status, stream_ptr, to_device_async
     dev = D.device
     lib = _lib.lib()
     H = to_device_async(np.ascontiguousarray(h), torch.float64, dev)
@@ -94,7 +94,7 @@ def replicated_als(F, D, E, K, J, R, h, v, w, max_iters, tol, normalize):
     vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     _lib.check(lib.dp2_als_run(vp(F), vp(D), vp(E), K, J, R, vp(H), vp(V), vp(W), vp(polar), max_iters, float(tol),
                                int(bool(normalize)), vp(trace), vp(tstamp), vp(iters), 0, vp(ws), ws.numel(),
-                               vp(status), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "als_run")
+                               vp(status), stream_ptr()), "als_run")
     return H, V, W, polar, trace, tstamp, iters, status
 
 
@@ -134,6 +134,7 @@ class GpuAlsOps:
         self.status = new_status(dev)
 
     def phase(self, ph, it=0, red_in=None):
+        from .tensor import stream_ptr
         vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
         n = 2 * self.R * self.R if ph in (1, 3) else 1
         out = self.red[:n] if ph in (1, 3, 5) else None
@@ -141,7 +142,7 @@ class GpuAlsOps:
             ph, vp(self.F), vp(self.D), vp(self.E), self.K, self.J, self.R, vp(self.H), vp(self.V), vp(self.W),
             vp(self.polar), it, self.tol, self.normalize, vp(self.trace), vp(self.tstamp), vp(self.iters),
             vp(red_in), vp(out), vp(self.ws), self.ws.numel(), vp(self.status),
-            C.c_void_p(torch.cuda.current_stream().cuda_stream)), f"als_phase{ph}")
+            stream_ptr()), f"als_phase{ph}")
         return out.clone() if out is not None else None
 
 

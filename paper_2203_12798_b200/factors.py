@@ -138,6 +138,7 @@ def device_to_numpy(t, out=None):
     import torch
 
     from . import _lib
+    from .tensor import stream_ptr
     src = t.contiguous()
     if out is None:
         out = np.empty(tuple(t.shape), dtype={torch.float64: np.float64, torch.float32: np.float32,
@@ -147,7 +148,7 @@ def device_to_numpy(t, out=None):
     with torch.cuda.device(src.device):
         _lib.check(_lib.lib().dp2_d2h_staged(C.c_void_p(out.ctypes.data), C.c_void_p(src.data_ptr()),
                                              src.numel() * src.element_size(),
-                                             C.c_void_p(torch.cuda.current_stream().cuda_stream)), "d2h_staged")
+                                             stream_ptr()), "d2h_staged")
     return out
 
 

@@ -123,7 +123,7 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     from . import _lib
     K = len(widths)
     out = torch.empty((K, n, sp), dtype=torch.float64, device=device)
-    from .tensor import to_device_async
+    from .tensor import stream_ptr, to_device_async
     if s_dev is None:
         s_dev = to_device_async(list(widths), torch.int32, device)
     ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
@@ -133,7 +133,7 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
     _lib.check(_lib.lib().dp2_omega_generate(C.c_uint64(seed & _MASK64), K, n, vp(s_dev), sp, vp(ids), vp(out),
                                              vp(recs), cap, vp(nrec), vp(redo),
-                                             C.c_void_p(torch.cuda.current_stream().cuda_stream)), "omega")
+                                             stream_ptr()), "omega")
     # one readback: record count, per-slice redo flags and the records
     nrec_h, redo_h_t, recs_h = bufs["nrec_h"], bufs["redo_h"], bufs["recs_h"]
     nrec_h.copy_(nrec, non_blocking=True)
@@ -145,7 +145,7 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
             from concurrent.futures import ThreadPoolExecutor
             _REPLAY_POOL = ThreadPoolExecutor(1)
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream())
+        ev.record()
         fut = _REPLAY_POOL.submit(_replay_check, ev, nrec_h, redo_h_t, recs_h, cap)
         bufs["busy"] = fut
         return out, fut
@@ -198,25 +198,31 @@ def stage2_omega_launch(seed, rows, width, device):
     return _stage2_omega_enqueue(seed, rows, width, device, torch.cuda.current_stream(device))
 
 
+_WIDTH_DEV = {}
+
+
 def _stage2_omega_enqueue(seed, rows, width, device, main):
     import ctypes as C
 
     from . import _lib
-    from .tensor import to_device_async
+    from .tensor import stream_ptr, to_device_async
     out = torch.empty((rows, width), dtype=torch.float64, device=device)
-    w_dev = to_device_async(np.array([width], np.int32), torch.int32, device)
+    key = (str(device), int(width))
+    w_dev = _WIDTH_DEV.get(key)
+    if w_dev is None:  # the width as a device int32, uploaded once per (device, width)
+        w_dev = _WIDTH_DEV[key] = to_device_async(np.array([width], np.int32), torch.int32, device)
     cap = max(4096, rows * width // 1000)
     bufs = _scratch(device, 1, cap)
     vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     _lib.check(_lib.lib().dp2_omega_generate_stream(C.c_uint64(seed & _MASK64), rows, width, vp(w_dev), vp(out),
                                                     vp(bufs["recs"]), cap, vp(bufs["nrec"]), vp(bufs["redo"]),
-                                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+                                                    stream_ptr()),
                "omega_stream")
     bufs["nrec_h"].copy_(bufs["nrec"], non_blocking=True)
     bufs["redo_h"].copy_(bufs["redo"], non_blocking=True)
     bufs["recs_h"].copy_(bufs["recs"], non_blocking=True)
     ev = torch.cuda.Event()
-    ev.record(torch.cuda.current_stream())
+    ev.record()
     return dict(out=out, ev=ev, bufs=bufs, cap=cap, seed=seed, rows=rows, width=width, keep=w_dev, main=main)
 
 

@@ -39,7 +39,9 @@ def device():
 
 
 def stream_ptr():
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """Raw handle of the current CUDA stream (torch's C accessor: no Stream
+    object per call -- a fit passes it a dozen times on its enqueue path)."""
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
 
 
 _COPY_STREAMS = {}
@@ -400,10 +402,9 @@ def to_device_async(values, dtype, dev):
     nbytes = src.numel() * src.element_size()
     if nbytes:
         _lib.check(_lib.lib().dp2_copy_h2d_small(C.c_void_p(out.data_ptr()), C.c_void_p(src.data_ptr()), nbytes,
-                                                  C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)),
-                   "copy_h2d_small")
+                                                  stream_ptr()), "copy_h2d_small")
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(dev))
+        ev.record()
         _SMALL_KEEP.append((src, ev))
         if len(_SMALL_KEEP) > _SMALL_KEEP_MAX:
             _SMALL_KEEP[:] = [(t, e) for t, e in _SMALL_KEEP if not e.query()]
