@@ -199,7 +199,6 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
   // orthonormalise to rounding.  A failure past that takes CGS2.  (Q2 enters
   // stage 2 only through its range.)
   // mode: 1 shifted, 2 plain, 3 last plain (pivot floor 1e-3), 4 done
-  // (mode 0, a plain first attempt falling back to 1, is kept for reference)
   bool chol = true;
   int mode = 1;
   while (mode < 4) {
@@ -217,16 +216,12 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
         if (tid < s) G[tid * SP + tid] += shift;
         __syncwarp();
       }
-      const double floor_rel = mode == 0 ? 1e-12 : (mode == 3 ? 1e-3 : 0.0);
+      const double floor_rel = mode == 3 ? 1e-3 : 0.0;
       const bool okk = chol_reg<SP>(G, SP, L, SP, dinv, s, floor_rel);
       if (tid == 0) ok_s = okk;
     }
     __syncthreads();
     if (!ok_s) {
-      if (mode == 0) {  // Z untouched: retry shifted
-        mode = 1;
-        continue;
-      }
       chol = false;
       break;
     }
@@ -246,7 +241,7 @@ __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, in
         if (i < s) Z[r * LD + i] = q[i];
     }
     __syncthreads();
-    mode = mode == 0 ? 3 : mode + 1;
+    ++mode;
   }
   if (!chol) {
     for (int i = tid; i < J * SP; i += 256) {
