@@ -79,8 +79,12 @@ int64_t dp2_launch_count(int32_t reset);
  * (DMMA) and for fp32 with J <= 512 (tcgen05 tf32 pass), two per SM for the
  * fp32 FFMA pass.  Planning aid for dp2_plan_pieces(nseg). */
 int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms);
-/* fp32 streaming-pass engine: 0 = tcgen05 tf32 tensor cores where eligible
- * (default), 1 = FFMA kernel everywhere.  Returns the previous setting. */
+/* fp32-storage streaming-pass engine: 1 = fp32 FFMA products (default; the
+ * fp32 mode of BASELINE.json), 0 = single-pass tf32 products on tcgen05
+ * tensor cores where eligible (opt-in speed mode: ~5e-4 relative product
+ * error, passes the 1e-3 fp32-mode bound on c2 but not on slices of ~50 rows).
+ * The environment variable DP2_SKETCH_ENGINE sets the initial value.
+ * Returns the previous setting. */
 int32_t dp2_set_sketch_engine(int32_t engine);
 /* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
 int dp2_status_init(int64_t* status_dev, void* stream);

@@ -67,12 +67,26 @@ def greedy_partition(row_counts, workers):
     return sets, loads
 
 
-def _slice_map(fn, n, threads):
-    """P/scheduler.py:85-122 -- slot-per-slice map; results in slice order."""
+def _slice_map(fn, n, threads, groups=None):
+    """P/scheduler.py:85-122 -- slot-per-slice map over worker-owned groups
+    (contiguous chunks by default, P/scheduler.py:54-66); results in slice
+    order."""
     if threads <= 1 or n <= 1:
         return [fn(k) for k in range(n)]
-    with ThreadPoolExecutor(max_workers=threads) as pool:
-        return list(pool.map(fn, range(n)))
+    if groups is None:
+        parts = min(threads, n)
+        base, extra = divmod(n, parts)
+        bounds = np.cumsum([0] + [base + (1 if i < extra else 0) for i in range(parts)])
+        groups = [range(int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:])]
+    out = [None] * n
+
+    def run(group):
+        for k in group:
+            out[k] = fn(k)
+
+    with ThreadPoolExecutor(max_workers=min(threads, len(groups))) as pool:
+        list(pool.map(run, groups))
+    return out
 
 
 # --------------------------------------------------------------------------
@@ -181,7 +195,9 @@ def compress(slices, rank, seed=0, oversampling=None, power_iters=1,
     def one(k):
         return randomized_svd(slices[k], rank, derived_seed(seed, k), oversampling, power_iters)
 
-    trips = _slice_map(one, len(slices), threads)
+    # slices owned per worker by the Alg. 4 LPT plan (P/compress.py:93-94, 105)
+    groups = greedy_partition([x.shape[0] for x in slices], threads)[0] if threads > 1 else None
+    trips = _slice_map(one, len(slices), threads, groups=groups)
     merged = np.concatenate([v * s for (_, s, v) in trips], axis=1)
     over2 = oversampling if stage2_oversampling == "same" else stage2_oversampling
     d, e, f = randomized_svd(merged, rank, derived_seed(seed, len(slices)), over2, power_iters)
@@ -213,62 +229,68 @@ def update_rotations(comp, h, v, w, threads=1):
     return _slice_map(rot, comp.K, threads)
 
 
-def rotated_cores(comp, rots):
+def rotated_cores(comp, rots, threads=1):
     """P/solver.py:67-78 -- Theta_k = (P_k Z_k^T) F_k, stacked (K, R, R)."""
-    return np.stack([(p @ z.T) @ comp.block(k) for k, (z, p, _) in enumerate(rots)])
+    return np.stack(_slice_map(lambda k: (rots[k][1] @ rots[k][0].T) @ comp.block(k), comp.K, threads))
 
 
-def mttkrp_mode1(comp, rots, w, v):
+def mttkrp_mode1(comp, rots, w, v, threads=1):
     """P/solver.py:81-89 (Lemma 1)."""
-    th = rotated_cores(comp, rots)
+    th = rotated_cores(comp, rots, threads)
     cc = core_cols(comp, v)
     return np.einsum("rij,jr->ir", np.einsum("kr,kij->rij", w, th), cc)
 
 
-def mttkrp_mode2(comp, rots, w, h):
+def mttkrp_mode2(comp, rots, w, h, threads=1):
     """P/solver.py:92-100 (Lemma 2)."""
-    th = rotated_cores(comp, rots)
+    th = rotated_cores(comp, rots, threads)
     summed = np.einsum("kr,kar->ar", w, np.einsum("kba,br->kar", th, h))
     return comp.D @ (comp.E[:, None] * summed)
 
 
-def mttkrp_mode3(comp, rots, v, h):
+def mttkrp_mode3(comp, rots, v, h, threads=1):
     """P/solver.py:103-111 (Lemma 3)."""
-    th = rotated_cores(comp, rots)
+    th = rotated_cores(comp, rots, threads)
     cc = core_cols(comp, v)
     return np.einsum("ir,kir->kr", h, np.einsum("kij,jr->kir", th, cc))
 
 
-def update_factors(comp, rots, h, v, w, normalize=True):
+def update_factors(comp, rots, h, v, w, normalize=True, threads=1):
     """P/solver.py:114-130 -- Gauss-Seidel H, V, W sweep with pinv solves."""
-    h = mttkrp_mode1(comp, rots, w, v) @ pinv_small((w.T @ w) * (v.T @ v))
+    h = mttkrp_mode1(comp, rots, w, v, threads) @ pinv_small((w.T @ w) * (v.T @ v))
     if normalize:
         h, w = push_col_norms(h, w)
-    v = mttkrp_mode2(comp, rots, w, h) @ pinv_small((w.T @ w) * (h.T @ h))
+    v = mttkrp_mode2(comp, rots, w, h, threads) @ pinv_small((w.T @ w) * (h.T @ h))
     if normalize:
         v, w = push_col_norms(v, w)
-    w = mttkrp_mode3(comp, rots, v, h) @ pinv_small((v.T @ v) * (h.T @ h))
+    w = mttkrp_mode3(comp, rots, v, h, threads) @ pinv_small((v.T @ v) * (h.T @ h))
     return h, v, w
 
 
-def convergence_metric(comp, rots, h, v, w):
+def convergence_metric(comp, rots, h, v, w, threads=1):
     """P/solver.py:133-149 -- sum_k ||Theta_k E D^T - (H*w_k) V^T||^2,
     reduced in ascending slice order."""
     basis = comp.E[:, None] * comp.D.T
-    parts = []
-    for k, (z, p, _) in enumerate(rots):
+    vt = v.T
+
+    def residual(k):
+        z, p, _ = rots[k]
         buf = ((p @ z.T) @ comp.block(k)) @ basis
-        buf -= (h * w[k]) @ v.T
-        parts.append(float(np.dot(buf.ravel(), buf.ravel())))
-    return float(np.add.reduce(np.asarray(parts)))
+        buf -= (h * w[k]) @ vt
+        return float(np.dot(buf.ravel(), buf.ravel()))
+
+    return float(np.add.reduce(np.asarray(_slice_map(residual, comp.K, threads))))
 
 
 def fit_dpar2(slices, rank, max_iters=32, tol=1e-6, seed=0, normalize=True,
-              oversampling=None, threads=1, comp=None, timings=None):
+              oversampling=None, threads=1, comp=None, timings=None, als_threads=1):
     """P/solver.py:152-190 -- compress once, iterate, stop on
     ``prev == 0 or |prev - e| <= tol * prev``; Q_k = A_k Z_k P_k^T from the
     last iteration.  ``oversampling`` replays the config-4 harness (the
-    reference's fit_dpar2 pins it to the default)."""
+    reference's fit_dpar2 pins it to the default).  ``threads`` are the
+    compression's slice threads, ``als_threads`` the per-slice maps of the
+    iterations (the reference uses one resolved count for both,
+    P/solver.py:162-189; values never depend on either)."""
     if max_iters < 1:
         raise ValueError("max_iters must be >= 1")
     t0 = time.perf_counter()
@@ -279,16 +301,16 @@ def fit_dpar2(slices, rank, max_iters=32, tol=1e-6, seed=0, normalize=True,
     trace, seconds, converged, prev, rots = [], [], False, None, None
     for _ in range(max_iters):
         tick = time.perf_counter()
-        rots = update_rotations(comp, h, v, w, threads=1)
-        h, v, w = update_factors(comp, rots, h, v, w, normalize=normalize)
-        e = convergence_metric(comp, rots, h, v, w)
+        rots = update_rotations(comp, h, v, w, threads=als_threads)
+        h, v, w = update_factors(comp, rots, h, v, w, normalize=normalize, threads=als_threads)
+        e = convergence_metric(comp, rots, h, v, w, threads=als_threads)
         trace.append(e)
         seconds.append(time.perf_counter() - tick)
         if prev is not None and (prev == 0.0 or abs(prev - e) <= tol * prev):
             converged = True
             break
         prev = e
-    q = [comp.bases[k] @ (rots[k][0] @ rots[k][1].T) for k in range(comp.K)]
+    q = _slice_map(lambda k: comp.bases[k] @ (rots[k][0] @ rots[k][1].T), comp.K, als_threads)
     if timings is not None:
         timings.update(preprocess=t1 - t0, iterations=sum(seconds), total=time.perf_counter() - t0)
     return dict(H=h, V=v, W=w, Q=q, objective=trace, seconds=seconds, converged=converged,

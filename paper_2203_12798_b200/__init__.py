@@ -16,7 +16,7 @@ from .scheduler import PartitionPlan, greedy_partition, resolve_threads
 __version__ = "0.1.0"
 
 from .tensor import IrregularTensor  # noqa: E402
-from .compress import CompressedTensor, compress, reconstruct_slice  # noqa: E402
+from .compress import CompressedTensor, compress, reconstruct_slice, set_fp32_products  # noqa: E402
 from .solver import (Rotations, convergence_metric, fit_dpar2, mttkrp_mode1, mttkrp_mode2,  # noqa: E402
                      mttkrp_mode3, rotated_cores, update_factors, update_rotations)
 from .analysis import fitness  # noqa: E402
@@ -25,7 +25,7 @@ from .archive import fit_compressed, load_archive, load_compressed, save_archive
 _LAZY = ["IrregularTensor", "CompressedTensor", "compress", "reconstruct_slice", "fit_dpar2", "update_rotations",
          "rotated_cores", "mttkrp_mode1", "mttkrp_mode2", "mttkrp_mode3", "update_factors", "convergence_metric",
          "fitness", "Rotations", "load_archive", "save_archive", "load_compressed", "save_compressed",
-         "fit_compressed"]
+         "fit_compressed", "set_fp32_products"]
 
 __all__ = sorted(list(_LAZY) + [
     "ArchiveFormatError", "DecompositionError", "DegenerateInputError", "NonFiniteInputError", "NumericFailure", "RankTooLargeError",

@@ -705,7 +705,14 @@ __global__ void __launch_bounds__(256) b_tile_kernel(const double* B, int64_t K,
 }  // namespace tcs
 
 namespace {
-int g_engine = 0;  // 0: tensor cores when eligible, 1: FFMA kernel
+// 0: tf32 tensor cores when eligible (opt-in: single-pass tf32 products),
+// 1: fp32 FFMA kernel (default: fp32 products, the fp32 mode BASELINE.json
+// states).  DP2_SKETCH_ENGINE overrides the default at load time.
+int initial_engine() {
+  const char* e = getenv("DP2_SKETCH_ENGINE");
+  return e && *e ? atoi(e) : 1;
+}
+int g_engine = initial_engine();
 }
 
 void set_sketch_engine(int e) { g_engine = e; }

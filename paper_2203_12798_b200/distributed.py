@@ -158,15 +158,23 @@ class DistributedFit:
     """This rank's shard of a synthetic BASELINE-model tensor, fitted jointly
     with the other ranks (bench.py's N > 1 path)."""
 
-    def __init__(self, cfg, seed, rank, world):
+    def __init__(self, cfg, seed, rank, world, host_slices=None):
+        """``host_slices``: this rank's slices (``synth.generate(cfg, seed,
+        slices=shard)``) to upload; default: draw them on the device."""
         from . import synth
         from .tensor import IrregularTensor
         rows_all, _, _ = synth.shared_factors(cfg, seed)
         shards, loads = shard_slices(rows_all, world)
         self.local_ids = shards[rank]
         self.rank, self.world, self.cfg, self.seed = rank, world, cfg, seed
-        X, rows, _, _ = synth.generate_device(cfg, seed, slices=self.local_ids)
-        self.tensor = IrregularTensor.from_packed(X, rows, cfg.cols)
+        if host_slices is not None:
+            up = IrregularTensor(host_slices, dtype=cfg.dtype)
+            up.wait_upload()
+            rows = up.row_counts
+            self.tensor = IrregularTensor.from_packed(up.X, rows, cfg.cols, dtype=cfg.dtype)
+        else:
+            X, rows, _, _ = synth.generate_device(cfg, seed, slices=self.local_ids)
+            self.tensor = IrregularTensor.from_packed(X, rows, cfg.cols)
         self.local_rows = int(sum(rows))
         self.total_rows = int(sum(rows_all))
         self.total_entries = self.total_rows * cfg.cols

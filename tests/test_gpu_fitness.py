@@ -34,7 +34,7 @@ def test_zero_pass_fitness_fallbacks():
     rng = np.random.default_rng(5)
     xs = [rng.standard_normal((int(m), 25)) for m in rng.integers(10, 90, size=8)]
     d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
-    # fp32 store: M comes from tf32 products -> the streaming pass
+    # fp32 store: M comes from fp32 (or tf32) products -> the streaming pass
     t32 = dp.IrregularTensor([x.astype(np.float32) for x in xs], dtype="f32")
     f32, _ = dp.fit_dpar2(t32, 4, dp.SolverOptions(max_iters=5, tol=0.0))
     assert _zero_pass_terms(t32, f32, d) is None

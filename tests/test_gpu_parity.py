@@ -279,6 +279,14 @@ def test_speculative_omega_redo_path(monkeypatch):
     import importlib
     import paper_2203_12798_b200 as dp
     solver = importlib.import_module("paper_2203_12798_b200.solver")
+    prev = dp.set_fp32_products("tf32")  # the speculative Omega belongs to the tensor-core pass
+    try:
+        _speculative_redo(dp, solver, monkeypatch)
+    finally:
+        dp.set_fp32_products(prev)
+
+
+def _speculative_redo(dp, solver, monkeypatch):
     rng = np.random.default_rng(5)
     xs = [rng.standard_normal((int(m), 64)).astype(np.float32) for m in rng.integers(40, 120, size=9)]
     t = dp.IrregularTensor(xs, dtype="f32")
