@@ -80,12 +80,20 @@ int64_t dp2_launch_count(int32_t reset);
  * fp32 FFMA pass.  Planning aid for dp2_plan_pieces(nseg). */
 int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms);
 /* fp32-storage streaming-pass engine: 1 = fp32 FFMA products (default; the
- * fp32 mode of BASELINE.json), 0 = single-pass tf32 products on tcgen05
- * tensor cores where eligible (opt-in speed mode: ~5e-4 relative product
- * error, passes the 1e-3 fp32-mode bound on c2 but not on slices of ~50 rows).
+ * fp32 mode of BASELINE.json), 2 = fp64 DMMA products on the exactly upcast
+ * values (where dp2_sketch_kind reports 3), 0 = single-pass tf32 products on
+ * tcgen05 tensor cores where eligible (opt-in speed mode: ~5e-4 relative
+ * product error, passes the 1e-3 fp32-mode bound on c2 but not on slices of
+ * ~50 rows).
  * The environment variable DP2_SKETCH_ENGINE sets the initial value.
  * Returns the previous setting. */
 int32_t dp2_set_sketch_engine(int32_t engine);
+/* Which streaming pass a dp2_stream_pass(st, sp, ...) call takes (xsq / gram:
+ * whether the per-piece sums of squares / Y^T Y partials are requested):
+ * 0 = fp64 DMMA per-tile pass, 1 = fp32 FFMA pass, 2 = tf32 tcgen05 pass,
+ * 3 = warp-specialised fp64 DMMA pass (fp64, or fp32 storage with engine 2);
+ * -1 on invalid arguments. */
+int32_t dp2_sketch_kind(const dp2_store* st, int32_t sp, int32_t xsq, int32_t gram);
 /* status block: words 0 and 2/3 <- INT64_MAX, others 0 */
 int dp2_status_init(int64_t* status_dev, void* stream);
 /* Stream-ordered upload of a small PINNED host buffer by a kernel reading it

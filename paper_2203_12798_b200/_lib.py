@@ -41,6 +41,7 @@ _SIGS = {
     "dp2_status_init": (c_i32, [c_vp, c_vp]),
     "dp2_stream_segments": (c_i32, [c_i32, c_i64, c_i32]),
     "dp2_set_sketch_engine": (c_i32, [c_i32]),
+    "dp2_sketch_kind": (c_i32, [P(Store), c_i32, c_i32, c_i32]),
     "dp2_greedy_partition": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i64), P(c_i32), P(c_i64)]),
     "dp2_piece_capacity": (c_i64, [c_i64, c_i32]),
     "dp2_plan_pieces": (c_i32, [P(c_i64), c_i64, c_i32, P(c_i32), P(c_i64), P(c_i32), P(c_i32), P(c_i32),

@@ -294,8 +294,17 @@ int dp2_stream_pass(const dp2_store* st, const double* b_dev, int32_t sp, double
                     double* g_part, double* xsq_part, int64_t* status_dev, void* stream) {
   if (!store_ok(st) || sp < 1 || !b_dev || !out_part) return fail_arg("invalid stream-pass arguments");
   if (g_part && sp > 32) return fail_arg("g_part needs sp <= 32");
+  const int kind = dp2_sketch_kind(st, sp, xsq_part != nullptr, g_part != nullptr);
   cudaError_t e = dp2::run_sketch(st, b_dev, sp, out_part, y_out, xsq_part, status_dev, S(stream), g_part);
-  return e == cudaSuccess ? ok(dp2::sketch_tc_eligible(st, sp) ? 2 : 1) : fail(e, "dp2_stream_pass");
+  return e == cudaSuccess ? ok(kind >= 2 ? 2 : 1) : fail(e, "dp2_stream_pass");
+}
+
+int32_t dp2_sketch_kind(const dp2_store* st, int32_t sp, int32_t xsq, int32_t gram) {
+  if (!store_ok(st) || sp < 1) return -1;
+  if (dp2::sketch_tc_eligible(st, sp)) return 2;
+  const bool s64 = dp2::sketch64_eligible(st, sp, xsq != 0, gram != 0);
+  if (st->dtype == DP2_F64) return s64 ? 3 : 0;
+  return (dp2::sketch_engine() == 2 && s64) ? 3 : 1;
 }
 
 size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
@@ -316,7 +325,9 @@ static int stage1_impl(const dp2_store* st, const double* omega_dev, const int32
   // complete; the tensor-core pass adds its two B-image kernels and
   // gram_y_piece_kernel.  sp > 32: 8 kernels [+ the sign fill].
   const int tc = dp2::sketch_tc_eligible(st, sp) ? 3 : 0;
-  const int n = sp <= 32 ? (a_signs ? 11 : 12) + tc : (a_signs ? 9 : 8);
+  // the warp-specialised DMMA pass adds its B-image kernel per pass
+  const int img = (dp2_sketch_kind(st, sp, 0, 0) == 3 ? 1 : 0) + (dp2_sketch_kind(st, sp, 0, sp <= 32) == 3 ? 1 : 0);
+  const int n = (sp <= 32 ? (a_signs ? 11 : 12) + tc : (a_signs ? 9 : 8)) + img;
   return e == cudaSuccess ? ok(n) : fail(e, "dp2_stage1");
 }
 

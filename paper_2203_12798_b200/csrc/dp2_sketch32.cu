@@ -281,6 +281,8 @@ int sketch32_njs(int J) { return (J + 1023) / 1024; }
 cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                            double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
   if (sketch_tc_eligible(st, sp)) return run_sketch_tc(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
+  if (sketch_engine() == 2 && sketch64_eligible(st, sp, xsq_part != nullptr, g_part != nullptr))
+    return run_sketch64(st, B, sp, out_part, y_out, status, stream, g_part);  // fp64 products on upcast X
   const int J = (int)st->J;
   Sketch32Params prm{};
   prm.X = static_cast<const float*>(st->X);

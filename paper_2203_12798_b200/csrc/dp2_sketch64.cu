@@ -1,0 +1,508 @@
+// Stage-1 streaming sketch pass on the fp64 tensor pipe (DMMA), warp-specialised.
+//
+// Same contract as the other streaming passes (dp2_stage1.cu run_sketch): for
+// every piece p (segment x slice) of the store
+//     out_part[p] (J x sp) = X_p^T (X_p B_k)          (P/linalg.py:124-126 fused)
+// plus, on request, the Y = X_k B_k rows (y_out) and G_p = Y_p^T Y_p (g_part).
+// X is fp64 (the reference's precision) or fp32 (exactly upcast; fp64
+// products), B is fp64 (Omega_k or Q_Z,k).
+//
+// The pass is FP64-compute-bound on B200 (4 s flops per 8 (or 4) bytes of X
+// against a measured 36.9 TF/s DMMA peak and 6.5 TB/s HBM), so the design
+// goal is to keep the DMMA pipe issuing: every role runs its own loop over
+// the CTA's tiles (8 rows) and hands off through mbarriers, never a block-wide
+// barrier.
+//
+//   producer (1 warp)   TMA bulk copies: X rows of tile n into ring stage n % NS
+//                       (padded row stride: conflict-free fragment loads), and
+//                       per piece the slice's B image (fragment-major, one
+//                       bulk copy per quarter of J).
+//   A warps (4)         Y_t (8 x SG) partial over their quarter of J:
+//                       DMMA m8n8k4 with B fragments from the shared image
+//                       (two accumulator sets to halve the dependent chain);
+//                       partial -> ypart ring.
+//   aux (1 warp)        sums the 4 partials -> Y_t (rows past the piece zeroed),
+//                       publishes it in B-fragment layout (yfin ring), flags
+//                       non-finite values (status word 0 = lowest slice: a
+//                       NaN / Inf anywhere in X_k reaches Y), writes Y rows and
+//                       accumulates G = Y^T Y with DMMA (Y^T fragments are
+//                       the B fragments), flushes G per piece.
+//   B warps (16)        Z (J x SG) += X_t^T Y_t for their sixteenth of J, held
+//                       in registers across the piece; flushed per piece.
+//
+// Column groups of SG = 8 NT sketch columns run as separate CTAs (grid.y).
+// Eligible: J <= 512 (B image <= 96 KB + a 3-stage X ring in 227 KB).
+#include "dp2_common.cuh"
+#include "dp2_internal.h"
+
+namespace dp2 {
+namespace s64 {
+
+constexpr int TM = 8;           // rows per tile (one DMMA row block)
+constexpr int NA = 4;           // warps computing Y partials (split of J)
+constexpr int NB = 16;          // warps accumulating Z (split of J)
+constexpr int MBMAX = 4;        // J-blocks of 8 per B warp (J <= 512)
+constexpr int NY = 2;           // ypart / yfin ring depth
+// warp w runs on SM sub-partition w % 4: one A warp and four B warps per
+// sub-partition keep the DMMA work per sub-partition equal
+constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
+constexpr int NWARPS = 2 + NA + NB;
+constexpr int NTHREADS = 32 * NWARPS;
+
+struct Params {
+  const void* X;
+  int64_t ldx;
+  int J, JP, L, sp, ns, rowbytes;
+  const double* img;        // K x ng x (JP/4) x NT x 32 fragment-major B images
+  const int32_t* piece_slice;
+  const int64_t* piece_row0;
+  const int32_t* piece_rows;
+  const int32_t* seg_begin;
+  double* out_part;         // npieces x J x sp
+  double* y_out;            // total_rows x sp or null
+  double* g_part;           // npieces x sp x sp or null (single column group)
+  int64_t* status;
+  uint32_t off_img, off_yp, off_yf, off_bar;
+};
+
+DP2_DEV uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+DP2_DEV void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+DP2_DEV void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+DP2_DEV bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a protocol error traps instead of hanging the GPU
+DP2_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try(bar, parity)) return;
+    if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
+  }
+}
+DP2_DEV void warp_arrive(uint32_t bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+DP2_DEV void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+DP2_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// barrier slots
+enum { B_XFULL = 0, B_XEMPTY = 4, B_OFULL = 8, B_OEMPTY = 12, B_YPFULL = 16, B_YPEMPTY = 18, B_YFULL = 20,
+       B_YEMPTY = 22, B_COUNT = 24 };
+
+template <typename T, int NT>
+__global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
+  constexpr int SG = 8 * NT;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = blockIdx.x, grp = blockIdx.y, ng = gridDim.y;
+  const int J = prm.J, JP = prm.JP, L = prm.L, sp = prm.sp, NS = prm.ns;
+  const int col0 = grp * SG;
+  T* xs = reinterpret_cast<T*>(smem);                                  // [NS][TM][L]
+  double* img = reinterpret_cast<double*>(smem + prm.off_img);          // [JP/4][NT][32]
+  double* ypart = reinterpret_cast<double*>(smem + prm.off_yp);         // [NY][NA][TM][SG]
+  double* yfin = reinterpret_cast<double*>(smem + prm.off_yf);          // [NY][2][NT][32]
+  const uint32_t bar0 = su32(smem + prm.off_bar);
+  auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
+
+  // zero the X ring (pad columns are never written; stale rows must be finite)
+  for (int i = threadIdx.x; i < NS * TM * L; i += NTHREADS) xs[i] = T(0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(bar(B_XFULL + s), 1);
+      mbar_init(bar(B_XEMPTY + s), NA + NB);
+      mbar_init(bar(B_OFULL + s), 1);
+      mbar_init(bar(B_OEMPTY + s), 1);
+    }
+    for (int b = 0; b < NY; ++b) {
+      mbar_init(bar(B_YPFULL + b), NA);
+      mbar_init(bar(B_YPEMPTY + b), 1);
+      mbar_init(bar(B_YFULL + b), 1);
+      mbar_init(bar(B_YEMPTY + b), NB);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
+  if (pbeg >= pend) return;
+  const int ksq = JP / 16;  // k-steps per A warp (a quarter of J)
+
+  if (warp == WARP_PROD) {
+    // ------------------------------------------------------------ producer
+    const char* Xb = reinterpret_cast<const char*>(prm.X);
+    const uint32_t qbytes = (uint32_t)ksq * NT * 32 * 8;
+    int n = 0;
+    for (int p = pbeg; p < pend; ++p) {
+      const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
+      const int64_t row0 = prm.piece_row0[p];
+      const int pi = p - pbeg;
+      // B image of this slice, quarter by quarter as each A warp frees it
+      const double* src = prm.img + ((size_t)ks * ng + grp) * (size_t)(JP / 4) * NT * 32;
+      if (lane < NA) {
+        if (pi > 0) mbar_wait(bar(B_OEMPTY + lane), (pi - 1) & 1);
+        mbar_expect_tx(bar(B_OFULL + lane), qbytes);
+        bulk_load(su32(img) + (uint32_t)lane * qbytes, src + (size_t)lane * ksq * NT * 32, qbytes,
+                  bar(B_OFULL + lane));
+      }
+      for (int t = 0; t * TM < rows; ++t, ++n) {
+        const int s = n % NS;
+        const int valid = min(TM, rows - t * TM);
+        if (n >= NS) mbar_wait(bar(B_XEMPTY + s), ((n / NS) - 1) & 1);
+        if (lane == 0) mbar_expect_tx(bar(B_XFULL + s), (uint32_t)(valid * prm.rowbytes));
+        __syncwarp();
+        if (lane < valid)
+          bulk_load(su32(xs + ((size_t)s * TM + lane) * L),
+                    Xb + (size_t)(row0 + (int64_t)t * TM + lane) * prm.ldx * sizeof(T), (uint32_t)prm.rowbytes,
+                    bar(B_XFULL + s));
+      }
+    }
+  } else if (warp >= WARP_A0 && warp < WARP_A0 + NA) {
+    // ------------------------------------------------------------ A warps: Y partials
+    const int a = warp - WARP_A0;
+    const int r = lane >> 2, q = lane & 3;
+    int n = 0;
+    for (int p = pbeg; p < pend; ++p) {
+      const int rows = prm.piece_rows[p];
+      const int pi = p - pbeg;
+      mbar_wait(bar(B_OFULL + a), pi & 1);
+      const double* im = img + (size_t)a * ksq * NT * 32 + lane;
+      for (int t = 0; t * TM < rows; ++t, ++n) {
+        const int s = n % NS, b = n % NY;
+        mbar_wait(bar(B_XFULL + s), (n / NS) & 1);
+        const T* xr = xs + ((size_t)s * TM + r) * L + a * (JP / 4) + q;
+        double c0[NT][2], c1[NT][2];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) c0[j][0] = c0[j][1] = c1[j][0] = c1[j][1] = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < ksq; k += 2) {
+          const double x0 = (double)xr[4 * k], x1 = (double)xr[4 * k + 4];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            dmma_8x8x4(c0[j][0], c0[j][1], x0, im[(k * NT + j) * 32]);
+            dmma_8x8x4(c1[j][0], c1[j][1], x1, im[((k + 1) * NT + j) * 32]);
+          }
+        }
+        // partial -> ypart[b][a] (C fragment: row r, cols 8j + 2q, +1)
+        if (n >= NY) mbar_wait(bar(B_YPEMPTY + b), ((n / NY) - 1) & 1);
+        double* yp = ypart + (((size_t)b * NA + a) * TM + r) * SG + 2 * q;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          double2 v;
+          v.x = c0[j][0] + c1[j][0];
+          v.y = c0[j][1] + c1[j][1];
+          *reinterpret_cast<double2*>(yp + 8 * j) = v;
+        }
+        warp_arrive(bar(B_YPFULL + b));
+        warp_arrive(bar(B_XEMPTY + s));
+      }
+      warp_arrive(bar(B_OEMPTY + a));
+    }
+  } else if (warp == WARP_AUX) {
+    // ------------------------------------------------------------ aux: Y_t, Y rows, G, non-finite
+    const bool do_g = prm.g_part != nullptr;
+    double g[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    int n = 0;
+    for (int p = pbeg; p < pend; ++p) {
+      const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
+      const int64_t row0 = prm.piece_row0[p];
+      int bad = 0;
+      for (int t = 0; t * TM < rows; ++t, ++n) {
+        const int b = n % NY;
+        const int valid = min(TM, rows - t * TM);
+        mbar_wait(bar(B_YPFULL + b), (n / NY) & 1);
+        if (n >= NY) mbar_wait(bar(B_YEMPTY + b), ((n / NY) - 1) & 1);
+        // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
+        //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
+        double* yf = yfin + (size_t)b * 2 * NT * 32;
+        const double* ypb = ypart + (size_t)b * NA * TM * SG;
+        double fr[2][NT];
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
+            double v = 0.0;
+#pragma unroll
+            for (int aa = 0; aa < NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
+            v = row < valid ? v : 0.0;
+            bad |= !isfinite(v);
+            fr[k2][j] = v;
+            yf[(k2 * NT + j) * 32 + lane] = v;
+          }
+        warp_arrive(bar(B_YFULL + b));
+        warp_arrive(bar(B_YPEMPTY + b));
+        if (prm.y_out != nullptr) {
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              const int row = 4 * k2 + (lane & 3), col = col0 + 8 * j + (lane >> 2);
+              if (row < valid && col < sp) prm.y_out[(row0 + (int64_t)t * TM + row) * sp + col] = fr[k2][j];
+            }
+        }
+        if (do_g) {
+#pragma unroll
+          for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma_8x8x4(g[i][j][0], g[i][j][1], fr[k2][i], fr[k2][j]);
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) status_min(prm.status, ST_NONFINITE, ks);
+      if (do_g) {
+        double* gp = prm.g_part + (size_t)p * sp * sp;
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int rr = 8 * i + (lane >> 2), cc = 8 * j + 2 * (lane & 3);
+            if (rr < sp && cc < sp) {
+              gp[(size_t)rr * sp + cc] = g[i][j][0];
+              if (cc + 1 < sp) gp[(size_t)rr * sp + cc + 1] = g[i][j][1];
+            }
+            g[i][j][0] = g[i][j][1] = 0.0;
+          }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ B warps: Z += X_t^T Y_t
+    const int bw = warp - WARP_B0;
+    const int MB = JP / (8 * NB);  // J-blocks of 8 per B warp (<= MBMAX)
+    const int jb0 = bw * MB;
+    double z[MBMAX][NT][2];
+#pragma unroll
+    for (int i = 0; i < MBMAX; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) z[i][j][0] = z[i][j][1] = 0.0;
+    int n = 0;
+    for (int p = pbeg; p < pend; ++p) {
+      const int rows = prm.piece_rows[p];
+      for (int t = 0; t * TM < rows; ++t, ++n) {
+        const int s = n % NS, b = n % NY;
+        mbar_wait(bar(B_XFULL + s), (n / NS) & 1);
+        mbar_wait(bar(B_YFULL + b), (n / NY) & 1);
+        const double* yf = yfin + (size_t)b * 2 * NT * 32 + lane;
+        const T* xb = xs + ((size_t)s * TM + (lane & 3)) * L + 8 * jb0 + (lane >> 2);
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) {
+          double yv[NT];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) yv[j] = yf[(k2 * NT + j) * 32];
+#pragma unroll
+          for (int i = 0; i < MBMAX; ++i) {
+            if (i < MB) {
+              const double xv = (double)xb[(size_t)4 * k2 * L + 8 * i];
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma_8x8x4(z[i][j][0], z[i][j][1], xv, yv[j]);
+            }
+          }
+        }
+        warp_arrive(bar(B_YEMPTY + b));
+        warp_arrive(bar(B_XEMPTY + s));
+      }
+      // piece complete: flush Z rows 8 (jb0 + i) + (lane >> 2), cols col0 + 8 j + 2 (lane & 3) (+1)
+      double* out = prm.out_part + (size_t)p * J * sp;
+#pragma unroll
+      for (int i = 0; i < MBMAX; ++i) {
+        if (i < MB) {
+          const int m = 8 * (jb0 + i) + (lane >> 2);
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int c = col0 + 8 * j + 2 * (lane & 3);
+            if (m < J && c < sp) {
+              if (c + 1 < sp) {
+                double2 v;
+                v.x = z[i][j][0];
+                v.y = z[i][j][1];
+                *reinterpret_cast<double2*>(out + (size_t)m * sp + c) = v;
+              } else {
+                out[(size_t)m * sp + c] = z[i][j][0];
+              }
+            }
+            z[i][j][0] = z[i][j][1] = 0.0;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Fragment-major B images: img[k][g][ks][j][l] = B[k][4 ks + (l & 3)][8 (NT g + j) + (l >> 2)]
+// (0 outside J x sp).
+__global__ void image_kernel(const double* B, int64_t K, int J, int JP, int sp, int NT, int ng, double* img) {
+  const int64_t per = (int64_t)(JP / 4) * NT * 32;
+  const int64_t total = K * ng * per;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)(e % 32);
+    const int j = (int)((e / 32) % NT);
+    const int ks = (int)((e / (32 * NT)) % (JP / 4));
+    const int g = (int)((e / per) % ng);
+    const int64_t k = e / (per * ng);
+    const int row = 4 * ks + (l & 3), col = 8 * (NT * g + j) + (l >> 2);
+    img[e] = (row < J && col < sp) ? B[((size_t)k * J + row) * sp + col] : 0.0;
+  }
+}
+
+struct Plan {
+  int NT, ng, JP, L, ns;
+  size_t smem;
+  uint32_t off_img, off_yp, off_yf, off_bar;
+};
+
+bool plan(int J, int sp, int elem, Plan* pl) {
+  if (J < 1 || J > 512 || sp < 8 || sp % 8) return false;
+  const int nbt = sp / 8;
+  const int NT = nbt <= 3 ? nbt : 3;  // groups of <= 3 column blocks (last one zero padded)
+  const int ng = (nbt + NT - 1) / NT;
+  const int JP = (J + 8 * NB - 1) / (8 * NB) * (8 * NB);
+  int L = JP + (elem == 8 ? 4 : 4);  // elements: 8 B -> L % 16 == 4; 4 B -> L % 32 == 4
+  if (elem == 8) {
+    while (L % 16 != 4) ++L;
+  } else {
+    while (L % 32 != 4) ++L;
+  }
+  const int SG = 8 * NT;
+  const size_t img = (size_t)(JP / 4) * NT * 32 * 8;
+  const size_t yp = (size_t)NY * NA * TM * SG * 8, yf = (size_t)NY * 2 * NT * 32 * 8;
+  const size_t stage = (size_t)TM * L * elem;
+  const size_t cap = 227 * 1024;
+  int ns = 4;
+  while (ns >= 2 && ns * stage + img + yp + yf + 8 * B_COUNT + 256 > cap) --ns;
+  if (ns < 2) return false;
+  pl->NT = NT;
+  pl->ng = ng;
+  pl->JP = JP;
+  pl->L = L;
+  pl->ns = ns;
+  size_t off = ns * stage;
+  off = (off + 127) & ~(size_t)127;
+  pl->off_img = (uint32_t)off;
+  off += img;
+  pl->off_yp = (uint32_t)off;
+  off += yp;
+  pl->off_yf = (uint32_t)off;
+  off += yf;
+  pl->off_bar = (uint32_t)((off + 7) & ~(size_t)7);
+  pl->smem = pl->off_bar + 8 * B_COUNT;
+  return true;
+}
+
+// per-device image scratch (grown on demand, kept)
+double* image_scratch(size_t bytes, cudaError_t* err) {
+  static double* buf[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) {
+    *err = cudaErrorInvalidDevice;
+    return nullptr;
+  }
+  if (cap[dev] < bytes) {
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    *err = cudaMalloc(&buf[dev], bytes);
+    if (*err != cudaSuccess) return nullptr;
+    cap[dev] = bytes;
+  }
+  *err = cudaSuccess;
+  return buf[dev];
+}
+
+template <typename T, int NT>
+cudaError_t launch(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
+  auto kern = sketch64_kernel<T, NT>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(nseg, pl.ng), NTHREADS, pl.smem, st>>>(prm);
+  return cudaGetLastError();
+}
+
+}  // namespace s64
+
+bool sketch64_eligible(const dp2_store* st, int sp, bool xsq, bool gram) {
+  if (xsq) return false;  // the per-piece sums of squares live in the older passes
+  static const bool off = getenv("DP2_SKETCH64") && atoi(getenv("DP2_SKETCH64")) == 0;
+  if (off) return false;
+  const int elem = st->dtype == DP2_F64 ? 8 : 4;
+  if ((st->J * elem) % 16 != 0 || (st->ldx * elem) % 16 != 0 || reinterpret_cast<uintptr_t>(st->X) % 16 != 0)
+    return false;
+  s64::Plan pl{};
+  return s64::plan((int)st->J, sp, elem, &pl) && (!gram || pl.ng == 1);  // G needs one column group
+}
+
+cudaError_t run_sketch64(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                         int64_t* status, cudaStream_t stream, double* g_part) {
+  const int elem = st->dtype == DP2_F64 ? 8 : 4;
+  s64::Plan pl{};
+  if (!s64::plan((int)st->J, sp, elem, &pl)) return cudaErrorInvalidValue;
+  const int J = (int)st->J;
+  const size_t img_elems = (size_t)st->K * pl.ng * (pl.JP / 4) * pl.NT * 32;
+  cudaError_t e = cudaSuccess;
+  double* img = s64::image_scratch(img_elems * 8, &e);
+  if (!img) return e;
+  s64::image_kernel<<<1184, 256, 0, stream>>>(B, st->K, J, pl.JP, sp, pl.NT, pl.ng, img);
+  s64::Params prm{};
+  prm.X = st->X;
+  prm.ldx = st->ldx;
+  prm.J = J;
+  prm.JP = pl.JP;
+  prm.L = pl.L;
+  prm.sp = sp;
+  prm.ns = pl.ns;
+  prm.rowbytes = (J * elem + 15) / 16 * 16;
+  prm.img = img;
+  prm.piece_slice = st->piece_slice;
+  prm.piece_row0 = st->piece_row0;
+  prm.piece_rows = st->piece_rows;
+  prm.seg_begin = st->seg_begin;
+  prm.out_part = out_part;
+  prm.y_out = y_out;
+  prm.g_part = (pl.ng == 1) ? g_part : nullptr;
+  prm.status = status;
+  prm.off_img = pl.off_img;
+  prm.off_yp = pl.off_yp;
+  prm.off_yf = pl.off_yf;
+  prm.off_bar = pl.off_bar;
+  const int nseg = st->nseg;
+  if (elem == 8) {
+    switch (pl.NT) {
+      case 1: return s64::launch<double, 1>(prm, pl, nseg, stream);
+      case 2: return s64::launch<double, 2>(prm, pl, nseg, stream);
+      default: return s64::launch<double, 3>(prm, pl, nseg, stream);
+    }
+  }
+  switch (pl.NT) {
+    case 1: return s64::launch<float, 1>(prm, pl, nseg, stream);
+    case 2: return s64::launch<float, 2>(prm, pl, nseg, stream);
+    default: return s64::launch<float, 3>(prm, pl, nseg, stream);
+  }
+}
+
+}  // namespace dp2

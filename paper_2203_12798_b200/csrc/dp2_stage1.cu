@@ -670,6 +670,8 @@ static constexpr size_t kXTileBudget = 150 * 1024;
 cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                        double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
   if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
+  if (sketch64_eligible(st, sp, xsq_part != nullptr, g_part != nullptr))
+    return run_sketch64(st, B, sp, out_part, y_out, status, stream, g_part);
   const int J = (int)st->J;
   const int elem = 8;
   SketchParams prm{};
@@ -754,7 +756,10 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   }
   // the per-piece sums of squares are not consumed by stage 1 (the fitness
   // uses dp2_slice_stats); the tensor-core pass flags non-finite input from Y
-  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, sketch_tc_eligible(st, sp) ? nullptr : xsq, status, stream);
+  // (the tensor-core and DMMA passes flag non-finite input from Y instead)
+  const bool s64 = (st->dtype == DP2_F64 || sketch_engine() == 2) && sketch64_eligible(st, sp, false, false);
+  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, (sketch_tc_eligible(st, sp) || s64) ? nullptr : xsq,
+                             status, stream);
   if (e != cudaSuccess) return e;
   if (timing) cudaEventRecord(ev[1], stream);
   if (sp <= 32) {
