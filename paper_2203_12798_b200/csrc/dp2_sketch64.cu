@@ -35,6 +35,10 @@
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 namespace dp2 {
 namespace s64 {
 
@@ -63,6 +67,7 @@ struct Params {
   double* g_part;           // npieces x sp x sp or null (single column group)
   int64_t* status;
   uint32_t off_img, off_yp, off_yf, off_bar;
+  unsigned long long* dbg;  // DP2_S64_DEBUG: per-warp wait cycles by barrier class, or null
 };
 
 DP2_DEV uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -105,11 +110,24 @@ DP2_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t b
                : "memory");
 }
 
+// wait with cycle accounting into dacc[k] when DBG (DP2_S64_DEBUG=1)
+#define S64_WAIT(barexpr, par, k)                        \
+  do {                                                   \
+    if (DBG) {                                           \
+      const long long t0_ = clock64();                   \
+      mbar_wait(barexpr, par);                           \
+      dacc[k] += (unsigned long long)(clock64() - t0_);  \
+    } else {                                             \
+      mbar_wait(barexpr, par);                           \
+    }                                                    \
+  } while (0)
+enum { D_XFULL = 0, D_XEMPTY, D_OFULL, D_OEMPTY, D_YPFULL, D_YPEMPTY, D_YFULL, D_YEMPTY, D_TOTAL, D_N = 10 };
+
 // barrier slots
 enum { B_XFULL = 0, B_XEMPTY = 4, B_OFULL = 8, B_OEMPTY = 12, B_YPFULL = 16, B_YPEMPTY = 18, B_YFULL = 20,
        B_YEMPTY = 22, B_COUNT = 24 };
 
-template <typename T, int NT>
+template <typename T, int NT, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   constexpr int SG = 8 * NT;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -147,6 +165,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
   if (pbeg >= pend) return;
   const int ksq = JP / 16;  // k-steps per A warp (a quarter of J)
+  unsigned long long dacc[DBG ? D_N : 1] = {};
+  const long long tstart = DBG ? clock64() : 0;
 
   if (warp == WARP_PROD) {
     // ------------------------------------------------------------ producer
@@ -160,7 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       // B image of this slice, quarter by quarter as each A warp frees it
       const double* src = prm.img + ((size_t)ks * ng + grp) * (size_t)(JP / 4) * NT * 32;
       if (lane < NA) {
-        if (pi > 0) mbar_wait(bar(B_OEMPTY + lane), (pi - 1) & 1);
+        if (pi > 0) S64_WAIT(bar(B_OEMPTY + lane), (pi - 1) & 1, D_OEMPTY);
         mbar_expect_tx(bar(B_OFULL + lane), qbytes);
         bulk_load(su32(img) + (uint32_t)lane * qbytes, src + (size_t)lane * ksq * NT * 32, qbytes,
                   bar(B_OFULL + lane));
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int s = n % NS;
         const int valid = min(TM, rows - t * TM);
-        if (n >= NS) mbar_wait(bar(B_XEMPTY + s), ((n / NS) - 1) & 1);
+        if (n >= NS) S64_WAIT(bar(B_XEMPTY + s), ((n / NS) - 1) & 1, D_XEMPTY);
         if (lane == 0) mbar_expect_tx(bar(B_XFULL + s), (uint32_t)(valid * prm.rowbytes));
         __syncwarp();
         if (lane < valid)
@@ -185,11 +205,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     for (int p = pbeg; p < pend; ++p) {
       const int rows = prm.piece_rows[p];
       const int pi = p - pbeg;
-      mbar_wait(bar(B_OFULL + a), pi & 1);
+      S64_WAIT(bar(B_OFULL + a), pi & 1, D_OFULL);
       const double* im = img + (size_t)a * ksq * NT * 32 + lane;
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int s = n % NS, b = n % NY;
-        mbar_wait(bar(B_XFULL + s), (n / NS) & 1);
+        S64_WAIT(bar(B_XFULL + s), (n / NS) & 1, D_XFULL);
         const T* xr = xs + ((size_t)s * TM + r) * L + a * (JP / 4) + q;
         double c0[NT][2], c1[NT][2];
 #pragma unroll
@@ -204,7 +224,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
           }
         }
         // partial -> ypart[b][a] (C fragment: row r, cols 8j + 2q, +1)
-        if (n >= NY) mbar_wait(bar(B_YPEMPTY + b), ((n / NY) - 1) & 1);
+        if (n >= NY) S64_WAIT(bar(B_YPEMPTY + b), ((n / NY) - 1) & 1, D_YPEMPTY);
         double* yp = ypart + (((size_t)b * NA + a) * TM + r) * SG + 2 * q;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
@@ -234,8 +254,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int b = n % NY;
         const int valid = min(TM, rows - t * TM);
-        mbar_wait(bar(B_YPFULL + b), (n / NY) & 1);
-        if (n >= NY) mbar_wait(bar(B_YEMPTY + b), ((n / NY) - 1) & 1);
+        S64_WAIT(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
+        if (n >= NY) S64_WAIT(bar(B_YEMPTY + b), ((n / NY) - 1) & 1, D_YEMPTY);
         // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
         //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
         double* yf = yfin + (size_t)b * 2 * NT * 32;
@@ -305,8 +325,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       const int rows = prm.piece_rows[p];
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int s = n % NS, b = n % NY;
-        mbar_wait(bar(B_XFULL + s), (n / NS) & 1);
-        mbar_wait(bar(B_YFULL + b), (n / NY) & 1);
+        S64_WAIT(bar(B_XFULL + s), (n / NS) & 1, D_XFULL);
+        S64_WAIT(bar(B_YFULL + b), (n / NY) & 1, D_YFULL);
         const double* yf = yfin + (size_t)b * 2 * NT * 32 + lane;
         const T* xb = xs + ((size_t)s * TM + (lane & 3)) * L + 8 * jb0 + (lane >> 2);
 #pragma unroll
@@ -350,6 +370,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         }
       }
     }
+  }
+  if (DBG && lane == 0) {
+    dacc[D_TOTAL] = (unsigned long long)(clock64() - tstart);
+    unsigned long long* d = prm.dbg + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * NWARPS + warp) * D_N;
+    for (int i = 0; i < D_N; ++i) d[i] = dacc[i];
   }
 }
 
@@ -437,11 +462,60 @@ double* image_scratch(size_t bytes, cudaError_t* err) {
 
 template <typename T, int NT>
 cudaError_t launch(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
-  auto kern = sketch64_kernel<T, NT>;
+  auto kern = prm.dbg ? sketch64_kernel<T, NT, true> : sketch64_kernel<T, NT, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   kern<<<dim3(nseg, pl.ng), NTHREADS, pl.smem, st>>>(prm);
   return cudaGetLastError();
+}
+
+cudaError_t launch_any(int elem, int NT, const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
+  if (elem == 8) {
+    switch (NT) {
+      case 1: return launch<double, 1>(prm, pl, nseg, st);
+      case 2: return launch<double, 2>(prm, pl, nseg, st);
+      default: return launch<double, 3>(prm, pl, nseg, st);
+    }
+  }
+  switch (NT) {
+    case 1: return launch<float, 1>(prm, pl, nseg, st);
+    case 2: return launch<float, 2>(prm, pl, nseg, st);
+    default: return launch<float, 3>(prm, pl, nseg, st);
+  }
+}
+
+// DP2_S64_DEBUG: run with per-warp wait accounting and print the share of
+// cycles each role spends waiting on each barrier class (debug aid; syncs)
+cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg, cudaStream_t stream) {
+  const size_t nd = (size_t)nseg * pl.ng * NWARPS * D_N;
+  unsigned long long *dh = nullptr, *dd = nullptr;
+  cudaError_t e = cudaHostAlloc(&dh, nd * 8, cudaHostAllocMapped);
+  if (e != cudaSuccess) return e;
+  memset(dh, 0, nd * 8);
+  cudaHostGetDevicePointer(&dd, dh, 0);
+  prm.dbg = dd;
+  e = launch_any(elem, NT, prm, pl, nseg, stream);
+  cudaStreamSynchronize(stream);
+  const char* names[] = {"xfull", "xempty", "ofull", "oempty", "ypfull", "ypempty", "yfull", "yempty"};
+  const char* roles[] = {"A", "B", "prod", "aux"};
+  for (int role = 0; role < 4; ++role) {
+    double acc[D_N] = {};
+    int cnt = 0;
+    for (size_t c = 0; c < (size_t)nseg * pl.ng; ++c)
+      for (int w = 0; w < NWARPS; ++w) {
+        const int r = (w >= WARP_A0 && w < WARP_A0 + NA) ? 0 : (w >= WARP_B0 && w < WARP_B0 + NB) ? 1
+                      : w == WARP_PROD ? 2 : 3;
+        if (r != role) continue;
+        ++cnt;
+        for (int i = 0; i < D_N; ++i) acc[i] += (double)dh[(c * NWARPS + w) * D_N + i];
+      }
+    fprintf(stderr, "[s64] %-4s total %.0f kcyc:", roles[role], acc[D_TOTAL] / (cnt ? cnt : 1) / 1e3);
+    for (int i = 0; i < 8; ++i)
+      if (acc[i] > 0) fprintf(stderr, " %s %.1f%%", names[i], 100.0 * acc[i] / acc[D_TOTAL]);
+    fprintf(stderr, "\n");
+  }
+  cudaFreeHost(dh);
+  return e;
 }
 
 }  // namespace s64
@@ -491,18 +565,9 @@ cudaError_t run_sketch64(const dp2_store* st, const double* B, int sp, double* o
   prm.off_yf = pl.off_yf;
   prm.off_bar = pl.off_bar;
   const int nseg = st->nseg;
-  if (elem == 8) {
-    switch (pl.NT) {
-      case 1: return s64::launch<double, 1>(prm, pl, nseg, stream);
-      case 2: return s64::launch<double, 2>(prm, pl, nseg, stream);
-      default: return s64::launch<double, 3>(prm, pl, nseg, stream);
-    }
-  }
-  switch (pl.NT) {
-    case 1: return s64::launch<float, 1>(prm, pl, nseg, stream);
-    case 2: return s64::launch<float, 2>(prm, pl, nseg, stream);
-    default: return s64::launch<float, 3>(prm, pl, nseg, stream);
-  }
+  static const bool dbg = getenv("DP2_S64_DEBUG") && atoi(getenv("DP2_S64_DEBUG")) != 0;
+  if (dbg) return s64::launch_debug(elem, pl.NT, prm, pl, nseg, stream);
+  return s64::launch_any(elem, pl.NT, prm, pl, nseg, stream);
 }
 
 }  // namespace dp2
