@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     // ------------------------------------------------------------ producer
     const char* Xb = reinterpret_cast<const char*>(prm.X);
     const uint32_t qbytes = (uint32_t)ksq * NT * 32 * 8;
-    int n = 0;
+    int n = 0, rs = 0, rph = 0;  // tile count, ring stage and its phase
     for (int p = pbeg; p < pend; ++p) {
       const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
       const int64_t row0 = prm.piece_row0[p];
@@ -186,9 +186,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
                   bar(B_OFULL + lane));
       }
       for (int t = 0; t * TM < rows; ++t, ++n) {
-        const int s = n % NS;
+        const int s = rs;
         const int valid = min(TM, rows - t * TM);
-        if (n >= NS) S64_WAIT(bar(B_XEMPTY + s), ((n / NS) - 1) & 1, D_XEMPTY);
+        if (n >= NS) S64_WAIT(bar(B_XEMPTY + s), rph ^ 1, D_XEMPTY);
+        if (++rs == NS) { rs = 0; rph ^= 1; }
         if (lane == 0) mbar_expect_tx(bar(B_XFULL + s), (uint32_t)(valid * prm.rowbytes));
         __syncwarp();
         if (lane < valid)
@@ -201,15 +202,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     // ------------------------------------------------------------ A warps: Y partials
     const int a = warp - WARP_A0;
     const int r = lane >> 2, q = lane & 3;
-    int n = 0;
+    int n = 0, rs = 0, rph = 0;
     for (int p = pbeg; p < pend; ++p) {
       const int rows = prm.piece_rows[p];
       const int pi = p - pbeg;
       S64_WAIT(bar(B_OFULL + a), pi & 1, D_OFULL);
       const double* im = img + (size_t)a * ksq * NT * 32 + lane;
       for (int t = 0; t * TM < rows; ++t, ++n) {
-        const int s = n % NS, b = n % NY;
-        S64_WAIT(bar(B_XFULL + s), (n / NS) & 1, D_XFULL);
+        const int s = rs, b = n % NY;
+        S64_WAIT(bar(B_XFULL + s), rph, D_XFULL);
+        if (++rs == NS) { rs = 0; rph ^= 1; }
         const T* xr = xs + ((size_t)s * TM + r) * L + a * (JP / 4) + q;
         double c0[NT][2], c1[NT][2];
 #pragma unroll
@@ -320,12 +322,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     for (int i = 0; i < MBMAX; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) z[i][j][0] = z[i][j][1] = 0.0;
-    int n = 0;
+    int n = 0, rs = 0, rph = 0;
     for (int p = pbeg; p < pend; ++p) {
       const int rows = prm.piece_rows[p];
       for (int t = 0; t * TM < rows; ++t, ++n) {
-        const int s = n % NS, b = n % NY;
-        S64_WAIT(bar(B_XFULL + s), (n / NS) & 1, D_XFULL);
+        const int s = rs, b = n % NY;
+        S64_WAIT(bar(B_XFULL + s), rph, D_XFULL);
+        if (++rs == NS) { rs = 0; rph ^= 1; }
         S64_WAIT(bar(B_YFULL + b), (n / NY) & 1, D_YFULL);
         const double* yf = yfin + (size_t)b * 2 * NT * 32 + lane;
         const T* xb = xs + ((size_t)s * TM + (lane & 3)) * L + 8 * jb0 + (lane >> 2);

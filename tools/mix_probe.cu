@@ -79,6 +79,11 @@ int main() {
   long long h[2];
   cudaMemcpy(h, l, 16, cudaMemcpyDeviceToHost);
   printf("{\"dmma_dependent_latency_cycles\": %lld}\n", h[0]);
+  for (int w : {4, 8}) {  // 1 / 2 warps per SM sub-partition: can one warp saturate the DMMA pipe?
+    run<3, 0>(sms, d, w);
+    run<6, 0>(sms, d, w);
+    run<12, 0>(sms, d, w);
+  }
   for (int w : {8, 16}) {
     run<8, 0>(sms, d, w);
     run<0, 8>(sms, d, w);
