@@ -321,8 +321,8 @@ def main():
                    "l2": "inputs larger than L2 (X %.1f GB >> 126 MB)" % (total_entries * (
                        8 if cfg.dtype == "f64" else 4) / 1e9),
                    "precision": ("fp64 storage and arithmetic (DMMA / DFMA), the reference's precision"
-                                 if cfg.dtype == "f64" else "fp32 storage, fp32 sketch products (FFMA), "
-                                 "fp64 factorizations / stage 2 / ALS")},
+                                 if cfg.dtype == "f64" else "fp32 storage, fp64 sketch products on the exactly "
+                                 "upcast values (DMMA), fp64 factorizations / stage 2 / ALS")},
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -79,9 +79,10 @@ int64_t dp2_launch_count(int32_t reset);
  * (DMMA) and for fp32 with J <= 512 (tcgen05 tf32 pass), two per SM for the
  * fp32 FFMA pass.  Planning aid for dp2_plan_pieces(nseg). */
 int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms);
-/* fp32-storage streaming-pass engine: 1 = fp32 FFMA products (default; the
- * fp32 mode of BASELINE.json), 2 = fp64 DMMA products on the exactly upcast
- * values (where dp2_sketch_kind reports 3), 0 = single-pass tf32 products on
+/* fp32-storage streaming-pass engine: 2 = fp64 DMMA products on the exactly
+ * upcast values where dp2_sketch_kind reports 3, else fp32 FFMA products
+ * (default; at least the fp32 mode of BASELINE.json), 1 = fp32 FFMA products
+ * everywhere, 0 = single-pass tf32 products on
  * tcgen05 tensor cores where eligible (opt-in speed mode: ~5e-4 relative
  * product error, passes the 1e-3 fp32-mode bound on c2 but not on slices of
  * ~50 rows).

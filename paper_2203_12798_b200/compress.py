@@ -84,19 +84,21 @@ class CompressedTensor:
                     cores=self.cores.cpu().numpy())
 
 
-_FP32_ENGINES = {"tf32": 0, "fp32": 1}
+_FP32_ENGINES = {"tf32": 0, "fp32": 1, "fp64": 2}
 
 
 def set_fp32_products(mode):
     """Arithmetic of the stage-1 sketch products for fp32-storage tensors:
-    ``"fp32"`` (default; FFMA products, fp32 accumulation within a tile, fp64
-    across tiles -- the fp32 mode of BASELINE.json) or ``"tf32"`` (opt-in
-    speed mode: single-pass tf32 products on the tcgen05 tensor cores, ~5e-4
-    relative product error).  Returns the previous mode."""
+    ``"fp64"`` (default; fp64 DMMA products on the exactly upcast values where
+    the warp-specialised pass applies, J <= 512, else ``"fp32"``), ``"fp32"``
+    (FFMA products, fp32 accumulation within a tile, fp64 across tiles -- the
+    fp32 mode of BASELINE.json) or ``"tf32"`` (opt-in speed mode: single-pass
+    tf32 products on the tcgen05 tensor cores, ~5e-4 relative product error).
+    Returns the previous mode."""
     if mode not in _FP32_ENGINES:
         raise ValueError(f"fp32 product mode must be one of {sorted(_FP32_ENGINES)}, got {mode!r}")
     prev = int(_lib.lib().dp2_set_sketch_engine(_FP32_ENGINES[mode]))
-    return {v: k for k, v in _FP32_ENGINES.items()}.get(prev, "fp32")
+    return {v: k for k, v in _FP32_ENGINES.items()}.get(prev, "fp64")
 
 
 def nseg_for(tensor: IrregularTensor):

@@ -706,11 +706,13 @@ __global__ void __launch_bounds__(256) b_tile_kernel(const double* B, int64_t K,
 
 namespace {
 // 0: tf32 tensor cores when eligible (opt-in: single-pass tf32 products),
-// 1: fp32 FFMA kernel (default: fp32 products, the fp32 mode BASELINE.json
-// states).  DP2_SKETCH_ENGINE overrides the default at load time.
+// 1: fp32 FFMA kernel, 2 (default): fp64 DMMA products on the exactly upcast
+// values where the warp-specialised pass is eligible (J <= 512), else the FFMA
+// kernel -- both at least the fp32 mode BASELINE.json states.
+// DP2_SKETCH_ENGINE overrides the default at load time.
 int initial_engine() {
   const char* e = getenv("DP2_SKETCH_ENGINE");
-  return e && *e ? atoi(e) : 1;
+  return e && *e ? atoi(e) : 2;
 }
 int g_engine = initial_engine();
 }

@@ -2,8 +2,10 @@
 named below) through the CUDA path against the CPU oracle on the SAME input.
 
 * c2 in full (K=1000, J=512, I_k ~ U{500..4000}, 1.18e9 entries) in fp64 (the
-  configuration ``bench.py`` measures), in the fp32 mode (fp32 storage, fp32
-  sketch products) and in the opt-in tf32 mode (single-pass tf32 products on
+  configuration ``bench.py`` measures), in the fp32 mode (fp32 storage; fp64
+  DMMA sketch products on the upcast values by default, fp32 FFMA products
+  via ``set_fp32_products("fp32")``) and in the opt-in tf32 mode (single-pass
+  tf32 products on
   the tcgen05 tensor cores, ``set_fp32_products("tf32")``, bench.py's
   labelled sub-record);
 * c3: a 240-slice K-subset of the heavy-tailed tensor (lognormal I_k, random
@@ -97,6 +99,17 @@ def test_c2_full_fp32_mode(c2_host):
     xs = [x.astype(np.float32) for x in c2_host]
     errs, fit, fit_o = _compare(xs, 10, 32, "f32", FP32)
     print(f"c2 fp32: fitness {fit:.10f} oracle {fit_o:.10f}; errors {errs}")
+
+
+def test_c2_full_fp32_ffma_products(c2_host):
+    import paper_2203_12798_b200 as dp
+    xs = [x.astype(np.float32) for x in c2_host]
+    prev = dp.set_fp32_products("fp32")
+    try:
+        errs, fit, fit_o = _compare(xs, 10, 32, "f32", FP32)
+    finally:
+        dp.set_fp32_products(prev)
+    print(f"c2 fp32 (FFMA products): fitness {fit:.10f} oracle {fit_o:.10f}; errors {errs}")
 
 
 def test_c2_full_tf32_mode(c2_host):
