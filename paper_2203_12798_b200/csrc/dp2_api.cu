@@ -358,7 +358,7 @@ int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_
   cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
                                   static_cast<char*>(ws), status_dev, S(stream));
   // our own kernels only (the DGEMMs run in cuBLAS when it is available)
-  return e == cudaSuccess ? ok(dp2::stage2_uses_blas() ? 3 : 11) : fail(e, "dp2_stage2");
+  return e == cudaSuccess ? ok(11) : fail(e, "dp2_stage2");
 }
 
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }

@@ -40,7 +40,6 @@ cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out
                        double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part = nullptr);
 
 size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R);
-bool stage2_uses_blas();  // stage-2 GEMMs through cuBLAS (dlopen) instead of the fallback kernels
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
                        double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t stream);
 

@@ -1,99 +1,103 @@
 // Stage 2: randomized SVD of the concatenated right parts
 // M = [V_1 S_1 | ... | V_K S_K] (J x KR, P/compress.py:108-111), fp64.
 //
-//   Y  = M Omega2           (J x s2)     nn split-K partials + ordered reduce
-//   Z  = M^T Y              (KR x s2)    tn
+//   Y  = M Omega2           (J x s2)     DMMA split-K partials + ordered reduce
+//   Z  = M^T Y              (KR x s2)    DMMA
 //   Y2 = M Z                (J x s2)     = the reference's M (M^T M Omega2)
 //   Q2 = orth(Y2)                        CholQR2 in one CTA (CGS2 fallback; the reference's np.linalg.qr)
 //   C  = M^T Q2             (KR x s2)    B2 = Q2^T M = C^T
 //   B2 B2^T = C^T C = U mu U^T           register Jacobi (block Jacobi fallback); E = sqrt(mu_R)
 //   D = Q2 U_R (sign rule, P/linalg.py:62-70), F = C U_R / E (same flips)
-#include <dlfcn.h>
-
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 #include "dp2_small_linalg.cuh"
 
+#include <algorithm>
+
 namespace dp2 {
 
-// ---------------------------------------------------------------- cuBLAS
-// The four products with M and the Gram C^T C are plain dense fp64 GEMMs
-// (M is J x KR, e.g. 512 x 10^4): cuBLAS DGEMM (fp64 tensor cores) when the
-// library can be opened at run time, else the kernels below.  Loaded with
-// dlopen so libdpar2 has no link-time dependency on it; cuBLAS results are
-// bitwise reproducible on a given GPU.
-namespace {
-typedef int (*blas_create_t)(void**);
-typedef int (*blas_stream_t)(void*, cudaStream_t);
-typedef int (*blas_dgemm_t)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
-                            const double*, double*, int);
-struct Blas {
-  bool tried = false;
-  blas_create_t create = nullptr;
-  blas_stream_t stream = nullptr;
-  blas_dgemm_t dgemm = nullptr;
-  void* handle[64] = {};
-};
-Blas& blas() {
-  static Blas b;
-  if (!b.tried) {
-    b.tried = true;
-    const char* names[] = {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12", "libcublas.so"};
-    void* lib = nullptr;
-    for (const char* n : names)
-      if ((lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
-    if (lib) {
-      b.create = reinterpret_cast<blas_create_t>(dlsym(lib, "cublasCreate_v2"));
-      b.stream = reinterpret_cast<blas_stream_t>(dlsym(lib, "cublasSetStream_v2"));
-      b.dgemm = reinterpret_cast<blas_dgemm_t>(dlsym(lib, "cublasDgemm_v2"));
-      if (!b.create || !b.stream || !b.dgemm) b.create = nullptr;
+// ---------------------------------------------------------------- skinny fp64 GEMMs (DMMA)
+// The four products with M (J x KR) and the Gram C^T C are tall-skinny fp64
+// GEMMs: every output is s2 (<= ~100) columns wide, so they stream M (or C)
+// once with m8n8k4 DMMA fragments read straight from global memory (M is
+// L2-resident between the passes: 41 MB at c2) and write per-split partials
+// that a fixed-order reduction sums (deterministic, like the reference's
+// ascending reductions).
+
+// part[ks] (m x n) = A[:, ks-th K range] B[ks-th K range, :], A row-major (m x K),
+// B row-major (K x n).  Block: 8 warps; warp w -> output rows 64 bx + 8 w,
+// columns 24 bz .. +24 (3 DMMA n-blocks).
+__global__ void __launch_bounds__(256) nn_dmma_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
+                                                       int64_t K, const double* __restrict__ B, int ldb, int n,
+                                                       int64_t kc, double* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 64 + warp * 8 + (lane >> 2);
+  const int ks = blockIdx.y, c0 = blockIdx.z * 24;
+  const int64_t k0 = (int64_t)ks * kc, k1 = imin64(K, k0 + kc);
+  const bool rok = row < m;
+  const double* a = A + (rok ? row : 0) * lda + (lane & 3);
+  const int bcol = c0 + (lane >> 2);
+  double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+  for (int64_t k = k0; k < k1; k += 4) {
+    const int64_t kk = k + (lane & 3);
+    const bool kok = kk < k1;
+    const double av = (rok && kok) ? __ldg(a + k) : 0.0;
+    const double* b = B + (kok ? kk : 0) * ldb;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = bcol + 8 * j;
+      const double bv = (kok && c < n) ? __ldg(b + c) : 0.0;
+      dmma_8x8x4(acc[j][0], acc[j][1], av, bv);
     }
   }
-  return b;
-}
-// column-major C (m x n) = op(A) op(B); false when cuBLAS is unavailable
-bool dgemm_cm(cudaStream_t st, bool ta, bool tb, int m, int n, int k, const double* A, int lda, const double* B,
-              int ldb, double* C, int ldc) {
-  Blas& b = blas();
-  if (!b.create) return false;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-  if (!b.handle[dev] && b.create(&b.handle[dev]) != 0) {
-    b.handle[dev] = nullptr;
-    return false;
-  }
-  if (b.stream(b.handle[dev], st) != 0) return false;
-  const double one = 1.0, zero = 0.0;
-  return b.dgemm(b.handle[dev], ta ? 1 : 0, tb ? 1 : 0, m, n, k, &one, A, lda, B, ldb, &zero, C, ldc) == 0;
-}
-}  // namespace
-
-bool stage2_uses_blas() { return blas().create != nullptr; }
-
-constexpr int kChunk = 1024;  // split-K chunk of the KR dimension
-
-// out_part[chunk][i][c] = sum_{n in chunk} A[i][n] * B[n][c],  c in [32g, 32g+32) & < sb
-__global__ void __launch_bounds__(256) nn_partial_kernel(const double* A, int64_t lda, int64_t N,
-                                                          const double* B, int ldb, int sb,
-                                                          double* out_part, int64_t m) {
-  __shared__ double red[32];
-  const int64_t i = blockIdx.x;
-  const int chunk = blockIdx.y, g = blockIdx.z;
-  const int64_t n0 = (int64_t)chunk * kChunk, n1 = imin64(N, n0 + kChunk);
-  const int c0 = g * 32, cw = min(32, sb - c0);
-  double acc[32];
+  // C fragment: row (lane >> 2) of the warp's block, columns 8 j + 2 (lane & 3), +1
+  const int64_t orow = (int64_t)blockIdx.x * 64 + warp * 8 + (lane >> 2);
+  if (orow < m) {
+    double* o = part + ((size_t)ks * m + orow) * n;
 #pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-  for (int64_t n = n0 + threadIdx.x; n < n1; n += blockDim.x) {
-    const double a = A[i * lda + n];
-    const double* b = B + n * ldb + c0;
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (c < cw) acc[c] = fma(a, b[c], acc[c]);
+    for (int j = 0; j < 3; ++j) {
+      const int c = c0 + 8 * j + 2 * (lane & 3);
+      if (c < n) o[c] = acc[j][0];
+      if (c + 1 < n) o[c + 1] = acc[j][1];
+    }
   }
-  for (int c = 0; c < cw; ++c) {
-    const double s = block_sum(acc[c], red);
-    if (threadIdx.x == 0) out_part[((size_t)chunk * m + i) * sb + c0 + c] = s;
+}
+
+// part[ms] (K x n) = A[ms-th m range, :]^T B[ms-th m range, :], A row-major (m x K),
+// B row-major (m x n).  Warp w -> output rows (columns of A) 64 bx + 8 w, +8.
+__global__ void __launch_bounds__(256) tn_dmma_kernel(const double* __restrict__ A, int64_t lda, int64_t m,
+                                                       int64_t K, const double* __restrict__ B, int ldb, int n,
+                                                       int64_t mc, double* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t acol = (int64_t)blockIdx.x * 64 + warp * 8 + (lane >> 2);  // A-fragment row = column of A
+  const int c0 = blockIdx.z * 24, ms = blockIdx.y;
+  const int64_t m0 = (int64_t)ms * mc, m1 = imin64(m, m0 + mc);
+  const bool cok = acol < K;
+  const int bcol = c0 + (lane >> 2);
+  double acc[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+  for (int64_t i = m0; i < m1; i += 4) {
+    const int64_t ii = i + (lane & 3);
+    const bool iok = ii < m1;
+    const double av = (cok && iok) ? __ldg(A + ii * lda + acol) : 0.0;
+    const double* b = B + (iok ? ii : 0) * ldb;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = bcol + 8 * j;
+      const double bv = (iok && c < n) ? __ldg(b + c) : 0.0;
+      dmma_8x8x4(acc[j][0], acc[j][1], av, bv);
+    }
+  }
+  const int64_t orow = (int64_t)blockIdx.x * 64 + warp * 8 + (lane >> 2);
+  if (orow < K) {
+    double* o = part + ((size_t)ms * K + orow) * n;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = c0 + 8 * j + 2 * (lane & 3);
+      if (c < n) o[c] = acc[j][0];
+      if (c + 1 < n) o[c + 1] = acc[j][1];
+    }
   }
 }
 
@@ -106,73 +110,15 @@ __global__ void reduce_parts_kernel(const double* part, int nparts, int64_t size
   }
 }
 
-// out[n][c] = sum_i A[i][n] * B[i][c]   (A m x N row-major, B m x sb), c group g
-__global__ void __launch_bounds__(256) tn_kernel(const double* A, int64_t lda, int64_t m, int64_t N,
-                                                  const double* B, int ldb, int sb, double* out,
-                                                  int ldo) {
-  __shared__ double bt[32 * 32];
-  const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int c0 = blockIdx.y * 32, cw = min(32, sb - c0);
-  double acc[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = 0.0;
-  for (int64_t i0 = 0; i0 < m; i0 += 32) {
-    const int ir = (int)imin64(32, m - i0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
-      const int r = e / 32, c = e % 32;
-      bt[e] = (r < ir && c < cw) ? B[(i0 + r) * ldb + c0 + c] : 0.0;
-    }
-    __syncthreads();
-    if (n < N) {
-      for (int r = 0; r < ir; ++r) {
-        const double a = A[(i0 + r) * lda + n];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = fma(a, bt[r * 32 + c], acc[c]);
-      }
-    }
-  }
-  if (n < N)
-    for (int c = 0; c < cw; ++c) out[n * ldo + c0 + c] = acc[c];
-}
-
-// partial Gram over row chunks: part[chunk][a][b] = sum_{n in chunk} C[n][a] C[n][b]
-__global__ void __launch_bounds__(256) gram_partial_kernel(const double* C, int64_t N, int ld, int s,
-                                                            double* part) {
-  __shared__ double tile[1056];
-  const int chunk = blockIdx.x;
-  const int64_t n0 = (int64_t)chunk * kChunk, n1 = imin64(N, n0 + kChunk);
-  const int ntri = s * (s + 1) / 2;
-  const int trows = max(1, 1056 / s);
-  for (int e0 = 0; e0 < ntri; e0 += blockDim.x) {
-    const int e = e0 + threadIdx.x;
-    int a = 0, b = 0;
-    if (e < ntri) {
-      int rem = e;
-      while (rem >= s - a) { rem -= s - a; ++a; }
-      b = a + rem;
-    }
-    double acc = 0.0;
-    for (int64_t r0 = n0; r0 < n1; r0 += trows) {
-      const int rr = (int)imin64(trows, n1 - r0);
-      __syncthreads();
-      for (int i = threadIdx.x; i < rr * s; i += blockDim.x) tile[i] = C[(r0 + i / s) * ld + (i % s)];
-      __syncthreads();
-      if (e < ntri)
-        for (int r = 0; r < rr; ++r) acc = fma(tile[r * s + a], tile[r * s + b], acc);
-    }
-    if (e < ntri) {
-      part[(size_t)chunk * s * s + a * s + b] = acc;
-      part[(size_t)chunk * s * s + b * s + a] = acc;
-    }
-  }
-}
-
-// single block: eig(BB) -> E, D = Q2 U_R with the sign rule, Uf = U_R * sign / E
 // Q2 = orth(Y2) (J x s, row-major, in place), one CTA: the J x SP slab in
-// shared memory, CholQR twice (G = Y^T Y on DMMA, register Cholesky, row
-// substitution) -- orthonormal to rounding for kappa(Y2) below ~1e6 (first
-// pivot floor 1e-12); otherwise CGS2 with re-randomisation, like cgs2_kernel.
+// shared memory, shifted CholeskyQR3 (G = Y^T Y on DMMA, register Cholesky,
+// row substitution): a shifted pass, a plain pass, then a plain pass whose
+// pivots must stay above 1e-3 of the largest -- i.e. the columns entering it
+// are orthonormal to ~1e-3 -- else CGS2 with re-randomisation (cgs2_smem).
+// The middle pass has no pivot floor: its job is to finish what the shifted
+// pass started, and a (numerically) rank-deficient Y2 -- noiseless rank-R
+// data with s2 > R -- is caught by the last pass's floor or leaves
+// orthonormal columns either way (tests/test_gpu_stage2.py).
 template <int SP>
 __global__ void __launch_bounds__(256) orth2_cholqr_kernel(double* Y2, int J, int s) {
   constexpr int LD = SP + 1, NBLK = GramBlocks<SP>::NBLK;
@@ -287,6 +233,7 @@ DP2_DEV bool eig_reg_any(double* A, int s, double* U) {
   return false;
 }
 
+// single block: eig(BB) -> E, D = Q2 U_R with the sign rule, Uf = U_R * sign / E
 __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, const double* Q2, int64_t J,
                                                             int R, double* D, double* E, double* Uf,
                                                             double* Ubuf, int64_t* status) {
@@ -368,20 +315,33 @@ __global__ void f_kernel(const double* C, int64_t N, int s, const double* Uf, in
 }
 
 namespace {
+// split of the reduction dimension for the split-K products: about two CTAs
+// per SM in total, chunks of >= 256
+int splits_for(int64_t red, int64_t tiles, int sms) {
+  const int64_t want = (2 * (int64_t)sms + tiles - 1) / tiles;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (red + 255) / 256));
+}
+int64_t chunk_for(int64_t red, int splits) { return ((red + splits - 1) / splits + 3) / 4 * 4; }
+
 struct S2Layout {
-  size_t parts, Y, Z, Y2, C, bbp, BB, Uf, Ubuf, total;
+  size_t parts, Y, Z, Y2, C, BB, Uf, Ubuf, total;
+  int ks_nn, ms_g;
 };
 S2Layout s2_layout(int64_t J, int64_t KR, int s2, int R) {
   S2Layout L{};
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ng = (s2 + 23) / 24;
+  L.ks_nn = splits_for(KR, ((J + 63) / 64) * ng, sms);
+  L.ms_g = splits_for(KR, ((s2 + 63) / 64) * ng, sms);
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-  const size_t nch = (KR + kChunk - 1) / kChunk;
-  L.parts = take(nch * J * s2 * 8);
+  L.parts = take(std::max((size_t)L.ks_nn * J * s2, (size_t)L.ms_g * s2 * s2) * 8);
   L.Y = take(J * s2 * 8);
   L.Z = take(KR * s2 * 8);
   L.Y2 = take(J * s2 * 8);
   L.C = take(KR * s2 * 8);
-  L.bbp = take(nch * s2 * s2 * 8);
   L.BB = take(s2 * s2 * 8);
   L.Uf = take(s2 * R * 8);
   L.Ubuf = take(s2 * s2 * 8);
@@ -400,33 +360,32 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   double* Z = reinterpret_cast<double*>(ws + L.Z);
   double* Y2 = reinterpret_cast<double*>(ws + L.Y2);
   double* C = reinterpret_cast<double*>(ws + L.C);
-  double* bbp = reinterpret_cast<double*>(ws + L.bbp);
   double* BB = reinterpret_cast<double*>(ws + L.BB);
   double* Uf = reinterpret_cast<double*>(ws + L.Uf);
   double* Ubuf = reinterpret_cast<double*>(ws + L.Ubuf);
-  const int nch = (int)((KR + kChunk - 1) / kChunk);
-  const int ng = (s2 + 31) / 32;
-  // row-major M (J x KR) is column-major (KR x J); row-major B (KR x s2) is
-  // column-major (s2 x KR): Y = M B  <=>  Y_cm (s2 x J) = B_cm M_cm
+  const unsigned ng = (unsigned)((s2 + 23) / 24);
+  // out (J x s2) = M B (B: KR x s2): split over KR, ordered reduction
   auto nn = [&](const double* B, double* out) {
-    if (dgemm_cm(st, false, false, s2, (int)J, (int)KR, B, s2, M, (int)KR, out, s2)) return;
-    nn_partial_kernel<<<dim3((unsigned)J, nch, ng), 256, 0, st>>>(M, KR, KR, B, s2, s2, parts, J);
-    reduce_parts_kernel<<<(unsigned)((J * s2 + 255) / 256), 256, 0, st>>>(parts, nch, J * s2, out);
+    const int64_t kc = chunk_for(KR, L.ks_nn);
+    const int ks = (int)((KR + kc - 1) / kc);
+    nn_dmma_kernel<<<dim3((unsigned)((J + 63) / 64), ks, ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, kc, parts);
+    reduce_parts_kernel<<<(unsigned)((J * s2 + 255) / 256), 256, 0, st>>>(parts, ks, J * s2, out);
   };
-  // Z = M^T Y  <=>  Z_cm (s2 x KR) = Y_cm M_cm^T
+  // out (KR x s2) = M^T B (B: J x s2): one split, written in place
   auto tn = [&](const double* B, double* out) {
-    if (dgemm_cm(st, false, true, s2, (int)KR, (int)J, B, s2, M, (int)KR, out, s2)) return;
-    tn_kernel<<<dim3((unsigned)((KR + 255) / 256), ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, out, s2);
+    tn_dmma_kernel<<<dim3((unsigned)((KR + 63) / 64), 1, ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, J, out);
   };
   nn(omega2, Y);
   tn(Y, Z);
   nn(Z, Y2);
   if (!run_orth2(Y2, J, s2, st)) cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
   tn(Y2, C);
-  // BB = C^T C  <=>  C_cm C_cm^T (symmetric, so layout-neutral)
-  if (!dgemm_cm(st, false, true, s2, s2, (int)KR, C, s2, C, s2, BB, s2)) {
-    gram_partial_kernel<<<nch, 256, 0, st>>>(C, KR, s2, s2, bbp);
-    reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(bbp, nch, (int64_t)s2 * s2, BB);
+  // BB = C^T C (s2 x s2): split over the KR rows of C, ordered reduction
+  {
+    const int64_t mc = chunk_for(KR, L.ms_g);
+    const int ms = (int)((KR + mc - 1) / mc);
+    tn_dmma_kernel<<<dim3((unsigned)((s2 + 63) / 64), ms, ng), 256, 0, st>>>(C, s2, KR, s2, C, s2, s2, mc, parts);
+    reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(parts, ms, (int64_t)s2 * s2, BB);
   }
   stage2_final_kernel<<<1, 256, 0, st>>>(BB, s2, Y2, J, R, D, E, Uf, Ubuf, status);
   f_kernel<<<(unsigned)imin64((KR * R + 255) / 256, 4096), 256, 0, st>>>(C, KR, s2, Uf, R, F);

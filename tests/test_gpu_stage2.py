@@ -1,0 +1,66 @@
+"""Stage 2 (P/compress.py:108-111: the randomized SVD of M = [V_k S_k]) on the
+library's own DMMA kernels, against the oracle's compress on the same input:
+D (J x R) and F (KR x R) sign-aligned within 1e-7, E within 1e-9 relative
+(the c1 golden bounds), and D^T D = I.  Shapes: c2 (J=512, KR=10^4, s2=20),
+c4-like p = R = 50 (s2 = 100 -> five 24-column groups), the c5 width J=1000,
+and a noiseless planted rank-R tensor with s2 > R (the orthonormalisation of
+a rank-deficient Y2)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_signed(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    s = np.sign(np.sum(a * b, axis=0))
+    s[s == 0] = 1.0
+    return float(np.abs(a * s - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def _check(xs, R, oversampling=None, tol_d=1e-7, tol_e=1e-9):
+    from threadpoolctl import threadpool_limits
+
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    t = dp.IrregularTensor(xs)
+    rsvd = dp.RsvdParams(rank=R, oversampling=oversampling, seed=0)
+    comp = dp.compress(t, R, rsvd=rsvd)
+    with threadpool_limits(limits=1):
+        o = orc.compress([np.asarray(x, np.float64) for x in xs], R, seed=0, oversampling=oversampling,
+                         threads=os.cpu_count() or 1)
+    D, E, F = comp.col_basis.cpu().numpy(), comp.weights.cpu().numpy(), comp.cores.cpu().numpy()
+    assert np.abs(D.T @ D - np.eye(R)).max() <= 1e-10
+    assert float(np.abs(E - o.E).max() / o.E.max()) <= tol_e
+    assert rel_signed(D, o.D) <= tol_d, rel_signed(D, o.D)
+    # F's columns flip with D's (the sign rule is applied to D)
+    sg = np.sign(np.sum(D * o.D, axis=0))
+    assert float(np.abs(F * sg - o.F).max() / np.abs(o.F).max()) <= tol_d
+
+
+def test_stage2_c2_shape():
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c2"], num_slices=400)
+    _check(synth.generate(cfg, 0, threads=os.cpu_count()), 10)
+
+
+def test_stage2_wide_sketch_p_equals_r():
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c2"], num_slices=200, rank=50)
+    _check(synth.generate(cfg, 0, threads=os.cpu_count()), 50, oversampling=50)
+
+
+def test_stage2_c5_width():
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c5"], num_slices=40, dtype="f64")
+    _check(synth.generate(cfg, 0, threads=os.cpu_count()), 10)
+
+
+def test_stage2_noiseless_rank_deficient_y2():
+    """Exact rank-R data, s2 = R + 10 > R: Y2 = M M^T M Omega2 has numerical
+    rank R; Q2 must still be orthonormal and D, E, F match the reference."""
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=60, noise=0.0, rank=6)
+    _check(synth.generate(cfg, 1), 6, tol_d=1e-6, tol_e=1e-8)
