@@ -292,6 +292,21 @@ size_t dp2_fitness_workspace(const dp2_store* st);
 int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H, const double* V,
                 const double* W, double* out2_dev, void* ws, size_t ws_bytes, void* stream);
 
+/* out (K x n) = A^T B for row-major A (m x K) and B (m x n), fp64 on the DMMA
+ * pipe (the tall-skinny product of stage 2): the fit's M^T V for the
+ * zero-pass fitness. */
+int dp2_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int32_t n, double* out, void* stream);
+/* Zero-pass fitness terms (P/analysis.py:23-45 restated): for
+ * factors fresh from a fit on an fp64 tensor, with G_k = H diag(w_k),
+ * B_k = V^T M_k (MtV = M^T V, K R x R) and the polar factors Pi_k,
+ *   ||X_k - Q_k G_k V^T||^2 = ||X_k||^2 - 2 tr(Pi_k G_k B_k) + ||G_k V^T||^2;
+ * out2_dev = [sum_k ||X_k||^2, sum_k residual_k], slice-order reductions.
+ * sqnorm: per-slice ||X_k||^2 (dp2_slice_stats). */
+size_t dp2_zero_pass_workspace(int64_t K, int32_t R);
+int dp2_fitness_zero_pass(const double* MtV, int64_t K, int64_t J, int32_t R, const double* H, const double* V,
+                          const double* W, const double* polar, const double* sqnorm, double* out2_dev, void* ws,
+                          size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,10 @@ _SIGS = {
     "dp2_assemble_q_signed": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "dp2_fitness_workspace": (c_sz, [P(Store)]),
     "dp2_fitness": (c_i32, [P(Store), c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "dp2_gemm_tn": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_vp, c_vp]),
+    "dp2_zero_pass_workspace": (c_sz, [c_i64, c_i32]),
+    "dp2_fitness_zero_pass": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                      c_vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -3,16 +3,18 @@
 One streaming pass over the packed store computes both sum ||X_k||^2 and
 sum ||X_k - Q_k (H * w_k) V^T||^2 (fixed-order reductions).
 
-Zero-pass form for factors fresh from ``fit_dpar2`` on an
-fp64 tensor: with G_k = H diag(w_k) and Q_k orthonormal,
+Zero-pass form for device factors fresh from ``fit_dpar2``
+(``output="device"``) on an fp64 tensor: with G_k = H diag(w_k) and Q_k
+orthonormal,
 
     ||X_k - Q_k G_k V^T||^2 = ||X_k||^2 - 2 <Q_k^T X_k, G_k V^T> + ||G_k V^T||^2
 
 and stage 1 already holds Q_k^T X_k: Q_k = A_k Pi_k with A_k = Y_k P_k and
 C_k = X_k^T Y_k from the second pass, so Q_k^T X_k = Pi_k^T (C_k P_k)^T =
 Pi_k^T M_k^T, M_k the slice's (signed) block of the stage-1 matrix M.  The fit
-keeps V^T M (R x KR); the fitness is then R x R work per slice, no pass over X
-(||X_k||^2 comes from the tensor's stored slice norms).  Rank-deficient slices
+keeps M^T V (KR x R, dp2_gemm_tn); the fitness is then R x R work per slice in
+one library kernel (dp2_fitness_zero_pass), no pass over X (||X_k||^2 comes
+from the tensor's stored slice norms).  Rank-deficient slices
 (completed A_k columns are not Y_k P_k) and fp32 stores (M from tf32
 products) use the streaming pass.
 """
@@ -31,25 +33,34 @@ from .tensor import IrregularTensor, stream_ptr
 
 
 def _zero_pass_terms(tensor, factors, d):
-    """(sum ||X_k||^2, sum residual) from the fit's V^T M, or None when the
-    factors do not carry it for this tensor (or it does not apply)."""
+    """(sum ||X_k||^2, sum residual) from the fit's M^T V (dp2_fitness_zero_pass),
+    or None when it does not apply: the factors are not the device factors of
+    a fit of this very tensor, or were modified since (V compared with the
+    fit's private copy; Q by identity and version counter), or a slice was
+    rank deficient (its completed A_k columns are not Y_k P_k)."""
     zp = getattr(factors, "_zero_pass", None)
     if not zp or zp["tensor"]() is not tensor:
+        return None
+    if factors.Q is not zp["Q"] or factors.Q_packed is not zp["Q_packed"] or \
+            factors.Q_packed._version != zp["Q_version"]:
         return None
     R = factors.H.shape[1]
     if int(zp["rank_found"].min().item()) < R:
         return None
     V = d(factors.V)
-    if not torch.equal(V, zp["V"]):  # V^T M was formed with the fit's V
+    if not torch.equal(V, zp["V"]):  # M^T V was formed with the fit's V
         return None
     H, W = d(factors.H), d(factors.W)
-    K = W.shape[0]
-    G = H[None, :, :] * W[:, None, :]                               # G_k = H diag(w_k)
-    B = zp["VtM"].reshape(R, K, R).permute(1, 0, 2)                 # B_k = V^T M_k
-    cross = (zp["polar"] * torch.bmm(G, B).transpose(1, 2)).sum(dim=(1, 2))   # tr(Pi_k G_k B_k)
-    norm = (torch.matmul(G, V.t() @ V) * G).sum(dim=(1, 2))         # ||G_k V^T||^2
-    sq = tensor.slice_sq_norms()
-    return float(sq.sum().item()), float((sq - 2.0 * cross + norm).sum().item())
+    K, J = W.shape[0], V.shape[0]
+    dev = V.device
+    lib = _lib.lib()
+    ws = workspace(lib.dp2_zero_pass_workspace(K, R), dev)
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    _lib.check(lib.dp2_fitness_zero_pass(_vp(zp["MtV"]), K, J, R, _vp(H), _vp(V), _vp(W), _vp(zp["polar"]),
+                                         _vp(tensor.slice_sq_norms()), _vp(out), _vp(ws), ws.numel(), stream_ptr()),
+               "fitness_zero_pass")
+    total, resid = out.cpu().tolist()
+    return total, resid
 
 
 def fitness(tensor: IrregularTensor, factors: Parafac2Factors, threads=None, zero_pass=True):

@@ -452,4 +452,23 @@ int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H
   return e == cudaSuccess ? ok(2) : fail(e, "dp2_fitness");
 }
 
+int dp2_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int32_t n, double* out, void* stream) {
+  if (!A || !B || !out || m < 1 || K < 1 || n < 1) return fail_arg("invalid arguments");
+  cudaError_t e = dp2::run_gemm_tn(A, m, K, B, n, out, S(stream));
+  return e == cudaSuccess ? ok(1) : fail(e, "dp2_gemm_tn");
+}
+
+size_t dp2_zero_pass_workspace(int64_t K, int32_t R) { return dp2::zero_pass_bytes(K, R); }
+
+int dp2_fitness_zero_pass(const double* MtV, int64_t K, int64_t J, int32_t R, const double* H, const double* V,
+                          const double* W, const double* polar, const double* sqnorm, double* out2_dev, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if (!MtV || !H || !V || !W || !polar || !sqnorm || !out2_dev || K < 1 || J < 1 || R < 1 || R > 64 ||
+      ws_bytes < dp2::zero_pass_bytes(K, R))
+    return fail_arg("invalid arguments");
+  cudaError_t e = dp2::run_zero_pass_fitness(MtV, K, J, R, H, V, W, polar, sqnorm, out2_dev, static_cast<char*>(ws),
+                                             S(stream));
+  return e == cudaSuccess ? ok(3) : fail(e, "dp2_fitness_zero_pass");
+}
+
 }  // extern "C"

@@ -96,6 +96,10 @@ Staging g_stage;
 
 cudaError_t ensure_staging(int dev) {
   if (g_stage.device == dev) return cudaSuccess;
+  // the ring's last copies may still be landing (an earlier call that
+  // returned on an error): finish them before the buffers go away
+  for (int i = 0; i < kRing; ++i)
+    if (g_stage.ev[i]) cudaEventSynchronize(g_stage.ev[i]);
   for (int i = 0; i < kRing; ++i) {
     if (g_stage.buf[i]) cudaFreeHost(g_stage.buf[i]);
     if (g_stage.ev[i]) cudaEventDestroy(g_stage.ev[i]);
@@ -137,13 +141,19 @@ cudaError_t d2h_staged(void* dst, const void* src, size_t n, cudaStream_t st) {
     if (ei == cudaSuccess) ei = cudaEventRecord(g_stage.ev[i % kRing], st);
     return ei;
   };
+  // on any error, drain the stream before returning: chunk copies already
+  // issued into the pinned ring must not land after the next call reuses it
+  auto bail = [&](cudaError_t err) {
+    cudaStreamSynchronize(st);
+    return err;
+  };
   for (size_t i = 0; i < std::min<size_t>(kRing, nch); ++i)
-    if ((e = issue(i)) != cudaSuccess) return e;
+    if ((e = issue(i)) != cudaSuccess) return bail(e);
   for (size_t i = 0; i < nch; ++i) {
-    if ((e = cudaEventSynchronize(g_stage.ev[i % kRing])) != cudaSuccess) return e;
+    if ((e = cudaEventSynchronize(g_stage.ev[i % kRing])) != cudaSuccess) return bail(e);
     const size_t o = i * kChunk, nb = std::min(kChunk, n - o);
     g_stage.team->run(d + o, g_stage.buf[i % kRing], nb);
-    if (i + kRing < nch && (e = issue(i + kRing)) != cudaSuccess) return e;
+    if (i + kRing < nch && (e = issue(i + kRing)) != cudaSuccess) return bail(e);
   }
   return cudaSuccess;
 }

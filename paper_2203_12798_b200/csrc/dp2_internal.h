@@ -72,6 +72,12 @@ cudaError_t run_assemble_q(const dp2_store* st, const double* A, int R, const do
 size_t fitness_bytes(const dp2_store* st);
 cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const double* H, const double* V,
                         const double* W, double* out2, char* ws, cudaStream_t stream);
+cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out,
+                        cudaStream_t st);
+size_t zero_pass_bytes(int64_t K, int R);
+cudaError_t run_zero_pass_fitness(const double* MtV, int64_t K, int64_t J, int R, const double* H, const double* V,
+                                  const double* W, const double* polar, const double* sq, double* out2, char* ws,
+                                  cudaStream_t st);
 cudaError_t run_slice_stats(const dp2_store* st, double* sqnorm, int64_t* status, cudaStream_t stream);
 
 cudaError_t run_omega(uint64_t seed, int64_t K, int J, const int32_t* s_k, int sp, const int64_t* slice_ids,

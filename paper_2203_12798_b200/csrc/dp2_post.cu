@@ -270,4 +270,70 @@ cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const doubl
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- zero-pass fitness
+// for factors fresh from fit_dpar2 on an fp64 tensor,
+//   ||X_k - Q_k G_k V^T||^2 = ||X_k||^2 - 2 tr(Pi_k G_k B_k) + ||G_k V^T||^2,
+// G_k = H diag(w_k), B_k = V^T M_k (M_k the slice's block of the stage-1 M,
+// MtV = M^T V holds B_k^T), Pi_k the polar factor (Q_k^T X_k = Pi_k^T M_k^T).
+// One warp per slice; terms[k] = sq_k - 2 cross_k + norm_k.
+__global__ void zero_pass_terms_kernel(const double* MtV, const double* H, const double* W, const double* polar,
+                                       const double* VV, const double* sq, int64_t K, int R, double* terms) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= K) return;
+  const double* w = W + k * R;
+  const double* Bt = MtV + k * R * R;  // Bt[c][b] = B_k[b][c]
+  const double* P = polar + k * R * R;
+  double cross = 0.0, norm = 0.0;
+  for (int e = lane; e < R * R; e += 32) {
+    const int j = e / R, i = e % R;
+    // (G_k B_k)[j][i] = sum_b H[j][b] w[b] B_k[b][i]
+    double gb = 0.0;
+    for (int b = 0; b < R; ++b) gb = fma(H[j * R + b] * w[b], Bt[i * R + b], gb);
+    cross = fma(P[i * R + j], gb, cross);
+    // (G_k VV)[j][i] G_k[j][i]
+    double gv = 0.0;
+    for (int b = 0; b < R; ++b) gv = fma(H[j * R + b] * w[b], VV[b * R + i], gv);
+    norm = fma(gv, H[j * R + i] * w[i], norm);
+  }
+  cross = warp_sum(cross);
+  norm = warp_sum(norm);
+  if (lane == 0) terms[k] = sq[k] - 2.0 * cross + norm;
+}
+
+// out2 = [sum_k sq_k, sum_k terms_k] in slice order (one thread: deterministic)
+__global__ void zero_pass_reduce_kernel(const double* sq, const double* terms, int64_t K, double* out2) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int64_t k = 0; k < K; ++k) {
+    a += sq[k];
+    b += terms[k];
+  }
+  out2[0] = a;
+  out2[1] = b;
+}
+
+// VV = V^T V (R x R), one block, fixed-order sums over J
+__global__ void gram_v_kernel(const double* V, int64_t J, int R, double* VV) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int a = e / R, b = e % R;
+    double acc = 0.0;
+    for (int64_t j = 0; j < J; ++j) acc = fma(V[j * R + a], V[j * R + b], acc);
+    VV[e] = acc;
+  }
+}
+
+size_t zero_pass_bytes(int64_t K, int R) { return ((size_t)K + (size_t)R * R) * 8 + 512; }
+
+cudaError_t run_zero_pass_fitness(const double* MtV, int64_t K, int64_t J, int R, const double* H, const double* V,
+                                  const double* W, const double* polar, const double* sq, double* out2, char* ws,
+                                  cudaStream_t st) {
+  double* terms = reinterpret_cast<double*>(ws);
+  double* VV = terms + ((K + 31) & ~(int64_t)31);
+  gram_v_kernel<<<1, 256, 0, st>>>(V, J, R, VV);
+  zero_pass_terms_kernel<<<(unsigned)((K + 7) / 8), 256, 0, st>>>(MtV, H, W, polar, VV, sq, K, R, terms);
+  zero_pass_reduce_kernel<<<1, 32, 0, st>>>(sq, terms, K, out2);
+  return cudaGetLastError();
+}
+
 }  // namespace dp2

@@ -352,6 +352,15 @@ S2Layout s2_layout(int64_t J, int64_t KR, int s2, int R) {
 
 size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R) { return s2_layout(J, KR, s2, R).total; }
 
+// out (K x n) = A^T B for row-major A (m x K) and B (m x n): the tall-skinny
+// DMMA product of stage 2, exported for the fit's V^T M (zero-pass fitness)
+cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out,
+                        cudaStream_t st) {
+  tn_dmma_kernel<<<dim3((unsigned)((K + 63) / 64), 1, (unsigned)((n + 23) / 24)), 256, 0, st>>>(A, K, m, K, B, n, n,
+                                                                                                 m, out);
+  return cudaGetLastError();
+}
+
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
                        double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t st) {
   const S2Layout L = s2_layout(J, KR, s2, R);

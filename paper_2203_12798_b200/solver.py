@@ -2,9 +2,10 @@
 
 ``fit_dpar2(tensor, rank, opts) -> (Parafac2Factors, FitTrace)`` keeps the
 reference entry point, return values, errors and stop rule.  The whole
-iteration loop runs on the device (one CUDA graph; the stop rule
-``prev == 0 or |prev - e| <= tol * prev`` is evaluated by the last kernel of
-each iteration), so the host only launches and reads the trace at the end.
+iteration loop runs on the device (one cooperative persistent kernel for
+R <= 16, else a seven-kernel loop; the stop rule ``prev == 0 or |prev - e| <=
+tol * prev`` is evaluated on the device each iteration), so the host only
+launches and reads the trace at the end.
 
 The kernel-granular functions (update_rotations, mttkrp_mode1/2/3,
 update_factors, convergence_metric) mirror the reference's test-level API;
@@ -224,9 +225,15 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     launched = _als_launch(comp, h, v, w, opts.max_iters, opts.tol, normalize, use_graph=use_graph)
     Q = assemble_q(tensor, comp, launched[3])
     zero_pass = None
-    if tensor.dtype == "f64":  # V^T M (R x KR) for fitness without a pass over X (analysis.py)
-        zero_pass = dict(VtM=torch.mm(launched[1].t(), comp._stage1_M), V=launched[1], polar=launched[3],
-                         rank_found=comp.rank_found, tensor=weakref.ref(tensor))
+    if tensor.dtype == "f64" and output == "device":
+        # M^T V (KR x R) for the fitness without a pass over X (analysis.py); the
+        # fit's V is kept as a private copy so later edits of factors.V are seen
+        V = launched[1]
+        MtV = torch.empty((comp._stage1_M.shape[1], rank), dtype=torch.float64, device=V.device)
+        _lib.check(_lib.lib().dp2_gemm_tn(_vp(comp._stage1_M), comp._stage1_M.shape[0], comp._stage1_M.shape[1],
+                                          _vp(V), rank, _vp(MtV), stream_ptr()), "gemm_tn")
+        zero_pass = dict(MtV=MtV, V=V.clone(), polar=launched[3], rank_found=comp.rank_found,
+                         tensor=weakref.ref(tensor))
     comp._stage1_M = None
     q_host = None
     if output == "numpy":
@@ -252,5 +259,7 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
         # staged D2H (device_to_numpy): a fresh pinned destination per fit
         # costs ~0.5 ms/MB to pin, far more than the copy
         factors = factors.numpy(q_out=q_host.result())
+    if zero_pass is not None:  # valid while these very factor objects are unmodified
+        zero_pass.update(Q=factors.Q, Q_packed=factors.Q_packed, Q_version=factors.Q_packed._version)
     factors._zero_pass = zero_pass
     return factors, trace

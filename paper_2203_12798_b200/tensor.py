@@ -38,10 +38,14 @@ def device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def stream_ptr():
-    """Raw handle of the current CUDA stream (torch's C accessor: no Stream
-    object per call -- a fit passes it a dozen times on its enqueue path)."""
-    return C.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
+def stream_ptr(dev=None):
+    """Raw handle of the current CUDA stream of ``dev`` (default: the current
+    device; torch's C accessor: no Stream object per call -- a fit passes it a
+    dozen times on its enqueue path)."""
+    index = torch.cuda.current_device() if dev is None else torch.device(dev).index
+    if index is None:
+        index = torch.cuda.current_device()
+    return C.c_void_p(torch._C._cuda_getCurrentRawStream(index))
 
 
 _COPY_STREAMS = {}
@@ -401,10 +405,12 @@ def to_device_async(values, dtype, dev):
     out = torch.empty(tuple(src.shape), dtype=dtype, device=dev)
     nbytes = src.numel() * src.element_size()
     if nbytes:
-        _lib.check(_lib.lib().dp2_copy_h2d_small(C.c_void_p(out.data_ptr()), C.c_void_p(src.data_ptr()), nbytes,
-                                                  stream_ptr()), "copy_h2d_small")
-        ev = torch.cuda.Event()
-        ev.record()
+        # launched (and ordered) on dev's current stream, under dev's context
+        with torch.cuda.device(out.device):
+            _lib.check(_lib.lib().dp2_copy_h2d_small(C.c_void_p(out.data_ptr()), C.c_void_p(src.data_ptr()),
+                                                      nbytes, stream_ptr(out.device)), "copy_h2d_small")
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(out.device))
         _SMALL_KEEP.append((src, ev))
         if len(_SMALL_KEEP) > _SMALL_KEEP_MAX:
             _SMALL_KEEP[:] = [(t, e) for t, e in _SMALL_KEEP if not e.query()]
