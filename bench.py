@@ -299,10 +299,13 @@ def main():
     launches = int(_lib.lib().dp2_launch_count(1))
     clk = clocks.stop()
     ms = start.elapsed_time(stop) / args.steps
+    multi = None
     if sharded:
+        own = ms
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        multi = multi_gpu_record(runner, cfg, world, own)
     value = total_entries / (ms * 1e-3)
     # per-phase breakdown from one extra, untimed step (its timing events
     # synchronise mid-fit, which the timed steps must not do)
@@ -326,6 +329,8 @@ def main():
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if multi is not None:
+        line["multi_gpu"] = multi
     line.update(roofline_fields(tm, tr, tensor, cfg, sharded, runner if sharded else None))
     if not args.no_e2e:
         line["e2e"] = e2e_sharded(runner, cfg, opts, args) if sharded else e2e(xs, cfg, opts, args)
@@ -350,6 +355,45 @@ def main():
         emit(line)
     if sharded:
         dist.destroy_process_group()
+
+
+def multi_gpu_record(runner, cfg, world, own_ms):
+    """N > 1: the ALS split the fit used, measured NCCL costs on this box
+    (one R x R-partials allreduce and the M all-gather, CUDA events, after the
+    timed region), NCCL time per iteration, and every rank's own step time
+    (its share of the max-over-ranks clock)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2203_12798_b200 import distributed as D_
+    R, J, K = cfg.rank, cfg.cols, cfg.num_slices
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    part = torch.zeros(2 * R * R, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        dist.all_reduce(part)
+    dist.barrier()
+    ev[0].record()
+    for _ in range(32):
+        dist.all_reduce(part)
+    ev[1].record()
+    width = max(len(s) for s in runner.shards) * R
+    send = torch.zeros((J, width), dtype=torch.float64, device="cuda")
+    buf = torch.empty((world * J, width), dtype=torch.float64, device="cuda")
+    dist.all_gather_into_tensor(buf, send)
+    dist.barrier()
+    ev[2].record()
+    dist.all_gather_into_tensor(buf, send)
+    ev[3].record()
+    torch.cuda.synchronize()
+    ar_us = ev[0].elapsed_time(ev[1]) * 1e3 / 32
+    ag_ms = ev[2].elapsed_time(ev[3])
+    rank_ms = [torch.zeros(1, device="cuda") for _ in range(world)]
+    dist.all_gather(rank_ms, torch.tensor([own_ms], device="cuda"))
+    als = getattr(runner, "last_als", "replicated")
+    return {"als": als, "als_policy": "distributed.als_policy (DESIGN.md 7)",
+            "nccl_allreduce_us": ar_us, "nccl_ms_per_iter": (3 * ar_us * 1e-3) if als == "sharded" else 0.0,
+            "m_allgather_ms": ag_ms, "m_allgather_bytes_per_rank": J * width * 8,
+            "rank_ms_per_step": [float(x.item()) for x in rank_ms],
+            "rank_rows": [int(x) for x in runner.loads]}
 
 
 def roofline_fields(tm, tr, tensor, cfg, sharded, runner):

@@ -6,19 +6,22 @@
 * Stage 1: local, no communication; the per-slice sketch seeds use the
   GLOBAL slice index (derived_seed(seed, k), P/compress.py:96-103), so every
   slice gets exactly the reference's Omega_k wherever it lives.
-* Stage 2: M (J x KR) must be in global slice order (P/compress.py:108).  Each
-  rank scatters its J x R blocks into a zero J x KR buffer and one allreduce
-  (sum) assembles M exactly -- every entry has a single nonzero contributor, so
-  the sum is exact -- then stage 2 runs replicated (identical inputs, identical
-  outputs on every rank).
-* ALS (default ``als="replicated"``): after stage 2 every rank holds the full
-  compressed tensor (D, E and all K R x R cores F_k -- K R^2 doubles, tiny),
-  so each rank runs the single-GPU persistent ALS loop on all of it: no
-  per-iteration communication at all; Q is then assembled for the local
-  slices only (their A_k and polar factors).  ``als="sharded"`` keeps the
-  phase-split variant: D, E, H, V replicated, F rows / W rows / rotations
-  local, three allreduces of tiny buffers (2 R^2, 2 R^2, 1 doubles) per
-  iteration between the phases of ``dp2_als_phase``.
+* Stage 2: M (J x KR) must be in global slice order (P/compress.py:108).  One
+  all-gather of every rank's J x K_local R block (padded to the largest
+  shard) and a column permutation assemble it exactly (each rank sends 1/world
+  of M instead of allreducing a zero-padded J x KR buffer); stage 2 then runs
+  replicated (identical inputs, identical outputs on every rank).
+* ALS, ``als="auto"`` (default) picks by a measured cost model:
+  - ``"replicated"``: every rank holds the whole compressed tensor (D, E and
+    the K R x R cores -- tiny), so it runs the single-GPU persistent loop on
+    all of it with no per-iteration communication, then assembles Q for its
+    own slices (the winner at c2 scale: the persistent loop takes ~1.9 ms for
+    K = 1000);
+  - ``"sharded"``: D, E, H, V replicated; F rows, W rows and rotations local;
+    per iteration three allreduces of R x R sized partials between the phases
+    of ``dp2_als_phase`` (P/solver.py:81-111 and 133-149 are K-reductions),
+    the whole 32-iteration phase + NCCL sequence captured once in a CUDA graph
+    and replayed (the winner when K / world is large, e.g. c5: K = 20 000).
 
 The driver (``ShardedALS``) only sequences phases and collectives; the phase
 compute is a pluggable ``ops`` object (the C ABI on the GPU; the gloo tests on
@@ -43,18 +46,47 @@ def shard_slices(row_counts, world):
     return [sorted(s) for s in plan.sets], plan.loads
 
 
-def assemble_m(M_local, local_ids, K, R, group=None, cols=None):
-    """Exact J x KR M in global slice order from each rank's J x K_local R blocks
-    (``cols``: the device column index of the local blocks, see ``m_columns``)."""
+def gather_plan(shards, R, device):
+    """(block width, column permutation) of the all-gather M assembly: rank r
+    sends its J x K_r R block padded to ``width`` columns; global column
+    k R + c of M is column perm[k R + c] of the gathered J x (world width)."""
+    width = max(len(s) for s in shards) * R
+    K = sum(len(s) for s in shards)
+    perm = np.empty(K * R, dtype=np.int64)
+    for r, ids in enumerate(shards):
+        for li, k in enumerate(ids):
+            perm[k * R:(k + 1) * R] = r * width + li * R + np.arange(R)
+    if torch.device(device).type != "cuda":
+        return width, torch.from_numpy(perm)
+    from .tensor import to_device_async
+    return width, to_device_async(perm, torch.int64, device)
+
+
+def assemble_m(M_local, local_ids, K, R, group=None, shards=None, plan=None):
+    """Exact J x KR M in global slice order from each rank's J x K_local R
+    block: one all-gather (blocks padded to the largest shard) and a column
+    permutation.  ``shards``: every rank's global slice ids (needed for
+    world > 1); ``plan``: a cached ``gather_plan``."""
     J = M_local.shape[0]
-    full = torch.zeros((J, K * R), dtype=M_local.dtype, device=M_local.device)
-    if len(local_ids):
-        if cols is None:
-            cols = m_columns(local_ids, R, M_local.device)
-        full[:, cols] = M_local
-    if dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(full, group=group)
-    return full
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        if list(local_ids) == list(range(K)):
+            return M_local
+        full = torch.zeros((J, K * R), dtype=M_local.dtype, device=M_local.device)
+        full[:, m_columns(local_ids, R, M_local.device)] = M_local
+        return full
+    width, perm = plan if plan is not None else gather_plan(shards, R, M_local.device)
+    send = M_local
+    if send.shape[1] != width:
+        send = torch.zeros((J, width), dtype=M_local.dtype, device=M_local.device)
+        send[:, :M_local.shape[1]] = M_local
+    send = send.contiguous()
+    buf = torch.empty((world * J, width), dtype=M_local.dtype, device=M_local.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(buf, send, group=group)
+    else:
+        dist.all_gather(list(buf.view(world, J, width).unbind(0)), send, group=group)
+    return buf.view(world, J, width).permute(1, 0, 2).reshape(J, world * width).index_select(1, perm)
 
 
 def m_columns(local_ids, R, device):
@@ -146,6 +178,65 @@ class GpuAlsOps:
         return out.clone() if out is not None else None
 
 
+class GraphedShardedALS:
+    """The sharded loop with static buffers, captured once (all phases of all
+    iterations plus the NCCL allreduces between them) into a CUDA graph and
+    replayed per fit: no per-phase host launches.  Falls back to eager
+    sequencing if the capture is refused (e.g. a backend without graph-safe
+    collectives)."""
+
+    def __init__(self, K_local, J, R, max_iters, tol, normalize, dev, allreduce):
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.F = torch.zeros((K_local * R, R), **f64)
+        self.D = torch.zeros((J, R), **f64)
+        self.E = torch.zeros(R, **f64)
+        self.H = torch.zeros((R, R), **f64)
+        self.V = torch.zeros((J, R), **f64)
+        self.W = torch.zeros((K_local, R), **f64)
+        self.ops = GpuAlsOps(self.F, self.D, self.E, self.H, self.V, self.W, J, R, max_iters, tol, normalize)
+        self.allreduce, self.max_iters = allreduce, max_iters
+        self.graph = None
+        self.captured = False
+
+    def run(self, F_local, D, E, H, V, W):
+        from .tensor import new_status
+        for dst, src in ((self.F, F_local), (self.D, D), (self.E, E), (self.H, H), (self.V, V), (self.W, W)):
+            dst.copy_(src)
+        self.ops.status.copy_(new_status(self.F.device))
+        if self.graph is None:
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    ShardedALS(self.ops, self.allreduce).run(self.max_iters)
+                self.graph, self.captured = g, True
+            except Exception:  # capture refused: eager from now on
+                self.graph = False
+        if self.graph:
+            self.graph.replay()
+        else:
+            ShardedALS(self.ops, self.allreduce).run(self.max_iters)
+        return self.ops
+
+
+def als_policy(K, world, J, R, nccl_us=16.0):
+    """'replicated' or 'sharded' by the cost model of DESIGN.md §7, measured on
+    one B200 for 32 iterations at J = 1000 (tools/scratch/als_scale.py,
+    shard_cost.py): the persistent replicated loop costs ~0.9 ms + 0.9 us per
+    slice (K = 1000: 1.9 ms, 20 000: 18.8 ms); the graph-captured sharded
+    phase loop ~4 ms + 1.9 us per local slice (125: 5.8 ms, 2 500: 12.0 ms)
+    plus 96 allreduces of R x R partials (~16 us each, NCCL small-message
+    floor).  c2 (K = 1000) stays replicated at any world size; c5 (K = 20 000)
+    shards from 4 GPUs up."""
+    if world <= 1:
+        return "replicated"
+    if R > 16:  # the persistent loop covers R <= 16; beyond it both use the phase kernels
+        return "sharded"
+    t_rep = 0.9 + 0.9e-3 * K
+    k_local = -(-K // world)
+    t_shard = 4.0 + 1.9e-3 * k_local + 32 * 3 * nccl_us * 1e-3
+    return "sharded" if t_shard < t_rep else "replicated"
+
+
 def nccl_allreduce(group=None):
     def f(t):
         if dist.is_initialized() and dist.get_world_size(group) > 1:
@@ -165,6 +256,7 @@ class DistributedFit:
         from .tensor import IrregularTensor
         rows_all, _, _ = synth.shared_factors(cfg, seed)
         shards, loads = shard_slices(rows_all, world)
+        self.shards = shards
         self.local_ids = shards[rank]
         self.rank, self.world, self.cfg, self.seed = rank, world, cfg, seed
         if host_slices is not None:
@@ -181,7 +273,7 @@ class DistributedFit:
         self.K = cfg.num_slices
         self.loads = loads
 
-    def fit(self, R, opts, timings=None, als="replicated", tensor=None, _exact_omega=False):
+    def fit(self, R, opts, timings=None, als="auto", tensor=None, _exact_omega=False):
         """Fit the whole tensor with this rank's slices from ``tensor`` (default:
         the device-resident shard; a host-backed ``IrregularTensor`` of the same
         slices is uploaded in chunks overlapped with stage 1, as in
@@ -217,9 +309,14 @@ class DistributedFit:
         A, M_local, rank_found, status = res[:4]
         check = res[4] if len(res) > 4 else None
         om2 = stage2_omega_finish(om2h)  # tail replay + patch, while stage 1 runs
-        M = assemble_m(M_local, self.local_ids, K, R, cols=cols)
+        if getattr(self, "_gather", None) is None or self._gather[0] != (R, dev):
+            self._gather = ((R, dev), gather_plan(self.shards, R, dev))
+        M = assemble_m(M_local, self.local_ids, K, R, shards=self.shards, plan=self._gather[1])
         D, E, F = run_stage2(M, J, K * R, R, second.seed, s2, om2, status, timings=timings)
         normalize = bool(opts.normalize) if opts.normalize is not None else True
+        if als == "auto":
+            als = als_policy(K, self.world, J, R)
+        self.last_als = als
         if als == "replicated":
             h, v, w = initial_factors(J, K, R, opts.seed)
             H, V, W, polar, trace, tstamp, iters, st_als = replicated_als(
@@ -228,14 +325,19 @@ class DistributedFit:
             W_out = W.index_select(0, ids)
         else:
             h, v, w = initial_factors(J, len(self.local_ids), R, opts.seed)
-            H, V = torch.from_numpy(h).to(dev), torch.from_numpy(v).to(dev)
-            W = torch.from_numpy(w).to(dev)
-            ops = GpuAlsOps(local_rows(F, self.local_ids, R), D, E, H, V, W, J, R, opts.max_iters, opts.tol,
-                            normalize)
-            ShardedALS(ops, nccl_allreduce()).run(opts.max_iters)
-            st_als = ops.status
-            H, V, W_out, polar_local = ops.H, ops.V, ops.W, ops.polar
-            trace, tstamp, iters = ops.trace, ops.tstamp, ops.iters
+            key = (len(self.local_ids), J, R, opts.max_iters, float(opts.tol), normalize, dev)
+            if getattr(self, "_als_graph", None) is None or self._als_graph[0] != key:
+                self._als_graph = (key, GraphedShardedALS(len(self.local_ids), J, R, opts.max_iters, opts.tol,
+                                                          normalize, dev, nccl_allreduce()))
+            if getattr(self, "_ids_f", None) is None or self._ids_f[0] != (R, dev):
+                self._ids_f = ((R, dev), (torch.as_tensor(self.local_ids, device=dev)[:, None] * R +
+                                          torch.arange(R, device=dev)[None, :]).reshape(-1))
+            to = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)  # noqa: E731
+            ops = self._als_graph[1].run(F.index_select(0, self._ids_f[1]), D, E, to(h), to(v), to(w))
+            # the graph's static buffers are reused by the next fit: copy the results out
+            st_als = ops.status.clone()
+            H, V, W_out, polar_local = ops.H.clone(), ops.V.clone(), ops.W.clone(), ops.polar.clone()
+            trace, tstamp, iters = ops.trace.clone(), ops.tstamp.clone(), ops.iters.clone()
         from .compress import CompressedTensor
         comp = CompressedTensor(rank=R, A=A, row_off=t.row_off_host.copy(), col_basis=D, weights=E, cores=F,
                                 a_signs=a_signs)

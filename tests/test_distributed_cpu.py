@@ -1,5 +1,5 @@
 """Multi-GPU host logic on CPU with gloo, world size 2 (no GPU needed):
-LPT shard placement, exact M assembly by allreduce, and the sharded ALS phase
+LPT shard placement, exact M assembly by all-gather + column permutation, and the sharded ALS phase
 sequence (ShardedALS + 3 allreduces per iteration) against the single-process
 oracle, with the per-phase compute emulated in NumPy on each rank's slices."""
 import os
@@ -53,7 +53,7 @@ def _assemble(rank, world):
     shards, _ = D_.shard_slices([int(r) for r in np.random.default_rng(6).integers(1, 100, K)], world)
     ids = shards[rank]
     local = np.concatenate([M[:, k * R:(k + 1) * R] for k in ids], axis=1) if ids else np.zeros((J, 0))
-    full = D_.assemble_m(torch.from_numpy(local), ids, K, R)
+    full = D_.assemble_m(torch.from_numpy(local), ids, K, R, shards=shards)
     assert full.numpy().tobytes() == M.tobytes()
 
 
@@ -159,3 +159,34 @@ def _sharded_als(rank, world, tol):
 @pytest.mark.parametrize("tol", [0.0, 1e-3])
 def test_sharded_als_matches_oracle_gloo(tol):
     run_world(_sharded_als, 2, tol)
+
+
+def _assemble_uneven(rank, world):
+    K, J, R = 29, 5, 4
+    rows = [int(r) for r in np.random.default_rng(8).integers(1, 5000, K)]
+    M = np.random.default_rng(9).standard_normal((J, K * R))
+    shards, _ = D_.shard_slices(rows, world)
+    ids = shards[rank]
+    local = np.concatenate([M[:, k * R:(k + 1) * R] for k in ids], axis=1)
+    plan = D_.gather_plan(shards, R, "cpu")
+    full = D_.assemble_m(torch.from_numpy(local), ids, K, R, shards=shards, plan=plan)
+    assert full.numpy().tobytes() == M.tobytes()
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_assemble_m_allgather_uneven_shards(world):
+    """All-gather of padded per-rank blocks + column permutation == M, bit
+    for bit, for shards of different sizes (LPT over heavy-tailed rows)."""
+    run_world(_assemble_uneven, world)
+
+
+def test_als_policy_cost_model():
+    """The default ALS split (DistributedFit(als="auto")): replicated on one
+    GPU and for c2 (K = 1000) at any world size; sharded for c5 (K = 20 000)
+    from 4 GPUs; sharded whenever R > 16 (no persistent loop there)."""
+    assert D_.als_policy(1000, 1, 512, 10) == "replicated"
+    assert all(D_.als_policy(1000, w, 512, 10) == "replicated" for w in (2, 4, 8))
+    assert D_.als_policy(20000, 8, 1000, 10) == "sharded"
+    assert D_.als_policy(20000, 4, 1000, 10) == "sharded"
+    assert D_.als_policy(20000, 2, 1000, 10) == "replicated"
+    assert D_.als_policy(1000, 2, 512, 50) == "sharded"

@@ -76,3 +76,40 @@ def test_distributed_fit_replicated_als_world1_matches_fit():
     assert np.allclose(tr.objective, tr2.objective, rtol=1e-12, atol=0)
     q1, q2 = f.Q_packed.cpu().numpy(), g.Q_packed.cpu().numpy()
     assert np.abs(q1 - q2).max() <= 1e-10
+
+
+def _nccl_world1():
+    import socket
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    return dist
+
+
+@pytest.mark.parametrize("als", ["sharded", "replicated", "auto"])
+def test_distributed_fit_nccl_world1_matches_fit(als):
+    """DistributedFit over a real NCCL process group (world size 1 on this
+    box): the all-gather M assembly, and the sharded ALS captured with its
+    allreduces in a CUDA graph (replayed on the second fit) or the replicated
+    loop, reproduce fit_dpar2."""
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import distributed as D_, synth
+    _nccl_world1()
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=30)
+    runner = D_.DistributedFit(cfg, 4, 0, 1, host_slices=synth.generate(cfg, 4))
+    opts = dp.SolverOptions(max_iters=12, tol=0.0, seed=0)
+    g, tr2 = dp.fit_dpar2(runner.tensor, cfg.rank, opts, output="device")
+    for rep in range(2):  # second fit replays the captured graph
+        f, tr = runner.fit(cfg.rank, opts, als=als)
+        for key in ("H", "V", "W"):
+            a, b = getattr(f, key).cpu().numpy(), getattr(g, key).cpu().numpy()
+            assert np.abs(a - b).max() <= 1e-9 * max(np.abs(b).max(), 1.0), (als, rep, key)
+        assert np.allclose(tr.objective, tr2.objective, rtol=1e-10, atol=0)
+        q1, q2 = f.Q_packed.cpu().numpy(), g.Q_packed.cpu().numpy()
+        assert np.abs(q1 - q2).max() <= 1e-9
+    if als == "sharded":
+        assert runner._als_graph[1].captured, "the sharded loop was not captured in a CUDA graph"
