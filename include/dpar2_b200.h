@@ -200,6 +200,14 @@ int dp2_stage1_signs(const dp2_store* st, const double* omega_dev, const int32_t
                      int32_t rank, double* A_out, double* M_out, int32_t* rank_out, double* a_signs_out,
                      void* ws, size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
 
+/* dp2_stage1 / dp2_stage1_signs (a_signs_out nullable) with ``power_iters``
+ * power iterations (RsvdParams.power_iters, P/linalg.py:124-126): q sketch
+ * passes Z = X^T (X B) each followed by B <- orth(Z), then the final pass on B
+ * (q = 0: on Omega itself).  dp2_stage1 is q = 1. */
+int dp2_stage1_power(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
+                     int32_t power_iters, double* A_out, double* M_out, int32_t* rank_out, double* a_signs_out,
+                     void* ws, size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream);
+
 /* One streaming pass of stage 1 (the two sketch products of
  * P/linalg.py:124-127 fused per piece): for every piece p (segment x slice)
  *   out_part[p] (J x sp)  = X_p^T (X_p B_k),  B = b_dev[k] (K x J x sp, fp64)
@@ -215,6 +223,10 @@ int dp2_stream_pass(const dp2_store* st, const double* b_dev, int32_t sp, double
  * F (KR x rank), sign rule on D.  omega2_dev: KR x s2 (P/linalg.py:122-123
  * seeded with derived_seed(seed, K)). */
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank);
+/* dp2_stage2 with Y2 = (M M^T)^q M Omega2 (power_iters = q; dp2_stage2 is q = 1). */
+int dp2_stage2_power(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2,
+                     int32_t rank, int32_t power_iters, double* D_out, double* E_out, double* F_out, void* ws,
+                     size_t ws_bytes, int64_t* status_dev, void* stream);
 int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2,
                int32_t rank, double* D_out, double* E_out, double* F_out, void* ws, size_t ws_bytes,
                int64_t* status_dev, void* stream);

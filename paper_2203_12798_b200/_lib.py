@@ -62,7 +62,11 @@ _SIGS = {
                            P(c_f32), c_vp]),
     "dp2_stage1_signs": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
                                  P(c_f32), c_vp]),
+    "dp2_stage1_power": (c_i32, [P(Store), c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                 c_vp, P(c_f32), c_vp]),
     "dp2_stage2_workspace": (c_sz, [c_i64, c_i64, c_i32, c_i32]),
+    "dp2_stage2_power": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp,
+                                 c_vp]),
     "dp2_stage2": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp, c_vp]),
     "dp2_als_workspace": (c_sz, [c_i64, c_i64, c_i32]),
     "dp2_als_stamp_offset": (c_sz, [c_i64, c_i64, c_i32]),

@@ -137,8 +137,6 @@ def check_rank(tensor: IrregularTensor, rank, slice_ids=None):
 def stage2_params(base: RsvdParams, stage2, rank, K, J):
     second = stage2 if stage2 is not None else base
     second = replace(second, rank=rank, seed=derived_seed(second.seed, K))
-    if second.power_iters != 1:
-        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     return second, sketch_width(J, K * rank, rank, second.oversampling)
 
 
@@ -181,8 +179,6 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     (plus, with ``speculative``, the Omega replay check future or None --
     rng.omega_device).  With ``a_signs`` (device K x rank) A is returned up to
     its column signs, which go to ``a_signs`` (dp2_stage1_signs)."""
-    if base.power_iters != 1:
-        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
     dev = tensor.X.device
     widths, sp, s_dev = _stage1_setup(tensor, rank, base.oversampling, dev)
@@ -199,7 +195,8 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
     status = new_status(dev) if status is None else status
-    tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None, a_signs)
+    tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None, a_signs,
+                      base.power_iters)
     if timings is not None:
         timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
@@ -210,7 +207,8 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     return A, M, rank_found, status
 
 
-def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False, a_signs=None):
+def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False, a_signs=None,
+                 power_iters=1):
     """One dp2_stage1 call over ``tensor``'s slices (omega / s_dev / outputs
     already sliced to them); returns the phase timings when ``timed``."""
     nseg = nseg_for(tensor)
@@ -218,7 +216,11 @@ def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed
     lib = _lib.lib()
     ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), tensor.X.device)
     tm = (C.c_float * 8)() if timed else None
-    if a_signs is None:
+    if power_iters != 1:
+        _lib.check(lib.dp2_stage1_power(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, max(0, int(power_iters)),
+                                        _vp(A), _vp(M), _vp(rank_found), _vp(a_signs), _vp(ws), ws.numel(),
+                                        _vp(status), tm, stream_ptr()), "stage1")
+    elif a_signs is None:
         _lib.check(lib.dp2_stage1(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, _vp(A), _vp(M), _vp(rank_found),
                                   _vp(ws), ws.numel(), _vp(status), tm, stream_ptr()), "stage1")
     else:
@@ -244,8 +246,6 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
     stage 1 on a view of its slices with their global seeds, writing straight
     into the full A / rank buffers (M block copied into place).  Per-chunk
     status words merge with the slice offset."""
-    if base.power_iters != 1:
-        raise NotImplementedError("the device sketch implements power_iters=1 (the fit_dpar2 setting)")
     J, K = tensor.num_cols, tensor.num_slices
     rows = tensor.row_counts
     dev = tensor.X.device
@@ -277,7 +277,7 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
         Mc = torch.empty((J, (k1 - k0) * rank), dtype=torch.float64, device=dev)
         st_c = new_status(dev)
         _stage1_call(sub, rank, omega[k0:k1], s_dev[k0:k1], sp, A[r0:r1], Mc, rank_found[k0:k1], st_c,
-                     a_signs=None if a_signs is None else a_signs[k0:k1])
+                     a_signs=None if a_signs is None else a_signs[k0:k1], power_iters=base.power_iters)
         M[:, k0 * rank:k1 * rank].copy_(Mc)
         for sl in _ST_INDEX:
             idx = st_c[sl]
@@ -293,7 +293,7 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
     return A, M, rank_found, status
 
 
-def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None):
+def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None, power_iters=1):
     """Stage 2 (P/compress.py:109-111) on the device: D, E, F."""
     dev = M.device
     lib = _lib.lib()
@@ -308,8 +308,8 @@ def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)] if timings is not None else None
     if ev:
         ev[0].record()
-    _lib.check(lib.dp2_stage2(_vp(M), J, KR, _vp(om2), s2, rank, _vp(D), _vp(E), _vp(F), _vp(ws2), ws2.numel(),
-                              _vp(status), stream_ptr()), "stage2")
+    _lib.check(lib.dp2_stage2_power(_vp(M), J, KR, _vp(om2), s2, rank, max(0, int(power_iters)), _vp(D), _vp(E),
+                                    _vp(F), _vp(ws2), ws2.numel(), _vp(status), stream_ptr()), "stage2")
     if ev:
         ev[1].record()
         torch.cuda.synchronize()
@@ -369,7 +369,8 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     # device ahead of stage 1; its few tail draws are replayed and patched
     # now, while stage 1 runs
     om2 = stage2_omega(second.seed, K * rank, s2) if om2h is None else stage2_omega_finish(om2h)
-    D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2, status, timings=timings)
+    D, E, F = run_stage2(M, J, K * rank, rank, second.seed, s2, om2, status, timings=timings,
+                         power_iters=second.power_iters)
     comp = CompressedTensor(rank=rank, A=A, row_off=tensor.row_off_host.copy(), col_basis=D, weights=E,
                             cores=F, rank_found=rank_found, a_signs=a_signs)
     comp._omega_check = check

@@ -313,13 +313,14 @@ size_t dp2_stage1_workspace(const dp2_store* st, int32_t sp, int32_t rank) {
 
 static int stage1_impl(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp,
                        int32_t rank, double* A_out, double* M_out, int32_t* rank_out, void* ws, size_t ws_bytes,
-                       int64_t* status_dev, float* timing_ms, void* stream, double* a_signs) {
+                       int64_t* status_dev, float* timing_ms, void* stream, double* a_signs, int power_iters = 1) {
   if (!store_ok(st)) return fail_arg("invalid store");
   if (rank < 1 || rank > 64 || sp < rank || sp % 8 != 0 || (sp > 32 && sp % 32 != 0) || sp > 256)
     return fail_arg("invalid rank / sketch width");
+  if (power_iters < 0 || power_iters > 64) return fail_arg("power_iters out of range");
   if (ws_bytes < dp2::stage1_layout(st, sp, rank).total) return fail_arg("workspace too small");
   cudaError_t e = dp2::run_stage1(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out,
-                                  static_cast<char*>(ws), status_dev, timing_ms, S(stream), a_signs);
+                                  static_cast<char*>(ws), status_dev, timing_ms, S(stream), a_signs, power_iters);
   // sp <= 32: 2 streaming passes + orth (Gram, Cholesky, substitution, CGS2
   // fallback) + gather, factor, A + candidates, signs, [apply signs],
   // complete; the tensor-core pass adds its two B-image kernels and
@@ -346,19 +347,35 @@ int dp2_stage1_signs(const dp2_store* st, const double* omega_dev, const int32_t
                      stream, a_signs_out);
 }
 
+int dp2_stage1_power(const dp2_store* st, const double* omega_dev, const int32_t* s_dev, int32_t sp, int32_t rank,
+                     int32_t power_iters, double* A_out, double* M_out, int32_t* rank_out, double* a_signs_out,
+                     void* ws, size_t ws_bytes, int64_t* status_dev, float* timing_ms, void* stream) {
+  return stage1_impl(st, omega_dev, s_dev, sp, rank, A_out, M_out, rank_out, ws, ws_bytes, status_dev, timing_ms,
+                     stream, a_signs_out, power_iters);
+}
+
 size_t dp2_stage2_workspace(int64_t J, int64_t KR, int32_t s2, int32_t rank) {
   return dp2::stage2_bytes(J, KR, s2, rank);
+}
+
+int dp2_stage2_power(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2,
+                     int32_t rank, int32_t power_iters, double* D_out, double* E_out, double* F_out, void* ws,
+                     size_t ws_bytes, int64_t* status_dev, void* stream) {
+  if (rank < 1 || rank > 64 || s2 < rank || s2 > 150 || J < 1 || KR < 1) return fail_arg("invalid stage-2 shape");
+  if (power_iters < 0 || power_iters > 64) return fail_arg("power_iters out of range");
+  if (ws_bytes < dp2::stage2_bytes(J, KR, s2, rank)) return fail_arg("workspace too small");
+  cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
+                                  static_cast<char*>(ws), status_dev, S(stream), power_iters);
+  // our own DMMA GEMM kernels + ordered reductions + orth + final
+  return e == cudaSuccess ? ok(8 + 3 * power_iters)
+                          : fail(e, "dp2_stage2");
 }
 
 int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2, int32_t rank,
                double* D_out, double* E_out, double* F_out, void* ws, size_t ws_bytes, int64_t* status_dev,
                void* stream) {
-  if (rank < 1 || rank > 64 || s2 < rank || s2 > 150 || J < 1 || KR < 1) return fail_arg("invalid stage-2 shape");
-  if (ws_bytes < dp2::stage2_bytes(J, KR, s2, rank)) return fail_arg("workspace too small");
-  cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
-                                  static_cast<char*>(ws), status_dev, S(stream));
-  // our own kernels only (the DGEMMs run in cuBLAS when it is available)
-  return e == cudaSuccess ? ok(11) : fail(e, "dp2_stage2");
+  return dp2_stage2_power(M_dev, J, KR, omega2_dev, s2, rank, 1, D_out, E_out, F_out, ws, ws_bytes, status_dev,
+                          stream);
 }
 
 size_t dp2_als_workspace(int64_t K, int64_t J, int32_t R) { return dp2::als_bytes(K, J, R); }

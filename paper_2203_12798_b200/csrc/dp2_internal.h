@@ -18,7 +18,7 @@ struct Stage1Layout {
 Stage1Layout stage1_layout(const dp2_store* st, int sp, int R);
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
-                       float* timing, cudaStream_t stream, double* a_signs = nullptr);
+                       float* timing, cudaStream_t stream, double* a_signs = nullptr, int power_iters = 1);
 cudaError_t run_stage1_small(const dp2_store* st, const int32_t* s_dev, int sp, int R, const double* part1,
                              const double* part2, const double* gpart, double* qz, double* Ct, double* CCg,
                              double* Gg, const double* y2, double* Pm, double* Sv, double* sgn, double* cand_abs,
@@ -41,7 +41,8 @@ cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out
 
 size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R);
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
-                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t stream);
+                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t stream,
+                       int power_iters = 1);
 
 size_t als_bytes(int64_t K, int64_t J, int R);
 size_t als_stamp_offset(int64_t K, int64_t J, int R);

@@ -739,7 +739,7 @@ Stage1Layout stage1_layout(const dp2_store* st, int sp, int R) {
 
 cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* s_dev, int sp, int R,
                        double* A_out, double* M_out, int32_t* rank_out, char* ws, int64_t* status,
-                       float* timing, cudaStream_t stream, double* a_signs) {
+                       float* timing, cudaStream_t stream, double* a_signs, int power_iters) {
   const Stage1Layout L = stage1_layout(st, sp, R);
   double* part = reinterpret_cast<double*>(ws + L.part);
   double* qz = reinterpret_cast<double*>(ws + L.qz);
@@ -758,10 +758,28 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   // uses dp2_slice_stats); the tensor-core pass flags non-finite input from Y
   // (the tensor-core and DMMA passes flag non-finite input from Y instead)
   const bool s64 = (st->dtype == DP2_F64 || sketch_engine() == 2) && sketch64_eligible(st, sp, false, false);
-  cudaError_t e = run_sketch(st, omega, sp, part, nullptr, (sketch_tc_eligible(st, sp) || s64) ? nullptr : xsq,
-                             status, stream);
-  if (e != cudaSuccess) return e;
+  // power iterations (P/linalg.py:124-126): q sketch passes Z = X^T (X B),
+  // each followed by B <- orth(Z) (range-preserving; it also keeps the
+  // iteration well conditioned), then the final pass Y = X B.  q = 0: the
+  // final pass runs on Omega itself (range(X Omega)).
+  const int q = power_iters < 0 ? 0 : power_iters;
+  cudaError_t e = cudaSuccess;
+  if (q > 0) {
+    e = run_sketch(st, omega, sp, part, nullptr, (sketch_tc_eligible(st, sp) || s64) ? nullptr : xsq, status,
+                   stream);
+    if (e != cudaSuccess) return e;
+  }
   if (timing) cudaEventRecord(ev[1], stream);
+  // orth of pass partials -> qz; then the extra power iterations (q > 1)
+  auto orth_and_more = [&](auto&& orth) -> cudaError_t {
+    if (q == 0) return cudaMemcpyAsync(qz, omega, (size_t)K * J * sp * 8, cudaMemcpyDeviceToDevice, stream);
+    cudaError_t eo = orth();
+    for (int it = 1; it < q && eo == cudaSuccess; ++it) {
+      eo = run_sketch(st, qz, sp, part, nullptr, nullptr, status, stream);
+      if (eo == cudaSuccess) eo = orth();
+    }
+    return eo;
+  };
   if (sp <= 32) {
     double* gpart = reinterpret_cast<double*>(ws + L.gpart);
     double* CCg = reinterpret_cast<double*>(ws + L.CCg);
@@ -776,12 +794,12 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
                               reinterpret_cast<int32_t*>(ws + L.cand_neg), A_out, M_out, rank_out, status, phase,
                               stream, tc, gpart, a_signs);
     };
-    if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) {
-      e = small(0);
-      if (e != cudaSuccess) return e;
-    } else {
+    e = orth_and_more([&]() -> cudaError_t {
+      if ((size_t)J * (sp + 1) * 8 <= 200 * 1024) return small(0);
       orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
-    }
+      return cudaGetLastError();
+    });
+    if (e != cudaSuccess) return e;
     if (timing) cudaEventRecord(ev[2], stream);
     // the tensor-core pass stores Y in fp32: its accumulator precision, half the bytes
     e = tc ? run_sketch_tc(st, qz, sp, part, y2, nullptr, status, stream, nullptr, true)
@@ -806,7 +824,11 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
     }
     return e;
   }
-  orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
+  e = orth_and_more([&]() -> cudaError_t {
+    orth_kernel<<<K, 256, 0, stream>>>(part, st->slice_piece, s_dev, J, sp, qz);
+    return cudaGetLastError();
+  });
+  if (e != cudaSuccess) return e;
   if (timing) cudaEventRecord(ev[2], stream);
   e = run_sketch(st, qz, sp, part, y2, nullptr, status, stream);
   if (e != cudaSuccess) return e;

@@ -362,7 +362,8 @@ cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, 
 }
 
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
-                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t st) {
+                       double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t st,
+                       int power_iters) {
   const S2Layout L = s2_layout(J, KR, s2, R);
   double* parts = reinterpret_cast<double*>(ws + L.parts);
   double* Y = reinterpret_cast<double*>(ws + L.Y);
@@ -384,9 +385,21 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
   auto tn = [&](const double* B, double* out) {
     tn_dmma_kernel<<<dim3((unsigned)((KR + 63) / 64), 1, ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, J, out);
   };
-  nn(omega2, Y);
-  tn(Y, Z);
-  nn(Z, Y2);
+  // Y2 = (M M^T)^q M Omega2 (P/linalg.py:124-126; no re-orthonormalisation,
+  // as the reference), ping-ponging between Y and Y2
+  const int q = power_iters < 0 ? 0 : power_iters;
+  if (q == 0) {
+    nn(omega2, Y2);
+  } else {
+    nn(omega2, Y);
+    for (int it = 0; it < q; ++it) {
+      double* src = (it % 2 == 0) ? Y : Y2;
+      double* dst = (it % 2 == 0) ? Y2 : Y;
+      tn(src, Z);
+      nn(Z, dst);
+    }
+    if (q % 2 == 0) cudaMemcpyAsync(Y2, Y, (size_t)J * s2 * 8, cudaMemcpyDeviceToDevice, st);
+  }
   if (!run_orth2(Y2, J, s2, st)) cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
   tn(Y2, C);
   // BB = C^T C (s2 x s2): split over the KR rows of C, ordered reduction

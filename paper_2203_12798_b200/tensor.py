@@ -97,6 +97,10 @@ class IrregularTensor:
     def __init__(self, slices, dtype="f64"):
         if dtype not in _TORCH:
             raise ValueError(f"dtype must be 'f64' or 'f32', got {dtype!r}")
+        # a reference container (P/tensor.py:34-80) passes through the CLI seam
+        # (P/cli.py:45, 113-121): take its slices
+        if not isinstance(slices, (list, tuple)) and hasattr(slices, "slices"):
+            slices = list(slices.slices)
         if len(slices) < 1:
             raise ShapeMismatchError("tensor needs at least one slice")
         cols = None

@@ -64,3 +64,21 @@ def test_stage2_noiseless_rank_deficient_y2():
     from paper_2203_12798_b200 import synth
     cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=60, noise=0.0, rank=6)
     _check(synth.generate(cfg, 1), 6, tol_d=1e-6, tol_e=1e-8)
+
+
+@pytest.mark.parametrize("q", [0, 2, 3])
+def test_compress_power_iters_match_oracle(q):
+    """RsvdParams.power_iters != 1 (P/linalg.py:124-126) through both stages:
+    the stage-1 bases, D, E and F match the oracle's compress(power_iters=q)."""
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c1"], num_slices=30)
+    xs = synth.generate(cfg, 2)
+    comp = dp.compress(dp.IrregularTensor(xs), 10, rsvd=dp.RsvdParams(rank=10, power_iters=q, seed=0))
+    o = orc.compress(xs, 10, seed=0, power_iters=q)
+    A = comp.A.cpu().numpy()
+    Ao = np.concatenate(o.bases)
+    assert rel_signed(A, Ao) <= 1e-6, rel_signed(A, Ao)
+    assert float(np.abs(comp.weights.cpu().numpy() - o.E).max() / o.E.max()) <= 1e-8
+    assert rel_signed(comp.col_basis.cpu().numpy(), o.D) <= 1e-6
