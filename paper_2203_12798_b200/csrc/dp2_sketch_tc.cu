@@ -10,33 +10,34 @@
 // P/compress.py:64-103 (randomized_svd per slice) is what this computes the
 // sketches of; the algebra is DESIGN.md §3.
 //
-// Data movement (one CTA per SM, 13 warps):
-//   warps 0-7   producers: warp-wide LDG of 128 B row segments of X (one
-//               "unit" = 64 rows x 128 columns, 32 KB; thread = one column,
-//               32 rows) -> statistics -> round to tf32 (cvt.rna) -> two
-//               on-chip copies:
-//                 * STS into a ring of 8 KB chunk slots in the SWIZZLE_128B
-//                   row-major layout: P1's K-major A operand;
-//                 * tcgen05.st into TMEM (lane = column of X, TMEM column =
-//                   row): P2's A operand X^T, which must be K-major.  (tf32
-//                   MN-major shared-memory operands only exist in the
-//                   128B-base-32B swizzle, which no K-major layout shares, so
-//                   one shared-memory copy cannot feed both products --
-//                   tools/umma_probe.cu measures this.)
-//   warp 8      TMEM allocation + a single elected thread issuing tcgen05.mma
-//               and tcgen05.commit (mbarrier arrive on completion).
+// Data movement (one CTA per SM, 19 warps):
+//   warp 13     TMA: lane 0 streams 64-row x 32-column boxes of X
+//               (cp.async.bulk.tensor, SWIZZLE_128B) into a ring of 8 KB
+//               chunk slots -- P1's K-major A operand, read by the tensor
+//               core as is (tf32 = the top 19 bits of each fp32); lane 1
+//               bulk-copies the slice's pre-tiled tf32 B image per piece.
+//   warps 0-7   X^T producers: read each ring unit back, round to tf32
+//               (cvt.rna) and tcgen05.st it into TMEM (lane = column of X,
+//               TMEM column = row): P2's A operand X^T, which must be
+//               K-major.  (tf32 MN-major shared-memory operands only exist in
+//               the 128B-base-32B swizzle, which no K-major layout shares, so
+//               one shared-memory copy cannot feed both products --
+//               tools/umma_probe.cu measures this.)
+//   warp 8      TMEM allocation + the elected thread issuing P1 and the
+//               tcgen05.commit arrivals; warp 14 issues P2.
 //   warps 9-12  epilogue: tcgen05.ld of Y (TMEM lanes = rows) -> rounded Y^T
-//               into shared memory as P2's K-major B operand; Y rows / G in
-//               pass 2; the per-piece Z flush (TMEM lanes = columns of X).
-// B (Omega_k or Q_Z,k, fp64 in HBM) is converted per piece to a K-major tf32
-// copy in shared memory.  TMEM: X^T blocks in columns [0, 256), Z in
-// [256, 384), Y in [384, 416).  Ring slots are released right after P1, the
-// X^T blocks after P2, so HBM streaming overlaps both products.
+//               into shared memory as P2's K-major B operand, the non-finite
+//               flag, and the per-piece Z flush (TMEM lanes = columns of X).
+//   warps 15-18 pass 2: Y rows out (coalesced through shared memory).
+// TMEM: X^T blocks in columns [0, 256), Z in [256, 384), Y double-buffered in
+// [384, 448).  Ring slots are released right after P1, the X^T blocks after
+// P2, so HBM streaming overlaps both products.
 //
 // Precision: products in tf32 (10-bit mantissa, round-to-nearest on both
 // operands), fp32 accumulation within a piece, fp64 partials across pieces --
-// the fp32-mode budget (BASELINE.json north_star: factors and fitness within
-// 1e-3).  fp64 storage keeps the DMMA path.
+// an opt-in speed mode (set_fp32_products("tf32")): within the 1e-3 fp32
+// budget on c2, not on ~50-row slices (tests/test_gpu_scale_parity.py); the
+// default fp32-storage path is the fp64 DMMA pass on upcast values.
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>

@@ -66,10 +66,15 @@ def test_stage2_noiseless_rank_deficient_y2():
     _check(synth.generate(cfg, 1), 6, tol_d=1e-6, tol_e=1e-8)
 
 
-@pytest.mark.parametrize("q", [0, 2, 3])
-def test_compress_power_iters_match_oracle(q):
+@pytest.mark.parametrize("q,tol", [(0, 1e-6), (2, 1e-6), (3, 1e-3)])
+def test_compress_power_iters_match_oracle(q, tol):
     """RsvdParams.power_iters != 1 (P/linalg.py:124-126) through both stages:
-    the stage-1 bases, D, E and F match the oracle's compress(power_iters=q)."""
+    the stage-1 bases, D, E and F match the oracle's compress(power_iters=q).
+    The reference forms (X X^T)^q X Omega without re-orthonormalising, so its
+    weakest sketch directions lose accuracy as kappa^(2q+1); ours
+    re-orthonormalises each iteration (the same range in exact arithmetic).
+    At q = 3 the two therefore agree only to the reference's own rounding on
+    the weakest column (~4e-4 measured); q <= 2 to 1e-6."""
     import paper_2203_12798_b200 as dp
     from oracle import dpar2_oracle as orc
     from paper_2203_12798_b200 import synth
@@ -79,6 +84,6 @@ def test_compress_power_iters_match_oracle(q):
     o = orc.compress(xs, 10, seed=0, power_iters=q)
     A = comp.A.cpu().numpy()
     Ao = np.concatenate(o.bases)
-    assert rel_signed(A, Ao) <= 1e-6, rel_signed(A, Ao)
-    assert float(np.abs(comp.weights.cpu().numpy() - o.E).max() / o.E.max()) <= 1e-8
-    assert rel_signed(comp.col_basis.cpu().numpy(), o.D) <= 1e-6
+    assert rel_signed(A, Ao) <= tol, rel_signed(A, Ao)
+    assert float(np.abs(comp.weights.cpu().numpy() - o.E).max() / o.E.max()) <= tol * 1e-2
+    assert rel_signed(comp.col_basis.cpu().numpy(), o.D) <= tol
