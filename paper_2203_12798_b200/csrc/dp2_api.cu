@@ -367,8 +367,9 @@ int dp2_stage2_power(const double* M_dev, int64_t J, int64_t KR, const double* o
   cudaError_t e = dp2::run_stage2(M_dev, J, KR, omega2_dev, s2, rank, D_out, E_out, F_out,
                                   static_cast<char*>(ws), status_dev, S(stream), power_iters);
   // our own DMMA GEMM kernels + ordered reductions + orth + final
-  return e == cudaSuccess ? ok(8 + 3 * power_iters)
-                          : fail(e, "dp2_stage2");
+  // launches: nn (2) per M-product, tn (1, +1 reduction when split), orth, gram (2), final, F
+  const int tn = dp2::gemm_tn_splits(J, KR, s2) > 1 ? 2 : 1;
+  return e == cudaSuccess ? ok(2 + power_iters * (tn + 2) + 1 + tn + 2 + 2) : fail(e, "dp2_stage2");
 }
 
 int dp2_stage2(const double* M_dev, int64_t J, int64_t KR, const double* omega2_dev, int32_t s2, int32_t rank,
@@ -471,7 +472,7 @@ int dp2_fitness(const dp2_store* st, const double* Q, int32_t R, const double* H
 
 int dp2_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int32_t n, double* out, void* stream) {
   if (!A || !B || !out || m < 1 || K < 1 || n < 1) return fail_arg("invalid arguments");
-  cudaError_t e = dp2::run_gemm_tn(A, m, K, B, n, out, S(stream));
+  cudaError_t e = dp2::run_gemm_tn(A, m, K, B, n, out, S(stream), nullptr);
   return e == cudaSuccess ? ok(1) : fail(e, "dp2_gemm_tn");
 }
 

@@ -35,6 +35,7 @@
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -382,18 +383,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
 }
 
 // Fragment-major B images: img[k][g][ks][j][l] = B[k][4 ks + (l & 3)][8 (NT g + j) + (l >> 2)]
-// (0 outside J x sp).
-__global__ void image_kernel(const double* B, int64_t K, int J, int JP, int sp, int NT, int ng, double* img) {
-  const int64_t per = (int64_t)(JP / 4) * NT * 32;
-  const int64_t total = K * ng * per;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int l = (int)(e % 32);
-    const int j = (int)((e / 32) % NT);
-    const int ks = (int)((e / (32 * NT)) % (JP / 4));
-    const int g = (int)((e / per) % ng);
-    const int64_t k = e / (per * ng);
-    const int row = 4 * ks + (l & 3), col = 8 * (NT * g + j) + (l >> 2);
-    img[e] = (row < J && col < sp) ? B[((size_t)k * J + row) * sp + col] : 0.0;
+// (0 outside J x sp).  One warp per (k, g, ks) unit: NT coalesced 256-byte
+// stores, reads of 4 rows x 64 bytes per fragment.
+template <int NT>
+__global__ void __launch_bounds__(256) image_kernel(const double* __restrict__ B, int64_t K, int J, int JP, int sp,
+                                                     int ng, double* __restrict__ img) {
+  const int lane = threadIdx.x & 31;
+  const int nks = JP / 4;
+  const int64_t units = K * ng * nks;
+  const int row_in = lane & 3, col_in = lane >> 2;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < units;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int ks = (int)(u % nks);
+    const int64_t kg = u / nks;
+    const int g = (int)(kg % ng);
+    const int64_t k = kg / ng;
+    const int row = 4 * ks + row_in;
+    const double* src = B + ((size_t)k * J + (row < J ? row : 0)) * sp;
+    double* dst = img + (size_t)u * NT * 32 + lane;
+#pragma unroll
+    for (int jj = 0; jj < NT; ++jj) {
+      const int col = 8 * (NT * g + jj) + col_in;
+      dst[jj * 32] = (row < J && col < sp) ? __ldg(src + col) : 0.0;
+    }
   }
 }
 
@@ -544,7 +556,13 @@ cudaError_t run_sketch64(const dp2_store* st, const double* B, int sp, double* o
   cudaError_t e = cudaSuccess;
   double* img = s64::image_scratch(img_elems * 8, &e);
   if (!img) return e;
-  s64::image_kernel<<<1184, 256, 0, stream>>>(B, st->K, J, pl.JP, sp, pl.NT, pl.ng, img);
+  {
+    const int64_t warps = st->K * pl.ng * (pl.JP / 4);
+    const unsigned blocks = (unsigned)std::min<int64_t>((warps + 7) / 8, 148 * 16);
+    if (pl.NT == 1) s64::image_kernel<1><<<blocks, 256, 0, stream>>>(B, st->K, J, pl.JP, sp, pl.ng, img);
+    else if (pl.NT == 2) s64::image_kernel<2><<<blocks, 256, 0, stream>>>(B, st->K, J, pl.JP, sp, pl.ng, img);
+    else s64::image_kernel<3><<<blocks, 256, 0, stream>>>(B, st->K, J, pl.JP, sp, pl.ng, img);
+  }
   s64::Params prm{};
   prm.X = st->X;
   prm.ldx = st->ldx;

@@ -314,6 +314,10 @@ __global__ void f_kernel(const double* C, int64_t N, int s, const double* Uf, in
   }
 }
 
+int gemm_tn_splits(int64_t m, int64_t K, int n);
+cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out,
+                        cudaStream_t st, double* parts);
+
 namespace {
 // split of the reduction dimension for the split-K products: about two CTAs
 // per SM in total, chunks of >= 256
@@ -337,7 +341,8 @@ S2Layout s2_layout(int64_t J, int64_t KR, int s2, int R) {
   L.ms_g = splits_for(KR, ((s2 + 63) / 64) * ng, sms);
   size_t off = 0;
   auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-  L.parts = take(std::max((size_t)L.ks_nn * J * s2, (size_t)L.ms_g * s2 * s2) * 8);
+  L.parts = take(std::max({(size_t)L.ks_nn * J * s2, (size_t)L.ms_g * s2 * s2,
+                           (size_t)gemm_tn_splits(J, KR, s2) * KR * s2}) * 8);
   L.Y = take(J * s2 * 8);
   L.Z = take(KR * s2 * 8);
   L.Y2 = take(J * s2 * 8);
@@ -353,11 +358,28 @@ S2Layout s2_layout(int64_t J, int64_t KR, int s2, int R) {
 size_t stage2_bytes(int64_t J, int64_t KR, int s2, int R) { return s2_layout(J, KR, s2, R).total; }
 
 // out (K x n) = A^T B for row-major A (m x K) and B (m x n): the tall-skinny
-// DMMA product of stage 2, exported for the fit's V^T M (zero-pass fitness)
+// DMMA product of stage 2 (also the fit's M^T V for the zero-pass fitness).
+// The reduction over m is split so that ~4 CTAs per SM keep enough loads of A
+// in flight; the splits' partials (in ``parts``, >= ms K n doubles, or written
+// straight to ``out`` when ms = 1) are summed in order.
+int gemm_tn_splits(int64_t m, int64_t K, int n) {
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ctas = ((K + 63) / 64) * ((n + 23) / 24);
+  const int64_t want = (4 * (int64_t)sms + ctas - 1) / ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (m + 63) / 64));
+}
+
 cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out,
-                        cudaStream_t st) {
-  tn_dmma_kernel<<<dim3((unsigned)((K + 63) / 64), 1, (unsigned)((n + 23) / 24)), 256, 0, st>>>(A, K, m, K, B, n, n,
-                                                                                                 m, out);
+                        cudaStream_t st, double* parts) {
+  const int ms = parts ? gemm_tn_splits(m, K, n) : 1;
+  const int64_t mc = ((m + ms - 1) / ms + 3) / 4 * 4;
+  const int msr = (int)((m + mc - 1) / mc);
+  tn_dmma_kernel<<<dim3((unsigned)((K + 63) / 64), msr, (unsigned)((n + 23) / 24)), 256, 0, st>>>(
+      A, K, m, K, B, n, n, mc, msr == 1 ? out : parts);
+  if (msr > 1)
+    reduce_parts_kernel<<<(unsigned)std::min<int64_t>((K * n + 255) / 256, 4096), 256, 0, st>>>(parts, msr, K * n,
+                                                                                                  out);
   return cudaGetLastError();
 }
 
@@ -381,10 +403,9 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
     nn_dmma_kernel<<<dim3((unsigned)((J + 63) / 64), ks, ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, kc, parts);
     reduce_parts_kernel<<<(unsigned)((J * s2 + 255) / 256), 256, 0, st>>>(parts, ks, J * s2, out);
   };
-  // out (KR x s2) = M^T B (B: J x s2): one split, written in place
-  auto tn = [&](const double* B, double* out) {
-    tn_dmma_kernel<<<dim3((unsigned)((KR + 63) / 64), 1, ng), 256, 0, st>>>(M, KR, J, KR, B, s2, s2, J, out);
-  };
+  // out (KR x s2) = M^T B (B: J x s2): split over J so that ~4 CTAs per SM
+  // stream M (a latency-bound read otherwise), ordered reduction
+  auto tn = [&](const double* B, double* out) { run_gemm_tn(M, J, KR, B, s2, out, st, parts); };
   // Y2 = (M M^T)^q M Omega2 (P/linalg.py:124-126; no re-orthonormalisation,
   // as the reference), ping-ponging between Y and Y2
   const int q = power_iters < 0 ? 0 : power_iters;
