@@ -57,7 +57,8 @@ constexpr int NTHREADS = 32 * NWARPS;
 struct Params {
   const void* X;
   int64_t ldx;
-  int J, JP, L, sp, ns, rowbytes;
+  int J, JP, L, sp, ns;
+  int rowbytes[2];          // bytes of each row copied by CTA 0 / 1 of the pair (its columns)
   const double* img;        // K x ng x (JP/4) x NT x 32 fragment-major B images
   const int32_t* piece_slice;
   const int64_t* piece_row0;
@@ -111,6 +112,46 @@ DP2_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t b
                : "memory");
 }
 
+// ---- cluster (CTA pair) primitives: the partner's shared memory (DSMEM)
+DP2_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+DP2_DEV uint32_t mapa(uint32_t local_addr, uint32_t rank) {  // same smem variable in CTA ``rank``
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+DP2_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+DP2_DEV bool mbar_try_cluster(uint32_t bar, uint32_t parity) {  // acquire at cluster scope
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+DP2_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  if (mbar_try_cluster(bar, parity)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try_cluster(bar, parity)) return;
+    if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
+  }
+}
+DP2_DEV void st_cluster_v2(uint32_t cluster_addr, double a, double b) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(cluster_addr), "d"(a), "d"(b) : "memory");
+}
+DP2_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // wait with cycle accounting into dacc[k] when DBG (DP2_S64_DEBUG=1)
 #define S64_WAIT(barexpr, par, k)                        \
   do {                                                   \
@@ -122,23 +163,43 @@ DP2_DEV void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t b
       mbar_wait(barexpr, par);                           \
     }                                                    \
   } while (0)
+#define S64_WAIT_CL(barexpr, par, k)                     \
+  do {                                                   \
+    if (DBG) {                                           \
+      const long long t0_ = clock64();                   \
+      mbar_wait_cluster(barexpr, par);                   \
+      dacc[k] += (unsigned long long)(clock64() - t0_);  \
+    } else {                                             \
+      mbar_wait_cluster(barexpr, par);                   \
+    }                                                    \
+  } while (0)
 enum { D_XFULL = 0, D_XEMPTY, D_OFULL, D_OEMPTY, D_YPFULL, D_YPEMPTY, D_YFULL, D_YEMPTY, D_TOTAL, D_N = 10 };
 
 // barrier slots
-enum { B_XFULL = 0, B_XEMPTY = 4, B_OFULL = 8, B_OEMPTY = 12, B_YPFULL = 16, B_YPEMPTY = 18, B_YFULL = 20,
-       B_YEMPTY = 22, B_COUNT = 24 };
+constexpr int MAXS = 12;  // X ring stages
+enum { B_XFULL = 0, B_XEMPTY = MAXS, B_OFULL = 2 * MAXS, B_OEMPTY = 2 * MAXS + NA, B_YPFULL = 2 * MAXS + 2 * NA,
+       B_YPEMPTY = B_YPFULL + NY, B_YFULL = B_YPEMPTY + NY, B_YEMPTY = B_YFULL + NY, B_COUNT = B_YEMPTY + NY };
 
-template <typename T, int NT, bool DBG>
+// CL = 2: a CTA pair (thread-block cluster) shares each segment, CTA c
+// handling columns [c JH, (c + 1) JH) of J (JH = JP / 2): half the B image and
+// half-width X stages per CTA -- so about three times the ring depth -- with
+// the four local Y partials of each tile exchanged through DSMEM (each CTA's
+// aux sums all eight in the same global order, so both hold the identical
+// Y_t for their B warps).
+template <typename T, int NT, int CL, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   constexpr int SG = 8 * NT;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seg = blockIdx.x, grp = blockIdx.y, ng = gridDim.y;
+  const int crank = CL == 2 ? (int)cluster_rank() : 0;
+  const int seg = blockIdx.x / CL, grp = blockIdx.y, ng = gridDim.y;
   const int J = prm.J, JP = prm.JP, L = prm.L, sp = prm.sp, NS = prm.ns;
+  const int JH = JP / CL;            // columns of J owned by this CTA
+  const int jofs = crank * JH;       // its first column
   const int col0 = grp * SG;
   T* xs = reinterpret_cast<T*>(smem);                                  // [NS][TM][L]
-  double* img = reinterpret_cast<double*>(smem + prm.off_img);          // [JP/4][NT][32]
-  double* ypart = reinterpret_cast<double*>(smem + prm.off_yp);         // [NY][NA][TM][SG]
+  double* img = reinterpret_cast<double*>(smem + prm.off_img);          // [JH/4][NT][32]
+  double* ypart = reinterpret_cast<double*>(smem + prm.off_yp);         // [NY][CL NA][TM][SG]
   double* yfin = reinterpret_cast<double*>(smem + prm.off_yf);          // [NY][2][NT][32]
   const uint32_t bar0 = su32(smem + prm.off_bar);
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
@@ -146,15 +207,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   // zero the X ring (pad columns are never written; stale rows must be finite)
   for (int i = threadIdx.x; i < NS * TM * L; i += NTHREADS) xs[i] = T(0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(bar(B_XFULL + s), 1);
       mbar_init(bar(B_XEMPTY + s), NA + NB);
-      mbar_init(bar(B_OFULL + s), 1);
-      mbar_init(bar(B_OEMPTY + s), 1);
+    }
+    for (int a = 0; a < NA; ++a) {
+      mbar_init(bar(B_OFULL + a), 1);
+      mbar_init(bar(B_OEMPTY + a), 1);
     }
     for (int b = 0; b < NY; ++b) {
-      mbar_init(bar(B_YPFULL + b), NA);
-      mbar_init(bar(B_YPEMPTY + b), 1);
+      mbar_init(bar(B_YPFULL + b), CL * NA);  // both CTAs' A warps
+      mbar_init(bar(B_YPEMPTY + b), CL);      // both CTAs' aux warps read this CTA's partials
       mbar_init(bar(B_YFULL + b), 1);
       mbar_init(bar(B_YEMPTY + b), NB);
     }
@@ -162,10 +225,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
+  if constexpr (CL == 2) cluster_sync();  // the partner's barriers exist before any remote arrival
+  const uint32_t peer = crank ^ 1;
 
   const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
-  if (pbeg >= pend) return;
-  const int ksq = JP / 16;  // k-steps per A warp (a quarter of J)
+  const int ksq = JH / (4 * NA);  // k-steps per A warp (its share of this CTA's columns)
   unsigned long long dacc[DBG ? D_N : 1] = {};
   const long long tstart = DBG ? clock64() : 0;
 
@@ -179,23 +243,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       const int64_t row0 = prm.piece_row0[p];
       const int pi = p - pbeg;
       // B image of this slice, quarter by quarter as each A warp frees it
-      const double* src = prm.img + ((size_t)ks * ng + grp) * (size_t)(JP / 4) * NT * 32;
+      const double* src = prm.img + ((size_t)ks * ng + grp) * (size_t)(JP / 4) * NT * 32 +
+                          (size_t)crank * (JH / 4) * NT * 32;
       if (lane < NA) {
         if (pi > 0) S64_WAIT(bar(B_OEMPTY + lane), (pi - 1) & 1, D_OEMPTY);
         mbar_expect_tx(bar(B_OFULL + lane), qbytes);
         bulk_load(su32(img) + (uint32_t)lane * qbytes, src + (size_t)lane * ksq * NT * 32, qbytes,
                   bar(B_OFULL + lane));
       }
+      const int rowbytes = prm.rowbytes[crank];
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int s = rs;
         const int valid = min(TM, rows - t * TM);
         if (n >= NS) S64_WAIT(bar(B_XEMPTY + s), rph ^ 1, D_XEMPTY);
         if (++rs == NS) { rs = 0; rph ^= 1; }
-        if (lane == 0) mbar_expect_tx(bar(B_XFULL + s), (uint32_t)(valid * prm.rowbytes));
+        if (lane == 0) mbar_expect_tx(bar(B_XFULL + s), (uint32_t)(valid * rowbytes));
         __syncwarp();
-        if (lane < valid)
+        if (lane < valid && rowbytes > 0)
           bulk_load(su32(xs + ((size_t)s * TM + lane) * L),
-                    Xb + (size_t)(row0 + (int64_t)t * TM + lane) * prm.ldx * sizeof(T), (uint32_t)prm.rowbytes,
+                    Xb + ((size_t)(row0 + (int64_t)t * TM + lane) * prm.ldx + jofs) * sizeof(T), (uint32_t)rowbytes,
                     bar(B_XFULL + s));
       }
     }
@@ -213,7 +279,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         const int s = rs, b = n % NY;
         S64_WAIT(bar(B_XFULL + s), rph, D_XFULL);
         if (++rs == NS) { rs = 0; rph ^= 1; }
-        const T* xr = xs + ((size_t)s * TM + r) * L + a * (JP / 4) + q;
+        const T* xr = xs + ((size_t)s * TM + r) * L + a * (JH / NA) + q;
         double c0[NT][2], c1[NT][2];
 #pragma unroll
         for (int j = 0; j < NT; ++j) c0[j][0] = c0[j][1] = c1[j][0] = c1[j][1] = 0.0;
@@ -228,22 +294,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         }
         // partial -> ypart[b][a] (C fragment: row r, cols 8j + 2q, +1)
         if (n >= NY) S64_WAIT(bar(B_YPEMPTY + b), ((n / NY) - 1) & 1, D_YPEMPTY);
-        double* yp = ypart + (((size_t)b * NA + a) * TM + r) * SG + 2 * q;
+        // slot crank NA + a of the pair-wide partial ring, written into both
+        // CTAs' copies (the partner's through DSMEM)
+        double* yp = ypart + (((size_t)b * CL * NA + crank * NA + a) * TM + r) * SG + 2 * q;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
           double2 v;
           v.x = c0[j][0] + c1[j][0];
           v.y = c0[j][1] + c1[j][1];
           *reinterpret_cast<double2*>(yp + 8 * j) = v;
+          if constexpr (CL == 2) st_cluster_v2(mapa(su32(yp + 8 * j), peer), v.x, v.y);
         }
         warp_arrive(bar(B_YPFULL + b));
+        if constexpr (CL == 2) {  // the partner's aux sums this CTA's partials too
+          if (lane == 0) mbar_arrive_cluster(mapa(bar(B_YPFULL + b), peer));
+        }
         warp_arrive(bar(B_XEMPTY + s));
       }
       warp_arrive(bar(B_OEMPTY + a));
     }
   } else if (warp == WARP_AUX) {
     // ------------------------------------------------------------ aux: Y_t, Y rows, G, non-finite
-    const bool do_g = prm.g_part != nullptr;
+    const bool do_g = prm.g_part != nullptr && crank == 0;  // one CTA of the pair writes G
     double g[NT][NT][2];
 #pragma unroll
     for (int i = 0; i < NT; ++i)
@@ -257,21 +329,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       for (int t = 0; t * TM < rows; ++t, ++n) {
         const int b = n % NY;
         const int valid = min(TM, rows - t * TM);
-        S64_WAIT(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
+        if constexpr (CL == 2) S64_WAIT_CL(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
+        else S64_WAIT(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
         if (n >= NY) S64_WAIT(bar(B_YEMPTY + b), ((n / NY) - 1) & 1, D_YEMPTY);
         // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
         //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
         double* yf = yfin + (size_t)b * 2 * NT * 32;
-        const double* ypb = ypart + (size_t)b * NA * TM * SG;
+        const double* ypb = ypart + (size_t)b * CL * NA * TM * SG;
         double fr[2][NT];
 #pragma unroll
         for (int k2 = 0; k2 < 2; ++k2)
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
-            double v = 0.0;
+            double v = 0.0;  // slots in pair order (CTA 0's partials, then CTA 1's): same sum in both CTAs
 #pragma unroll
-            for (int aa = 0; aa < NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
+            for (int aa = 0; aa < CL * NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
             v = row < valid ? v : 0.0;
             bad |= !isfinite(v);
             fr[k2][j] = v;
@@ -279,7 +352,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
           }
         warp_arrive(bar(B_YFULL + b));
         warp_arrive(bar(B_YPEMPTY + b));
-        if (prm.y_out != nullptr) {
+        if constexpr (CL == 2) {
+          if (lane == 0) mbar_arrive_cluster(mapa(bar(B_YPEMPTY + b), peer));
+        }
+        if (prm.y_out != nullptr && crank == 0) {
 #pragma unroll
           for (int k2 = 0; k2 < 2; ++k2)
 #pragma unroll
@@ -316,7 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   } else {
     // ------------------------------------------------------------ B warps: Z += X_t^T Y_t
     const int bw = warp - WARP_B0;
-    const int MB = JP / (8 * NB);  // J-blocks of 8 per B warp (<= MBMAX)
+    const int MB = JH / (8 * NB);  // J-blocks of 8 per B warp (<= MBMAX)
     const int jb0 = bw * MB;
     double z[MBMAX][NT][2];
 #pragma unroll
@@ -355,7 +431,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
 #pragma unroll
       for (int i = 0; i < MBMAX; ++i) {
         if (i < MB) {
-          const int m = 8 * (jb0 + i) + (lane >> 2);
+          const int m = jofs + 8 * (jb0 + i) + (lane >> 2);
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const int c = col0 + 8 * j + 2 * (lane & 3);
@@ -375,6 +451,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       }
     }
   }
+  if constexpr (CL == 2) cluster_sync();  // the partner may still read this CTA's partials / barriers
   if (DBG && lane == 0) {
     dacc[D_TOTAL] = (unsigned long long)(clock64() - tstart);
     unsigned long long* d = prm.dbg + ((size_t)(blockIdx.y * gridDim.x + blockIdx.x) * NWARPS + warp) * D_N;
@@ -409,8 +486,20 @@ __global__ void __launch_bounds__(256) image_kernel(const double* __restrict__ B
   }
 }
 
+// CTA pairs split J when DP2_S64_PAIRS=1 and that costs at most ~15% column
+// padding.  Off by default: measured at c2 fp64 the pair version (9 ring
+// stages of half-width X, partials exchanged by DSMEM stores) ran 8.3 / 8.8 ms
+// per pass against 4.2 / 4.4 ms for single CTAs -- with half of J per CTA the
+// 8-row tile carries too little DMMA work per hand-off (A warps 48, B warps
+// 12 per tile) to amortise the per-tile barrier and fragment-load overhead.
+bool uses_pairs(int J) {
+  static const bool on = getenv("DP2_S64_PAIRS") && atoi(getenv("DP2_S64_PAIRS")) != 0;
+  const int JP2 = (J + 16 * NB - 1) / (16 * NB) * (16 * NB);
+  return on && J >= 256 && J <= 512 && JP2 * 100 <= J * 115;
+}
+
 struct Plan {
-  int NT, ng, JP, L, ns;
+  int NT, ng, JP, L, ns, CL;
   size_t smem;
   uint32_t off_img, off_yp, off_yf, off_bar;
 };
@@ -420,21 +509,24 @@ bool plan(int J, int sp, int elem, Plan* pl) {
   const int nbt = sp / 8;
   const int NT = nbt <= 3 ? nbt : 3;  // groups of <= 3 column blocks (last one zero padded)
   const int ng = (nbt + NT - 1) / NT;
-  const int JP = (J + 8 * NB - 1) / (8 * NB) * (8 * NB);
-  int L = JP + (elem == 8 ? 4 : 4);  // elements: 8 B -> L % 16 == 4; 4 B -> L % 32 == 4
+  const int CL = uses_pairs(J) ? 2 : 1;
+  const int JP = CL == 2 ? (J + 16 * NB - 1) / (16 * NB) * (16 * NB) : (J + 8 * NB - 1) / (8 * NB) * (8 * NB);
+  const int JH = JP / CL;
+  int L = JH + 4;  // elements: 8 B -> L % 16 == 4; 4 B -> L % 32 == 4
   if (elem == 8) {
     while (L % 16 != 4) ++L;
   } else {
     while (L % 32 != 4) ++L;
   }
   const int SG = 8 * NT;
-  const size_t img = (size_t)(JP / 4) * NT * 32 * 8;
-  const size_t yp = (size_t)NY * NA * TM * SG * 8, yf = (size_t)NY * 2 * NT * 32 * 8;
+  const size_t img = (size_t)(JH / 4) * NT * 32 * 8;
+  const size_t yp = (size_t)NY * CL * NA * TM * SG * 8, yf = (size_t)NY * 2 * NT * 32 * 8;
   const size_t stage = (size_t)TM * L * elem;
   const size_t cap = 227 * 1024;
-  int ns = 4;
+  int ns = MAXS;
   while (ns >= 2 && ns * stage + img + yp + yf + 8 * B_COUNT + 256 > cap) --ns;
   if (ns < 2) return false;
+  pl->CL = CL;
   pl->NT = NT;
   pl->ng = ng;
   pl->JP = JP;
@@ -475,13 +567,33 @@ double* image_scratch(size_t bytes, cudaError_t* err) {
   return buf[dev];
 }
 
-template <typename T, int NT>
-cudaError_t launch(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
-  auto kern = prm.dbg ? sketch64_kernel<T, NT, true> : sketch64_kernel<T, NT, false>;
+template <typename T, int NT, int CL>
+cudaError_t launch_cl(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
+  auto kern = prm.dbg ? sketch64_kernel<T, NT, CL, true> : sketch64_kernel<T, NT, CL, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(nseg, pl.ng), NTHREADS, pl.smem, st>>>(prm);
-  return cudaGetLastError();
+  if (CL == 1) {
+    kern<<<dim3(nseg, pl.ng), NTHREADS, pl.smem, st>>>(prm);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL * nseg, pl.ng);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, prm);
+}
+
+template <typename T, int NT>
+cudaError_t launch(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
+  return pl.CL == 2 ? launch_cl<T, NT, 2>(prm, pl, nseg, st) : launch_cl<T, NT, 1>(prm, pl, nseg, st);
 }
 
 cudaError_t launch_any(int elem, int NT, const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
@@ -502,7 +614,7 @@ cudaError_t launch_any(int elem, int NT, const Params& prm, const Plan& pl, int 
 // DP2_S64_DEBUG: run with per-warp wait accounting and print the share of
 // cycles each role spends waiting on each barrier class (debug aid; syncs)
 cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg, cudaStream_t stream) {
-  const size_t nd = (size_t)nseg * pl.ng * NWARPS * D_N;
+  const size_t nd = (size_t)nseg * pl.CL * pl.ng * NWARPS * D_N;
   unsigned long long *dh = nullptr, *dd = nullptr;
   cudaError_t e = cudaHostAlloc(&dh, nd * 8, cudaHostAllocMapped);
   if (e != cudaSuccess) return e;
@@ -516,7 +628,7 @@ cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg,
   for (int role = 0; role < 4; ++role) {
     double acc[D_N] = {};
     int cnt = 0;
-    for (size_t c = 0; c < (size_t)nseg * pl.ng; ++c)
+    for (size_t c = 0; c < (size_t)nseg * pl.CL * pl.ng; ++c)
       for (int w = 0; w < NWARPS; ++w) {
         const int r = (w >= WARP_A0 && w < WARP_A0 + NA) ? 0 : (w >= WARP_B0 && w < WARP_B0 + NB) ? 1
                       : w == WARP_PROD ? 2 : 3;
@@ -534,6 +646,8 @@ cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg,
 }
 
 }  // namespace s64
+
+bool sketch64_pairs(int64_t J) { return s64::uses_pairs((int)J); }
 
 bool sketch64_eligible(const dp2_store* st, int sp, bool xsq, bool gram) {
   if (xsq) return false;  // the per-piece sums of squares live in the older passes
@@ -571,7 +685,13 @@ cudaError_t run_sketch64(const dp2_store* st, const double* B, int sp, double* o
   prm.L = pl.L;
   prm.sp = sp;
   prm.ns = pl.ns;
-  prm.rowbytes = (J * elem + 15) / 16 * 16;
+  {  // each CTA of a pair copies its own columns of every row
+    const int JH = pl.JP / pl.CL;
+    for (int c = 0; c < 2; ++c) {
+      const int cols = c < pl.CL ? std::max(0, std::min(JH, J - c * JH)) : 0;
+      prm.rowbytes[c] = (cols * elem + 15) / 16 * 16;
+    }
+  }
   prm.img = img;
   prm.piece_slice = st->piece_slice;
   prm.piece_row0 = st->piece_row0;

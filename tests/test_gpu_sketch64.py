@@ -106,3 +106,17 @@ def test_sketch64_flags_lowest_nonfinite_slice(dtype):
         slices = [s.astype(np.float32) for s in slices]
     *_, res = run_pass(slices, 128, 24, 3, dtype)
     assert res["status"][0] == 2
+
+
+def test_sketch64_cta_pairs_match_numpy():
+    """The CTA-pair (thread-block cluster) variant of the pass, DP2_S64_PAIRS=1:
+    each CTA of a pair owns half of J, the Y partials cross over DSMEM.  Run in
+    a subprocess (the switch is read once per process)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_gpu_sketch64 as T; "
+            "[T.test_sketch64_matches_numpy(d, c) for d in ('f64', 'f32') for c in (1, 4, 6)]; "
+            "T.test_sketch64_flags_lowest_nonfinite_slice('f64')")
+    env = dict(__import__("os").environ, DP2_S64_PAIRS="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
