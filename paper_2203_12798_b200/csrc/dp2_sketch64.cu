@@ -43,7 +43,7 @@
 namespace dp2 {
 namespace s64 {
 
-constexpr int TM = 8;           // rows per tile (one DMMA row block)
+constexpr int TMAX = 16;        // rows per tile: TM = 8 (J > 256 per CTA), 16 (J <= 256)
 constexpr int NA = 4;           // warps computing Y partials (split of J)
 constexpr int NB = 16;          // warps accumulating Z (split of J)
 constexpr int MBMAX = 4;        // J-blocks of 8 per B warp (J <= 512)
@@ -186,9 +186,12 @@ enum { B_XFULL = 0, B_XEMPTY = MAXS, B_OFULL = 2 * MAXS, B_OEMPTY = 2 * MAXS + N
 // the four local Y partials of each tile exchanged through DSMEM (each CTA's
 // aux sums all eight in the same global order, so both hold the identical
 // Y_t for their B warps).
-template <typename T, int NT, int CL, bool DBG>
+template <typename T, int NT, int CL, int TM, bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   constexpr int SG = 8 * NT;
+  constexpr int RB = TM / 8;            // DMMA row blocks per tile (A warps)
+  constexpr int K2 = TM / 4;            // k-steps of 4 rows per tile (B warps, G)
+  constexpr int SETS = RB == 1 ? 2 : 1; // independent accumulator sets in the A loop
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int crank = CL == 2 ? (int)cluster_rank() : 0;
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   T* xs = reinterpret_cast<T*>(smem);                                  // [NS][TM][L]
   double* img = reinterpret_cast<double*>(smem + prm.off_img);          // [JH/4][NT][32]
   double* ypart = reinterpret_cast<double*>(smem + prm.off_yp);         // [NY][CL NA][TM][SG]
-  double* yfin = reinterpret_cast<double*>(smem + prm.off_yf);          // [NY][2][NT][32]
+  double* yfin = reinterpret_cast<double*>(smem + prm.off_yf);          // [NY][K2][NT][32]
   const uint32_t bar0 = su32(smem + prm.off_bar);
   auto bar = [&](int i) { return bar0 + 8u * (uint32_t)i; };
 
@@ -280,16 +283,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         S64_WAIT(bar(B_XFULL + s), rph, D_XFULL);
         if (++rs == NS) { rs = 0; rph ^= 1; }
         const T* xr = xs + ((size_t)s * TM + r) * L + a * (JH / NA) + q;
-        double c0[NT][2], c1[NT][2];
+        double c[SETS][RB][NT][2];
 #pragma unroll
-        for (int j = 0; j < NT; ++j) c0[j][0] = c0[j][1] = c1[j][0] = c1[j][1] = 0.0;
+        for (int u = 0; u < SETS; ++u)
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) c[u][rb][j][0] = c[u][rb][j][1] = 0.0;
 #pragma unroll 4
-        for (int k = 0; k < ksq; k += 2) {
-          const double x0 = (double)xr[4 * k], x1 = (double)xr[4 * k + 4];
+        for (int k = 0; k < ksq; k += SETS) {
 #pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            dmma_8x8x4(c0[j][0], c0[j][1], x0, im[(k * NT + j) * 32]);
-            dmma_8x8x4(c1[j][0], c1[j][1], x1, im[((k + 1) * NT + j) * 32]);
+          for (int u = 0; u < SETS; ++u) {
+            double x[RB];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) x[rb] = (double)xr[(size_t)8 * rb * L + 4 * (k + u)];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              const double o = im[((k + u) * NT + j) * 32];
+#pragma unroll
+              for (int rb = 0; rb < RB; ++rb) dmma_8x8x4(c[u][rb][j][0], c[u][rb][j][1], x[rb], o);
+            }
           }
         }
         // partial -> ypart[b][a] (C fragment: row r, cols 8j + 2q, +1)
@@ -298,13 +311,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         // CTAs' copies (the partner's through DSMEM)
         double* yp = ypart + (((size_t)b * CL * NA + crank * NA + a) * TM + r) * SG + 2 * q;
 #pragma unroll
-        for (int j = 0; j < NT; ++j) {
-          double2 v;
-          v.x = c0[j][0] + c1[j][0];
-          v.y = c0[j][1] + c1[j][1];
-          *reinterpret_cast<double2*>(yp + 8 * j) = v;
-          if constexpr (CL == 2) st_cluster_v2(mapa(su32(yp + 8 * j), peer), v.x, v.y);
-        }
+        for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            double2 v;
+            v.x = SETS == 2 ? c[0][rb][j][0] + c[SETS - 1][rb][j][0] : c[0][rb][j][0];
+            v.y = SETS == 2 ? c[0][rb][j][1] + c[SETS - 1][rb][j][1] : c[0][rb][j][1];
+            double* dst = yp + (size_t)8 * rb * SG + 8 * j;
+            *reinterpret_cast<double2*>(dst) = v;
+            if constexpr (CL == 2) st_cluster_v2(mapa(su32(dst), peer), v.x, v.y);
+          }
         warp_arrive(bar(B_YPFULL + b));
         if constexpr (CL == 2) {  // the partner's aux sums this CTA's partials too
           if (lane == 0) mbar_arrive_cluster(mapa(bar(B_YPFULL + b), peer));
@@ -334,11 +350,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         if (n >= NY) S64_WAIT(bar(B_YEMPTY + b), ((n / NY) - 1) & 1, D_YEMPTY);
         // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
         //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
-        double* yf = yfin + (size_t)b * 2 * NT * 32;
+        double* yf = yfin + (size_t)b * K2 * NT * 32;
         const double* ypb = ypart + (size_t)b * CL * NA * TM * SG;
-        double fr[2][NT];
+        double fr[K2][NT];
 #pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2)
+        for (int k2 = 0; k2 < K2; ++k2)
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
@@ -357,7 +373,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         }
         if (prm.y_out != nullptr && crank == 0) {
 #pragma unroll
-          for (int k2 = 0; k2 < 2; ++k2)
+          for (int k2 = 0; k2 < K2; ++k2)
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
               const int row = 4 * k2 + (lane & 3), col = col0 + 8 * j + (lane >> 2);
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         }
         if (do_g) {
 #pragma unroll
-          for (int k2 = 0; k2 < 2; ++k2)
+          for (int k2 = 0; k2 < K2; ++k2)
 #pragma unroll
             for (int i = 0; i < NT; ++i)
 #pragma unroll
@@ -407,10 +423,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         S64_WAIT(bar(B_XFULL + s), rph, D_XFULL);
         if (++rs == NS) { rs = 0; rph ^= 1; }
         S64_WAIT(bar(B_YFULL + b), (n / NY) & 1, D_YFULL);
-        const double* yf = yfin + (size_t)b * 2 * NT * 32 + lane;
+        const double* yf = yfin + (size_t)b * K2 * NT * 32 + lane;
         const T* xb = xs + ((size_t)s * TM + (lane & 3)) * L + 8 * jb0 + (lane >> 2);
 #pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) {
+        for (int k2 = 0; k2 < K2; ++k2) {
           double yv[NT];
 #pragma unroll
           for (int j = 0; j < NT; ++j) yv[j] = yf[(k2 * NT + j) * 32];
@@ -499,7 +515,7 @@ bool uses_pairs(int J) {
 }
 
 struct Plan {
-  int NT, ng, JP, L, ns, CL;
+  int NT, ng, JP, L, ns, CL, TM;
   size_t smem;
   uint32_t off_img, off_yp, off_yf, off_bar;
 };
@@ -512,6 +528,8 @@ bool plan(int J, int sp, int elem, Plan* pl) {
   const int CL = uses_pairs(J) ? 2 : 1;
   const int JP = CL == 2 ? (J + 16 * NB - 1) / (16 * NB) * (16 * NB) : (J + 8 * NB - 1) / (8 * NB) * (8 * NB);
   const int JH = JP / CL;
+  // tile height: keep ~96 DMMAs per A warp and ~24 per B warp per tile as J shrinks
+  const int TM = JH > 256 ? 8 : 16;  // (32-row tiles at J <= 128 spill: the aux's Y_t fragments)
   int L = JH + 4;  // elements: 8 B -> L % 16 == 4; 4 B -> L % 32 == 4
   if (elem == 8) {
     while (L % 16 != 4) ++L;
@@ -520,13 +538,14 @@ bool plan(int J, int sp, int elem, Plan* pl) {
   }
   const int SG = 8 * NT;
   const size_t img = (size_t)(JH / 4) * NT * 32 * 8;
-  const size_t yp = (size_t)NY * CL * NA * TM * SG * 8, yf = (size_t)NY * 2 * NT * 32 * 8;
+  const size_t yp = (size_t)NY * CL * NA * TM * SG * 8, yf = (size_t)NY * (TM / 4) * NT * 32 * 8;
   const size_t stage = (size_t)TM * L * elem;
   const size_t cap = 227 * 1024;
   int ns = MAXS;
   while (ns >= 2 && ns * stage + img + yp + yf + 8 * B_COUNT + 256 > cap) --ns;
   if (ns < 2) return false;
   pl->CL = CL;
+  pl->TM = TM;
   pl->NT = NT;
   pl->ng = ng;
   pl->JP = JP;
@@ -567,9 +586,9 @@ double* image_scratch(size_t bytes, cudaError_t* err) {
   return buf[dev];
 }
 
-template <typename T, int NT, int CL>
+template <typename T, int NT, int CL, int TM>
 cudaError_t launch_cl(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
-  auto kern = prm.dbg ? sketch64_kernel<T, NT, CL, true> : sketch64_kernel<T, NT, CL, false>;
+  auto kern = prm.dbg ? sketch64_kernel<T, NT, CL, TM, true> : sketch64_kernel<T, NT, CL, TM, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   if (CL == 1) {
@@ -591,9 +610,14 @@ cudaError_t launch_cl(const Params& prm, const Plan& pl, int nseg, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
+template <typename T, int NT, int CL>
+cudaError_t launch_tm(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
+  return pl.TM == 8 ? launch_cl<T, NT, CL, 8>(prm, pl, nseg, st) : launch_cl<T, NT, CL, 16>(prm, pl, nseg, st);
+}
+
 template <typename T, int NT>
 cudaError_t launch(const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {
-  return pl.CL == 2 ? launch_cl<T, NT, 2>(prm, pl, nseg, st) : launch_cl<T, NT, 1>(prm, pl, nseg, st);
+  return pl.CL == 2 ? launch_tm<T, NT, 2>(prm, pl, nseg, st) : launch_tm<T, NT, 1>(prm, pl, nseg, st);
 }
 
 cudaError_t launch_any(int elem, int NT, const Params& prm, const Plan& pl, int nseg, cudaStream_t st) {

@@ -467,13 +467,37 @@ struct RowsParams {
   double* A;            // total_rows x R
 };
 
+// Rows of A = Y P for the large-sketch path (sp > 32), 16 columns at a time:
+// P (s x R) staged in shared memory, one row per thread, the y row read once
+// per column group, accumulation in a ascending (the same order in the
+// candidate pass and in the final write, so the stored A and the sign rule
+// see the same numbers).
+struct ACols {
+  double acc[16];
+};
+DP2_DEV void a_row_cols(const double* __restrict__ y, int s, const double* Ps, int R, int c0, int cw, ACols& o) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) o.acc[c] = 0.0;
+  for (int a = 0; a < s; ++a) {
+    const double ya = __ldg(y + a);
+    const double* pr = Ps + a * R + c0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c < cw) o.acc[c] = fma(ya, pr[c], o.acc[c]);
+  }
+}
+
+// Per-piece argmax candidates of |A[:, c]| (first row on ties).
 __global__ void __launch_bounds__(256) argmax_kernel(RowsParams prm) {
-  const int p = blockIdx.x, tid = threadIdx.x, R = prm.R, sp = prm.sp;
+  extern __shared__ __align__(16) double Ps[];  // s x R
+  __shared__ double wabs[8][16];
+  __shared__ int64_t wrow[8][16];
+  __shared__ int wneg[8][16];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, R = prm.R, sp = prm.sp;
   const int k = prm.piece_slice[p], s = prm.s_k[k];
-  __shared__ double babs[256];
-  __shared__ int64_t brow[256];
-  __shared__ int bneg[256];
   const double* Pk = prm.Pm + (size_t)k * sp * R;
+  for (int i = tid; i < s * R; i += blockDim.x) Ps[i] = Pk[i];
+  __syncthreads();
   const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
   const int64_t base = prm.row_off[k];
   for (int c0 = 0; c0 < R; c0 += 16) {
@@ -484,40 +508,45 @@ __global__ void __launch_bounds__(256) argmax_kernel(RowsParams prm) {
 #pragma unroll
     for (int c = 0; c < 16; ++c) { best[c] = -1.0; brw[c] = INT64_MAX; bng[c] = 0; }
     for (int64_t i = r0 + tid; i < r0 + nr; i += blockDim.x) {
-      const double* y = prm.y2 + i * sp;
+      ACols o;
+      a_row_cols(prm.y2 + i * sp, s, Ps, R, c0, cw, o);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        if (c >= cw) break;
-        double acc = 0.0;
-        for (int a = 0; a < s; ++a) acc = fma(y[a], Pk[a * R + c0 + c], acc);
-        const double v = fabs(acc);
-        if (v > best[c]) { best[c] = v; brw[c] = i - base; bng[c] = acc < 0.0; }
+        const double v = fabs(o.acc[c]);
+        if (c < cw && v > best[c]) { best[c] = v; brw[c] = i - base; bng[c] = o.acc[c] < 0.0; }
       }
     }
-    for (int c = 0; c < cw; ++c) {
-      babs[tid] = best[c];
-      brow[tid] = brw[c];
-      bneg[tid] = bng[c];
-      __syncthreads();
-      for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (tid < o) {
-          const double va = babs[tid], vb = babs[tid + o];
-          const int64_t ra = brow[tid], rb = brow[tid + o];
-          if (vb > va || (vb == va && rb < ra)) {
-            babs[tid] = vb;
-            brow[tid] = rb;
-            bneg[tid] = bneg[tid + o];
-          }
+    // warp argmax (larger |a|, then lower row), then across the 8 warps in order
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      double v = best[c];
+      int64_t rw = brw[c];
+      int ng = bng[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int64_t orw = __shfl_xor_sync(0xffffffffu, rw, o);
+        const int ong = __shfl_xor_sync(0xffffffffu, ng, o);
+        if (ov > v || (ov == v && orw < rw)) { v = ov; rw = orw; ng = ong; }
+      }
+      if (lane == 0) { wabs[warp][c] = v; wrow[warp][c] = rw; wneg[warp][c] = ng; }
+    }
+    __syncthreads();
+    if (tid < cw) {
+      double v = -1.0;
+      int64_t rw = INT64_MAX;
+      int ng = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (wabs[w][tid] > v || (wabs[w][tid] == v && wrow[w][tid] < rw)) {
+          v = wabs[w][tid];
+          rw = wrow[w][tid];
+          ng = wneg[w][tid];
         }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        prm.cand_abs[(size_t)p * R + c0 + c] = babs[0];
-        prm.cand_row[(size_t)p * R + c0 + c] = brow[0];
-        prm.cand_neg[(size_t)p * R + c0 + c] = bneg[0];
-      }
-      __syncthreads();
+      prm.cand_abs[(size_t)p * R + c0 + tid] = v;
+      prm.cand_row[(size_t)p * R + c0 + tid] = rw;
+      prm.cand_neg[(size_t)p * R + c0 + tid] = ng;
     }
+    __syncthreads();
   }
 }
 
@@ -553,18 +582,24 @@ __global__ void __launch_bounds__(128) signs_kernel(const int32_t* slice_piece, 
   }
 }
 
+// A rows with the signed P (same accumulation order as argmax_kernel).
 __global__ void __launch_bounds__(256) assemble_a_kernel(RowsParams prm) {
-  const int p = blockIdx.x, R = prm.R, sp = prm.sp;
+  extern __shared__ __align__(16) double Ps[];  // s x R (signed)
+  const int p = blockIdx.x, tid = threadIdx.x, R = prm.R, sp = prm.sp;
   const int k = prm.piece_slice[p], s = prm.s_k[k];
   const double* Pk = prm.Pm + (size_t)k * sp * R;
+  for (int i = tid; i < s * R; i += blockDim.x) Ps[i] = Pk[i];
+  __syncthreads();
   const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
-  for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) {
-    const int64_t i = r0 + e / R;
-    const int c = (int)(e % R);
-    const double* y = prm.y2 + i * sp;
-    double acc = 0.0;
-    for (int a = 0; a < s; ++a) acc = fma(y[a], Pk[a * R + c], acc);
-    prm.A[i * R + c] = acc;
+  for (int64_t i = r0 + tid; i < r0 + nr; i += blockDim.x) {
+    for (int c0 = 0; c0 < R; c0 += 16) {
+      const int cw = min(16, R - c0);
+      ACols o;
+      a_row_cols(prm.y2 + i * sp, s, Ps, R, c0, cw, o);
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < cw) prm.A[i * R + c0 + c] = o.acc[c];
+    }
   }
 }
 
@@ -850,7 +885,7 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   fp.sp = sp;
   fp.R = R;
   const size_t fsm = (3 * (size_t)sp * (sp + 1) + 4 * sp) * 8;
-  fp.use_smem = fsm <= 96 * 1024;
+  fp.use_smem = fsm <= 200 * 1024;  // sp <= 64 (R <= 32 at p = R); beyond, global scratch
   if (fp.use_smem) {
     e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
     if (e != cudaSuccess) return e;
@@ -872,10 +907,14 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   rp.cand_neg = reinterpret_cast<int32_t*>(ws + L.cand_neg);
   rp.A = A_out;
   const int P = (int)st->npieces;
-  argmax_kernel<<<P, 256, 0, stream>>>(rp);
+  const size_t psm = (size_t)sp * R * 8;  // P staged in shared memory (<= 128 x 64 doubles)
+  e = cudaFuncSetAttribute(argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(assemble_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+  if (e != cudaSuccess) return e;
+  argmax_kernel<<<P, 256, psm, stream>>>(rp);
   signs_kernel<<<K, 128, 0, stream>>>(st->slice_piece, rp.cand_abs, rp.cand_row, rp.cand_neg, Pm, Sv, Vt,
                                       K, J, sp, R, M_out);
-  assemble_a_kernel<<<P, 256, 0, stream>>>(rp);
+  assemble_a_kernel<<<P, 256, psm, stream>>>(rp);
   complete_kernel<<<K, 256, 0, stream>>>(st->row_off, rank_out, R, A_out);
   if (a_signs) fill_kernel<<<(K * R + 255) / 256, 256, 0, stream>>>(a_signs, (int64_t)K * R, 1.0);  // A is signed
   e = cudaGetLastError();
