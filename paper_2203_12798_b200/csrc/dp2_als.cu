@@ -1016,6 +1016,8 @@ cudaError_t launch_persist(int R, const PsArgs& p, const AlsBufs& b, cudaStream_
   if (R <= 8) return launch_persist_b(R, p, b, sms, st);
   if (R <= 12) return launch_persist_c(R, p, b, sms, st);
   if (R <= 16) return launch_persist_d(R, p, b, sms, st);
+  if (R == 20) return launch_persist_e(R, p, b, sms, st);
+  if (R == 24) return launch_persist_f(R, p, b, sms, st);
   return cudaErrorInvalidValue;
 }
 
@@ -1035,7 +1037,7 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
   a.polar = polar;
   a.theta = b.theta;
   SolveArgs sv = solve_args(D, E, H, V, W, J, R, normalize, b, status);
-  if (persist_enabled() && R <= 16) {
+  if (persist_enabled() && (R <= 16 || R == 20 || R == 24)) {  // instantiated ranks (dp2_als_ps*.cu)
     PsArgs p{};
     p.F = F;
     p.D = D;

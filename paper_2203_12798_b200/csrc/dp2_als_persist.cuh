@@ -1,5 +1,5 @@
-// Persistent ALS loop: kernel template and launcher (instantiated for R = 1..16
-// in dp2_als_ps{a,b,c,d}.cu, dispatched from dp2_als.cu).
+// Persistent ALS loop: kernel template and launcher (instantiated for R = 1..16,
+// 20 and 24 in dp2_als_ps{a..f}.cu, dispatched from dp2_als.cu).
 //
 // The whole iteration loop of P/solver.py:152-184 in ONE cooperative launch:
 // every CTA is resident, slices are owned by warps (warp w of the grid handles
@@ -603,5 +603,8 @@ cudaError_t launch_persist_a(int R, const PsArgs& p, const AlsBufs& b, int sms, 
 cudaError_t launch_persist_b(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
 cudaError_t launch_persist_c(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
 cudaError_t launch_persist_d(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+cudaError_t launch_persist_e(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+cudaError_t launch_persist_f(int R, const PsArgs& p, const AlsBufs& b, int sms, cudaStream_t st);
+
 
 }  // namespace dp2
