@@ -75,7 +75,7 @@ int32_t dp2_stream_segments(int32_t dtype, int64_t J, int32_t sms) {
   // the DMMA pass as CTA pairs: one segment per pair
   const bool dmma = dtype == DP2_F64 || dp2::sketch_engine() == 2;
   if (dmma && dp2::sketch64_pairs(J)) return sms / 2 > 0 ? sms / 2 : 1;
-  return (dtype == DP2_F64 || J <= 512) ? sms : 2 * sms;
+  return (dtype == DP2_F64 || J <= 512 || (dmma && J <= 1024)) ? sms : 2 * sms;
 }
 
 int32_t dp2_set_sketch_engine(int32_t engine) {

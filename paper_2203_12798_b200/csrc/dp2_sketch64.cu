@@ -46,7 +46,6 @@ namespace s64 {
 constexpr int TMAX = 16;        // rows per tile: TM = 8 (J > 256 per CTA), 16 (J <= 256)
 constexpr int NA = 4;           // warps computing Y partials (split of J)
 constexpr int NB = 16;          // warps accumulating Z (split of J)
-constexpr int MBMAX = 4;        // J-blocks of 8 per B warp (J <= 512)
 constexpr int NY = 2;           // ypart / yfin ring depth
 // warp w runs on SM sub-partition w % 4: one A warp and four B warps per
 // sub-partition keep the DMMA work per sub-partition equal
@@ -408,7 +407,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   } else {
     // ------------------------------------------------------------ B warps: Z += X_t^T Y_t
     const int bw = warp - WARP_B0;
-    const int MB = JH / (8 * NB);  // J-blocks of 8 per B warp (<= MBMAX)
+    // J-blocks of 8 per B warp: <= 4 at J <= 512; J <= 1024 runs one sketch
+    // column block per CTA (NT = 1) with up to 8
+    constexpr int MBMAX = NT == 1 ? 8 : 4;
+    const int MB = JH / (8 * NB);
     const int jb0 = bw * MB;
     double z[MBMAX][NT][2];
 #pragma unroll
@@ -521,9 +523,12 @@ struct Plan {
 };
 
 bool plan(int J, int sp, int elem, Plan* pl) {
-  if (J < 1 || J > 512 || sp < 8 || sp % 8) return false;
+  if (J < 1 || J > 1024 || sp < 8 || sp % 8) return false;
   const int nbt = sp / 8;
-  const int NT = nbt <= 3 ? nbt : 3;  // groups of <= 3 column blocks (last one zero padded)
+  // groups of <= 3 column blocks (last one zero padded); above J = 512 the
+  // image of 3 blocks no longer fits next to the X ring: one block per CTA
+  // group (X is then streamed once per block -- the pass stays DMMA-bound)
+  const int NT = J > 512 ? 1 : (nbt <= 3 ? nbt : 3);
   const int ng = (nbt + NT - 1) / NT;
   const int CL = uses_pairs(J) ? 2 : 1;
   const int JP = CL == 2 ? (J + 16 * NB - 1) / (16 * NB) * (16 * NB) : (J + 8 * NB - 1) / (8 * NB) * (8 * NB);

@@ -822,7 +822,11 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
     double* sgn = reinterpret_cast<double*>(ws + L.sgn);
     // the tensor-core pass leaves G to gram_y_piece_kernel (run_stage1_small; partials into gpart)
     const bool tc = sketch_tc_eligible(st, sp);
-    double* gp = tc ? nullptr : gpart;
+    // G = Y^T Y comes from pass 2 unless that pass cannot form it (the
+    // tensor-core pass, or the DMMA pass split into column groups at J > 512):
+    // then small(1) forms it from the stored Y rows
+    const bool dmma_nog = !tc && s64 && !sketch64_eligible(st, sp, false, true);
+    double* gp = (tc || dmma_nog) ? nullptr : gpart;
     auto small = [&](int phase) {
       return run_stage1_small(st, s_dev, sp, R, part, part, gp, qz, qz, CCg, Gg, y2, Pm, Sv, sgn,
                               reinterpret_cast<double*>(ws + L.cand_abs), reinterpret_cast<int64_t*>(ws + L.cand_row),

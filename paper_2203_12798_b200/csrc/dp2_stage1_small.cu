@@ -849,6 +849,13 @@ cudaError_t post_t(const dp2_store* st, const int32_t* s_dev, int R, const doubl
                    double* M, int32_t* rank_out, int64_t* status, cudaStream_t stream, double* a_signs) {
   const int K = (int)st->K, J = (int)st->J, P = (int)st->npieces;
   cudaError_t e = cudaSuccess;
+  if (!gpart && !y32) {  // DMMA pass in column groups (J > 512): G partials per piece from its fp64 Y rows
+    const size_t gs = (size_t)8 * 32 * (SP + 2) * 8 + (size_t)8 * GramBlocks<SP>::NBLK * 64 * 8;
+    e = cudaFuncSetAttribute(gram_y_piece_kernel<double, SP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gs);
+    if (e != cudaSuccess) return e;
+    gram_y_piece_kernel<double, SP><<<P, 256, gs, stream>>>(y2, st->piece_row0, st->piece_rows, gscratch);
+    gpart = gscratch;
+  }
   if (!gpart) {  // tensor-core pass: G partials per piece from its fp32 Y rows
     static const bool dmma = getenv("DP2_GRAM_DMMA") && atoi(getenv("DP2_GRAM_DMMA")) != 0;
     if (dmma) {

@@ -71,7 +71,8 @@ SHAPES = [
     ([256, 129], 300, 32, 3, False),              # sp = 32: two column groups (G elsewhere)
     ([700] * 6, 512, 16, 5, True),
     ([41, 600, 999], 512, 128, 7, False),         # c4-like (s = 2R = 100 -> sp 128): six groups
-    ([3000, 17], 256, 24, 148, True),             # many more segments than rows per segment
+    ([3000, 17], 256, 24, 148, True),             # many more segments than rows per segment (16-row tiles)
+    ([300, 77, 1200], 1000, 24, 4, False),        # the c5 width: one column block per CTA group (G elsewhere)
 ]
 
 
