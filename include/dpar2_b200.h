@@ -156,6 +156,12 @@ int dp2_omega_generate_stream(uint64_t seed, int64_t rows, int32_t width, const 
  * vals[i] and ok[i] = 1, or ok[i] = 0 when the device's acceptance decision
  * differed (the slice must then be regenerated on the host). */
 int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, int32_t* ok);
+/* Replay (multithreaded) and patch in one call: the accepted values are
+ * scattered into out_dev (K x J x sp, slice k's J x widths_host[k] block) on
+ * ``stream``; records whose acceptance decision differs set redo_host[slice]
+ * = 1 (the caller regenerates those slices); *patched_out = values patched. */
+int dp2_omega_patch(const dp2_tail_record* recs, int64_t count, int64_t J, const int32_t* widths_host, int32_t sp,
+                    double* out_dev, int32_t* redo_host, int32_t* patched_out, void* stream);
 
 /* ------------------------------------------------------------------ tensor checks
  * Per-slice squared Frobenius norms (sqnorm_dev[K]) and the lowest slice with

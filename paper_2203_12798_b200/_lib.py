@@ -52,6 +52,7 @@ _SIGS = {
     "dp2_omega_generate": (c_i32, [C.c_uint64, c_i64, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                    c_vp]),
     "dp2_omega_replay": (c_i32, [c_vp, c_i64, P(c_f64), P(c_i32)]),
+    "dp2_omega_patch": (c_i32, [c_vp, c_i64, c_i64, c_vp, c_i32, c_vp, c_vp, P(c_i32), c_vp]),
     "dp2_slice_stats": (c_i32, [P(Store), c_vp, c_vp, c_vp]),
     "dp2_copy_h2d_small": (c_i32, [c_vp, c_vp, c_sz, c_vp]),
     "dp2_sketch_uses_tc": (c_i32, [P(Store), c_i32]),

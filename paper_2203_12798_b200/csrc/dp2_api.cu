@@ -4,6 +4,8 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "dp2_internal.h"
@@ -230,6 +232,91 @@ int dp2_omega_replay(const dp2_tail_record* recs, int64_t count, double* vals, i
     ok_out[n] = good;
   }
   return DP2_OK;
+}
+
+// Replay + patch in one call (the exact-Omega path of rng.omega_device):
+// records replayed on host threads, the accepted values scattered into
+// out_dev[slice][index / w][index % w] (w = widths_host[slice], row stride sp)
+// by a kernel reading a library-owned pinned buffer through UVA; slices whose
+// acceptance decision differs get redo_host[slice] = 1.
+static __global__ void omega_patch_kernel(const int64_t* idx, const double* val, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[((const volatile int64_t*)idx)[i]] = ((const volatile double*)val)[i];
+}
+
+namespace {
+struct PatchBuf {
+  int64_t* idx = nullptr;
+  double* val = nullptr;
+  int64_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+PatchBuf g_patch[64];
+std::mutex g_patch_mu;
+}  // namespace
+
+int dp2_omega_patch(const dp2_tail_record* recs, int64_t count, int64_t J, const int32_t* widths_host, int32_t sp,
+                    double* out_dev, int32_t* redo_host, int32_t* patched_out, void* stream) {
+  if (count < 0 || (count && (!recs || !widths_host || !out_dev || !redo_host))) return fail_arg("invalid patch arguments");
+  if (patched_out) *patched_out = 0;
+  if (count == 0) return DP2_OK;
+  std::vector<double> vals((size_t)count);
+  std::vector<int32_t> okv((size_t)count);
+  const int hw = (int)std::thread::hardware_concurrency();
+  // (thread start-up costs ~20 us each: only very large record counts use a team)
+  const int nt = count < 32768 ? 1 : std::max(1, std::min(16, hw));
+  std::vector<std::thread> team;
+  std::vector<int> rc(nt, DP2_OK);
+  const int64_t chunk = (count + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = t * chunk, b = std::min(count, a + chunk);
+    if (a >= b) break;
+    auto fn = [&, a, b, t] { rc[t] = dp2_omega_replay(recs + a, b - a, vals.data() + a, okv.data() + a); };
+    if (nt == 1) fn(); else team.emplace_back(fn);
+  }
+  for (auto& th : team) th.join();
+  for (int r : rc)
+    if (r != DP2_OK) return r;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(cudaErrorInvalidDevice, "dp2_omega_patch");
+  std::lock_guard<std::mutex> g(g_patch_mu);
+  PatchBuf& pb = g_patch[dev];
+  if (pb.done) cudaEventSynchronize(pb.done);  // the previous patch kernel is done reading the buffer
+  if (pb.cap < count) {
+    if (pb.idx) cudaFreeHost(pb.idx);
+    if (pb.val) cudaFreeHost(pb.val);
+    pb.idx = nullptr;
+    pb.val = nullptr;
+    pb.cap = 0;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&pb.idx), count * 8, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&pb.val), count * 8, cudaHostAllocDefault);
+    if (e != cudaSuccess) return fail(e, "dp2_omega_patch");
+    pb.cap = count;
+    if (!pb.done && (e = cudaEventCreateWithFlags(&pb.done, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(e, "dp2_omega_patch");
+  }
+  int64_t n = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const dp2_tail_record& r = recs[i];
+    if (!okv[i]) {
+      redo_host[r.slice] = 1;
+      continue;
+    }
+    const int64_t w = widths_host[r.slice];
+    pb.idx[n] = r.slice * (J * sp) + (r.index / w) * sp + r.index % w;
+    pb.val[n] = vals[i];
+    ++n;
+  }
+  if (n) {
+    omega_patch_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 64), 256, 0, S(stream)>>>(pb.idx, pb.val, n,
+                                                                                                 out_dev);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventRecord(pb.done, S(stream));
+    if (e != cudaSuccess) return fail(e, "dp2_omega_patch");
+  }
+  if (patched_out) *patched_out = (int32_t)n;
+  return n ? ok(1) : DP2_OK;
 }
 
 // ---------------------------------------------------------------- host checks

@@ -155,25 +155,19 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     if count > cap:
         redo_h[:] = 1  # record overflow: regenerate everything on the host (never expected)
     patched = 0
-    if count:
-        r = recs_h[:min(count, cap)].numpy().view(_REC).reshape(-1)
-        vals = np.empty(r.size)
-        okv = np.empty(r.size, dtype=np.int32)
-        # replay each attempt with the C library's log1p (dp2_omega_replay) --
-        # the function the reference sampler calls (npy_log1p); NumPy's
-        # np.log1p ufunc may use a SIMD implementation with different rounding
-        _lib.check(_lib.lib().dp2_omega_replay(C.c_void_p(r.ctypes.data), r.size,
-                                               vals.ctypes.data_as(C.POINTER(C.c_double)),
-                                               okv.ctypes.data_as(C.POINTER(C.c_int32))), "omega_replay")
-        ok = okv != 0
-        redo_h[r["slice"][~ok]] = 1
-        good = ok & (redo_h[r["slice"]] == 0)
-        if good.any():
-            w = np.asarray(widths)[r["slice"][good]]
-            flat = r["slice"][good] * (n * sp) + (r["index"][good] // w) * sp + r["index"][good] % w
-            idx = to_device_async(flat, torch.int64, device)
-            out.view(-1).index_copy_(0, idx, to_device_async(vals[good], torch.float64, device))
-            patched = int(good.sum())
+    if count and count <= cap:
+        # replay each attempt with the C library's log1p -- the function the
+        # reference sampler calls (npy_log1p); NumPy's np.log1p ufunc may use a
+        # SIMD implementation with different rounding -- and scatter the exact
+        # values into Omega on the stream (dp2_omega_patch, host threads + one kernel)
+        w32 = widths if isinstance(widths, np.ndarray) and widths.dtype == np.int32 else \
+            np.ascontiguousarray(widths, dtype=np.int32)
+        npatch = C.c_int32(0)
+        _lib.check(_lib.lib().dp2_omega_patch(C.c_void_p(recs_h.data_ptr()), count, n,
+                                              C.c_void_p(w32.ctypes.data), sp, C.c_void_p(out.data_ptr()),
+                                              C.c_void_p(redo_h.ctypes.data), C.byref(npatch), stream_ptr()),
+                   "omega_patch")
+        patched = int(npatch.value)
     bad = np.nonzero(redo_h)[0]
     if bad.size:
         ids_h = list(range(K)) if slice_ids is None else list(slice_ids)
