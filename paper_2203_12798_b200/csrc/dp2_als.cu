@@ -1,11 +1,14 @@
 // Compressed-space ALS (P/solver.py:39-190), fp64.
 //
-// One iteration = 7 stream-ordered, graph-capturable launches:
+// One iteration = 9 stream-ordered, graph-capturable launches:
 //   rotate  (warp/slice) T_k = (F_k cc) diag(w_k) H^T; polar Pi_k = Z_k P_k^T by
 //           one-sided Jacobi warm-started from the previous iteration's P_k;
-//           Theta_k = Pi_k^T F_k; mode-1 and gram(W) partials
+//           Theta_k = Pi_k^T F_k; mode-1 and gram(W) partials.  32 < R <= 56:
+//           one CTA per slice (CTA-parallel Jacobi rounds, cold start)
+//   reduce  (n/32 CTAs)  ordered sum of the per-CTA mode-1 / gram(W) slots
 //   solve_h (1 CTA)      H = G1 pinv(W'W * V'V); column norms -> nh
 //   mode2   (warp/slice) sum_k (w_k nh) (Theta_k^T H), gram(W nh) partials
+//   reduce  (n/32 CTAs)  the same for the mode-2 slots
 //   solve_v (1 CTA)      V = D (E * summed) pinv(...); norms; V'V, cc', pinv3
 //   mode3   (warp/slice) G3 row, W_k = G3_k pinv3; L_k = [Theta_k E | -H W_k]
 //   metric  (DMMA)       e = ||L N^T||_F^2 with N = [D V] (J x 2R): the
@@ -22,6 +25,7 @@
 #include "dp2_als_persist.cuh"
 #include <cstdio>
 #include <cstdlib>
+// #define DP2_ROT_DEBUG 1
 
 namespace dp2 {
 
@@ -63,6 +67,38 @@ DP2_DEV void reduce_slots_warp(const double* slots, int nslots, int n, double* o
     for (int w = lane + 256; w < nslots; w += 32) s += slots[(size_t)w * n + e];
     s = warp_sum(s);
     if (lane == 0) out[e] = s;
+  }
+}
+
+// In-place ordered reduction of nslots per-CTA slots (n doubles each) into
+// slot 0, two slot arrays at once (blockIdx.y): CTA x sums entries
+// 32x .. 32x+31 (coalesced rows), warp w slots w, w + 8, ... in order, and the
+// 8 warp partials combine in warp order -- deterministic, and spread over
+// n/32 SMs instead of the single solve CTA.
+__global__ void __launch_bounds__(256) reduce_slots_kernel(const int32_t* ctl, double* s0, double* s1, int nslots,
+                                                           int n) {
+  if (ctl[0]) return;
+  double* slots = blockIdx.y ? s1 : s0;
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (e < n) {
+    int w = warp;
+    for (; w + 24 < nslots; w += 32) {
+      const double a = slots[(size_t)w * n + e], b = slots[(size_t)(w + 8) * n + e];
+      const double c = slots[(size_t)(w + 16) * n + e], d = slots[(size_t)(w + 24) * n + e];
+      acc += (a + b) + (c + d);
+    }
+    for (; w < nslots; w += 8) acc += slots[(size_t)w * n + e];
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && e < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    slots[e] = t;
   }
 }
 
@@ -254,6 +290,232 @@ __global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
     __syncthreads();
     combine_warps(wbase + (acc1 - Ts), wstride, b.wpb, R * R, b.s_g1 + (size_t)blockIdx.x * R * R);
     combine_warps(wbase + (acc2 - Ts), wstride, b.wpb, R * R, b.s_wtw + (size_t)blockIdx.x * R * R);
+  }
+}
+
+// ------------------------------------------------------------ large R (R > 32)
+// One CTA per slice: the one-sided Jacobi SVD of T_k parallel over the CTA --
+// each round's independent column pairs (round-robin ordering) spread over
+// the warps, each pair's three dot products and its column updates spread
+// over the lanes -- instead of one warp doing all pairs and elements serially
+// (the generic kernel above: ~25 ms per iteration at K = 1000, R = 50).
+// ``pt``: the round-robin pairs, pt[r * np + i] = (p << 16) | q (rr_pair_table).
+DP2_DEV void rr_pair_table(int n, int* pt) {
+  const int ne = n + (n & 1), np = ne / 2;
+  for (int e = threadIdx.x; e < (ne - 1) * np; e += blockDim.x) {
+    int p, q;
+    rr_pair(ne, e / np, e % np, p, q);
+    pt[e] = (p << 16) | q;
+  }
+}
+
+DP2_DEV int jacobi_onesided_cta(double* T, int ldt, double* V, int ldv, int n, const int* pt, int* flag,
+                                int max_sweeps = 60) {
+  // a pair per 8-lane group (4 per warp): a round of <= 28 pairs (n <= 56) is
+  // one pass over the 256-thread CTA; lane `sub` of a group holds elements
+  // sub, sub + 8, ... of the pair's two columns in registers between the dot
+  // products (3 shuffle levels) and the rotation
+  constexpr int KM = 7;
+  const int sub = threadIdx.x & 7, grp = threadIdx.x >> 3;
+  if (n < 2) return 0;
+  const int ne = n + (n & 1), np = ne / 2;
+  const double tol = n * kEps;  // rounding floor of the length-n dot products
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < ne - 1; ++r) {
+      int p = 0, q = n;
+      if (grp < np) {
+        const int pq = pt[r * np + grp];
+        p = pq >> 16;
+        q = pq & 0xffff;
+      }
+      const bool live = q < n;
+      double* tp = T + p * ldt;
+      double* tq = T + (live ? q : p) * ldt;
+      double x[KM], y[KM];
+      double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+      for (int m = 0; m < KM; ++m) {
+        const int k = sub + 8 * m;
+        x[m] = (live && k < n) ? tp[k] : 0.0;
+        y[m] = (live && k < n) ? tq[k] : 0.0;
+        al = fma(x[m], x[m], al);
+        be = fma(y[m], y[m], be);
+        ga = fma(x[m], y[m], ga);
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+#ifdef DP2_ROT_DEBUG
+      if (live && sub == 0 && blockIdx.x == 0) {
+        const float rel = (float)(ga * ga / (al * be + 1e-300));
+        atomicMax(flag + 1, __float_as_int(rel));
+        if (ga != 0.0 && ga * ga > (tol * tol) * (al * be)) atomicAdd(flag + 2, 1);
+      }
+#endif
+      if (live && ga != 0.0 && ga * ga > (tol * tol) * (al * be)) {
+        double c, sn;
+        rot_params(be - al, ga, c, sn);
+        double* vp = V + p * ldv;
+        double* vq = V + q * ldv;
+#pragma unroll
+        for (int m = 0; m < KM; ++m) {
+          const int k = sub + 8 * m;
+          if (k < n) {
+            tp[k] = c * x[m] - sn * y[m];
+            tq[k] = sn * x[m] + c * y[m];
+            const double a = vp[k], b = vq[k];
+            vp[k] = c * a - sn * b;
+            vq[k] = sn * a + c * b;
+          }
+        }
+        if (sub == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+#ifdef DP2_ROT_DEBUG
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+      printf("  sweep %d maxrel %.3e rots %d\n", sweep, __int_as_float(flag[1]), flag[2]);
+      flag[1] = flag[2] = 0;
+    }
+#endif
+    if (*flag == 0) break;
+    __syncthreads();  // everyone has read the flag before it is reset
+  }
+  return sweep + 1;
+}
+
+__host__ __device__ inline size_t rotate_cta_doubles(int R) {
+  return (size_t)2 * R * R /* Fs, Pi */ + (size_t)2 * R * (R + 1) /* Ts, Vr */ + (size_t)R + 16 /* norms, flag */ +
+         (size_t)(R + 1) * (R + 2) / 4 + 1 /* pair table */;
+}
+
+// One CTA per slice, 32 < R <= 56: T_k = (F_k cc) diag(w_k) H^T
+// (P/solver.py:55-58), its polar factor U V^T by the CTA-parallel one-sided
+// Jacobi SVD (with the orthonormal completion of warp_polar for singular
+// T_k), Theta_k = Pi_k^T F_k, and the mode-1 partials into this CTA's slots.
+// Shared memory is trimmed to ~2 (R^2 + R (R + 1)) doubles (cc and H are read
+// through L1; Th, T and Theta share the Jacobi buffers) so two CTAs fit per SM
+// -- the Jacobi rounds are latency-bound.  Cold start every iteration: the
+// previous right factor does not shorten the sweeps here (T_k's small
+// singular values are clustered and their vectors move between iterations).
+__global__ void __launch_bounds__(256) als_rotate_cta_kernel(SliceArgs a, AlsBufs b) {
+  if (b.ctl[0]) return;
+  extern __shared__ __align__(16) double sm[];
+  const int R = a.R, RR = R * R, ldt = R + 1, tid = threadIdx.x, nt = blockDim.x;
+  const double* __restrict__ cc = b.cc;
+  const double* __restrict__ H = a.H;
+  double* Fs = sm;
+  double* Pi = Fs + RR;  // T, then the polar factor
+  double* Ts = Pi + RR;  // Th (row-major, before the Jacobi), the columns of T V, then Theta
+  double* Vr = Ts + R * ldt;
+  double* nrm = Vr + R * ldt;
+  int* flag = reinterpret_cast<int*>(nrm + R + 8);
+  int* pt = flag + 16;
+  rr_pair_table(R, pt);
+  double* acc1 = a.mode1 ? b.s_g1 + (size_t)blockIdx.x * RR : nullptr;  // this CTA's partial slots
+  double* acc2 = a.mode1 ? b.s_wtw + (size_t)blockIdx.x * RR : nullptr;
+  if (a.mode1)
+    for (int e = tid; e < RR; e += nt) acc1[e] = acc2[e] = 0.0;
+  for (int64_t k = blockIdx.x; k < a.K; k += gridDim.x) {
+    const double* Fk = a.F + k * RR;
+    const double* wk = a.W + k * R;
+    for (int e = tid; e < RR; e += nt) Fs[e] = Fk[e];
+    __syncthreads();
+    double* Th = Ts;
+    for (int e = tid; e < RR; e += nt) {  // Th = (F_k cc) * w_k
+      const int i = e / R, c = e - i * R;
+      double s = 0.0;
+      for (int q = 0; q < R; ++q) s = fma(Fs[i * R + q], __ldg(cc + q * R + c), s);
+      Th[e] = s * __ldg(wk + c);
+    }
+    __syncthreads();
+    for (int e = tid; e < RR; e += nt) {  // T = Th H^T
+      const int i = e / R, d = e - i * R;
+      double s = 0.0;
+      for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], __ldg(H + d * R + c), s);
+      Pi[e] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < RR; e += nt) {  // columns of T, V = I
+      const int c = e / R, i = e - c * R;
+      Ts[c * ldt + i] = Pi[i * R + c];
+      Vr[c * ldt + i] = c == i ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int sw = jacobi_onesided_cta(Ts, ldt, Vr, ldt, R, pt, flag);
+    if (sw > 60 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.status + ST_SWEEPCAP), 1ull);
+    for (int i = tid >> 5; i < R; i += nt >> 5) {  // column norms
+      double sq = 0.0;
+      for (int d = tid & 31; d < R; d += 32) sq = fma(Ts[i * ldt + d], Ts[i * ldt + d], sq);
+      sq = warp_sum(sq);
+      if ((tid & 31) == 0) nrm[i] = sqrt(sq);
+    }
+    __syncthreads();
+    for (int e = tid; e < RR; e += nt) {
+      const int i = e / R, d = e - i * R;
+      const double n = nrm[i];
+      Ts[i * ldt + d] = n > 1e-300 ? Ts[i * ldt + d] / n : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {  // (numerically) singular T_k: complete Z orthonormally, as warp_polar
+      for (int i = 0; i < R; ++i) {
+        if (nrm[i] > 1e-300) continue;
+        for (int t = 0; t < R; ++t) {
+          double* z = Ts + i * ldt;
+          for (int d = 0; d < R; ++d) z[d] = (d == t) ? 1.0 : 0.0;
+          for (int pass = 0; pass < 2; ++pass)
+            for (int c = 0; c < R; ++c) {
+              if (c == i || !(nrm[c] > 1e-300)) continue;
+              double dd = 0.0;
+              for (int d = 0; d < R; ++d) dd = fma(Ts[c * ldt + d], z[d], dd);
+              for (int d = 0; d < R; ++d) z[d] = fma(-dd, Ts[c * ldt + d], z[d]);
+            }
+          double n2 = 0.0;
+          for (int d = 0; d < R; ++d) n2 = fma(z[d], z[d], n2);
+          if (n2 > 0.25) {
+            const double inv = 1.0 / sqrt(n2);
+            for (int d = 0; d < R; ++d) z[d] *= inv;
+            nrm[i] = 1.0;
+            break;
+          }
+        }
+        if (!(nrm[i] > 1e-300)) status_min(a.status, ST_POLAR, k);
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < RR; e += nt) {  // Pi[d][c] = sum_i Z[d][i] V[c][i]
+      const int d = e / R, c = e - d * R;
+      double s = 0.0;
+      for (int i = 0; i < R; ++i) s = fma(Ts[i * ldt + d], Vr[i * ldt + c], s);
+      Pi[e] = s;
+      if (a.polar) a.polar[k * RR + e] = s;
+    }
+    __syncthreads();
+    double* Tht = Ts;
+    for (int e = tid; e < RR; e += nt) {  // Theta = Pi^T F
+      const int i = e / R, c = e - i * R;
+      double s = 0.0;
+      for (int d = 0; d < R; ++d) s = fma(Pi[d * R + i], Fs[d * R + c], s);
+      Tht[e] = s;
+      a.theta[k * RR + e] = s;
+    }
+    __syncthreads();
+    if (a.mode1) {  // g1[i][r] += w[k][r] (Theta cc)[i][r];  wtw[i][r] += w[k][i] w[k][r]
+      for (int e = tid; e < RR; e += nt) {
+        const int i = e / R, r = e - i * R;
+        double s = 0.0;
+        for (int q = 0; q < R; ++q) s = fma(Tht[i * R + q], __ldg(cc + q * R + r), s);
+        acc1[e] += __ldg(wk + r) * s;
+        acc2[e] += __ldg(wk + i) * __ldg(wk + r);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -857,6 +1119,11 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.nbm = metric_blocks(K, R);
   rot_cfg(K, R, b.wpbr, b.nbr);
   if (b.nbr <= 0) { b.nbr = b.nb; b.wpbr = b.wpb; }
+  if (R > 32 && R <= 56) {  // als_rotate_cta_kernel: two CTAs per SM, CTA-strided slices
+    const int64_t cap = 2 * (int64_t)sm_count();
+    b.nbr = (int)(K < cap ? K : cap);
+    b.wpbr = 8;
+  }
   return b;
 }
 
@@ -925,6 +1192,12 @@ cudaError_t launch_rotate(const SliceArgs& a, const AlsBufs& b, cudaStream_t st,
     DP2_ROT_CASE(13) DP2_ROT_CASE(14) DP2_ROT_CASE(15) DP2_ROT_CASE(16)
 #undef DP2_ROT_CASE
     default:
+      if (a.R > 32 && a.R <= 56) {  // CTA-parallel Jacobi (R <= ~56)
+        const size_t smc = rotate_cta_doubles(a.R) * 8;
+        if (setattr) return set_smem((const void*)als_rotate_cta_kernel, smc);
+        als_rotate_cta_kernel<<<b.nbr, 256, smc, st>>>(a, b);
+        return cudaGetLastError();
+      }
       if (setattr) return set_smem((const void*)als_rotate_kernel, rotate_smem(a.R, b.wpb));
       als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(a.R, b.wpb), st>>>(a, b);
       return cudaGetLastError();
@@ -954,9 +1227,15 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   a.warm = 1;
   cudaError_t e0 = launch_rotate(a, b, st);
   if (e0 != cudaSuccess) return e0;
-  als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(sv, b);
+  SolveArgs s1 = sv;  // slots pre-reduced into slot 0 on n/32 CTAs
+  const int RR = R * R, gx = (RR + 31) / 32;
+  reduce_slots_kernel<<<dim3(gx, 2), 256, 0, st>>>(b.ctl, b.s_g1, b.s_wtw, sv.nslots_h, RR);
+  s1.nslots_h = 1;
+  als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(s1, b);
   als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(sv, b);
+  reduce_slots_kernel<<<dim3(gx, 2), 256, 0, st>>>(b.ctl, b.s_m2, b.s_wtw2, sv.nslots, RR);
+  s1.nslots = 1;
+  als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(s1, b);
   a.write_w = 1;
   a.write_l = 1;
   a.Wout = sv.W;
@@ -1031,7 +1310,7 @@ cudaError_t als_run(const double* F, const double* D, const double* E, int64_t K
                     double* H, double* V, double* W, double* polar, int max_iters, double tol,
                     int normalize, double* trace, int64_t* tstamp, int32_t* iters, int use_graph,
                     char* ws, int64_t* status, cudaStream_t st, int64_t* launches) {
-  if (launches) *launches = 1 + 7 * (int64_t)max_iters;
+  if (launches) *launches = 1 + 9 * (int64_t)max_iters;
   AlsBufs b = make_bufs(ws, K, J, R);
   SliceArgs a = slice_args(F, D, E, H, V, W, K, J, R, status);
   a.polar = polar;

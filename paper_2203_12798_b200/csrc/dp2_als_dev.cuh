@@ -250,7 +250,16 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
   }
   __syncthreads();
   if (fast) return;
-  if (threadIdx.x < 32) {
+  if (RC == 0 && R > 32) {  // large R: the whole block on the Jacobi rounds
+    __shared__ int jflag;
+    const int sw = jacobi_eig_block(A, R, U, R, R, cs, &jflag);
+    if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int i = 0; i < R; ++i) m = fmax(m, fabs(A[i * R + i]));
+      lmax = m;
+    }
+  } else if (threadIdx.x < 32) {
     const int sw = jacobi_eig_warp(A, R, U, R, R, cs);
     if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
     if (threadIdx.x == 0) {

@@ -17,12 +17,15 @@ def main(path, top=30):
     stall_cols = [i for i, n in enumerate(h) if n.startswith("stall_") and "Not Issued" not in n]
     inst, samp, src = defaultdict(float), defaultdict(float), {}
     stalls = defaultdict(lambda: defaultdict(float))
-    line = None
+    line, fname = None, rows[0][1].rsplit("/", 1)[-1] if rows[0][:1] == ["File Path"] else ""
     for r in rows[hdr + 1:]:
+        if r[:1] == ["File Path"]:
+            fname, line = r[1].rsplit("/", 1)[-1], None
+            continue
         if len(r) < 3:
             continue
         if r[0]:
-            line = int(r[0]) if r[0].isdigit() else None
+            line = (fname, int(r[0])) if r[0].isdigit() else None
             src[line] = r[1]
         if line is None or len(r) <= ie or not r[ie]:
             continue
@@ -38,7 +41,7 @@ def main(path, top=30):
     for ln in sorted(samp, key=lambda k: -samp[k])[:top]:
         top_st = sorted(stalls[ln].items(), key=lambda kv: -kv[1])[:2]
         st = " ".join(f"{k[6:]}={v:.0f}" for k, v in top_st if v)
-        print(f"{ln:5d} samp {samp[ln]:5.0f} ({100 * samp[ln] / max(tot_s, 1):4.1f}%) inst {inst[ln]:8.0f}  {st:30s} "
+        print(f"{ln[0][:14]:>14s}:{ln[1]:<5d} samp {samp[ln]:5.0f} ({100 * samp[ln] / max(tot_s, 1):4.1f}%) inst {inst[ln]:8.0f}  {st:30s} "
               f"{src.get(ln, '').strip()[:70]}")
 
 
