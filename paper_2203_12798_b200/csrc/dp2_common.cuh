@@ -155,32 +155,35 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
         cs[3 * i + 2] = (double)(p * 1024 + q);
       }
       __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int it = tid; it < n * np; it += nt) {
-        const int i = it / np, pr = it % np;
+      // columns: A <- A J, V <- V J (a pair per warp, lanes over the rows)
+      const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+      for (int pr = warp; pr < np; pr += nw) {
         const double s = cs[3 * pr + 1];
         if (s == 0.0) continue;
         const double c = cs[3 * pr];
         const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
-        double a = A[i * lda + p], b = A[i * lda + q];
-        A[i * lda + p] = c * a - s * b;
-        A[i * lda + q] = s * a + c * b;
-        a = V[i * ldv + p];
-        b = V[i * ldv + q];
-        V[i * ldv + p] = c * a - s * b;
-        V[i * ldv + q] = s * a + c * b;
+        for (int i = lane; i < n; i += 32) {
+          double a = A[i * lda + p], b = A[i * lda + q];
+          A[i * lda + p] = c * a - s * b;
+          A[i * lda + q] = s * a + c * b;
+          a = V[i * ldv + p];
+          b = V[i * ldv + q];
+          V[i * ldv + p] = c * a - s * b;
+          V[i * ldv + q] = s * a + c * b;
+        }
       }
       __syncthreads();
       // rows: A <- J^T A
-      for (int it = tid; it < n * np; it += nt) {
-        const int pr = it / n, j = it % n;
+      for (int pr = warp; pr < np; pr += nw) {
         const double s = cs[3 * pr + 1];
         if (s == 0.0) continue;
         const double c = cs[3 * pr];
         const int pq = (int)cs[3 * pr + 2], p = pq >> 10, q = pq & 1023;
-        const double a = A[p * lda + j], b = A[q * lda + j];
-        A[p * lda + j] = c * a - s * b;
-        A[q * lda + j] = s * a + c * b;
+        for (int j = lane; j < n; j += 32) {
+          const double a = A[p * lda + j], b = A[q * lda + j];
+          A[p * lda + j] = c * a - s * b;
+          A[q * lda + j] = s * a + c * b;
+        }
       }
       __syncthreads();
     }

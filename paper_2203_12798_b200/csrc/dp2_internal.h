@@ -91,6 +91,6 @@ cudaError_t d2h_staged(void* dst, const void* src, size_t n, cudaStream_t st);
 uint64_t derived_seed_host(uint64_t seed, uint64_t index);
 
 // shared small kernels (stage 1 / stage 2)
-__global__ void cgs2_kernel(double* Q, int64_t rows, int ld, int ncols, int64_t batch_stride);
+__global__ void cgs2_cols_kernel(double* Q, int64_t rows, int ncols, double* scr);
 
 }  // namespace dp2

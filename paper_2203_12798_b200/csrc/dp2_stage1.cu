@@ -234,37 +234,41 @@ __global__ void __launch_bounds__(256, 1) sketch_kernel(SketchParams prm) {
 // first s_k columns with classical Gram-Schmidt + one reorthogonalisation.
 // Exactly-zero columns are replaced by unit vectors (the reference's
 // Householder QR likewise returns a full orthonormal Q for a zero sketch).
-__device__ void cgs2_columns(double* Q, int64_t rows, int ld, int ncols, double* h, double* red) {
+// Element (r, c) of Q is Q[r * rs + c * cs]: cs = 1 for row-major Q, rs = 1
+// (columns contiguous) for coalesced column sweeps.
+__device__ void cgs2_columns(double* Q, int64_t rows, int64_t rs, int64_t cs, int ncols, double* h, double* red) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int c = 0; c < ncols; ++c) {
+    double* qc = Q + c * cs;
     for (int attempt = 0;; ++attempt) {
       if (attempt > 0) {  // replacement unit vector e_{(c + attempt - 1) mod rows}
         const int64_t e = (int64_t)(c + attempt - 1) % rows;
-        for (int64_t i = tid; i < rows; i += nt) Q[i * ld + c] = (i == e) ? 1.0 : 0.0;
+        for (int64_t i = tid; i < rows; i += nt) qc[i * rs] = (i == e) ? 1.0 : 0.0;
         __syncthreads();
       }
       for (int pass = 0; pass < 2; ++pass) {
         for (int i = warp; i < c; i += nw) {
+          const double* qi = Q + i * cs;
           double s = 0.0;
-          for (int64_t r = lane; r < rows; r += 32) s = fma(Q[r * ld + i], Q[r * ld + c], s);
+          for (int64_t r = lane; r < rows; r += 32) s = fma(qi[r * rs], qc[r * rs], s);
           s = warp_sum(s);
           if (lane == 0) h[i] = s;
         }
         __syncthreads();
         for (int64_t r = tid; r < rows; r += nt) {
-          double acc = Q[r * ld + c];
-          for (int i = 0; i < c; ++i) acc = fma(-h[i], Q[r * ld + i], acc);
-          Q[r * ld + c] = acc;
+          double acc = qc[r * rs];
+          for (int i = 0; i < c; ++i) acc = fma(-h[i], Q[r * rs + i * cs], acc);
+          qc[r * rs] = acc;
         }
         __syncthreads();
       }
       double part = 0.0;
-      for (int64_t r = tid; r < rows; r += nt) part = fma(Q[r * ld + c], Q[r * ld + c], part);
+      for (int64_t r = tid; r < rows; r += nt) part = fma(qc[r * rs], qc[r * rs], part);
       const double nrm2 = block_sum(part, red);
       const bool ok = attempt == 0 ? (nrm2 > 1e-300) : (nrm2 > 0.25);
       if (ok || attempt > rows + 1) {
         const double inv = nrm2 > 0.0 ? 1.0 / sqrt(nrm2) : 0.0;
-        for (int64_t r = tid; r < rows; r += nt) Q[r * ld + c] *= inv;
+        for (int64_t r = tid; r < rows; r += nt) qc[r * rs] *= inv;
         __syncthreads();
         break;
       }
@@ -272,12 +276,16 @@ __device__ void cgs2_columns(double* Q, int64_t rows, int ld, int ncols, double*
   }
 }
 
-__global__ void __launch_bounds__(256) orth_kernel(const double* part, const int32_t* slice_piece,
+// The CGS2 runs on a column-major copy of the slice's Q (coalesced dot
+// products and updates; row-major Q would touch one sector per row) held in
+// the slice's first piece partial, which is dead once summed.
+__global__ void __launch_bounds__(256) orth_kernel(double* part, const int32_t* slice_piece,
                                                     const int32_t* s_k, int J, int sp, double* Q) {
   __shared__ double h[256];
   __shared__ double red[32];
   const int k = blockIdx.x;
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
+  const int s = s_k[k];
   double* Qk = Q + (size_t)k * J * sp;
   for (int64_t i = threadIdx.x; i < (int64_t)J * sp; i += blockDim.x) {
     double acc = 0.0;
@@ -285,20 +293,45 @@ __global__ void __launch_bounds__(256) orth_kernel(const double* part, const int
     Qk[i] = acc;
   }
   __syncthreads();
-  cgs2_columns(Qk, J, sp, s_k[k], h, red);
+  if (p1 == p0) {  // no piece (empty slice): row-major in place
+    cgs2_columns(Qk, J, sp, 1, s, h, red);
+    return;
+  }
+  double* Qc = part + (size_t)p0 * J * sp;  // s x J, column c at Qc + c J
+  for (int64_t i = threadIdx.x; i < (int64_t)J * s; i += blockDim.x) {
+    const int64_t c = i / J, r = i - c * J;
+    Qc[i] = Qk[r * sp + c];
+  }
+  __syncthreads();
+  cgs2_columns(Qc, J, 1, J, s, h, red);
+  for (int64_t i = threadIdx.x; i < (int64_t)J * s; i += blockDim.x) {
+    const int64_t r = i / s, c = i - r * s;
+    Qk[r * sp + c] = Qc[c * J + r];
+  }
 }
 
-// generic batched CGS2 (stage 2 uses it on single tall matrices)
-__global__ void __launch_bounds__(256) cgs2_kernel(double* Q, int64_t rows, int ld, int ncols,
-                                                    int64_t batch_stride) {
+// CGS2 of one tall row-major Q (rows x ncols) through a column-major copy in
+// ``scr`` (rows x ncols doubles): the stage-2 orthonormalisation for s2 > 32.
+__global__ void __launch_bounds__(256) cgs2_cols_kernel(double* Q, int64_t rows, int ncols, double* scr) {
   __shared__ double h[256];
   __shared__ double red[32];
-  cgs2_columns(Q + blockIdx.x * batch_stride, rows, ld, ncols, h, red);
+  for (int64_t i = threadIdx.x; i < rows * ncols; i += blockDim.x) {
+    const int64_t c = i / rows, r = i - c * rows;
+    scr[i] = Q[r * ncols + c];
+  }
+  __syncthreads();
+  cgs2_columns(scr, rows, 1, rows, ncols, h, red);
+  for (int64_t i = threadIdx.x; i < rows * ncols; i += blockDim.x) {
+    const int64_t r = i / ncols, c = i - r * ncols;
+    Q[i] = scr[c * rows + r];
+  }
 }
 
+
 // ============================================================ per-slice factor
-// smem: G, CC, W (s x s each, ld = s+1), vectors.  Falls back to the global
-// scratch ``scr`` (3*sp*(sp+1) doubles per slice) when s is large.
+// Two s x s work matrices (ld = s + 1) in shared memory when they fit in the
+// dynamic allocation (s <= ~105), else in the slice's global scratch
+// (3*sp*(sp+1) + 4*sp doubles per slice, which also holds T = W / sqrt(lam)).
 struct FactorParams {
   const double* part;       // npieces x J x sp (C^T partials)
   const int32_t* slice_piece;
@@ -312,25 +345,103 @@ struct FactorParams {
   int32_t* rank_out;        // K
   double* scr;              // global scratch
   int64_t* status;
-  int J, sp, R, use_smem;
+  int J, sp, R, smem_bytes;
 };
 
+constexpr int kGramRows = 32;   // row tile of the streamed grams
+constexpr int kGramBlk = 4;     // upper-triangle 4 x 4 output blocks per thread (s <= 160 at 256 threads)
+
+// dst (s x s, ld) = src^T src over nrows rows of src (row stride lds, first s
+// columns), full symmetric.  Rows stream once through ``tile`` (kGramRows x
+// s4 doubles); thread t accumulates the upper-triangle 4 x 4 output blocks t,
+// t + nt, ... in registers, each summed in row order.
+DP2_DEV void gram_cols_cta(const double* src, int64_t nrows, int lds, int s, double* dst, int ld, double* tile) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nb4 = (s + 3) / 4, s4 = nb4 * 4, nbt = nb4 * (nb4 + 1) / 2;
+  int bi[kGramBlk], bj[kGramBlk];
+#pragma unroll
+  for (int m = 0; m < kGramBlk; ++m) {
+    const int e = tid + m * nt;
+    bi[m] = -1;
+    bj[m] = 0;
+    if (e < nbt) {
+      int a = 0, rem = e;
+      while (rem >= nb4 - a) {
+        rem -= nb4 - a;
+        ++a;
+      }
+      bi[m] = a;
+      bj[m] = a + rem;
+    }
+  }
+  double acc[kGramBlk][16];
+#pragma unroll
+  for (int m = 0; m < kGramBlk; ++m)
+#pragma unroll
+    for (int x = 0; x < 16; ++x) acc[m][x] = 0.0;
+  for (int64_t r0 = 0; r0 < nrows; r0 += kGramRows) {
+    const int rr = (int)(nrows - r0 < kGramRows ? nrows - r0 : kGramRows);
+    __syncthreads();
+    for (int i = tid; i < kGramRows * s4; i += nt) {
+      const int r = i / s4, c = i - r * s4;
+      tile[i] = (r < rr && c < s) ? src[(r0 + r) * lds + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < kGramBlk; ++m) {
+      if (bi[m] < 0) continue;
+      const double* ta = tile + bi[m] * 4;
+      const double* tb = tile + bj[m] * 4;
+      for (int r = 0; r < rr; ++r) {
+        const double2 a01 = *reinterpret_cast<const double2*>(ta + r * s4);
+        const double2 a23 = *reinterpret_cast<const double2*>(ta + r * s4 + 2);
+        const double2 b01 = *reinterpret_cast<const double2*>(tb + r * s4);
+        const double2 b23 = *reinterpret_cast<const double2*>(tb + r * s4 + 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[m][x * 4 + y] = fma(av[x], bv[y], acc[m][x * 4 + y]);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < kGramBlk; ++m) {
+    if (bi[m] < 0) continue;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int a = bi[m] * 4 + x, b = bj[m] * 4 + y;
+        if (a < s && b < s) {
+          dst[a * ld + b] = acc[m][x * 4 + y];
+          dst[b * ld + a] = acc[m][x * 4 + y];
+        }
+      }
+  }
+  __syncthreads();
+}
+
+__host__ __device__ inline size_t factor_smem_bytes(int s) {
+  return (2 * (size_t)s * (s + 1) + (size_t)kGramRows * ((s + 3) / 4 * 4) + 4 * (size_t)s + 8) * 8;
+}
+
 __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  extern __shared__ __align__(16) double fsm[];
+  const int k = blockIdx.x, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   const int J = prm.J, sp = prm.sp, R = prm.R, s = prm.s_k[k];
-  const int ld = sp + 1;
-  double* base = prm.use_smem ? reinterpret_cast<double*>(smem_raw)
-                              : prm.scr + (size_t)k * (3 * (size_t)sp * ld + 4 * sp);
-  double* G = base;
-  double* CC = G + sp * ld;
-  double* W = CC + sp * ld;
-  double* lam = W + sp * ld;       // sp
-  double* cs = lam + sp;           // 3*(sp/2+1) <= 2 sp + 3
+  const int ld = s + 1;
+  const bool in_smem = factor_smem_bytes(s) <= (size_t)prm.smem_bytes;
+  double* gscr = prm.scr + (size_t)k * (3 * (size_t)sp * (sp + 1) + 4 * sp);
+  double* A = in_smem ? fsm : gscr;
+  double* B = A + (size_t)s * ld;
+  double* tile = in_smem ? B + (size_t)s * ld : fsm;          // kGramRows x s4
+  double* lam = tile + (size_t)kGramRows * ((s + 3) / 4 * 4);  // s
+  double* cs = lam + s;                                        // 3*(s/2+1)
+  double* Tg = gscr + 2 * (size_t)sp * (sp + 1);               // s x s (ld = s), global: T = W[:, perm] / sqrt(lam)
   __shared__ int perm[160];
   __shared__ int flag;
-  __shared__ double red[32];
-  __shared__ double tile[1056];
+  __shared__ double Sloc[64];
 
   // 1. C^T = sum of piece partials
   const int p0 = prm.slice_piece[k], p1 = prm.slice_piece[k + 1];
@@ -340,94 +451,90 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
     for (int p = p0; p < p1; ++p) acc += prm.part[(size_t)p * J * sp + i];
     Ct[i] = acc;
   }
-  // 2./3. G = Y^T Y over the slice rows, CC = C C^T over J: upper triangles
-  const int ntri = s * (s + 1) / 2;
-  auto tri = [&](int e, int& a, int& b) {  // e -> (a <= b)
-    a = 0;
-    int rem = e;
-    while (rem >= s - a) { rem -= s - a; ++a; }
-    b = a + rem;
-  };
   __syncthreads();
-  for (int which = 0; which < 2; ++which) {
-    const double* src = which == 0 ? prm.y2 + prm.row_off[k] * sp : Ct;
-    const int64_t nrows = which == 0 ? prm.row_off[k + 1] - prm.row_off[k] : J;
-    double* dst = which == 0 ? G : CC;
-    for (int e0 = 0; e0 < ntri; e0 += nt) {
-      const int e = e0 + tid;
-      int a = 0, b = 0;
-      if (e < ntri) tri(e, a, b);
-      double acc = 0.0;
-      const int trows = max(1, 1056 / max(s, 1));
-      for (int64_t r0 = 0; r0 < nrows; r0 += trows) {
-        const int rr = (int)(nrows - r0 < trows ? nrows - r0 : trows);
-        __syncthreads();
-        for (int i = tid; i < rr * s; i += nt) tile[i] = src[(r0 + i / s) * sp + (i % s)];
-        __syncthreads();
-        if (e < ntri)
-          for (int r = 0; r < rr; ++r) acc = fma(tile[r * s + a], tile[r * s + b], acc);
-      }
-      if (e < ntri) { dst[a * ld + b] = acc; dst[b * ld + a] = acc; }
-    }
-    __syncthreads();
-  }
-  // 4. eig(G) -> W, lambda (descending)
-  int sw = jacobi_eig_block(G, ld, W, ld, s, cs, &flag);
+  // 2. G = Y^T Y over the slice rows (A); 3. eig(G) -> eigenvectors (B), lambda (descending)
+  gram_cols_cta(prm.y2 + prm.row_off[k] * sp, prm.row_off[k + 1] - prm.row_off[k], sp, s, A, ld, tile);
+  int sw = jacobi_eig_block(A, ld, B, ld, s, cs, &flag);
   if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
-  sort_desc_perm(G, ld, s, perm);
-  for (int i = tid; i < s; i += nt) lam[i] = G[perm[i] * ld + perm[i]];
+  sort_desc_perm(A, ld, s, perm);
+  for (int i = tid; i < s; i += nt) lam[i] = A[perm[i] * ld + perm[i]];
   __syncthreads();
-  // T = W[:, perm] / sqrt(lambda) for lambda > tau * lambda_max  (into G)
+  // T = W[:, perm] / sqrt(lambda) for lambda > tau * lambda_max (global Tg, s x rp, ld s)
   const double lmax = lam[0] > 0.0 ? lam[0] : 0.0;
   int rp = 0;
   for (int i = 0; i < s; ++i) rp += (lam[i] > 1e-13 * lmax && lam[i] > 0.0) ? 1 : 0;
-  for (int i = tid; i < s * s; i += nt) {
-    const int a = i / s, c = i % s;
-    G[a * ld + c] = c < rp ? W[a * ld + perm[c]] / sqrt(lam[c]) : 0.0;
+  for (int i = tid; i < s * rp; i += nt) {
+    const int a = i / rp, c = i - a * rp;
+    Tg[a * s + c] = B[a * ld + perm[c]] / sqrt(lam[c]);
   }
   __syncthreads();
-  // tmp = CC T (s x rp) into W, then Bg = T^T tmp (rp x rp) into CC
-  for (int i = tid; i < s * rp; i += nt) {
-    const int a = i / rp, c = i % rp;
+  // 4. CC = C C^T over J (A), then tmp = CC T in place (A[:, :rp]), 4 rows per warp pass
+  gram_cols_cta(Ct, J, sp, s, A, ld, tile);
+  for (int a0 = warp * 4; a0 < s; a0 += nw * 4) {
+    double o[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) o[x][m] = 0.0;
+    for (int b = 0; b < s; ++b) {
+      double t[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int c = lane + 32 * m;
+        t[m] = c < rp ? Tg[b * s + c] : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const double cab = a0 + x < s ? A[(a0 + x) * ld + b] : 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) o[x][m] = fma(cab, t[m], o[x][m]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int c = lane + 32 * m;
+        if (a0 + x < s && c < rp) A[(a0 + x) * ld + c] = o[x][m];
+      }
+    __syncwarp();
+  }
+  __syncthreads();
+  // Bg = T^T tmp (rp x rp, B), symmetrised
+  for (int i = tid; i < rp * rp; i += nt) {
+    const int a = i / rp, c = i - a * rp;
     double acc = 0.0;
-    for (int b = 0; b < s; ++b) acc = fma(CC[a * ld + b], G[b * ld + c], acc);
-    W[a * ld + c] = acc;
+    for (int b = 0; b < s; ++b) acc = fma(Tg[b * s + a], A[b * ld + c], acc);
+    B[a * ld + c] = acc;
   }
   __syncthreads();
   for (int i = tid; i < rp * rp; i += nt) {
-    const int a = i / rp, c = i % rp;
-    double acc = 0.0;
-    for (int b = 0; b < s; ++b) acc = fma(G[b * ld + a], W[b * ld + c], acc);
-    CC[a * ld + c] = acc;
-  }
-  __syncthreads();
-  for (int i = tid; i < rp * rp; i += nt) {  // symmetrise
-    const int a = i / rp, c = i % rp;
+    const int a = i / rp, c = i - a * rp;
     if (a < c) {
-      const double m = 0.5 * (CC[a * ld + c] + CC[c * ld + a]);
-      CC[a * ld + c] = m;
-      CC[c * ld + a] = m;
+      const double m = 0.5 * (B[a * ld + c] + B[c * ld + a]);
+      B[a * ld + c] = m;
+      B[c * ld + a] = m;
     }
   }
   __syncthreads();
-  sw = jacobi_eig_block(CC, ld, W, ld, rp, cs, &flag);
+  sw = jacobi_eig_block(B, ld, A, ld, rp, cs, &flag);
   if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
-  sort_desc_perm(CC, ld, rp, perm);
+  sort_desc_perm(B, ld, rp, perm);
   // 5. P = T U[:, :R], S = sqrt(mu)
   double* Pk = prm.Pm + (size_t)k * sp * R;
   double* Sk = prm.Sv + (size_t)k * R;
   for (int i = tid; i < sp * R; i += nt) {
-    const int a = i / R, r = i % R;
+    const int a = i / R, r = i - a * R;
     double acc = 0.0;
     if (a < s && r < rp) {
       const int col = perm[r];
-      for (int b = 0; b < rp; ++b) acc = fma(G[a * ld + b], W[b * ld + col], acc);
+      for (int b = 0; b < rp; ++b) acc = fma(Tg[a * s + b], A[b * ld + col], acc);
     }
     Pk[a * R + r] = acc;
   }
-  __shared__ double Sloc[64];
   for (int r = tid; r < R; r += nt) {
-    const double mu = r < rp ? CC[perm[r] * ld + perm[r]] : 0.0;
+    const double mu = r < rp ? B[perm[r] * ld + perm[r]] : 0.0;
     Sloc[r] = mu > 0.0 ? sqrt(mu) : 0.0;
     Sk[r] = Sloc[r];
   }
@@ -888,13 +995,14 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   fp.J = J;
   fp.sp = sp;
   fp.R = R;
-  const size_t fsm = (3 * (size_t)sp * (sp + 1) + 4 * sp) * 8;
-  fp.use_smem = fsm <= 200 * 1024;  // sp <= 64 (R <= 32 at p = R); beyond, global scratch
-  if (fp.use_smem) {
-    e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    if (e != cudaSuccess) return e;
-  }
-  factor_kernel<<<K, 256, fp.use_smem ? fsm : 0, stream>>>(fp);
+  // the two work matrices in shared memory for every s up to sp when they fit
+  // (s <= ~105), else per slice in the global scratch (the gram tile stays)
+  size_t fsm = factor_smem_bytes(sp);
+  if (fsm > 210 * 1024) fsm = 210 * 1024;
+  fp.smem_bytes = (int)fsm;
+  e = cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  if (e != cudaSuccess) return e;
+  factor_kernel<<<K, 256, fsm, stream>>>(fp);
   if (timing) cudaEventRecord(ev[4], stream);
   RowsParams rp{};
   rp.y2 = y2;

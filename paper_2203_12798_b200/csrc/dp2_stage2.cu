@@ -236,7 +236,7 @@ DP2_DEV bool eig_reg_any(double* A, int s, double* U) {
 // single block: eig(BB) -> E, D = Q2 U_R with the sign rule, Uf = U_R * sign / E
 __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, const double* Q2, int64_t J,
                                                             int R, double* D, double* E, double* Uf,
-                                                            double* Ubuf, int64_t* status) {
+                                                            double* Ubuf, int64_t* status, int eig_smem) {
   __shared__ double cs[3 * 80];
   __shared__ int flag;
   __shared__ int perm[160];
@@ -253,8 +253,25 @@ __global__ void __launch_bounds__(256) stage2_final_kernel(double* BB, int s, co
   }
   __syncthreads();
   if (!reg_ok) {
-    const int sw = jacobi_eig_block(BB, s, Ubuf, s, s, cs, &flag);
+    // block Jacobi on shared-memory copies (ld s + 1) when they fit (s2 <= ~110)
+    extern __shared__ __align__(16) double esm[];
+    const bool in_sm = (size_t)2 * s * (s + 1) * 8 <= (size_t)eig_smem;
+    double* A = in_sm ? esm : BB;
+    double* U = in_sm ? esm + (size_t)s * (s + 1) : Ubuf;
+    const int la = in_sm ? s + 1 : s;
+    if (in_sm) {
+      for (int e = tid; e < s * s; e += nt) A[(e / s) * la + e % s] = BB[e];
+      __syncthreads();
+    }
+    const int sw = jacobi_eig_block(A, la, U, la, s, cs, &flag);
     if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+    if (in_sm) {
+      for (int e = tid; e < s * s; e += nt) {
+        BB[e] = A[(e / s) * la + e % s];
+        Ubuf[e] = U[(e / s) * la + e % s];
+      }
+      __syncthreads();
+    }
   }
   sort_desc_perm(BB, s, s, perm);
   for (int r = tid; r < R; r += nt) {
@@ -421,7 +438,7 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
     }
     if (q % 2 == 0) cudaMemcpyAsync(Y2, Y, (size_t)J * s2 * 8, cudaMemcpyDeviceToDevice, st);
   }
-  if (!run_orth2(Y2, J, s2, st)) cgs2_kernel<<<1, 256, 0, st>>>(Y2, J, s2, s2, 0);
+  if (!run_orth2(Y2, J, s2, st)) cgs2_cols_kernel<<<1, 256, 0, st>>>(Y2, J, s2, Y);  // Y is dead: column-major copy
   tn(Y2, C);
   // BB = C^T C (s2 x s2): split over the KR rows of C, ordered reduction
   {
@@ -430,7 +447,15 @@ cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* ome
     tn_dmma_kernel<<<dim3((unsigned)((s2 + 63) / 64), ms, ng), 256, 0, st>>>(C, s2, KR, s2, C, s2, s2, mc, parts);
     reduce_parts_kernel<<<(s2 * s2 + 255) / 256, 256, 0, st>>>(parts, ms, (int64_t)s2 * s2, BB);
   }
-  stage2_final_kernel<<<1, 256, 0, st>>>(BB, s2, Y2, J, R, D, E, Uf, Ubuf, status);
+  {
+    const size_t esm = (size_t)2 * s2 * (s2 + 1) * 8;
+    const int eb = esm <= 200 * 1024 ? (int)esm : 0;
+    if (eb) {
+      const cudaError_t ea = cudaFuncSetAttribute(stage2_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, eb);
+      if (ea != cudaSuccess) return ea;
+    }
+    stage2_final_kernel<<<1, 256, eb, st>>>(BB, s2, Y2, J, R, D, E, Uf, Ubuf, status, eb);
+  }
   f_kernel<<<(unsigned)imin64((KR * R + 255) / 256, 4096), 256, 0, st>>>(C, KR, s2, Uf, R, F);
   return cudaGetLastError();
 }
