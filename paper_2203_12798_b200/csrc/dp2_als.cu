@@ -3,8 +3,9 @@
 // One iteration = 9 stream-ordered, graph-capturable launches:
 //   rotate  (warp/slice) T_k = (F_k cc) diag(w_k) H^T; polar Pi_k = Z_k P_k^T by
 //           one-sided Jacobi warm-started from the previous iteration's P_k;
-//           Theta_k = Pi_k^T F_k; mode-1 and gram(W) partials.  32 < R <= 56:
-//           one CTA per slice (CTA-parallel Jacobi rounds, cold start)
+//           Theta_k = Pi_k^T F_k; mode-1 and gram(W) partials.  16 < R <= 56:
+//           one CTA per slice, polar factor by Newton-Schulz on DMMA R x R
+//           matmuls (CTA-parallel Jacobi fallback)
 //   reduce  (n/32 CTAs)  ordered sum of the per-CTA mode-1 / gram(W) slots
 //   solve_h (1 CTA)      H = G1 pinv(W'W * V'V); column norms -> nh
 //   mode2   (warp/slice) sum_k (w_k nh) (Theta_k^T H), gram(W nh) partials
@@ -395,126 +396,341 @@ __host__ __device__ inline size_t rotate_cta_doubles(int R) {
          (size_t)(R + 1) * (R + 2) / 4 + 1 /* pair table */;
 }
 
-// One CTA per slice, 32 < R <= 56: T_k = (F_k cc) diag(w_k) H^T
-// (P/solver.py:55-58), its polar factor U V^T by the CTA-parallel one-sided
-// Jacobi SVD (with the orthonormal completion of warp_polar for singular
-// T_k), Theta_k = Pi_k^T F_k, and the mode-1 partials into this CTA's slots.
-// Shared memory is trimmed to ~2 (R^2 + R (R + 1)) doubles (cc and H are read
-// through L1; Th, T and Theta share the Jacobi buffers) so two CTAs fit per SM
-// -- the Jacobi rounds are latency-bound.  Cold start every iteration: the
-// previous right factor does not shorten the sweeps here (T_k's small
-// singular values are clustered and their vectors move between iterations).
-__global__ void __launch_bounds__(256) als_rotate_cta_kernel(SliceArgs a, AlsBufs b) {
+// Polar factor of the R x R matrix T (row-major, ld R, in shared memory) by
+// the CTA-parallel one-sided Jacobi SVD T V = Z Sigma (round-robin pairs over
+// the warps, each pair's dot products and updates over 8 lanes), with the
+// orthonormal completion of warp_polar for a (numerically) singular T:
+// Pi = Z V^T (row-major, ld R).  Ts / Vr: R x (R + 1) scratch; nrm: R + 16
+// doubles (flag after them); pt: the round-robin pair table.  The fallback of
+// als_rotate_ns_kernel (R <= 56).
+DP2_DEV void cta_polar_jacobi(const double* T, double* Pi, double* Ts, double* Vr, double* nrm, int* flag,
+                              const int* pt, int R, int64_t k, int64_t* status) {
+  const int RR = R * R, ldt = R + 1, tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < RR; e += nt) {  // columns of T, V = I
+    const int c = e / R, i = e - c * R;
+    Ts[c * ldt + i] = T[i * R + c];
+    Vr[c * ldt + i] = c == i ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int sw = jacobi_onesided_cta(Ts, ldt, Vr, ldt, R, pt, flag);
+  if (sw > 60 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
+  for (int i = tid >> 5; i < R; i += nt >> 5) {  // column norms
+    double sq = 0.0;
+    for (int d = tid & 31; d < R; d += 32) sq = fma(Ts[i * ldt + d], Ts[i * ldt + d], sq);
+    sq = warp_sum(sq);
+    if ((tid & 31) == 0) nrm[i] = sqrt(sq);
+  }
+  __syncthreads();
+  for (int e = tid; e < RR; e += nt) {
+    const int i = e / R, d = e - i * R;
+    const double n = nrm[i];
+    Ts[i * ldt + d] = n > 1e-300 ? Ts[i * ldt + d] / n : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {  // (numerically) singular T_k: complete Z orthonormally, as warp_polar
+    for (int i = 0; i < R; ++i) {
+      if (nrm[i] > 1e-300) continue;
+      for (int t = 0; t < R; ++t) {
+        double* z = Ts + i * ldt;
+        for (int d = 0; d < R; ++d) z[d] = (d == t) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int c = 0; c < R; ++c) {
+            if (c == i || !(nrm[c] > 1e-300)) continue;
+            double dd = 0.0;
+            for (int d = 0; d < R; ++d) dd = fma(Ts[c * ldt + d], z[d], dd);
+            for (int d = 0; d < R; ++d) z[d] = fma(-dd, Ts[c * ldt + d], z[d]);
+          }
+        double n2 = 0.0;
+        for (int d = 0; d < R; ++d) n2 = fma(z[d], z[d], n2);
+        if (n2 > 0.25) {
+          const double inv = 1.0 / sqrt(n2);
+          for (int d = 0; d < R; ++d) z[d] *= inv;
+          nrm[i] = 1.0;
+          break;
+        }
+      }
+      if (!(nrm[i] > 1e-300)) status_min(status, ST_POLAR, k);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < RR; e += nt) {  // Pi[d][c] = sum_i Z[d][i] V[c][i]
+    const int d = e / R, c = e - d * R;
+    double s = 0.0;
+    for (int i = 0; i < R; ++i) s = fma(Ts[i * ldt + d], Vr[i * ldt + c], s);
+    Pi[e] = s;
+  }
+  __syncthreads();
+}
+
+// ---- CTA matmuls on the fp64 tensor pipe (DMMA m8n8k4) for 16 < R <= 56.
+// Square NP x NP operands (NP = R rounded up to 8), C = op(A) op(B); shared
+// operands are zero-padded to NP with row stride ld = 4 (mod 16) doubles
+// (conflict-free fragment loads), global operands (ld R) are read with
+// predicates.  Warp w owns the 8 x 8 output tiles w, w + 8, ... (two at a
+// time: independent accumulator chains); every lane calls epi(m, n, c0, c1)
+// for its elements (m, n), (m, n + 1) -- the ownership is static, so
+// per-element read-modify-writes across calls are race-free.
+__host__ __device__ inline bool rot_ns(int R) { return R > 16 && R <= 56; }  // als_rotate_ns_kernel range
+__host__ __device__ inline int ns_np(int R) { return (R + 7) & ~7; }
+__host__ __device__ inline int ns_ld(int R) { return ((ns_np(R) + 15) & ~15) + 4; }
+__host__ __device__ inline size_t rotate_ns_doubles(int R) {
+  const size_t mat = (size_t)ns_np(R) * ns_ld(R), ns = 3 * mat + 32, jac = rotate_cta_doubles(R) + (size_t)R * R;
+  return ns > jac ? ns : jac;
+}
+
+template <bool TA, bool GA, bool TB, bool GB>
+struct MmOp {
+  const double* A;
+  int lda;
+  const double* B;
+  int ldb;
+  int R;
+  DP2_DEV double a(int m, int k) const {
+    if (GA && (m >= R || k >= R)) return 0.0;
+    return TA ? A[k * lda + m] : A[m * lda + k];
+  }
+  DP2_DEV double b(int k, int n) const {
+    if (GB && (k >= R || n >= R)) return 0.0;
+    return TB ? B[n * ldb + k] : B[k * ldb + n];
+  }
+};
+
+// A = X (shared, ld), B = Y = a (3I - a^2 S) / 2 from the shared S (scaled
+// Newton-Schulz step)
+struct MmOpY {
+  const double* X;
+  const double* S;
+  int ld, R;
+  double sa, sa2;
+  DP2_DEV double a(int m, int k) const { return X[m * ld + k]; }
+  DP2_DEV double b(int k, int n) const { return sa * ((k == n && k < R ? 1.5 : 0.0) - 0.5 * sa2 * S[k * ld + n]); }
+};
+
+template <int NP, class Op, class Epi>
+DP2_DEV void cta_mm(const Op& op, Epi epi) {  // 256 threads; warp w owns tiles w, w + 8, ...
+  constexpr int NT = NP / 8, NTILES = NT * NT, MT = (NTILES + 7) / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  double c[MT][2];
+  int m0[MT], n0[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int t = warp + 8 * i < NTILES ? warp + 8 * i : 0;
+    m0[i] = (t / NT) * 8;
+    n0[i] = (t % NT) * 8;
+    c[i][0] = c[i][1] = 0.0;
+  }
+  // all of the warp's tiles at once: MT independent accumulator chains
+#pragma unroll 2
+  for (int k0 = 0; k0 < NP; k0 += 4) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+      if (warp + 8 * i < NTILES) dmma_8x8x4(c[i][0], c[i][1], op.a(m0[i] + r, k0 + q), op.b(k0 + q, n0[i] + r));
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+    if (warp + 8 * i < NTILES) epi(m0[i] + r, n0[i] + 2 * q, c[i][0], c[i][1]);
+}
+
+// One CTA per slice (CTA-strided), 16 < R <= 56: T_k = (F_k cc) diag(w_k) H^T
+// (P/solver.py:55-58) and its orthogonal polar factor Pi_k = Z_k P_k^T -- the
+// only part of SVD(T_k) the reference consumes (P/solver.py:59, :71) -- by
+// the Newton-Schulz iteration X <- X (3I - X^T X) / 2 from X0 = T / sqrt(m),
+// m = min(||T^T T||_1, ||T^T T||_F) >= sigma_max^2 (so every singular value
+// of X0 is in (0, 1]): R x R matmuls on the fp64 tensor pipe only, no
+// divisions or data-dependent rotations on the critical path.  It stops when
+// ||I - X^T X||_F < 1e-12 after one more step (quadratic convergence: the
+// result is orthogonal to rounding).  A singular or extremely ill-conditioned
+// T_k (no convergence in 100 steps) falls back to the CTA-parallel one-sided
+// Jacobi with orthonormal completion (cta_polar_jacobi).  Then Theta_k =
+// Pi_k^T F_k (P/solver.py:67-75) and the mode-1 partials into this CTA's
+// slots (ordered by slice within the CTA).
+template <int NP>
+__global__ void __launch_bounds__(256, 2) als_rotate_ns_kernel(SliceArgs a, AlsBufs b) {
   if (b.ctl[0]) return;
   extern __shared__ __align__(16) double sm[];
-  const int R = a.R, RR = R * R, ldt = R + 1, tid = threadIdx.x, nt = blockDim.x;
+  constexpr int LD = ((NP + 15) & ~15) + 4;
+  const int R = a.R, RR = R * R, tid = threadIdx.x, nt = blockDim.x;
+  const size_t MAT = (size_t)NP * LD;
+  double* X = sm;
+  double* S = X + MAT;
+  double* Xn = S + MAT;
+  double* red = Xn + MAT;  // [1] col-sum max, [2] ||S||_F^2, [4 + (it & 1)] ||I - S||_F^2 of step it
   const double* __restrict__ cc = b.cc;
   const double* __restrict__ H = a.H;
-  double* Fs = sm;
-  double* Pi = Fs + RR;  // T, then the polar factor
-  double* Ts = Pi + RR;  // Th (row-major, before the Jacobi), the columns of T V, then Theta
-  double* Vr = Ts + R * ldt;
-  double* nrm = Vr + R * ldt;
-  int* flag = reinterpret_cast<int*>(nrm + R + 8);
-  int* pt = flag + 16;
-  rr_pair_table(R, pt);
   double* acc1 = a.mode1 ? b.s_g1 + (size_t)blockIdx.x * RR : nullptr;  // this CTA's partial slots
   double* acc2 = a.mode1 ? b.s_wtw + (size_t)blockIdx.x * RR : nullptr;
   if (a.mode1)
     for (int e = tid; e < RR; e += nt) acc1[e] = acc2[e] = 0.0;
+  for (int e = tid; e < 3 * (int)MAT; e += nt) sm[e] = 0.0;  // zero padding stays zero
+  __syncthreads();
   for (int64_t k = blockIdx.x; k < a.K; k += gridDim.x) {
     const double* Fk = a.F + k * RR;
     const double* wk = a.W + k * R;
-    for (int e = tid; e < RR; e += nt) Fs[e] = Fk[e];
+    // Th = (F_k cc) diag(w_k) -> S
+    cta_mm<NP>(MmOp<false, true, false, true>{Fk, R, cc, R, R}, [&](int m, int n, double c0, double c1) {
+      S[m * LD + n] = n < R ? c0 * __ldg(wk + n) : 0.0;
+      S[m * LD + n + 1] = n + 1 < R ? c1 * __ldg(wk + n + 1) : 0.0;
+    });
+    if (tid < 6) red[tid] = 0.0;
     __syncthreads();
-    double* Th = Ts;
-    for (int e = tid; e < RR; e += nt) {  // Th = (F_k cc) * w_k
-      const int i = e / R, c = e - i * R;
-      double s = 0.0;
-      for (int q = 0; q < R; ++q) s = fma(Fs[i * R + q], __ldg(cc + q * R + c), s);
-      Th[e] = s * __ldg(wk + c);
+    // T = Th H^T -> X
+    cta_mm<NP>(MmOp<false, false, true, true>{S, LD, H, R, R}, [&](int m, int n, double c0, double c1) {
+      X[m * LD + n] = c0;
+      X[m * LD + n + 1] = c1;
+    });
+    __syncthreads();
+    // S = T^T T; m = min(max column |.| sum, Frobenius norm) of S >= sigma_max(T)^2
+    cta_mm<NP>(MmOp<true, false, false, false>{X, LD, X, LD, R}, [&](int m, int n, double c0, double c1) {
+      S[m * LD + n] = c0;
+      S[m * LD + n + 1] = c1;
+    });
+    __syncthreads();
+    {
+      double f = 0.0;
+      for (int e = tid; e < NP * NP; e += nt) {
+        const double v = S[(e / NP) * LD + e % NP];
+        f = fma(v, v, f);
+      }
+      f = warp_sum(f);
+      if ((tid & 31) == 0) atomicAdd(red + 2, f);
+      if (tid < NP) {
+        double cs = 0.0;
+        for (int i = 0; i < NP; ++i) cs += fabs(S[i * LD + tid]);
+        atomicMax(reinterpret_cast<unsigned long long*>(red + 1), (unsigned long long)__double_as_longlong(cs));
+      }
     }
     __syncthreads();
-    for (int e = tid; e < RR; e += nt) {  // T = Th H^T
-      const int i = e / R, d = e - i * R;
-      double s = 0.0;
-      for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], __ldg(H + d * R + c), s);
-      Pi[e] = s;
+    const double mb = fmin(red[1], sqrt(red[2]));
+    bool done = false;
+    if (mb > 0.0 && isfinite(mb)) {
+      const double al = 1.0 / sqrt(mb), al2 = 1.0 / mb;
+      for (int e = tid; e < NP * NP; e += nt) {  // X0 = al T, S0 = X0^T X0
+        const int i = e / NP, j = e % NP;
+        X[i * LD + j] *= al;
+        S[i * LD + j] *= al2;
+      }
+      __syncthreads();
+      double* Xc = X;
+      double* Xo = Xn;
+      bool last = false;
+      // scaled Newton-Schulz (the optimally scaled cubic of Chen & Chow):
+      // with every singular value of X in [lb, 1], X <- a X (3I - a^2 X^T X) / 2,
+      // a^2 = 3 / (1 + lb + lb^2), maps [lb, 1] into [lb', 1],
+      // lb' = a lb (3 - a^2 lb^2) / 2 (~2.6 lb for small lb against 1.5 lb
+      // unscaled).  lb starts at 1e-7 (a smaller true sigma_min only grows more
+      // slowly) and is raised to the bound sqrt(1 - ||I - X^T X||_F) once
+      // that is < 1, so the last steps are the plain quadratic iteration.
+      double lb = 1e-7;
+      for (int it = 0; it < 100; ++it) {
+        const double a2 = 3.0 / (1.0 + lb + lb * lb), a = sqrt(a2);
+        // Xo = Xc Y, Y = a (3I - a^2 S) / 2 formed in the fragment loads
+        cta_mm<NP>(MmOpY{Xc, S, LD, R, a, a2}, [&](int m, int n, double c0, double c1) {
+          Xo[m * LD + n] = c0;
+          Xo[m * LD + n + 1] = c1;
+        });
+        __syncthreads();
+        // every thread has read the previous step's error: recycle its slot
+        if (tid == 0) red[4 + ((it + 1) & 1)] = 0.0;
+        lb = fmin(1.0, 0.5 * a * lb * (3.0 - a2 * lb * lb));
+        double* t = Xc;
+        Xc = Xo;
+        Xo = t;
+        if (last) { done = true; break; }
+        // S = Xc^T Xc, with ||I - S||_F^2
+        double ep = 0.0;
+        cta_mm<NP>(MmOp<true, false, false, false>{Xc, LD, Xc, LD, R}, [&](int m, int n, double c0, double c1) {
+          const double d0 = (m == n && m < R ? 1.0 : 0.0) - c0, d1 = (m == n + 1 && m < R ? 1.0 : 0.0) - c1;
+          ep = fma(d0, d0, fma(d1, d1, ep));
+          S[m * LD + n] = c0;
+          S[m * LD + n + 1] = c1;
+        });
+        ep = warp_sum(ep);
+        if ((tid & 31) == 0) atomicAdd(red + 4 + (it & 1), ep);
+        __syncthreads();
+        const double e2 = red[4 + (it & 1)];
+        if (!isfinite(e2)) break;
+        if (e2 < 1.0) lb = fmax(lb, sqrt(1.0 - sqrt(e2)));
+        if (e2 < 1e-24) last = true;  // one more step squares the error
+#ifdef DP2_NS_DEBUG
+        if (tid == 0 && blockIdx.x < 2 && (it % 5 == 0 || last)) printf("k %lld it %d e2 %.3e lb %.3e\n", (long long)k, it, e2, lb);
+#endif
+      }
+      if (done && Xc != X) {  // result into X
+        for (int e = tid; e < NP * NP; e += nt) X[(e / NP) * LD + e % NP] = Xc[(e / NP) * LD + e % NP];
+        __syncthreads();
+      }
     }
-    __syncthreads();
-    for (int e = tid; e < RR; e += nt) {  // columns of T, V = I
-      const int c = e / R, i = e - c * R;
-      Ts[c * ldt + i] = Pi[i * R + c];
-      Vr[c * ldt + i] = c == i ? 1.0 : 0.0;
+    double* Pi = X;  // polar factor, padded layout (ld LD)
+    if (!done) {     // fallback: T again (row-major, ld R) -> Jacobi -> Pi (ld R) -> padded X
+      double* Tr = sm;
+      double* Pr = Tr + RR;
+      double* Ts = Pr + RR;
+      double* Vr = Ts + R * (R + 1);
+      double* nrm = Vr + R * (R + 1);
+      int* flag = reinterpret_cast<int*>(nrm + R + 8);
+      int* pt = flag + 16;
+      __syncthreads();
+      for (int e = tid; e < RR; e += nt) {  // Th = (F_k cc) diag(w_k) into Pr
+        const int i = e / R, c = e - i * R;
+        double s = 0.0;
+        for (int q = 0; q < R; ++q) s = fma(__ldg(Fk + i * R + q), __ldg(cc + q * R + c), s);
+        Pr[e] = s * __ldg(wk + c);
+      }
+      rr_pair_table(R, pt);
+      __syncthreads();
+      for (int e = tid; e < RR; e += nt) {  // T = Th H^T
+        const int i = e / R, d = e - i * R;
+        double s = 0.0;
+        for (int c = 0; c < R; ++c) s = fma(Pr[i * R + c], __ldg(H + d * R + c), s);
+        Tr[e] = s;
+      }
+      __syncthreads();
+      cta_polar_jacobi(Tr, Pr, Ts, Vr, nrm, flag, pt, R, k, a.status);
+      double pv[(56 * 56 + 255) / 256];
+#pragma unroll
+      for (int u = 0; u < (56 * 56 + 255) / 256; ++u) {
+        const int e = tid + 256 * u;
+        pv[u] = e < RR ? Pr[e] : 0.0;
+      }
+      __syncthreads();
+      for (int e = tid; e < 3 * (int)MAT; e += nt) sm[e] = 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < (56 * 56 + 255) / 256; ++u) {
+        const int e = tid + 256 * u;
+        if (e < RR) X[(e / R) * LD + e % R] = pv[u];
+      }
+      __syncthreads();
     }
+    if (a.polar)
+      for (int e = tid; e < RR; e += nt) a.polar[k * RR + e] = Pi[(e / R) * LD + e % R];
+    // Theta = Pi^T F_k -> S (and out)
+    cta_mm<NP>(MmOp<true, false, false, true>{Pi, LD, Fk, R, R}, [&](int m, int n, double c0, double c1) {
+      S[m * LD + n] = c0;
+      S[m * LD + n + 1] = c1;
+      if (m < R) {
+        if (n < R) a.theta[k * RR + m * R + n] = c0;
+        if (n + 1 < R) a.theta[k * RR + m * R + n + 1] = c1;
+      }
+    });
     __syncthreads();
-    const int sw = jacobi_onesided_cta(Ts, ldt, Vr, ldt, R, pt, flag);
-    if (sw > 60 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.status + ST_SWEEPCAP), 1ull);
-    for (int i = tid >> 5; i < R; i += nt >> 5) {  // column norms
-      double sq = 0.0;
-      for (int d = tid & 31; d < R; d += 32) sq = fma(Ts[i * ldt + d], Ts[i * ldt + d], sq);
-      sq = warp_sum(sq);
-      if ((tid & 31) == 0) nrm[i] = sqrt(sq);
-    }
-    __syncthreads();
-    for (int e = tid; e < RR; e += nt) {
-      const int i = e / R, d = e - i * R;
-      const double n = nrm[i];
-      Ts[i * ldt + d] = n > 1e-300 ? Ts[i * ldt + d] / n : 0.0;
-    }
-    __syncthreads();
-    if (tid == 0) {  // (numerically) singular T_k: complete Z orthonormally, as warp_polar
-      for (int i = 0; i < R; ++i) {
-        if (nrm[i] > 1e-300) continue;
-        for (int t = 0; t < R; ++t) {
-          double* z = Ts + i * ldt;
-          for (int d = 0; d < R; ++d) z[d] = (d == t) ? 1.0 : 0.0;
-          for (int pass = 0; pass < 2; ++pass)
-            for (int c = 0; c < R; ++c) {
-              if (c == i || !(nrm[c] > 1e-300)) continue;
-              double dd = 0.0;
-              for (int d = 0; d < R; ++d) dd = fma(Ts[c * ldt + d], z[d], dd);
-              for (int d = 0; d < R; ++d) z[d] = fma(-dd, Ts[c * ldt + d], z[d]);
-            }
-          double n2 = 0.0;
-          for (int d = 0; d < R; ++d) n2 = fma(z[d], z[d], n2);
-          if (n2 > 0.25) {
-            const double inv = 1.0 / sqrt(n2);
-            for (int d = 0; d < R; ++d) z[d] *= inv;
-            nrm[i] = 1.0;
-            break;
+    if (a.mode1)  // g1[i][r] += w[k][r] (Theta cc)[i][r];  wtw[i][r] += w[k][i] w[k][r]
+      cta_mm<NP>(MmOp<false, false, false, true>{S, LD, cc, R, R}, [&](int m, int n, double c0, double c1) {
+        if (m < R) {
+          const double wm = __ldg(wk + m);
+          if (n < R) {
+            const double wn = __ldg(wk + n);
+            acc1[m * R + n] += wn * c0;
+            acc2[m * R + n] += wm * wn;
+          }
+          if (n + 1 < R) {
+            const double wn = __ldg(wk + n + 1);
+            acc1[m * R + n + 1] += wn * c1;
+            acc2[m * R + n + 1] += wm * wn;
           }
         }
-        if (!(nrm[i] > 1e-300)) status_min(a.status, ST_POLAR, k);
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < RR; e += nt) {  // Pi[d][c] = sum_i Z[d][i] V[c][i]
-      const int d = e / R, c = e - d * R;
-      double s = 0.0;
-      for (int i = 0; i < R; ++i) s = fma(Ts[i * ldt + d], Vr[i * ldt + c], s);
-      Pi[e] = s;
-      if (a.polar) a.polar[k * RR + e] = s;
-    }
-    __syncthreads();
-    double* Tht = Ts;
-    for (int e = tid; e < RR; e += nt) {  // Theta = Pi^T F
-      const int i = e / R, c = e - i * R;
-      double s = 0.0;
-      for (int d = 0; d < R; ++d) s = fma(Pi[d * R + i], Fs[d * R + c], s);
-      Tht[e] = s;
-      a.theta[k * RR + e] = s;
-    }
-    __syncthreads();
-    if (a.mode1) {  // g1[i][r] += w[k][r] (Theta cc)[i][r];  wtw[i][r] += w[k][i] w[k][r]
-      for (int e = tid; e < RR; e += nt) {
-        const int i = e / R, r = e - i * R;
-        double s = 0.0;
-        for (int q = 0; q < R; ++q) s = fma(Tht[i * R + q], __ldg(cc + q * R + r), s);
-        acc1[e] += __ldg(wk + r) * s;
-        acc2[e] += __ldg(wk + i) * __ldg(wk + r);
-      }
-    }
+      });
     __syncthreads();
   }
 }
@@ -1061,7 +1277,8 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.L = take(K * RR * 2);
   int wr = 0, nr = 0;
   rot_cfg(K, R, wr, nr);
-  const size_t ns = nr > (int)nb ? (size_t)nr : nb;
+  size_t ns = nr > (int)nb ? (size_t)nr : nb;
+  if (rot_ns(R) && ns < 2 * (size_t)sm_count()) ns = 2 * (size_t)sm_count();  // als_rotate_ns_kernel slots
   L.s_g1 = take(ns * RR);
   L.s_wtw = take(ns * RR);
   L.s_m2 = take(nb * RR);
@@ -1119,7 +1336,7 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.nbm = metric_blocks(K, R);
   rot_cfg(K, R, b.wpbr, b.nbr);
   if (b.nbr <= 0) { b.nbr = b.nb; b.wpbr = b.wpb; }
-  if (R > 32 && R <= 56) {  // als_rotate_cta_kernel: two CTAs per SM, CTA-strided slices
+  if (rot_ns(R)) {  // als_rotate_ns_kernel: two CTAs per SM, CTA-strided slices
     const int64_t cap = 2 * (int64_t)sm_count();
     b.nbr = (int)(K < cap ? K : cap);
     b.wpbr = 8;
@@ -1192,11 +1409,19 @@ cudaError_t launch_rotate(const SliceArgs& a, const AlsBufs& b, cudaStream_t st,
     DP2_ROT_CASE(13) DP2_ROT_CASE(14) DP2_ROT_CASE(15) DP2_ROT_CASE(16)
 #undef DP2_ROT_CASE
     default:
-      if (a.R > 32 && a.R <= 56) {  // CTA-parallel Jacobi (R <= ~56)
-        const size_t smc = rotate_cta_doubles(a.R) * 8;
-        if (setattr) return set_smem((const void*)als_rotate_cta_kernel, smc);
-        als_rotate_cta_kernel<<<b.nbr, 256, smc, st>>>(a, b);
-        return cudaGetLastError();
+      if (rot_ns(a.R)) {  // CTA Newton-Schulz on the fp64 tensor pipe (Jacobi fallback)
+        const size_t smc = rotate_ns_doubles(a.R) * 8;
+        const void* f = nullptr;
+        switch (ns_np(a.R)) {
+          case 24: f = (const void*)als_rotate_ns_kernel<24>; break;
+          case 32: f = (const void*)als_rotate_ns_kernel<32>; break;
+          case 40: f = (const void*)als_rotate_ns_kernel<40>; break;
+          case 48: f = (const void*)als_rotate_ns_kernel<48>; break;
+          default: f = (const void*)als_rotate_ns_kernel<56>; break;
+        }
+        if (setattr) return set_smem(f, smc);
+        void* args[] = {(void*)&a, (void*)&b};
+        return cudaLaunchKernel(f, dim3(b.nbr), dim3(256), args, smc, st);
       }
       if (setattr) return set_smem((const void*)als_rotate_kernel, rotate_smem(a.R, b.wpb));
       als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(a.R, b.wpb), st>>>(a, b);

@@ -123,7 +123,7 @@ def test_c2_full_tf32_mode(c2_host):
     print(f"c2 tf32: fitness {fit:.10f} oracle {fit_o:.10f}; errors {errs}")
 
 
-@pytest.mark.parametrize("R", [20, 50])
+@pytest.mark.parametrize("R", [20, 30, 40, 50])
 def test_c4_rank_sweep_oversampling_equals_rank(c2_host, R):
     errs, fit, fit_o = _compare(c2_host, R, 32, "f64", FP64, oversampling=R)
     print(f"c4 R={R}: fitness {fit:.10f} oracle {fit_o:.10f}; errors {errs}")

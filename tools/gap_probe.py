@@ -1,4 +1,4 @@
-"""Device idle gaps inside consecutive warm fit_dpar2 steps (c2 fp32): kernel
+"""Device idle gaps inside consecutive warm fit_dpar2 steps (c2, --dtype f32 or f64): kernel
 intervals from torch.profiler (CUPTI), gaps > 5 us listed with the kernels
 around them -- where the host, not the GPU, sets the pace.
 
@@ -20,8 +20,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--stack", action="store_true", help="list the host calls inside the largest gap")
+    ap.add_argument("--dtype", default="f32")
     a = ap.parse_args()
-    cfg = synth.scaled(synth.CONFIGS["c2"], dtype="f32")
+    cfg = synth.scaled(synth.CONFIGS["c2"], dtype=a.dtype)
     X, rows, _, _ = synth.generate_device(cfg, 0)
     t = dp.IrregularTensor.from_packed(X, rows, cfg.cols)
     opts = dp.SolverOptions(max_iters=32, tol=0.0, seed=0)
