@@ -12,7 +12,7 @@ orthonormal,
 and stage 1 already holds Q_k^T X_k: Q_k = A_k Pi_k with A_k = Y_k P_k and
 C_k = X_k^T Y_k from the second pass, so Q_k^T X_k = Pi_k^T (C_k P_k)^T =
 Pi_k^T M_k^T, M_k the slice's (signed) block of the stage-1 matrix M.  The fit
-keeps M^T V (KR x R, dp2_gemm_tn); the fitness is then R x R work per slice in
+keeps M and forms M^T V (KR x R, dp2_gemm_tn) on the first call; the fitness is then R x R work per slice in
 one library kernel (dp2_fitness_zero_pass), no pass over X (||X_k||^2 comes
 from the tensor's stored slice norms).  Rank-deficient slices
 (completed A_k columns are not Y_k P_k) and fp32 stores (M from tf32
@@ -54,6 +54,12 @@ def _zero_pass_terms(tensor, factors, d):
     K, J = W.shape[0], V.shape[0]
     dev = V.device
     lib = _lib.lib()
+    if zp.get("MtV") is None:  # M^T V (KR x R) on the first call; M is then released
+        M = zp.pop("M")
+        MtV = torch.empty((M.shape[1], R), dtype=torch.float64, device=dev)
+        _lib.check(lib.dp2_gemm_tn(_vp(M), M.shape[0], M.shape[1], _vp(zp["V"]), R, _vp(MtV), stream_ptr()),
+                   "gemm_tn")
+        zp["MtV"] = MtV
     ws = workspace(lib.dp2_zero_pass_workspace(K, R), dev)
     out = torch.empty(2, dtype=torch.float64, device=dev)
     _lib.check(lib.dp2_fitness_zero_pass(_vp(zp["MtV"]), K, J, R, _vp(H), _vp(V), _vp(W), _vp(zp["polar"]),

@@ -18,7 +18,8 @@ import torch
 from . import _lib
 from .errors import NumericFailure, RankTooLargeError
 from .linalg import RsvdParams, derived_seed, padded_width, sketch_width
-from .rng import omega_device, stage2_omega, stage2_omega_finish, stage2_omega_launch  # noqa: F401
+from .rng import (omega_device, omega_device_finish, omega_device_launch, stage2_omega,  # noqa: F401
+                  stage2_omega_finish, stage2_omega_launch)
 from .scheduler import resolve_threads
 from .tensor import IrregularTensor, new_status, sm_count, stream_ptr
 
@@ -160,8 +161,8 @@ def _stage1_setup(tensor, rank, oversampling, dev):
     key = (rank, oversampling)
     if key not in cache:
         from .tensor import to_device_async
-        widths = sketch_widths(tensor.row_counts, tensor.num_cols, rank, oversampling)
-        sp = padded_width(max(widths))
+        widths = np.asarray(sketch_widths(tensor.row_counts, tensor.num_cols, rank, oversampling), dtype=np.int32)
+        sp = padded_width(int(widths.max()))
         cache[key] = (widths, sp, to_device_async(widths, torch.int32, dev))
     return cache[key]
 
@@ -172,31 +173,37 @@ def _uses_tc(sub, sp):
 
 
 def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, timings=None, status=None,
-               speculative=False, a_signs=None):
+               speculative=False, a_signs=None, omega_pre=None):
     """Stage 1 on the device for the tensor's slices (global ids ``slice_ids``
     select the per-slice seeds in a multi-GPU shard).  Returns A (sum I_k x R),
     M (J x K_local R, local slice order) and the per-slice numerical ranks
     (plus, with ``speculative``, the Omega replay check future or None --
     rng.omega_device).  With ``a_signs`` (device K x rank) A is returned up to
-    its column signs, which go to ``a_signs`` (dp2_stage1_signs)."""
+    its column signs, which go to ``a_signs`` (dp2_stage1_signs).
+    ``omega_pre``: an already enqueued exact Omega (rng.omega_device_launch),
+    finished here after the outputs are allocated."""
     J, K = tensor.num_cols, tensor.num_slices
     dev = tensor.X.device
     widths, sp, s_dev = _stage1_setup(tensor, rank, base.oversampling, dev)
     t0 = time.perf_counter()
     rstats = {}
     check = None
-    if speculative and _uses_tc(tensor, sp):
-        omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True,
-                                    s_dev=s_dev)
-    else:
-        omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats, s_dev=s_dev)
-    t_omega = time.perf_counter() - t0
+    if omega_pre is None:
+        if speculative and _uses_tc(tensor, sp):
+            omega, check = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, speculative=True,
+                                        s_dev=s_dev)
+        else:
+            omega = omega_device(base.seed, J, widths, sp, dev, slice_ids=slice_ids, stats=rstats, s_dev=s_dev)
     A = torch.empty((int(tensor.row_off_host[-1]), rank), dtype=torch.float64, device=dev)
     M = torch.empty((J, K * rank), dtype=torch.float64, device=dev)
     rank_found = torch.empty(K, dtype=torch.int32, device=dev)
     status = new_status(dev) if status is None else status
+    prep = _stage1_prep(tensor, sp, rank)
+    if omega_pre is not None:  # the generator ran while the host got here
+        omega = omega_device_finish(omega_pre, stats=rstats)
+    t_omega = time.perf_counter() - t0
     tm = _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timings is not None, a_signs,
-                      base.power_iters)
+                      base.power_iters, prep=prep)
     if timings is not None:
         timings.update(rstats)
         timings.update(omega_host_s=t_omega, stage1_sketch1_ms=tm[0], stage1_orth_ms=tm[1],
@@ -207,14 +214,19 @@ def run_stage1(tensor: IrregularTensor, rank, base: RsvdParams, slice_ids=None, 
     return A, M, rank_found, status
 
 
+def _stage1_prep(tensor, sp, rank):
+    """(store, keepalive, workspace) of a dp2_stage1 call."""
+    st, keep = tensor.store(nseg_for(tensor))
+    ws = workspace(_lib.lib().dp2_stage1_workspace(C.byref(st), sp, rank), tensor.X.device)
+    return st, keep, ws
+
+
 def _stage1_call(tensor, rank, omega, s_dev, sp, A, M, rank_found, status, timed=False, a_signs=None,
-                 power_iters=1):
+                 power_iters=1, prep=None):
     """One dp2_stage1 call over ``tensor``'s slices (omega / s_dev / outputs
     already sliced to them); returns the phase timings when ``timed``."""
-    nseg = nseg_for(tensor)
-    st, keep = tensor.store(nseg)
+    st, keep, ws = prep if prep is not None else _stage1_prep(tensor, sp, rank)
     lib = _lib.lib()
-    ws = workspace(lib.dp2_stage1_workspace(C.byref(st), sp, rank), tensor.X.device)
     tm = (C.c_float * 8)() if timed else None
     if power_iters != 1:
         _lib.check(lib.dp2_stage1_power(C.byref(st), _vp(omega), _vp(s_dev), sp, rank, max(0, int(power_iters)),
@@ -354,15 +366,21 @@ def compress_async(tensor: IrregularTensor, rank, rsvd: RsvdParams | None = None
     resolve_threads(threads)
     base = rsvd if rsvd is not None else RsvdParams(rank=rank)
     J, K = tensor.num_cols, tensor.num_slices
-    second, s2 = stage2_params(base, stage2, rank, K, J)
     spec = not exact_omega
+    chunked = len(tensor._upload_events) > 1
+    pre = None
+    if not chunked:  # the critical path starts with stage 1's Omega: enqueue it first
+        widths, sp, s_dev = _stage1_setup(tensor, rank, base.oversampling, tensor.X.device)
+        if not (spec and _uses_tc(tensor, sp)):
+            pre = omega_device_launch(base.seed, J, widths, sp, tensor.X.device, s_dev=s_dev)
+    second, s2 = stage2_params(base, stage2, rank, K, J)
     # DP2_OMEGA2_HOST=1: draw Omega_2 with NumPy while stage 1 runs (A/B knob)
     om2h = None if _OMEGA2_HOST else stage2_omega_launch(second.seed, K * rank, s2, tensor.X.device)
     a_signs = torch.empty((K, rank), dtype=torch.float64, device=tensor.X.device) if defer_signs else None
-    if len(tensor._upload_events) > 1:
+    if chunked:
         res = run_stage1_chunked(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
     else:
-        res = run_stage1(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs)
+        res = run_stage1(tensor, rank, base, timings=timings, speculative=spec, a_signs=a_signs, omega_pre=pre)
     A, M, rank_found, status = res[:4]
     check = res[4] if len(res) > 4 else None
     # stage-2 Omega (one stream, P/compress.py:109-111): generated on the

@@ -118,6 +118,24 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     background thread; returns ``(omega, future)`` whose result reports
     ``omega_mismatch`` (an acceptance decision differing from the reference's,
     practically never: the caller then recomputes with the exact path)."""
+    h = omega_device_launch(seed, n, widths, sp, device, slice_ids=slice_ids, s_dev=s_dev)
+    if speculative:
+        global _REPLAY_POOL
+        if _REPLAY_POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _REPLAY_POOL = ThreadPoolExecutor(1)
+        bufs = h["bufs"]
+        fut = _REPLAY_POOL.submit(_replay_check, h["ev"], bufs["nrec_h"], bufs["redo_h"], bufs["recs_h"], h["cap"])
+        bufs["busy"] = fut
+        return h["out"], fut
+    return omega_device_finish(h, stats=stats)
+
+
+def omega_device_launch(seed, n, widths, sp, device, slice_ids=None, s_dev=None):
+    """First half of the exact ``omega_device``: enqueue the generator and the
+    readback of its tail records on the current stream, record an event, and
+    return a handle for ``omega_device_finish`` -- the host is free (and the
+    stream can take more work) until the records are needed."""
     import ctypes as C
 
     from . import _lib
@@ -127,7 +145,7 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
     if s_dev is None:
         s_dev = to_device_async(list(widths), torch.int32, device)
     ids = None if slice_ids is None else to_device_async(list(slice_ids), torch.int64, device)
-    cap = max(4096, 8 * K + n * max(widths) * K // 1000)
+    cap = max(4096, 8 * K + n * int(np.max(widths)) * K // 1000)
     bufs = _scratch(device, K, cap)
     recs, nrec, redo = bufs["recs"], bufs["nrec"], bufs["redo"]  # zeroed by dp2_omega_generate
     vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)  # noqa: E731
@@ -135,31 +153,37 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
                                              vp(recs), cap, vp(nrec), vp(redo),
                                              stream_ptr()), "omega")
     # one readback: record count, per-slice redo flags and the records
+    bufs["nrec_h"].copy_(nrec, non_blocking=True)
+    bufs["redo_h"].copy_(redo, non_blocking=True)
+    bufs["recs_h"].copy_(recs, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return dict(out=out, ev=ev, bufs=bufs, cap=cap, seed=seed, n=n, widths=widths, sp=sp, slice_ids=slice_ids,
+                keep=(s_dev, ids))
+
+
+def omega_device_finish(h, stats=None):
+    """Second half of the exact ``omega_device``: wait for the tail records
+    only (the handle's event, not the stream), replay each attempt with the C
+    library's log1p -- the function the reference sampler calls (npy_log1p);
+    NumPy's np.log1p ufunc may use a SIMD implementation with different
+    rounding -- and scatter the exact values into Omega on the stream
+    (dp2_omega_patch).  Slices whose acceptance decision differs, or a record
+    overflow, are regenerated with NumPy (never expected)."""
+    import ctypes as C
+
+    from . import _lib
+    from .tensor import stream_ptr
+    out, bufs, cap, widths, n, sp = h["out"], h["bufs"], h["cap"], h["widths"], h["n"], h["sp"]
+    K = len(widths)
+    h["ev"].synchronize()
     nrec_h, redo_h_t, recs_h = bufs["nrec_h"], bufs["redo_h"], bufs["recs_h"]
-    nrec_h.copy_(nrec, non_blocking=True)
-    redo_h_t.copy_(redo, non_blocking=True)
-    recs_h.copy_(recs, non_blocking=True)
-    if speculative:
-        global _REPLAY_POOL
-        if _REPLAY_POOL is None:
-            from concurrent.futures import ThreadPoolExecutor
-            _REPLAY_POOL = ThreadPoolExecutor(1)
-        ev = torch.cuda.Event()
-        ev.record()
-        fut = _REPLAY_POOL.submit(_replay_check, ev, nrec_h, redo_h_t, recs_h, cap)
-        bufs["busy"] = fut
-        return out, fut
-    torch.cuda.current_stream().synchronize()
     count = int(nrec_h[0])
     redo_h = redo_h_t.numpy().copy()
     if count > cap:
         redo_h[:] = 1  # record overflow: regenerate everything on the host (never expected)
     patched = 0
     if count and count <= cap:
-        # replay each attempt with the C library's log1p -- the function the
-        # reference sampler calls (npy_log1p); NumPy's np.log1p ufunc may use a
-        # SIMD implementation with different rounding -- and scatter the exact
-        # values into Omega on the stream (dp2_omega_patch, host threads + one kernel)
         w32 = widths if isinstance(widths, np.ndarray) and widths.dtype == np.int32 else \
             np.ascontiguousarray(widths, dtype=np.int32)
         npatch = C.c_int32(0)
@@ -170,9 +194,10 @@ def omega_device(seed, n, widths, sp, device, slice_ids=None, stats=None, specul
         patched = int(npatch.value)
     bad = np.nonzero(redo_h)[0]
     if bad.size:
+        slice_ids = h["slice_ids"]
         ids_h = list(range(K)) if slice_ids is None else list(slice_ids)
-        host = omega_host(seed, n, [widths[k] for k in bad], sp, slice_ids=[ids_h[k] for k in bad])
-        out[torch.from_numpy(bad).to(device)] = host.to(device)
+        host = omega_host(h["seed"], n, [widths[k] for k in bad], sp, slice_ids=[ids_h[k] for k in bad])
+        out[torch.from_numpy(bad).to(out.device)] = host.to(out.device)
     if stats is not None:
         stats.update(omega_tail_events=count, omega_patched=patched, omega_host_regenerated=int(bad.size))
     return out

@@ -226,13 +226,10 @@ def fit_dpar2(tensor, rank, opts: SolverOptions | None = None, output="numpy", t
     Q = assemble_q(tensor, comp, launched[3])
     zero_pass = None
     if tensor.dtype == "f64" and output == "device":
-        # M^T V (KR x R) for the fitness without a pass over X (analysis.py); the
-        # fit's V is kept as a private copy so later edits of factors.V are seen
-        V = launched[1]
-        MtV = torch.empty((comp._stage1_M.shape[1], rank), dtype=torch.float64, device=V.device)
-        _lib.check(_lib.lib().dp2_gemm_tn(_vp(comp._stage1_M), comp._stage1_M.shape[0], comp._stage1_M.shape[1],
-                                          _vp(V), rank, _vp(MtV), stream_ptr()), "gemm_tn")
-        zero_pass = dict(MtV=MtV, V=V.clone(), polar=launched[3], rank_found=comp.rank_found,
+        # the stage-1 M is kept for the fitness without a pass over X
+        # (analysis.py: M^T V is formed on the first fitness call); the fit's
+        # V is kept as a private copy so later edits of factors.V are seen
+        zero_pass = dict(M=comp._stage1_M, V=launched[1].clone(), polar=launched[3], rank_found=comp.rank_found,
                          tensor=weakref.ref(tensor))
     comp._stage1_M = None
     q_host = None

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--stack", action="store_true", help="list the host calls inside the largest gap")
     ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--timeline", action="store_true", help="print the device events of the last step with the idle gap before each")
     a = ap.parse_args()
     cfg = synth.scaled(synth.CONFIGS["c2"], dtype=a.dtype)
     X, rows, _, _ = synth.generate_device(cfg, 0)
@@ -56,6 +57,15 @@ def main():
     for (p, n), g in sorted(agg.items(), key=lambda kv: -kv[1])[:25]:
         if g / a.steps > 5:
             print(f"{g / a.steps:9.1f} us/step  after {p:50s} before {n}")
+    if a.timeline:
+        n_per = len(ev) // a.steps
+        last = ev[-n_per:]
+        t0 = last[0].time_range.start
+        prev_end = t0
+        for e in last:
+            gap = e.time_range.start - prev_end
+            print(f"{e.time_range.start - t0:9.1f} +{max(0.0, gap):7.1f} {e.time_range.end - e.time_range.start:8.1f}  {e.name[:70]}")
+            prev_end = max(prev_end, e.time_range.end)
     if a.stack:  # host events overlapping the largest single gap
         big = max(range(len(ev) - 1), key=lambda i: ev[i + 1].time_range.start - ev[i].time_range.end)
         g0, g1 = ev[big].time_range.end, ev[big + 1].time_range.start
