@@ -422,6 +422,42 @@ DP2_DEV void gram_cols_cta(const double* src, int64_t nrows, int lds, int s, dou
   __syncthreads();
 }
 
+// Cholesky G = L L^T of the s x s symmetric matrix in A (lower triangle
+// overwritten by L), one column per step over the CTA; false (uniformly) when
+// a pivot is not above rel_floor * max_i G_ii or not finite.
+DP2_DEV bool cta_chol_lower(double* A, int ld, int s, double rel_floor, int* flag) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ double gmax_s;
+  if (tid == 0) {
+    double g = 0.0;
+    for (int i = 0; i < s; ++i) g = fmax(g, A[i * ld + i]);
+    gmax_s = g;
+    *flag = g > 0.0 && isfinite(g) ? 0 : 1;
+  }
+  __syncthreads();
+  if (*flag) return false;
+  const double floor = rel_floor * gmax_s;
+  for (int j = 0; j < s; ++j) {
+    if (tid == 0) {
+      const double d = A[j * ld + j];
+      if (d > floor && isfinite(d)) A[j * ld + j] = sqrt(d);
+      else *flag = 1;
+    }
+    __syncthreads();
+    if (*flag) return false;
+    const double il = 1.0 / A[j * ld + j];
+    for (int i = j + 1 + tid; i < s; i += nt) A[i * ld + j] *= il;
+    __syncthreads();
+    const int n = s - j - 1;
+    for (int e = tid; e < n * n; e += nt) {  // trailing lower triangle
+      const int i = j + 1 + e / n, c = j + 1 + e % n;
+      if (c <= i) A[i * ld + c] = fma(-A[i * ld + j], A[c * ld + j], A[i * ld + c]);
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 __host__ __device__ inline size_t factor_smem_bytes(int s) {
   return (2 * (size_t)s * (s + 1) + (size_t)kGramRows * ((s + 3) / 4 * 4) + 4 * (size_t)s + 8) * 8;
 }
@@ -454,20 +490,45 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
   __syncthreads();
   // 2. G = Y^T Y over the slice rows (A); 3. eig(G) -> eigenvectors (B), lambda (descending)
   gram_cols_cta(prm.y2 + prm.row_off[k] * sp, prm.row_off[k + 1] - prm.row_off[k], sp, s, A, ld, tile);
-  int sw = jacobi_eig_block(A, ld, B, ld, s, cs, &flag);
-  if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
-  sort_desc_perm(A, ld, s, perm);
-  for (int i = tid; i < s; i += nt) lam[i] = A[perm[i] * ld + perm[i]];
-  __syncthreads();
-  // T = W[:, perm] / sqrt(lambda) for lambda > tau * lambda_max (global Tg, s x rp, ld s)
-  const double lmax = lam[0] > 0.0 ? lam[0] : 0.0;
-  int rp = 0;
-  for (int i = 0; i < s; ++i) rp += (lam[i] > 1e-13 * lmax && lam[i] > 0.0) ? 1 : 0;
-  for (int i = tid; i < s * rp; i += nt) {
-    const int a = i / rp, c = i - a * rp;
-    Tg[a * s + c] = B[a * ld + perm[c]] / sqrt(lam[c]);
+  int rp = 0, sw = 0;
+  // 3. whitening T (Y T orthonormal): T = L^-T from the Cholesky factor of G
+  //    (the small-sketch path's relative pivot floor 1e-13, s sequential
+  //    column steps over the CTA); a rank-deficient sketch (pivot below the
+  //    floor) takes the eigen basis of G instead, dropping lambda <=
+  //    1e-13 lambda_max: T = W[:, perm] / sqrt(lambda)
+  if (cta_chol_lower(A, ld, s, 1e-13, &flag)) {
+    rp = s;
+    for (int c = tid; c < s; c += nt)  // L^-1 by forward substitution, column c per thread, into B
+      for (int i = 0; i < s; ++i) {
+        if (i < c) {
+          B[i * ld + c] = 0.0;
+          continue;
+        }
+        double t = i == c ? 1.0 : 0.0;
+        for (int m = c; m < i; ++m) t = fma(-A[i * ld + m], B[m * ld + c], t);
+        B[i * ld + c] = t / A[i * ld + i];
+      }
+    __syncthreads();
+    for (int i = tid; i < s * s; i += nt) {
+      const int a = i / s, c = i - a * s;
+      Tg[a * s + c] = B[c * ld + a];
+    }
+    __syncthreads();
+  } else {
+    gram_cols_cta(prm.y2 + prm.row_off[k] * sp, prm.row_off[k + 1] - prm.row_off[k], sp, s, A, ld, tile);
+    sw = jacobi_eig_block(A, ld, B, ld, s, cs, &flag);
+    if (sw > 40 && tid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(prm.status + ST_SWEEPCAP), 1ull);
+    sort_desc_perm(A, ld, s, perm);
+    for (int i = tid; i < s; i += nt) lam[i] = A[perm[i] * ld + perm[i]];
+    __syncthreads();
+    const double lmax = lam[0] > 0.0 ? lam[0] : 0.0;
+    for (int i = 0; i < s; ++i) rp += (lam[i] > 1e-13 * lmax && lam[i] > 0.0) ? 1 : 0;
+    for (int i = tid; i < s * rp; i += nt) {
+      const int a = i / rp, c = i - a * rp;
+      Tg[a * s + c] = B[a * ld + perm[c]] / sqrt(lam[c]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // 4. CC = C C^T over J (A), then tmp = CC T in place (A[:, :rp]), 4 rows per warp pass
   gram_cols_cta(Ct, J, sp, s, A, ld, tile);
   for (int a0 = warp * 4; a0 < s; a0 += nw * 4) {
