@@ -155,6 +155,8 @@ __global__ void als_prep_kernel(const double* D, const double* E, const double* 
     if (reset) {
       b.ctl[0] = 0;
       b.ctl[1] = 0;
+      if (b.pwarm)
+        for (int i = 0; i < 3; ++i) b.pwarm[i * (R * R + 8) + R * R] = 0.0;  // no warm pinv bases yet
     }
     if (tstamp) tstamp[0] = (int64_t)globaltimer_ns();
   }
@@ -1069,6 +1071,9 @@ __global__ void __launch_bounds__(256) als_metric_kernel(AlsBufs b, const double
   if (threadIdx.x == 0) b.s_e[blockIdx.x] = tot;
 }
 
+// rows per staged chunk of D / V in als_solve_v_kernel's large-J path (227 KB cap)
+__host__ __device__ inline int solve_v_jt(int R) { return R <= 50 ? 32 : 8; }
+
 struct SolveArgs {
   const double *D, *E;
   double *H, *V, *W;
@@ -1098,7 +1103,7 @@ __global__ void __launch_bounds__(512) als_solve_h_kernel(SolveArgs s, AlsBufs b
     b.WtW[e] = WtW[e];
   }
   __syncthreads();
-  block_pinv_sym(Mh, U, Pv, R, cs, s.status);
+  block_pinv_sym(Mh, U, Pv, R, cs, s.status, b.pwarm);
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, c = e % R;
     double acc = 0.0;
@@ -1157,7 +1162,7 @@ __global__ void __launch_bounds__(512) als_solve_v_kernel(SolveArgs s, AlsBufs b
     b.WtW2[e] = WtW2[e];
   }
   __syncthreads();
-  block_pinv_sym(Mv, U, Pv, R, cs, s.status);
+  block_pinv_sym(Mv, U, Pv, R, cs, s.status, b.pwarm ? b.pwarm + (R * R + 8) : nullptr);
   // V = D (E * summed) pinv = D EP with EP = (E * summed) pinv (R x R), so the
   // J-sized work is one product; D and V stay in smem when they fit
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
@@ -1167,33 +1172,101 @@ __global__ void __launch_bounds__(512) als_solve_v_kernel(SolveArgs s, AlsBufs b
     EP[e] = acc;
   }
   __syncthreads();
-  for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
-    const int64_t j = e / R;
-    const int r = (int)(e % R);
-    double acc = 0.0;
-    for (int q = 0; q < R; ++q) acc = fma(Dp[j * R + q], EP[q * R + r], acc);
-    Vs[e] = acc;
-  }
-  __syncthreads();
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int c = warp; c < R; c += nw) {
-      double part = 0.0;
-      for (int64_t j = lane; j < J; j += 32) part = fma(Vs[j * R + c], Vs[j * R + c], part);
-      const double n = sqrt(warp_sum(part));
-      if (lane == 0) nrm[c] = (s.normalize && !(n < 1e-300)) ? n : 1.0;
+  if (s.dsm) {
+    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
+      const int64_t j = e / R;
+      const int r = (int)(e % R);
+      double acc = 0.0;
+      for (int q = 0; q < R; ++q) acc = fma(Dp[j * R + q], EP[q * R + r], acc);
+      Vs[e] = acc;
     }
+    __syncthreads();
+    {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int c = warp; c < R; c += nw) {
+        double part = 0.0;
+        for (int64_t j = lane; j < J; j += 32) part = fma(Vs[j * R + c], Vs[j * R + c], part);
+        const double n = sqrt(warp_sum(part));
+        if (lane == 0) nrm[c] = (s.normalize && !(n < 1e-300)) ? n : 1.0;
+      }
+    }
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
+      const double v = Vs[e] / nrm[e % R];
+      Vs[e] = v;
+      s.V[e] = v;
+    }
+    __syncthreads();
+    gram_dv_warps(Dp, s.E, Vs, J, R, b.cc, b.VtV, Mv, b.HtH);
+    __syncthreads();
+  } else {
+    // D and V do not fit in shared memory: one sweep over row chunks of D
+    // (staged coalesced) computes V = D EP (unnormalised, into G2) and the
+    // unnormalised grams D^T V and V^T V in registers (thread entries e = tid
+    // + 512 u, rows in ascending order); the column norms are the diagonal of
+    // V^T V, and the normalised V, cc = E * (D^T V) and V^T V follow by
+    // scaling (P/solver.py:126-128, push_col_norms then the grams).
+    constexpr int MAXU = 8;  // R * R <= 4096 entries over 512 threads
+    const int JT = solve_v_jt(R);
+    double* Dc = EP + R * R;          // JT x R
+    double* Vc = Dc + JT * R;         // JT x R
+    double g1[MAXU], g2[MAXU];
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) g1[u] = g2[u] = 0.0;
+    const int nt = blockDim.x, tid = threadIdx.x;
+    for (int64_t j0 = 0; j0 < J; j0 += JT) {
+      const int nj = (int)(J - j0 < JT ? J - j0 : JT);
+      for (int e = tid; e < nj * R; e += nt) Dc[e] = Dp[j0 * R + e];
+      __syncthreads();
+      for (int e = tid; e < nj * R; e += nt) {
+        const int jj = e / R, r = e - jj * R;
+        double acc = 0.0;
+        for (int q = 0; q < R; ++q) acc = fma(Dc[jj * R + q], EP[q * R + r], acc);
+        Vc[e] = acc;
+        Vs[j0 * R + e] = acc;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < MAXU; ++u) {
+        const int e = tid + nt * u;
+        if (e < R * R) {
+          const int a = e / R, r = e - a * R;
+          double t1 = g1[u], t2 = g2[u];
+          for (int jj = 0; jj < nj; ++jj) {
+            const double v = Vc[jj * R + r];
+            t1 = fma(Dc[jj * R + a], v, t1);
+            t2 = fma(Vc[jj * R + a], v, t2);
+          }
+          g1[u] = t1;
+          g2[u] = t2;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      const int e = tid + nt * u;
+      if (e < R * R && e / R == e % R) {
+        const double n = sqrt(g2[u]);
+        nrm[e / R] = (s.normalize && !(n < 1e-300)) ? n : 1.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < MAXU; ++u) {
+      const int e = tid + nt * u;
+      if (e < R * R) {
+        const int a = e / R, r = e - a * R;
+        const double vtv = g2[u] / (nrm[a] * nrm[r]);
+        b.cc[e] = s.E[a] * (g1[u] / nrm[r]);
+        b.VtV[e] = vtv;
+        Mv[e] = vtv * b.HtH[e];
+      }
+    }
+    for (int64_t e = tid; e < J * R; e += nt) s.V[e] = Vs[e] / nrm[e % R];
+    __syncthreads();
   }
-  __syncthreads();
-  for (int64_t e = threadIdx.x; e < J * R; e += blockDim.x) {
-    const double v = Vs[e] / nrm[e % R];
-    Vs[e] = v;
-    s.V[e] = v;
-  }
-  __syncthreads();
-  gram_dv_warps(Dp, s.E, Vs, J, R, b.cc, b.VtV, Mv, b.HtH);
-  __syncthreads();
-  block_pinv_sym(Mv, U, Pv, R, cs, s.status);
+  block_pinv_sym(Mv, U, Pv, R, cs, s.status, b.pwarm ? b.pwarm + 2 * (R * R + 8) : nullptr);
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) b.pinv3[e] = Pv[e];
 }
 
@@ -1203,7 +1276,7 @@ namespace {
 
 struct AlsLayout {
   size_t theta, pprev, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, L, s_g1, s_wtw, s_m2, s_wtw2, s_e, G2, g3,
-      GD, ps_slots, ps_e, ps_C, ps_stamps, ps_gslots, ps_gcnt, ctl, total;
+      GD, ps_slots, ps_e, ps_C, ps_stamps, ps_gslots, ps_gcnt, pwarm, ctl, total;
 };
 
 int sm_count() {
@@ -1294,6 +1367,7 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.ps_stamps = take(64 * 16 * 8);
   L.ps_gslots = take(64 * 2 * RR);
   L.ps_gcnt = take(64 * 4);
+  L.pwarm = take(3 * (RR + 64));
   L.ctl = take(64);
   L.total = off;
   return L;
@@ -1329,6 +1403,7 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.ps_stamps = reinterpret_cast<int64_t*>(ws + L.ps_stamps);
   b.ps_gslots = d(L.ps_gslots);
   b.ps_gcnt = reinterpret_cast<unsigned*>(ws + L.ps_gcnt);
+  b.pwarm = d(L.pwarm);
   b.ctl = reinterpret_cast<int32_t*>(ws + L.ctl);
   b.nwt = total_warps(K, R);
   b.wpb = wpb_for(R);
@@ -1350,8 +1425,8 @@ size_t mode3_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * ((size
 size_t solve_smem(int R) { return (7 * (size_t)R * R + 3 * (R / 2 + 1) + 8) * 8; }
 // solve_v: + EP (R x R) + D, V (J x R each) when they fit in shared memory
 bool solve_v_dsm(int64_t J, int R) { return (solve_smem(R) + ((size_t)R * R + 2 * (size_t)J * R) * 8) <= 200 * 1024; }
-size_t solve_v_smem(int64_t J, int R) {
-  return solve_smem(R) + ((size_t)R * R + (solve_v_dsm(J, R) ? 2 * (size_t)J * R : 0)) * 8;
+size_t solve_v_smem(int64_t J, int R) {  // EP, then D and V, or two solve_v_jt(R)-row chunks of them
+  return solve_smem(R) + ((size_t)R * R + (solve_v_dsm(J, R) ? 2 * (size_t)J * R : 2 * (size_t)solve_v_jt(R) * R)) * 8;
 }
 
 cudaError_t set_smem(const void* f, size_t bytes) {
@@ -1435,7 +1510,7 @@ cudaError_t prepare(int R, const AlsBufs& b) {
   if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, acc2_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));
-  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, 200 * 1024);
+  if (e == cudaSuccess) e = set_smem((const void*)als_solve_v_kernel, 225 * 1024);  // + static smem <= 227 KB
   if (e == cudaSuccess) {
     SliceArgs a{};
     a.R = R;

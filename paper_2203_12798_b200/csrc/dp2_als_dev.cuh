@@ -9,6 +9,7 @@ namespace dp2 {
 
 struct AlsBufs {
   double *theta, *pprev, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2, *L;
+  double* pwarm;  // 3 x (R x R + 8): warm eigen bases of the solve_h / solve_v pinvs (block_pinv_sym)
   double *s_g1, *s_wtw, *s_m2, *s_wtw2, *s_e, *G2, *g3;
   double *GD, *ps_slots, *ps_e, *ps_C;  // persistent loop: D^T D, per-CTA partial slots, V = D C
   int64_t* ps_stamps;                  // persistent loop: optional phase stamps (64 iterations x 16)
@@ -238,8 +239,14 @@ DP2_DEV bool warp_fast_inverse(const double* A, int R, double* Lw, double* out, 
 }
 
 // RC > 0: R == RC known at compile time (no dispatch over the register inverses)
+// ``warm`` (optional, global R x R + 1): the eigenvector basis of the previous
+// call at this site and, in warm[R * R], 1.0 once it is valid.  The Jacobi
+// fallback then diagonalises W^T A W starting from V = W (the ALS Gram
+// products change little between iterations: a few sweeps instead of ~15
+// from the identity) and leaves its basis there for the next call.
 template <int RC = 0>
-DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status) {
+DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs, int64_t* status,
+                            double* warm = nullptr) {
   __shared__ double lmax;
   __shared__ int fast;
   if (threadIdx.x < 32) {
@@ -250,9 +257,33 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
   }
   __syncthreads();
   if (fast) return;
+  const bool wv = warm != nullptr && warm[R * R] == 1.0;
+  if (wv) {  // A <- W^T A W (symmetrised), U = W
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, c = e % R;
+      double acc = 0.0;
+      for (int q = 0; q < R; ++q) acc = fma(A[i * R + q], warm[q * R + c], acc);
+      out[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, c = e % R;
+      double acc = 0.0;
+      for (int q = 0; q < R; ++q) acc = fma(warm[q * R + i], out[q * R + c], acc);
+      U[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+      const int i = e / R, c = e % R;
+      A[e] = 0.5 * (U[i * R + c] + U[c * R + i]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) U[e] = warm[e];
+    __syncthreads();
+  }
   if (RC == 0 && R > 32) {  // large R: the whole block on the Jacobi rounds
     __shared__ int jflag;
-    const int sw = jacobi_eig_block(A, R, U, R, R, cs, &jflag);
+    const int sw = jacobi_eig_block(A, R, U, R, R, cs, &jflag, 40, !wv);
     if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
     if (threadIdx.x == 0) {
       double m = 0.0;
@@ -260,7 +291,7 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
       lmax = m;
     }
   } else if (threadIdx.x < 32) {
-    const int sw = jacobi_eig_warp(A, R, U, R, R, cs);
+    const int sw = jacobi_eig_warp(A, R, U, R, R, cs, 40, !wv);
     if (sw > 40 && threadIdx.x == 0) atomicAdd(reinterpret_cast<unsigned long long*>(status + ST_SWEEPCAP), 1ull);
     if (threadIdx.x == 0) {
       double m = 0.0;
@@ -269,6 +300,10 @@ DP2_DEV void block_pinv_sym(double* A, double* U, double* out, int R, double* cs
     }
   }
   __syncthreads();
+  if (warm) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) warm[e] = U[e];
+    if (threadIdx.x == 0) warm[R * R] = 1.0;
+  }
   const double tolr = R * lmax * 1e-12;
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
     const int i = e / R, j = e % R;

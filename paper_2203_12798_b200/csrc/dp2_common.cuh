@@ -128,9 +128,10 @@ DP2_DEV void rot_params(double d, double g, double& c, double& s) {
 // high relative accuracy in their small eigenvalues; n eps is the rounding
 // floor).  Returns sweeps used (max_sweeps+1 when the cap was hit).
 DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, double* cs, int* flag,
-                             int max_sweeps = 40) {
+                             int max_sweeps = 40, bool init_v = true) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < n * n; i += nt) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
+  if (init_v)  // else V holds a starting basis (the rotations accumulate onto it)
+    for (int i = tid; i < n * n; i += nt) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
   if (n < 2) { __syncthreads(); return 0; }
   const int ne = n + (n & 1), np = ne / 2;
   const double tol = n * kEps;
@@ -197,9 +198,11 @@ DP2_DEV int jacobi_eig_block(double* A, int lda, double* V, int ldv, int n, doub
 // Single-warp version of jacobi_eig_block (same ordering, rotations and
 // thresholds; __syncwarp instead of __syncthreads).  For the R x R pinvs and
 // other n <= 64 problems where a whole block would mostly idle.
-DP2_DEV int jacobi_eig_warp(double* A, int lda, double* V, int ldv, int n, double* cs, int max_sweeps = 40) {
+DP2_DEV int jacobi_eig_warp(double* A, int lda, double* V, int ldv, int n, double* cs, int max_sweeps = 40,
+                            bool init_v = true) {
   const int lane = threadIdx.x & 31;
-  for (int i = lane; i < n * n; i += 32) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
+  if (init_v)
+    for (int i = lane; i < n * n; i += 32) V[(i / n) * ldv + (i % n)] = (i / n == i % n) ? 1.0 : 0.0;
   __syncwarp();
   if (n < 2) return 0;
   const int ne = n + (n & 1), np = ne / 2;
