@@ -190,6 +190,7 @@ struct SliceArgs {
   int warm;       // rotate: warm start from b.pprev when b.ctl[1]
   int write_w;    // mode3: W_k = G3_k pinv3 (else write G3 into Wout)
   int write_l;    // mode3: emit L_k rows for the metric GEMM
+  const double* g3_in;  // mode3: precomputed G3 (K x R), else formed per slice
   int64_t* status;
 };
 
@@ -973,6 +974,35 @@ __global__ void als_mode2_kernel(SliceArgs a, AlsBufs b) {
   combine_warps(wbase + R * R, wstride, b.wpb, R * R, b.s_wtw2 + (size_t)blockIdx.x * R * R);
 }
 
+// ---- R > 16: modes 2 and 3 as GEMMs over the Theta stack (K x R^2):
+//   mode 2: T = Theta^T W (R^2 x R, T[(q, a)][r] = sum_k w_kr Theta_k[q][a]), then
+//           summed[a][r] = nh_r sum_q H[q][r] T[(q, a)][r] and gram(W nh)
+//           (the reference's sum_k w_k nh (Theta_k^T H), P/solver.py:93-101,
+//           summed over k first)
+//   mode 3: G3 = Theta Z (K x R), Z[(i, j)][r] = H[i][r] cc[j][r]
+//           (P/solver.py:104-111)
+// on the DMMA skinny-GEMM kernels of stage 2 (ordered split-K reductions).
+__global__ void als_m2_finish_kernel(const int32_t* ctl, const double* t3, const double* wtw, const double* H,
+                                     const double* nh, int R, double* summed, double* wtw2) {
+  if (ctl[0]) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < R * R; e += gridDim.x * blockDim.x) {
+    const int a = e / R, r = e % R;
+    double s = 0.0;
+    for (int q = 0; q < R; ++q) s = fma(H[q * R + r], t3[((size_t)q * R + a) * R + r], s);
+    summed[e] = nh[r] * s;
+    wtw2[e] = (nh[a] * nh[r]) * wtw[e];
+  }
+}
+
+__global__ void als_z_kernel(const int32_t* ctl, const double* H, const double* cc, int R, double* zz) {
+  if (ctl[0]) return;
+  const int n = R * R * R;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int r = e % R, ij = e / R, i = ij / R, j = ij % R;
+    zz[e] = H[i * R + r] * cc[j * R + r];
+  }
+}
+
 // G3 row, new W row, and the metric operator rows L_k = [Theta_k E | -H W_k]
 __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
   if (b.ctl[0]) return;
@@ -990,6 +1020,10 @@ __global__ void als_mode3_kernel(SliceArgs a, AlsBufs b) {
     __syncwarp();
     // G3[r] = sum_i H[i][r] sum_j Theta[i][j] cc[j][r]   (P/solver.py:109-111)
     for (int r = lane; r < R; r += 32) {
+      if (a.g3_in) {
+        g3[r] = a.g3_in[k * R + r];
+        continue;
+      }
       double s = 0.0;
       for (int i = 0; i < R; ++i) {
         double h = 0.0;
@@ -1276,7 +1310,7 @@ namespace {
 
 struct AlsLayout {
   size_t theta, pprev, cc, nh, HtH, VtV, pinv3, G1, WtW, summed, WtW2, L, s_g1, s_wtw, s_m2, s_wtw2, s_e, G2, g3,
-      GD, ps_slots, ps_e, ps_C, ps_stamps, ps_gslots, ps_gcnt, pwarm, ctl, total;
+      GD, ps_slots, ps_e, ps_C, ps_stamps, ps_gslots, ps_gcnt, pwarm, t3, zz, gp, ctl, total;
 };
 
 int sm_count() {
@@ -1368,6 +1402,13 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   L.ps_gslots = take(64 * 2 * RR);
   L.ps_gcnt = take(64 * 4);
   L.pwarm = take(3 * (RR + 64));
+  {  // R > 16: R^3 buffers and the split-K partials of the mode-2 stack products
+    const size_t r3 = (size_t)R * R * R * 8;
+    const int sp = std::max(gemm_tn_splits(K, (int64_t)R * R, R), gemm_tn_splits(K, R, R));
+    L.t3 = take(R > 16 ? r3 : 8);
+    L.zz = take(R > 16 ? r3 : 8);
+    L.gp = take(R > 16 ? (size_t)sp * r3 : 8);
+  }
   L.ctl = take(64);
   L.total = off;
   return L;
@@ -1404,6 +1445,9 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   b.ps_gslots = d(L.ps_gslots);
   b.ps_gcnt = reinterpret_cast<unsigned*>(ws + L.ps_gcnt);
   b.pwarm = d(L.pwarm);
+  b.t3 = d(L.t3);
+  b.zz = d(L.zz);
+  b.gp = d(L.gp);
   b.ctl = reinterpret_cast<int32_t*>(ws + L.ctl);
   b.nwt = total_warps(K, R);
   b.wpb = wpb_for(R);
@@ -1532,13 +1576,27 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   reduce_slots_kernel<<<dim3(gx, 2), 256, 0, st>>>(b.ctl, b.s_g1, b.s_wtw, sv.nslots_h, RR);
   s1.nslots_h = 1;
   als_solve_h_kernel<<<1, 512, solve_smem(R), st>>>(s1, b);
-  als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
-  reduce_slots_kernel<<<dim3(gx, 2), 256, 0, st>>>(b.ctl, b.s_m2, b.s_wtw2, sv.nslots, RR);
+  const bool gemm = R > 16;  // modes 2 / 3 on the stack GEMMs (als_m2_finish_kernel)
+  if (gemm) {
+    cudaError_t eg = run_gemm_tn(a.theta, a.K, (int64_t)RR, a.W, R, b.t3, st, b.gp);
+    if (eg == cudaSuccess) eg = run_gemm_tn(a.W, a.K, R, a.W, R, b.zz, st, b.gp);
+    if (eg != cudaSuccess) return eg;
+    als_m2_finish_kernel<<<(RR + 255) / 256, 256, 0, st>>>(b.ctl, b.t3, b.zz, a.H, b.nh, R, b.s_m2, b.s_wtw2);
+  } else {
+    als_mode2_kernel<<<b.nb, nt, acc2_smem(R, b.wpb), st>>>(a, b);
+    reduce_slots_kernel<<<dim3(gx, 2), 256, 0, st>>>(b.ctl, b.s_m2, b.s_wtw2, sv.nslots, RR);
+  }
   s1.nslots = 1;
   als_solve_v_kernel<<<1, 512, solve_v_smem(sv.J, R), st>>>(s1, b);
   a.write_w = 1;
   a.write_l = 1;
   a.Wout = sv.W;
+  if (gemm) {
+    als_z_kernel<<<(RR * R + 255) / 256, 256, 0, st>>>(b.ctl, a.H, b.cc, R, b.zz);
+    cudaError_t eg = run_gemm_nn(a.theta, a.K, (int64_t)RR, b.zz, R, b.g3, st);
+    if (eg != cudaSuccess) return eg;
+    a.g3_in = b.g3;
+  }
   als_mode3_kernel<<<b.nb, nt, mode3_smem(R, b.wpb), st>>>(a, b);
   cudaError_t e = launch_metric(b, a.D, sv.V, a.J, R, a.K, st);
   if (e != cudaSuccess) return e;

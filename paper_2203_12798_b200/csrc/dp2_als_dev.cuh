@@ -9,6 +9,7 @@ namespace dp2 {
 
 struct AlsBufs {
   double *theta, *pprev, *cc, *nh, *HtH, *VtV, *pinv3, *G1, *WtW, *summed, *WtW2, *L;
+  double *t3, *zz, *gp;  // R > 16 GEMM form of modes 2/3: R^3 stack product, R^3 operand, split-K partials
   double* pwarm;  // 3 x (R x R + 8): warm eigen bases of the solve_h / solve_v pinvs (block_pinv_sym)
   double *s_g1, *s_wtw, *s_m2, *s_wtw2, *s_e, *G2, *g3;
   double *GD, *ps_slots, *ps_e, *ps_C;  // persistent loop: D^T D, per-CTA partial slots, V = D C

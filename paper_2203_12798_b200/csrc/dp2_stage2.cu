@@ -400,6 +400,14 @@ cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, 
   return cudaGetLastError();
 }
 
+// out (m x n) = A B, A row-major (m x K), B row-major (K x n): one K range
+// (no split; m / 64 x n / 24 CTAs), for the ALS's slice-stack products.
+cudaError_t run_gemm_nn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out, cudaStream_t st) {
+  nn_dmma_kernel<<<dim3((unsigned)((m + 63) / 64), 1, (unsigned)((n + 23) / 24)), 256, 0, st>>>(A, K, m, K, B, n, n,
+                                                                                                 K, out);
+  return cudaGetLastError();
+}
+
 cudaError_t run_stage2(const double* M, int64_t J, int64_t KR, const double* omega2, int s2, int R,
                        double* D, double* E, double* F, char* ws, int64_t* status, cudaStream_t st,
                        int power_iters) {
