@@ -1405,9 +1405,10 @@ AlsLayout als_layout(int64_t K, int64_t J, int R) {
   {  // R > 16: R^3 buffers and the split-K partials of the mode-2 stack products
     const size_t r3 = (size_t)R * R * R * 8;
     const int sp = std::max(gemm_tn_splits(K, (int64_t)R * R, R), gemm_tn_splits(K, R, R));
+    const size_t nnp = (size_t)gemm_nn_splits(K, (int64_t)R * R, R) * K * R * 8;
     L.t3 = take(R > 16 ? r3 : 8);
     L.zz = take(R > 16 ? r3 : 8);
-    L.gp = take(R > 16 ? (size_t)sp * r3 : 8);
+    L.gp = take(R > 16 ? std::max((size_t)sp * r3, nnp) : 8);
   }
   L.ctl = take(64);
   L.total = off;
@@ -1593,7 +1594,7 @@ cudaError_t launch_iteration(const SliceArgs& base, const SolveArgs& sv, const A
   a.Wout = sv.W;
   if (gemm) {
     als_z_kernel<<<(RR * R + 255) / 256, 256, 0, st>>>(b.ctl, a.H, b.cc, R, b.zz);
-    cudaError_t eg = run_gemm_nn(a.theta, a.K, (int64_t)RR, b.zz, R, b.g3, st);
+    cudaError_t eg = run_gemm_nn(a.theta, a.K, (int64_t)RR, b.zz, R, b.g3, st, b.gp);
     if (eg != cudaSuccess) return eg;
     a.g3_in = b.g3;
   }

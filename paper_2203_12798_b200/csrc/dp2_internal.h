@@ -77,7 +77,9 @@ cudaError_t run_fitness(const dp2_store* st, const double* Q, int R, const doubl
 int gemm_tn_splits(int64_t m, int64_t K, int n);
 cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out,
                         cudaStream_t st, double* parts = nullptr);
-cudaError_t run_gemm_nn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out, cudaStream_t st);
+int gemm_nn_splits(int64_t m, int64_t K, int n);
+cudaError_t run_gemm_nn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out, cudaStream_t st,
+                        double* parts = nullptr);
 size_t zero_pass_bytes(int64_t K, int R);
 cudaError_t run_zero_pass_fitness(const double* MtV, int64_t K, int64_t J, int R, const double* H, const double* V,
                                   const double* W, const double* polar, const double* sq, double* out2, char* ws,

@@ -618,8 +618,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
 }
 
 // ============================================================ signs and A
-// a_r(i) = sum_c y2[i][c] P[c][r], fixed FMA order (shared by both kernels so
-// the argmax sees exactly the stored values up to an exact sign flip).
+// a_r(i) = sum_c y2[i][c] P[c][r] (large-sketch path: arows_kernel)
 struct RowsParams {
   const double* y2;
   const int64_t* row_off;
@@ -635,94 +634,12 @@ struct RowsParams {
   double* A;            // total_rows x R
 };
 
-// Rows of A = Y P for the large-sketch path (sp > 32), 16 columns at a time:
-// P (s x R) staged in shared memory, one row per thread, the y row read once
-// per column group, accumulation in a ascending (the same order in the
-// candidate pass and in the final write, so the stored A and the sign rule
-// see the same numbers).
-struct ACols {
-  double acc[16];
-};
-DP2_DEV void a_row_cols(const double* __restrict__ y, int s, const double* Ps, int R, int c0, int cw, ACols& o) {
-#pragma unroll
-  for (int c = 0; c < 16; ++c) o.acc[c] = 0.0;
-  for (int a = 0; a < s; ++a) {
-    const double ya = __ldg(y + a);
-    const double* pr = Ps + a * R + c0;
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c < cw) o.acc[c] = fma(ya, pr[c], o.acc[c]);
-  }
-}
-
-// Per-piece argmax candidates of |A[:, c]| (first row on ties).
-__global__ void __launch_bounds__(256) argmax_kernel(RowsParams prm) {
-  extern __shared__ __align__(16) double Ps[];  // s x R
-  __shared__ double wabs[8][16];
-  __shared__ int64_t wrow[8][16];
-  __shared__ int wneg[8][16];
-  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, R = prm.R, sp = prm.sp;
-  const int k = prm.piece_slice[p], s = prm.s_k[k];
-  const double* Pk = prm.Pm + (size_t)k * sp * R;
-  for (int i = tid; i < s * R; i += blockDim.x) Ps[i] = Pk[i];
-  __syncthreads();
-  const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
-  const int64_t base = prm.row_off[k];
-  for (int c0 = 0; c0 < R; c0 += 16) {
-    const int cw = min(16, R - c0);
-    double best[16];
-    int64_t brw[16];
-    int bng[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) { best[c] = -1.0; brw[c] = INT64_MAX; bng[c] = 0; }
-    for (int64_t i = r0 + tid; i < r0 + nr; i += blockDim.x) {
-      ACols o;
-      a_row_cols(prm.y2 + i * sp, s, Ps, R, c0, cw, o);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const double v = fabs(o.acc[c]);
-        if (c < cw && v > best[c]) { best[c] = v; brw[c] = i - base; bng[c] = o.acc[c] < 0.0; }
-      }
-    }
-    // warp argmax (larger |a|, then lower row), then across the 8 warps in order
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      double v = best[c];
-      int64_t rw = brw[c];
-      int ng = bng[c];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-        const int64_t orw = __shfl_xor_sync(0xffffffffu, rw, o);
-        const int ong = __shfl_xor_sync(0xffffffffu, ng, o);
-        if (ov > v || (ov == v && orw < rw)) { v = ov; rw = orw; ng = ong; }
-      }
-      if (lane == 0) { wabs[warp][c] = v; wrow[warp][c] = rw; wneg[warp][c] = ng; }
-    }
-    __syncthreads();
-    if (tid < cw) {
-      double v = -1.0;
-      int64_t rw = INT64_MAX;
-      int ng = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-        if (wabs[w][tid] > v || (wabs[w][tid] == v && wrow[w][tid] < rw)) {
-          v = wabs[w][tid];
-          rw = wrow[w][tid];
-          ng = wneg[w][tid];
-        }
-      prm.cand_abs[(size_t)p * R + c0 + tid] = v;
-      prm.cand_row[(size_t)p * R + c0 + tid] = rw;
-      prm.cand_neg[(size_t)p * R + c0 + tid] = ng;
-    }
-    __syncthreads();
-  }
-}
-
 // Combine candidates, fold the signs into P, write M's column block k.
 __global__ void __launch_bounds__(128) signs_kernel(const int32_t* slice_piece, const double* cand_abs,
                                                      const int64_t* cand_row, const int32_t* cand_neg,
                                                      double* Pm, const double* Sv, const double* Vt,
-                                                     int K, int J, int sp, int R, double* M) {
+                                                     int K, int J, int sp, int R, double* M,
+                                                     double* sgn_out = nullptr) {
   const int k = blockIdx.x, tid = threadIdx.x;
   __shared__ double sgn[64];
   const int p0 = slice_piece[k], p1 = slice_piece[k + 1];
@@ -736,6 +653,7 @@ __global__ void __launch_bounds__(128) signs_kernel(const int32_t* slice_piece, 
       if (va > ba || (va == ba && ra < br)) { ba = va; br = ra; bn = cand_neg[(size_t)p * R + r]; }
     }
     sgn[r] = bn ? -1.0 : 1.0;
+    if (sgn_out) sgn_out[(size_t)k * R + r] = sgn[r];
   }
   __syncthreads();
   double* Pk = Pm + (size_t)k * sp * R;
@@ -750,25 +668,89 @@ __global__ void __launch_bounds__(128) signs_kernel(const int32_t* slice_piece, 
   }
 }
 
-// A rows with the signed P (same accumulation order as argmax_kernel).
-__global__ void __launch_bounds__(256) assemble_a_kernel(RowsParams prm) {
-  extern __shared__ __align__(16) double Ps[];  // s x R (signed)
-  const int p = blockIdx.x, tid = threadIdx.x, R = prm.R, sp = prm.sp;
+// Large-sketch path, one pass over Y: A = Y P (unsigned) for the rows of
+// piece p and the piece's argmax candidates of |A[:, c]| (first row on ties).
+// One warp per row (rows r0 + w, r0 + w + 8, ...: ascending per warp), lanes
+// over the columns c = lane, lane + 32; the y row is read coalesced into
+// registers and broadcast by shuffle, P (s x R) is staged in shared memory;
+// accumulation over a ascending.  The stored A is the exact array the
+// candidates saw (the signs are applied after, apply_signs_kernel).
+__global__ void __launch_bounds__(256) arows_kernel(RowsParams prm) {
+  extern __shared__ __align__(16) double Ps[];  // s x R
+  __shared__ double wabs[8][64];
+  __shared__ int64_t wrow[8][64];
+  __shared__ int wneg[8][64];
+  const int p = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, R = prm.R, sp = prm.sp;
   const int k = prm.piece_slice[p], s = prm.s_k[k];
   const double* Pk = prm.Pm + (size_t)k * sp * R;
   for (int i = tid; i < s * R; i += blockDim.x) Ps[i] = Pk[i];
   __syncthreads();
   const int64_t r0 = prm.piece_row0[p], nr = prm.piece_rows[p];
-  for (int64_t i = r0 + tid; i < r0 + nr; i += blockDim.x) {
-    for (int c0 = 0; c0 < R; c0 += 16) {
-      const int cw = min(16, R - c0);
-      ACols o;
-      a_row_cols(prm.y2 + i * sp, s, Ps, R, c0, cw, o);
+  const int64_t base = prm.row_off[k];
+  const int c0 = lane, c1 = lane + 32;
+  double best0 = -1.0, best1 = -1.0;
+  int64_t brw0 = INT64_MAX, brw1 = INT64_MAX;
+  int bng0 = 0, bng1 = 0;
+  for (int64_t i = r0 + warp; i < r0 + nr; i += 8) {
+    const double* y = prm.y2 + i * sp;
+    double yv[4];
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (c < cw) prm.A[i * R + c0 + c] = o.acc[c];
+    for (int t = 0; t < 4; ++t) yv[t] = lane + 32 * t < s ? __ldg(y + lane + 32 * t) : 0.0;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (32 * t >= s) break;
+      const int n = min(32, s - 32 * t);
+      for (int q = 0; q < n; ++q) {
+        const double ya = __shfl_sync(0xffffffffu, yv[t], q);
+        const double* pr = Ps + (32 * t + q) * R;
+        if (c0 < R) a0 = fma(ya, pr[c0], a0);
+        if (c1 < R) a1 = fma(ya, pr[c1], a1);
+      }
+    }
+    double* arow = prm.A + i * R;
+    if (c0 < R) {
+      arow[c0] = a0;
+      const double v = fabs(a0);
+      if (v > best0) { best0 = v; brw0 = i - base; bng0 = a0 < 0.0; }
+    }
+    if (c1 < R) {
+      arow[c1] = a1;
+      const double v = fabs(a1);
+      if (v > best1) { best1 = v; brw1 = i - base; bng1 = a1 < 0.0; }
     }
   }
+  wabs[warp][c0] = best0;
+  wrow[warp][c0] = brw0;
+  wneg[warp][c0] = bng0;
+  wabs[warp][c1] = best1;
+  wrow[warp][c1] = brw1;
+  wneg[warp][c1] = bng1;
+  __syncthreads();
+  if (tid < R) {  // across the warps: larger |a|, then lower row
+    double v = -1.0;
+    int64_t rw = INT64_MAX;
+    int ng = 0;
+    for (int w = 0; w < 8; ++w)
+      if (wabs[w][tid] > v || (wabs[w][tid] == v && wrow[w][tid] < rw)) {
+        v = wabs[w][tid];
+        rw = wrow[w][tid];
+        ng = wneg[w][tid];
+      }
+    prm.cand_abs[(size_t)p * R + tid] = v;
+    prm.cand_row[(size_t)p * R + tid] = rw;
+    prm.cand_neg[(size_t)p * R + tid] = ng;
+  }
+}
+
+// A[i][c] *= sgn[k][c] for the rows of piece p (coalesced rows)
+__global__ void __launch_bounds__(256) apply_signs_kernel(RowsParams prm, const double* sgn) {
+  const int p = blockIdx.x, R = prm.R;
+  const int k = prm.piece_slice[p];
+  const int64_t r0 = prm.piece_row0[p], n = (int64_t)prm.piece_rows[p] * R;
+  double* a = prm.A + r0 * R;
+  const double* sg = sgn + (size_t)k * R;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) a[e] *= sg[e % R];
 }
 
 __global__ void fill_kernel(double* x, int64_t n, double v) {
@@ -1081,13 +1063,14 @@ cudaError_t run_stage1(const dp2_store* st, const double* omega, const int32_t* 
   rp.A = A_out;
   const int P = (int)st->npieces;
   const size_t psm = (size_t)sp * R * 8;  // P staged in shared memory (<= 128 x 64 doubles)
-  e = cudaFuncSetAttribute(argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(assemble_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+  e = cudaFuncSetAttribute(arows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
   if (e != cudaSuccess) return e;
-  argmax_kernel<<<P, 256, psm, stream>>>(rp);
+  // one pass over Y: unsigned A + candidates; signs into P, M and sgn; signed A
+  double* sgn = reinterpret_cast<double*>(ws + L.sgn);
+  arows_kernel<<<P, 256, psm, stream>>>(rp);
   signs_kernel<<<K, 128, 0, stream>>>(st->slice_piece, rp.cand_abs, rp.cand_row, rp.cand_neg, Pm, Sv, Vt,
-                                      K, J, sp, R, M_out);
-  assemble_a_kernel<<<P, 256, psm, stream>>>(rp);
+                                      K, J, sp, R, M_out, sgn);
+  apply_signs_kernel<<<P, 256, 0, stream>>>(rp, sgn);
   complete_kernel<<<K, 256, 0, stream>>>(st->row_off, rank_out, R, A_out);
   if (a_signs) fill_kernel<<<(K * R + 255) / 256, 256, 0, stream>>>(a_signs, (int64_t)K * R, 1.0);  // A is signed
   e = cudaGetLastError();

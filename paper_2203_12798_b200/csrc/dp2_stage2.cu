@@ -400,11 +400,27 @@ cudaError_t run_gemm_tn(const double* A, int64_t m, int64_t K, const double* B, 
   return cudaGetLastError();
 }
 
-// out (m x n) = A B, A row-major (m x K), B row-major (K x n): one K range
-// (no split; m / 64 x n / 24 CTAs), for the ALS's slice-stack products.
-cudaError_t run_gemm_nn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out, cudaStream_t st) {
-  nn_dmma_kernel<<<dim3((unsigned)((m + 63) / 64), 1, (unsigned)((n + 23) / 24)), 256, 0, st>>>(A, K, m, K, B, n, n,
-                                                                                                 K, out);
+// out (m x n) = A B, A row-major (m x K), B row-major (K x n), for the ALS's
+// slice-stack products: split over K for ~4 CTAs per SM (gemm_nn_splits),
+// the partials (``parts``, >= splits m n doubles) summed in order.
+int gemm_nn_splits(int64_t m, int64_t K, int n) {
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ctas = ((m + 63) / 64) * ((n + 23) / 24);
+  const int64_t want = (4 * (int64_t)sms + ctas - 1) / ctas;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (K + 63) / 64));
+}
+
+cudaError_t run_gemm_nn(const double* A, int64_t m, int64_t K, const double* B, int n, double* out, cudaStream_t st,
+                        double* parts) {
+  const int ks = parts ? gemm_nn_splits(m, K, n) : 1;
+  const int64_t kc = ((K + ks - 1) / ks + 3) / 4 * 4;
+  const int ksr = (int)((K + kc - 1) / kc);
+  nn_dmma_kernel<<<dim3((unsigned)((m + 63) / 64), ksr, (unsigned)((n + 23) / 24)), 256, 0, st>>>(
+      A, K, m, K, B, n, n, kc, ksr == 1 ? out : parts);
+  if (ksr > 1)
+    reduce_parts_kernel<<<(unsigned)std::min<int64_t>((m * n + 255) / 256, 4096), 256, 0, st>>>(parts, ksr, m * n,
+                                                                                                  out);
   return cudaGetLastError();
 }
 
