@@ -131,8 +131,8 @@ def check_rank(tensor: IrregularTensor, rank, slice_ids=None):
         k = int(short[0])
         ids = range(tensor.num_slices) if slice_ids is None else slice_ids
         raise RankTooLargeError(f"rank {rank} exceeds row count {int(rows[k])} of slice {list(ids)[k]}")
-    if rank > 64:
-        raise RankTooLargeError(f"rank {rank} exceeds the device limit of 64")
+    if rank > 56:
+        raise RankTooLargeError(f"rank {rank} exceeds the device limit of 56")
 
 
 def stage2_params(base: RsvdParams, stage2, rank, K, J):

@@ -208,94 +208,6 @@ DP2_DEV void load_cta_common(const SliceArgs& a, const AlsBufs& b, CtaShared& s,
   __syncthreads();
 }
 
-__global__ void als_rotate_kernel(SliceArgs a, AlsBufs b) {
-  if (b.ctl[0]) return;
-  extern __shared__ __align__(16) double sm[];
-  const int R = a.R, ldt = ldt_for(R), lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  CtaShared cs = carve_cta(sm, R);
-  const size_t wstride = warp_smem_doubles(R);
-  double* wbase = sm + cta_shared_doubles(R);
-  double* Ts = wbase + (size_t)wib * wstride;
-  double* Vr = Ts + R * ldt;
-  double* Fs = Vr + R * ldt;
-  double* Th = Fs + R * R;
-  double* Pi = Th + R * R;
-  double* acc1 = Pi + R * R;
-  double* acc2 = acc1 + R * R;
-  double* tmp = acc2 + R * R;  // 4R
-  load_cta_common(a, b, cs, true, false);
-  const bool warm = a.warm && b.ctl[1];
-  for (int e = lane; e < R * R; e += 32) { acc1[e] = 0.0; acc2[e] = 0.0; }
-  const int gw = blockIdx.x * b.wpb + wib;
-  for (int64_t k = gw; k < a.K; k += b.nwt) {
-    const double* Fk = a.F + k * R * R;
-    const double* wk = a.W + k * R;
-    for (int e = lane; e < R * R; e += 32) Fs[e] = Fk[e];
-    // warm start: Vr = P_prev (column-major), else identity
-    for (int e = lane; e < R * R; e += 32) {
-      const int i = e / R, d = e % R;  // Vr[col i][row d]
-      Vr[i * ldt + d] = warm ? b.pprev[k * R * R + e] : (i == d ? 1.0 : 0.0);
-    }
-    __syncwarp();
-    // Th <- (F_k cc) * w_k   (reference: (core_block(k) @ core_cols) * w[k])
-    for (int e = lane; e < R * R; e += 32) {
-      const int i = e / R, c = e % R;
-      double s = 0.0;
-      for (int q = 0; q < R; ++q) s = fma(Fs[i * R + q], cs.cc[q * R + c], s);
-      Th[e] = s * wk[c];
-    }
-    __syncwarp();
-    // Pi <- T = Th H^T (row-major scratch), then Ts = T Vr (column-major)
-    for (int e = lane; e < R * R; e += 32) {
-      const int i = e / R, d = e % R;
-      double s = 0.0;
-      for (int c = 0; c < R; ++c) s = fma(Th[i * R + c], cs.H[d * R + c], s);
-      Pi[e] = s;
-    }
-    __syncwarp();
-    for (int e = lane; e < R * R; e += 32) {
-      const int c = e / R, i = e % R;  // Ts[col c][row i] = sum_d T[i][d] Vr[col c][row d]
-      double s = 0.0;
-      if (warm)
-        for (int d = 0; d < R; ++d) s = fma(Pi[i * R + d], Vr[c * ldt + d], s);
-      else
-        s = Pi[i * R + c];
-      Ts[c * ldt + i] = s;
-    }
-    __syncwarp();
-    warp_polar(Ts, Vr, ldt, R, Pi, tmp, a.status, k);
-    for (int e = lane; e < R * R; e += 32) {  // keep P_k for the next warm start
-      const int i = e / R, d = e % R;
-      b.pprev[k * R * R + e] = Vr[i * ldt + d];
-    }
-    // Theta = Pi^T F
-    for (int e = lane; e < R * R; e += 32) {
-      const int i = e / R, c = e % R;
-      double s = 0.0;
-      for (int d = 0; d < R; ++d) s = fma(Pi[d * R + i], Fs[d * R + c], s);
-      Th[e] = s;
-      a.theta[k * R * R + e] = s;
-      if (a.polar) a.polar[k * R * R + e] = Pi[e];
-    }
-    __syncwarp();
-    if (a.mode1) {
-      // g1[i][r] += w[k][r] * (Theta cc)[i][r];  wtw[i][r] += w[k][i] w[k][r]
-      for (int e = lane; e < R * R; e += 32) {
-        const int i = e / R, r = e % R;
-        double s = 0.0;
-        for (int q = 0; q < R; ++q) s = fma(Th[i * R + q], cs.cc[q * R + r], s);
-        acc1[e] += wk[r] * s;
-        acc2[e] += wk[i] * wk[r];
-      }
-    }
-    __syncwarp();
-  }
-  if (a.mode1) {
-    __syncthreads();
-    combine_warps(wbase + (acc1 - Ts), wstride, b.wpb, R * R, b.s_g1 + (size_t)blockIdx.x * R * R);
-    combine_warps(wbase + (acc2 - Ts), wstride, b.wpb, R * R, b.s_wtw + (size_t)blockIdx.x * R * R);
-  }
-}
 
 // ------------------------------------------------------------ large R (R > 32)
 // One CTA per slice: the one-sided Jacobi SVD of T_k parallel over the CTA --
@@ -1464,7 +1376,6 @@ AlsBufs make_bufs(char* ws, int64_t K, int64_t J, int R) {
   return b;
 }
 
-size_t rotate_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * warp_smem_doubles(R)) * 8; }
 size_t acc2_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * 3 * (size_t)R * R) * 8; }
 size_t mode3_smem(int R, int wpb) { return (cta_shared_doubles(R) + wpb * ((size_t)R * R + 2 * (size_t)R)) * 8; }
 size_t solve_smem(int R) { return (7 * (size_t)R * R + 3 * (R / 2 + 1) + 8) * 8; }
@@ -1481,6 +1392,7 @@ cudaError_t set_smem(const void* f, size_t bytes) {
     char buf[96];
     snprintf(buf, sizeof(buf), "dynamic smem attribute %zu bytes", bytes);
     note_error(buf);
+    (void)cudaGetLastError();  // reported here: do not leave it for later launch checks
   }
   return e;
 }
@@ -1543,15 +1455,13 @@ cudaError_t launch_rotate(const SliceArgs& a, const AlsBufs& b, cudaStream_t st,
         void* args[] = {(void*)&a, (void*)&b};
         return cudaLaunchKernel(f, dim3(b.nbr), dim3(256), args, smc, st);
       }
-      if (setattr) return set_smem((const void*)als_rotate_kernel, rotate_smem(a.R, b.wpb));
-      als_rotate_kernel<<<b.nb, 32 * b.wpb, rotate_smem(a.R, b.wpb), st>>>(a, b);
-      return cudaGetLastError();
+      note_error("rank above the device limit of 56");
+      return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t prepare(int R, const AlsBufs& b) {
-  cudaError_t e = set_smem((const void*)als_rotate_kernel, rotate_smem(R, b.wpb));
-  if (e == cudaSuccess) e = set_smem((const void*)als_mode2_kernel, acc2_smem(R, b.wpb));
+  cudaError_t e = set_smem((const void*)als_mode2_kernel, acc2_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode1_kernel, acc2_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_mode3_kernel, mode3_smem(R, b.wpb));
   if (e == cudaSuccess) e = set_smem((const void*)als_solve_h_kernel, solve_smem(R));

@@ -177,10 +177,11 @@ def test_random_instances_vs_live_oracle(seed):
         assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
 
 
-@pytest.mark.parametrize("R", [12, 16, 17, 24])
+@pytest.mark.parametrize("R", [12, 16, 17, 24, 33, 56])
 def test_larger_ranks_vs_live_oracle(R):
     """Ranks either side of the solves' register inverse (R <= 16) and its
-    Cholesky fallback (dp2_als.cu block_pinv_sym)."""
+    Cholesky fallback (dp2_als.cu block_pinv_sym), the Newton-Schulz CTA
+    rotation (17 <= R <= 56) and the device rank limit (56)."""
     import paper_2203_12798_b200 as dp
     from oracle import dpar2_oracle as orc
     rng = np.random.default_rng(2000 + R)
@@ -211,6 +212,9 @@ def test_errors_mirror_reference():
         dp.compress(dp.IrregularTensor([np.ones((6, 5)), np.ones((2, 5))]), 3)
     with pytest.raises(ValueError):
         dp.fit_dpar2(t, 2, dp.SolverOptions(max_iters=0))
+    wide = dp.IrregularTensor([rng.random((70, 60)) for _ in range(3)])
+    with pytest.raises(dp.RankTooLargeError, match="device limit of 56"):
+        dp.compress(wide, 57)
 
 
 def test_degenerate_slices():
