@@ -3,9 +3,10 @@
 ``fit_dpar2(tensor, rank, opts) -> (Parafac2Factors, FitTrace)`` keeps the
 reference entry point, return values, errors and stop rule.  The whole
 iteration loop runs on the device (one cooperative persistent kernel for
-R <= 16, else a seven-kernel loop; the stop rule ``prev == 0 or |prev - e| <=
-tol * prev`` is evaluated on the device each iteration), so the host only
-launches and reads the trace at the end.
+R <= 16 and R = 20, 24, else a stream-ordered loop of per-phase kernels --
+CTA Newton-Schulz rotations, Theta-stack GEMMs, single-CTA solves; the stop
+rule ``prev == 0 or |prev - e| <= tol * prev`` is evaluated on the device each
+iteration), so the host only launches and reads the trace at the end.
 
 The kernel-granular functions (update_rotations, mttkrp_mode1/2/3,
 update_factors, convergence_metric) mirror the reference's test-level API;
