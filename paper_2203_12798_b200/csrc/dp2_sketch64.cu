@@ -24,11 +24,11 @@
 //   aux (1 warp)        sums the 4 partials -> Y_t (rows past the piece zeroed),
 //                       publishes it in B-fragment layout (yfin ring), flags
 //                       non-finite values (status word 0 = lowest slice: a
-//                       NaN / Inf anywhere in X_k reaches Y), writes Y rows and
-//                       accumulates G = Y^T Y with DMMA (Y^T fragments are
-//                       the B fragments), flushes G per piece.
+//                       NaN / Inf anywhere in X_k reaches Y), writes Y rows.
 //   B warps (16)        Z (J x SG) += X_t^T Y_t for their sixteenth of J, held
-//                       in registers across the piece; flushed per piece.
+//                       in registers across the piece; flushed per piece.  The
+//                       first NT^2 also accumulate one 8 x 8 tile of G = Y^T Y
+//                       each (Y^T fragments are the B fragments).
 //
 // Column groups of SG = 8 NT sketch columns run as separate CTAs (grid.y).
 // Eligible: J <= 512 (B image <= 96 KB + a 3-stage X ring in 227 KB).
@@ -329,13 +329,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       warp_arrive(bar(B_OEMPTY + a));
     }
   } else if (warp == WARP_AUX) {
-    // ------------------------------------------------------------ aux: Y_t, Y rows, G, non-finite
-    const bool do_g = prm.g_part != nullptr && crank == 0;  // one CTA of the pair writes G
-    double g[NT][NT][2];
-#pragma unroll
-    for (int i = 0; i < NT; ++i)
-#pragma unroll
-      for (int j = 0; j < NT; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    // ------------------------------------------------------------ aux: Y_t, Y rows, non-finite
     int n = 0;
     for (int p = pbeg; p < pend; ++p) {
       const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
@@ -379,30 +373,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
               if (row < valid && col < sp) prm.y_out[(row0 + (int64_t)t * TM + row) * sp + col] = fr[k2][j];
             }
         }
-        if (do_g) {
-#pragma unroll
-          for (int k2 = 0; k2 < K2; ++k2)
-#pragma unroll
-            for (int i = 0; i < NT; ++i)
-#pragma unroll
-              for (int j = 0; j < NT; ++j) dmma_8x8x4(g[i][j][0], g[i][j][1], fr[k2][i], fr[k2][j]);
-        }
       }
       if (__any_sync(0xffffffffu, bad) && lane == 0) status_min(prm.status, ST_NONFINITE, ks);
-      if (do_g) {
-        double* gp = prm.g_part + (size_t)p * sp * sp;
-#pragma unroll
-        for (int i = 0; i < NT; ++i)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int rr = 8 * i + (lane >> 2), cc = 8 * j + 2 * (lane & 3);
-            if (rr < sp && cc < sp) {
-              gp[(size_t)rr * sp + cc] = g[i][j][0];
-              if (cc + 1 < sp) gp[(size_t)rr * sp + cc + 1] = g[i][j][1];
-            }
-            g[i][j][0] = g[i][j][1] = 0.0;
-          }
-      }
     }
   } else {
     // ------------------------------------------------------------ B warps: Z += X_t^T Y_t
@@ -417,6 +389,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     for (int i = 0; i < MBMAX; ++i)
 #pragma unroll
       for (int j = 0; j < NT; ++j) z[i][j][0] = z[i][j][1] = 0.0;
+    // G = Y^T Y per piece (pass 2): 8 x 8 tile (gi, gj) owned by B warp
+    // gi NT + gj -- Y^T fragments are the B fragments this warp loads anyway,
+    // so the 2 NT^2 DMMAs per tile spread over the sub-partitions (the aux
+    // warp alone made its sub-partition the slowest)
+    const bool g_own = prm.g_part != nullptr && crank == 0 && bw < NT * NT;
+    const int gi = bw / NT, gj = bw - (bw / NT) * NT;
+    double g0 = 0.0, g1 = 0.0;
     int n = 0, rs = 0, rph = 0;
     for (int p = pbeg; p < pend; ++p) {
       const int rows = prm.piece_rows[p];
@@ -432,6 +411,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
           double yv[NT];
 #pragma unroll
           for (int j = 0; j < NT; ++j) yv[j] = yf[(k2 * NT + j) * 32];
+          if (g_own) {
+            double ya = 0.0, yb = 0.0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+              ya = j == gi ? yv[j] : ya;
+              yb = j == gj ? yv[j] : yb;
+            }
+            dmma_8x8x4(g0, g1, ya, yb);
+          }
 #pragma unroll
           for (int i = 0; i < MBMAX; ++i) {
             if (i < MB) {
@@ -443,6 +431,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         }
         warp_arrive(bar(B_YEMPTY + b));
         warp_arrive(bar(B_XEMPTY + s));
+      }
+      if (g_own) {  // G tile (gi, gj): rows 8 gi + (lane >> 2), cols 8 gj + 2 (lane & 3) (+1)
+        double* gp = prm.g_part + (size_t)p * sp * sp;
+        const int rr = 8 * gi + (lane >> 2), cc = 8 * gj + 2 * (lane & 3);
+        if (rr < sp && cc < sp) {
+          gp[(size_t)rr * sp + cc] = g0;
+          if (cc + 1 < sp) gp[(size_t)rr * sp + cc + 1] = g1;
+        }
+        g0 = g1 = 0.0;
       }
       // piece complete: flush Z rows 8 (jb0 + i) + (lane >> 2), cols col0 + 8 j + 2 (lane & 3) (+1)
       double* out = prm.out_part + (size_t)p * J * sp;
