@@ -306,13 +306,23 @@ def run_stage1_chunked(tensor: IrregularTensor, rank, base: RsvdParams, timings=
 
 
 def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None, power_iters=1):
-    """Stage 2 (P/compress.py:109-111) on the device: D, E, F."""
+    """Stage 2 (P/compress.py:109-111) on the device: D, E, F.
+
+    A sketch wider than M's short side (s2 > min(J, KR), e.g. an explicit
+    oversampling on few slices) spans range(M) with its first min(J, KR)
+    columns already (almost surely, and exactly what the reference's
+    Householder QR of the rank-deficient Y then keeps), so the device runs on
+    those columns of the reference's Omega_2 -- the same D, E, F."""
     dev = M.device
     lib = _lib.lib()
     om2 = om2 if isinstance(om2, torch.Tensor) else torch.from_numpy(om2)
     if om2.device.type == "cpu" and not om2.is_pinned():
         om2 = om2.pin_memory()
     om2 = om2.to(dev, non_blocking=True)
+    cap = int(min(J, KR))
+    if s2 > cap >= rank:
+        om2 = om2[:, :cap].contiguous()
+        s2 = cap
     D = torch.empty((J, rank), dtype=torch.float64, device=dev)
     E = torch.empty(rank, dtype=torch.float64, device=dev)
     F = torch.empty((KR, rank), dtype=torch.float64, device=dev)

@@ -458,6 +458,43 @@ DP2_DEV bool cta_chol_lower(double* A, int ld, int s, double rel_floor, int* fla
   return true;
 }
 
+// tmp = CC T in place: rows a0 .. a0 + 3 of A (s x s, stride ld) per warp
+// pass, read in full before the warp overwrites their first rp columns;
+// T (s x rp) is Tg with row stride s.  Covers rp <= 32 MC columns.
+template <int MC>
+DP2_DEV void cc_times_t(double* A, int ld, const double* Tg, int s, int rp, int warp, int nw, int lane) {
+  for (int a0 = warp * 4; a0 < s; a0 += nw * 4) {
+    double o[4][MC];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int m = 0; m < MC; ++m) o[x][m] = 0.0;
+    for (int b = 0; b < s; ++b) {
+      double t[MC];
+#pragma unroll
+      for (int m = 0; m < MC; ++m) {
+        const int c = lane + 32 * m;
+        t[m] = c < rp ? Tg[b * s + c] : 0.0;
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const double cab = a0 + x < s ? A[(a0 + x) * ld + b] : 0.0;
+#pragma unroll
+        for (int m = 0; m < MC; ++m) o[x][m] = fma(cab, t[m], o[x][m]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int m = 0; m < MC; ++m) {
+        const int c = lane + 32 * m;
+        if (a0 + x < s && c < rp) A[(a0 + x) * ld + c] = o[x][m];
+      }
+    __syncwarp();
+  }
+}
+
 __host__ __device__ inline size_t factor_smem_bytes(int s) {
   return (2 * (size_t)s * (s + 1) + (size_t)kGramRows * ((s + 3) / 4 * 4) + 4 * (size_t)s + 8) * 8;
 }
@@ -475,7 +512,7 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
   double* lam = tile + (size_t)kGramRows * ((s + 3) / 4 * 4);  // s
   double* cs = lam + s;                                        // 3*(s/2+1)
   double* Tg = gscr + 2 * (size_t)sp * (sp + 1);               // s x s (ld = s), global: T = W[:, perm] / sqrt(lam)
-  __shared__ int perm[160];
+  __shared__ int perm[256];  // s <= sp <= 256 (dp2_stage1)
   __shared__ int flag;
   __shared__ double Sloc[64];
 
@@ -529,38 +566,11 @@ __global__ void __launch_bounds__(256) factor_kernel(FactorParams prm) {
     }
     __syncthreads();
   }
-  // 4. CC = C C^T over J (A), then tmp = CC T in place (A[:, :rp]), 4 rows per warp pass
+  // 4. CC = C C^T over J (A), then tmp = CC T in place (A[:, :rp]), 4 rows per
+  // warp pass; a lane holds columns lane + 32 m, m < MC (MC = 8 when rp > 128)
   gram_cols_cta(Ct, J, sp, s, A, ld, tile);
-  for (int a0 = warp * 4; a0 < s; a0 += nw * 4) {
-    double o[4][4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int m = 0; m < 4; ++m) o[x][m] = 0.0;
-    for (int b = 0; b < s; ++b) {
-      double t[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int c = lane + 32 * m;
-        t[m] = c < rp ? Tg[b * s + c] : 0.0;
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        const double cab = a0 + x < s ? A[(a0 + x) * ld + b] : 0.0;
-#pragma unroll
-        for (int m = 0; m < 4; ++m) o[x][m] = fma(cab, t[m], o[x][m]);
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int c = lane + 32 * m;
-        if (a0 + x < s && c < rp) A[(a0 + x) * ld + c] = o[x][m];
-      }
-    __syncwarp();
-  }
+  if (rp <= 128) cc_times_t<4>(A, ld, Tg, s, rp, warp, nw, lane);
+  else cc_times_t<8>(A, ld, Tg, s, rp, warp, nw, lane);
   __syncthreads();
   // Bg = T^T tmp (rp x rp, B), symmetrised
   for (int i = tid; i < rp * rp; i += nt) {
@@ -693,12 +703,12 @@ __global__ void __launch_bounds__(256) arows_kernel(RowsParams prm) {
   int bng0 = 0, bng1 = 0;
   for (int64_t i = r0 + warp; i < r0 + nr; i += 8) {
     const double* y = prm.y2 + i * sp;
-    double yv[4];
+    double yv[8];  // s <= 256 (dp2_stage1's sketch-width bound)
 #pragma unroll
-    for (int t = 0; t < 4; ++t) yv[t] = lane + 32 * t < s ? __ldg(y + lane + 32 * t) : 0.0;
+    for (int t = 0; t < 8; ++t) yv[t] = lane + 32 * t < s ? __ldg(y + lane + 32 * t) : 0.0;
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < 8; ++t) {
       if (32 * t >= s) break;
       const int n = min(32, s - 32 * t);
       for (int q = 0; q < n; ++q) {

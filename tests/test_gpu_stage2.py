@@ -87,3 +87,33 @@ def test_compress_power_iters_match_oracle(q, tol):
     assert rel_signed(A, Ao) <= tol, rel_signed(A, Ao)
     assert float(np.abs(comp.weights.cpu().numpy() - o.E).max() / o.E.max()) <= tol * 1e-2
     assert rel_signed(comp.col_basis.cpu().numpy(), o.D) <= tol
+
+
+def test_wide_stage1_sketch_above_128_columns():
+    """s = R + p > 128 (sp = 160): the large-sketch stage-1 path (the CC T
+    product over more than 128 columns, one pass over Y for A and the sign
+    candidates) against the oracle's per-slice rSVD: U_k sign-exact (the
+    reference's sign rule) within 1e-7, and D / E / F (s2 = 142 < K R)."""
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    rng = np.random.default_rng(11)
+    R, p, J = 12, 130, 200
+    xs = [rng.standard_normal((int(m), J)) @ np.diag(np.linspace(2.0, 0.5, J)) for m in rng.integers(160, 260, size=16)]
+    t = dp.IrregularTensor(xs)
+    comp = dp.compress(t, R, rsvd=dp.RsvdParams(rank=R, oversampling=p, seed=0))
+    o = orc.compress(xs, R, seed=0, oversampling=p, keep_stage1=True)
+    for k in range(len(xs)):
+        A = comp.slice_bases[k].cpu().numpy()
+        U = o.stage1[k][0]
+        assert float(np.abs(A - U).max()) <= 1e-7, k
+    _check(xs, R, oversampling=p)
+
+
+def test_stage2_sketch_wider_than_m():
+    """s2 = R + p > K R (few slices, explicit oversampling): Y2 = M Omega_2 is
+    rank deficient; the result is the reference's (range(M) either way)."""
+    rng = np.random.default_rng(12)
+    xs = [rng.standard_normal((int(m), 120)) for m in rng.integers(90, 140, size=5)]
+    _check(xs, 8, oversampling=60)  # s2 = 68 > K R = 40
+    ys = [rng.standard_normal((int(m), 200)) for m in rng.integers(160, 260, size=6)]
+    _check(ys, 12, oversampling=130)  # s2 = 142 > K R = 72 (D^T D was 43 off the identity before the cap)
