@@ -163,6 +163,8 @@ def _stage1_setup(tensor, rank, oversampling, dev):
         from .tensor import to_device_async
         widths = np.asarray(sketch_widths(tensor.row_counts, tensor.num_cols, rank, oversampling), dtype=np.int32)
         sp = padded_width(int(widths.max()))
+        if sp > 256:
+            raise ValueError(f"sketch width rank + oversampling = {int(widths.max())} exceeds the device limit of 256")
         cache[key] = (widths, sp, to_device_async(widths, torch.int32, dev))
     return cache[key]
 
@@ -323,6 +325,8 @@ def run_stage2(M, J, KR, rank, seed2, s2, om2, status, timings=None, power_iters
     if s2 > cap >= rank:
         om2 = om2[:, :cap].contiguous()
         s2 = cap
+    if s2 > 150:
+        raise ValueError(f"stage-2 sketch width {s2} exceeds the device limit of 150")
     D = torch.empty((J, rank), dtype=torch.float64, device=dev)
     E = torch.empty(rank, dtype=torch.float64, device=dev)
     F = torch.empty((KR, rank), dtype=torch.float64, device=dev)
