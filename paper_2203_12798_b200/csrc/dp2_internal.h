@@ -32,6 +32,8 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
                           double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part, bool y32 = false);
 // fp64 DMMA warp-specialised pass (dp2_sketch64.cu): fp64 or fp32 (upcast) storage
 bool sketch64_eligible(const dp2_store* st, int sp, bool xsq, bool gram);
+cudaError_t run_sketch_generic(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                               double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part);
 bool sketch64_pairs(int64_t J);  // the DMMA pass runs as CTA pairs (one segment per pair)
 cudaError_t run_sketch64(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
                          int64_t* status, cudaStream_t stream, double* g_part);

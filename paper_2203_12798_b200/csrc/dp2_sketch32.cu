@@ -308,9 +308,12 @@ cudaError_t run_sketch_f32(const dp2_store* st, const double* B, int sp, double*
   const int sg = 8 * cpl;
   const size_t need32 = ((size_t)2 * 32 * prm.lds + (size_t)((J + 3) / 4) * 4 * sg + 9 * 32 * sg) * 4;
   const size_t need16 = ((size_t)2 * 16 * prm.lds + (size_t)((J + 3) / 4) * 4 * sg + 9 * 16 * sg) * 4;
+  const size_t need8 = ((size_t)2 * 8 * prm.lds + (size_t)((J + 3) / 4) * 4 * sg + 9 * 8 * sg) * 4;
   if (need32 <= 220 * 1024) return by_cpl<32>(prm, cpl, jt, st->nseg, ng, njs, stream);
   if (need16 <= 220 * 1024) return by_cpl<16>(prm, cpl, jt, st->nseg, ng, njs, stream);
-  return by_cpl<8>(prm, cpl, jt, st->nseg, ng, njs, stream);  // J ~ 1000: B image + 2 x 8-row tiles
+  if (need8 <= 220 * 1024) return by_cpl<8>(prm, cpl, jt, st->nseg, ng, njs, stream);  // J ~ 1000
+  // the B image no longer fits: the generic pass (B from L2), fp64 products
+  return run_sketch_generic(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
 }
 
 }  // namespace dp2

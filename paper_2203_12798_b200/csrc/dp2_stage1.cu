@@ -862,13 +862,14 @@ cudaError_t dispatch_mt(const SketchParams& prm, int mt, int nt, int nseg, int n
 // Smem budget per CTA for the X tiles (both buffers).
 static constexpr size_t kXTileBudget = 150 * 1024;
 
-cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
-                       double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
-  if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
-  if (sketch64_eligible(st, sp, xsq_part != nullptr, g_part != nullptr))
-    return run_sketch64(st, B, sp, out_part, y_out, status, stream, g_part);
+// The generic streaming pass (per-tile DMMA, B from L2 each k-step: no
+// J-sized shared-memory image): fp64 storage outside the warp-specialised
+// pass's shapes, and fp32 storage whose B image does not fit the FFMA pass
+// (J above ~1300) -- fp64 products on the exactly upcast values.
+cudaError_t run_sketch_generic(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                               double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
   const int J = (int)st->J;
-  const int elem = 8;
+  const int elem = st->dtype == DP2_F64 ? 8 : 4;
   SketchParams prm{};
   prm.X = st->X;
   prm.ldx = st->ldx;
@@ -894,8 +895,19 @@ cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out
   const int tm = (size_t)2 * 16 * prm.lds * elem <= kXTileBudget ? 16 : 8;
   if ((size_t)2 * tm * prm.lds * elem > 200 * 1024) return cudaErrorInvalidValue;
   const int nseg = st->nseg;
+  if (elem == 4)
+    return tm == 16 ? dispatch_mt<float, 16>(prm, mt, nt, nseg, ng, njs, stream)
+                    : dispatch_mt<float, 8>(prm, mt, nt, nseg, ng, njs, stream);
   return tm == 16 ? dispatch_mt<double, 16>(prm, mt, nt, nseg, ng, njs, stream)
                   : dispatch_mt<double, 8>(prm, mt, nt, nseg, ng, njs, stream);
+}
+
+cudaError_t run_sketch(const dp2_store* st, const double* B, int sp, double* out_part, double* y_out,
+                       double* xsq_part, int64_t* status, cudaStream_t stream, double* g_part) {
+  if (st->dtype == DP2_F32) return run_sketch_f32(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
+  if (sketch64_eligible(st, sp, xsq_part != nullptr, g_part != nullptr))
+    return run_sketch64(st, B, sp, out_part, y_out, status, stream, g_part);
+  return run_sketch_generic(st, B, sp, out_part, y_out, xsq_part, status, stream, g_part);
 }
 
 int sketch_njs(int J) {

@@ -195,6 +195,26 @@ def test_larger_ranks_vs_live_oracle(R):
         assert rel_signed(getattr(f, key), o[key]) <= FACTOR_TOL, key
 
 
+@pytest.mark.parametrize("J,dtype", [(1500, "f64"), (1500, "f32"), (777, "f64")])
+def test_wide_and_odd_column_counts_vs_live_oracle(J, dtype):
+    """J above the warp-specialised DMMA pass's 1024 (the generic fp64 pass /
+    the FFMA fp32 pass) and an odd J (no 16-byte row alignment)."""
+    import paper_2203_12798_b200 as dp
+    from oracle import dpar2_oracle as orc
+    rng = np.random.default_rng(J)
+    R, K = 10, 10
+    xs = [rng.standard_normal((int(m), R)) @ rng.standard_normal((R, J)) + 0.1 * rng.standard_normal((int(m), J))
+          for m in rng.integers(200, 600, size=K)]
+    o = orc.fit_dpar2(xs, R, 8, 0.0, 0)
+    xin = [x.astype(np.float32) for x in xs] if dtype == "f32" else xs
+    t = dp.IrregularTensor(xin, dtype=dtype)
+    f, tr = dp.fit_dpar2(t, R, dp.SolverOptions(max_iters=8, tol=0.0))
+    tol_f, tol_x = (1e-6, 1e-5) if dtype == "f64" else (1e-3, 1e-3)
+    assert abs(dp.fitness(t, f) - orc.fitness(xs, o["H"], o["V"], o["W"], o["Q"])) <= tol_f
+    for key in ("H", "V", "W"):
+        assert rel_signed(getattr(f, key), o[key]) <= tol_x, key
+
+
 def test_errors_mirror_reference():
     import paper_2203_12798_b200 as dp
     rng = np.random.default_rng(0)
