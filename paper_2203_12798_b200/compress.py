@@ -133,6 +133,10 @@ def check_rank(tensor: IrregularTensor, rank, slice_ids=None):
         raise RankTooLargeError(f"rank {rank} exceeds row count {int(rows[k])} of slice {list(ids)[k]}")
     if rank > 56:
         raise RankTooLargeError(f"rank {rank} exceeds the device limit of 56")
+    jmax = 1588 if tensor.dtype == "f64" else 3176  # two 8-row X tiles of the generic pass in 200 KB
+    if tensor.num_cols > jmax:
+        raise ValueError(f"column count {tensor.num_cols} exceeds the device limit of {jmax} for {tensor.dtype} "
+                         f"storage")
 
 
 def stage2_params(base: RsvdParams, stage2, rank, K, J):

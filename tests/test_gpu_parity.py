@@ -235,6 +235,8 @@ def test_errors_mirror_reference():
     wide = dp.IrregularTensor([rng.random((70, 60)) for _ in range(3)])
     with pytest.raises(dp.RankTooLargeError, match="device limit of 56"):
         dp.compress(wide, 57)
+    with pytest.raises(ValueError, match="column count 1600 exceeds the device limit of 1588"):
+        dp.compress(dp.IrregularTensor([rng.random((20, 1600)) for _ in range(2)]), 4)
 
 
 def test_degenerate_slices():
