@@ -80,6 +80,13 @@ struct Params {
   double* g_part;
   int64_t* status;
   uint32_t off_b, off_y, off_yrow, off_bar;
+  // J split across a CTA pair (J > 512): each CTA of the cluster streams JH
+  // columns of every tile and the pair exchanges fp32 Y partials through
+  // distributed shared memory (csize 1: one CTA per segment, JH = Jp)
+  int csize, JH, nseg;
+  uint32_t bstride;    // floats per slice image (Jp x sp)
+  uint32_t off_pbuf;   // peer Y-partial buffers (2 x TM x sp fp32), csize 2
+  double* xsq_hi;      // rank 1's per-piece sums of squares (added by the host), csize 2
   unsigned long long* dbg;  // per-CTA wait-time counters (DP2_TC_DEBUG), or null
   int y32;                  // y_out holds fp32 rows (the accumulator's own precision) instead of fp64
 };
@@ -112,6 +119,47 @@ DP2_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
     if (mbar_try(bar, parity)) return;
     if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
   }
+}
+// cluster-scope variants (J split across a CTA pair)
+DP2_DEV bool mbar_try_cl(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+DP2_DEV void mbar_wait_cl(uint32_t bar, uint32_t parity) {
+  if (mbar_try_cl(bar, parity)) return;
+  const long long t0 = clock64();
+  for (uint32_t n = 1;; ++n) {
+    if (mbar_try_cl(bar, parity)) return;
+    if ((n & 255u) == 0 && clock64() - t0 > 20000000000ll) __trap();
+  }
+}
+DP2_DEV uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// address of the same shared-memory location in CTA `rank` of the cluster
+DP2_DEV uint32_t cl_map(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+DP2_DEV void cl_arrive_remote(uint32_t cl_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_bar) : "memory");
+}
+DP2_DEV void cl_st_v4(uint32_t cl_addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cl_addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+DP2_DEV void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 DP2_DEV unsigned long long gtime() {
   unsigned long long t;
@@ -195,7 +243,9 @@ enum : int {
   BAR_YFULL = 16,   // [2] Y accumulator b holds tile t (P1 commit)
   BAR_YFREE = 18,   // [2] epilogue has read Y accumulator b
   BAR_YSTFREE = 20, // P2 has consumed the Y^T staging buffer
-  BAR_RING = 24     // nss x full, nss x empty
+  BAR_PFULL = 21,   // [2] csize 2: the peer's Y partial of tile t landed in pbuf[t % 2]
+  BAR_PFREE = 23,   // [2] csize 2: the peer has read the partial this CTA wrote into its pbuf[b]
+  BAR_RING = 25     // nss x full, nss x empty
 };
 
 struct Unit {  // 64 rows x 128 columns of one tile
@@ -275,17 +325,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint32_t tmem_slot;
   __shared__ double red[32];
-  const int seg = blockIdx.x;
-  const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg + 1];
-  if (pbeg >= pend) return;
+  // csize 2: the CTA pair (cluster) c walks segments 2c and 2c + 1 (adjacent
+  // row ranges: their pieces are consecutive), CTA rank r over the columns
+  // [r JH, (r + 1) JH) of every tile
+  const int csize = prm.csize;
+  const uint32_t crank = csize > 1 ? cl_rank() : 0u;
+  const int seg = csize > 1 ? (int)(blockIdx.x / 2) * 2 : (int)blockIdx.x;
+  const int seg_end = csize > 1 ? min(seg + 2, prm.nseg) : seg + 1;
+  const int pbeg = prm.seg_begin[seg], pend = prm.seg_begin[seg_end];
+  if (pbeg >= pend) return;  // both CTAs of a pair return together
+  const int j0 = (int)crank * prm.JH;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t base = (su32(smem_raw) + 1023u) & ~1023u;
   unsigned char* gbase = smem_raw + (base - su32(smem_raw));
-  const int J = prm.J, Jp = prm.Jp, sp = prm.sp, n2 = prm.n2, nslot = prm.nslot, nsup = prm.nsup;
+  const int J = prm.J, sp = prm.sp, n2 = prm.n2, nslot = prm.nslot, nsup = prm.nsup;
   const int nss = nslot / 4;  // superslots (4 chunks = one 128-column unit)
   const uint32_t ring = base, bsm = base + prm.off_b, ysm = base + prm.off_y;
   float* yrow = reinterpret_cast<float*>(gbase + prm.off_yrow);
+  const uint32_t pbuf = base + prm.off_pbuf;
+  const float* pbuf_f = reinterpret_cast<const float*>(gbase + prm.off_pbuf);
+  const bool pass2 = prm.y_out != nullptr || prm.g_part != nullptr;  // Y rows and/or G wanted
+  const bool auxon = pass2 && crank == 0;  // the pair's Y rows / G come from rank 0
   const uint32_t bars = base + prm.off_bar;
   auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
 
@@ -294,7 +355,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     mbar_init(bar(BAR_BFREE), 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar(BAR_YFULL + b), 1);
-      mbar_init(bar(BAR_YFREE + b), (prm.y_out || prm.g_part) ? NEPI + NAUX : NEPI);
+      mbar_init(bar(BAR_YFREE + b), auxon ? NEPI + NAUX : NEPI);
+      mbar_init(bar(BAR_PFULL + b), NEPI);  // every main epilogue thread of the peer
+      mbar_init(bar(BAR_PFREE + b), (pass2 && crank == 1) ? NEPI + NAUX : NEPI);  // the peer's readers
     }
     mbar_init(bar(BAR_YSTFREE), 1);
     mbar_init(bar(BAR_YSFULL), NEPI);
@@ -325,6 +388,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
   tc_before();
   __syncthreads();
   tc_after();
+  if (csize > 1) cl_sync();  // the peer's barriers are initialised before any remote arrive
   const uint32_t tmem = tmem_slot;
   const unsigned long long t_start = prm.dbg ? gtime() : 0ull;
   unsigned long long dacc[16] = {};  // wait-time accounting (DP2_TC_DEBUG)
@@ -365,7 +429,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       for (int p = pbeg; p < pend; ++p, ++pidx) {
         if (pidx > 0) TWAIT(bar(BAR_BFREE), (uint32_t)(pidx - 1) & 1u, 1);
         mbar_expect_tx(bar(BAR_BFULL), prm.bbytes);
-        bulk_load(bsm, prm.btile + (size_t)prm.piece_slice[p] * (prm.bbytes / 4), prm.bbytes, bar(BAR_BFULL));
+        bulk_load(bsm, prm.btile + (size_t)prm.piece_slice[p] * prm.bstride + crank * (prm.bbytes / 4), prm.bbytes,
+                  bar(BAR_BFULL));
       }
     }
     if (lane == 0) {
@@ -378,7 +443,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         const int row = (int)(cur.row0 + (int64_t)cur.t * TM);
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)
-          tma_load_2d(ring + (uint32_t)(ss * 4 + ch) * CHUNK, &xmap, cur.jb * 128 + ch * 32, row,
+          tma_load_2d(ring + (uint32_t)(ss * 4 + ch) * CHUNK, &xmap, j0 + cur.jb * 128 + ch * 32, row,
                       bar(BAR_RING + ss));
         if (++ss == nss) { ss = 0; ++fill; }
         cur = next_unit(cur);
@@ -456,7 +521,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
             t += red[w];
             b |= red[16 + w] != 0.0;
           }
-          prm.xsq_part[cur.p] = t;
+          (crank ? prm.xsq_hi : prm.xsq_part)[cur.p] = t;
           if (b) status_min(prm.status, ST_NONFINITE, prm.piece_slice[cur.p]);
         }
         named_sync(1, NXT);
@@ -548,14 +613,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     const int q = warp & 3, et = aux ? tid - AUX0 : tid - EPI0;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     unsigned char* yb = gbase + prm.off_y;
-    const bool pass2 = prm.y_out != nullptr || prm.g_part != nullptr;  // Y rows and/or G wanted
     const bool do_g = prm.g_part != nullptr;
     const int ng = sp * sp;
     double gacc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     uint32_t tcount = 0;
     int pidx = 0;
     const int r = 16 * q + lane;  // M = 64 accumulator: row 16 q + l lives in TMEM lane 32 q + l (l < 16)
-    for (int p = pbeg; p < pend && (!aux || pass2); ++p, ++pidx) {
+    for (int p = pbeg; p < pend && (!aux || auxon); ++p, ++pidx) {
       const int prows = prm.piece_rows[p];
       const int ntiles = (prows + TM - 1) / TM;
       for (int t = 0; t < ntiles; ++t, ++tcount) {
@@ -567,6 +631,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         tmem_ld32(tmem + lane_off + YCOL2 + 32 * b, v);
         tc_before();
         mbar_arrive(bar(BAR_YFREE + b));  // P1 may refill accumulator b once both groups read it
+        if (csize > 1) {
+          // J split: Y_t = own partial + the peer's (fp32 addition commutes, so
+          // both CTAs form the same bits).  The main group sends its partial
+          // into the peer's pbuf[b] once the peer has read tile t - 2 there.
+          const uint32_t peer = crank ^ 1u;
+          const uint32_t roff = (b * TM + (uint32_t)r) * (uint32_t)sp;
+          if (!aux) {
+            if (tcount >= 2) mbar_wait_cl(bar(BAR_PFREE + b), ((tcount >> 1) - 1) & 1u);
+            if (lane < 16) {
+              const uint32_t dst = cl_map(pbuf + roff * 4u, peer);
+#pragma unroll
+              for (int c = 0; c < 32; c += 4)
+                if (c < sp)
+                  cl_st_v4(dst + (uint32_t)c * 4u, __uint_as_float(v[c]), __uint_as_float(v[c + 1]),
+                           __uint_as_float(v[c + 2]), __uint_as_float(v[c + 3]));
+            }
+            cl_arrive_remote(cl_map(bar(BAR_PFULL + b), peer));
+          }
+          mbar_wait_cl(bar(BAR_PFULL + b), (tcount >> 1) & 1u);
+          if (lane < 16)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c < sp) v[c] = __float_as_uint(__uint_as_float(v[c]) + pbuf_f[roff + c]);
+          cl_arrive_remote(cl_map(bar(BAR_PFREE + b), peer));
+        }
         const int rows = min(TM, prows - t * TM);
         const bool valid = lane < 16 && r < rows;
         if (!aux) {
@@ -636,7 +725,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         for (int jb = 0; jb < nsup; ++jb) {
           uint32_t z[32];
           tmem_ld32(tmem + lane_off + ZCOL + jb * 32, z);
-          const int j = jb * 128 + q * 32 + lane;
+          const int j = j0 + jb * 128 + q * 32 + lane;
           if (j < J)
 #pragma unroll
             for (int c = 0; c < 32; ++c)
@@ -667,6 +756,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
 #pragma unroll
     for (int k = 0; k < 16; ++k)
       if (dacc[k]) atomicAdd(prm.dbg + blockIdx.x * 16 + k, dacc[k]);
+  }
+  if (csize > 1) {  // no CTA leaves while its peer may still write its shared memory
+    __syncwarp();
+    cl_sync();
   }
   tc_before();
   __syncthreads();
@@ -703,6 +796,12 @@ __global__ void __launch_bounds__(256) b_tile_kernel(const double* B, int64_t K,
   }
 }
 
+// xsq[p] += hi[p]: the CTA pair's two column halves of each piece's sum of squares
+__global__ void add_pieces_kernel(double* xsq, const double* hi, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) xsq[i] += hi[i];
+}
+
 }  // namespace tcs
 
 namespace {
@@ -722,26 +821,35 @@ void set_sketch_engine(int e) { g_engine = e; }
 int sketch_engine() { return g_engine; }
 
 // shared-memory plan; 0 when the shape is not eligible for the tensor-core pass
+// J <= 512: one CTA per segment over all columns; 512 < J <= 1024: a CTA
+// pair (cluster of 2) per two segments, each CTA over JH = Jp / 2 columns
+// (TMEM holds X^T and Z of at most 512 columns: 64 + 32 TMEM columns per
+// 128 columns of X, plus the Y accumulators)
 static size_t tc_plan(int J, int sp, tcs::Params* prm) {
-  if (J < 1 || J > 512 || sp < 8 || sp > 32 || sp % 8) return 0;
-  const int Jp = (J + 127) / 128 * 128, nch = Jp / 32, n2 = (sp + 15) / 16 * 16;
-  const size_t fixed = (size_t)sp * Jp * 4 + (size_t)2 * n2 * 128 + (size_t)tcs::TM * (sp + 1) * 4;
+  if (J < 1 || J > 1024 || sp < 8 || sp > 32 || sp % 8) return 0;
+  const int csize = J > 512 ? 2 : 1;
+  const int Jp = (J + 128 * csize - 1) / (128 * csize) * (128 * csize), JH = Jp / csize;
+  const int n2 = (sp + 15) / 16 * 16;
+  const size_t pb = csize > 1 ? (size_t)2 * tcs::TM * sp * 4 : 0;
+  const size_t fixed = (size_t)sp * JH * 4 + (size_t)2 * n2 * 128 + (size_t)tcs::TM * (sp + 1) * 4 + pb + 16;
   const size_t cap = 227 * 1024 - 1024 - fixed;
   int nslot = (int)(cap / tcs::CHUNK) / 4 * 4;
   nslot = nslot > 24 ? 24 : nslot;
-  (void)nch;
   if (nslot < 8) return 0;
   const int nss = nslot / 4;
   prm->J = J;
   prm->Jp = Jp;
+  prm->JH = JH;
+  prm->csize = csize;
   prm->sp = sp;
   prm->n2 = n2;
   prm->nslot = nslot;
-  prm->nsup = Jp / 128;
+  prm->nsup = JH / 128;
   prm->off_b = (uint32_t)nslot * tcs::CHUNK;
-  prm->off_y = prm->off_b + (uint32_t)sp * Jp * 4;
+  prm->off_y = prm->off_b + (uint32_t)sp * JH * 4;
   prm->off_yrow = prm->off_y + 2u * n2 * 128;
-  prm->off_bar = (prm->off_yrow + (uint32_t)tcs::TM * (sp + 1) * 4 + 7u) & ~7u;
+  prm->off_pbuf = (prm->off_yrow + (uint32_t)tcs::TM * (sp + 1) * 4 + 15u) & ~15u;
+  prm->off_bar = (prm->off_pbuf + (uint32_t)pb + 7u) & ~7u;
   return prm->off_bar + 8u * (tcs::BAR_RING + 2 * nss) + 1024;
 }
 
@@ -766,10 +874,13 @@ bool sketch_tc_eligible(const dp2_store* st, int sp) {
          tc_plan((int)st->J, sp, &prm) != 0 && encode_fn() != nullptr;
 }
 
-// per-device scratch for the pre-tiled B images (grown on demand, kept)
-static float* btile_scratch(size_t bytes, cudaError_t* err) {
-  static float* buf[64] = {};
-  static size_t cap[64] = {};
+// per-device scratch (grown on demand, kept): the pre-tiled B images (slot
+// 0) and rank 1's per-piece sums of squares of the CTA-pair pass (slot 1)
+static float* btile_scratch(size_t bytes, cudaError_t* err, int slot = 0) {
+  static float* bufs[2][64] = {};
+  static size_t caps[2][64] = {};
+  float** buf = bufs[slot];
+  size_t* cap = caps[slot];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) {
@@ -795,10 +906,16 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
   const size_t smem = tc_plan((int)st->J, sp, &prm);
   if (smem == 0 || encode_fn() == nullptr) return cudaErrorInvalidValue;
   // B images: one bulk copy per piece replaces per-element conversion in the kernel
-  prm.bbytes = (uint32_t)prm.Jp * sp * 4;
+  prm.bbytes = (uint32_t)prm.JH * sp * 4;  // the part one CTA loads
+  prm.bstride = (uint32_t)prm.Jp * sp;     // floats per slice image
+  prm.nseg = st->nseg;
   cudaError_t be;
-  float* bt = btile_scratch((size_t)st->K * prm.bbytes, &be);
+  float* bt = btile_scratch((size_t)st->K * prm.bstride * 4, &be);
   if (!bt) return be;
+  if (prm.csize > 1 && xsq_part) {
+    prm.xsq_hi = reinterpret_cast<double*>(btile_scratch((size_t)st->npieces * 8, &be, 1));
+    if (!prm.xsq_hi) return be;
+  }
   tcs::b_tile_kernel<<<(unsigned)(st->K < 2048 ? st->K : 2048), 256, 0, stream>>>(B, st->K, prm.J, prm.Jp, sp, bt);
   prm.btile = bt;
   // X as a 2-D tensor (J columns, total_rows rows, row pitch ldx*4 B); boxes
@@ -834,8 +951,29 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
     cudaMalloc(&prm.dbg, (size_t)st->nseg * 16 * sizeof(unsigned long long));
     cudaMemsetAsync(prm.dbg, 0, (size_t)st->nseg * 16 * sizeof(unsigned long long), stream);
   }
-  tcs::sketch_tc_kernel<<<st->nseg, tcs::NTHREADS, smem, stream>>>(prm, xmap);
-  e = cudaGetLastError();
+  if (prm.csize == 1) {
+    tcs::sketch_tc_kernel<<<st->nseg, tcs::NTHREADS, smem, stream>>>(prm, xmap);
+    e = cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * ((st->nseg + 1) / 2)));
+    cfg.blockDim = dim3(tcs::NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, tcs::sketch_tc_kernel, prm, xmap);
+    if (e == cudaSuccess && xsq_part) {
+      tcs::add_pieces_kernel<<<(unsigned)((st->npieces + 255) / 256), 256, 0, stream>>>(xsq_part, prm.xsq_hi,
+                                                                                       st->npieces);
+      e = cudaGetLastError();
+    }
+  }
   if (debug && e == cudaSuccess) {
     std::vector<unsigned long long> h((size_t)st->nseg * 16);
     cudaMemcpyAsync(h.data(), prm.dbg, h.size() * 8, cudaMemcpyDeviceToHost, stream);

@@ -152,6 +152,20 @@ def test_c5_shaped_subset_fp32():
     print(f"c5 subset (K=96, J=1000): fitness {fit:.8f} oracle {fit_o:.8f}; {errs}")
 
 
+def test_c5_shaped_subset_tf32_mode():
+    """J = 1000 in the opt-in tf32 mode: the tcgen05 pass on a CTA pair (J split)."""
+    import paper_2203_12798_b200 as dp
+    from paper_2203_12798_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS["c5"], num_slices=96)
+    xs = synth.generate(cfg, 0, threads=_threads())
+    prev = dp.set_fp32_products("tf32")
+    try:
+        errs, fit, fit_o = _compare(xs, 10, 32, "f32", FP32)
+    finally:
+        dp.set_fp32_products(prev)
+    print(f"c5 subset tf32 (K=96, J=1000): fitness {fit:.8f} oracle {fit_o:.8f}; {errs}")
+
+
 def test_c5_shaped_subset_fp64():
     """The J = 1000 shape through the fp64 path (DMMA pass at J > 512)."""
     from paper_2203_12798_b200 import synth

@@ -72,6 +72,13 @@ SHAPES = [
     ([90, 33, 400], 100, 8, 2),
     ([256, 129], 300, 32, 3),
     ([700] * 6, 512, 16, 5),
+    # J > 512: the tensor-core pass splits the columns across a CTA pair
+    # (cluster of 2, Y partials exchanged through distributed shared memory);
+    # odd nseg leaves the last pair one segment
+    ([300, 500, 257, 64], 1000, 24, 5),
+    ([700, 700, 700], 1024, 16, 4),
+    ([130, 1, 77, 260], 600, 8, 3),
+    ([400, 900], 520, 32, 6),
 ]
 
 
@@ -95,6 +102,28 @@ def test_stream_pass_matches_numpy(engine, case):
         # tensor-core pass: fp32 partials of 32 squares, fp64 across them
         assert abs(res["sq"][p] - np.sum(Xp * Xp)) <= (1e-6 if engine == 0 else 1e-9) * np.sum(Xp * Xp), p
     assert res["status"][0] == _lib.INT64_MAX
+
+
+@pytest.mark.parametrize("J", [600, 1000, 1024])
+def test_stream_pass_tc_pair_eligible(J):
+    """512 < J <= 1024 runs the tcgen05 CTA-pair pass (not a fallback) in the tf32 mode."""
+    import ctypes as C
+    slices = [np.ones((70, J), np.float32)]
+    t = dp.IrregularTensor.from_packed(torch.from_numpy(np.concatenate(slices)).cuda(), [70], J, check=False)
+    st, keep = t.store(4)
+    prev = _lib.lib().dp2_set_sketch_engine(0)
+    try:
+        assert _lib.lib().dp2_sketch_uses_tc(C.byref(st), 24) == 1
+    finally:
+        _lib.lib().dp2_set_sketch_engine(prev)
+
+
+def test_stream_pass_tc_pair_flags_nonfinite():
+    rng = np.random.default_rng(4)
+    slices = [rng.standard_normal((m, 1000)) for m in (100, 150, 80)]
+    slices[2][40, 900] = np.nan  # in the second CTA's column half
+    *_, res = run_pass(slices, 1000, 24, 3, 0)
+    assert res["status"][0] == 2
 
 
 def test_stream_pass_tc_flags_nonfinite():

@@ -40,7 +40,11 @@ def main():
     ap.add_argument("--configs", default="c1,c3,c5shard")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fp32-products", default=None, choices=["fp64", "fp32", "tf32"],
+                    help="products of fp32-storage tensors (default: the library default, fp64 DMMA)")
     a = ap.parse_args()
+    if a.fp32_products:
+        dp.set_fp32_products(a.fp32_products)
     out = {}
     for name in a.configs.split(","):
         cfg, ids = workload(name)
@@ -65,7 +69,10 @@ def main():
                    entries=entries, ms_per_fit=ms, entries_per_s=entries / (ms * 1e-3),
                    stage1_ms=tm["stage1_ms"], sketch_pass_ms=[tm["stage1_sketch1_ms"], tm["stage1_sketch2_ms"]],
                    stage2_ms=tm["stage2_ms"], als_per_iter_us=float(np.mean(tr.seconds)) * 1e6,
-                   fitness=dp.fitness(t, f), generation_s=gen_s)
+                   fitness=dp.fitness(t, f), generation_s=gen_s,
+                   fp32_products=a.fp32_products or "default")
+        w = 8 if cfg.dtype == "f64" else 4
+        rec["pass_hbm_gbs"] = [entries * w / (ms_ * 1e-3) / 1e9 for ms_ in rec["sketch_pass_ms"]]
         out[name] = rec
         print(name, json.dumps(rec), flush=True)
         del t, X, f
