@@ -41,6 +41,7 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 #include <cudaTypedefs.h>
 
@@ -84,6 +85,7 @@ struct Params {
   // columns of every tile and the pair exchanges fp32 Y partials through
   // distributed shared memory (csize 1: one CTA per segment, JH = Jp)
   int csize, JH, nseg;
+  int nxs, zcol, ycol;  // TMEM plan: X^T slots, Z and Y column bases
   uint32_t bstride;    // floats per slice image (Jp x sp)
   uint32_t off_pbuf;   // peer Y-partial buffers (2 x TM x sp fp32), csize 2
   double* xsq_hi;      // rank 1's per-piece sums of squares (added by the host), csize 2
@@ -239,13 +241,13 @@ DP2_DEV uint32_t swz(int row, int col) {
 // barrier slots (uint64 each) after off_bar
 enum : int {
   BAR_BFULL = 0, BAR_BFREE, BAR_YSFULL = 3, BAR_ZFULL, BAR_ZFREE,
-  BAR_XT = 8,       // 4 x (full, free) for the TMEM X^T blocks
   BAR_YFULL = 16,   // [2] Y accumulator b holds tile t (P1 commit)
   BAR_YFREE = 18,   // [2] epilogue has read Y accumulator b
   BAR_YSTFREE = 20, // P2 has consumed the Y^T staging buffer
   BAR_PFULL = 21,   // [2] csize 2: the peer's Y partial of tile t landed in pbuf[t % 2]
   BAR_PFREE = 23,   // [2] csize 2: the peer has read the partial this CTA wrote into its pbuf[b]
-  BAR_RING = 25     // nss x full, nss x empty
+  BAR_XT = 26,      // up to 8 x (full, free) for the TMEM X^T slots
+  BAR_RING = 42     // nss x full, nss x empty
 };
 
 struct Unit {  // 64 rows x 128 columns of one tile
@@ -318,8 +320,9 @@ DP2_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, u
       : "memory");
 }
 
-// TMEM columns: X^T blocks [0, 64 nsup), Z [XT_END, +32 nsup), Y [YCOL2, +32)
-constexpr int ZCOL = 256, YCOL2 = 384;
+// TMEM columns: nxs X^T slots of 64 columns [0, 64 nxs) -- a ring over the
+// units (tile, 128-column block), nxs > nsup so the X^T producers can run
+// ahead of P2 into the next tile --, Z [zcol, +32 nsup), Y [ycol, +64)
 
 __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     mbar_init(bar(BAR_YSFULL), NEPI);
     mbar_init(bar(BAR_ZFULL), 1);
     mbar_init(bar(BAR_ZFREE), NEPI);
-    for (int jb = 0; jb < 4; ++jb) {
+    for (int jb = 0; jb < prm.nxs; ++jb) {
       mbar_init(bar(BAR_XT + 2 * jb), NXT / 32);
       mbar_init(bar(BAR_XT + 2 * jb + 1), 1);
     }
@@ -463,7 +466,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     double sq = 0.0;
     int bad = 0;
     Unit cur = first_unit(pbeg);
-    uint32_t tcount = 0, rph = 0;  // ring slot ss = ucount % nss with parity rph = (ucount / nss) & 1
+    uint32_t rph = 0;  // ring slot ss = ucount % nss with parity rph = (ucount / nss) & 1
+    int xs = 0;        // X^T slot = ucount % nxs, used for the xuse-th time
+    uint32_t xuse = 0;
     int ss = 0;
     while (cur.p < pend) {
       if (tid == 0) TWAIT(bar(BAR_RING + ss), rph, 2);
@@ -495,17 +500,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = tf32r(v[i]);
-      if (tcount > 0) {
-        if (tid == 0) TWAIT(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u, 3);
-        else mbar_wait(bar(BAR_XT + 2 * cur.jb + 1), (tcount - 1) & 1u);
+      if (xuse > 0) {
+        if (tid == 0) TWAIT(bar(BAR_XT + 2 * xs + 1), (xuse - 1) & 1u, 3);
+        else mbar_wait(bar(BAR_XT + 2 * xs + 1), (xuse - 1) & 1u);
       }
       tc_after();
-      tmem_st32(tmem + lane_off + (uint32_t)(cur.jb * 64 + 32 * h), v);
+      tmem_st32(tmem + lane_off + (uint32_t)(xs * 64 + 32 * h), v);
       tc_before();
-      warp_arrive(bar(BAR_XT + 2 * cur.jb));
+      warp_arrive(bar(BAR_XT + 2 * xs));
+      if (++xs == prm.nxs) { xs = 0; ++xuse; }
       if (++ss == nss) { ss = 0; rph ^= 1u; }
       const Unit nx = next_unit(cur);
-      if (nx.jb == 0) ++tcount;
       if (nx.p != cur.p && stats) {  // piece complete: sum of squares, non-finite flag
         const double tot = warp_sum(sq);
         const int anybad = __any_sync(0xffffffffu, bad);
@@ -543,8 +548,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     const uint32_t lbo = 1u << 16;
     const uint32_t ring_lo = (ring >> 4) | lbo, b_lo = (bsm >> 4) | lbo, y_lo = (ysm >> 4) | lbo;
     const uint32_t bch = (uint32_t)sp * 8;  // one 32-column chunk of B^T, in 16 B units
-    uint32_t tcount = 0, rph = 0;
-    int ss = 0, pidx = 0;
+    uint32_t tcount = 0, rph = 0, xuse = 0;
+    int ss = 0, pidx = 0, xs = 0;
+    const uint32_t zcol = (uint32_t)prm.zcol, ycol = (uint32_t)prm.ycol;
 #define MWAIT(barexpr, par, k)        \
   do {                                \
     if (lane == 0)                    \
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
             for (int ch = 0; ch < 4; ++ch)
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                tc_mma_ss_e(tmem + YCOL2 + 32 * b, a0 + ch * (CHUNK / 16) + kk * 2, b0 + ch * bch + kk * 2, dhi,
+                tc_mma_ss_e(tmem + ycol + 32 * b, a0 + ch * (CHUNK / 16) + kk * 2, b0 + ch * bch + kk * 2, dhi,
                             id1, (jb | ch | kk) != 0);
             tc_commit_e(bar(BAR_RING + nss + ss));
             if (prm.dbg && lane == 0) dacc[11] += gtime() - tp1;
@@ -587,14 +593,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
           if (t == 0 && pidx > 0) MWAIT(bar(BAR_ZFREE), (uint32_t)(pidx - 1) & 1u, 7);
           tc_after();
           for (int jb = 0; jb < nsup; ++jb) {
-            MWAIT(bar(BAR_XT + 2 * jb), tcount & 1u, 8);
+            MWAIT(bar(BAR_XT + 2 * xs), xuse & 1u, 8);
             tc_after();
             const unsigned long long tp2 = prm.dbg ? gtime() : 0ull;
 #pragma unroll
             for (int k = 0; k < TM / 8; ++k)
-              tc_mma_ts_e(tmem + ZCOL + jb * 32, tmem + jb * 64 + k * 8, y_lo + (k >> 2) * (n2 * 8) + (k & 3) * 2,
+              tc_mma_ts_e(tmem + zcol + jb * 32, tmem + xs * 64 + k * 8, y_lo + (k >> 2) * (n2 * 8) + (k & 3) * 2,
                           dhi, id2, (t > 0 || k > 0) ? 1u : 0u);
-            tc_commit_e(bar(BAR_XT + 2 * jb + 1));
+            tc_commit_e(bar(BAR_XT + 2 * xs + 1));
+            if (++xs == prm.nxs) { xs = 0; ++xuse; }
             if (prm.dbg && lane == 0) dacc[12] += gtime() - tp2;
           }
           tc_commit_e(bar(BAR_YSTFREE));
@@ -628,7 +635,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         else mbar_wait(bar(BAR_YFULL + b), (tcount >> 1) & 1u);
         tc_after();
         uint32_t v[32];
-        tmem_ld32(tmem + lane_off + YCOL2 + 32 * b, v);
+        tmem_ld32(tmem + lane_off + prm.ycol + 32 * b, v);
         tc_before();
         mbar_arrive(bar(BAR_YFREE + b));  // P1 may refill accumulator b once both groups read it
         if (csize > 1) {
@@ -724,7 +731,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
         double* out = prm.out_part + (size_t)p * J * sp;
         for (int jb = 0; jb < nsup; ++jb) {
           uint32_t z[32];
-          tmem_ld32(tmem + lane_off + ZCOL + jb * 32, z);
+          tmem_ld32(tmem + lane_off + prm.zcol + jb * 32, z);
           const int j = j0 + jb * 128 + q * 32 + lane;
           if (j < J)
 #pragma unroll
@@ -845,6 +852,10 @@ static size_t tc_plan(int J, int sp, tcs::Params* prm) {
   prm->n2 = n2;
   prm->nslot = nslot;
   prm->nsup = JH / 128;
+  // TMEM: Z 32 nsup + Y 64 columns, the rest (<= 8 slots) X^T
+  prm->nxs = std::min(8, (512 - 32 * prm->nsup - 64) / 64);
+  prm->zcol = 64 * prm->nxs;
+  prm->ycol = prm->zcol + 32 * prm->nsup;
   prm->off_b = (uint32_t)nslot * tcs::CHUNK;
   prm->off_y = prm->off_b + (uint32_t)sp * JH * 4;
   prm->off_yrow = prm->off_y + 2u * n2 * 128;
@@ -967,6 +978,12 @@ cudaError_t run_sketch_tc(const dp2_store* st, const double* B, int sp, double* 
     cfg.stream = stream;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (getenv("DP2_TC_DEBUG")) {
+      int ncl = 0;
+      cudaOccupancyMaxActiveClusters(&ncl, (void*)tcs::sketch_tc_kernel, &cfg);
+      fprintf(stderr, "[dp2 tc] CTA pairs: %u launched, %d co-resident, smem %zu, JH %d, nslot %d\n",
+              cfg.gridDim.x / 2, ncl, smem, prm.JH, prm.nslot);
+    }
     e = cudaLaunchKernelEx(&cfg, tcs::sketch_tc_kernel, prm, xmap);
     if (e == cudaSuccess && xsq_part) {
       tcs::add_pieces_kernel<<<(unsigned)((st->npieces + 255) / 256), 256, 0, stream>>>(xsq_part, prm.xsq_hi,
