@@ -160,6 +160,9 @@ DP2_DEV void cl_st_v4(uint32_t cl_addr, float a, float b, float c, float d) {
   asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cl_addr), "f"(a), "f"(b), "f"(c), "f"(d)
                : "memory");
 }
+DP2_DEV void cl_st_f32(uint32_t cl_addr, float a) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cl_addr), "f"(a) : "memory");
+}
 DP2_DEV void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -359,8 +362,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar(BAR_YFULL + b), 1);
       mbar_init(bar(BAR_YFREE + b), auxon ? NEPI + NAUX : NEPI);
-      mbar_init(bar(BAR_PFULL + b), NEPI);  // every main epilogue thread of the peer
-      mbar_init(bar(BAR_PFREE + b), (pass2 && crank == 1) ? NEPI + NAUX : NEPI);  // the peer's readers
+      mbar_init(bar(BAR_PFULL + b), NEPI / 32);  // one per main epilogue warp of the peer
+      mbar_init(bar(BAR_PFREE + b), (pass2 && crank == 1) ? (NEPI + NAUX) / 32 : NEPI / 32);  // the peer's readers
     }
     mbar_init(bar(BAR_YSTFREE), 1);
     mbar_init(bar(BAR_YSFULL), NEPI);
@@ -642,26 +645,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch_tc_kernel(Params prm, cons
           // J split: Y_t = own partial + the peer's (fp32 addition commutes, so
           // both CTAs form the same bits).  The main group sends its partial
           // into the peer's pbuf[b] once the peer has read tile t - 2 there.
+          // pbuf[b] is column-major (TM rows per column): 16 lanes store / load
+          // 64 contiguous bytes per column, conflict-free.  One remote arrive
+          // per warp: __syncwarp orders the lanes' accesses before lane 0's
+          // release at cluster scope.
           const uint32_t peer = crank ^ 1u;
-          const uint32_t roff = (b * TM + (uint32_t)r) * (uint32_t)sp;
+          const uint32_t roff = b * (uint32_t)sp * TM + (uint32_t)r;
           if (!aux) {
             if (tcount >= 2) mbar_wait_cl(bar(BAR_PFREE + b), ((tcount >> 1) - 1) & 1u);
             if (lane < 16) {
               const uint32_t dst = cl_map(pbuf + roff * 4u, peer);
 #pragma unroll
-              for (int c = 0; c < 32; c += 4)
-                if (c < sp)
-                  cl_st_v4(dst + (uint32_t)c * 4u, __uint_as_float(v[c]), __uint_as_float(v[c + 1]),
-                           __uint_as_float(v[c + 2]), __uint_as_float(v[c + 3]));
+              for (int c = 0; c < 32; ++c)
+                if (c < sp) cl_st_f32(dst + (uint32_t)(c * TM) * 4u, __uint_as_float(v[c]));
             }
-            cl_arrive_remote(cl_map(bar(BAR_PFULL + b), peer));
+            __syncwarp();
+            if (lane == 0) cl_arrive_remote(cl_map(bar(BAR_PFULL + b), peer));
           }
           mbar_wait_cl(bar(BAR_PFULL + b), (tcount >> 1) & 1u);
           if (lane < 16)
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              if (c < sp) v[c] = __float_as_uint(__uint_as_float(v[c]) + pbuf_f[roff + c]);
-          cl_arrive_remote(cl_map(bar(BAR_PFREE + b), peer));
+              if (c < sp) v[c] = __float_as_uint(__uint_as_float(v[c]) + pbuf_f[roff + c * TM]);
+          __syncwarp();
+          if (lane == 0) cl_arrive_remote(cl_map(bar(BAR_PFREE + b), peer));
         }
         const int rows = min(TM, prows - t * TM);
         const bool valid = lane < 16 && r < rows;
