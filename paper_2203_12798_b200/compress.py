@@ -91,10 +91,11 @@ _FP32_ENGINES = {"tf32": 0, "fp32": 1, "fp64": 2}
 def set_fp32_products(mode):
     """Arithmetic of the stage-1 sketch products for fp32-storage tensors:
     ``"fp64"`` (default; fp64 DMMA products on the exactly upcast values where
-    the warp-specialised pass applies, J <= 512, else ``"fp32"``), ``"fp32"``
+    the warp-specialised pass applies, J <= 1024, else ``"fp32"``), ``"fp32"``
     (FFMA products, fp32 accumulation within a tile, fp64 across tiles -- the
     fp32 mode of BASELINE.json) or ``"tf32"`` (opt-in speed mode: single-pass
-    tf32 products on the tcgen05 tensor cores, ~5e-4 relative product error).
+    tf32 products on the tcgen05 tensor cores, ~5e-4 relative product error;
+    J <= 1024, above 512 on CTA pairs splitting the columns).
     Returns the previous mode."""
     if mode not in _FP32_ENGINES:
         raise ValueError(f"fp32 product mode must be one of {sorted(_FP32_ENGINES)}, got {mode!r}")

@@ -29,9 +29,22 @@
 //               into shared memory as P2's K-major B operand, the non-finite
 //               flag, and the per-piece Z flush (TMEM lanes = columns of X).
 //   warps 15-18 pass 2: Y rows out (coalesced through shared memory).
-// TMEM: X^T blocks in columns [0, 256), Z in [256, 384), Y double-buffered in
-// [384, 448).  Ring slots are released right after P1, the X^T blocks after
-// P2, so HBM streaming overlaps both products.
+// TMEM: a ring of nxs X^T slots of 64 columns (nxs = 5 at J = 512: one unit
+// more than a tile, so the X^T producers run ahead of P2 into the next tile),
+// Z (32 columns per 128 columns of X), Y double-buffered (64 columns).  Ring
+// slots are released right after P1, the X^T slots after P2, so HBM
+// streaming overlaps both products.
+//
+// 512 < J <= 1024 (c5): X^T and Z of all J columns exceed TMEM, so a CTA
+// pair (thread-block cluster of 2) shares each pair of segments: CTA r
+// streams columns [r JH, (r + 1) JH) of every tile (JH = Jp / 2 <= 512) and
+// loads its half of the B image; P1 yields a partial Y_t over those columns,
+// the main epilogue group stores it into the peer's shared memory
+// (st.shared::cluster, one remote mbarrier arrive per warp), and each CTA
+// adds the two partials (fp32 addition commutes: both hold the same Y_t) to
+// stage Y^T for its own P2, Z over its columns and the Z flush of its rows of
+// the partial.  Rank 0 writes Y rows / G (pass 2); rank 1's per-piece sums of
+// squares go to a scratch array that a small kernel adds.
 //
 // Precision: products in tf32 (10-bit mantissa, round-to-nearest on both
 // operands), fp32 accumulation within a piece, fp64 partials across pieces --
