@@ -16,12 +16,12 @@
 //   producer (1 warp)   TMA bulk copies: X rows of tile n into ring stage n % NS
 //                       (padded row stride: conflict-free fragment loads), and
 //                       per piece the slice's B image (fragment-major, one
-//                       bulk copy per quarter of J).
-//   A warps (4)         Y_t (8 x SG) partial over their quarter of J:
+//                       bulk copy per A warp share of J).
+//   A warps (8)         Y_t (8 x SG) partial over their eighth of J:
 //                       DMMA m8n8k4 with B fragments from the shared image
 //                       (two accumulator sets to halve the dependent chain);
 //                       partial -> ypart ring.
-//   aux (1 warp)        sums the 4 partials -> Y_t (rows past the piece zeroed),
+//   aux (2 warps)       sum the 8 partials -> Y_t (half of its fragments each) (rows past the piece zeroed),
 //                       publishes it in B-fragment layout (yfin ring), flags
 //                       non-finite values (status word 0 = lowest slice: a
 //                       NaN / Inf anywhere in X_k reaches Y), writes Y rows.
@@ -44,14 +44,25 @@ namespace dp2 {
 namespace s64 {
 
 constexpr int TMAX = 16;        // rows per tile: TM = 8 (J > 256 per CTA), 16 (J <= 256)
-constexpr int NA = 4;           // warps computing Y partials (split of J)
+constexpr int NA = 8;           // warps computing Y partials (split of J): two per SM sub-partition
 constexpr int NB = 16;          // warps accumulating Z (split of J)
 constexpr int NY = 2;           // ypart / yfin ring depth
-// warp w runs on SM sub-partition w % 4: one A warp and four B warps per
-// sub-partition keep the DMMA work per sub-partition equal
+// warp w runs on SM sub-partition w % 4: two A warps and four B warps per
+// sub-partition keep the DMMA work per sub-partition equal.  A lone
+// shared-memory-fed DMMA stream reaches only 76% of the pipe rate, two reach
+// 95% (tools/dmma_lds_probe.cu), so the A product -- the critical path, which
+// runs alone whenever the B warps wait for Y_t -- is spread over two warps per
+// sub-partition.  The A and B roles fill whole warpgroups (4 warps) so that
+// setmaxnreg can move registers from the A warps to the B warps (24
+// accumulator doubles each): 26 warps launch with 72 registers per thread.
 constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
-constexpr int NWARPS = 2 + NA + NB;
+constexpr int NAUX = 2;         // warps summing the partials into Y_t (a split of its fragments)
+constexpr int NWARPS = 1 + NAUX + NA + NB;
 constexpr int NTHREADS = 32 * NWARPS;
+constexpr int REGS_LAUNCH = 65536 / NTHREADS / 8 * 8;  // what __launch_bounds__(NTHREADS, 1) allows
+constexpr int REGS_A = 56, REGS_B = 80;
+static_assert(NA % 4 == 0 && NB % 4 == 0, "the A and B roles fill whole warpgroups");
+static_assert(NA * REGS_A + NB * REGS_B <= (NA + NB) * REGS_LAUNCH, "the B warps' increase comes from the A warps");
 
 struct Params {
   const void* X;
@@ -147,6 +158,10 @@ DP2_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
 DP2_DEV void st_cluster_v2(uint32_t cluster_addr, double a, double b) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(cluster_addr), "d"(a), "d"(b) : "memory");
 }
+template <int N>
+DP2_DEV void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+DP2_DEV void reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
 DP2_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -219,8 +234,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     }
     for (int b = 0; b < NY; ++b) {
       mbar_init(bar(B_YPFULL + b), CL * NA);  // both CTAs' A warps
-      mbar_init(bar(B_YPEMPTY + b), CL);      // both CTAs' aux warps read this CTA's partials
-      mbar_init(bar(B_YFULL + b), 1);
+      mbar_init(bar(B_YPEMPTY + b), CL * NAUX);  // both CTAs' aux warps read this CTA's partials
+      mbar_init(bar(B_YFULL + b), NAUX);
       mbar_init(bar(B_YEMPTY + b), NB);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -235,7 +250,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
   unsigned long long dacc[DBG ? D_N : 1] = {};
   const long long tstart = DBG ? clock64() : 0;
 
-  if (warp == WARP_PROD) {
+  // ------------------------------------------------------------ aux: Y_t, Y rows, non-finite
+  // aux warp ax owns the fragments f = k2 NT + j with f % NAUX == ax
+  auto aux_role = [&](const int ax) {
+    constexpr int NF = (K2 * NT + NAUX - 1) / NAUX;
+    int n = 0;
+    for (int p = pbeg; p < pend; ++p) {
+      const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
+      const int64_t row0 = prm.piece_row0[p];
+      int bad = 0;
+      for (int t = 0; t * TM < rows; ++t, ++n) {
+        const int b = n % NY;
+        const int valid = min(TM, rows - t * TM);
+        if constexpr (CL == 2) S64_WAIT_CL(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
+        else S64_WAIT(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
+        if (n >= NY) S64_WAIT(bar(B_YEMPTY + b), ((n / NY) - 1) & 1, D_YEMPTY);
+        // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
+        //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
+        double* yf = yfin + (size_t)b * K2 * NT * 32;
+        const double* ypb = ypart + (size_t)b * CL * NA * TM * SG;
+        double fr[NF];
+#pragma unroll
+        for (int i = 0; i < NF; ++i) {
+          const int f = ax + i * NAUX;
+          if (f < K2 * NT) {
+            const int k2 = f / NT, j = f - k2 * NT;
+            const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
+            double v = 0.0;  // slots in pair order (CTA 0's partials, then CTA 1's): same sum in both CTAs
+#pragma unroll
+            for (int aa = 0; aa < CL * NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
+            v = row < valid ? v : 0.0;
+            bad |= !isfinite(v);
+            fr[i] = v;
+            yf[f * 32 + lane] = v;
+          }
+        }
+        warp_arrive(bar(B_YFULL + b));
+        warp_arrive(bar(B_YPEMPTY + b));
+        if constexpr (CL == 2) {
+          if (lane == 0) mbar_arrive_cluster(mapa(bar(B_YPEMPTY + b), peer));
+        }
+        if (prm.y_out != nullptr && crank == 0) {
+#pragma unroll
+          for (int i = 0; i < NF; ++i) {
+            const int f = ax + i * NAUX;
+            if (f < K2 * NT) {
+              const int k2 = f / NT, j = f - k2 * NT;
+              const int row = 4 * k2 + (lane & 3), col = col0 + 8 * j + (lane >> 2);
+              if (row < valid && col < sp) prm.y_out[(row0 + (int64_t)t * TM + row) * sp + col] = fr[i];
+            }
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) status_min(prm.status, ST_NONFINITE, ks);
+    }
+  };
+  // the A and B warpgroups first re-balance their registers (REGS_*)
+  if (warp >= WARP_PROD) {
+   if (warp == WARP_PROD) {
     // ------------------------------------------------------------ producer
     const char* Xb = reinterpret_cast<const char*>(prm.X);
     const uint32_t qbytes = (uint32_t)ksq * NT * 32 * 8;
@@ -244,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
       const int64_t row0 = prm.piece_row0[p];
       const int pi = p - pbeg;
-      // B image of this slice, quarter by quarter as each A warp frees it
+      // B image of this slice, share by share as each A warp frees it
       const double* src = prm.img + ((size_t)ks * ng + grp) * (size_t)(JP / 4) * NT * 32 +
                           (size_t)crank * (JH / 4) * NT * 32;
       if (lane < NA) {
@@ -267,7 +339,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
                     bar(B_XFULL + s));
       }
     }
-  } else if (warp >= WARP_A0 && warp < WARP_A0 + NA) {
+   } else {
+    aux_role(warp - WARP_AUX);
+   }
+  } else if (warp < WARP_A0 + NA) {
+    reg_dec<REGS_A>();
     // ------------------------------------------------------------ A warps: Y partials
     const int a = warp - WARP_A0;
     const int r = lane >> 2, q = lane & 3;
@@ -328,55 +404,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       }
       warp_arrive(bar(B_OEMPTY + a));
     }
-  } else if (warp == WARP_AUX) {
-    // ------------------------------------------------------------ aux: Y_t, Y rows, non-finite
-    int n = 0;
-    for (int p = pbeg; p < pend; ++p) {
-      const int ks = prm.piece_slice[p], rows = prm.piece_rows[p];
-      const int64_t row0 = prm.piece_row0[p];
-      int bad = 0;
-      for (int t = 0; t * TM < rows; ++t, ++n) {
-        const int b = n % NY;
-        const int valid = min(TM, rows - t * TM);
-        if constexpr (CL == 2) S64_WAIT_CL(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
-        else S64_WAIT(bar(B_YPFULL + b), (n / NY) & 1, D_YPFULL);
-        if (n >= NY) S64_WAIT(bar(B_YEMPTY + b), ((n / NY) - 1) & 1, D_YEMPTY);
-        // element e of the B-fragment image: ks2 = e / (NT*32), j = (e / 32) % NT, lane' = e % 32
-        //   -> Y[4 ks2 + (lane' & 3)][8 j + (lane' >> 2)]
-        double* yf = yfin + (size_t)b * K2 * NT * 32;
-        const double* ypb = ypart + (size_t)b * CL * NA * TM * SG;
-        double fr[K2][NT];
-#pragma unroll
-        for (int k2 = 0; k2 < K2; ++k2)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) {
-            const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
-            double v = 0.0;  // slots in pair order (CTA 0's partials, then CTA 1's): same sum in both CTAs
-#pragma unroll
-            for (int aa = 0; aa < CL * NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
-            v = row < valid ? v : 0.0;
-            bad |= !isfinite(v);
-            fr[k2][j] = v;
-            yf[(k2 * NT + j) * 32 + lane] = v;
-          }
-        warp_arrive(bar(B_YFULL + b));
-        warp_arrive(bar(B_YPEMPTY + b));
-        if constexpr (CL == 2) {
-          if (lane == 0) mbar_arrive_cluster(mapa(bar(B_YPEMPTY + b), peer));
-        }
-        if (prm.y_out != nullptr && crank == 0) {
-#pragma unroll
-          for (int k2 = 0; k2 < K2; ++k2)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              const int row = 4 * k2 + (lane & 3), col = col0 + 8 * j + (lane >> 2);
-              if (row < valid && col < sp) prm.y_out[(row0 + (int64_t)t * TM + row) * sp + col] = fr[k2][j];
-            }
-        }
-      }
-      if (__any_sync(0xffffffffu, bad) && lane == 0) status_min(prm.status, ST_NONFINITE, ks);
-    }
   } else {
+    reg_inc<REGS_B>();
     // ------------------------------------------------------------ B warps: Z += X_t^T Y_t
     const int bw = warp - WARP_B0;
     // J-blocks of 8 per B warp: <= 4 at J <= 512; J <= 1024 runs one sketch
@@ -657,7 +686,7 @@ cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg,
     for (size_t c = 0; c < (size_t)nseg * pl.CL * pl.ng; ++c)
       for (int w = 0; w < NWARPS; ++w) {
         const int r = (w >= WARP_A0 && w < WARP_A0 + NA) ? 0 : (w >= WARP_B0 && w < WARP_B0 + NB) ? 1
-                      : w == WARP_PROD ? 2 : 3;
+                      : w == WARP_PROD ? 2 : 3;  // every aux warp
         if (r != role) continue;
         ++cnt;
         for (int i = 0; i < D_N; ++i) acc[i] += (double)dh[(c * NWARPS + w) * D_N + i];
