@@ -52,17 +52,20 @@ constexpr int NY = 2;           // ypart / yfin ring depth
 // shared-memory-fed DMMA stream reaches only 76% of the pipe rate, two reach
 // 95% (tools/dmma_lds_probe.cu), so the A product -- the critical path, which
 // runs alone whenever the B warps wait for Y_t -- is spread over two warps per
-// sub-partition.  The A and B roles fill whole warpgroups (4 warps) so that
-// setmaxnreg can move registers from the A warps to the B warps (24
-// accumulator doubles each): 26 warps launch with 72 registers per thread.
+// sub-partition.  Every role group fills whole warpgroups (4 warps; the last
+// one is the producer, the aux warps and an idle warp) so that setmaxnreg can
+// move registers from the other groups to the B warps (24 accumulator doubles
+// each): 28 warps launch with 72 registers per thread.
 constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
 constexpr int NAUX = 2;         // warps summing the partials into Y_t (a split of its fragments)
-constexpr int NWARPS = 1 + NAUX + NA + NB;
+constexpr int NMISC = 4;        // producer + aux warps, padded to a warpgroup
+constexpr int NWARPS = NMISC + NA + NB;
 constexpr int NTHREADS = 32 * NWARPS;
 constexpr int REGS_LAUNCH = 65536 / NTHREADS / 8 * 8;  // what __launch_bounds__(NTHREADS, 1) allows
-constexpr int REGS_A = 56, REGS_B = 80;
-static_assert(NA % 4 == 0 && NB % 4 == 0, "the A and B roles fill whole warpgroups");
-static_assert(NA * REGS_A + NB * REGS_B <= (NA + NB) * REGS_LAUNCH, "the B warps' increase comes from the A warps");
+constexpr int REGS_A = 64, REGS_B = 80, REGS_MISC = 56;
+static_assert(NA % 4 == 0 && NB % 4 == 0 && 1 + NAUX <= NMISC, "role groups fill whole warpgroups");
+static_assert(NA * REGS_A + NB * REGS_B + NMISC * REGS_MISC <= NWARPS * REGS_LAUNCH,
+              "the B warps' increase comes from the other groups");
 
 struct Params {
   const void* X;
@@ -305,8 +308,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
       if (__any_sync(0xffffffffu, bad) && lane == 0) status_min(prm.status, ST_NONFINITE, ks);
     }
   };
-  // the A and B warpgroups first re-balance their registers (REGS_*)
+  // every role group first re-balances its registers (REGS_*)
   if (warp >= WARP_PROD) {
+   reg_dec<REGS_MISC>();
    if (warp == WARP_PROD) {
     // ------------------------------------------------------------ producer
     const char* Xb = reinterpret_cast<const char*>(prm.X);
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
                     bar(B_XFULL + s));
       }
     }
-   } else {
+   } else if (warp < WARP_AUX + NAUX) {
     aux_role(warp - WARP_AUX);
    }
   } else if (warp < WARP_A0 + NA) {
@@ -684,7 +688,7 @@ cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg,
     double acc[D_N] = {};
     int cnt = 0;
     for (size_t c = 0; c < (size_t)nseg * pl.CL * pl.ng; ++c)
-      for (int w = 0; w < NWARPS; ++w) {
+      for (int w = 0; w < WARP_AUX + NAUX; ++w) {
         const int r = (w >= WARP_A0 && w < WARP_A0 + NA) ? 0 : (w >= WARP_B0 && w < WARP_B0 + NB) ? 1
                       : w == WARP_PROD ? 2 : 3;  // every aux warp
         if (r != role) continue;
