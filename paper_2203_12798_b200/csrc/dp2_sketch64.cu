@@ -21,7 +21,7 @@
 //                       DMMA m8n8k4 with B fragments from the shared image
 //                       (two accumulator sets to halve the dependent chain);
 //                       partial -> ypart ring.
-//   aux (2 warps)       sum the 8 partials -> Y_t (half of its fragments each) (rows past the piece zeroed),
+//   aux (3 warps)       sum the 8 partials -> Y_t (a third of its fragments each) (rows past the piece zeroed),
 //                       publishes it in B-fragment layout (yfin ring), flags
 //                       non-finite values (status word 0 = lowest slice: a
 //                       NaN / Inf anywhere in X_k reaches Y), writes Y rows.
@@ -53,17 +53,17 @@ constexpr int NY = 2;           // ypart / yfin ring depth
 // 95% (tools/dmma_lds_probe.cu), so the A product -- the critical path, which
 // runs alone whenever the B warps wait for Y_t -- is spread over two warps per
 // sub-partition.  Every role group fills whole warpgroups (4 warps; the last
-// one is the producer, the aux warps and an idle warp) so that setmaxnreg can
+// one is the producer and the aux warps) so that setmaxnreg can
 // move registers from the other groups to the B warps (24 accumulator doubles
 // each): 28 warps launch with 72 registers per thread.
 constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
-constexpr int NAUX = 2;         // warps summing the partials into Y_t (a split of its fragments)
-constexpr int NMISC = 4;        // producer + aux warps, padded to a warpgroup
+constexpr int NAUX = 3;         // warps summing the partials into Y_t (a split of its fragments)
+constexpr int NMISC = 4;        // producer + aux warps: one warpgroup
 constexpr int NWARPS = NMISC + NA + NB;
 constexpr int NTHREADS = 32 * NWARPS;
 constexpr int REGS_LAUNCH = 65536 / NTHREADS / 8 * 8;  // what __launch_bounds__(NTHREADS, 1) allows
 constexpr int REGS_A = 64, REGS_B = 80, REGS_MISC = 56;
-static_assert(NA % 4 == 0 && NB % 4 == 0 && 1 + NAUX <= NMISC, "role groups fill whole warpgroups");
+static_assert(NA % 4 == 0 && NB % 4 == 0 && NMISC % 4 == 0 && 1 + NAUX <= NMISC && REGS_A <= REGS_LAUNCH, "role groups fill whole warpgroups");
 static_assert(NA * REGS_A + NB * REGS_B + NMISC * REGS_MISC <= NWARPS * REGS_LAUNCH,
               "the B warps' increase comes from the other groups");
 
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     aux_role(warp - WARP_AUX);
    }
   } else if (warp < WARP_A0 + NA) {
-    reg_dec<REGS_A>();
+    if constexpr (REGS_A < REGS_LAUNCH) reg_dec<REGS_A>();
     // ------------------------------------------------------------ A warps: Y partials
     const int a = warp - WARP_A0;
     const int r = lane >> 2, q = lane & 3;
