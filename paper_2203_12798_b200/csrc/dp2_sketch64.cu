@@ -45,27 +45,43 @@ namespace s64 {
 
 constexpr int TMAX = 16;        // rows per tile: TM = 8 (J > 256 per CTA), 16 (J <= 256)
 constexpr int NA = 8;           // warps computing Y partials (split of J): two per SM sub-partition
-constexpr int NB = 16;          // warps accumulating Z (split of J)
 constexpr int NY = 2;           // ypart / yfin ring depth
-// warp w runs on SM sub-partition w % 4: two A warps and four B warps per
+// warp w runs on SM sub-partition w % 4: two A warps and NB / 4 B warps per
 // sub-partition keep the DMMA work per sub-partition equal.  A lone
 // shared-memory-fed DMMA stream reaches only 76% of the pipe rate, two reach
 // 95% (tools/dmma_lds_probe.cu), so the A product -- the critical path, which
 // runs alone whenever the B warps wait for Y_t -- is spread over two warps per
 // sub-partition.  Every role group fills whole warpgroups (4 warps; the last
-// one is the producer and the aux warps) so that setmaxnreg can
-// move registers from the other groups to the B warps (24 accumulator doubles
-// each): 28 warps launch with 72 registers per thread.
-constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
+// one is the producer and the aux warps) so that setmaxnreg can move registers
+// from the other groups to the B warps (their Z accumulators).
 constexpr int NAUX = 3;         // warps summing the partials into Y_t (a split of its fragments)
 constexpr int NMISC = 4;        // producer + aux warps: one warpgroup
-constexpr int NWARPS = NMISC + NA + NB;
-constexpr int NTHREADS = 32 * NWARPS;
-constexpr int REGS_LAUNCH = 65536 / NTHREADS / 8 * 8;  // what __launch_bounds__(NTHREADS, 1) allows
-constexpr int REGS_A = 64, REGS_B = 80, REGS_MISC = 56;
-static_assert(NA % 4 == 0 && NB % 4 == 0 && NMISC % 4 == 0 && 1 + NAUX <= NMISC && REGS_A <= REGS_LAUNCH, "role groups fill whole warpgroups");
-static_assert(NA * REGS_A + NB * REGS_B + NMISC * REGS_MISC <= NWARPS * REGS_LAUNCH,
-              "the B warps' increase comes from the other groups");
+constexpr int REGS_A = 64, REGS_MISC = 56;
+constexpr int NB_MAX = 16;
+// NT sketch column blocks per CTA.  NT >= 2 (J <= 512): 16 B warps (Z rows
+// split 16 ways, 24 accumulator doubles each at NT = 3), 28 warps launched at
+// 72 registers, B warps raised to 80.  NT = 1 (one column block per CTA: J up
+// to 1024): 8 B warps of up to 16 J-blocks (32 accumulator doubles), 20 warps
+// launched at 96 registers -- measured on the c5 shard (J = 1000) 34.6 / 34.9
+// ms per pass against 37.5 / 37.5 with 16 B warps; at c2 (NT = 3) 8 B warps of
+// 48 accumulator doubles made no difference (3.80 / 3.89) and c3 (J = 256)
+// slower (19.4 / 20.5 against 18.3 / 19.2).
+template <int NT>
+struct Lay {
+  static constexpr int NB = NT == 1 ? 8 : 16;  // warps accumulating Z (split of J)
+  static constexpr int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
+  static constexpr int NWARPS = NMISC + NA + NB;
+  static constexpr int NTHREADS = 32 * NWARPS;
+  static constexpr int REGS_LAUNCH = 65536 / NTHREADS / 8 * 8;  // what __launch_bounds__(NTHREADS, 1) allows
+  static constexpr int REGS_B = NT == 1 ? 128 : 80;
+  static_assert(NA % 4 == 0 && NB % 4 == 0 && NMISC % 4 == 0 && 1 + NAUX <= NMISC && REGS_A <= REGS_LAUNCH &&
+                    NB <= NB_MAX,
+                "role groups fill whole warpgroups");
+  static_assert(NA * REGS_A + NB * REGS_B + NMISC * REGS_MISC <= NWARPS * REGS_LAUNCH,
+                "the B warps' increase comes from the other groups");
+};
+inline int nb_of(int NT) { return NT == 1 ? Lay<1>::NB : Lay<3>::NB; }
+inline int nwarps_of(int NT) { return NMISC + NA + nb_of(NT); }
 
 struct Params {
   const void* X;
@@ -204,7 +220,11 @@ enum { B_XFULL = 0, B_XEMPTY = MAXS, B_OFULL = 2 * MAXS, B_OEMPTY = 2 * MAXS + N
 // aux sums all eight in the same global order, so both hold the identical
 // Y_t for their B warps).
 template <typename T, int NT, int CL, int TM, bool DBG>
-__global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
+__global__ void __launch_bounds__(Lay<NT>::NTHREADS, 1) sketch64_kernel(Params prm) {
+  using LY = Lay<NT>;
+  constexpr int NB = LY::NB, WARP_A0 = LY::WARP_A0, WARP_B0 = LY::WARP_B0, WARP_PROD = LY::WARP_PROD,
+                WARP_AUX = LY::WARP_AUX, NWARPS = LY::NWARPS, NTHREADS = LY::NTHREADS, REGS_B = LY::REGS_B,
+                REGS_LAUNCH = LY::REGS_LAUNCH;
   constexpr int SG = 8 * NT;
   constexpr int RB = TM / 8;            // DMMA row blocks per tile (A warps)
   constexpr int K2 = TM / 4;            // k-steps of 4 rows per tile (B warps, G)
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     const int bw = warp - WARP_B0;
     // J-blocks of 8 per B warp: <= 4 at J <= 512; J <= 1024 runs one sketch
     // column block per CTA (NT = 1) with up to 8
-    constexpr int MBMAX = NT == 1 ? 8 : 4;
+    constexpr int MBMAX = (NT == 1 ? 128 : 64) / NB;
     const int MB = JH / (8 * NB);
     const int jb0 = bw * MB;
     double z[MBMAX][NT][2];
@@ -426,9 +446,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
     // gi NT + gj -- Y^T fragments are the B fragments this warp loads anyway,
     // so the 2 NT^2 DMMAs per tile spread over the sub-partitions (the aux
     // warp alone made its sub-partition the slowest)
-    const bool g_own = prm.g_part != nullptr && crank == 0 && bw < NT * NT;
-    const int gi = bw / NT, gj = bw - (bw / NT) * NT;
-    double g0 = 0.0, g1 = 0.0;
+    constexpr int GT = (NT * NT + NB - 1) / NB;  // G tiles per B warp: tile bw + i NB
+    const bool g_on = prm.g_part != nullptr && crank == 0;
+    double g[GT][2];
+#pragma unroll
+    for (int i = 0; i < GT; ++i) g[i][0] = g[i][1] = 0.0;
     int n = 0, rs = 0, rph = 0;
     for (int p = pbeg; p < pend; ++p) {
       const int rows = prm.piece_rows[p];
@@ -444,14 +466,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
           double yv[NT];
 #pragma unroll
           for (int j = 0; j < NT; ++j) yv[j] = yf[(k2 * NT + j) * 32];
-          if (g_own) {
-            double ya = 0.0, yb = 0.0;
+          if (g_on) {
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              ya = j == gi ? yv[j] : ya;
-              yb = j == gj ? yv[j] : yb;
+            for (int i = 0; i < GT; ++i) {
+              const int gt = bw + i * NB;
+              if (gt < NT * NT) {
+                const int gi = gt / NT, gj = gt - gi * NT;
+                double ya = 0.0, yb = 0.0;
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                  ya = j == gi ? yv[j] : ya;
+                  yb = j == gj ? yv[j] : yb;
+                }
+                dmma_8x8x4(g[i][0], g[i][1], ya, yb);
+              }
             }
-            dmma_8x8x4(g0, g1, ya, yb);
           }
 #pragma unroll
           for (int i = 0; i < MBMAX; ++i) {
@@ -465,14 +494,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) sketch64_kernel(Params prm) {
         warp_arrive(bar(B_YEMPTY + b));
         warp_arrive(bar(B_XEMPTY + s));
       }
-      if (g_own) {  // G tile (gi, gj): rows 8 gi + (lane >> 2), cols 8 gj + 2 (lane & 3) (+1)
+      if (g_on) {  // G tile (gi, gj): rows 8 gi + (lane >> 2), cols 8 gj + 2 (lane & 3) (+1)
         double* gp = prm.g_part + (size_t)p * sp * sp;
-        const int rr = 8 * gi + (lane >> 2), cc = 8 * gj + 2 * (lane & 3);
-        if (rr < sp && cc < sp) {
-          gp[(size_t)rr * sp + cc] = g0;
-          if (cc + 1 < sp) gp[(size_t)rr * sp + cc + 1] = g1;
+#pragma unroll
+        for (int i = 0; i < GT; ++i) {
+          const int gt = bw + i * NB;
+          if (gt < NT * NT) {
+            const int gi = gt / NT, gj = gt - gi * NT;
+            const int rr = 8 * gi + (lane >> 2), cc = 8 * gj + 2 * (lane & 3);
+            if (rr < sp && cc < sp) {
+              gp[(size_t)rr * sp + cc] = g[i][0];
+              if (cc + 1 < sp) gp[(size_t)rr * sp + cc + 1] = g[i][1];
+            }
+          }
+          g[i][0] = g[i][1] = 0.0;
         }
-        g0 = g1 = 0.0;
       }
       // piece complete: flush Z rows 8 (jb0 + i) + (lane >> 2), cols col0 + 8 j + 2 (lane & 3) (+1)
       double* out = prm.out_part + (size_t)p * J * sp;
@@ -542,7 +578,7 @@ __global__ void __launch_bounds__(256) image_kernel(const double* __restrict__ B
 // 12 per tile) to amortise the per-tile barrier and fragment-load overhead.
 bool uses_pairs(int J) {
   static const bool on = getenv("DP2_S64_PAIRS") && atoi(getenv("DP2_S64_PAIRS")) != 0;
-  const int JP2 = (J + 16 * NB - 1) / (16 * NB) * (16 * NB);
+  const int JP2 = (J + 16 * NB_MAX - 1) / (16 * NB_MAX) * (16 * NB_MAX);
   return on && J >= 256 && J <= 512 && JP2 * 100 <= J * 115;
 }
 
@@ -561,6 +597,7 @@ bool plan(int J, int sp, int elem, Plan* pl) {
   const int NT = J > 512 ? 1 : (nbt <= 3 ? nbt : 3);
   const int ng = (nbt + NT - 1) / NT;
   const int CL = uses_pairs(J) ? 2 : 1;
+  const int NB = nb_of(NT);
   const int JP = CL == 2 ? (J + 16 * NB - 1) / (16 * NB) * (16 * NB) : (J + 8 * NB - 1) / (8 * NB) * (8 * NB);
   const int JH = JP / CL;
   // tile height: keep ~96 DMMAs per A warp and ~24 per B warp per tile as J shrinks
@@ -627,12 +664,12 @@ cudaError_t launch_cl(const Params& prm, const Plan& pl, int nseg, cudaStream_t 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   if (CL == 1) {
-    kern<<<dim3(nseg, pl.ng), NTHREADS, pl.smem, st>>>(prm);
+    kern<<<dim3(nseg, pl.ng), Lay<NT>::NTHREADS, pl.smem, st>>>(prm);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(CL * nseg, pl.ng);
-  cfg.blockDim = dim3(NTHREADS);
+  cfg.blockDim = dim3(Lay<NT>::NTHREADS);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -673,6 +710,8 @@ cudaError_t launch_any(int elem, int NT, const Params& prm, const Plan& pl, int 
 // DP2_S64_DEBUG: run with per-warp wait accounting and print the share of
 // cycles each role spends waiting on each barrier class (debug aid; syncs)
 cudaError_t launch_debug(int elem, int NT, Params prm, const Plan& pl, int nseg, cudaStream_t stream) {
+  const int NB = nb_of(NT), NWARPS = nwarps_of(NT);
+  const int WARP_A0 = 0, WARP_B0 = NA, WARP_PROD = NA + NB, WARP_AUX = NA + NB + 1;
   const size_t nd = (size_t)nseg * pl.CL * pl.ng * NWARPS * D_N;
   unsigned long long *dh = nullptr, *dd = nullptr;
   cudaError_t e = cudaHostAlloc(&dh, nd * 8, cudaHostAllocMapped);
