@@ -299,9 +299,11 @@ __global__ void __launch_bounds__(Lay<NT>::NTHREADS, 1) sketch64_kernel(Params p
           if (f < K2 * NT) {
             const int k2 = f / NT, j = f - k2 * NT;
             const int row = 4 * k2 + (lane & 3), col = 8 * j + (lane >> 2);
-            double v = 0.0;  // slots in pair order (CTA 0's partials, then CTA 1's): same sum in both CTAs
+            // slots in pair order (CTA 0's partials, then CTA 1's): same sum in both CTAs.  The adds
+            // queue behind the DMMAs on the FP64 pipe (the aux warps' busy time), so none is spent on 0 + p
+            double v = ypb[(size_t)row * SG + col];
 #pragma unroll
-            for (int aa = 0; aa < CL * NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
+            for (int aa = 1; aa < CL * NA; ++aa) v += ypb[((size_t)aa * TM + row) * SG + col];
             v = row < valid ? v : 0.0;
             bad |= !isfinite(v);
             fr[i] = v;
