@@ -177,6 +177,29 @@ DP2_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
 DP2_DEV void st_cluster_v2(uint32_t cluster_addr, double a, double b) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(cluster_addr), "d"(a), "d"(b) : "memory");
 }
+// Exact fp32 -> fp64 widening.  F2F.F64.F32 runs at 16 lanes/clk/SM and
+// competes with the DMMAs for the FP64 pipe, so with INT the exponent is
+// re-biased with integer instructions instead (zero keeps its sign; denormals
+// / Inf / NaN -- exponent 0 or 255 -- take the conversion instruction).
+// Measured: c3 (J = 256, NT = 3: one conversion per 3 DMMAs) 18.3 / 19.1 ->
+// 16.8 / 17.7 ms per pass; the c5 shard (NT = 1: one conversion per DMMA, ~9
+// integer instructions each) 34.4 -> 56.3 ms, issue-bound -- so NT = 1 keeps
+// the conversion instruction.
+template <bool INT>
+DP2_DEV double widen(double x) { return x; }
+template <bool INT>
+DP2_DEV double widen(float x) {
+  if constexpr (!INT) return (double)x;
+  const uint32_t u = __float_as_uint(x), a = u & 0x7fffffffu;
+  uint32_t hi = ((a >> 3) + 0x38000000u) | (u & 0x80000000u);
+  const uint32_t lo = u << 29;  // 0 for +-0
+  if (a - 0x00800000u >= 0x7f000000u) {  // exponent 0 or 255
+    if (a != 0u) return (double)x;
+    hi = u;
+  }
+  return __hiloint2double((int)hi, (int)lo);
+}
+
 template <int N>
 DP2_DEV void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
 template <int N>
@@ -397,7 +420,7 @@ __global__ void __launch_bounds__(Lay<NT>::NTHREADS, 1) sketch64_kernel(Params p
           for (int u = 0; u < SETS; ++u) {
             double x[RB];
 #pragma unroll
-            for (int rb = 0; rb < RB; ++rb) x[rb] = (double)xr[(size_t)8 * rb * L + 4 * (k + u)];
+            for (int rb = 0; rb < RB; ++rb) x[rb] = widen<(NT > 1)>(xr[(size_t)8 * rb * L + 4 * (k + u)]);
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
               const double o = im[((k + u) * NT + j) * 32];
@@ -487,7 +510,7 @@ __global__ void __launch_bounds__(Lay<NT>::NTHREADS, 1) sketch64_kernel(Params p
 #pragma unroll
           for (int i = 0; i < MBMAX; ++i) {
             if (i < MB) {
-              const double xv = (double)xb[(size_t)4 * k2 * L + 8 * i];
+              const double xv = widen<(NT > 1)>(xb[(size_t)4 * k2 * L + 8 * i]);
 #pragma unroll
               for (int j = 0; j < NT; ++j) dmma_8x8x4(z[i][j][0], z[i][j][1], xv, yv[j]);
             }
