@@ -251,7 +251,9 @@ __global__ void __launch_bounds__(Lay<NT>::NTHREADS, 1) sketch64_kernel(Params p
   constexpr int SG = 8 * NT;
   constexpr int RB = TM / 8;            // DMMA row blocks per tile (A warps)
   constexpr int K2 = TM / 4;            // k-steps of 4 rows per tile (B warps, G)
-  constexpr int SETS = RB == 1 ? 2 : 1; // independent accumulator sets in the A loop
+  // one accumulator set: with two A warps and the B warps sharing the pipe a warp's NT (x RB) chains are
+  // spaced beyond the DMMA latency, and a second set costs 2 NT adds per tile on the contended FP64 pipe
+  constexpr int SETS = 1;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int crank = CL == 2 ? (int)cluster_rank() : 0;
