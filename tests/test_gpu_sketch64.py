@@ -109,6 +109,32 @@ def test_sketch64_flags_lowest_nonfinite_slice(dtype):
     assert res["status"][0] == 2
 
 
+@pytest.mark.parametrize("J,sp", [(128, 24), (600, 8)])
+def test_sketch64_fp32_widening_is_exact_on_denormals_and_zeros(J, sp):
+    """fp32 storage is upcast inside the pass -- with integer instructions when
+    NT > 1 (csrc/dp2_sketch64.cu widen) -- and must equal the exact value for
+    +-0, denormals and the smallest / largest normals (P/tensor.py: the oracle
+    sees the fp32 values upcast exactly)."""
+    rng = np.random.default_rng(11)
+    tiny = np.float32(1.1754944e-38)  # FLT_MIN
+    pool = np.array([0.0, -0.0, 1.4e-45, -1.4e-45, 7e-42, -3e-40, 5.8e-39, tiny, -tiny, 2.5e-38, -9e-38],
+                    dtype=np.float32)
+    slices = [pool[rng.integers(0, len(pool), size=(m, J))] for m in (150, 37, 260)]
+    X, B, ps, row0, prow, res = run_pass(slices, J, sp, 3, "f32", want_g=False)
+    assert res["kind"] == 3
+    for p in range(len(ps)):
+        Xp = X[row0[p]:row0[p] + prow[p]]
+        Yp = Xp @ B[ps[p]]
+        assert rel(res["y"][row0[p]:row0[p] + prow[p]], Yp) < 1e-12, p
+        assert rel(res["out"][p], Xp.T @ Yp) < 1e-12, p
+    big = [np.where(rng.random((90, J)) < 0.5, np.float32(3.4028235e38), np.float32(-1.7e38)).astype(np.float32)]
+    X, B, ps, row0, prow, res = run_pass(big, J, sp, 2, "f32", want_g=False)
+    for p in range(len(ps)):
+        Xp = X[row0[p]:row0[p] + prow[p]]
+        assert rel(res["y"][row0[p]:row0[p] + prow[p]], Xp @ B[ps[p]]) < 1e-12, p
+    assert res["status"][0] == _lib.INT64_MAX
+
+
 def test_sketch64_cta_pairs_match_numpy():
     """The CTA-pair (thread-block cluster) variant of the pass, DP2_S64_PAIRS=1:
     each CTA of a pair owns half of J, the Y partials cross over DSMEM.  Run in
