@@ -629,7 +629,8 @@ bool plan(int J, int sp, int elem, Plan* pl) {
   const int JH = JP / CL;
   // tile height: keep ~96 DMMAs per A warp and ~24 per B warp per tile as J shrinks
   const int TM = JH > 256 ? 8 : 16;  // (32-row tiles at J <= 128 spill: the aux's Y_t fragments; 16-row tiles at
-                                     // J = 1000 fp32, 2 ring stages: 35.6 ms per c5-shard pass against 33.8)
+                                     // J = 1000 fp32, 2 ring stages: 35.6 ms per c5-shard pass against 33.8; 8-row tiles at J = 256:
+                                     // 19.4 / 18.6 ms per c3 pass against 16.8 / 17.6)
   int L = JH + 4;  // elements: 8 B -> L % 16 == 4; 4 B -> L % 32 == 4
   if (elem == 8) {
     while (L % 16 != 4) ++L;
