@@ -19,19 +19,23 @@
 //                       bulk copy per A warp share of J).
 //   A warps (8)         Y_t (8 x SG) partial over their eighth of J:
 //                       DMMA m8n8k4 with B fragments from the shared image
-//                       (two accumulator sets to halve the dependent chain);
-//                       partial -> ypart ring.
-//   aux (3 warps)       sum the 8 partials -> Y_t (a third of its fragments each) (rows past the piece zeroed),
-//                       publishes it in B-fragment layout (yfin ring), flags
-//                       non-finite values (status word 0 = lowest slice: a
-//                       NaN / Inf anywhere in X_k reaches Y), writes Y rows.
-//   B warps (16)        Z (J x SG) += X_t^T Y_t for their sixteenth of J, held
-//                       in registers across the piece; flushed per piece.  The
-//                       first NT^2 also accumulate one 8 x 8 tile of G = Y^T Y
-//                       each (Y^T fragments are the B fragments).
+//                       (one accumulator set); partial -> ypart ring.
+//   aux (3 warps)       each sums the 8 partials of a third of Y_t's fragments
+//                       (rows past the piece zeroed), publishes them in
+//                       B-fragment layout (yfin ring), flags non-finite values
+//                       (status word 0 = lowest slice: a NaN / Inf anywhere in
+//                       X_k reaches Y), writes Y rows.
+//   B warps (16 / 8)    Z (J x SG) += X_t^T Y_t for their share of J (a
+//                       sixteenth; an eighth when NT = 1), held in registers
+//                       across the piece; flushed per piece.  They also
+//                       accumulate the 8 x 8 tiles of G = Y^T Y (tile t on B
+//                       warp t % NB: Y^T fragments are the B fragments).
+// Roles fill whole warpgroups; setmaxnreg moves registers from the A and
+// producer / aux groups to the B warps (struct Lay).
 //
 // Column groups of SG = 8 NT sketch columns run as separate CTAs (grid.y).
-// Eligible: J <= 512 (B image <= 96 KB + a 3-stage X ring in 227 KB).
+// J <= 512: up to 3 column blocks per CTA (B image <= 96 KB + a 3-stage X
+// ring in 227 KB); 512 < J <= 1024: one column block per CTA.
 #include "dp2_common.cuh"
 #include "dp2_internal.h"
 
